@@ -1,0 +1,263 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY (checker / CPU baseline, never the product).
+//
+// A thin extern "C" veneer over the UNMODIFIED reference library, compiled from
+// the reference sources where they lie (/root/reference/proj/src, see
+// oracle/Makefile) into oracle/_ref/libmugv_ref.so.  Python tests and bench.py's
+// reference arm drive it through ctypes.  Every entry point calls the
+// reference's own public API:
+//   - dit::init_dit_params                       proj/src/dit.cpp:143-183
+//   - open_gates-style gate randomisation        proj/tests/test_dit.cpp:35-41
+//   - flow::interpolate / apply_condition_mask   proj/src/flowtrain.cpp:9-20,83-100
+//   - dit::velocity_rows_graph (+taps)           proj/src/dit.cpp:320-334
+//   - flow::flow_loss_graph, Tape::backward      proj/src/flowtrain.cpp:40-42, autodiff.cpp:82-92
+//   - the per-sample loop of FlowTrainer::step   proj/src/flowtrain.cpp:257-279 (minus AdamW)
+//   - dit::predict_velocity / dit::dit_forward   proj/src/dit.cpp:361-396
+//   - flow::make_batch                           proj/src/flowtrain.cpp:231-250
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "mugv/dit.hpp"
+#include "mugv/flowtrain.hpp"
+
+using namespace mugv;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct RefCfg {
+    int64_t depth, hidden, heads, text_dim, c_z;
+    int32_t rope[3];
+};
+
+dit::DitConfig to_cfg(const RefCfg* c) {
+    dit::DitConfig cfg;
+    cfg.depth = c->depth;
+    cfg.hidden = c->hidden;
+    cfg.heads = c->heads;
+    cfg.text_dim = c->text_dim;
+    cfg.c_z = c->c_z;
+    cfg.rope_split = {c->rope[0], c->rope[1], c->rope[2]};
+    return cfg;
+}
+
+struct Handle {
+    ParameterSet p;
+    std::vector<std::string> names;
+    void refresh() { names = p.names(); }
+};
+
+dit::TokenGrid geom_of(const int64_t* d, int64_t c_z) {
+    // grid_geom from proj/tests/test_flow.cpp:35-37: coords/dims only
+    return dit::latent_rows(Tensor::zeros({d[0], 2 * d[1], 2 * d[2], c_z}));
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const DimensionError& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const ConfigError& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const InputError& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const NumericError& e) {
+        g_err = e.what();
+        return 4;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 9;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// ---- Rng pins ----
+void ref_rng_normal_fill(uint64_t seed, int64_t skip_uniform, int64_t n, double stddev, double* out) {
+    Rng r(seed);
+    for (int64_t i = 0; i < skip_uniform; ++i) r.uniform();
+    Tensor t = r.normal_tensor({n}, stddev);
+    std::memcpy(out, t.data(), sizeof(double) * static_cast<size_t>(n));
+}
+
+void ref_rng_uniform_fill(uint64_t seed, int64_t n, double lo, double hi, double* out) {
+    Rng r(seed);
+    Tensor t = r.uniform_tensor({n}, lo, hi);
+    std::memcpy(out, t.data(), sizeof(double) * static_cast<size_t>(n));
+}
+
+// ---- parameters ----
+void* ref_params_create(const RefCfg* c, uint64_t seed, int open_gates, uint64_t gate_seed, double gate_std,
+                        double gate_b_std) {
+    Handle* h = nullptr;
+    int rc = guard([&] {
+        auto cfg = to_cfg(c);
+        Rng r(seed);
+        auto hh = std::make_unique<Handle>();
+        hh->p = dit::init_dit_params(cfg, r);
+        if (open_gates) {
+            Rng g(gate_seed);
+            hh->p.at("dit.mod.w") = g.normal_tensor(hh->p.at("dit.mod.w").shape(), gate_std);
+            hh->p.at("dit.mod.b") = g.normal_tensor(hh->p.at("dit.mod.b").shape(), gate_std);
+            hh->p.at("dit.final.w") = g.normal_tensor(hh->p.at("dit.final.w").shape(), gate_std);
+            hh->p.at("dit.final.b") = g.normal_tensor(hh->p.at("dit.final.b").shape(), gate_b_std);
+        }
+        hh->refresh();
+        h = hh.release();
+    });
+    return rc == 0 ? h : nullptr;
+}
+
+void ref_params_destroy(void* h) { delete static_cast<Handle*>(h); }
+int64_t ref_params_count(void* h) { return static_cast<int64_t>(static_cast<Handle*>(h)->names.size()); }
+const char* ref_params_name(void* h, int64_t i) { return static_cast<Handle*>(h)->names[static_cast<size_t>(i)].c_str(); }
+int64_t ref_params_numel(void* h, int64_t i) {
+    auto* hh = static_cast<Handle*>(h);
+    return hh->p.at(hh->names[static_cast<size_t>(i)]).numel();
+}
+double* ref_params_data(void* h, int64_t i) {
+    auto* hh = static_cast<Handle*>(h);
+    return hh->p.at(hh->names[static_cast<size_t>(i)]).data();
+}
+
+// ---- make_batch pin (flowtrain.cpp:231-250) ----
+// grids: n pointers to (U,h,w,c_z) tensors with dims[3*i..]; outputs noise rows (N,4c_z), t, masked flag.
+int ref_make_batch(int64_t n, const int64_t* dims, int64_t c_z, const double* const* grids, double fps,
+                   double mask_prob, uint64_t seed, double* const* noise_out, double* t_out, int32_t* masked_out) {
+    return guard([&] {
+        std::vector<Tensor> gs;
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t* d = dims + 3 * i;
+            Tensor g({d[0], d[1], d[2], c_z});
+            std::memcpy(g.data(), grids[i], sizeof(double) * static_cast<size_t>(g.numel()));
+            gs.push_back(std::move(g));
+        }
+        Rng r(seed);
+        flow::FlowBatch b = flow::make_batch(gs, Tensor::zeros({1, 1}), fps, mask_prob, r);
+        for (int64_t i = 0; i < n; ++i) {
+            const auto& s = b.samples[static_cast<size_t>(i)];
+            std::memcpy(noise_out[i], s.noise.data(), sizeof(double) * static_cast<size_t>(s.noise.numel()));
+            t_out[i] = s.t;
+            masked_out[i] = s.mask.any() ? 1 : 0;
+        }
+    });
+}
+
+// ---- the hot path: FlowTrainer::step forward + backward (no AdamW) ----
+// dims: n x (U, Hp, Wp); clean/noise: (N_i, 4c_z) rows; cond: n x {0,1} first-frame flag.
+// V_out[i] (N_i, 4c_z) and taps_out[i] ((depth+3) tensors concatenated: patch emb (N,H),
+// block outputs (N,H) x depth, final proj (N,H), velocity (N,4c_z)) may be null.
+// grads_out: one pointer per parameter in sorted-name order, or null.
+int ref_flow_fwdbwd(void* h, const RefCfg* c, int64_t n, const int64_t* dims, const double* const* clean,
+                    const double* const* noise, const double* t, const int32_t* cond, const double* text, int64_t L,
+                    double fps, double* loss_out, double* const* V_out, double* const* taps_out,
+                    double* const* grads_out) {
+    return guard([&] {
+        auto* hh = static_cast<Handle*>(h);
+        auto cfg = to_cfg(c);
+        dit::validate(cfg);
+        Tensor text_t({L, cfg.text_dim});
+        std::memcpy(text_t.data(), text, sizeof(double) * static_cast<size_t>(text_t.numel()));
+        Tape tp;
+        ParamVars pv = register_params(tp, hh->p, grads_out != nullptr, "dit.");
+        Var tx = tp.constant(text_t);
+        Var total;
+        std::vector<std::vector<Var>> all_taps(static_cast<size_t>(n));
+        std::vector<Var> vs;
+        for (int64_t i = 0; i < n; ++i) {
+            dit::TokenGrid geom = geom_of(dims + 3 * i, cfg.c_z);
+            int64_t N = geom.n(), D = cfg.patch_dim();
+            Tensor cr({N, D}), nz({N, D});
+            std::memcpy(cr.data(), clean[i], sizeof(double) * static_cast<size_t>(N * D));
+            std::memcpy(nz.data(), noise[i], sizeof(double) * static_cast<size_t>(N * D));
+            flow::ConditionMask mask = cond[i] ? flow::first_frame_mask(geom, cr) : flow::no_condition(N);
+            flow::Interpolated ip = flow::interpolate(cr, nz, t[i]);
+            Tensor ts = Tensor::full({N}, t[i]);
+            flow::MaskedInput mi = flow::apply_condition_mask(ip.x_t, ts, mask, geom);
+            Var v = dit::velocity_rows_graph(tp, tp.constant(mi.rows), geom, tx, mi.timesteps, fps, pv, cfg,
+                                             taps_out ? &all_taps[static_cast<size_t>(i)] : nullptr);
+            vs.push_back(v);
+            Var l = flow::flow_loss_graph(tp, v, ip.v_target, mi.loss_mask);
+            total = (i == 0) ? l : tp.add(total, l);
+        }
+        total = tp.scale(total, 1.0 / static_cast<real>(n));
+        *loss_out = tp.val(total)[0];
+        for (int64_t i = 0; i < n; ++i) {
+            if (V_out && V_out[i]) {
+                const Tensor& V = tp.val(vs[static_cast<size_t>(i)]);
+                std::memcpy(V_out[i], V.data(), sizeof(double) * static_cast<size_t>(V.numel()));
+            }
+            if (taps_out && taps_out[i]) {
+                double* dst = taps_out[i];
+                for (Var tv : all_taps[static_cast<size_t>(i)]) {
+                    const Tensor& T = tp.val(tv);
+                    std::memcpy(dst, T.data(), sizeof(double) * static_cast<size_t>(T.numel()));
+                    dst += T.numel();
+                }
+            }
+        }
+        if (grads_out) {
+            if (!std::isfinite(*loss_out)) throw NumericError("flow loss is not finite");
+            tp.backward(total);
+            auto grads = collect_grads(tp, pv);
+            size_t k = 0;
+            for (const auto& nm : hh->names) {
+                if (grads_out[k]) {
+                    const Tensor& g = grads.at(nm);
+                    std::memcpy(grads_out[k], g.data(), sizeof(double) * static_cast<size_t>(g.numel()));
+                }
+                ++k;
+            }
+        }
+    });
+}
+
+// predict_velocity (dit.cpp:388-396) on a row-major grid of dims (U,Hp,Wp).
+int ref_predict_velocity(void* h, const RefCfg* c, const int64_t* dims, const double* rows, const double* tau,
+                         const double* text, int64_t L, double fps, double* out) {
+    return guard([&] {
+        auto* hh = static_cast<Handle*>(h);
+        auto cfg = to_cfg(c);
+        dit::TokenGrid geom = geom_of(dims, cfg.c_z);
+        int64_t N = geom.n();
+        Tensor r({N, cfg.patch_dim()}), ts({N}), tx({L, cfg.text_dim});
+        std::memcpy(r.data(), rows, sizeof(double) * static_cast<size_t>(r.numel()));
+        std::memcpy(ts.data(), tau, sizeof(double) * static_cast<size_t>(N));
+        std::memcpy(tx.data(), text, sizeof(double) * static_cast<size_t>(tx.numel()));
+        Tensor v = dit::predict_velocity(r, geom, tx, ts, fps, hh->p, cfg);
+        std::memcpy(out, v.data(), sizeof(double) * static_cast<size_t>(v.numel()));
+    });
+}
+
+// dit_forward (dit.cpp:361-375): tokens (N, hidden) in, (N, hidden) out.
+int ref_dit_forward(void* h, const RefCfg* c, const int64_t* dims, const double* tokens, const double* tau,
+                    const double* text, int64_t L, double fps, double* out) {
+    return guard([&] {
+        auto* hh = static_cast<Handle*>(h);
+        auto cfg = to_cfg(c);
+        dit::TokenGrid geom = geom_of(dims, cfg.c_z);
+        int64_t N = geom.n();
+        geom.tokens = Tensor({N, cfg.hidden});
+        std::memcpy(geom.tokens.data(), tokens, sizeof(double) * static_cast<size_t>(N * cfg.hidden));
+        Tensor ts({N}), tx({L, cfg.text_dim});
+        std::memcpy(ts.data(), tau, sizeof(double) * static_cast<size_t>(N));
+        std::memcpy(tx.data(), text, sizeof(double) * static_cast<size_t>(tx.numel()));
+        dit::TokenGrid o = dit::dit_forward(geom, tx, dit::GlobalSignals{ts, fps}, hh->p, cfg);
+        std::memcpy(out, o.tokens.data(), sizeof(double) * static_cast<size_t>(o.tokens.numel()));
+    });
+}
+
+}  // extern "C"

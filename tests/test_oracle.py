@@ -1,0 +1,136 @@
+"""Pin the oracle (numpy/C restatement) against the reference: golden fixtures
+generated from the reference itself (tests/golden/make_golden.py) and, when the
+compiled reference (oracle/_ref) is present, live calls into it."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.golden.make_golden import CASES, build_case
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+needs_ref = pytest.mark.skipif(O.ref_lib() is None, reason="oracle/_ref not built (no reference sources)")
+
+
+def nerr(a, b):
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_restatement_matches_golden(name):
+    g = np.load(os.path.join(GOLDEN, f"{name}.npz"))
+    spec = json.loads(str(g["spec"]))
+    cfg, P, text, samples = build_case(name, CASES[name])
+    assert spec["cfg"]["hidden"] == cfg.hidden
+    out = O.flow_fwdbwd(P, cfg, samples, text, 8.0, grads=True, with_taps=True)
+    assert abs(out["loss"] - float(g["loss"])) <= 1e-12 * abs(float(g["loss"]))
+    for i, s in enumerate(samples):
+        assert bool(g[f"cond.{i}"]) == s.cond
+        assert nerr(out["V"][i], g[f"V.{i}"]) < 1e-12
+        taps = np.concatenate([t.ravel() for t in out["taps"][i]])
+        assert nerr(taps[g[f"taps_idx.{i}"]], g[f"taps_val.{i}"]) < 1e-12
+        assert abs(np.linalg.norm(taps) - float(g[f"taps_norm.{i}"])) < 1e-12 * float(g[f"taps_norm.{i}"])
+    for k, gv in out["grads"].items():
+        gv = gv.ravel()
+        if f"g:{k}" in g:
+            assert nerr(gv, g[f"g:{k}"]) < 1e-12, k
+        else:
+            ref_n = float(g[f"gn:{k}"])
+            assert abs(np.linalg.norm(gv) - ref_n) <= 1e-12 * max(ref_n, 1e-300) + 1e-300, k
+            assert nerr(gv[g[f"gi:{k}"]], g[f"gv:{k}"]) < 1e-11 or ref_n == 0.0, k
+
+
+def test_flow_loss_hand_case():
+    """proj/tests/test_flow.cpp:63-99: flow_loss = 5/3; masked rows get exactly zero gradient."""
+    cfg = O.DitConfig(depth=1, hidden=12, heads=2, text_dim=6, c_z=2, rope_split=(2, 2, 2))
+    pred = np.array([[1.0, 2.0, 3.0]])
+    tgt = np.array([[0.0, 2.0, 5.0]])
+    assert abs(float(np.mean((pred - tgt) ** 2)) - 5.0 / 3.0) < 1e-15
+    # all-masked sample: U=1 with first-frame conditioning -> loss 0 and zero grads (SURVEY 8c side finding)
+    P = O.open_gates(O.init_dit_params(cfg, O.Rng(1)), 2)
+    g = O.Rng(3).uniform_tensor((1, 4, 4, 2), -1, 1)
+    s = O.make_batch([g], 1.0, O.Rng(5))
+    assert s[0].cond
+    out = O.flow_fwdbwd(P, cfg, s, O.Rng(4).normal_tensor((2, 6)))
+    assert out["loss"] == 0.0
+    assert all(np.all(v == 0) for v in out["grads"].values())
+
+
+def test_patch_rows_golden_positions():
+    """proj/tests/test_dit.cpp:74-97 (bit-exact index math) via the C restatement."""
+    grid = O.Rng(11).uniform_tensor((2, 8, 8, 24), -1.0, 1.0)
+    rows, coords, dims = O.latent_rows(grid)
+    assert rows.shape == (32, 96) and dims == (2, 4, 4)
+    assert list(coords[0]) == [0, 0, 0] and list(coords[1]) == [0, 0, 1]
+    assert list(coords[5]) == [0, 1, 1] and list(coords[16]) == [1, 0, 0]
+    assert rows[1, 0] == grid[0, 0, 2, 0] and rows[1, 24] == grid[0, 0, 3, 0]
+    assert np.array_equal(O.rows_to_grid(rows, coords, dims), grid)
+    perm = np.random.default_rng(0).permutation(32)
+    assert np.array_equal(O.rows_to_grid(rows[perm], coords[perm], dims), grid)
+    bad = coords.copy()
+    bad[3] = bad[4]
+    with pytest.raises(ValueError):
+        O.rows_to_grid(rows, bad, dims)
+
+
+def test_default_rope_split():
+    """dit.cpp:65-90; default_rope_split(64,{4,4,4}) = (22,22,20)."""
+    assert O.default_rope_split(64, (4, 4, 4)) == (22, 22, 20)
+    assert sum(O.default_rope_split(144, (16, 45, 80))) == 144
+
+
+@needs_ref
+def test_rng_matches_reference():
+    L = O.ref_lib()
+    for seed, skip, n, std in [(0, 0, 10, 1.0), (7, 3, 1001, 0.5), (2**63 + 5, 1, 4, 2.0)]:
+        a = np.empty(n)
+        L.ref_rng_normal_fill(seed, skip, n, std, a.ctypes.data)
+        r = O.Rng(seed)
+        for _ in range(skip):
+            r.uniform()
+        assert np.array_equal(a, r.normal_tensor((n,), std))
+    a = np.empty(777)
+    L.ref_rng_uniform_fill(99, 777, -1.0, 1.0, a.ctypes.data)
+    assert np.array_equal(a, O.Rng(99).uniform_tensor((777,), -1.0, 1.0))
+
+
+@needs_ref
+def test_make_batch_matches_reference():
+    import ctypes
+    L = O.ref_lib()
+    g = O.Rng(3)
+    grids = [g.uniform_tensor(s, -1, 1) for s in [(2, 4, 4, 2), (3, 2, 6, 2), (1, 2, 2, 2)]]
+    dims = np.array([x.shape[:3] for x in grids], dtype=np.int64)
+    noise = [np.empty((x.shape[0] * x.shape[1] * x.shape[2] // 4, 8)) for x in grids]
+    t = np.empty(3)
+    m = np.empty(3, dtype=np.int32)
+    gp = (ctypes.c_void_p * 3)(*[x.ctypes.data for x in grids])
+    npp = (ctypes.c_void_p * 3)(*[x.ctypes.data for x in noise])
+    assert L.ref_make_batch(3, dims.ctypes.data, 2, gp, 8.0, 0.5, 5, npp, t.ctypes.data, m.ctypes.data) == 0
+    s = O.make_batch(grids, 0.5, O.Rng(5))
+    for i in range(3):
+        assert np.array_equal(s[i].noise, noise[i])
+        assert s[i].t == t[i] and int(s[i].cond) == m[i]
+
+
+@needs_ref
+def test_restatement_matches_live_reference_10b_width():
+    """10B dims (H3456, 24x144, text 64x4096), depth 1, N=8: fwd+bwd vs the reference."""
+    cfg = O.paper_config(depth=1)
+    gs = O.gate_std_for(cfg.hidden)
+    ref = O.RefModel(cfg, 1, 2, gs, gs / 4)
+    init = O.open_gates(O.init_dit_params(cfg, O.Rng(1)), 2, gs, gs / 4)
+    grid = O.Rng(3).uniform_tensor((2, 2, 4, 24), -1.0, 1.0)
+    text = O.Rng(4).normal_tensor((64, 4096))
+    s = O.make_batch([grid], 0.0, O.Rng(5))
+    s[0].cond = True
+    r = ref.flow_fwdbwd(s, text, 8.0, grads=True)
+    o = O.flow_fwdbwd(init, cfg, s, text, 8.0, grads=True)
+    assert abs(r["loss"] - o["loss"]) < 1e-12 * abs(r["loss"])
+    assert nerr(o["V"][0], r["V"][0]) < 1e-12
+    for k in init:
+        assert nerr(o["grads"][k], r["grads"][k]) < 1e-10 or np.abs(r["grads"][k]).max() == 0, k
