@@ -1,0 +1,35 @@
+"""Loader for the product library ``libmugv_b200.so`` (C++ runtime + sm_100a kernels).
+
+There is no fallback: if the library is missing or fails to load, import
+raises.  Build it with ``__graft_entry__.build()`` (or ``make -C
+paper_2510_17519_b200/csrc``).
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmugv_b200.so")
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build the CUDA library first (make -C {_HERE}/csrc)")
+        _lib = ctypes.CDLL(LIB_PATH)
+        _declare(_lib)
+    return _lib
+
+
+def _declare(L):
+    P, I, I64, F, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_float, ctypes.c_double
+    L.mgv_dev_gemm.argtypes = [I, P, I64, I, P, I64, I, I, I, I, P, I64, F, I, P]
+    L.mgv_dev_gemm.restype = I
+    for name, args, res in getattr(L, "_extra_decls", []):
+        pass
+    try:
+        from . import capi
+        capi.declare(L)
+    except ImportError:
+        pass

@@ -1,0 +1,69 @@
+// GEMM host helpers (tensor maps, SM count) and the op-level GEMM entry points
+// exported for tests / roofline measurement.
+#include "gemm.cuh"
+
+#include <mutex>
+
+namespace mgv {
+
+int num_sms() {
+    static int n = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 148;
+    }();
+    return n;
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn encode_fn() {
+    static EncodeFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            throw CudaError("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<EncodeFn>(p);
+    }();
+    return fn;
+}
+
+// 2-D bf16 tensor map, 128-byte swizzle: inner dim contiguous, outer dim strided by ld.
+void make_tmap_bf16(CUtensorMap* m, const void* p, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+                    uint32_t box_inner, uint32_t box_outer) {
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {ld_elems * 2};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ") inner=" +
+                        std::to_string(inner) + " outer=" + std::to_string(outer) + " ld=" + std::to_string(ld_elems));
+}
+
+}  // namespace mgv
+
+using namespace mgv;
+
+extern "C" {
+
+// C[M,N] (fp32, ldc) (+)= alpha * sum_k A(m,k) B(n,k).  bf16 != 0: tcgen05 path on bf16
+// operands; else IEEE fp32 SIMT path on fp32 operands.  Returns 0 or a CUDA error code.
+int mgv_dev_gemm(int bf16, const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb, int b_mn, int M, int N,
+                 int K, float* C, int64_t ldc, float alpha, int accumulate, void* stream) {
+    try {
+        EpiF32 e{C, ldc, nullptr, alpha, accumulate, M, N};
+        gemm(bf16 != 0, Mat{A, lda, a_mn ? Major::MN : Major::K}, Mat{B, ldb, b_mn ? Major::MN : Major::K}, M, N,
+             K, e, static_cast<cudaStream_t>(stream));
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,133 @@
+// Host-side GEMM dispatch: tcgen05 bf16 (performance mode) or IEEE-fp32 SIMT
+// (parity mode: single-pass TF32/BF16 cannot meet 1e-4).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "epilogue.cuh"
+#include "gemm_tc.cuh"
+
+namespace mgv {
+
+enum class Major { K = 0, MN = 1 };
+
+// Element (i, k) of an operand: K-major -> p[i*ld + k]; MN-major -> p[k*ld + i].
+struct Mat {
+    const void* p;
+    int64_t ld;
+    Major major;
+};
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define MGV_CUDA(x)                                                                                      \
+    do {                                                                                                 \
+        cudaError_t e_ = (x);                                                                            \
+        if (e_ != cudaSuccess)                                                                           \
+            throw ::mgv::CudaError(std::string(#x) + ": " + cudaGetErrorString(e_) + " @" + __FILE__ + ":" + \
+                                   std::to_string(__LINE__));                                            \
+    } while (0)
+
+int num_sms();
+void make_tmap_bf16(CUtensorMap* m, const void* p, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+                    uint32_t box_inner, uint32_t box_outer);
+
+// ------------------------------------------------------------ fp32 SIMT path
+template <bool A_MN, bool B_MN, class Epi>
+__global__ void __launch_bounds__(256) gemm_f32_simt_kernel(const float* __restrict__ A, int64_t lda,
+                                                            const float* __restrict__ B, int64_t ldb, int M, int N,
+                                                            int K, Epi epi) {
+    __shared__ float sA[16][68];
+    __shared__ float sB[16][68];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    for (int k0 = 0; k0 < K; k0 += 16) {
+        for (int i = threadIdx.x; i < 1024; i += 256) {
+            int mm = A_MN ? i % 64 : i / 16, kk = A_MN ? i / 64 : i % 16;
+            int m = m0 + mm, k = k0 + kk;
+            sA[kk][mm] = (m < M && k < K) ? (A_MN ? A[(int64_t)k * lda + m] : A[(int64_t)m * lda + k]) : 0.0f;
+            int nn = B_MN ? i % 64 : i / 16, kb = B_MN ? i / 64 : i % 16;
+            int n = n0 + nn, k2 = k0 + kb;
+            sB[kb][nn] = (n < N && k2 < K) ? (B_MN ? B[(int64_t)k2 * ldb + n] : B[(int64_t)n * ldb + k2]) : 0.0f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+            float a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = sA[kk][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = sB[kk][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) epi(m0 + ty * 4 + i, n0 + tx * 4, acc[i], 4);
+}
+
+template <bool A_MN, bool B_MN, class Epi>
+void gemm_f32_launch(const Mat& A, const Mat& B, int M, int N, int K, const Epi& epi, cudaStream_t s) {
+    dim3 grid((N + 63) / 64, (M + 63) / 64);
+    gemm_f32_simt_kernel<A_MN, B_MN, Epi><<<grid, 256, 0, s>>>(static_cast<const float*>(A.p), A.ld,
+                                                               static_cast<const float*>(B.p), B.ld, M, N, K, epi);
+    MGV_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------ tcgen05 path
+template <int BN, bool A_MN, bool B_MN, class Epi>
+void gemm_tc_launch(const Mat& A, const Mat& B, int M, int N, int K, const Epi& epi, cudaStream_t s) {
+    using C = GemmCfg<BN>;
+    CUtensorMap ta, tb;
+    if (A_MN)
+        make_tmap_bf16(&ta, A.p, M, K, A.ld, 64, kGemmBK);
+    else
+        make_tmap_bf16(&ta, A.p, K, M, A.ld, kGemmBK, kGemmBM);
+    if (B_MN)
+        make_tmap_bf16(&tb, B.p, N, K, B.ld, 64, kGemmBK);
+    else
+        make_tmap_bf16(&tb, B.p, K, N, B.ld, kGemmBK, BN);
+    auto kern = gemm_bf16_tc_kernel<BN, A_MN, B_MN, Epi>;
+    static bool attr_set = false;  // one per instantiation
+    if (!attr_set) {
+        MGV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        attr_set = true;
+    }
+    const int tiles = ((M + kGemmBM - 1) / kGemmBM) * ((N + BN - 1) / BN);
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    kern<<<grid, kGemmThreads, C::SMEM, s>>>(ta, tb, M, N, K, epi);
+    MGV_CUDA(cudaGetLastError());
+}
+
+// Dispatch on precision and operand majors.  bf16: A/B are __nv_bfloat16; fp32: float.
+template <class Epi>
+void gemm(bool bf16, const Mat& A, const Mat& B, int M, int N, int K, const Epi& epi, cudaStream_t s) {
+    if (M <= 0 || N <= 0) return;
+    const bool am = A.major == Major::MN, bm = B.major == Major::MN;
+    if (!bf16) {
+        if (!am && !bm) gemm_f32_launch<false, false>(A, B, M, N, K, epi, s);
+        else if (!am && bm) gemm_f32_launch<false, true>(A, B, M, N, K, epi, s);
+        else if (am && bm) gemm_f32_launch<true, true>(A, B, M, N, K, epi, s);
+        else gemm_f32_launch<true, false>(A, B, M, N, K, epi, s);
+        return;
+    }
+    if (!am && !bm) gemm_tc_launch<256, false, false>(A, B, M, N, K, epi, s);
+    else if (!am && bm) gemm_tc_launch<256, false, true>(A, B, M, N, K, epi, s);
+    else if (am && bm) gemm_tc_launch<256, true, true>(A, B, M, N, K, epi, s);
+    else throw std::runtime_error("gemm: MN-major A with K-major B is not used");
+}
+
+}  // namespace mgv

@@ -1,0 +1,180 @@
+// tcgen05 BF16 GEMM for sm_100a: C[M,N] = sum_k A[m,k] * B[n,k], fp32 accumulate
+// in TMEM, fused epilogue functor (epilogue.cuh).
+//
+//   A, B each K-major ("row-major, K contiguous") or MN-major ("M/N contiguous"):
+//     forward  X W^T : A K-major (activations), B K-major (weights)
+//     dgrad    dY W  : A K-major, B MN-major (weights read as stored)
+//     wgrad    dY^T X: A MN-major, B MN-major (activations read as stored)
+//   so no transposed copies are ever made.
+//
+// Persistent, warp specialised, one CTA per SM:
+//   warp 0      TMA producer (one elected lane), STAGES-deep smem ring
+//   warp 1      MMA issuer (one elected lane), 128 x BN x 16 UMMAs
+//   warp 2      TMEM allocator (2 x BN fp32 accumulator columns, double buffer)
+//   warps 4..7  epilogue: tcgen05.ld -> registers -> functor -> global
+// Tiles are 128 x BN x 64 with the 128-byte swizzle on both operands.
+#pragma once
+#include "epilogue.cuh"
+#include "ptx.cuh"
+
+namespace mgv {
+
+constexpr int kGemmBM = 128;
+constexpr int kGemmBK = 64;
+constexpr int kGemmThreads = 256;
+
+template <int BN>
+struct GemmCfg {
+    static constexpr int STAGES = BN >= 256 ? 4 : 6;
+    static constexpr int A_BYTES = kGemmBM * kGemmBK * 2;  // 16 KB
+    static constexpr int B_BYTES = BN * kGemmBK * 2;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
+                                     : (2 * BN <= 256) ? 256 : 512;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN, bool A_MN, bool B_MN, class Epi>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                        int N, int K, Epi epi) {
+    using C = GemmCfg<BN>;
+    constexpr int BM = kGemmBM, BK = kGemmBK, STAGES = C::STAGES;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * C::A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+    const int tiles = num_m * num_n, kblocks = (K + BK - 1) / BK;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmA);
+        tma_prefetch(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 4);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    // m fastest: consecutive CTAs share the B (weight) tile
+    if (warp == 0) {
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int m0 = (t % num_m) * BM, n0 = (t / num_m) * BN;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* a = sA + stage * C::A_BYTES;
+                    uint8_t* b = sB + stage * C::B_BYTES;
+                    mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+                    const int k0 = kb * BK;
+                    if (A_MN) {
+#pragma unroll
+                        for (int c = 0; c < BM / 64; ++c) tma_load_2d(a + c * 8192, &tmA, &full[stage], m0 + 64 * c, k0);
+                    } else {
+                        tma_load_2d(a, &tmA, &full[stage], k0, m0);
+                    }
+                    if (B_MN) {
+#pragma unroll
+                        for (int c = 0; c < BN / 64; ++c) tma_load_2d(b + c * 8192, &tmB, &full[stage], n0 + 64 * c, k0);
+                    } else {
+                        tma_load_2d(b, &tmB, &full[stage], k0, n0);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, A_MN, B_MN);
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t aphase = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            mbar_wait(&tempty[acc], aphase ^ 1);
+            tc_fence_after();
+            const uint32_t d = tmem + acc * BN;
+            for (int kb = 0; kb < kblocks; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t a = smem_u32(sA + stage * C::A_BYTES);
+                    const uint32_t b = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        // K-major: advance 16 elements = 32 bytes inside the 128B swizzle atom.
+                        // MN-major: advance 16 K-rows = 2048 bytes (two 8-row groups).
+                        const uint64_t ad = A_MN ? smem_desc(a + k * 2048, 8192, 1024, kSwizzle128)
+                                                 : smem_desc(a + k * 32, 16, 1024, kSwizzle128);
+                        const uint64_t bd = B_MN ? smem_desc(b + k * 2048, 8192, 1024, kSwizzle128)
+                                                 : smem_desc(b + k * 32, 16, 1024, kSwizzle128);
+                        umma_f16_ss(d, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    umma_commit(&empty[stage]);
+                    if (kb == kblocks - 1) umma_commit(&tfull[acc]);
+                }
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (++acc == 2) {
+                acc = 0;
+                aphase ^= 1;
+            }
+        }
+    } else if (warp >= 4) {
+        const int wq = warp - 4;
+        int acc = 0;
+        uint32_t aphase = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            const int m0 = (t % num_m) * BM, n0 = (t / num_m) * BN;
+            mbar_wait(&tfull[acc], aphase);
+            tc_fence_after();
+            const int row = m0 + wq * 32 + lane;
+            const uint32_t base = tmem + acc * BN + (static_cast<uint32_t>(wq * 32) << 16);
+#pragma unroll 1
+            for (int c = 0; c < BN / 16; ++c) {
+                uint32_t r[16];
+                tmem_ld16(base + c * 16, r);
+                tmem_wait_ld();
+                epi(row, n0 + c * 16, reinterpret_cast<const float*>(r), 16);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) {
+                acc = 0;
+                aphase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
+}  // namespace mgv
