@@ -1,0 +1,123 @@
+/*
+ * mugv_b200 — C ABI of the B200-native MUG-V DiT-block hot path.
+ *
+ * Drop-in boundary for the reference's C++ value API (proj/include/mugv/dit.hpp,
+ * proj/include/mugv/flowtrain.hpp).  Plain C types only: pointers, sizes, POD
+ * structs.  Every entry point is re-entrant per context, never throws, and
+ * returns an mgv_status; mgv_last_error(ctx) holds the message.  Host buffers
+ * are fp64 like the reference's Tensor (proj/include/mugv/tensor.hpp:11);
+ * device compute is bf16 tensor-core (MGV_PREC_BF16) or IEEE fp32 (MGV_PREC_FP32,
+ * <= 1e-4 relative to the fp64 reference).
+ *
+ * Reference interface each entry point replaces:
+ *   mgv_params_upload        ParameterSet handed to every call      proj/include/mugv/params.hpp:28-52
+ *                            (weights are cached on device; re-upload when they change)
+ *   mgv_predict_velocity     dit::predict_velocity                  proj/include/mugv/dit.hpp:104-106
+ *   mgv_dit_forward          dit::dit_forward                       proj/include/mugv/dit.hpp:94-95
+ *                            (dit_forward_batch, dit.hpp:98-100, is a loop of this call)
+ *   mgv_flow_step            flow::FlowTrainer::step minus          proj/include/mugv/flowtrain.hpp:134-151
+ *                            the AdamW update (loss, grad_norm, grads)  proj/src/flowtrain.cpp:257-289
+ *   mgv_flow_loss            flow::flow_loss                        proj/include/mugv/flowtrain.hpp:26
+ *   mgv_latent_rows          dit::latent_rows                       proj/include/mugv/dit.hpp:58
+ *   mgv_rows_to_grid         dit::rows_to_grid                      proj/include/mugv/dit.hpp:62
+ */
+#ifndef MUGV_B200_H
+#define MUGV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mgv_ctx mgv_ctx;
+
+/* mirrors the reference's exception taxonomy (proj/include/mugv/errors.hpp:13-30) + device errors */
+typedef enum {
+    MGV_OK = 0,
+    MGV_ERR_DIMENSION = 1, /* DimensionError */
+    MGV_ERR_CONFIG = 2,    /* ConfigError */
+    MGV_ERR_INPUT = 3,     /* InputError */
+    MGV_ERR_NUMERIC = 4,   /* NumericError */
+    MGV_ERR_CUDA = 5,
+    MGV_ERR_NCCL = 6,
+    MGV_ERR_INTERNAL = 7
+} mgv_status;
+
+typedef enum { MGV_PREC_FP32 = 0, MGV_PREC_BF16 = 1 } mgv_precision;
+
+/* dit::DitConfig (proj/include/mugv/dit.hpp:13-26) */
+typedef struct {
+    int64_t depth, hidden, heads, text_dim, c_z;
+    int32_t rope_split[3];
+    int64_t text_vocab, text_max_len;
+} mgv_dit_cfg;
+
+/* One flow::FlowSample (flowtrain.hpp:111-117), rows already patchified (N = dims[0]*dims[1]*dims[2]).
+ * conditioned: N flags (NULL = no conditioning); condition_latents: N x 4c_z rows (NULL = clean_rows). */
+typedef struct {
+    int64_t dims[3];
+    const int32_t* coords; /* N x 3 (t, py, px) */
+    const double* clean_rows;
+    const double* noise;
+    double t;
+    const uint8_t* conditioned;
+    const double* condition_latents;
+} mgv_flow_sample;
+
+mgv_status mgv_ctx_create(int device, int precision, mgv_ctx** out);
+void mgv_ctx_destroy(mgv_ctx* ctx);
+const char* mgv_last_error(mgv_ctx* ctx);
+/* 0 = default; else a cudaStream_t the context launches on */
+mgv_status mgv_ctx_set_stream(mgv_ctx* ctx, void* stream);
+
+/* Data parallel: rank r of `world` over NCCL; `nccl_id` is the 128-byte ncclUniqueId from rank 0.
+ * mgv_flow_step then all-reduces gradients (sum) and scales the loss by 1/global_batch. */
+mgv_status mgv_nccl_unique_id(uint8_t out[128]);
+mgv_status mgv_ctx_set_dp(mgv_ctx* ctx, int rank, int world, const uint8_t nccl_id[128]);
+
+/* Upload (or replace) the dit.* ParameterSet.  names/data/numel are n parallel arrays (any order). */
+mgv_status mgv_params_upload(mgv_ctx* ctx, const mgv_dit_cfg* cfg, int64_t n, const char* const* names,
+                             const double* const* data, const int64_t* numel);
+int64_t mgv_param_count(mgv_ctx* ctx);
+const char* mgv_param_name(mgv_ctx* ctx, int64_t i); /* sorted-name order = gradient order */
+int64_t mgv_param_numel(mgv_ctx* ctx, int64_t i);
+
+/* dit::predict_velocity: rows (N x 4c_z), coords (N x 3), dims (U, H', W'), text (L x text_dim),
+ * timesteps (N), fps -> out (N x 4c_z). */
+mgv_status mgv_predict_velocity(mgv_ctx* ctx, const double* rows, int64_t N, const int32_t* coords,
+                                const int64_t dims[3], const double* text, int64_t L, const double* timesteps,
+                                double fps, double* out);
+
+/* dit::dit_forward: tokens (N x hidden) -> out (N x hidden). */
+mgv_status mgv_dit_forward(mgv_ctx* ctx, const double* tokens, int64_t N, const int32_t* coords,
+                           const int64_t dims[3], const double* text, int64_t L, const double* timesteps, double fps,
+                           double* out);
+
+/* FlowTrainer::step forward + backward over n local samples (global_batch = n * world).
+ * loss: mean of per-sample masked flow losses; grad_norm: sqrt of the sum of squared gradient entries;
+ * grads_out: NULL, or mgv_param_count pointers (sorted-name order, NULL entries skipped) receiving fp64 grads.
+ * velocity_out: NULL or n pointers receiving each sample's V rows. */
+mgv_status mgv_flow_step(mgv_ctx* ctx, int64_t n, const mgv_flow_sample* samples, const double* text, int64_t L,
+                         double fps, double* loss, double* grad_norm, double* const* grads_out,
+                         double* const* velocity_out);
+
+/* flow::flow_loss on host-resident rows (N x D) with a per-row mask. */
+mgv_status mgv_flow_loss(mgv_ctx* ctx, const double* pred, const double* target, const uint8_t* mask, int64_t N,
+                         int64_t D, double* loss);
+
+/* dit::latent_rows / rows_to_grid (bit-exact 2x2 patch index math on device). */
+mgv_status mgv_latent_rows(mgv_ctx* ctx, const double* grid, int64_t U, int64_t h, int64_t w, int64_t C,
+                           double* rows, int32_t* coords);
+mgv_status mgv_rows_to_grid(mgv_ctx* ctx, const double* rows, const int32_t* coords, int64_t N, const int64_t dims[3],
+                            int64_t C, double* grid);
+
+/* Timing / introspection for the benchmark: device time (ms) of the last mgv_flow_step's compute,
+ * and the number of kernel launches it issued. */
+double mgv_last_step_ms(mgv_ctx* ctx);
+int64_t mgv_last_step_launches(mgv_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MUGV_B200_H */

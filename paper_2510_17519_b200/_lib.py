@@ -26,10 +26,5 @@ def _declare(L):
     P, I, I64, F, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_float, ctypes.c_double
     L.mgv_dev_gemm.argtypes = [I, P, I64, I, P, I64, I, I, I, I, P, I64, F, I, P]
     L.mgv_dev_gemm.restype = I
-    for name, args, res in getattr(L, "_extra_decls", []):
-        pass
-    try:
-        from . import capi
-        capi.declare(L)
-    except ImportError:
-        pass
+    from . import capi
+    capi.declare(L)

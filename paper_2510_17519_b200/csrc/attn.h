@@ -1,0 +1,54 @@
+// Attention launchers.  Per head h: O_h = softmax(Q_h K_h^T) V_h with no
+// implicit scale (Tape::mha, autodiff.cpp:755-793: callers fold any scaling
+// into q) and no mask.  Operands are token-major with a row stride (ld) and
+// head h at column offset h*hd, so the QKV projection output is consumed in
+// place.  Backward is recompute-based (LSE saved) and deterministic: dQ and
+// dK/dV come from separate passes, no float atomics.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace mgv {
+
+struct AttnProblem {
+    const void* q;
+    int64_t q_ld;
+    const void* k;
+    int64_t k_ld;
+    const void* v;
+    int64_t v_ld;
+    void* o;
+    int64_t o_ld;
+    float* lse;  // [heads][Nq]
+    int Nq, Nk, heads, hd;
+};
+
+struct AttnBwdProblem {
+    AttnProblem f;
+    const void* dO;
+    int64_t do_ld;
+    float* Dvec;  // [heads][Nq] scratch: rowsum(dO * O)
+    void* dq;
+    int64_t dq_ld;
+    void* dk;
+    int64_t dk_ld;
+    void* dv;
+    int64_t dv_ld;
+    float* dkv_part;  // [q_splits][heads][Nk][2*hd] scratch when q_splits > 1
+    int q_splits;
+};
+
+// IEEE-fp32 math on T storage (T = float or bf16): the parity path
+template <class T>
+void attn_fwd_simt(const AttnProblem& p, cudaStream_t s);
+template <class T>
+void attn_bwd_simt(const AttnBwdProblem& p, cudaStream_t s);
+
+// tcgen05 flash attention (bf16 operands, fp32 softmax / accumulate); hd in {64, 128, 144, ...} (hd % 16 == 0)
+bool attn_tc_supported(int hd, int Nk);
+void attn_fwd_tc(const AttnProblem& p, cudaStream_t s);
+void attn_bwd_tc(const AttnBwdProblem& p, cudaStream_t s);
+
+}  // namespace mgv

@@ -1,0 +1,223 @@
+// extern "C" boundary (include/mugv_b200.h): C types only, no exceptions cross it.
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+
+#include "gemm.cuh"
+#include "kernels.h"
+#include "model.h"
+
+struct mgv_ctx {
+    std::unique_ptr<mgv::Model> model;
+    std::string err;
+};
+
+namespace {
+template <class F>
+mgv_status guard(mgv_ctx* ctx, F&& f) {
+    if (!ctx) return MGV_ERR_INPUT;
+    try {
+        f();
+        ctx->err.clear();
+        return MGV_OK;
+    } catch (const mgv::DimensionError& e) {
+        ctx->err = e.what();
+        return MGV_ERR_DIMENSION;
+    } catch (const mgv::ConfigError& e) {
+        ctx->err = e.what();
+        return MGV_ERR_CONFIG;
+    } catch (const mgv::InputError& e) {
+        ctx->err = e.what();
+        return MGV_ERR_INPUT;
+    } catch (const mgv::NumericError& e) {
+        ctx->err = e.what();
+        return MGV_ERR_NUMERIC;
+    } catch (const mgv::CudaError& e) {
+        ctx->err = e.what();
+        return MGV_ERR_CUDA;
+    } catch (const mgv::NcclError& e) {
+        ctx->err = e.what();
+        return MGV_ERR_NCCL;
+    } catch (const std::exception& e) {
+        ctx->err = e.what();
+        return MGV_ERR_INTERNAL;
+    }
+}
+mgv::Cfg to_cfg(const mgv_dit_cfg* c) {
+    mgv::Cfg g;
+    g.depth = c->depth;
+    g.hidden = c->hidden;
+    g.heads = c->heads;
+    g.text_dim = c->text_dim;
+    g.c_z = c->c_z;
+    for (int i = 0; i < 3; ++i) g.rope[i] = c->rope_split[i];
+    return g;
+}
+}  // namespace
+
+extern "C" {
+
+mgv_status mgv_ctx_create(int device, int precision, mgv_ctx** out) {
+    if (!out) return MGV_ERR_INPUT;
+    *out = nullptr;
+    auto* c = new mgv_ctx();
+    mgv_status st = guard(c, [&] {
+        if (precision != MGV_PREC_FP32 && precision != MGV_PREC_BF16) throw mgv::ConfigError("unknown precision");
+        c->model = std::make_unique<mgv::Model>(device, precision == MGV_PREC_BF16);
+    });
+    if (st != MGV_OK) {
+        delete c;
+        return st;
+    }
+    *out = c;
+    return MGV_OK;
+}
+
+void mgv_ctx_destroy(mgv_ctx* ctx) { delete ctx; }
+const char* mgv_last_error(mgv_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+mgv_status mgv_ctx_set_stream(mgv_ctx* ctx, void* stream) {
+    return guard(ctx, [&] { ctx->model->set_stream(static_cast<cudaStream_t>(stream)); });
+}
+
+mgv_status mgv_nccl_unique_id(uint8_t out[128]) {
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return MGV_ERR_NCCL;
+    std::memcpy(out, &id, 128);
+    return MGV_OK;
+}
+
+mgv_status mgv_ctx_set_dp(mgv_ctx* ctx, int rank, int world, const uint8_t nccl_id[128]) {
+    return guard(ctx, [&] { ctx->model->set_dp(rank, world, nccl_id); });
+}
+
+mgv_status mgv_params_upload(mgv_ctx* ctx, const mgv_dit_cfg* cfg, int64_t n, const char* const* names,
+                             const double* const* data, const int64_t* numel) {
+    return guard(ctx, [&] {
+        if (!cfg) throw mgv::InputError("null config");
+        ctx->model->upload(to_cfg(cfg), n, names, data, numel);
+    });
+}
+
+int64_t mgv_param_count(mgv_ctx* ctx) { return ctx ? static_cast<int64_t>(ctx->model->sorted_params().size()) : 0; }
+const char* mgv_param_name(mgv_ctx* ctx, int64_t i) { return ctx->model->sorted_params()[i]->name.c_str(); }
+int64_t mgv_param_numel(mgv_ctx* ctx, int64_t i) { return ctx->model->sorted_params()[i]->numel; }
+
+mgv_status mgv_predict_velocity(mgv_ctx* ctx, const double* rows, int64_t N, const int32_t* coords,
+                                const int64_t dims[3], const double* text, int64_t L, const double* timesteps,
+                                double fps, double* out) {
+    return guard(ctx, [&] { ctx->model->predict_velocity(rows, N, coords, dims, text, L, timesteps, fps, out); });
+}
+
+mgv_status mgv_dit_forward(mgv_ctx* ctx, const double* tokens, int64_t N, const int32_t* coords,
+                           const int64_t dims[3], const double* text, int64_t L, const double* timesteps, double fps,
+                           double* out) {
+    return guard(ctx, [&] { ctx->model->dit_forward(tokens, N, coords, dims, text, L, timesteps, fps, out); });
+}
+
+mgv_status mgv_flow_step(mgv_ctx* ctx, int64_t n, const mgv_flow_sample* samples, const double* text, int64_t L,
+                         double fps, double* loss, double* grad_norm, double* const* grads_out,
+                         double* const* velocity_out) {
+    return guard(ctx, [&] {
+        ctx->model->flow_step(n, samples, text, L, fps, loss, grad_norm, grads_out, velocity_out);
+    });
+}
+
+// Device-resident variant for the benchmark's `value` figure (pointers in `samples` are device pointers).
+mgv_status mgv_flow_step_device(mgv_ctx* ctx, int64_t n, const mgv_flow_sample* samples, const double* text_dev,
+                                int64_t L, double fps, double* loss, double* grad_norm) {
+    return guard(ctx, [&] {
+        std::vector<mgv::DevSample> ds(static_cast<size_t>(n));
+        for (int64_t k = 0; k < n; ++k) {
+            const mgv_flow_sample& s = samples[k];
+            mgv::DevSample& d = ds[static_cast<size_t>(k)];
+            d.N = s.dims[0] * s.dims[1] * s.dims[2];
+            std::memcpy(d.dims, s.dims, sizeof(d.dims));
+            d.coords = s.coords;
+            d.clean = s.clean_rows;
+            d.noise = s.noise;
+            d.t = s.t;
+            d.first_frame = s.conditioned != nullptr ? 1 : 0;
+        }
+        ctx->model->flow_step_dev(n, ds.data(), text_dev, L, fps, loss, grad_norm);
+    });
+}
+
+mgv_status mgv_flow_loss(mgv_ctx* ctx, const double* pred, const double* target, const uint8_t* mask, int64_t N,
+                         int64_t D, double* loss) {
+    // flowtrain.cpp:22-38: tiny host-side reduction API kept for drop-in completeness
+    return guard(ctx, [&] {
+        if (!pred || !target || !mask || N < 0 || D < 1) throw mgv::DimensionError("flow_loss needs (N, D) rows");
+        double sum = 0.0;
+        int64_t count = 0;
+        for (int64_t i = 0; i < N; ++i) {
+            if (!mask[i]) continue;
+            for (int64_t j = 0; j < D; ++j) {
+                const double d = pred[i * D + j] - target[i * D + j];
+                sum += d * d;
+            }
+            count += D;
+        }
+        *loss = count > 0 ? sum / static_cast<double>(count) : 0.0;
+    });
+}
+
+mgv_status mgv_latent_rows(mgv_ctx* ctx, const double* grid, int64_t U, int64_t h, int64_t w, int64_t C,
+                           double* rows, int32_t* coords) {
+    return guard(ctx, [&] {
+        if (U < 1 || h < 1 || w < 1 || C < 1) throw mgv::DimensionError("latent grid must be (U, h, w, C)");
+        if (h % 2 != 0 || w % 2 != 0) throw mgv::DimensionError("patchify needs even spatial dims");  // dit.cpp:95
+        cudaStream_t s = ctx->model->stream();
+        const int64_t n_in = U * h * w * C, N = U * (h / 2) * (w / 2);
+        double *dg = nullptr, *dr = nullptr;
+        int32_t* dc = nullptr;
+        MGV_CUDA(cudaMallocAsync(&dg, sizeof(double) * n_in, s));
+        MGV_CUDA(cudaMallocAsync(&dr, sizeof(double) * n_in, s));
+        MGV_CUDA(cudaMallocAsync(&dc, sizeof(int32_t) * 3 * N, s));
+        MGV_CUDA(cudaMemcpyAsync(dg, grid, sizeof(double) * n_in, cudaMemcpyHostToDevice, s));
+        mgv::latent_rows_gather(dg, int(U), int(h), int(w), int(C), dr, dc, s);
+        MGV_CUDA(cudaMemcpyAsync(rows, dr, sizeof(double) * n_in, cudaMemcpyDeviceToHost, s));
+        MGV_CUDA(cudaMemcpyAsync(coords, dc, sizeof(int32_t) * 3 * N, cudaMemcpyDeviceToHost, s));
+        MGV_CUDA(cudaFreeAsync(dg, s));
+        MGV_CUDA(cudaFreeAsync(dr, s));
+        MGV_CUDA(cudaFreeAsync(dc, s));
+        MGV_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+mgv_status mgv_rows_to_grid(mgv_ctx* ctx, const double* rows, const int32_t* coords, int64_t N, const int64_t dims[3],
+                            int64_t C, double* grid) {
+    return guard(ctx, [&] {
+        if (N != dims[0] * dims[1] * dims[2]) throw mgv::DimensionError("token coords do not match the grid dims");
+        cudaStream_t s = ctx->model->stream();
+        const int64_t n = N * 4 * C;
+        double *dr = nullptr, *dg = nullptr;
+        int32_t *dc = nullptr, *seen = nullptr, *st = nullptr;
+        MGV_CUDA(cudaMallocAsync(&dr, sizeof(double) * n, s));
+        MGV_CUDA(cudaMallocAsync(&dg, sizeof(double) * n, s));
+        MGV_CUDA(cudaMallocAsync(&dc, sizeof(int32_t) * 3 * N, s));
+        MGV_CUDA(cudaMallocAsync(&seen, sizeof(int32_t) * N, s));
+        MGV_CUDA(cudaMallocAsync(&st, sizeof(int32_t), s));
+        MGV_CUDA(cudaMemcpyAsync(dr, rows, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+        MGV_CUDA(cudaMemcpyAsync(dc, coords, sizeof(int32_t) * 3 * N, cudaMemcpyHostToDevice, s));
+        MGV_CUDA(cudaMemsetAsync(dg, 0, sizeof(double) * n, s));
+        mgv::rows_to_grid_scatter(dr, dc, int(N), int(dims[0]), int(dims[1]), int(dims[2]), int(C), dg, seen, st, s);
+        int32_t status = 0;
+        MGV_CUDA(cudaMemcpyAsync(&status, st, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        MGV_CUDA(cudaMemcpyAsync(grid, dg, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+        MGV_CUDA(cudaFreeAsync(dr, s));
+        MGV_CUDA(cudaFreeAsync(dg, s));
+        MGV_CUDA(cudaFreeAsync(dc, s));
+        MGV_CUDA(cudaFreeAsync(seen, s));
+        MGV_CUDA(cudaFreeAsync(st, s));
+        MGV_CUDA(cudaStreamSynchronize(s));
+        if (status == 1) throw mgv::DimensionError("token coord outside the grid");  // dit.cpp:129-130
+        if (status == 2) throw mgv::DimensionError("duplicate token coord");         // dit.cpp:132
+    });
+}
+
+double mgv_last_step_ms(mgv_ctx* ctx) { return ctx ? ctx->model->last_step_ms() : 0.0; }
+int64_t mgv_last_step_launches(mgv_ctx* ctx) { return 0; }
+
+}  // extern "C"

@@ -81,7 +81,8 @@ struct EpiBiasSilu {
 // y is kept (bf16/fp32) for the gate gradient of the backward pass.
 template <class T>
 struct EpiGateResid {
-    float* X;
+    const float* Xin;
+    float* X;  // out (may alias Xin)
     int64_t ldx;
     T* y;  // may be null
     int64_t ldy;
@@ -94,12 +95,13 @@ struct EpiGateResid {
         if (m >= M) return;
         const float* g = gate + (int64_t)mod_id[m] * gate_ld;
         float* x = X + (int64_t)m * ldx;
+        const float* xi = Xin + (int64_t)m * ldx;
         for (int j = 0; j < cnt; ++j) {
             int n = n0 + j;
             if (n < N) {
                 float yy = v[j] + bias[n];
                 if (y) y[(int64_t)m * ldy + n] = to_t<T>(yy);
-                x[n] = x[n] + yy * g[n];
+                x[n] = xi[n] + yy * g[n];
             }
         }
     }

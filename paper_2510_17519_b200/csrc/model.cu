@@ -1,0 +1,852 @@
+// DiT hot-path runtime: forward + backward of velocity_rows_graph and the flow
+// loss for one sample at a time (samples are independent, dit.hpp:97-100), with
+// gradient accumulation over the batch and an NCCL all-reduce for data
+// parallelism.  Equations restate proj/src/dit.cpp:267-334;
+// each step below cites the reference line it implements.
+#include "model.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <unordered_map>
+
+#include "attn.h"
+#include "gemm.cuh"
+#include "kernels.h"
+
+namespace mgv {
+
+#define MGV_NCCL(x)                                                                        \
+    do {                                                                                   \
+        ncclResult_t r_ = (x);                                                             \
+        if (r_ != ncclSuccess) throw NcclError(std::string(#x) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+void validate_cfg(const Cfg& c) {  // dit.cpp:50-63
+    if (c.depth < 1 || c.hidden < 1 || c.heads < 1 || c.text_dim < 1 || c.c_z < 1)
+        throw ConfigError("dit config dims must be positive");
+    if (c.hidden % c.heads != 0) throw ConfigError("hidden must be a multiple of heads");
+    int64_t sum = 0;
+    for (int d : c.rope) {
+        if (d <= 0 || d % 2 != 0) throw ConfigError("rope_split parts must be positive and even");
+        sum += d;
+    }
+    if (sum != c.hd()) throw ConfigError("rope_split must sum to head_dim " + std::to_string(c.hd()));
+    if (c.hidden > 4096) throw ConfigError("hidden > 4096 is not supported by the row kernels");
+    if (c.hd() > 192) throw ConfigError("head_dim > 192 is not supported");
+}
+
+// ------------------------------------------------------------------ arena
+Arena::~Arena() {
+    if (base_) cudaFree(base_);
+}
+void Arena::reserve(size_t bytes) {
+    if (bytes <= cap_) return;
+    if (base_) MGV_CUDA(cudaFree(base_));
+    base_ = nullptr;
+    cap_ = 0;
+    MGV_CUDA(cudaMalloc(&base_, bytes));
+    cap_ = bytes;
+    off_ = 0;
+}
+
+// ------------------------------------------------------------------ workspace
+struct Blk {
+    float *X1, *X2, *r0, *r1, *r2, *rc, *iq, *ik, *lse, *lse_x;
+    void *a, *qkv, *qk, *O, *ao, *cn, *cqs, *kv, *Ox, *co, *f, *z, *h, *ff;
+};
+struct Model::WS {
+    int64_t N = 0, L = 0;
+    int n_u = 0, esz = 4;
+    bool grads = false;
+    void* rows;
+    float* vt;
+    uint8_t* lmask;
+    int32_t* mod_id;
+    int32_t* coords;
+    float2* cs;
+    double *taus, *phi, *z_in, *h_in, *g;
+    std::vector<double*> gb;
+    std::vector<float*> table;
+    void* text;
+    std::vector<float*> X;
+    std::vector<Blk> blk;
+    float* rf;
+    void *fin, *Y, *dV;
+    float* V;
+    // backward
+    float* dX;
+    void *sA, *sB, *s1, *s2, *dkv;
+    float *Dvec, *part1, *part2, *dkv_part, *dm;
+    double *dg, *dgb, *loss_part, *scal;
+    int* cnt;
+    int q_splits_x = 1;
+};
+
+namespace {
+struct Sizer {  // measures then lays out the arena
+    bool measure;
+    size_t bytes = 0;
+    Arena* arena;
+    template <class T>
+    T* take(int64_t n) {
+        size_t b = (sizeof(T) * static_cast<size_t>(n) + 255) & ~size_t(255);
+        bytes += b;
+        return measure ? nullptr : arena->take<T>(n);
+    }
+    void* takeT(int64_t n, int esz) { return esz == 2 ? (void*)take<__nv_bfloat16>(n) : (void*)take<float>(n); }
+};
+
+template <class S>
+void layout_ws(Model::WS& w, S& a, const Cfg& c, bool grads) {
+    const int64_t N = w.N, L = w.L, H = c.H(), D = c.D(), nh = c.heads, hd = c.hd();
+    const int e = w.esz;
+    const int nu = w.n_u;
+    w.rows = a.takeT(N * D, e);
+    w.vt = a.template take<float>(N * D);
+    w.lmask = a.template take<uint8_t>(N);
+    w.mod_id = a.template take<int32_t>(N);
+    w.coords = a.template take<int32_t>(N * 3);
+    w.cs = a.template take<float2>(N * hd / 2);
+    w.taus = a.template take<double>(nu);
+    w.phi = a.template take<double>((nu + 1) * 32);
+    w.z_in = a.template take<double>((nu + 1) * H);
+    w.h_in = a.template take<double>((nu + 1) * H);
+    w.g = a.template take<double>((nu + 1) * H);
+    w.gb.assign(c.depth, nullptr);
+    w.table.assign(c.depth, nullptr);
+    for (int i = 0; i < c.depth; ++i) {
+        w.gb[i] = a.template take<double>(nu * H);
+        w.table[i] = a.template take<float>(nu * 6 * H);
+    }
+    w.text = a.takeT(L * c.text_dim, e);
+    const int nX = grads ? c.depth + 1 : 2;
+    w.X.assign(nX, nullptr);
+    for (int i = 0; i < nX; ++i) w.X[i] = a.template take<float>(N * H);
+    const int nB = grads ? c.depth : 1;
+    w.blk.assign(nB, Blk{});
+    for (int i = 0; i < nB; ++i) {
+        Blk& b = w.blk[i];
+        b.X1 = a.template take<float>(N * H);
+        b.X2 = a.template take<float>(N * H);
+        b.r0 = a.template take<float>(N);
+        b.r1 = a.template take<float>(N);
+        b.r2 = a.template take<float>(N);
+        b.rc = a.template take<float>(N);
+        b.iq = a.template take<float>(N * nh);
+        b.ik = a.template take<float>(N * nh);
+        b.lse = a.template take<float>(N * nh);
+        b.lse_x = a.template take<float>(N * nh);
+        b.a = a.takeT(N * H, e);
+        b.qkv = a.takeT(N * 3 * H, e);
+        b.qk = a.takeT(N * 2 * H, e);
+        b.O = a.takeT(N * H, e);
+        b.ao = a.takeT(N * H, e);
+        b.cn = a.takeT(N * H, e);
+        b.cqs = a.takeT(N * H, e);
+        b.kv = a.takeT(L * 2 * H, e);
+        b.Ox = a.takeT(N * H, e);
+        b.co = a.takeT(N * H, e);
+        b.f = a.takeT(N * H, e);
+        b.z = a.takeT(N * 4 * H, e);
+        b.h = a.takeT(N * 4 * H, e);
+        b.ff = a.takeT(N * H, e);
+    }
+    w.rf = a.template take<float>(N);
+    w.fin = a.takeT(N * H, e);
+    w.Y = a.takeT(N * H, e);
+    w.V = a.template take<float>(N * D);
+    w.dV = a.takeT(N * D, e);
+    w.loss_part = a.template take<double>(row_chunks(N) + 1024);
+    w.scal = a.template take<double>(8);
+    w.cnt = a.template take<int>(8);
+    if (grads) {
+        const int chunks = row_chunks(N);
+        w.dX = a.template take<float>(N * H);
+        w.sA = a.takeT(N * 4 * H, e);
+        w.sB = a.takeT(N * 3 * H, e);
+        w.s1 = a.takeT(N * H, e);
+        w.s2 = a.takeT(N * H, e);
+        w.dkv = a.takeT(L * 2 * H, e);
+        w.Dvec = a.template take<float>(N * nh);
+        w.part1 = a.template take<float>((int64_t)chunks * std::max<int64_t>(4 * H, 2 * H));
+        w.part2 = a.template take<float>((int64_t)chunks * std::max<int64_t>(4 * H, 2 * H));
+        w.q_splits_x = static_cast<int>(std::min<int64_t>(64, (N + 31) / 32));
+        w.dkv_part = a.template take<float>((int64_t)w.q_splits_x * nh * L * 2 * hd);
+        w.dm = a.template take<float>(nu * 6 * H);
+        w.dg = a.template take<double>(nu * H);
+        w.dgb = a.template take<double>(nu * H);
+    }
+}
+}  // namespace
+
+void Model::plan_workspace(int64_t N, int64_t L, int n_u) {
+    // (called through the templated entry points with ws_ fields preset)
+    (void)N;
+    (void)L;
+    (void)n_u;
+}
+
+// ------------------------------------------------------------------ model
+Model::Model(int device, bool bf16) : device_(device), bf16_(bf16) {
+    MGV_CUDA(cudaSetDevice(device));
+    ws_ = new WS();
+}
+
+Model::~Model() {
+    cudaSetDevice(device_);
+    for (auto& kv : params_) {
+        if (kv.second.f32) cudaFree(kv.second.f32);
+        if (kv.second.bf) cudaFree(kv.second.bf);
+    }
+    if (grad_buf_) cudaFree(grad_buf_);
+    if (comm_) ncclCommDestroy(comm_);
+    delete ws_;
+}
+
+void Model::set_dp(int rank, int world, const uint8_t id[128]) {
+    if (world < 1 || rank < 0 || rank >= world) throw InputError("bad data-parallel rank/world");
+    if (comm_) {
+        ncclCommDestroy(comm_);
+        comm_ = nullptr;
+    }
+    rank_ = rank;
+    world_ = world;
+    if (world == 1) return;
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    MGV_CUDA(cudaSetDevice(device_));
+    MGV_NCCL(ncclCommInitRank(&comm_, world, uid, rank));
+}
+
+static bool is_matrix(const std::string& n) {
+    static const char* mats[] = {"patch.w", "attn.qkv.w", "attn.out.w", "xattn.q.w", "xattn.kv.w",
+                                 "xattn.out.w", "ffn.in.w", "ffn.out.w", "final.w", "out.w"};
+    for (const char* m : mats) {
+        const size_t l = std::strlen(m);
+        if (n.size() >= l && n.compare(n.size() - l, l, m) == 0 && n.find("gmlp") == std::string::npos) return true;
+    }
+    return false;
+}
+
+__global__ void f64_to_f32_bf16(const double* src, int64_t n, float* f, __nv_bfloat16* b) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const float v = static_cast<float>(src[e]);
+        f[e] = v;
+        if (b) b[e] = __float2bfloat16_rn(v);
+    }
+}
+__global__ void f32_to_f64(const float* src, int64_t n, double* dst) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        dst[e] = static_cast<double>(src[e]);
+}
+static int grid_of(int64_t n) { return static_cast<int>(std::min<int64_t>((n + 255) / 256, 1 << 20)); }
+
+void Model::upload(const Cfg& cfg, int64_t n, const char* const* names, const double* const* data,
+                   const int64_t* numel) {
+    validate_cfg(cfg);
+    MGV_CUDA(cudaSetDevice(device_));
+    const int64_t H = cfg.hidden, D = cfg.D();
+    // expected dit.* names and shapes (dit.cpp:143-183)
+    std::map<std::string, std::vector<int64_t>> want;
+    want["dit.patch.w"] = {H, D};
+    want["dit.patch.b"] = {H};
+    want["dit.gmlp.in.w"] = {H, 32};
+    want["dit.gmlp.in.b"] = {H};
+    want["dit.gmlp.out.w"] = {H, H};
+    want["dit.gmlp.out.b"] = {H};
+    want["dit.mod.w"] = {6 * H, H};
+    want["dit.mod.b"] = {6 * H};
+    for (int i = 0; i < cfg.depth; ++i) {
+        auto b = [&](const char* s) { return "dit.blk." + std::to_string(i) + "." + s; };
+        want[b("gscale")] = {H};
+        want[b("attn.qkv.w")] = {3 * H, H};
+        want[b("attn.qkv.b")] = {3 * H};
+        want[b("attn.temp")] = {cfg.heads};
+        want[b("attn.out.w")] = {H, H};
+        want[b("attn.out.b")] = {H};
+        want[b("xattn.prenorm.g")] = {H};
+        want[b("xattn.q.w")] = {H, H};
+        want[b("xattn.q.b")] = {H};
+        want[b("xattn.kv.w")] = {2 * H, cfg.text_dim};
+        want[b("xattn.kv.b")] = {2 * H};
+        want[b("xattn.out.w")] = {H, H};
+        want[b("xattn.out.b")] = {H};
+        want[b("xattn.postnorm.g")] = {H};
+        want[b("ffn.in.w")] = {4 * H, H};
+        want[b("ffn.in.b")] = {4 * H};
+        want[b("ffn.out.w")] = {H, 4 * H};
+        want[b("ffn.out.b")] = {H};
+    }
+    want["dit.final.g"] = {H};
+    want["dit.final.w"] = {H, H};
+    want["dit.final.b"] = {H};
+    want["dit.out.w"] = {D, H};
+    want["dit.out.b"] = {D};
+    std::map<std::string, int64_t> given;
+    for (int64_t i = 0; i < n; ++i) {
+        std::string nm(names[i]);
+        if (nm.rfind("dit.", 0) != 0) continue;  // register_params(..., "dit.") (flowtrain.cpp:260)
+        given[nm] = i;
+    }
+    for (auto& kv : want)
+        if (!given.count(kv.first)) throw InputError("no parameter named \"" + kv.first + "\"");  // params.cpp:24-28
+    // (re)allocate when the configuration changed
+    const bool same = have_params_ && cfg.depth == cfg_.depth && cfg.hidden == cfg_.hidden &&
+                      cfg.heads == cfg_.heads && cfg.text_dim == cfg_.text_dim && cfg.c_z == cfg_.c_z;
+    if (!same) {
+        for (auto& kv : params_) {
+            if (kv.second.f32) cudaFree(kv.second.f32);
+            if (kv.second.bf) cudaFree(kv.second.bf);
+        }
+        params_.clear();
+        sorted_.clear();
+        if (grad_buf_) cudaFree(grad_buf_);
+        grad_buf_ = nullptr;
+        int64_t total = 0;
+        for (auto& kv : want) {
+            DevParam p;
+            p.name = kv.first;
+            p.shape = kv.second;
+            p.numel = 1;
+            for (auto d : p.shape) p.numel *= d;
+            MGV_CUDA(cudaMalloc(&p.f32, sizeof(float) * p.numel));
+            if (bf16_ && is_matrix(p.name)) MGV_CUDA(cudaMalloc(&p.bf, sizeof(__nv_bfloat16) * p.numel));
+            p.grad_off = total;
+            total += (p.numel + 63) / 64 * 64;
+            params_[p.name] = p;
+        }
+        grad_numel_ = total;
+        MGV_CUDA(cudaMalloc(&grad_buf_, sizeof(float) * total));
+        for (auto& kv : params_) {
+            kv.second.grad = grad_buf_ + kv.second.grad_off;
+            sorted_.push_back(&kv.second);
+        }
+    }
+    cfg_ = cfg;
+    double* staging = nullptr;
+    int64_t stage_n = 0;
+    for (auto& kv : params_) stage_n = std::max(stage_n, kv.second.numel);
+    MGV_CUDA(cudaMalloc(&staging, sizeof(double) * stage_n));
+    for (auto& kv : params_) {
+        DevParam& p = kv.second;
+        const int64_t gi = given[p.name];
+        if (numel[gi] != p.numel)
+            throw DimensionError("parameter " + p.name + " has " + std::to_string(numel[gi]) + " elements, expected " +
+                                 std::to_string(p.numel));
+        MGV_CUDA(cudaMemcpyAsync(staging, data[gi], sizeof(double) * p.numel, cudaMemcpyHostToDevice, stream_));
+        f64_to_f32_bf16<<<grid_of(p.numel), 256, 0, stream_>>>(staging, p.numel, p.f32, p.bf);
+        MGV_CUDA(cudaGetLastError());
+    }
+    MGV_CUDA(cudaStreamSynchronize(stream_));
+    cudaFree(staging);
+    have_params_ = true;
+}
+
+const DevParam& Model::P(const std::string& name) const {
+    auto it = params_.find(name);
+    if (it == params_.end()) throw InputError("no parameter named \"" + name + "\"");
+    return it->second;
+}
+const void* Model::W(const std::string& name) const {
+    const DevParam& p = P(name);
+    return bf16_ ? static_cast<const void*>(p.bf) : static_cast<const void*>(p.f32);
+}
+float* Model::G(const std::string& name) const { return P(name).grad; }
+
+// ------------------------------------------------------------------ helpers
+namespace {
+inline Mat KM(const void* p, int64_t ld) { return Mat{p, ld, Major::K}; }
+inline Mat MN(const void* p, int64_t ld) { return Mat{p, ld, Major::MN}; }
+template <class T>
+inline T* tp(void* p) { return static_cast<T*>(p); }
+template <class T>
+inline const T* tp(const void* p) { return static_cast<const T*>(p); }
+template <class T>
+inline void* off(void* p, int64_t n) { return static_cast<T*>(p) + n; }
+template <class T>
+inline const void* off(const void* p, int64_t n) { return static_cast<const T*>(p) + n; }
+}  // namespace
+
+template <class T>
+static void attention_fwd(bool bf16, const AttnProblem& p, cudaStream_t s) {
+    if (bf16 && attn_tc_supported(p.hd, p.Nk))
+        attn_fwd_tc(p, s);
+    else
+        attn_fwd_simt<T>(p, s);
+}
+template <class T>
+static void attention_bwd(bool bf16, const AttnBwdProblem& p, cudaStream_t s) {
+    if (bf16 && attn_tc_supported(p.f.hd, p.f.Nk))
+        attn_bwd_tc(p, s);
+    else
+        attn_bwd_simt<T>(p, s);
+}
+
+// ------------------------------------------------------------------ block forward (dit.cpp:279-313)
+template <class T>
+void Model::block_fwd(int i, int64_t N) {
+    WS& w = *ws_;
+    const bool bf = bf16_;
+    cudaStream_t s = stream_;
+    const int64_t H = cfg_.H(), nh = cfg_.heads, hd = cfg_.hd(), L = w.L;
+    Blk& b = w.blk[w.grads ? i : 0];
+    const float* Xin = w.X[w.grads ? i : (i % 2)];
+    float* Xout = w.X[w.grads ? i + 1 : ((i + 1) % 2)];
+    const float* tab = w.table[i];
+    const int64_t tld = 6 * H;
+    const int n = static_cast<int>(N);
+    // self-attention: a = rms(x)(1+sc1)+sh1 (dit.cpp:287)
+    rms_mod<T>(Xin, n, H, tab, tld, 0, H, w.mod_id, tp<T>(b.a), b.r0, s);
+    gemm(bf, KM(b.a, H), KM(W(blk(i, "attn.qkv.w")), H), n, 3 * H, H,
+         EpiStore<T>{tp<T>(b.qkv), 3 * H, P(blk(i, "attn.qkv.b")).f32, 1.0f, n, int(3 * H)}, s);  // dit.cpp:288
+    qk_norm_rope<T>(tp<T>(b.qkv), n, H, nh, P(blk(i, "attn.temp")).f32, w.cs, tp<T>(b.qk), b.iq, b.ik, s);  // :289-294
+    AttnProblem ap{b.qk, 2 * H, off<T>(b.qk, H), 2 * H, off<T>(b.qkv, 2 * H), 3 * H, b.O, H, b.lse,
+                   n, n, int(nh), int(hd)};
+    attention_fwd<T>(bf, ap, s);  // mha (autodiff.cpp:755-793)
+    gemm(bf, KM(b.O, H), KM(W(blk(i, "attn.out.w")), H), n, H, H,
+         EpiGateResid<T>{Xin, b.X1, H, tp<T>(b.ao), H, P(blk(i, "attn.out.b")).f32, tab + 2 * H, tld, w.mod_id, n,
+                         int(H)},
+         s);  // x += ao * gt1 (dit.cpp:295-297)
+    // cross-attention (dit.cpp:300-305)
+    rms_gain<T>(b.X1, n, H, P(blk(i, "xattn.prenorm.g")).f32, tp<T>(b.cn), b.r1, s);
+    const float xscale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd)));
+    gemm(bf, KM(b.cn, H), KM(W(blk(i, "xattn.q.w")), H), n, H, H,
+         EpiStore<T>{tp<T>(b.cqs), H, P(blk(i, "xattn.q.b")).f32, xscale, n, int(H)}, s);
+    gemm(bf, KM(w.text, cfg_.text_dim), KM(W(blk(i, "xattn.kv.w")), cfg_.text_dim), int(L), 2 * H, cfg_.text_dim,
+         EpiStore<T>{tp<T>(b.kv), 2 * H, P(blk(i, "xattn.kv.b")).f32, 1.0f, int(L), int(2 * H)}, s);
+    AttnProblem xp{b.cqs, H, b.kv, 2 * H, off<T>(b.kv, H), 2 * H, b.Ox, H, b.lse_x, n, int(L), int(nh), int(hd)};
+    attention_fwd<T>(bf, xp, s);
+    gemm(bf, KM(b.Ox, H), KM(W(blk(i, "xattn.out.w")), H), n, H, H,
+         EpiStore<T>{tp<T>(b.co), H, P(blk(i, "xattn.out.b")).f32, 1.0f, n, int(H)}, s);
+    postnorm_resid<T>(b.X1, tp<T>(b.co), n, H, P(blk(i, "xattn.postnorm.g")).f32, b.X2, b.rc, s);
+    // feed-forward (dit.cpp:308-311)
+    rms_mod<T>(b.X2, n, H, tab, tld, 3 * H, 4 * H, w.mod_id, tp<T>(b.f), b.r2, s);
+    gemm(bf, KM(b.f, H), KM(W(blk(i, "ffn.in.w")), H), n, 4 * H, H,
+         EpiBiasSilu<T>{tp<T>(b.z), tp<T>(b.h), 4 * H, P(blk(i, "ffn.in.b")).f32, n, int(4 * H)}, s);
+    gemm(bf, KM(b.h, 4 * H), KM(W(blk(i, "ffn.out.w")), 4 * H), n, H, 4 * H,
+         EpiGateResid<T>{b.X2, Xout, H, tp<T>(b.ff), H, P(blk(i, "ffn.out.b")).f32, tab + 5 * H, tld, w.mod_id, n,
+                         int(H)},
+         s);
+}
+
+// ------------------------------------------------------------------ block backward
+template <class T>
+void Model::block_bwd(int i, int64_t N) {
+    WS& w = *ws_;
+    const bool bf = bf16_;
+    cudaStream_t s = stream_;
+    const int64_t H = cfg_.H(), nh = cfg_.heads, hd = cfg_.hd(), L = w.L;
+    const int n = static_cast<int>(N), nu = w.n_u, chunks = row_chunks(n);
+    Blk& b = w.blk[i];
+    const float* Xin = w.X[i];
+    const float* tab = w.table[i];
+    const int64_t tld = 6 * H;
+    float* dX = w.dX;
+    float* dm = w.dm;
+    // ---- FFN (dit.cpp:308-311)
+    gate_bwd<T>(dX, tp<T>(b.ff), tab, tld, 5 * H, w.mod_id, nu, n, H, tp<T>(w.s1), w.part1, w.part2, s);
+    reduce_chunks_grouped(w.part1, chunks, nu, H, dm + 5 * H, 6 * H, 1.0f, 0, s);  // d gt2
+    reduce_chunks(w.part2, chunks, H, G(blk(i, "ffn.out.b")), 1.0f, 1, s);
+    gemm(bf, MN(w.s1, H), MN(b.h, 4 * H), H, 4 * H, n, EpiF32{G(blk(i, "ffn.out.w")), 4 * H, nullptr, 1.0f, 1, int(H), int(4 * H)}, s);
+    gemm(bf, KM(w.s1, H), MN(W(blk(i, "ffn.out.w")), 4 * H), n, 4 * H, H,
+         EpiSiluBwd<T>{tp<T>(w.sA), tp<T>(b.z), 4 * H, n, int(4 * H)}, s);  // dz = (dff W2) silu'(z)
+    colsum<T>(tp<T>(w.sA), 4 * H, n, 4 * H, w.part1, s);
+    reduce_chunks(w.part1, chunks, 4 * H, G(blk(i, "ffn.in.b")), 1.0f, 1, s);
+    gemm(bf, MN(w.sA, 4 * H), MN(b.f, H), 4 * H, H, n, EpiF32{G(blk(i, "ffn.in.w")), H, nullptr, 1.0f, 1, int(4 * H), int(H)}, s);
+    gemm(bf, KM(w.sA, 4 * H), MN(W(blk(i, "ffn.in.w")), H), n, H, 4 * H,
+         EpiStore<T>{tp<T>(w.s1), H, nullptr, 1.0f, n, int(H)}, s);  // df
+    rms_mod_bwd<T>(tp<T>(w.s1), b.X2, b.r2, tab, tld, 3 * H, 4 * H, w.mod_id, nu, n, H, dX, w.part1, w.part2, s);
+    reduce_chunks_grouped(w.part1, chunks, nu, H, dm + 3 * H, 6 * H, 1.0f, 0, s);  // d sh2
+    reduce_chunks_grouped(w.part2, chunks, nu, H, dm + 4 * H, 6 * H, 1.0f, 0, s);  // d sc2
+    // ---- cross-attention (dit.cpp:300-305)
+    postnorm_bwd<T>(dX, tp<T>(b.co), b.rc, P(blk(i, "xattn.postnorm.g")).f32, n, H, tp<T>(w.s1), w.part1, s);
+    reduce_chunks(w.part1, chunks, H, G(blk(i, "xattn.postnorm.g")), 1.0f, 1, s);
+    colsum<T>(tp<T>(w.s1), H, n, H, w.part1, s);
+    reduce_chunks(w.part1, chunks, H, G(blk(i, "xattn.out.b")), 1.0f, 1, s);
+    gemm(bf, MN(w.s1, H), MN(b.Ox, H), H, H, n, EpiF32{G(blk(i, "xattn.out.w")), H, nullptr, 1.0f, 1, int(H), int(H)}, s);
+    gemm(bf, KM(w.s1, H), MN(W(blk(i, "xattn.out.w")), H), n, H, H, EpiStore<T>{tp<T>(w.s2), H, nullptr, 1.0f, n, int(H)}, s);
+    AttnBwdProblem xb{AttnProblem{b.cqs, H, b.kv, 2 * H, off<T>(b.kv, H), 2 * H, b.Ox, H, b.lse_x, n, int(L), int(nh), int(hd)},
+                      w.s2, H, w.Dvec, w.s1, H, w.dkv, 2 * H, off<T>(w.dkv, H), 2 * H, w.dkv_part, w.q_splits_x};
+    attention_bwd<T>(bf, xb, s);
+    const float xscale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd)));
+    gemm(bf, MN(w.dkv, 2 * H), MN(w.text, cfg_.text_dim), 2 * H, cfg_.text_dim, int(L),
+         EpiF32{G(blk(i, "xattn.kv.w")), cfg_.text_dim, nullptr, 1.0f, 1, int(2 * H), int(cfg_.text_dim)}, s);
+    colsum<T>(tp<T>(w.dkv), 2 * H, int(L), 2 * H, w.part1, s);
+    reduce_chunks(w.part1, row_chunks(int(L)), 2 * H, G(blk(i, "xattn.kv.b")), 1.0f, 1, s);
+    colsum<T>(tp<T>(w.s1), H, n, H, w.part1, s);
+    reduce_chunks(w.part1, chunks, H, G(blk(i, "xattn.q.b")), xscale, 1, s);
+    gemm(bf, MN(w.s1, H), MN(b.cn, H), H, H, n, EpiF32{G(blk(i, "xattn.q.w")), H, nullptr, xscale, 1, int(H), int(H)}, s);
+    gemm(bf, KM(w.s1, H), MN(W(blk(i, "xattn.q.w")), H), n, H, H, EpiStore<T>{tp<T>(w.s2), H, nullptr, xscale, n, int(H)}, s);
+    rms_gain_bwd<T>(tp<T>(w.s2), b.X1, b.r1, P(blk(i, "xattn.prenorm.g")).f32, n, H, dX, 1, w.part1, s);
+    reduce_chunks(w.part1, chunks, H, G(blk(i, "xattn.prenorm.g")), 1.0f, 1, s);
+    // ---- self-attention (dit.cpp:287-297)
+    gate_bwd<T>(dX, tp<T>(b.ao), tab, tld, 2 * H, w.mod_id, nu, n, H, tp<T>(w.s1), w.part1, w.part2, s);
+    reduce_chunks_grouped(w.part1, chunks, nu, H, dm + 2 * H, 6 * H, 1.0f, 0, s);  // d gt1
+    reduce_chunks(w.part2, chunks, H, G(blk(i, "attn.out.b")), 1.0f, 1, s);
+    gemm(bf, MN(w.s1, H), MN(b.O, H), H, H, n, EpiF32{G(blk(i, "attn.out.w")), H, nullptr, 1.0f, 1, int(H), int(H)}, s);
+    gemm(bf, KM(w.s1, H), MN(W(blk(i, "attn.out.w")), H), n, H, H, EpiStore<T>{tp<T>(w.s2), H, nullptr, 1.0f, n, int(H)}, s);
+    AttnBwdProblem ab{AttnProblem{b.qk, 2 * H, off<T>(b.qk, H), 2 * H, off<T>(b.qkv, 2 * H), 3 * H, b.O, H, b.lse, n, n, int(nh), int(hd)},
+                      w.s2, H, w.Dvec, w.sB, 3 * H, off<T>(w.sB, H), 3 * H, off<T>(w.sB, 2 * H), 3 * H, nullptr, 1};
+    attention_bwd<T>(bf, ab, s);
+    qk_norm_rope_bwd<T>(tp<T>(w.sB), tp<T>(b.qkv), n, H, nh, P(blk(i, "attn.temp")).f32, w.cs, b.iq, b.ik, w.part1, s);
+    reduce_chunks(w.part1, chunks, nh, G(blk(i, "attn.temp")), 1.0f, 1, s);
+    colsum<T>(tp<T>(w.sB), 3 * H, n, 3 * H, w.part1, s);
+    reduce_chunks(w.part1, chunks, 3 * H, G(blk(i, "attn.qkv.b")), 1.0f, 1, s);
+    gemm(bf, MN(w.sB, 3 * H), MN(b.a, H), 3 * H, H, n, EpiF32{G(blk(i, "attn.qkv.w")), H, nullptr, 1.0f, 1, int(3 * H), int(H)}, s);
+    gemm(bf, KM(w.sB, 3 * H), MN(W(blk(i, "attn.qkv.w")), H), n, H, 3 * H, EpiStore<T>{tp<T>(w.s1), H, nullptr, 1.0f, n, int(H)}, s);
+    rms_mod_bwd<T>(tp<T>(w.s1), Xin, b.r0, tab, tld, 0, H, w.mod_id, nu, n, H, dX, w.part1, w.part2, s);
+    reduce_chunks_grouped(w.part1, chunks, nu, H, dm, 6 * H, 1.0f, 0, s);      // d sh1
+    reduce_chunks_grouped(w.part2, chunks, nu, H, dm + H, 6 * H, 1.0f, 0, s);  // d sc1
+    // ---- shared modulation head (dit.cpp:280-283)
+    modulation_bwd(dm, w.gb[i], P("dit.mod.w").f32, nu, H, G("dit.mod.w"), G("dit.mod.b"), w.dgb, s);
+    gscale_bwd(w.dgb, w.g, P(blk(i, "gscale")).f32, nu, H, G(blk(i, "gscale")), w.dg, s);
+}
+
+// ------------------------------------------------------------------ sample forward / backward
+// rows_in: (N, D) T on device (for velocity) or null with X[0] preloaded (dit_forward).
+template <class T>
+void Model::forward_sample(const DevSample& smp, const void* rows_in, const double* taus_unique, int n_u,
+                           const int32_t* mod_id, double fps, bool grads, bool head, void* out) {
+    (void)smp;
+    (void)taus_unique;
+    (void)mod_id;
+    (void)out;
+    WS& w = *ws_;
+    cudaStream_t s = stream_;
+    const bool bf = bf16_;
+    const int64_t H = cfg_.H(), D = cfg_.D();
+    const int n = static_cast<int>(w.N);
+    // global embedding + per-block modulation tables over the n_u unique timesteps (dit.cpp:236-255, 280-283)
+    global_embed(w.taus, n_u, fps, P("dit.gmlp.in.w").f32, P("dit.gmlp.in.b").f32, P("dit.gmlp.out.w").f32,
+                 P("dit.gmlp.out.b").f32, H, w.phi, w.z_in, w.h_in, w.g, s);
+    for (int i = 0; i < cfg_.depth; ++i)
+        modulation_table(w.g, P(blk(i, "gscale")).f32, P("dit.mod.w").f32, P("dit.mod.b").f32, n_u, H, w.gb[i],
+                         w.table[i], s);
+    rope_table(w.coords, n, cfg_.rope[0], cfg_.rope[1], cfg_.rope[2], w.cs, s);
+    if (head)  // patch embedding (dit.cpp:327)
+        gemm(bf, KM(rows_in, D), KM(W("dit.patch.w"), D), n, H, D,
+             EpiF32{w.X[0], H, P("dit.patch.b").f32, 1.0f, 0, n, int(H)}, s);
+    (void)grads;
+    for (int i = 0; i < cfg_.depth; ++i) block_fwd<T>(i, w.N);
+    const float* Xf = w.X[w.grads ? cfg_.depth : (cfg_.depth % 2)];
+    rms_gain<T>(Xf, n, H, P("dit.final.g").f32, tp<T>(w.fin), w.rf, s);  // dit.cpp:314
+    if (head) {
+        gemm(bf, KM(w.fin, H), KM(W("dit.final.w"), H), n, H, H,
+             EpiStore<T>{tp<T>(w.Y), H, P("dit.final.b").f32, 1.0f, n, int(H)}, s);  // dit.cpp:315
+        gemm(bf, KM(w.Y, H), KM(W("dit.out.w"), H), n, D, H, EpiF32{w.V, D, P("dit.out.b").f32, 1.0f, 0, n, int(D)},
+             s);  // dit.cpp:331
+    } else {
+        gemm(bf, KM(w.fin, H), KM(W("dit.final.w"), H), n, H, H,
+             EpiF32{static_cast<float*>(out), H, P("dit.final.b").f32, 1.0f, 0, n, int(H)}, s);
+    }
+}
+
+template <class T>
+void Model::backward_sample(const void* dV) {
+    WS& w = *ws_;
+    cudaStream_t s = stream_;
+    const bool bf = bf16_;
+    const int64_t H = cfg_.H(), D = cfg_.D();
+    const int n = static_cast<int>(w.N), chunks = row_chunks(n), nu = w.n_u;
+    // heads (dit.cpp:331, 314-315)
+    gemm(bf, MN(dV, D), MN(w.Y, H), int(D), H, n, EpiF32{G("dit.out.w"), H, nullptr, 1.0f, 1, int(D), int(H)}, s);
+    colsum<T>(tp<T>(dV), D, n, D, w.part1, s);
+    reduce_chunks(w.part1, chunks, D, G("dit.out.b"), 1.0f, 1, s);
+    gemm(bf, KM(dV, D), MN(W("dit.out.w"), H), n, H, D, EpiStore<T>{tp<T>(w.s1), H, nullptr, 1.0f, n, int(H)}, s);
+    gemm(bf, MN(w.s1, H), MN(w.fin, H), H, H, n, EpiF32{G("dit.final.w"), H, nullptr, 1.0f, 1, int(H), int(H)}, s);
+    colsum<T>(tp<T>(w.s1), H, n, H, w.part1, s);
+    reduce_chunks(w.part1, chunks, H, G("dit.final.b"), 1.0f, 1, s);
+    gemm(bf, KM(w.s1, H), MN(W("dit.final.w"), H), n, H, H, EpiStore<T>{tp<T>(w.s2), H, nullptr, 1.0f, n, int(H)}, s);
+    rms_gain_bwd<T>(tp<T>(w.s2), w.X[cfg_.depth], w.rf, P("dit.final.g").f32, n, H, w.dX, 0, w.part1, s);
+    reduce_chunks(w.part1, chunks, H, G("dit.final.g"), 1.0f, 1, s);
+    MGV_CUDA(cudaMemsetAsync(w.dg, 0, sizeof(double) * nu * H, s));
+    for (int i = static_cast<int>(cfg_.depth) - 1; i >= 0; --i) block_bwd<T>(i, w.N);
+    // patch embedding (rows are constants, dit.cpp:327)
+    convert_f32<T>(w.dX, (int64_t)n * H, tp<T>(w.s1), s);
+    gemm(bf, MN(w.s1, H), MN(w.rows, D), H, int(D), n, EpiF32{G("dit.patch.w"), D, nullptr, 1.0f, 1, int(H), int(D)}, s);
+    colsum<float>(w.dX, H, n, H, w.part1, s);
+    reduce_chunks(w.part1, chunks, H, G("dit.patch.b"), 1.0f, 1, s);
+    // global embedding MLPs (dit.cpp:245-254)
+    global_embed_bwd(w.dg, nu, w.phi, w.z_in, w.h_in, P("dit.gmlp.out.w").f32, H, G("dit.gmlp.in.w"),
+                     G("dit.gmlp.in.b"), G("dit.gmlp.out.w"), G("dit.gmlp.out.b"), s);
+}
+
+// ------------------------------------------------------------------ flow step
+template <class T>
+void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* text_dev, int64_t L, double fps,
+                           double* loss, double* grad_norm, double* const* v_dev) {
+    if (!have_params_) throw InputError("no parameters uploaded");
+    if (n < 1) throw InputError("empty batch");  // flowtrain.cpp:258
+    WS& w = *ws_;
+    cudaStream_t s = stream_;
+    const int64_t H = cfg_.H(), D = cfg_.D();
+    int64_t maxN = 0;
+    for (int64_t k = 0; k < n; ++k) maxN = std::max(maxN, samples[k].N);
+    // workspace
+    w.N = maxN;
+    w.L = L;
+    w.n_u = 2;
+    w.esz = bf16_ ? 2 : 4;
+    w.grads = true;
+    {
+        Sizer sz{true, 0, &arena_};
+        layout_ws(w, sz, cfg_, true);
+        arena_.reserve(sz.bytes);
+        arena_.reset();
+        Sizer real{false, 0, &arena_};
+        layout_ws(w, real, cfg_, true);
+    }
+    MGV_CUDA(cudaMemsetAsync(grad_buf_, 0, sizeof(float) * grad_numel_, s));
+    convert_rows<T>(text_dev, L * cfg_.text_dim, tp<T>(w.text), s);
+    const int64_t B_global = n * world_;
+    double loss_sum = 0.0;
+    cudaEvent_t e0, e1;
+    MGV_CUDA(cudaEventCreate(&e0));
+    MGV_CUDA(cudaEventCreate(&e1));
+    MGV_CUDA(cudaEventRecord(e0, s));
+    std::vector<double> sample_loss(n);
+    for (int64_t k = 0; k < n; ++k) {
+        const DevSample& sm = samples[k];
+        w.N = sm.N;
+        const int N = static_cast<int>(sm.N);
+        MGV_CUDA(cudaMemcpyAsync(w.coords, sm.coords, sizeof(int32_t) * 3 * N, cudaMemcpyDeviceToDevice, s));
+        // interpolate + condition mask (flowtrain.cpp:265-267); taus {t, 0} (dit.cpp:242 dedup)
+        prep_flow_sample<T>(sm.clean, sm.noise, w.coords, N, int(D), sm.t, sm.first_frame, tp<T>(w.rows),
+                            w.vt, w.lmask, w.mod_id, s);
+        const double taus[2] = {sm.t, 0.0};
+        MGV_CUDA(cudaMemcpyAsync(w.taus, taus, sizeof(taus), cudaMemcpyHostToDevice, s));
+        w.n_u = sm.first_frame ? 2 : 1;
+        forward_sample<T>(sm, w.rows, taus, w.n_u, w.mod_id, fps, true, true, nullptr);
+        if (v_dev && v_dev[k]) f32_to_f64<<<grid_of(N * D), 256, 0, s>>>(w.V, N * D, v_dev[k]);
+        // masked mean loss (autodiff.cpp:466-491)
+        count_mask(w.lmask, N, w.cnt, s);
+        flow_loss_fwd<T>(w.V, w.vt, w.lmask, N, int(D), w.loss_part, s);
+        sum_double(w.loss_part, row_chunks(N), w.scal, s);
+        int cnt = 0;
+        double sq = 0.0;
+        MGV_CUDA(cudaMemcpyAsync(&cnt, w.cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
+        MGV_CUDA(cudaMemcpyAsync(&sq, w.scal, sizeof(double), cudaMemcpyDeviceToHost, s));
+        MGV_CUDA(cudaStreamSynchronize(s));
+        const double lb = cnt > 0 ? sq / (static_cast<double>(cnt) * D) : 0.0;
+        sample_loss[k] = lb;
+        loss_sum += lb;
+        if (!std::isfinite(lb)) throw NumericError("flow loss is not finite");  // flowtrain.cpp:276
+        if (cnt == 0) continue;  // all rows masked: zero loss, zero gradient (autodiff.cpp:482)
+        const float coef = static_cast<float>(2.0 / (static_cast<double>(B_global) * cnt * D));
+        flow_loss_bwd<T>(w.V, w.vt, w.lmask, N, int(D), coef, tp<T>(w.dV), s);
+        backward_sample<T>(w.dV);
+    }
+    if (world_ > 1) {
+        MGV_NCCL(ncclAllReduce(grad_buf_, grad_buf_, grad_numel_, ncclFloat, ncclSum, comm_, s));
+        double* dl = w.scal + 1;
+        MGV_CUDA(cudaMemcpyAsync(dl, &loss_sum, sizeof(double), cudaMemcpyHostToDevice, s));
+        MGV_NCCL(ncclAllReduce(dl, dl, 1, ncclDouble, ncclSum, comm_, s));
+        MGV_CUDA(cudaMemcpyAsync(&loss_sum, dl, sizeof(double), cudaMemcpyDeviceToHost, s));
+    }
+    sumsq(grad_buf_, grad_numel_, w.loss_part, w.scal + 2, s);  // grad_norm (flowtrain.cpp:284-289)
+    double gsq = 0.0;
+    MGV_CUDA(cudaMemcpyAsync(&gsq, w.scal + 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    MGV_CUDA(cudaEventRecord(e1, s));
+    MGV_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.0f;
+    MGV_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    last_ms_ = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *loss = loss_sum / static_cast<double>(B_global);  // flowtrain.cpp:273
+    *grad_norm = std::sqrt(gsq);
+}
+
+void Model::flow_step_dev(int64_t n, const DevSample* samples, const double* text_dev, int64_t L, double fps,
+                          double* loss, double* grad_norm, double* const* v_dev) {
+    MGV_CUDA(cudaSetDevice(device_));
+    if (bf16_)
+        flow_step_impl<__nv_bfloat16>(n, samples, text_dev, L, fps, loss, grad_norm, v_dev);
+    else
+        flow_step_impl<float>(n, samples, text_dev, L, fps, loss, grad_norm, v_dev);
+}
+
+// host-buffer flow step: validate, stage to device, run, read back
+static void validate_mask_host(const mgv_flow_sample& s, int64_t N) {  // flowtrain.cpp:61-81
+    if (!s.conditioned) return;
+    std::vector<int> unit(static_cast<size_t>(s.dims[0]), -1);
+    for (int64_t i = 0; i < N; ++i) {
+        const int u = s.coords[3 * i];
+        if (u < 0 || u >= s.dims[0]) throw DimensionError("condition mask does not match the token grid");
+        const int f = s.conditioned[i] ? 1 : 0;
+        int& seen = unit[static_cast<size_t>(u)];
+        if (seen == -1)
+            seen = f;
+        else if (seen != f)
+            throw InputError("conditioned tokens must cover whole latent units");
+    }
+}
+
+void Model::flow_step(int64_t n, const mgv_flow_sample* samples, const double* text, int64_t L, double fps,
+                      double* loss, double* grad_norm, double* const* grads_out, double* const* v_out) {
+    MGV_CUDA(cudaSetDevice(device_));
+    if (n < 1) throw InputError("empty batch");
+    if (L < 1 || L > 1 << 20) throw DimensionError("text embeddings must be (L, text_dim)");
+    const int64_t D = cfg_.D();
+    std::vector<DevSample> ds(n);
+    std::vector<void*> allocs;
+    auto dalloc = [&](size_t bytes) {
+        void* p = nullptr;
+        MGV_CUDA(cudaMallocAsync(&p, bytes, stream_));
+        allocs.push_back(p);
+        return p;
+    };
+    try {
+        for (int64_t k = 0; k < n; ++k) {
+            const mgv_flow_sample& s = samples[k];
+            const int64_t N = s.dims[0] * s.dims[1] * s.dims[2];
+            if (N < 1) throw DimensionError("empty token grid");
+            if (!(s.t >= 0.0 && s.t <= 1.0)) throw InputError("interpolation time outside [0, 1]");  // flowtrain.cpp:11
+            validate_mask_host(s, N);
+            bool cond_any = false;
+            if (s.conditioned)
+                for (int64_t i = 0; i < N && !cond_any; ++i) cond_any = s.conditioned[i] != 0;
+            DevSample d;
+            d.N = N;
+            std::memcpy(d.dims, s.dims, sizeof(d.dims));
+            auto* c = static_cast<int32_t*>(dalloc(sizeof(int32_t) * 3 * N));
+            MGV_CUDA(cudaMemcpyAsync(c, s.coords, sizeof(int32_t) * 3 * N, cudaMemcpyHostToDevice, stream_));
+            auto* cl = static_cast<double*>(dalloc(sizeof(double) * N * D));
+            auto* nz = static_cast<double*>(dalloc(sizeof(double) * N * D));
+            // the conditioned rows carry condition_latents (default: clean rows, first_frame_mask)
+            MGV_CUDA(cudaMemcpyAsync(cl, s.clean_rows, sizeof(double) * N * D, cudaMemcpyHostToDevice, stream_));
+            MGV_CUDA(cudaMemcpyAsync(nz, s.noise, sizeof(double) * N * D, cudaMemcpyHostToDevice, stream_));
+            d.coords = c;
+            d.clean = cl;
+            d.noise = nz;
+            d.t = s.t;
+            if (cond_any) {
+                // the device prep marks unit-0 rows; general masks are validated unit-aligned above and we
+                // require them to be exactly the first unit (first_frame_mask), the only producer in the reference
+                for (int64_t i = 0; i < N; ++i)
+                    if ((s.conditioned[i] != 0) != (s.coords[3 * i] == 0))
+                        throw InputError("only first-frame conditioning masks are supported on device");
+                if (s.condition_latents && s.condition_latents != s.clean_rows)
+                    throw InputError("condition_latents must be the clean rows (first_frame_mask)");
+                d.first_frame = 1;
+            }
+            ds[k] = d;
+        }
+        auto* tx = static_cast<double*>(dalloc(sizeof(double) * L * cfg_.text_dim));
+        MGV_CUDA(cudaMemcpyAsync(tx, text, sizeof(double) * L * cfg_.text_dim, cudaMemcpyHostToDevice, stream_));
+        std::vector<double*> vdev(n, nullptr);
+        if (v_out)
+            for (int64_t k = 0; k < n; ++k)
+                if (v_out[k]) vdev[k] = static_cast<double*>(dalloc(sizeof(double) * ds[k].N * D));
+        flow_step_dev(n, ds.data(), tx, L, fps, loss, grad_norm, v_out ? vdev.data() : nullptr);
+        if (v_out)
+            for (int64_t k = 0; k < n; ++k)
+                if (v_out[k])
+                    MGV_CUDA(cudaMemcpyAsync(v_out[k], vdev[k], sizeof(double) * ds[k].N * D, cudaMemcpyDeviceToHost,
+                                             stream_));
+        if (grads_out) {
+            int64_t maxn = 0;
+            for (auto* p : sorted_) maxn = std::max(maxn, p->numel);
+            auto* gd = static_cast<double*>(dalloc(sizeof(double) * maxn));
+            for (size_t k = 0; k < sorted_.size(); ++k) {
+                if (!grads_out[k]) continue;
+                f32_to_f64<<<grid_of(sorted_[k]->numel), 256, 0, stream_>>>(sorted_[k]->grad, sorted_[k]->numel, gd);
+                MGV_CUDA(cudaMemcpyAsync(grads_out[k], gd, sizeof(double) * sorted_[k]->numel, cudaMemcpyDeviceToHost,
+                                         stream_));
+                MGV_CUDA(cudaStreamSynchronize(stream_));
+            }
+        }
+        MGV_CUDA(cudaStreamSynchronize(stream_));
+    } catch (...) {
+        for (void* p : allocs) cudaFreeAsync(p, stream_);
+        throw;
+    }
+    for (void* p : allocs) cudaFreeAsync(p, stream_);
+}
+
+// ------------------------------------------------------------------ value API (forward only)
+template <class T>
+void Model::value_forward(const double* in, int64_t N, const int32_t* coords, const int64_t dims[3],
+                          const double* text, int64_t L, const double* tau, double fps, double* out, bool velocity) {
+    if (!have_params_) throw InputError("no parameters uploaded");
+    WS& w = *ws_;
+    cudaStream_t s = stream_;
+    const int64_t H = cfg_.H(), D = cfg_.D();
+    if (N != dims[0] * dims[1] * dims[2]) throw DimensionError("token count does not match the grid");
+    // unique timesteps -> modulation rows (dit.cpp:239-242 validates each)
+    std::vector<double> uniq;
+    std::vector<int32_t> mid(static_cast<size_t>(N));
+    std::unordered_map<uint64_t, int> seen;
+    for (int64_t i = 0; i < N; ++i) {
+        if (!(tau[i] >= 0.0 && tau[i] <= 1.0)) throw InputError("timestep outside [0, 1]");
+        uint64_t key;
+        std::memcpy(&key, &tau[i], sizeof(key));
+        if (tau[i] == 0.0) key = 0;  // +0 / -0
+        auto it = seen.find(key);
+        if (it == seen.end()) {
+            it = seen.emplace(key, static_cast<int>(uniq.size())).first;
+            uniq.push_back(tau[i]);
+        }
+        mid[static_cast<size_t>(i)] = it->second;
+    }
+    w.N = N;
+    w.L = L;
+    w.n_u = static_cast<int>(uniq.size());
+    w.esz = bf16_ ? 2 : 4;
+    w.grads = false;
+    {
+        Sizer sz{true, 0, &arena_};
+        layout_ws(w, sz, cfg_, false);
+        arena_.reserve(sz.bytes);
+        arena_.reset();
+        Sizer real{false, 0, &arena_};
+        layout_ws(w, real, cfg_, false);
+    }
+    const int64_t in_cols = velocity ? D : H;
+    double* din = nullptr;
+    MGV_CUDA(cudaMallocAsync(&din, sizeof(double) * std::max(N * in_cols, L * cfg_.text_dim), s));
+    MGV_CUDA(cudaMemcpyAsync(w.coords, coords, sizeof(int32_t) * 3 * N, cudaMemcpyHostToDevice, s));
+    MGV_CUDA(cudaMemcpyAsync(w.mod_id, mid.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, s));
+    MGV_CUDA(cudaMemcpyAsync(w.taus, uniq.data(), sizeof(double) * uniq.size(), cudaMemcpyHostToDevice, s));
+    MGV_CUDA(cudaMemcpyAsync(din, text, sizeof(double) * L * cfg_.text_dim, cudaMemcpyHostToDevice, s));
+    convert_rows<T>(din, L * cfg_.text_dim, tp<T>(w.text), s);
+    MGV_CUDA(cudaMemcpyAsync(din, in, sizeof(double) * N * in_cols, cudaMemcpyHostToDevice, s));
+    float* outf = nullptr;
+    MGV_CUDA(cudaMallocAsync(&outf, sizeof(float) * N * std::max(H, D), s));
+    DevSample dummy;
+    if (velocity) {
+        convert_rows<T>(din, N * D, tp<T>(w.rows), s);
+        forward_sample<T>(dummy, w.rows, uniq.data(), w.n_u, nullptr, fps, false, true, nullptr);
+        f32_to_f64<<<grid_of(N * D), 256, 0, s>>>(w.V, N * D, din);
+        MGV_CUDA(cudaMemcpyAsync(out, din, sizeof(double) * N * D, cudaMemcpyDeviceToHost, s));
+    } else {
+        // tokens enter the residual stream directly (dit.cpp:369)
+        f64_to_f32_bf16<<<grid_of(N * H), 256, 0, s>>>(din, N * H, w.X[0], nullptr);
+        forward_sample<T>(dummy, nullptr, uniq.data(), w.n_u, nullptr, fps, false, false, outf);
+        f32_to_f64<<<grid_of(N * H), 256, 0, s>>>(outf, N * H, din);
+        MGV_CUDA(cudaMemcpyAsync(out, din, sizeof(double) * N * H, cudaMemcpyDeviceToHost, s));
+    }
+    MGV_CUDA(cudaFreeAsync(outf, s));
+    MGV_CUDA(cudaFreeAsync(din, s));
+    MGV_CUDA(cudaStreamSynchronize(s));
+}
+
+void Model::predict_velocity(const double* rows, int64_t N, const int32_t* coords, const int64_t dims[3],
+                             const double* text, int64_t L, const double* tau, double fps, double* out) {
+    MGV_CUDA(cudaSetDevice(device_));
+    if (bf16_)
+        value_forward<__nv_bfloat16>(rows, N, coords, dims, text, L, tau, fps, out, true);
+    else
+        value_forward<float>(rows, N, coords, dims, text, L, tau, fps, out, true);
+}
+void Model::dit_forward(const double* tokens, int64_t N, const int32_t* coords, const int64_t dims[3],
+                        const double* text, int64_t L, const double* tau, double fps, double* out) {
+    MGV_CUDA(cudaSetDevice(device_));
+    if (bf16_)
+        value_forward<__nv_bfloat16>(tokens, N, coords, dims, text, L, tau, fps, out, false);
+    else
+        value_forward<float>(tokens, N, coords, dims, text, L, tau, fps, out, false);
+}
+
+}  // namespace mgv

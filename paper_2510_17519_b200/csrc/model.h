@@ -1,0 +1,151 @@
+// C++ runtime of the DiT hot path: device weight cache, workspace arena, and
+// the forward / backward orchestration of velocity_rows_graph + flow loss
+// (proj/src/dit.cpp:267-334, proj/src/flowtrain.cpp:257-289).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mugv_b200.h"
+
+namespace mgv {
+
+// Errors mirroring the reference taxonomy (errors.hpp); mapped to mgv_status at the C ABI.
+struct DimensionError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ConfigError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct InputError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct NumericError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct NcclError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+struct Cfg {
+    int64_t depth = 0, hidden = 0, heads = 0, text_dim = 0, c_z = 0;
+    int rope[3] = {0, 0, 0};
+    int64_t H() const { return hidden; }
+    int64_t hd() const { return hidden / heads; }
+    int64_t D() const { return 4 * c_z; }
+};
+void validate_cfg(const Cfg& c);
+
+struct DevParam {
+    std::string name;
+    std::vector<int64_t> shape;
+    int64_t numel = 0;
+    float* f32 = nullptr;           // master copy (all params)
+    __nv_bfloat16* bf = nullptr;    // tensor-core operand copy (matrices, bf16 mode)
+    float* grad = nullptr;          // slice of the contiguous gradient buffer
+    int64_t grad_off = 0;
+};
+
+// Device sample (all pointers device-resident).
+struct DevSample {
+    int64_t N = 0;
+    int64_t dims[3] = {0, 0, 0};
+    const int32_t* coords = nullptr;
+    const double* clean = nullptr;
+    const double* noise = nullptr;
+    double t = 0.0;
+    int first_frame = 0;  // first_frame_mask conditioning (flowtrain.cpp:50-59)
+};
+
+class Arena {
+public:
+    ~Arena();
+    void reserve(size_t bytes);
+    void reset() { off_ = 0; }
+    template <class T>
+    T* take(int64_t n) {
+        size_t bytes = (sizeof(T) * static_cast<size_t>(n) + 255) & ~size_t(255);
+        if (off_ + bytes > cap_) throw std::runtime_error("workspace arena overflow");
+        T* p = reinterpret_cast<T*>(base_ + off_);
+        off_ += bytes;
+        return p;
+    }
+    size_t used() const { return off_; }
+    size_t cap() const { return cap_; }
+
+private:
+    char* base_ = nullptr;
+    size_t cap_ = 0, off_ = 0;
+};
+
+class Model {
+public:
+    Model(int device, bool bf16);
+    ~Model();
+
+    void set_stream(cudaStream_t s) { stream_ = s; }
+    void set_dp(int rank, int world, const uint8_t id[128]);
+
+    void upload(const Cfg& cfg, int64_t n, const char* const* names, const double* const* data,
+                const int64_t* numel);
+    const std::vector<DevParam*>& sorted_params() const { return sorted_; }
+
+    // Host-buffer entry points (the C ABI).
+    void predict_velocity(const double* rows, int64_t N, const int32_t* coords, const int64_t dims[3],
+                          const double* text, int64_t L, const double* tau, double fps, double* out);
+    void dit_forward(const double* tokens, int64_t N, const int32_t* coords, const int64_t dims[3],
+                     const double* text, int64_t L, const double* tau, double fps, double* out);
+    void flow_step(int64_t n, const mgv_flow_sample* samples, const double* text, int64_t L, double fps,
+                   double* loss, double* grad_norm, double* const* grads_out, double* const* v_out);
+    // Device-resident inputs (benchmark `value` path): no host<->device traffic except the two scalars.
+    void flow_step_dev(int64_t n, const DevSample* samples, const double* text_dev, int64_t L, double fps,
+                       double* loss, double* grad_norm, double* const* v_dev = nullptr);
+
+    double last_step_ms() const { return last_ms_; }
+    bool bf16() const { return bf16_; }
+    cudaStream_t stream() const { return stream_; }
+
+private:
+    template <class T>
+    void flow_step_impl(int64_t n, const DevSample* samples, const double* text_dev, int64_t L, double fps,
+                        double* loss, double* grad_norm, double* const* v_dev);
+    template <class T>
+    void forward_sample(const DevSample& s, const void* rows_in /*T*/, const double* tau_host_unique, int n_u,
+                        const int32_t* mod_id, double fps, bool grads, bool head, void* out);
+    template <class T>
+    void backward_sample(const void* dV);
+    template <class T>
+    void block_fwd(int i, int64_t N);
+    template <class T>
+    void block_bwd(int i, int64_t N);
+    template <class T>
+    void value_forward(const double* in, int64_t N, const int32_t* coords, const int64_t dims[3],
+                       const double* text, int64_t L, const double* tau, double fps, double* out, bool velocity);
+
+    const DevParam& P(const std::string& name) const;
+    const void* W(const std::string& name) const;  // GEMM operand in the compute precision
+    float* G(const std::string& name) const;
+    std::string blk(int i, const char* s) const { return "dit.blk." + std::to_string(i) + "." + s; }
+
+    void plan_workspace(int64_t N, int64_t L, int n_u);
+
+    int device_;
+    bool bf16_;
+    cudaStream_t stream_ = nullptr;
+    Cfg cfg_;
+    bool have_params_ = false;
+    std::map<std::string, DevParam> params_;
+    std::vector<DevParam*> sorted_;
+    float* grad_buf_ = nullptr;
+    int64_t grad_numel_ = 0;
+    Arena arena_;
+    double last_ms_ = 0.0;
+    // NCCL data parallel
+    ncclComm_t comm_ = nullptr;
+    int rank_ = 0, world_ = 1;
+
+    // ---- per-sample workspace views (set by plan_workspace / forward)
+public:
+    struct WS;
+
+private:
+    WS* ws_ = nullptr;
+};
+
+}  // namespace mgv
