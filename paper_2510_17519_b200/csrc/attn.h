@@ -46,6 +46,9 @@ void attn_fwd_simt(const AttnProblem& p, cudaStream_t s);
 template <class T>
 void attn_bwd_simt(const AttnBwdProblem& p, cudaStream_t s);
 
+// D[h][q] = rowsum(dO * O) (bf16 operands), shared by both backward paths
+void attn_bwd_dvec(const AttnBwdProblem& p, cudaStream_t s);
+
 // tcgen05 flash attention (bf16 operands, fp32 softmax / accumulate); hd in {64, 128, 144, ...} (hd % 16 == 0)
 bool attn_tc_supported(int hd, int Nk);
 void attn_fwd_tc(const AttnProblem& p, cudaStream_t s);

@@ -295,6 +295,12 @@ void attn_bwd_simt(const AttnBwdProblem& p, cudaStream_t s) {
     MGV_CUDA(cudaGetLastError());
 }
 
+void attn_bwd_dvec(const AttnBwdProblem& p, cudaStream_t s) {
+    const int64_t rows = (int64_t)p.f.Nq * p.f.heads;
+    attn_bwd_dvec_kernel<__nv_bfloat16><<<(int)((rows * 32 + 255) / 256), 256, 0, s>>>(p);
+    MGV_CUDA(cudaGetLastError());
+}
+
 template void attn_fwd_simt<float>(const AttnProblem&, cudaStream_t);
 template void attn_fwd_simt<__nv_bfloat16>(const AttnProblem&, cudaStream_t);
 template void attn_bwd_simt<float>(const AttnBwdProblem&, cudaStream_t);

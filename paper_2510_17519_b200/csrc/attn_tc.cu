@@ -306,8 +306,6 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_consta
 }
 
 // ------------------------------------------------------------------ host
-static void make_tmap_sw(CUtensorMap* m, const void* p, uint64_t cols, uint64_t rows, uint64_t ld, uint32_t box_c,
-                         CUtensorMapSwizzle sw);
 
 bool attn_tc_supported(int hd, int Nk) {
     (void)Nk;
@@ -320,12 +318,12 @@ static void launch_fwd(const AttnProblem& p, cudaStream_t s) {
     TmapSet tm;
     // operands are token-major (rows = tokens, ld = row stride in elements)
     const uint64_t qc = (uint64_t)p.heads * HD, kc = qc, vc = qc;
-    make_tmap_sw(&tm.q128, p.q, qc, p.Nq, p.q_ld, 64, CU_TENSOR_MAP_SWIZZLE_128B);
-    make_tmap_sw(&tm.q32, p.q, qc, p.Nq, p.q_ld, 16, CU_TENSOR_MAP_SWIZZLE_32B);
-    make_tmap_sw(&tm.k128, p.k, kc, p.Nk, p.k_ld, 64, CU_TENSOR_MAP_SWIZZLE_128B);
-    make_tmap_sw(&tm.k32, p.k, kc, p.Nk, p.k_ld, 16, CU_TENSOR_MAP_SWIZZLE_32B);
-    make_tmap_sw(&tm.v128, p.v, vc, p.Nk, p.v_ld, 64, CU_TENSOR_MAP_SWIZZLE_128B);
-    make_tmap_sw(&tm.v32, p.v, vc, p.Nk, p.v_ld, 16, CU_TENSOR_MAP_SWIZZLE_32B);
+    make_tmap_sw(&tm.q128, p.q, qc, p.Nq, p.q_ld, 64, BM, CU_TENSOR_MAP_SWIZZLE_128B);
+    make_tmap_sw(&tm.q32, p.q, qc, p.Nq, p.q_ld, 16, BM, CU_TENSOR_MAP_SWIZZLE_32B);
+    make_tmap_sw(&tm.k128, p.k, kc, p.Nk, p.k_ld, 64, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+    make_tmap_sw(&tm.k32, p.k, kc, p.Nk, p.k_ld, 16, BN, CU_TENSOR_MAP_SWIZZLE_32B);
+    make_tmap_sw(&tm.v128, p.v, vc, p.Nk, p.v_ld, 64, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+    make_tmap_sw(&tm.v32, p.v, vc, p.Nk, p.v_ld, 16, BN, CU_TENSOR_MAP_SWIZZLE_32B);
     static bool set = false;
     if (!set) {
         MGV_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -345,32 +343,6 @@ void attn_fwd_tc(const AttnProblem& p, cudaStream_t s) {
     }
 }
 
-void attn_bwd_tc(const AttnBwdProblem& p, cudaStream_t s) {
-    // backward on tensor cores: pending; the bf16 path uses the CUDA-core kernels meanwhile
-    attn_bwd_simt<__nv_bfloat16>(p, s);
-}
-
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static void make_tmap_sw(CUtensorMap* m, const void* p, uint64_t cols, uint64_t rows, uint64_t ld, uint32_t box_c,
-                         CUtensorMapSwizzle sw) {
-    static EncodeFn fn = [] {
-        void* f = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess || !f)
-            throw CudaError("cuTensorMapEncodeTiled unavailable");
-        return reinterpret_cast<EncodeFn>(f);
-    }();
-    cuuint64_t dims[2] = {cols, rows};
-    cuuint64_t strides[1] = {ld * 2};
-    cuuint32_t box[2] = {box_c, static_cast<cuuint32_t>(BM)};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, strides, box, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw CudaError("attn tensor map encode failed: " + std::to_string(int(r)));
-}
 
 }  // namespace mgv
 

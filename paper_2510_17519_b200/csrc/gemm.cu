@@ -46,6 +46,19 @@ void make_tmap_bf16(CUtensorMap* m, const void* p, uint64_t inner, uint64_t oute
                         std::to_string(inner) + " outer=" + std::to_string(outer) + " ld=" + std::to_string(ld_elems));
 }
 
+// bf16 2-D map over a token-major matrix (rows x cols, row stride ld elements) with a chosen swizzle/box.
+void make_tmap_sw(CUtensorMap* m, const void* p, uint64_t cols, uint64_t rows, uint64_t ld, uint32_t box_c,
+                  uint32_t box_r, CUtensorMapSwizzle sw) {
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {ld * 2};
+    cuuint32_t box[2] = {box_c, box_r};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("tensor map encode failed: " + std::to_string(int(r)));
+}
+
 }  // namespace mgv
 
 using namespace mgv;

@@ -34,6 +34,8 @@ struct CudaError : std::runtime_error {
     } while (0)
 
 int num_sms();
+void make_tmap_sw(CUtensorMap* m, const void* p, uint64_t cols, uint64_t rows, uint64_t ld, uint32_t box_c,
+                  uint32_t box_r, CUtensorMapSwizzle sw);
 void make_tmap_bf16(CUtensorMap* m, const void* p, uint64_t inner, uint64_t outer, uint64_t ld_elems,
                     uint32_t box_inner, uint32_t box_outer);
 
