@@ -112,10 +112,19 @@ mgv_status mgv_latent_rows(mgv_ctx* ctx, const double* grid, int64_t U, int64_t 
 mgv_status mgv_rows_to_grid(mgv_ctx* ctx, const double* rows, const int32_t* coords, int64_t N, const int64_t dims[3],
                             int64_t C, double* grid);
 
+/* mgv_flow_step with DEVICE-resident sample/text buffers (same struct, device pointers): the
+ * benchmark's inputs-already-in-HBM figure.  No gradients or velocities are read back. */
+mgv_status mgv_flow_step_device(mgv_ctx* ctx, int64_t n, const mgv_flow_sample* samples, const double* text_dev,
+                                int64_t L, double fps, double* loss, double* grad_norm);
+
 /* Timing / introspection for the benchmark: device time (ms) of the last mgv_flow_step's compute,
  * and the number of kernel launches it issued. */
 double mgv_last_step_ms(mgv_ctx* ctx);
 int64_t mgv_last_step_launches(mgv_ctx* ctx);
+/* Per-phase CUDA-event timing ("attn_fwd", "attn_bwd", "blocks_fwd", ...), accumulated over steps. */
+mgv_status mgv_prof_enable(mgv_ctx* ctx, int on);
+int64_t mgv_prof_count(mgv_ctx* ctx);
+const char* mgv_prof_entry(mgv_ctx* ctx, int64_t i, double* ms, int64_t* launches);
 
 #ifdef __cplusplus
 }

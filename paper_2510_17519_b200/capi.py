@@ -95,13 +95,22 @@ def declare(L):
     L.mgv_last_step_ms.restype = D
     L.mgv_last_step_launches.argtypes = [P]
     L.mgv_last_step_launches.restype = I64
+    L.mgv_prof_enable.argtypes = [P, I]
+    L.mgv_prof_enable.restype = I
+    L.mgv_prof_count.argtypes = [P]
+    L.mgv_prof_count.restype = I64
+    L.mgv_prof_entry.argtypes = [P, I64, ctypes.POINTER(D), ctypes.POINTER(I64)]
+    L.mgv_prof_entry.restype = ctypes.c_char_p
+    L.mgv_dev_attn_fwd.restype = I
+    L.mgv_dev_attn_bwd.restype = I
 
 
 # symbols include/mugv_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = ["mgv_ctx_create", "mgv_ctx_destroy", "mgv_last_error", "mgv_ctx_set_stream", "mgv_nccl_unique_id",
            "mgv_ctx_set_dp", "mgv_params_upload", "mgv_param_count", "mgv_param_name", "mgv_param_numel",
            "mgv_predict_velocity", "mgv_dit_forward", "mgv_flow_step", "mgv_flow_loss", "mgv_latent_rows",
-           "mgv_rows_to_grid", "mgv_last_step_ms", "mgv_last_step_launches"]
+           "mgv_rows_to_grid", "mgv_flow_step_device", "mgv_last_step_ms", "mgv_last_step_launches",
+           "mgv_prof_enable", "mgv_prof_count", "mgv_prof_entry"]
 
 
 @dataclass
@@ -273,5 +282,26 @@ class Context:
             out["V"] = v_arrs
         return out
 
+    def flow_step_device(self, samples_c, text_dev_ptr, L, fps=8.0):
+        """mgv_flow_step_device: samples_c is a ctypes array of mgv_flow_sample holding DEVICE pointers."""
+        loss, gn = D(), D()
+        self._check(self._L.mgv_flow_step_device(self.h, len(samples_c), samples_c, text_dev_ptr, L, fps,
+                                                  ctypes.byref(loss), ctypes.byref(gn)))
+        return loss.value, gn.value
+
     def last_step_ms(self) -> float:
         return self._L.mgv_last_step_ms(self.h)
+
+    def last_step_launches(self) -> int:
+        return self._L.mgv_last_step_launches(self.h)
+
+    def prof_enable(self, on=True):
+        self._check(self._L.mgv_prof_enable(self.h, 1 if on else 0))
+
+    def prof_stats(self) -> dict:
+        out = {}
+        for i in range(self._L.mgv_prof_count(self.h)):
+            ms, n = D(), I64()
+            name = self._L.mgv_prof_entry(self.h, i, ctypes.byref(ms), ctypes.byref(n)).decode()
+            out[name] = {"ms": ms.value, "launches": n.value}
+        return out

@@ -459,7 +459,7 @@ static void launch_bwd(const AttnBwdProblem& p, cudaStream_t s) {
             MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             set = true;
         }
-        attn_bwd_dkv_tc_kernel<HD><<<dim3((p.f.Nk + 127) / 128, p.f.heads), 256, smem, s>>>(m, p);
+        attn_bwd_dkv_tc_kernel<HD><<<dim3((p.f.Nk + 127) / 128, p.f.heads), 256, smem, s>>>(m, p); ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
     }
     {
@@ -473,7 +473,7 @@ static void launch_bwd(const AttnBwdProblem& p, cudaStream_t s) {
             MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             set = true;
         }
-        attn_bwd_dq_tc_kernel<HD><<<dim3((p.f.Nq + 127) / 128, p.f.heads), 256, smem, s>>>(m, p);
+        attn_bwd_dq_tc_kernel<HD><<<dim3((p.f.Nq + 127) / 128, p.f.heads), 256, smem, s>>>(m, p); ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
     }
 }

@@ -269,7 +269,7 @@ void attn_fwd_simt(const AttnProblem& p, cudaStream_t s) {
         set = true;
     }
     dim3 grid((p.Nq + BQ - 1) / BQ, p.heads);
-    attn_fwd_simt_kernel<T><<<grid, NT, smem, s>>>(p);
+    attn_fwd_simt_kernel<T><<<grid, NT, smem, s>>>(p); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -285,19 +285,19 @@ void attn_bwd_simt(const AttnBwdProblem& p, cudaStream_t s) {
         set = true;
     }
     const int64_t rows = (int64_t)p.f.Nq * p.f.heads;
-    attn_bwd_dvec_kernel<T><<<(int)((rows * 32 + 255) / 256), 256, 0, s>>>(p);
-    attn_bwd_dq_simt_kernel<T><<<dim3((p.f.Nq + BQ - 1) / BQ, p.f.heads), NT, smem, s>>>(p);
-    attn_bwd_dkv_simt_kernel<T><<<dim3((p.f.Nk + BK - 1) / BK, p.f.heads, p.q_splits), NT, smem, s>>>(p);
+    attn_bwd_dvec_kernel<T><<<(int)((rows * 32 + 255) / 256), 256, 0, s>>>(p); ::mgv::note_launch();
+    attn_bwd_dq_simt_kernel<T><<<dim3((p.f.Nq + BQ - 1) / BQ, p.f.heads), NT, smem, s>>>(p); ::mgv::note_launch();
+    attn_bwd_dkv_simt_kernel<T><<<dim3((p.f.Nk + BK - 1) / BK, p.f.heads, p.q_splits), NT, smem, s>>>(p); ::mgv::note_launch();
     if (p.q_splits > 1) {
         const int64_t total = (int64_t)p.f.heads * p.f.Nk * 2 * p.f.hd;
-        attn_dkv_reduce_kernel<T><<<(int)((total + 255) / 256), 256, 0, s>>>(p);
+        attn_dkv_reduce_kernel<T><<<(int)((total + 255) / 256), 256, 0, s>>>(p); ::mgv::note_launch();
     }
     MGV_CUDA(cudaGetLastError());
 }
 
 void attn_bwd_dvec(const AttnBwdProblem& p, cudaStream_t s) {
     const int64_t rows = (int64_t)p.f.Nq * p.f.heads;
-    attn_bwd_dvec_kernel<__nv_bfloat16><<<(int)((rows * 32 + 255) / 256), 256, 0, s>>>(p);
+    attn_bwd_dvec_kernel<__nv_bfloat16><<<(int)((rows * 32 + 255) / 256), 256, 0, s>>>(p); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 

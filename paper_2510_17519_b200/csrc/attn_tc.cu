@@ -330,7 +330,7 @@ static void launch_fwd(const AttnProblem& p, cudaStream_t s) {
         set = true;
     }
     dim3 grid((p.Nq + BM - 1) / BM, p.heads);
-    attn_fwd_tc_kernel<HD><<<grid, 256, C::SMEM, s>>>(tm, p);
+    attn_fwd_tc_kernel<HD><<<grid, 256, C::SMEM, s>>>(tm, p); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 

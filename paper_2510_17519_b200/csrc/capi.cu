@@ -1,6 +1,7 @@
 // extern "C" boundary (include/mugv_b200.h): C types only, no exceptions cross it.
 #include <cstring>
 #include <exception>
+#include <iterator>
 #include <memory>
 #include <string>
 
@@ -218,6 +219,22 @@ mgv_status mgv_rows_to_grid(mgv_ctx* ctx, const double* rows, const int32_t* coo
 }
 
 double mgv_last_step_ms(mgv_ctx* ctx) { return ctx ? ctx->model->last_step_ms() : 0.0; }
-int64_t mgv_last_step_launches(mgv_ctx* ctx) { return 0; }
+int64_t mgv_last_step_launches(mgv_ctx* ctx) { return ctx ? ctx->model->last_step_launches() : 0; }
+
+// Per-phase device timing for the benchmark (CUDA events on the context stream).
+mgv_status mgv_prof_enable(mgv_ctx* ctx, int on) {
+    return guard(ctx, [&] {
+        ctx->model->prof().on = on != 0;
+        ctx->model->prof().stats.clear();
+    });
+}
+int64_t mgv_prof_count(mgv_ctx* ctx) { return ctx ? static_cast<int64_t>(ctx->model->prof().stats.size()) : 0; }
+const char* mgv_prof_entry(mgv_ctx* ctx, int64_t i, double* ms, int64_t* n) {
+    auto it = ctx->model->prof().stats.begin();
+    std::advance(it, i);
+    *ms = it->second.ms;
+    *n = it->second.n;
+    return it->first.c_str();
+}
 
 }  // extern "C"

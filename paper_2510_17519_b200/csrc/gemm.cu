@@ -2,9 +2,14 @@
 // exported for tests / roofline measurement.
 #include "gemm.cuh"
 
+#include <atomic>
 #include <mutex>
 
 namespace mgv {
+
+static std::atomic<int64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 int num_sms() {
     static int n = [] {

@@ -34,6 +34,9 @@ struct CudaError : std::runtime_error {
     } while (0)
 
 int num_sms();
+// kernel-launch accounting (bench: gpu_launches)
+void note_launch();
+int64_t launch_count();
 void make_tmap_sw(CUtensorMap* m, const void* p, uint64_t cols, uint64_t rows, uint64_t ld, uint32_t box_c,
                   uint32_t box_r, CUtensorMapSwizzle sw);
 void make_tmap_bf16(CUtensorMap* m, const void* p, uint64_t inner, uint64_t outer, uint64_t ld_elems,
@@ -85,7 +88,7 @@ template <bool A_MN, bool B_MN, class Epi>
 void gemm_f32_launch(const Mat& A, const Mat& B, int M, int N, int K, const Epi& epi, cudaStream_t s) {
     dim3 grid((N + 63) / 64, (M + 63) / 64);
     gemm_f32_simt_kernel<A_MN, B_MN, Epi><<<grid, 256, 0, s>>>(static_cast<const float*>(A.p), A.ld,
-                                                               static_cast<const float*>(B.p), B.ld, M, N, K, epi);
+                                                               static_cast<const float*>(B.p), B.ld, M, N, K, epi); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -110,7 +113,7 @@ void gemm_tc_launch(const Mat& A, const Mat& B, int M, int N, int K, const Epi& 
     }
     const int tiles = ((M + kGemmBM - 1) / kGemmBM) * ((N + BN - 1) / BN);
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    kern<<<grid, kGemmThreads, C::SMEM, s>>>(ta, tb, M, N, K, epi);
+    kern<<<grid, kGemmThreads, C::SMEM, s>>>(ta, tb, M, N, K, epi); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 

@@ -66,9 +66,12 @@ void qk_norm_rope(const T* qkv, int N, int H, int heads, const float* temp, cons
 // part (row_chunks(N)) double partial sums of squared error over unmasked rows; dV = coef * (V - vt) on unmasked rows
 template <class T>
 void flow_loss_fwd(const float* V, const float* vt, const uint8_t* mask, int N, int D, double* part, cudaStream_t s);
+// dV = base / (count * D) * (V - vt) on unmasked rows (0 everywhere when count == 0)
 template <class T>
-void flow_loss_bwd(const float* V, const float* vt, const uint8_t* mask, int N, int D, float coef, T* dV,
-                   cudaStream_t s);
+void flow_loss_bwd(const float* V, const float* vt, const uint8_t* mask, int N, int D, float base, const int* count,
+                   T* dV, cudaStream_t s);
+// acc[0] += sum(part[0..n)) / (count * D)   (0 when count == 0), one thread, fixed order
+void flow_loss_accumulate(const double* part, int n, const int* count, int D, double* acc, cudaStream_t s);
 void count_mask(const uint8_t* mask, int N, int* count, cudaStream_t s);
 void sum_double(const double* part, int n, double* out, cudaStream_t s);  // fixed-order sum, one thread
 

@@ -83,7 +83,7 @@ template <class T>
 void prep_flow_sample(const double* clean, const double* noise, const int32_t* coords, int N, int D, double t,
                       int cond, T* rows, float* vt, uint8_t* lmask, int32_t* mod_id, cudaStream_t s) {
     prep_flow_sample_kernel<T><<<grid_for((int64_t)N * D), 256, 0, s>>>(clean, noise, coords, N, D, t, cond, rows, vt,
-                                                                        lmask, mod_id);
+                                                                        lmask, mod_id); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -94,7 +94,7 @@ __global__ void convert_rows_kernel(const double* src, int64_t n, T* dst) {
 }
 template <class T>
 void convert_rows(const double* src, int64_t n, T* dst, cudaStream_t s) {
-    convert_rows_kernel<T><<<grid_for(n), 256, 0, s>>>(src, n, dst);
+    convert_rows_kernel<T><<<grid_for(n), 256, 0, s>>>(src, n, dst); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 template <class T>
@@ -104,7 +104,7 @@ __global__ void convert_f32_kernel(const float* src, int64_t n, T* dst) {
 }
 template <class T>
 void convert_f32(const float* src, int64_t n, T* dst, cudaStream_t s) {
-    convert_f32_kernel<T><<<grid_for(n), 256, 0, s>>>(src, n, dst);
+    convert_f32_kernel<T><<<grid_for(n), 256, 0, s>>>(src, n, dst); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -128,7 +128,7 @@ __global__ void latent_rows_kernel(const double* grid, int U, int h, int w, int 
 }
 void latent_rows_gather(const double* grid, int U, int h, int w, int C, double* rows, int32_t* coords, cudaStream_t s) {
     const int64_t total = (int64_t)U * (h / 2) * (w / 2) * 4 * C;
-    latent_rows_kernel<<<grid_for(total), 256, 0, s>>>(grid, U, h, w, C, rows, coords);
+    latent_rows_kernel<<<grid_for(total), 256, 0, s>>>(grid, U, h, w, C, rows, coords); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -161,8 +161,8 @@ void rows_to_grid_scatter(const double* rows, const int32_t* coords, int N, int 
                           int32_t* seen, int32_t* status, cudaStream_t s) {
     MGV_CUDA(cudaMemsetAsync(seen, 0, sizeof(int32_t) * (size_t)U * Hp * Wp, s));
     MGV_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t), s));
-    rows_to_grid_check_kernel<<<grid_for(N), 256, 0, s>>>(coords, N, U, Hp, Wp, seen, status);
-    rows_to_grid_kernel<<<grid_for((int64_t)N * 4 * C), 256, 0, s>>>(rows, coords, N, U, Hp, Wp, C, grid, status);
+    rows_to_grid_check_kernel<<<grid_for(N), 256, 0, s>>>(coords, N, U, Hp, Wp, seen, status); ::mgv::note_launch();
+    rows_to_grid_kernel<<<grid_for((int64_t)N * 4 * C), 256, 0, s>>>(rows, coords, N, U, Hp, Wp, C, grid, status); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -193,7 +193,7 @@ __global__ void rope_table_kernel(const int32_t* coords, int N, int s0, int s1, 
     }
 }
 void rope_table(const int32_t* coords, int N, int s0, int s1, int s2, float2* cs, cudaStream_t s) {
-    rope_table_kernel<<<grid_for((int64_t)N * (s0 + s1 + s2) / 2), 256, 0, s>>>(coords, N, s0, s1, s2, cs);
+    rope_table_kernel<<<grid_for((int64_t)N * (s0 + s1 + s2) / 2), 256, 0, s>>>(coords, N, s0, s1, s2, cs); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -234,10 +234,10 @@ __global__ void add_fps_row(double* g, int n_u, int H) {  // g_u += g_fps (row n
 void global_embed(const double* taus, int n_u, double fps, const float* w_in, const float* b_in, const float* w_out,
                   const float* b_out, int H, double* phi, double* z_in, double* h_in, double* g, cudaStream_t s) {
     const int R = n_u + 1;
-    sinusoid_kernel<<<R, 32, 0, s>>>(taus, n_u, fps, phi);
-    gemv_rows_f64<1><<<grid_for((int64_t)R * H * 32), 256, 0, s>>>(phi, R, 32, w_in, b_in, H, z_in, h_in);
-    gemv_rows_f64<0><<<grid_for((int64_t)R * H * 32), 256, 0, s>>>(h_in, R, H, w_out, b_out, H, nullptr, g);
-    add_fps_row<<<grid_for((int64_t)n_u * H), 256, 0, s>>>(g, n_u, H);
+    sinusoid_kernel<<<R, 32, 0, s>>>(taus, n_u, fps, phi); ::mgv::note_launch();
+    gemv_rows_f64<1><<<grid_for((int64_t)R * H * 32), 256, 0, s>>>(phi, R, 32, w_in, b_in, H, z_in, h_in); ::mgv::note_launch();
+    gemv_rows_f64<0><<<grid_for((int64_t)R * H * 32), 256, 0, s>>>(h_in, R, H, w_out, b_out, H, nullptr, g); ::mgv::note_launch();
+    add_fps_row<<<grid_for((int64_t)n_u * H), 256, 0, s>>>(g, n_u, H); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 __global__ void mul_gscale(const double* g, const float* gs, int n_u, int H, double* gb) {
@@ -256,8 +256,8 @@ __global__ void gemv_rows_f64_to_f32(const double* in, int rows, int K, const fl
 }
 void modulation_table(const double* g, const float* gscale, const float* w_mod, const float* b_mod, int n_u, int H,
                       double* gb, float* table, cudaStream_t s) {
-    mul_gscale<<<grid_for((int64_t)n_u * H), 256, 0, s>>>(g, gscale, n_u, H, gb);
-    gemv_rows_f64_to_f32<<<grid_for((int64_t)n_u * 6 * H * 32), 256, 0, s>>>(gb, n_u, H, w_mod, b_mod, 6 * H, table);
+    mul_gscale<<<grid_for((int64_t)n_u * H), 256, 0, s>>>(g, gscale, n_u, H, gb); ::mgv::note_launch();
+    gemv_rows_f64_to_f32<<<grid_for((int64_t)n_u * 6 * H * 32), 256, 0, s>>>(gb, n_u, H, w_mod, b_mod, 6 * H, table); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -296,12 +296,12 @@ __global__ void __launch_bounds__(RT) rms_mod_kernel(const float* X, int N, int 
 template <class T>
 void rms_mod(const float* X, int N, int H, const float* table, int64_t tld, int sh_off, int sc_off,
              const int32_t* mod_id, T* out, float* r, cudaStream_t s) {
-    rms_mod_kernel<T><<<row_chunks(N), RT, 0, s>>>(X, N, H, table, tld, sh_off, sc_off, mod_id, 0, nullptr, out, r);
+    rms_mod_kernel<T><<<row_chunks(N), RT, 0, s>>>(X, N, H, table, tld, sh_off, sc_off, mod_id, 0, nullptr, out, r); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 template <class T>
 void rms_gain(const float* X, int N, int H, const float* g, T* out, float* r, cudaStream_t s) {
-    rms_mod_kernel<T><<<row_chunks(N), RT, 0, s>>>(X, N, H, nullptr, 0, 0, 0, nullptr, 1, g, out, r);
+    rms_mod_kernel<T><<<row_chunks(N), RT, 0, s>>>(X, N, H, nullptr, 0, 0, 0, nullptr, 1, g, out, r); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(RT) postnorm_resid_kernel(const float* X1, con
 }
 template <class T>
 void postnorm_resid(const float* X1, const T* co, int N, int H, const float* g, float* X2, float* rc, cudaStream_t s) {
-    postnorm_resid_kernel<T><<<row_chunks(N), RT, 0, s>>>(X1, co, N, H, g, X2, rc);
+    postnorm_resid_kernel<T><<<row_chunks(N), RT, 0, s>>>(X1, co, N, H, g, X2, rc); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -376,7 +376,7 @@ template <class T>
 void qk_norm_rope(const T* qkv, int N, int H, int heads, const float* temp, const float2* cs, T* qk, float* iq,
                   float* ik, cudaStream_t s) {
     const int64_t warps = (int64_t)N * heads * 2;
-    qk_norm_rope_kernel<T><<<grid_for(warps * 32), 256, 0, s>>>(qkv, N, H, heads, temp, cs, qk, iq, ik);
+    qk_norm_rope_kernel<T><<<grid_for(warps * 32), 256, 0, s>>>(qkv, N, H, heads, temp, cs, qk, iq, ik); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -399,22 +399,24 @@ __global__ void __launch_bounds__(RT) flow_loss_fwd_kernel(const float* V, const
 }
 template <class T>
 void flow_loss_fwd(const float* V, const float* vt, const uint8_t* mask, int N, int D, double* part, cudaStream_t s) {
-    flow_loss_fwd_kernel<T><<<row_chunks(N), RT, 0, s>>>(V, vt, mask, N, D, part);
+    flow_loss_fwd_kernel<T><<<row_chunks(N), RT, 0, s>>>(V, vt, mask, N, D, part); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 template <class T>
-__global__ void flow_loss_bwd_kernel(const float* V, const float* vt, const uint8_t* mask, int N, int D, float coef,
-                                     T* dV) {
+__global__ void flow_loss_bwd_kernel(const float* V, const float* vt, const uint8_t* mask, int N, int D, float base,
+                                     const int* count, T* dV) {
     const int64_t total = (int64_t)N * D;
+    const int cnt = *count;
+    const float coef = cnt > 0 ? static_cast<float>(static_cast<double>(base) / (static_cast<double>(cnt) * D)) : 0.0f;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int i = static_cast<int>(e / D);
         dV[e] = to_t<T>(mask[i] ? coef * (V[e] - vt[e]) : 0.0f);
     }
 }
 template <class T>
-void flow_loss_bwd(const float* V, const float* vt, const uint8_t* mask, int N, int D, float coef, T* dV,
-                   cudaStream_t s) {
-    flow_loss_bwd_kernel<T><<<grid_for((int64_t)N * D), 256, 0, s>>>(V, vt, mask, N, D, coef, dV);
+void flow_loss_bwd(const float* V, const float* vt, const uint8_t* mask, int N, int D, float base, const int* count,
+                   T* dV, cudaStream_t s) {
+    flow_loss_bwd_kernel<T><<<grid_for((int64_t)N * D), 256, 0, s>>>(V, vt, mask, N, D, base, count, dV); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 __global__ void count_mask_kernel(const uint8_t* mask, int N, int* count) {
@@ -426,7 +428,7 @@ __global__ void count_mask_kernel(const uint8_t* mask, int N, int* count) {
     if (threadIdx.x == 0) *count = static_cast<int>(c);
 }
 void count_mask(const uint8_t* mask, int N, int* count, cudaStream_t s) {
-    count_mask_kernel<<<1, RT, 0, s>>>(mask, N, count);
+    count_mask_kernel<<<1, RT, 0, s>>>(mask, N, count); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 __global__ void sum_double_kernel(const double* part, int n, double* out) {
@@ -434,8 +436,18 @@ __global__ void sum_double_kernel(const double* part, int n, double* out) {
     for (int i = 0; i < n; ++i) s += part[i];
     *out = s;
 }
+__global__ void flow_loss_acc_kernel(const double* part, int n, const int* count, int D, double* acc) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += part[i];
+    const int c = *count;
+    if (c > 0) acc[0] += s / (static_cast<double>(c) * D);
+}
+void flow_loss_accumulate(const double* part, int n, const int* count, int D, double* acc, cudaStream_t s) {
+    flow_loss_acc_kernel<<<1, 1, 0, s>>>(part, n, count, D, acc); ::mgv::note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
 void sum_double(const double* part, int n, double* out, cudaStream_t s) {
-    sum_double_kernel<<<1, 1, 0, s>>>(part, n, out);
+    sum_double_kernel<<<1, 1, 0, s>>>(part, n, out); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -486,7 +498,7 @@ template <class T>
 void gate_bwd(const float* dX, const T* y, const float* table, int64_t tld, int gate_off, const int32_t* mod_id,
               int n_u, int N, int H, T* dY, float* part_dgate, float* part_db, cudaStream_t s) {
     gate_bwd_kernel<T><<<row_chunks(N), RT, 0, s>>>(dX, y, table, tld, gate_off, mod_id, n_u, N, H, dY, part_dgate,
-                                                   part_db);
+                                                   part_db); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -566,14 +578,14 @@ void rms_mod_bwd(const T* dA, const float* X, const float* r, const float* table
                  const int32_t* mod_id, int n_u, int N, int H, float* dX, float* part_dsh, float* part_dsc,
                  cudaStream_t s) {
     rms_bwd_kernel<T, 0><<<row_chunks(N), RT, 0, s>>>(dA, X, r, table, tld, sh_off, sc_off, mod_id, n_u, nullptr, N, H,
-                                                     dX, 1, part_dsh, part_dsc);
+                                                     dX, 1, part_dsh, part_dsc); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 template <class T>
 void rms_gain_bwd(const T* dA, const float* X, const float* r, const float* g, int N, int H, float* dX, int accumulate,
                   float* part_dg, cudaStream_t s) {
     rms_bwd_kernel<T, 1><<<row_chunks(N), RT, 0, s>>>(dA, X, r, nullptr, 0, 0, 0, nullptr, 1, g, N, H, dX, accumulate,
-                                                     part_dg, nullptr);
+                                                     part_dg, nullptr); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -620,7 +632,7 @@ __global__ void __launch_bounds__(RT) postnorm_bwd_kernel(const float* dX, const
 template <class T>
 void postnorm_bwd(const float* dX, const T* co, const float* rc, const float* g, int N, int H, T* dco, float* part_dg,
                   cudaStream_t s) {
-    postnorm_bwd_kernel<T><<<row_chunks(N), RT, 0, s>>>(dX, co, rc, g, N, H, dco, part_dg);
+    postnorm_bwd_kernel<T><<<row_chunks(N), RT, 0, s>>>(dX, co, rc, g, N, H, dco, part_dg); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -683,7 +695,7 @@ __global__ void __launch_bounds__(256) qk_norm_rope_bwd_kernel(T* dqkv, const T*
 template <class T>
 void qk_norm_rope_bwd(T* dqkv, const T* qkv, int N, int H, int heads, const float* temp, const float2* cs,
                       const float* iq, const float* ik, float* part_dtemp, cudaStream_t s) {
-    qk_norm_rope_bwd_kernel<T><<<row_chunks(N), 256, 0, s>>>(dqkv, qkv, N, H, heads, temp, cs, iq, ik, part_dtemp);
+    qk_norm_rope_bwd_kernel<T><<<row_chunks(N), 256, 0, s>>>(dqkv, qkv, N, H, heads, temp, cs, iq, ik, part_dtemp); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -700,7 +712,7 @@ __global__ void colsum_kernel(const T* Y, int64_t ld, int N, int C, float* part)
 template <class T>
 void colsum(const T* Y, int64_t ld, int N, int C, float* part, cudaStream_t s) {
     dim3 grid(row_chunks(N), (C + 255) / 256);
-    colsum_kernel<T><<<grid, 256, 0, s>>>(Y, ld, N, C, part);
+    colsum_kernel<T><<<grid, 256, 0, s>>>(Y, ld, N, C, part); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 __global__ void reduce_chunks_kernel(const float* part, int chunks, int groups, int C, float* out, int64_t out_stride,
@@ -714,13 +726,13 @@ __global__ void reduce_chunks_kernel(const float* part, int chunks, int groups, 
     *o = accumulate ? *o + alpha * acc : alpha * acc;
 }
 void reduce_chunks(const float* part, int chunks, int C, float* out, float alpha, int accumulate, cudaStream_t s) {
-    reduce_chunks_kernel<<<grid_for(C), 256, 0, s>>>(part, chunks, 1, C, out, 0, alpha, accumulate);
+    reduce_chunks_kernel<<<grid_for(C), 256, 0, s>>>(part, chunks, 1, C, out, 0, alpha, accumulate); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 void reduce_chunks_grouped(const float* part, int chunks, int groups, int C, float* out, int64_t out_stride,
                            float alpha, int accumulate, cudaStream_t s) {
     reduce_chunks_kernel<<<grid_for((int64_t)groups * C), 256, 0, s>>>(part, chunks, groups, C, out, out_stride, alpha,
-                                                                     accumulate);
+                                                                     accumulate); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -752,8 +764,8 @@ __global__ void mod_dgrad_kernel(const float* dm, const float* w, int n_u, int H
 }
 void modulation_bwd(const float* dm, const double* gb, const float* w_mod, int n_u, int H, float* dw_mod,
                     float* db_mod, double* dgb, cudaStream_t s) {
-    mod_wgrad_kernel<<<grid_for((int64_t)6 * H * H), 256, 0, s>>>(dm, gb, n_u, H, dw_mod, db_mod);
-    mod_dgrad_kernel<<<dim3((H + 127) / 128, n_u), 128, 0, s>>>(dm, w_mod, n_u, H, dgb);
+    mod_wgrad_kernel<<<grid_for((int64_t)6 * H * H), 256, 0, s>>>(dm, gb, n_u, H, dw_mod, db_mod); ::mgv::note_launch();
+    mod_dgrad_kernel<<<dim3((H + 127) / 128, n_u), 128, 0, s>>>(dm, w_mod, n_u, H, dgb); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 __global__ void gscale_bwd_kernel(const double* dgb, const double* g, const float* gs, int n_u, int H, float* dgs,
@@ -769,7 +781,7 @@ __global__ void gscale_bwd_kernel(const double* dgb, const double* g, const floa
 }
 void gscale_bwd(const double* dgb, const double* g, const float* gscale, int n_u, int H, float* dgscale, double* dg,
                 cudaStream_t s) {
-    gscale_bwd_kernel<<<(H + 255) / 256, 256, 0, s>>>(dgb, g, gscale, n_u, H, dgscale, dg);
+    gscale_bwd_kernel<<<(H + 255) / 256, 256, 0, s>>>(dgb, g, gscale, n_u, H, dgscale, dg); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 // rows R = n_u + 1 (last = fps row, gradient = sum_u dg_u)
@@ -827,9 +839,9 @@ void global_embed_bwd(const double* dg, int n_u, const double* phi, const double
     // scratch dz lives after h_in's rows? keep it simple: allocate per call (tiny, (n_u+1) x H doubles)
     double* dz = nullptr;
     MGV_CUDA(cudaMallocAsync(&dz, sizeof(double) * (size_t)(n_u + 1) * H, s));
-    gmlp_out_bwd_kernel<<<grid_for((int64_t)H * H), 256, 0, s>>>(dg, n_u, h_in, H, dw_out, db_out);
-    gmlp_dz_kernel<<<dim3((H + 127) / 128, n_u + 1), 128, 0, s>>>(dg, n_u, z_in, w_out, H, dz);
-    gmlp_in_bwd_kernel<<<grid_for((int64_t)H * 32), 256, 0, s>>>(dz, n_u + 1, phi, H, dw_in, db_in);
+    gmlp_out_bwd_kernel<<<grid_for((int64_t)H * H), 256, 0, s>>>(dg, n_u, h_in, H, dw_out, db_out); ::mgv::note_launch();
+    gmlp_dz_kernel<<<dim3((H + 127) / 128, n_u + 1), 128, 0, s>>>(dg, n_u, z_in, w_out, H, dz); ::mgv::note_launch();
+    gmlp_in_bwd_kernel<<<grid_for((int64_t)H * 32), 256, 0, s>>>(dz, n_u + 1, phi, H, dw_in, db_in); ::mgv::note_launch();
     MGV_CUDA(cudaFreeAsync(dz, s));
     MGV_CUDA(cudaGetLastError());
 }
@@ -845,15 +857,15 @@ __global__ void sumsq_kernel(const float* x, int64_t n, double* part) {
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
 void sumsq(const float* x, int64_t n, double* part, double* out, cudaStream_t s) {
-    sumsq_kernel<<<1024, RT, 0, s>>>(x, n, part);
-    sum_double_kernel<<<1, 1, 0, s>>>(part, 1024, out);
+    sumsq_kernel<<<1024, RT, 0, s>>>(x, n, part); ::mgv::note_launch();
+    sum_double_kernel<<<1, 1, 0, s>>>(part, 1024, out); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 __global__ void fill_kernel(float* p, int64_t n, float v) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) p[e] = v;
 }
 void fill_f32(float* p, int64_t n, float v, cudaStream_t s) {
-    fill_kernel<<<grid_for(n), 256, 0, s>>>(p, n, v);
+    fill_kernel<<<grid_for(n), 256, 0, s>>>(p, n, v); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -870,7 +882,8 @@ void fill_f32(float* p, int64_t n, float v, cudaStream_t s) {
     template void qk_norm_rope<T>(const T*, int, int, int, const float*, const float2*, T*, float*, float*,           \
                                   cudaStream_t);                                                                      \
     template void flow_loss_fwd<T>(const float*, const float*, const uint8_t*, int, int, double*, cudaStream_t);      \
-    template void flow_loss_bwd<T>(const float*, const float*, const uint8_t*, int, int, float, T*, cudaStream_t);    \
+    template void flow_loss_bwd<T>(const float*, const float*, const uint8_t*, int, int, float, const int*, T*,       \
+                                   cudaStream_t);                                                                    \
     template void gate_bwd<T>(const float*, const T*, const float*, int64_t, int, const int32_t*, int, int, int, T*,  \
                               float*, float*, cudaStream_t);                                                          \
     template void rms_mod_bwd<T>(const T*, const float*, const float*, const float*, int64_t, int, int,               \

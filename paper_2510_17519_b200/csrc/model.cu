@@ -187,6 +187,60 @@ void Model::plan_workspace(int64_t N, int64_t L, int n_u) {
     (void)n_u;
 }
 
+// ------------------------------------------------------------------ profiler
+cudaEvent_t Prof::get() {
+    cudaEvent_t e;
+    if (!pool_.empty()) {
+        e = pool_.back();
+        pool_.pop_back();
+    } else {
+        MGV_CUDA(cudaEventCreate(&e));
+    }
+    used_.push_back(e);
+    return e;
+}
+void Prof::begin(const char* name, cudaStream_t s) {
+    if (!on) return;
+    Pend p{name, get(), nullptr};
+    MGV_CUDA(cudaEventRecord(p.a, s));
+    pend_.push_back(p);
+}
+void Prof::end(cudaStream_t s) {
+    if (!on) return;
+    for (auto it = pend_.rbegin(); it != pend_.rend(); ++it)
+        if (!it->b) {
+            it->b = get();
+            MGV_CUDA(cudaEventRecord(it->b, s));
+            return;
+        }
+}
+void Prof::end_step() {
+    for (auto& p : pend_) {
+        if (!p.b) continue;
+        float ms = 0.0f;
+        MGV_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+        Stat& st = stats[p.name];
+        st.ms += ms;
+        st.n += 1;
+    }
+    pend_.clear();
+    for (auto e : used_) pool_.push_back(e);
+    used_.clear();
+}
+Prof::~Prof() {
+    for (auto e : pool_) cudaEventDestroy(e);
+    for (auto e : used_) cudaEventDestroy(e);
+}
+
+__global__ void set_taus_kernel(double* taus, double t) {
+    taus[0] = t;
+    taus[1] = 0.0;
+}
+static void set_taus(double* taus, double t, cudaStream_t s) {
+    set_taus_kernel<<<1, 1, 0, s>>>(taus, t);
+    note_launch();
+}
+
 // ------------------------------------------------------------------ model
 Model::Model(int device, bool bf16) : device_(device), bf16_(bf16) {
     MGV_CUDA(cudaSetDevice(device));
@@ -335,7 +389,7 @@ void Model::upload(const Cfg& cfg, int64_t n, const char* const* names, const do
             throw DimensionError("parameter " + p.name + " has " + std::to_string(numel[gi]) + " elements, expected " +
                                  std::to_string(p.numel));
         MGV_CUDA(cudaMemcpyAsync(staging, data[gi], sizeof(double) * p.numel, cudaMemcpyHostToDevice, stream_));
-        f64_to_f32_bf16<<<grid_of(p.numel), 256, 0, stream_>>>(staging, p.numel, p.f32, p.bf);
+        f64_to_f32_bf16<<<grid_of(p.numel), 256, 0, stream_>>>(staging, p.numel, p.f32, p.bf); ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
     }
     MGV_CUDA(cudaStreamSynchronize(stream_));
@@ -403,7 +457,9 @@ void Model::block_fwd(int i, int64_t N) {
     qk_norm_rope<T>(tp<T>(b.qkv), n, H, nh, P(blk(i, "attn.temp")).f32, w.cs, tp<T>(b.qk), b.iq, b.ik, s);  // :289-294
     AttnProblem ap{b.qk, 2 * H, off<T>(b.qk, H), 2 * H, off<T>(b.qkv, 2 * H), 3 * H, b.O, H, b.lse,
                    n, n, int(nh), int(hd)};
+    prof_.begin("attn_fwd", s);
     attention_fwd<T>(bf, ap, s);  // mha (autodiff.cpp:755-793)
+    prof_.end(s);
     gemm(bf, KM(b.O, H), KM(W(blk(i, "attn.out.w")), H), n, H, H,
          EpiGateResid<T>{Xin, b.X1, H, tp<T>(b.ao), H, P(blk(i, "attn.out.b")).f32, tab + 2 * H, tld, w.mod_id, n,
                          int(H)},
@@ -416,7 +472,9 @@ void Model::block_fwd(int i, int64_t N) {
     gemm(bf, KM(w.text, cfg_.text_dim), KM(W(blk(i, "xattn.kv.w")), cfg_.text_dim), int(L), 2 * H, cfg_.text_dim,
          EpiStore<T>{tp<T>(b.kv), 2 * H, P(blk(i, "xattn.kv.b")).f32, 1.0f, int(L), int(2 * H)}, s);
     AttnProblem xp{b.cqs, H, b.kv, 2 * H, off<T>(b.kv, H), 2 * H, b.Ox, H, b.lse_x, n, int(L), int(nh), int(hd)};
+    prof_.begin("xattn_fwd", s);
     attention_fwd<T>(bf, xp, s);
+    prof_.end(s);
     gemm(bf, KM(b.Ox, H), KM(W(blk(i, "xattn.out.w")), H), n, H, H,
          EpiStore<T>{tp<T>(b.co), H, P(blk(i, "xattn.out.b")).f32, 1.0f, n, int(H)}, s);
     postnorm_resid<T>(b.X1, tp<T>(b.co), n, H, P(blk(i, "xattn.postnorm.g")).f32, b.X2, b.rc, s);
@@ -468,7 +526,9 @@ void Model::block_bwd(int i, int64_t N) {
     gemm(bf, KM(w.s1, H), MN(W(blk(i, "xattn.out.w")), H), n, H, H, EpiStore<T>{tp<T>(w.s2), H, nullptr, 1.0f, n, int(H)}, s);
     AttnBwdProblem xb{AttnProblem{b.cqs, H, b.kv, 2 * H, off<T>(b.kv, H), 2 * H, b.Ox, H, b.lse_x, n, int(L), int(nh), int(hd)},
                       w.s2, H, w.Dvec, w.s1, H, w.dkv, 2 * H, off<T>(w.dkv, H), 2 * H, w.dkv_part, w.q_splits_x};
+    prof_.begin("xattn_bwd", s);
     attention_bwd<T>(bf, xb, s);
+    prof_.end(s);
     const float xscale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd)));
     gemm(bf, MN(w.dkv, 2 * H), MN(w.text, cfg_.text_dim), 2 * H, cfg_.text_dim, int(L),
          EpiF32{G(blk(i, "xattn.kv.w")), cfg_.text_dim, nullptr, 1.0f, 1, int(2 * H), int(cfg_.text_dim)}, s);
@@ -488,7 +548,9 @@ void Model::block_bwd(int i, int64_t N) {
     gemm(bf, KM(w.s1, H), MN(W(blk(i, "attn.out.w")), H), n, H, H, EpiStore<T>{tp<T>(w.s2), H, nullptr, 1.0f, n, int(H)}, s);
     AttnBwdProblem ab{AttnProblem{b.qk, 2 * H, off<T>(b.qk, H), 2 * H, off<T>(b.qkv, 2 * H), 3 * H, b.O, H, b.lse, n, n, int(nh), int(hd)},
                       w.s2, H, w.Dvec, w.sB, 3 * H, off<T>(w.sB, H), 3 * H, off<T>(w.sB, 2 * H), 3 * H, nullptr, 1};
+    prof_.begin("attn_bwd", s);
     attention_bwd<T>(bf, ab, s);
+    prof_.end(s);
     qk_norm_rope_bwd<T>(tp<T>(w.sB), tp<T>(b.qkv), n, H, nh, P(blk(i, "attn.temp")).f32, w.cs, b.iq, b.ik, w.part1, s);
     reduce_chunks(w.part1, chunks, nh, G(blk(i, "attn.temp")), 1.0f, 1, s);
     colsum<T>(tp<T>(w.sB), 3 * H, n, 3 * H, w.part1, s);
@@ -528,7 +590,9 @@ void Model::forward_sample(const DevSample& smp, const void* rows_in, const doub
         gemm(bf, KM(rows_in, D), KM(W("dit.patch.w"), D), n, H, D,
              EpiF32{w.X[0], H, P("dit.patch.b").f32, 1.0f, 0, n, int(H)}, s);
     (void)grads;
+    prof_.begin("blocks_fwd", s);
     for (int i = 0; i < cfg_.depth; ++i) block_fwd<T>(i, w.N);
+    prof_.end(s);
     const float* Xf = w.X[w.grads ? cfg_.depth : (cfg_.depth % 2)];
     rms_gain<T>(Xf, n, H, P("dit.final.g").f32, tp<T>(w.fin), w.rf, s);  // dit.cpp:314
     if (head) {
@@ -561,7 +625,9 @@ void Model::backward_sample(const void* dV) {
     rms_gain_bwd<T>(tp<T>(w.s2), w.X[cfg_.depth], w.rf, P("dit.final.g").f32, n, H, w.dX, 0, w.part1, s);
     reduce_chunks(w.part1, chunks, H, G("dit.final.g"), 1.0f, 1, s);
     MGV_CUDA(cudaMemsetAsync(w.dg, 0, sizeof(double) * nu * H, s));
+    prof_.begin("blocks_bwd", s);
     for (int i = static_cast<int>(cfg_.depth) - 1; i >= 0; --i) block_bwd<T>(i, w.N);
+    prof_.end(s);
     // patch embedding (rows are constants, dit.cpp:327)
     convert_f32<T>(w.dX, (int64_t)n * H, tp<T>(w.s1), s);
     gemm(bf, MN(w.s1, H), MN(w.rows, D), H, int(D), n, EpiF32{G("dit.patch.w"), D, nullptr, 1.0f, 1, int(H), int(D)}, s);
@@ -580,10 +646,10 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
     if (n < 1) throw InputError("empty batch");  // flowtrain.cpp:258
     WS& w = *ws_;
     cudaStream_t s = stream_;
-    const int64_t H = cfg_.H(), D = cfg_.D();
+    const int64_t D = cfg_.D();
     int64_t maxN = 0;
     for (int64_t k = 0; k < n; ++k) maxN = std::max(maxN, samples[k].N);
-    // workspace
+    // workspace (arena grows only; the layout is re-derived for this batch)
     w.N = maxN;
     w.L = L;
     w.n_u = 2;
@@ -597,65 +663,60 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
         Sizer real{false, 0, &arena_};
         layout_ws(w, real, cfg_, true);
     }
-    MGV_CUDA(cudaMemsetAsync(grad_buf_, 0, sizeof(float) * grad_numel_, s));
-    convert_rows<T>(text_dev, L * cfg_.text_dim, tp<T>(w.text), s);
-    const int64_t B_global = n * world_;
-    double loss_sum = 0.0;
+    const int64_t launches0 = launch_count();
     cudaEvent_t e0, e1;
     MGV_CUDA(cudaEventCreate(&e0));
     MGV_CUDA(cudaEventCreate(&e1));
     MGV_CUDA(cudaEventRecord(e0, s));
-    std::vector<double> sample_loss(n);
+    prof_.begin_step();
+    MGV_CUDA(cudaMemsetAsync(grad_buf_, 0, sizeof(float) * grad_numel_, s));
+    MGV_CUDA(cudaMemsetAsync(w.scal, 0, sizeof(double) * 8, s));
+    convert_rows<T>(text_dev, L * cfg_.text_dim, tp<T>(w.text), s);
+    const int64_t B_global = n * world_;
     for (int64_t k = 0; k < n; ++k) {
         const DevSample& sm = samples[k];
         w.N = sm.N;
         const int N = static_cast<int>(sm.N);
         MGV_CUDA(cudaMemcpyAsync(w.coords, sm.coords, sizeof(int32_t) * 3 * N, cudaMemcpyDeviceToDevice, s));
         // interpolate + condition mask (flowtrain.cpp:265-267); taus {t, 0} (dit.cpp:242 dedup)
-        prep_flow_sample<T>(sm.clean, sm.noise, w.coords, N, int(D), sm.t, sm.first_frame, tp<T>(w.rows),
-                            w.vt, w.lmask, w.mod_id, s);
-        const double taus[2] = {sm.t, 0.0};
-        MGV_CUDA(cudaMemcpyAsync(w.taus, taus, sizeof(taus), cudaMemcpyHostToDevice, s));
+        prep_flow_sample<T>(sm.clean, sm.noise, w.coords, N, int(D), sm.t, sm.first_frame, tp<T>(w.rows), w.vt,
+                            w.lmask, w.mod_id, s);
         w.n_u = sm.first_frame ? 2 : 1;
-        forward_sample<T>(sm, w.rows, taus, w.n_u, w.mod_id, fps, true, true, nullptr);
-        if (v_dev && v_dev[k]) f32_to_f64<<<grid_of(N * D), 256, 0, s>>>(w.V, N * D, v_dev[k]);
-        // masked mean loss (autodiff.cpp:466-491)
+        set_taus(w.taus, sm.t, s);
+        forward_sample<T>(sm, w.rows, nullptr, w.n_u, w.mod_id, fps, true, true, nullptr);
+        if (v_dev && v_dev[k]) {
+            f32_to_f64<<<grid_of(N * D), 256, 0, s>>>(w.V, N * D, v_dev[k]);
+            note_launch();
+        }
+        // masked mean loss (autodiff.cpp:466-491), coefficient and accumulation on device
         count_mask(w.lmask, N, w.cnt, s);
         flow_loss_fwd<T>(w.V, w.vt, w.lmask, N, int(D), w.loss_part, s);
-        sum_double(w.loss_part, row_chunks(N), w.scal, s);
-        int cnt = 0;
-        double sq = 0.0;
-        MGV_CUDA(cudaMemcpyAsync(&cnt, w.cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
-        MGV_CUDA(cudaMemcpyAsync(&sq, w.scal, sizeof(double), cudaMemcpyDeviceToHost, s));
-        MGV_CUDA(cudaStreamSynchronize(s));
-        const double lb = cnt > 0 ? sq / (static_cast<double>(cnt) * D) : 0.0;
-        sample_loss[k] = lb;
-        loss_sum += lb;
-        if (!std::isfinite(lb)) throw NumericError("flow loss is not finite");  // flowtrain.cpp:276
-        if (cnt == 0) continue;  // all rows masked: zero loss, zero gradient (autodiff.cpp:482)
-        const float coef = static_cast<float>(2.0 / (static_cast<double>(B_global) * cnt * D));
-        flow_loss_bwd<T>(w.V, w.vt, w.lmask, N, int(D), coef, tp<T>(w.dV), s);
+        flow_loss_accumulate(w.loss_part, row_chunks(N), w.cnt, int(D), w.scal, s);  // scal[0] += l_b
+        flow_loss_bwd<T>(w.V, w.vt, w.lmask, N, int(D), static_cast<float>(2.0 / (double)B_global), w.cnt,
+                         tp<T>(w.dV), s);  // 2 (V - v*) / (B * n_b * D); all-masked -> 0
         backward_sample<T>(w.dV);
     }
     if (world_ > 1) {
+        prof_.begin("allreduce", s);
         MGV_NCCL(ncclAllReduce(grad_buf_, grad_buf_, grad_numel_, ncclFloat, ncclSum, comm_, s));
-        double* dl = w.scal + 1;
-        MGV_CUDA(cudaMemcpyAsync(dl, &loss_sum, sizeof(double), cudaMemcpyHostToDevice, s));
-        MGV_NCCL(ncclAllReduce(dl, dl, 1, ncclDouble, ncclSum, comm_, s));
-        MGV_CUDA(cudaMemcpyAsync(&loss_sum, dl, sizeof(double), cudaMemcpyDeviceToHost, s));
+        MGV_NCCL(ncclAllReduce(w.scal, w.scal, 1, ncclDouble, ncclSum, comm_, s));
+        prof_.end(s);
     }
     sumsq(grad_buf_, grad_numel_, w.loss_part, w.scal + 2, s);  // grad_norm (flowtrain.cpp:284-289)
-    double gsq = 0.0;
-    MGV_CUDA(cudaMemcpyAsync(&gsq, w.scal + 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    double host[3] = {0, 0, 0};
+    MGV_CUDA(cudaMemcpyAsync(host, w.scal, sizeof(double) * 3, cudaMemcpyDeviceToHost, s));
     MGV_CUDA(cudaEventRecord(e1, s));
     MGV_CUDA(cudaStreamSynchronize(s));
     float ms = 0.0f;
     MGV_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     last_ms_ = ms;
+    last_launches_ = launch_count() - launches0;
+    prof_.end_step();
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    *loss = loss_sum / static_cast<double>(B_global);  // flowtrain.cpp:273
-    *grad_norm = std::sqrt(gsq);
+    *loss = host[0] / static_cast<double>(B_global);  // flowtrain.cpp:273
+    if (!std::isfinite(*loss)) throw NumericError("flow loss is not finite");  // flowtrain.cpp:276
+    *grad_norm = std::sqrt(host[2]);
 }
 
 void Model::flow_step_dev(int64_t n, const DevSample* samples, const double* text_dev, int64_t L, double fps,
@@ -751,7 +812,7 @@ void Model::flow_step(int64_t n, const mgv_flow_sample* samples, const double* t
             auto* gd = static_cast<double*>(dalloc(sizeof(double) * maxn));
             for (size_t k = 0; k < sorted_.size(); ++k) {
                 if (!grads_out[k]) continue;
-                f32_to_f64<<<grid_of(sorted_[k]->numel), 256, 0, stream_>>>(sorted_[k]->grad, sorted_[k]->numel, gd);
+                f32_to_f64<<<grid_of(sorted_[k]->numel), 256, 0, stream_>>>(sorted_[k]->grad, sorted_[k]->numel, gd); ::mgv::note_launch();
                 MGV_CUDA(cudaMemcpyAsync(grads_out[k], gd, sizeof(double) * sorted_[k]->numel, cudaMemcpyDeviceToHost,
                                          stream_));
                 MGV_CUDA(cudaStreamSynchronize(stream_));
@@ -818,13 +879,13 @@ void Model::value_forward(const double* in, int64_t N, const int32_t* coords, co
     if (velocity) {
         convert_rows<T>(din, N * D, tp<T>(w.rows), s);
         forward_sample<T>(dummy, w.rows, uniq.data(), w.n_u, nullptr, fps, false, true, nullptr);
-        f32_to_f64<<<grid_of(N * D), 256, 0, s>>>(w.V, N * D, din);
+        f32_to_f64<<<grid_of(N * D), 256, 0, s>>>(w.V, N * D, din); ::mgv::note_launch();
         MGV_CUDA(cudaMemcpyAsync(out, din, sizeof(double) * N * D, cudaMemcpyDeviceToHost, s));
     } else {
         // tokens enter the residual stream directly (dit.cpp:369)
-        f64_to_f32_bf16<<<grid_of(N * H), 256, 0, s>>>(din, N * H, w.X[0], nullptr);
+        f64_to_f32_bf16<<<grid_of(N * H), 256, 0, s>>>(din, N * H, w.X[0], nullptr); ::mgv::note_launch();
         forward_sample<T>(dummy, nullptr, uniq.data(), w.n_u, nullptr, fps, false, false, outf);
-        f32_to_f64<<<grid_of(N * H), 256, 0, s>>>(outf, N * H, din);
+        f32_to_f64<<<grid_of(N * H), 256, 0, s>>>(outf, N * H, din); ::mgv::note_launch();
         MGV_CUDA(cudaMemcpyAsync(out, din, sizeof(double) * N * H, cudaMemcpyDeviceToHost, s));
     }
     MGV_CUDA(cudaFreeAsync(outf, s));

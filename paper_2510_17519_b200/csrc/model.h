@@ -74,6 +74,32 @@ private:
     size_t cap_ = 0, off_ = 0;
 };
 
+// Optional per-phase device timing (CUDA events on the launching stream), used by the
+// benchmark for the roofline figures.  Off by default; no host syncs when on.
+class Prof {
+public:
+    struct Stat {
+        double ms = 0.0;
+        int64_t n = 0;
+    };
+    bool on = false;
+    std::map<std::string, Stat> stats;
+    void begin_step() { pend_.clear(); }
+    void begin(const char* name, cudaStream_t s);
+    void end(cudaStream_t s);
+    void end_step();  // after the stream was synchronised
+    ~Prof();
+
+private:
+    struct Pend {
+        std::string name;
+        cudaEvent_t a, b;
+    };
+    cudaEvent_t get();
+    std::vector<Pend> pend_;
+    std::vector<cudaEvent_t> pool_, used_;
+};
+
 class Model {
 public:
     Model(int device, bool bf16);
@@ -98,6 +124,8 @@ public:
                        double* loss, double* grad_norm, double* const* v_dev = nullptr);
 
     double last_step_ms() const { return last_ms_; }
+    int64_t last_step_launches() const { return last_launches_; }
+    Prof& prof() { return prof_; }
     bool bf16() const { return bf16_; }
     cudaStream_t stream() const { return stream_; }
 
@@ -136,6 +164,8 @@ private:
     int64_t grad_numel_ = 0;
     Arena arena_;
     double last_ms_ = 0.0;
+    int64_t last_launches_ = 0;
+    Prof prof_;
     // NCCL data parallel
     ncclComm_t comm_ = nullptr;
     int rank_ = 0, world_ = 1;
