@@ -23,6 +23,9 @@ struct AttnProblem {
     int64_t o_ld;
     float* lse;  // [heads][Nq]
     int Nq, Nk, heads, hd;
+    // tensor-core path: V^T ([heads*hd][>= Nk], row h*hd+d holds v[:, h*hd+d]); null -> computed internally
+    const void* vt = nullptr;
+    int64_t vt_ld = 0;
 };
 
 struct AttnBwdProblem {
@@ -38,6 +41,13 @@ struct AttnBwdProblem {
     int64_t dv_ld;
     float* dkv_part;  // [q_splits][heads][Nk][2*hd] scratch when q_splits > 1
     int q_splits;
+    // tensor-core path: transposed Q, K, dO ([heads*hd][>= N] rows); provided by the caller's scratch
+    void* qt = nullptr;
+    int64_t qt_ld = 0;
+    void* kt = nullptr;
+    int64_t kt_ld = 0;
+    void* dot = nullptr;
+    int64_t dot_ld = 0;
 };
 
 // IEEE-fp32 math on T storage (T = float or bf16): the parity path

@@ -1,21 +1,24 @@
 // tcgen05 flash-attention backward for sm_100a, deterministic (no atomics):
-// the gradient of Tape::mha (autodiff.cpp:795-843) computed in two passes.
+// the gradient of Tape::mha (autodiff.cpp:795-843) in two passes.
 //
 //   dK/dV pass  CTA per (128-key tile, head), loops over 64-query tiles:
-//                 S^T = K Q^T, dP^T = V dO^T            (TMEM, N = 64)
+//                 S^T = K Q^T,  dP^T = V dO^T          (TMEM; Q^T/dO^T tiles read MN-major)
 //                 P^T = exp(S^T - lse), dS^T = P^T (dP^T - D)   (thread = key row)
-//                 dV += P^T dO, dK += dS^T Q            (TMEM accumulators, dO/Q read MN-major)
+//                 dV += P^T dO, dK += dS^T Q           (ONE N=hd MMA per step: dO^T/Q^T read K-major)
 //   dQ pass     CTA per (128-query tile, head), loops over 64-key tiles:
-//                 S = Q K^T, dP = dO V^T  (double-buffered in TMEM)
-//                 dS = P (dP - D)                       (thread = query row)
-//                 dQ += dS K                            (K read MN-major)
-// The MMA warp software-pipelines the next tile's S/dP products under the
-// current tile's elementwise work.  Layouts follow attn_tc.cu (64-col SW128
-// chunks + 16-col SW32 tail for head_dim 144).
+//                 S = Q K^T, dP = dO V^T               (double-buffered in TMEM)
+//                 dS = P (dP - D)                      (thread = query row)
+//                 dQ += dS K                           (K^T tile read K-major, N = hd)
+// The transposed operands (Q^T, K^T, V^T, dO^T: [heads*hd][tokens]) are made
+// once per step by a tiled transpose, so no MMA ever splits head_dim 144 into
+// 128 + 16.  The MMA warp issues the next tile's S/dP products under the
+// current tile's elementwise work.
 #include <cfloat>
+#include <vector>
 
 #include "attn.h"
 #include "gemm.cuh"
+#include "kernels.h"
 #include "ptx.cuh"
 
 namespace mgv {
@@ -24,13 +27,12 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 
-template <int HD, int R>
-struct Tile {
+template <int HD>
+struct BT {
     static constexpr int NF = HD / 64;
     static constexpr int TAIL = HD % 64;
-    static constexpr int CH = R * 128;  // bytes of one 64-column SW128 chunk
-    static constexpr int TB = R * 32;   // bytes of the 16-column SW32 tail
-    static constexpr int BYTES = NF * CH + (TAIL ? TB : 0);
+    static constexpr int ROW_TILE = NF * 16384 + (TAIL ? 4096 : 0);  // 128 tokens x HD, K-major over hd
+    static constexpr int T_TILE = HD * 128;                          // HD rows x 64 tokens (transposed, SW128)
 };
 
 __device__ __forceinline__ float ex2f(float x) {
@@ -39,54 +41,51 @@ __device__ __forceinline__ float ex2f(float x) {
     return y;
 }
 
-template <int HD, int R>
-__device__ __forceinline__ void load_tile_r(uint8_t* dst, const CUtensorMap* m128, const CUtensorMap* m32,
-                                            uint64_t* bar, int col0, int row0) {
-    using T = Tile<HD, R>;
+template <int HD>
+__device__ __forceinline__ void load_row_tile(uint8_t* dst, const CUtensorMap* m128, const CUtensorMap* m32,
+                                              uint64_t* bar, int col0, int row0) {
+    using T = BT<HD>;
 #pragma unroll
-    for (int c = 0; c < T::NF; ++c) tma_load_2d(dst + c * T::CH, m128, bar, col0 + c * 64, row0);
-    if (T::TAIL) tma_load_2d(dst + T::NF * T::CH, m32, bar, col0 + T::NF * 64, row0);
+    for (int c = 0; c < T::NF; ++c) tma_load_2d(dst + c * 16384, m128, bar, col0 + c * 64, row0);
+    if (T::TAIL) tma_load_2d(dst + T::NF * 16384, m32, bar, col0 + T::NF * 64, row0);
 }
 
-// D (+)= A B^T with A (128 rows, K-major over HD) and B (N rows, K-major over HD).
-template <int HD, int RA, int RB>
-__device__ __forceinline__ void mma_kmajor_hd(uint32_t d, uint32_t a, uint32_t b, uint32_t idesc) {
-    using TA = Tile<HD, RA>;
-    using TB = Tile<HD, RB>;
+// D[128 x 64] = A[128 x HD] . B^T where A is a 128-row tile K-major over hd and B^T is an
+// HD x 64 transposed tile read MN-major (N = 64 tokens, K = hd rows).
+template <int HD>
+__device__ __forceinline__ void mma_rows_x_t(uint32_t d, uint32_t a, uint32_t bt) {
+    using T = BT<HD>;
+    constexpr uint32_t id = idesc_bf16_f32(128, 64, false, true);
     int kk = 0;
 #pragma unroll
-    for (int c = 0; c < TA::NF; ++c)
+    for (int c = 0; c < T::NF; ++c)
 #pragma unroll
         for (int k = 0; k < 4; ++k, ++kk)
-            umma_f16_ss(d, smem_desc(a + c * TA::CH + k * 32, 16, 1024, kSwizzle128),
-                        smem_desc(b + c * TB::CH + k * 32, 16, 1024, kSwizzle128), idesc, kk > 0);
-    if (TA::TAIL)
-        umma_f16_ss(d, smem_desc(a + TA::NF * TA::CH, 16, 256, kSwizzle32),
-                    smem_desc(b + TB::NF * TB::CH, 16, 256, kSwizzle32), idesc, 1);
+            umma_f16_ss(d, smem_desc(a + c * 16384 + k * 32, 16, 1024, kSwizzle128),
+                        smem_desc(bt + kk * 2048, 16, 1024, kSwizzle128), id, kk > 0);
+    if (T::TAIL)
+        umma_f16_ss(d, smem_desc(a + T::NF * 16384, 16, 256, kSwizzle32),
+                    smem_desc(bt + kk * 2048, 16, 1024, kSwizzle128), id, 1);
 }
 
-// D[128 x HD] (+)= A[128 x KR] * B where A is a 128 x KR bf16 K-major SW128 chunk (KR = 64)
-// and B is an R=KR-row tile [KR][HD] read MN-major (N = HD split 128|64 + 16).
-template <int HD, int KR>
-__device__ __forceinline__ void mma_mn_hd(uint32_t d, uint32_t a, uint32_t b, bool acc_first) {
-    using TB = Tile<HD, KR>;
-    constexpr uint32_t idA = idesc_bf16_f32(128, TB::NF >= 2 ? 128 : 64, false, true);
-    constexpr uint32_t idT = idesc_bf16_f32(128, 16, false, true);
+// D[128 x HD] (+)= A[128 x 64] . B where A is a 128 x 64 K-major chunk (smem) and B is the HD x 64
+// transposed tile read K-major (N = HD rows, K = 64 tokens): one N = HD MMA per 16-token step.
+template <int HD>
+__device__ __forceinline__ void mma_chunk_x_t(uint32_t d, uint32_t a, uint32_t bt, bool acc_first) {
+    constexpr uint32_t id = idesc_bf16_f32(128, HD, false, false);
 #pragma unroll
-    for (int ks = 0; ks < KR / 16; ++ks) {
-        const uint64_t ad = smem_desc(a + ks * 32, 16, 1024, kSwizzle128);
-        const uint32_t acc = (acc_first || ks > 0) ? 1u : 0u;
-        umma_f16_ss(d, ad, smem_desc(b + ks * 2048, TB::CH, 1024, kSwizzle128), idA, acc);
-        if (TB::TAIL) umma_f16_ss(d + TB::NF * 64, ad, smem_desc(b + TB::NF * TB::CH + ks * 512, 0, 256, kSwizzle32), idT, acc);
-    }
+    for (int ks = 0; ks < 4; ++ks)
+        umma_f16_ss(d, smem_desc(a + ks * 32, 16, 1024, kSwizzle128), smem_desc(bt + ks * 32, 16, 1024, kSwizzle128),
+                    id, (acc_first || ks > 0) ? 1u : 0u);
 }
 
-// Row (thread) -> 64 bf16 values into a 128 x 64 SW128 K-major chunk.
+// thread row -> 64 bf16 values of a 128 x 64 SW128 K-major chunk
 __device__ __forceinline__ void st_row64(uint8_t* chunk, int row, const uint32_t* pk) {
+    const uint32_t base = smem_u32(chunk) + row * 128;
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-        *reinterpret_cast<uint4*>(chunk + row * 128 + ((u ^ (row & 7)) << 4)) =
-            make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(base + ((u ^ (row & 7)) << 4)), "r"(pk[4 * u]),
+                     "r"(pk[4 * u + 1]), "r"(pk[4 * u + 2]), "r"(pk[4 * u + 3]));
 }
 
 template <int HD>
@@ -108,8 +107,8 @@ __device__ __forceinline__ void store_acc_row(uint32_t taddr, __nv_bfloat16* out
 }
 
 struct BwdMaps {
-    CUtensorMap k128, k32, v128, v32;    // key tiles
-    CUtensorMap q128, q32, do128, do32;  // query tiles
+    CUtensorMap a128, a32, b128, b32;  // row tiles (dkv: K, V ; dq: Q, dO)
+    CUtensorMap ta, tb;                // transposed tiles (dkv: Q^T, dO^T ; dq: K^T, V^T)
 };
 
 }  // namespace
@@ -118,17 +117,16 @@ struct BwdMaps {
 template <int HD>
 __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_constant__ BwdMaps tm, AttnBwdProblem p) {
     constexpr int BKV = 128, BQ = 64;
-    using TK = Tile<HD, BKV>;
-    using TQ = Tile<HD, BQ>;
+    using T = BT<HD>;
     constexpr int DV_COL = 128, DK_COL = HD <= 128 ? 256 : 320;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sK = smem;
-    uint8_t* sV = sK + TK::BYTES;
-    uint8_t* sQ = sV + TK::BYTES;          // [2]
-    uint8_t* sdO = sQ + 2 * TQ::BYTES;     // [2]
-    uint8_t* sPT = sdO + 2 * TQ::BYTES;    // [2] x 16 KB
-    uint8_t* sdST = sPT + 2 * 16384;       // [2] x 16 KB
+    uint8_t* sV = sK + T::ROW_TILE;
+    uint8_t* sQt = sV + T::ROW_TILE;      // [2]
+    uint8_t* sdOt = sQt + 2 * T::T_TILE;  // [2]
+    uint8_t* sPT = sdOt + 2 * T::T_TILE;  // [2] x 16 KB
+    uint8_t* sdST = sPT + 2 * 16384;      // [2] x 16 KB
     float* sLse = reinterpret_cast<float*>(sdST + 2 * 16384);  // [2][64] (log2 domain)
     float* sD = sLse + 2 * BQ;                                  // [2][64]
     uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * BQ);
@@ -170,19 +168,18 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        // ---------------- producer: K, V once; Q, dO, lse, D per query tile
         if (lane == 0) {
-            mbar_arrive_expect_tx(kv_full, 2 * TK::BYTES);
-            load_tile_r<HD, BKV>(sK, &tm.k128, &tm.k32, kv_full, col, k0);
-            load_tile_r<HD, BKV>(sV, &tm.v128, &tm.v32, kv_full, col, k0);
+            mbar_arrive_expect_tx(kv_full, 2 * T::ROW_TILE);
+            load_row_tile<HD>(sK, &tm.a128, &tm.a32, kv_full, col, k0);
+            load_row_tile<HD>(sV, &tm.b128, &tm.b32, kv_full, col, k0);
         }
         for (int i = 0; i < nq; ++i) {
             const int st = i & 1;
             if (i >= 2) mbar_wait(&qd_empty[st], ((i - 2) >> 1) & 1);
             if (lane == 0) {
-                mbar_arrive_expect_tx(&qd_full[st], 2 * TQ::BYTES);
-                load_tile_r<HD, BQ>(sQ + st * TQ::BYTES, &tm.q128, &tm.q32, &qd_full[st], col, i * BQ);
-                load_tile_r<HD, BQ>(sdO + st * TQ::BYTES, &tm.do128, &tm.do32, &qd_full[st], col, i * BQ);
+                mbar_arrive_expect_tx(&qd_full[st], 2 * T::T_TILE);
+                tma_load_2d(sQt + st * T::T_TILE, &tm.ta, &qd_full[st], i * BQ, col);
+                tma_load_2d(sdOt + st * T::T_TILE, &tm.tb, &qd_full[st], i * BQ, col);
             }
             for (int c = lane; c < BQ; c += 32) {
                 const int q = i * BQ + c;
@@ -192,15 +189,13 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
             mbar_arrive(&lse_full[st]);
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer
-        constexpr uint32_t idS = idesc_bf16_f32(128, BQ, false, false);
         const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+        mbar_wait(kv_full, 0);
         auto issue_s = [&](int i) {
             const int st = i & 1;
-            mma_kmajor_hd<HD, BKV, BQ>(tmem + 0, aK, smem_u32(sQ + st * TQ::BYTES), idS);
-            mma_kmajor_hd<HD, BKV, BQ>(tmem + 64, aV, smem_u32(sdO + st * TQ::BYTES), idS);
+            mma_rows_x_t<HD>(tmem + 0, aK, smem_u32(sQt + st * T::T_TILE));
+            mma_rows_x_t<HD>(tmem + 64, aV, smem_u32(sdOt + st * T::T_TILE));
         };
-        mbar_wait(kv_full, 0);
         if (nq > 0) {
             mbar_wait(&qd_full[0], 0);
             tc_fence_after();
@@ -225,8 +220,8 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
             mbar_wait(p_full, i & 1);
             tc_fence_after();
             if (elect_one()) {
-                mma_mn_hd<HD, BQ>(tmem + DV_COL, smem_u32(sPT + st * 16384), smem_u32(sdO + st * TQ::BYTES), i > 0);
-                mma_mn_hd<HD, BQ>(tmem + DK_COL, smem_u32(sdST + st * 16384), smem_u32(sQ + st * TQ::BYTES), i > 0);
+                mma_chunk_x_t<HD>(tmem + DV_COL, smem_u32(sPT + st * 16384), smem_u32(sdOt + st * T::T_TILE), i > 0);
+                mma_chunk_x_t<HD>(tmem + DK_COL, smem_u32(sdST + st * 16384), smem_u32(sQt + st * T::T_TILE), i > 0);
                 umma_commit(&pd_done[st]);
                 umma_commit(&qd_empty[st]);
                 if (i == nq - 1) umma_commit(acc_done);
@@ -234,7 +229,6 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
             __syncwarp();
         }
     } else if (warp >= 4) {
-        // ---------------- elementwise: thread = key row
         const int wq = warp - 4, row = wq * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
         for (int i = 0; i < nq; ++i) {
@@ -254,9 +248,10 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
             const float* lse2 = sLse + st * BQ;
             const float* Dq = sD + st * BQ;
             uint32_t pk[BQ / 2], dk[BQ / 2];
+            const bool full = (i + 1) * BQ <= f.Nq;
 #pragma unroll
             for (int c = 0; c < BQ; c += 2) {
-                const bool v0 = i * BQ + c < f.Nq, v1 = i * BQ + c + 1 < f.Nq;
+                const bool v0 = full || i * BQ + c < f.Nq, v1 = full || i * BQ + c + 1 < f.Nq;
                 const float p0 = v0 ? ex2f(fmaf(s[c], kLog2e, -lse2[c])) : 0.0f;
                 const float p1 = v1 ? ex2f(fmaf(s[c + 1], kLog2e, -lse2[c + 1])) : 0.0f;
                 pk[c / 2] = pack_bf16(p0, p1);
@@ -289,16 +284,15 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
 template <int HD>
 __global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_constant__ BwdMaps tm, AttnBwdProblem p) {
     constexpr int BMQ = 128, BKV = 64;
-    using TQ = Tile<HD, BMQ>;
-    using TK = Tile<HD, BKV>;
+    using T = BT<HD>;
     constexpr int DQ_COL = 256;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;
-    uint8_t* sdO = sQ + TQ::BYTES;
-    uint8_t* sK = sdO + TQ::BYTES;    // [2]
-    uint8_t* sV = sK + 2 * TK::BYTES;  // [2]
-    uint8_t* sdS = sV + 2 * TK::BYTES;  // [2] x 16 KB
+    uint8_t* sdO = sQ + T::ROW_TILE;
+    uint8_t* sKt = sdO + T::ROW_TILE;    // [2]
+    uint8_t* sVt = sKt + 2 * T::T_TILE;  // [2]
+    uint8_t* sdS = sVt + 2 * T::T_TILE;  // [2] x 16 KB
     uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + 2 * 16384);
     uint64_t* q_full = bars;
     uint64_t* kv_full = bars + 1;   // [2]
@@ -337,23 +331,22 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_con
 
     if (warp == 0) {
         if (elect_one()) {
-            mbar_arrive_expect_tx(q_full, 2 * TQ::BYTES);
-            load_tile_r<HD, BMQ>(sQ, &tm.q128, &tm.q32, q_full, col, q0);
-            load_tile_r<HD, BMQ>(sdO, &tm.do128, &tm.do32, q_full, col, q0);
+            mbar_arrive_expect_tx(q_full, 2 * T::ROW_TILE);
+            load_row_tile<HD>(sQ, &tm.a128, &tm.a32, q_full, col, q0);
+            load_row_tile<HD>(sdO, &tm.b128, &tm.b32, q_full, col, q0);
             for (int j = 0; j < nkv; ++j) {
                 const int b = j & 1;
                 if (j >= 2) mbar_wait(&kv_empty[b], ((j - 2) >> 1) & 1);
-                mbar_arrive_expect_tx(&kv_full[b], 2 * TK::BYTES);
-                load_tile_r<HD, BKV>(sK + b * TK::BYTES, &tm.k128, &tm.k32, &kv_full[b], col, j * BKV);
-                load_tile_r<HD, BKV>(sV + b * TK::BYTES, &tm.v128, &tm.v32, &kv_full[b], col, j * BKV);
+                mbar_arrive_expect_tx(&kv_full[b], 2 * T::T_TILE);
+                tma_load_2d(sKt + b * T::T_TILE, &tm.ta, &kv_full[b], j * BKV, col);
+                tma_load_2d(sVt + b * T::T_TILE, &tm.tb, &kv_full[b], j * BKV, col);
             }
         }
     } else if (warp == 1) {
-        constexpr uint32_t idS = idesc_bf16_f32(128, BKV, false, false);
         const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO);
         auto issue_dq = [&](int j) {
             const int b = j & 1;
-            mma_mn_hd<HD, BKV>(tmem + DQ_COL, smem_u32(sdS + b * 16384), smem_u32(sK + b * TK::BYTES), j > 0);
+            mma_chunk_x_t<HD>(tmem + DQ_COL, smem_u32(sdS + b * 16384), smem_u32(sKt + b * T::T_TILE), j > 0);
             umma_commit(&ds_empty[b]);
             umma_commit(&kv_empty[b]);
         };
@@ -364,8 +357,8 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_con
             if (j >= 2) mbar_wait(&s_empty[b], ((j - 2) >> 1) & 1);
             tc_fence_after();
             if (elect_one()) {
-                mma_kmajor_hd<HD, BMQ, BKV>(tmem + b * 128, aQ, smem_u32(sK + b * TK::BYTES), idS);
-                mma_kmajor_hd<HD, BMQ, BKV>(tmem + b * 128 + 64, adO, smem_u32(sV + b * TK::BYTES), idS);
+                mma_rows_x_t<HD>(tmem + b * 128, aQ, smem_u32(sKt + b * T::T_TILE));
+                mma_rows_x_t<HD>(tmem + b * 128 + 64, adO, smem_u32(sVt + b * T::T_TILE));
                 umma_commit(&s_full[b]);
             }
             __syncwarp();
@@ -405,9 +398,10 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_con
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[b]);
             uint32_t dk[BKV / 2];
+            const bool full = (j + 1) * BKV <= f.Nk;
 #pragma unroll
             for (int c = 0; c < BKV; c += 2) {
-                const bool v0 = j * BKV + c < f.Nk, v1 = j * BKV + c + 1 < f.Nk;
+                const bool v0 = full || j * BKV + c < f.Nk, v1 = full || j * BKV + c + 1 < f.Nk;
                 const float p0 = v0 ? ex2f(fmaf(s[c], kLog2e, -lse2)) : 0.0f;
                 const float p1 = v1 ? ex2f(fmaf(s[c + 1], kLog2e, -lse2)) : 0.0f;
                 dk[c / 2] = pack_bf16(p0 * (dp[c] - Dq), p1 * (dp[c + 1] - Dq));
@@ -432,59 +426,74 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_con
 
 // ------------------------------------------------------------------ host
 template <int HD>
-static void make_maps(BwdMaps* m, const AttnBwdProblem& p, int krows, int qrows) {
+static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, const void* kt, int64_t kt_ld,
+                       const void* vt, int64_t vt_ld, const void* dot, int64_t dot_ld, cudaStream_t s) {
+    using T = BT<HD>;
     const AttnProblem& f = p.f;
     const uint64_t W = (uint64_t)f.heads * HD;
-    make_tmap_sw(&m->k128, f.k, W, f.Nk, f.k_ld, 64, krows, CU_TENSOR_MAP_SWIZZLE_128B);
-    make_tmap_sw(&m->k32, f.k, W, f.Nk, f.k_ld, 16, krows, CU_TENSOR_MAP_SWIZZLE_32B);
-    make_tmap_sw(&m->v128, f.v, W, f.Nk, f.v_ld, 64, krows, CU_TENSOR_MAP_SWIZZLE_128B);
-    make_tmap_sw(&m->v32, f.v, W, f.Nk, f.v_ld, 16, krows, CU_TENSOR_MAP_SWIZZLE_32B);
-    make_tmap_sw(&m->q128, f.q, W, f.Nq, f.q_ld, 64, qrows, CU_TENSOR_MAP_SWIZZLE_128B);
-    make_tmap_sw(&m->q32, f.q, W, f.Nq, f.q_ld, 16, qrows, CU_TENSOR_MAP_SWIZZLE_32B);
-    make_tmap_sw(&m->do128, p.dO, W, f.Nq, p.do_ld, 64, qrows, CU_TENSOR_MAP_SWIZZLE_128B);
-    make_tmap_sw(&m->do32, p.dO, W, f.Nq, p.do_ld, 16, qrows, CU_TENSOR_MAP_SWIZZLE_32B);
-}
-
-template <int HD>
-static void launch_bwd(const AttnBwdProblem& p, cudaStream_t s) {
     attn_bwd_dvec(p, s);
     {
-        using TK = Tile<HD, 128>;
-        using TQ = Tile<HD, 64>;
-        const int smem = 2 * TK::BYTES + 4 * TQ::BYTES + 4 * 16384 + 4 * 64 * 4 + 256 + 1024;
         BwdMaps m;
-        make_maps<HD>(&m, p, 128, 64);
+        make_tmap_sw(&m.a128, f.k, W, f.Nk, f.k_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+        make_tmap_sw(&m.a32, f.k, W, f.Nk, f.k_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
+        make_tmap_sw(&m.b128, f.v, W, f.Nk, f.v_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+        make_tmap_sw(&m.b32, f.v, W, f.Nk, f.v_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
+        make_tmap_sw(&m.ta, qt, f.Nq, W, qt_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
+        make_tmap_sw(&m.tb, dot, f.Nq, W, dot_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
+        const int smem = 2 * T::ROW_TILE + 4 * T::T_TILE + 4 * 16384 + 4 * 64 * 4 + 256 + 1024;
         static bool set = false;
         if (!set) {
             MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             set = true;
         }
-        attn_bwd_dkv_tc_kernel<HD><<<dim3((p.f.Nk + 127) / 128, p.f.heads), 256, smem, s>>>(m, p); ::mgv::note_launch();
+        attn_bwd_dkv_tc_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads), 256, smem, s>>>(m, p); ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
     }
     {
-        using TQ = Tile<HD, 128>;
-        using TK = Tile<HD, 64>;
-        const int smem = 2 * TQ::BYTES + 4 * TK::BYTES + 2 * 16384 + 256 + 1024;
         BwdMaps m;
-        make_maps<HD>(&m, p, 64, 128);
+        make_tmap_sw(&m.a128, f.q, W, f.Nq, f.q_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+        make_tmap_sw(&m.a32, f.q, W, f.Nq, f.q_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
+        make_tmap_sw(&m.b128, p.dO, W, f.Nq, p.do_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+        make_tmap_sw(&m.b32, p.dO, W, f.Nq, p.do_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
+        make_tmap_sw(&m.ta, kt, f.Nk, W, kt_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
+        make_tmap_sw(&m.tb, vt, f.Nk, W, vt_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
+        const int smem = 2 * T::ROW_TILE + 4 * T::T_TILE + 2 * 16384 + 256 + 1024;
         static bool set = false;
         if (!set) {
             MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             set = true;
         }
-        attn_bwd_dq_tc_kernel<HD><<<dim3((p.f.Nq + 127) / 128, p.f.heads), 256, smem, s>>>(m, p); ::mgv::note_launch();
+        attn_bwd_dq_tc_kernel<HD><<<dim3((f.Nq + 127) / 128, f.heads), 256, smem, s>>>(m, p); ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
     }
 }
 
 void attn_bwd_tc(const AttnBwdProblem& p, cudaStream_t s) {
-    switch (p.f.hd) {
-        case 64: launch_bwd<64>(p, s); break;
-        case 128: launch_bwd<128>(p, s); break;
-        case 144: launch_bwd<144>(p, s); break;
+    const AttnProblem& f = p.f;
+    const int W = f.heads * f.hd;
+    // transposed operands: use the caller's, else make them here
+    std::vector<__nv_bfloat16*> tmp;
+    auto make_t = [&](const void* src, int64_t ld, int rows, int64_t* out_ld) -> const void* {
+        const int64_t l = (rows + 7) / 8 * 8;
+        __nv_bfloat16* d = nullptr;
+        MGV_CUDA(cudaMallocAsync(&d, sizeof(__nv_bfloat16) * l * W, s));
+        transpose_bf16(static_cast<const __nv_bfloat16*>(src), ld, rows, W, d, l, s);
+        tmp.push_back(d);
+        *out_ld = l;
+        return d;
+    };
+    int64_t qt_ld = p.qt_ld, kt_ld = p.kt_ld, vt_ld = f.vt_ld, dot_ld = p.dot_ld;
+    const void* qt = p.qt ? p.qt : make_t(f.q, f.q_ld, f.Nq, &qt_ld);
+    const void* kt = p.kt ? p.kt : make_t(f.k, f.k_ld, f.Nk, &kt_ld);
+    const void* vt = f.vt ? f.vt : make_t(f.v, f.v_ld, f.Nk, &vt_ld);
+    const void* dot = p.dot ? p.dot : make_t(p.dO, p.do_ld, f.Nq, &dot_ld);
+    switch (f.hd) {
+        case 64: launch_bwd<64>(p, qt, qt_ld, kt, kt_ld, vt, vt_ld, dot, dot_ld, s); break;
+        case 128: launch_bwd<128>(p, qt, qt_ld, kt, kt_ld, vt, vt_ld, dot, dot_ld, s); break;
+        case 144: launch_bwd<144>(p, qt, qt_ld, kt, kt_ld, vt, vt_ld, dot, dot_ld, s); break;
         default: throw std::runtime_error("attn_bwd_tc: unsupported head_dim");
     }
+    for (auto* d : tmp) MGV_CUDA(cudaFreeAsync(d, s));
 }
 
 }  // namespace mgv

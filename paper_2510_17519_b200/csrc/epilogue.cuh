@@ -3,6 +3,10 @@
 // (row m, columns n0 .. n0+cnt-1, fp32 accumulators) to one of these, so the
 // bias / activation / gate / residual work of dit.cpp:288-311 is fused into
 // the GEMM that produces the values.
+//
+// The tensor-core epilogue calls them with cnt == 16 and n0 % 16 == 0; a
+// vector path (16-byte loads/stores) is taken whenever the row segment is in
+// range and 16-byte aligned, the scalar path otherwise.
 #pragma once
 #include <cuda_bf16.h>
 #include <cstdint>
@@ -15,7 +19,57 @@ template <> __device__ __forceinline__ __nv_bfloat16 to_t<__nv_bfloat16>(float v
 __device__ __forceinline__ float to_f(float v) { return v; }
 __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
 
-__device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + expf(-x)); }
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + __expf(-x)); }
+
+__device__ __forceinline__ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// 16 contiguous values <-> registers
+template <class T> struct Vec16;
+template <> struct Vec16<float> {
+    __device__ static void load(const float* p, float* v) {
+        const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            float4 x = q[i];
+            v[4 * i] = x.x; v[4 * i + 1] = x.y; v[4 * i + 2] = x.z; v[4 * i + 3] = x.w;
+        }
+    }
+    __device__ static void store(float* p, const float* v) {
+        float4* q = reinterpret_cast<float4*>(p);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) q[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+};
+template <> struct Vec16<__nv_bfloat16> {
+    __device__ static void load(const __nv_bfloat16* p, float* v) {
+        const uint4* q = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            uint4 x = q[i];
+            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&w[j]);
+                float2 f = __bfloat1622float2(b);
+                v[8 * i + 2 * j] = f.x;
+                v[8 * i + 2 * j + 1] = f.y;
+            }
+        }
+    }
+    __device__ static void store(__nv_bfloat16* p, const float* v) {
+        uint4* q = reinterpret_cast<uint4*>(p);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            uint32_t w[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                __nv_bfloat162 b = __floats2bfloat162_rn(v[8 * i + 2 * j], v[8 * i + 2 * j + 1]);
+                w[j] = *reinterpret_cast<uint32_t*>(&b);
+            }
+            q[i] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    }
+};
 
 // out[m, n] = alpha * (acc + bias[n])                     (plain linear + bias)
 template <class T>
@@ -27,10 +81,18 @@ struct EpiStore {
     int M, N;
     __device__ __forceinline__ void operator()(int m, int n0, const float* v, int cnt) const {
         if (m >= M) return;
-        T* o = out + (int64_t)m * ldo;
+        T* o = out + (int64_t)m * ldo + n0;
+        if (cnt == 16 && n0 + 16 <= N && al16(o) && (!bias || al16(bias + n0))) {
+            float r[16], b[16];
+            if (bias) Vec16<float>::load(bias + n0, b);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r[j] = alpha * (v[j] + (bias ? b[j] : 0.0f));
+            Vec16<T>::store(o, r);
+            return;
+        }
         for (int j = 0; j < cnt; ++j) {
             int n = n0 + j;
-            if (n < N) o[n] = to_t<T>(alpha * (v[j] + (bias ? bias[n] : 0.0f)));
+            if (n < N) o[j] = to_t<T>(alpha * (v[j] + (bias ? bias[n] : 0.0f)));
         }
     }
 };
@@ -45,12 +107,24 @@ struct EpiF32 {
     int M, N;
     __device__ __forceinline__ void operator()(int m, int n0, const float* v, int cnt) const {
         if (m >= M) return;
-        float* o = out + (int64_t)m * ldo;
+        float* o = out + (int64_t)m * ldo + n0;
+        if (cnt == 16 && n0 + 16 <= N && al16(o) && (!bias || al16(bias + n0))) {
+            float r[16], b[16], prev[16];
+            if (bias) Vec16<float>::load(bias + n0, b);
+            if (accumulate) Vec16<float>::load(o, prev);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                r[j] = alpha * (v[j] + (bias ? b[j] : 0.0f));
+                if (accumulate) r[j] += prev[j];
+            }
+            Vec16<float>::store(o, r);
+            return;
+        }
         for (int j = 0; j < cnt; ++j) {
             int n = n0 + j;
             if (n < N) {
                 float r = alpha * (v[j] + (bias ? bias[n] : 0.0f));
-                o[n] = accumulate ? o[n] + r : r;
+                o[j] = accumulate ? o[j] + r : r;
             }
         }
     }
@@ -66,18 +140,32 @@ struct EpiBiasSilu {
     int M, N;
     __device__ __forceinline__ void operator()(int m, int n0, const float* v, int cnt) const {
         if (m >= M) return;
+        T* zo = z + (int64_t)m * ld + n0;
+        T* ho = h + (int64_t)m * ld + n0;
+        if (cnt == 16 && n0 + 16 <= N && al16(zo) && al16(ho) && al16(bias + n0)) {
+            float b[16], zz[16], hh[16];
+            Vec16<float>::load(bias + n0, b);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                zz[j] = v[j] + b[j];
+                hh[j] = zz[j] * sigmoidf_(zz[j]);
+            }
+            Vec16<T>::store(zo, zz);
+            Vec16<T>::store(ho, hh);
+            return;
+        }
         for (int j = 0; j < cnt; ++j) {
             int n = n0 + j;
             if (n < N) {
                 float zz = v[j] + bias[n];
-                z[(int64_t)m * ld + n] = to_t<T>(zz);
-                h[(int64_t)m * ld + n] = to_t<T>(zz * sigmoidf_(zz));
+                zo[j] = to_t<T>(zz);
+                ho[j] = to_t<T>(zz * sigmoidf_(zz));
             }
         }
     }
 };
 
-// y = acc + b ; X += y * gate[mod_id[m], n]   (dit.cpp:295-297, 310-311)
+// y = acc + b ; X = Xin + y * gate[mod_id[m], n]   (dit.cpp:295-297, 310-311)
 // y is kept (bf16/fp32) for the gate gradient of the backward pass.
 template <class T>
 struct EpiGateResid {
@@ -93,15 +181,30 @@ struct EpiGateResid {
     int M, N;
     __device__ __forceinline__ void operator()(int m, int n0, const float* v, int cnt) const {
         if (m >= M) return;
-        const float* g = gate + (int64_t)mod_id[m] * gate_ld;
-        float* x = X + (int64_t)m * ldx;
-        const float* xi = Xin + (int64_t)m * ldx;
+        const float* g = gate + (int64_t)mod_id[m] * gate_ld + n0;
+        float* x = X + (int64_t)m * ldx + n0;
+        const float* xi = Xin + (int64_t)m * ldx + n0;
+        T* yo = y ? y + (int64_t)m * ldy + n0 : nullptr;
+        if (cnt == 16 && n0 + 16 <= N && al16(x) && al16(xi) && al16(g) && al16(bias + n0) && (!yo || al16(yo))) {
+            float b[16], gg[16], xx[16], yy[16];
+            Vec16<float>::load(bias + n0, b);
+            Vec16<float>::load(g, gg);
+            Vec16<float>::load(xi, xx);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                yy[j] = v[j] + b[j];
+                xx[j] = xx[j] + yy[j] * gg[j];
+            }
+            if (yo) Vec16<T>::store(yo, yy);
+            Vec16<float>::store(x, xx);
+            return;
+        }
         for (int j = 0; j < cnt; ++j) {
             int n = n0 + j;
             if (n < N) {
                 float yy = v[j] + bias[n];
-                if (y) y[(int64_t)m * ldy + n] = to_t<T>(yy);
-                x[n] = xi[n] + yy * g[n];
+                if (yo) yo[j] = to_t<T>(yy);
+                x[j] = xi[j] + yy * g[j];
             }
         }
     }
@@ -116,12 +219,25 @@ struct EpiSiluBwd {
     int M, N;
     __device__ __forceinline__ void operator()(int m, int n0, const float* v, int cnt) const {
         if (m >= M) return;
+        T* o = out + (int64_t)m * ld + n0;
+        const T* zi = z + (int64_t)m * ld + n0;
+        if (cnt == 16 && n0 + 16 <= N && al16(o) && al16(zi)) {
+            float zz[16], r[16];
+            Vec16<T>::load(zi, zz);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const float s = sigmoidf_(zz[j]);
+                r[j] = v[j] * (s + zz[j] * s * (1.0f - s));
+            }
+            Vec16<T>::store(o, r);
+            return;
+        }
         for (int j = 0; j < cnt; ++j) {
             int n = n0 + j;
             if (n < N) {
-                float zz = to_f(z[(int64_t)m * ld + n]);
+                float zz = to_f(zi[j]);
                 float s = sigmoidf_(zz);
-                out[(int64_t)m * ld + n] = to_t<T>(v[j] * (s + zz * s * (1.0f - s)));
+                o[j] = to_t<T>(v[j] * (s + zz * s * (1.0f - s)));
             }
         }
     }

@@ -900,3 +900,53 @@ INST(__nv_bfloat16)
 #undef INST
 
 }  // namespace mgv
+
+namespace mgv {
+// 64 x 64 tiles through shared memory: coalesced 16-byte reads along columns and writes along rows.
+__global__ void __launch_bounds__(256) transpose_bf16_kernel(const __nv_bfloat16* __restrict__ in, int64_t ld_in,
+                                                             int rows, int cols, __nv_bfloat16* __restrict__ out,
+                                                             int64_t ld_out) {
+    __shared__ __nv_bfloat16 t[64][66];
+    const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+    const int tx = threadIdx.x % 8, ty = threadIdx.x / 8;  // 8 x 32
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int r = ty + 32 * k;
+        const int gr = r0 + r, gc = c0 + tx * 8;
+        __nv_bfloat16 v[8];
+        if (gr < rows && gc + 8 <= cols && (((uintptr_t)(in + (int64_t)gr * ld_in + gc)) & 15) == 0) {
+            *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(in + (int64_t)gr * ld_in + gc);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                v[e] = (gr < rows && gc + e < cols) ? in[(int64_t)gr * ld_in + gc + e] : __float2bfloat16_rn(0.0f);
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) t[r][tx * 8 + e] = v[e];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int c = ty + 32 * k;  // output row = input column
+        const int gc = c0 + c, gr = r0 + tx * 8;
+        if (gc >= cols) continue;
+        __nv_bfloat16 v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = t[tx * 8 + e][c];
+        __nv_bfloat16* dst = out + (int64_t)gc * ld_out + gr;
+        if (gr + 8 <= rows && (((uintptr_t)dst) & 15) == 0) {
+            *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<uint4*>(v);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (gr + e < rows) dst[e] = v[e];
+        }
+    }
+}
+void transpose_bf16(const __nv_bfloat16* in, int64_t ld_in, int rows, int cols, __nv_bfloat16* out, int64_t ld_out,
+                    cudaStream_t s) {
+    dim3 grid((cols + 63) / 64, (rows + 63) / 64);
+    transpose_bf16_kernel<<<grid, 256, 0, s>>>(in, ld_in, rows, cols, out, ld_out); ::mgv::note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
+}  // namespace mgv

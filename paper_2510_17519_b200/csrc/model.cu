@@ -244,6 +244,11 @@ static void set_taus(double* taus, double t, cudaStream_t s) {
 // ------------------------------------------------------------------ model
 Model::Model(int device, bool bf16) : device_(device), bf16_(bf16) {
     MGV_CUDA(cudaSetDevice(device));
+    // keep stream-ordered scratch (attention operand transposes) cached across steps
+    cudaMemPool_t pool;
+    MGV_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    MGV_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     ws_ = new WS();
 }
 

@@ -53,3 +53,17 @@ for tc in [1]:
     ms = timeit(f, 3)
     fl = 4.0 * N * N * H
     print(f"attn fwd tc={tc} N={N}: {ms:8.3f} ms  {fl / ms / 1e9:7.1f} TFLOP/s")
+
+# attention backward (self) at the same shape
+dO = torch.randn(N, H, device=dev).bfloat16()
+Dv = torch.empty(heads, N, device=dev)
+dqkv = torch.empty(N, 3 * H, device=dev).bfloat16()
+i64 = ctypes.c_int64
+fb = lambda: L.mgv_dev_attn_bwd(1, P(qkv.data_ptr()), i64(3 * H), P(qkv[:, H:].data_ptr()), i64(3 * H),
+                                P(qkv[:, 2 * H:].data_ptr()), i64(3 * H), P(o.data_ptr()), i64(H), P(lse.data_ptr()),
+                                P(dO.data_ptr()), i64(H), P(Dv.data_ptr()), P(dqkv.data_ptr()), i64(3 * H),
+                                P(dqkv[:, H:].data_ptr()), i64(3 * H), P(dqkv[:, 2 * H:].data_ptr()), i64(3 * H),
+                                P(0), 1, N, N, heads, hd, P(stream))
+ms = timeit(fb, 2)
+fl = 8.0 * N * N * H
+print(f"attn bwd tc N={N}: {ms:8.3f} ms  {fl / ms / 1e9:7.1f} TFLOP/s (algorithmic 8N^2H)")
