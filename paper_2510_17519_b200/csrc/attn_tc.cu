@@ -1,26 +1,24 @@
 // tcgen05 flash attention forward for sm_100a (bf16 operands, fp32 softmax and
 // accumulation) -- Tape::mha forward (autodiff.cpp:755-793) at head_dim 144.
 //
-// One CTA per (128-query tile, head):
-//   warp 0      TMA producer: Q once, then K and V^T tiles (128 keys) through a
-//               2-stage ring
-//   warp 1      MMA issuer: S_j = Q K_j^T into TMEM buffer j%2, then
-//               O += P_{j-1} V_{j-1} with P read straight from TMEM (the TS form)
-//   warp 2      TMEM allocator: columns [0,128) S/P 0, [128,256) S/P 1, [256,256+hd) O
-//   warps 4..7  softmax, thread i = query row i = TMEM lane i: tcgen05.ld S ->
-//               online softmax in the log2 domain (ex2.approx) -> bf16 P written
-//               back over S with tcgen05.st -> signal.  O is rescaled in TMEM only
-//               when the running max grows by more than 2^8 (stale-max trick); the
-//               epilogue normalises O and writes lse.
-//
-// P lives in TMEM in the buffer its S came from, so softmax(j+1) never waits for
-// the P.V product of step j (only a rare O rescale does); the tensor core runs
-// S_{j+1} and PV_j back to back while the softmax warps work.
+// One CTA per (256 queries = two 128-row tiles A and B, head), 12 warps:
+//   warp 0        TMA producer: Q_A, Q_B once; then 112-key K tiles and V^T tiles
+//                 through a 2-stage ring (each K/V byte now serves 256 queries)
+//   warp 1        MMA issuer, ping-pong between the tiles:
+//                   S_A(j), PV_B(j-1), S_B(j), PV_A(j), S_A(j+1), ...
+//                 so the tensor core works on one tile while the other tile's
+//                 softmax runs.  P is read straight from TMEM (TS form).
+//   warp 2        TMEM allocator: S/P_A [0,112) S/P_B [112,224) O_A [224,368) O_B [368,512)
+//   warps 4..7    softmax of tile A  } thread i = query row i = TMEM lane i:
+//   warps 8..11   softmax of tile B  } tcgen05.ld S -> online softmax (log2 domain,
+//                 ex2.approx) -> bf16 P over S (tcgen05.st) -> signal.  O is rescaled
+//                 in TMEM only when the running max grows by more than 2^8.
+// Registers are rebalanced with setmaxnreg (producer group 56, softmax groups 224).
 //
 // head_dim 144 = 64 + 64 + 16: Q and K tiles are 64-column SW128 chunks plus a
-// 16-column SW32 tail (S = Q K^T walks 9 K-steps across them); V is consumed
-// transposed (V^T tile = hd rows x 128 keys, K-major) so O += P V is ONE
-// N = 144 MMA per 16-key step.
+// 16-column SW32 tail (S = Q K^T = 9 K-steps, N = 112); V is consumed transposed
+// (V^T tile = 144 rows x 128 keys, K-major) so O += P V is one N = 144 MMA per
+// 16-key step (7 steps per 112-key tile).
 #include <cfloat>
 
 #include "attn.h"
@@ -32,8 +30,8 @@ namespace mgv {
 
 namespace {
 
-constexpr int BM = 128;  // queries per CTA
-constexpr int BN = 128;  // keys per tile
+constexpr int BM = 128;  // queries per tile (two tiles per CTA)
+constexpr int BN = 112;  // keys per step (TMEM: 2 x (112 + 144) = 512 columns)
 constexpr float kLog2e = 1.4426950408889634f;
 
 template <int HD>
@@ -41,12 +39,17 @@ struct FwdCfg {
     static constexpr int NF = HD / 64;
     static constexpr int TAIL = HD % 64;
     static_assert(TAIL == 0 || TAIL == 16, "head_dim must be 64k or 64k+16");
-    static constexpr int QK_TILE = NF * 16384 + (TAIL ? 4096 : 0);  // 128 rows x HD (K-major over hd)
-    static constexpr int VT_CHUNK = HD * 128;                        // HD rows x 64 keys (SW128)
-    static constexpr int VT_TILE = 2 * VT_CHUNK;                     // HD rows x 128 keys
-    static constexpr int STAGE = QK_TILE + VT_TILE;
-    static constexpr int SMEM = QK_TILE + 2 * STAGE + 1024 + 256;
-    static constexpr int O_COL = 256;
+    static constexpr int Q_TILE = NF * 16384 + (TAIL ? 4096 : 0);    // 128 rows x HD
+    static constexpr int K_CHUNK = BN * 128;                          // 112 rows x 64 cols (SW128)
+    static constexpr int K_BYTES = NF * K_CHUNK + (TAIL ? BN * 32 : 0);  // TMA transaction bytes
+    static constexpr int K_TILE = (K_BYTES + 1023) / 1024 * 1024;        // smem footprint (1 KB aligned)
+    static constexpr int VT_CHUNK = HD * 128;                         // HD rows x 64 keys (SW128)
+    static constexpr int VT_TILE = 2 * VT_CHUNK;                      // HD rows x 128 keys (112 used)
+    static constexpr int STAGE = K_TILE + VT_TILE;
+    static constexpr int SMEM = 2 * Q_TILE + 2 * STAGE + 1024 + 256;
+    __host__ __device__ static constexpr int s_col(int t) { return t * BN; }
+    __host__ __device__ static constexpr int o_col(int t) { return 2 * BN + t * HD; }
+    static_assert(2 * BN + 2 * HD <= 512, "TMEM budget");
 };
 
 struct FwdMaps {
@@ -59,46 +62,36 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
-        "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
-        "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
-}
-
-template <int HD>
-__device__ __forceinline__ void load_qk_tile(uint8_t* dst, const CUtensorMap* m128, const CUtensorMap* m32,
-                                             uint64_t* bar, int col0, int row0) {
+template <int HD, int ROWS>
+__device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* m128, const CUtensorMap* m32,
+                                          uint64_t* bar, int col0, int row0) {
     using C = FwdCfg<HD>;
 #pragma unroll
-    for (int c = 0; c < C::NF; ++c) tma_load_2d(dst + c * 16384, m128, bar, col0 + c * 64, row0);
-    if (C::TAIL) tma_load_2d(dst + C::NF * 16384, m32, bar, col0 + C::NF * 64, row0);
+    for (int c = 0; c < C::NF; ++c) tma_load_2d(dst + c * ROWS * 128, m128, bar, col0 + c * 64, row0);
+    if (C::TAIL) tma_load_2d(dst + C::NF * ROWS * 128, m32, bar, col0 + C::NF * 64, row0);
 }
 
 }  // namespace
 
 template <int HD>
-__global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_constant__ FwdMaps tm, AttnProblem p) {
+__global__ void __launch_bounds__(384, 1) attn_fwd_tc_kernel(const __grid_constant__ FwdMaps tm, AttnProblem p) {
     using C = FwdCfg<HD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;
-    uint8_t* sStage = sQ + C::QK_TILE;  // [2] x (K tile | V^T tile)
+    uint8_t* sQ = smem;                      // [2] tiles
+    uint8_t* sStage = sQ + 2 * C::Q_TILE;    // [2] x (K tile | V^T tile)
     uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + 2 * C::STAGE);
-    uint64_t* q_full = bars;
-    uint64_t* k_full = bars + 1;    // [2]
-    uint64_t* v_full = bars + 3;    // [2]
-    uint64_t* kv_empty = bars + 5;  // [2]
-    uint64_t* s_full = bars + 7;    // [2]
-    uint64_t* p_full = bars + 9;    // [2]
-    uint64_t* pv_done = bars + 11;
+    uint64_t* q_full = bars;         // both Q tiles
+    uint64_t* k_full = bars + 1;     // [2]
+    uint64_t* v_full = bars + 3;     // [2]
+    uint64_t* kv_empty = bars + 5;   // [2]
+    uint64_t* s_full = bars + 7;     // [tile]
+    uint64_t* p_full = bars + 9;     // [tile]
+    uint64_t* pv_done = bars + 11;   // [tile]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int h = blockIdx.y, q0 = blockIdx.x * BM;
+    const int h = blockIdx.y, q0 = blockIdx.x * 2 * BM;
     const int nkv = (p.Nk + BN - 1) / BN;
     const int col = h * HD;
 
@@ -110,8 +103,8 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_consta
             mbar_init(&kv_empty[i], 1);
             mbar_init(&s_full[i], 1);
             mbar_init(&p_full[i], 4);
+            mbar_init(&pv_done[i], 1);
         }
-        mbar_init(pv_done, 1);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -120,86 +113,103 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_consta
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) {
-        if (elect_one()) {
-            tma_prefetch(&tm.q128);
-            tma_prefetch(&tm.k128);
-            tma_prefetch(&tm.vt);
-            mbar_arrive_expect_tx(q_full, C::QK_TILE);
-            load_qk_tile<HD>(sQ, &tm.q128, &tm.q32, q_full, col, q0);
-            for (int j = 0; j < nkv; ++j) {
-                const int st = j & 1;
-                if (j >= 2) mbar_wait(&kv_empty[st], ((j - 2) >> 1) & 1);
-                uint8_t* sK = sStage + st * C::STAGE;
-                uint8_t* sVt = sK + C::QK_TILE;
-                mbar_arrive_expect_tx(&k_full[st], C::QK_TILE);
-                load_qk_tile<HD>(sK, &tm.k128, &tm.k32, &k_full[st], col, j * BN);
-                mbar_arrive_expect_tx(&v_full[st], C::VT_TILE);
-                tma_load_2d(sVt, &tm.vt, &v_full[st], j * BN, col);
-                tma_load_2d(sVt + C::VT_CHUNK, &tm.vt, &v_full[st], j * BN + 64, col);
+    if (warp < 4) {
+        setmaxnreg_dec<56>();
+        if (warp == 0) {
+            if (elect_one()) {
+                tma_prefetch(&tm.q128);
+                tma_prefetch(&tm.k128);
+                tma_prefetch(&tm.vt);
+                mbar_arrive_expect_tx(q_full, 2 * C::Q_TILE);
+                load_rows<HD, BM>(sQ, &tm.q128, &tm.q32, q_full, col, q0);
+                load_rows<HD, BM>(sQ + C::Q_TILE, &tm.q128, &tm.q32, q_full, col, q0 + BM);
+                for (int j = 0; j < nkv; ++j) {
+                    const int st = j & 1;
+                    if (j >= 2) mbar_wait(&kv_empty[st], ((j - 2) >> 1) & 1);
+                    uint8_t* sK = sStage + st * C::STAGE;
+                    uint8_t* sVt = sK + C::K_TILE;
+                    mbar_arrive_expect_tx(&k_full[st], C::K_BYTES);
+                    load_rows<HD, BN>(sK, &tm.k128, &tm.k32, &k_full[st], col, j * BN);
+                    mbar_arrive_expect_tx(&v_full[st], C::VT_TILE);
+                    tma_load_2d(sVt, &tm.vt, &v_full[st], j * BN, col);
+                    tma_load_2d(sVt + C::VT_CHUNK, &tm.vt, &v_full[st], j * BN + 64, col);
+                }
+            }
+        } else if (warp == 1) {
+            constexpr uint32_t idS = idesc_bf16_f32(BM, BN, false, false);
+            constexpr uint32_t idO = idesc_bf16_f32(BM, HD, false, false);
+            auto issue_s = [&](int t, int j) {
+                const uint32_t aQ = smem_u32(sQ + t * C::Q_TILE);
+                const uint32_t aK = smem_u32(sStage + (j & 1) * C::STAGE);
+                const uint32_t d = tmem + C::s_col(t);
+                int kk = 0;
+#pragma unroll
+                for (int c = 0; c < C::NF; ++c)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k, ++kk)
+                        umma_f16_ss(d, smem_desc(aQ + c * 16384 + k * 32, 16, 1024, kSwizzle128),
+                                    smem_desc(aK + c * C::K_CHUNK + k * 32, 16, 1024, kSwizzle128), idS, kk > 0);
+                if (C::TAIL)
+                    umma_f16_ss(d, smem_desc(aQ + C::NF * 16384, 16, 256, kSwizzle32),
+                                smem_desc(aK + C::NF * C::K_CHUNK, 16, 256, kSwizzle32), idS, 1);
+                umma_commit(&s_full[t]);
+            };
+            auto issue_pv = [&](int t, int j) {
+                const uint32_t aVt = smem_u32(sStage + (j & 1) * C::STAGE + C::K_TILE);
+                const uint32_t pt = tmem + C::s_col(t);  // bf16 P packed 2 per column over S
+#pragma unroll
+                for (int ks = 0; ks < BN / 16; ++ks)
+                    umma_f16_ts(tmem + C::o_col(t), pt + ks * 8,
+                                smem_desc(aVt + (ks >> 2) * C::VT_CHUNK + (ks & 3) * 32, 16, 1024, kSwizzle128), idO,
+                                (j > 0 || ks > 0) ? 1u : 0u);
+                umma_commit(&pv_done[t]);
+            };
+            mbar_wait(q_full, 0);
+            for (int j = 0; j <= nkv; ++j) {
+                if (j < nkv) {
+                    mbar_wait(&k_full[j & 1], (j >> 1) & 1);
+                    tc_fence_after();
+                    if (elect_one()) issue_s(0, j);  // S_A(j): P_A(j-1) consumed by PV_A(j-1), issued earlier
+                    __syncwarp();
+                }
+                if (j >= 1) {  // PV_B(j-1), then the stage of step j-1 is free
+                    mbar_wait(&p_full[1], (j - 1) & 1);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        issue_pv(1, j - 1);
+                        umma_commit(&kv_empty[(j - 1) & 1]);
+                    }
+                    __syncwarp();
+                }
+                if (j < nkv) {
+                    if (elect_one()) issue_s(1, j);  // S_B(j)
+                    __syncwarp();
+                    mbar_wait(&p_full[0], j & 1);
+                    mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+                    tc_fence_after();
+                    if (elect_one()) issue_pv(0, j);  // PV_A(j)
+                    __syncwarp();
+                }
             }
         }
-    } else if (warp == 1) {
-        constexpr uint32_t idS = idesc_bf16_f32(BM, BN, false, false);
-        constexpr uint32_t idO = idesc_bf16_f32(BM, HD, false, false);
-        const uint32_t aQ = smem_u32(sQ);
-        mbar_wait(q_full, 0);
-        for (int j = 0; j <= nkv; ++j) {
-            if (j < nkv) {
-                const int st = j & 1;
-                const uint32_t aK = smem_u32(sStage + st * C::STAGE);
-                mbar_wait(&k_full[st], (j >> 1) & 1);
-                tc_fence_after();
-                if (elect_one()) {
-                    // S_j -> TMEM buffer j%2 (P_{j-2} there was consumed by PV_{j-2}, issued earlier)
-                    const uint32_t d = tmem + st * BN;
-                    int kk = 0;
-#pragma unroll
-                    for (int c = 0; c < C::NF; ++c)
-#pragma unroll
-                        for (int k = 0; k < 4; ++k, ++kk)
-                            umma_f16_ss(d, smem_desc(aQ + c * 16384 + k * 32, 16, 1024, kSwizzle128),
-                                        smem_desc(aK + c * 16384 + k * 32, 16, 1024, kSwizzle128), idS, kk > 0);
-                    if (C::TAIL)
-                        umma_f16_ss(d, smem_desc(aQ + C::NF * 16384, 16, 256, kSwizzle32),
-                                    smem_desc(aK + C::NF * 16384, 16, 256, kSwizzle32), idS, 1);
-                    umma_commit(&s_full[st]);
-                }
-                __syncwarp();
-            }
-            if (j >= 1) {
-                const int jp = j - 1, sp = jp & 1;
-                mbar_wait(&p_full[sp], (jp >> 1) & 1);
-                mbar_wait(&v_full[sp], (jp >> 1) & 1);
-                tc_fence_after();
-                if (elect_one()) {
-                    const uint32_t aVt = smem_u32(sStage + sp * C::STAGE + C::QK_TILE);
-                    const uint32_t pt = tmem + sp * BN;  // bf16 P packed 2 per column
-#pragma unroll
-                    for (int ks = 0; ks < BN / 16; ++ks)
-                        umma_f16_ts(tmem + C::O_COL, pt + ks * 8,
-                                    smem_desc(aVt + (ks >> 2) * C::VT_CHUNK + (ks & 3) * 32, 16, 1024, kSwizzle128),
-                                    idO, (jp > 0 || ks > 0) ? 1u : 0u);
-                    umma_commit(pv_done);
-                    umma_commit(&kv_empty[sp]);
-                }
-                __syncwarp();
-            }
-        }
-    } else if (warp >= 4) {
-        const int wq = warp - 4;
+    } else {
+        // ------------------------------------------------ softmax, tile t = 0 (warps 4-7) or 1 (8-11)
+        setmaxnreg_inc<224>();
+        const int t = (warp - 4) >> 2, wq = warp & 3;
         const int row = wq * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
+        const uint32_t sS = tmem + lane_base + C::s_col(t);
+        const uint32_t sO = tmem + lane_base + C::o_col(t);
         float m2 = -FLT_MAX;  // running max (log2 domain)
         float l = 0.0f;
         for (int j = 0; j < nkv; ++j) {
-            const int sb = j & 1;
-            mbar_wait(&s_full[sb], (j >> 1) & 1);
+            mbar_wait(&s_full[t], j & 1);
             tc_fence_after();
             float s[BN];
-#pragma unroll
-            for (int c = 0; c < BN / 32; ++c)
-                tmem_ld32(tmem + lane_base + sb * BN + c * 32, reinterpret_cast<uint32_t*>(s + c * 32));
+            tmem_ld32(sS + 0, reinterpret_cast<uint32_t*>(s));
+            tmem_ld32(sS + 32, reinterpret_cast<uint32_t*>(s + 32));
+            tmem_ld32(sS + 64, reinterpret_cast<uint32_t*>(s + 64));
+            tmem_ld16(sS + 96, reinterpret_cast<uint32_t*>(s + 96));
             tmem_wait_ld();
             const int kv0 = j * BN;
             if (kv0 + BN > p.Nk) {
@@ -207,7 +217,6 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_consta
                 for (int c = 0; c < BN; ++c)
                     if (kv0 + c >= p.Nk) s[c] = -FLT_MAX;
             }
-            // row max over raw logits with 8 independent chains (short dependency depth)
             float mx8[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) mx8[e] = s[e];
@@ -224,7 +233,6 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_consta
                 m_use = mx;
                 alpha = ex2(m2 - mx);
             }
-            // p = 2^(s*log2e - m): one FFMA + one MUFU per element; 8 independent partial sums
             float ps8[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) ps8[e] = 0.0f;
@@ -237,41 +245,39 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_consta
             }
             const float ps = ((ps8[0] + ps8[1]) + (ps8[2] + ps8[3])) + ((ps8[4] + ps8[5]) + (ps8[6] + ps8[7]));
             if (j >= 1 && __any_sync(0xffffffff, alpha != 1.0f)) {
-                // O must hold exactly PV_0..PV_{j-1} before it is rescaled
-                mbar_wait(pv_done, (j - 1) & 1);
+                mbar_wait(&pv_done[t], (j - 1) & 1);  // O holds exactly PV(0..j-1)
                 tc_fence_after();
-                const uint32_t ob = tmem + lane_base + C::O_COL;
 #pragma unroll 1
                 for (int c = 0; c < HD / 16; ++c) {
                     uint32_t r[16];
-                    tmem_ld16(ob + c * 16, r);
+                    tmem_ld16(sO + c * 16, r);
                     tmem_wait_ld();
 #pragma unroll
                     for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-                    tmem_st16(ob + c * 16, r);
+                    tmem_st16(sO + c * 16, r);
                 }
             }
             l = l * alpha + ps;
             m2 = m_use;
-            // P (bf16) over S in the same TMEM buffer: 64 packed columns
-            tmem_st32(tmem + lane_base + sb * BN, pk);
-            tmem_st32(tmem + lane_base + sb * BN + 32, pk + 32);
+            tmem_st32(sS + 0, pk);  // 56 packed columns over S
+            tmem_st16(sS + 32, pk + 32);
+            tmem_st8(sS + 48, pk + 48);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full[sb]);
+            if (lane == 0) mbar_arrive(&p_full[t]);
         }
         if (nkv > 0) {
-            mbar_wait(pv_done, (nkv - 1) & 1);
+            mbar_wait(&pv_done[t], (nkv - 1) & 1);
             tc_fence_after();
         }
-        const int q = q0 + row;
+        const int q = q0 + t * BM + row;
         const float inv = l > 0.0f ? 1.0f / l : 0.0f;
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.o) + (int64_t)q * p.o_ld + col;
 #pragma unroll 1
         for (int c = 0; c < HD / 16; ++c) {
             uint32_t r[16];
-            tmem_ld16(tmem + lane_base + C::O_COL + c * 16, r);
+            tmem_ld16(sO + c * 16, r);
             tmem_wait_ld();
             if (q < p.Nq) {
                 uint32_t o[8];
@@ -313,8 +319,8 @@ static void launch_fwd(const AttnProblem& p, const void* vt, int64_t vt_ld, cuda
         MGV_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         set = true;
     }
-    dim3 grid((p.Nq + BM - 1) / BM, p.heads);
-    attn_fwd_tc_kernel<HD><<<grid, 256, C::SMEM, s>>>(tm, p); ::mgv::note_launch();
+    dim3 grid((p.Nq + 2 * BM - 1) / (2 * BM), p.heads);
+    attn_fwd_tc_kernel<HD><<<grid, 384, C::SMEM, s>>>(tm, p); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
