@@ -79,6 +79,17 @@ __device__ __forceinline__ void mma_chunk_x_t(uint32_t d, uint32_t a, uint32_t b
                     id, (acc_first || ks > 0) ? 1u : 0u);
 }
 
+// D[128 x HD] (+)= A[128 x 64] . B with A read from TMEM (bf16 packed 2 per column, 32 columns)
+// and B the HD x 64 transposed tile read K-major: one N = HD MMA per 16-token step (TS form).
+template <int HD>
+__device__ __forceinline__ void mma_tmem_x_t(uint32_t d, uint32_t a_tmem, uint32_t bt, bool acc_first) {
+    constexpr uint32_t id = idesc_bf16_f32(128, HD, false, false);
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks)
+        umma_f16_ts(d, a_tmem + ks * 8, smem_desc(bt + ks * 32, 16, 1024, kSwizzle128), id,
+                    (acc_first || ks > 0) ? 1u : 0u);
+}
+
 // thread row -> 64 bf16 values of a 128 x 64 SW128 K-major chunk
 __device__ __forceinline__ void st_row64(uint8_t* chunk, int row, const uint32_t* pk) {
     const uint32_t base = smem_u32(chunk) + row * 128;
@@ -114,32 +125,32 @@ struct BwdMaps {
 }  // namespace
 
 // =====================================================================================  dK / dV
+// TMEM: S^T [0,64) dP^T [64,128) P^T [128,160) dS^T [160,192) dV [192,192+HD) dK [DK,DK+HD)
 template <int HD>
 __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_constant__ BwdMaps tm, AttnBwdProblem p) {
-    constexpr int BKV = 128, BQ = 64;
+    constexpr int BKV = 128, BQ = 64, NST = 4;
     using T = BT<HD>;
-    constexpr int DV_COL = 128, DK_COL = HD <= 128 ? 256 : 320;
+    constexpr int P_COL = 128, DS_COL = 160, DV_COL = 192, DK_COL = 192 + ((HD + 15) / 16) * 16;
+    static_assert(DK_COL + HD <= 512, "TMEM budget");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sK = smem;
     uint8_t* sV = sK + T::ROW_TILE;
-    uint8_t* sQt = sV + T::ROW_TILE;      // [2]
-    uint8_t* sdOt = sQt + 2 * T::T_TILE;  // [2]
-    uint8_t* sPT = sdOt + 2 * T::T_TILE;  // [2] x 16 KB
-    uint8_t* sdST = sPT + 2 * 16384;      // [2] x 16 KB
-    float* sLse = reinterpret_cast<float*>(sdST + 2 * 16384);  // [2][64] (log2 domain)
-    float* sD = sLse + 2 * BQ;                                  // [2][64]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * BQ);
+    uint8_t* sQt = sV + T::ROW_TILE;        // [NST]
+    uint8_t* sdOt = sQt + NST * T::T_TILE;  // [NST]
+    float* sLse = reinterpret_cast<float*>(sdOt + NST * T::T_TILE);  // [NST][64] (log2 domain)
+    float* sD = sLse + NST * BQ;                                      // [NST][64]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sD + NST * BQ);
     uint64_t* kv_full = bars;
-    uint64_t* qd_full = bars + 1;   // [2]
-    uint64_t* qd_empty = bars + 3;  // [2]
-    uint64_t* lse_full = bars + 5;  // [2]
-    uint64_t* s_full = bars + 7;
-    uint64_t* s_empty = bars + 8;
-    uint64_t* p_full = bars + 9;
-    uint64_t* pd_done = bars + 10;  // [2]
-    uint64_t* acc_done = bars + 12;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+    uint64_t* qd_full = bars + 1;         // [NST]
+    uint64_t* qd_empty = bars + 1 + NST;  // [NST]
+    uint64_t* lse_full = bars + 1 + 2 * NST;  // [NST]
+    uint64_t* s_full = bars + 1 + 3 * NST;
+    uint64_t* s_empty = s_full + 1;
+    uint64_t* p_full = s_full + 2;
+    uint64_t* pd_done = s_full + 3;
+    uint64_t* acc_done = s_full + 4;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 6);
 
     const AttnProblem& f = p.f;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -149,15 +160,15 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
 
     if (threadIdx.x == 0) {
         mbar_init(kv_full, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NST; ++i) {
             mbar_init(&qd_full[i], 1);
             mbar_init(&qd_empty[i], 1);
             mbar_init(&lse_full[i], 32);
-            mbar_init(&pd_done[i], 1);
         }
         mbar_init(s_full, 1);
         mbar_init(s_empty, 4);
         mbar_init(p_full, 4);
+        mbar_init(pd_done, 1);
         mbar_init(acc_done, 1);
         fence_barrier_init();
     }
@@ -174,8 +185,8 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
             load_row_tile<HD>(sV, &tm.b128, &tm.b32, kv_full, col, k0);
         }
         for (int i = 0; i < nq; ++i) {
-            const int st = i & 1;
-            if (i >= 2) mbar_wait(&qd_empty[st], ((i - 2) >> 1) & 1);
+            const int st = i % NST;
+            if (i >= NST) mbar_wait(&qd_empty[st], ((i / NST) - 1) & 1);
             if (lane == 0) {
                 mbar_arrive_expect_tx(&qd_full[st], 2 * T::T_TILE);
                 tma_load_2d(sQt + st * T::T_TILE, &tm.ta, &qd_full[st], i * BQ, col);
@@ -192,7 +203,7 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
         const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
         mbar_wait(kv_full, 0);
         auto issue_s = [&](int i) {
-            const int st = i & 1;
+            const int st = i % NST;
             mma_rows_x_t<HD>(tmem + 0, aK, smem_u32(sQt + st * T::T_TILE));
             mma_rows_x_t<HD>(tmem + 64, aV, smem_u32(sdOt + st * T::T_TILE));
         };
@@ -206,10 +217,10 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
             __syncwarp();
         }
         for (int i = 0; i < nq; ++i) {
-            const int st = i & 1;
+            const int st = i % NST;
             if (i + 1 < nq) {
-                mbar_wait(&qd_full[(i + 1) & 1], ((i + 1) >> 1) & 1);
-                mbar_wait(s_empty, i & 1);  // softmax(i) has read S^T_i / dP^T_i
+                mbar_wait(&qd_full[(i + 1) % NST], ((i + 1) / NST) & 1);
+                mbar_wait(s_empty, i & 1);  // elementwise(i) has read S^T_i / dP^T_i
                 tc_fence_after();
                 if (elect_one()) {
                     issue_s(i + 1);
@@ -220,9 +231,9 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
             mbar_wait(p_full, i & 1);
             tc_fence_after();
             if (elect_one()) {
-                mma_chunk_x_t<HD>(tmem + DV_COL, smem_u32(sPT + st * 16384), smem_u32(sdOt + st * T::T_TILE), i > 0);
-                mma_chunk_x_t<HD>(tmem + DK_COL, smem_u32(sdST + st * 16384), smem_u32(sQt + st * T::T_TILE), i > 0);
-                umma_commit(&pd_done[st]);
+                mma_tmem_x_t<HD>(tmem + DV_COL, tmem + P_COL, smem_u32(sdOt + st * T::T_TILE), i > 0);
+                mma_tmem_x_t<HD>(tmem + DK_COL, tmem + DS_COL, smem_u32(sQt + st * T::T_TILE), i > 0);
+                umma_commit(pd_done);
                 umma_commit(&qd_empty[st]);
                 if (i == nq - 1) umma_commit(acc_done);
             }
@@ -232,8 +243,8 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
         const int wq = warp - 4, row = wq * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
         for (int i = 0; i < nq; ++i) {
-            const int st = i & 1;
-            mbar_wait(&lse_full[st], (i >> 1) & 1);
+            const int st = i % NST;
+            mbar_wait(&lse_full[st], (i / NST) & 1);
             mbar_wait(s_full, i & 1);
             tc_fence_after();
             float s[BQ], dp[BQ];
@@ -257,10 +268,13 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
                 pk[c / 2] = pack_bf16(p0, p1);
                 dk[c / 2] = pack_bf16(p0 * (dp[c] - Dq[c]), p1 * (dp[c + 1] - Dq[c + 1]));  // autodiff.cpp:820
             }
-            if (i >= 2) mbar_wait(&pd_done[st], ((i - 2) >> 1) & 1);
-            st_row64(sPT + st * 16384, row, pk);
-            st_row64(sdST + st * 16384, row, dk);
-            fence_proxy_async();
+            if (i >= 1) {
+                mbar_wait(pd_done, (i - 1) & 1);  // dV/dK of tile i-1 have read P^T / dS^T
+                tc_fence_after();
+            }
+            tmem_st32(tmem + lane_base + P_COL, pk);
+            tmem_st32(tmem + lane_base + DS_COL, dk);
+            tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full);
@@ -281,28 +295,29 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
 }
 
 // =====================================================================================  dQ
+// TMEM: S[b] [b*128, b*128+64) dP[b] [b*128+64, b*128+128) dQ [256, 256+HD) dS [DS, DS+32)
 template <int HD>
 __global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_constant__ BwdMaps tm, AttnBwdProblem p) {
-    constexpr int BMQ = 128, BKV = 64;
+    constexpr int BMQ = 128, BKV = 64, NST = 4;
     using T = BT<HD>;
-    constexpr int DQ_COL = 256;
+    constexpr int DQ_COL = 256, DS_COL = 256 + ((HD + 15) / 16) * 16;
+    static_assert(DS_COL + 32 <= 512, "TMEM budget");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;
     uint8_t* sdO = sQ + T::ROW_TILE;
-    uint8_t* sKt = sdO + T::ROW_TILE;    // [2]
-    uint8_t* sVt = sKt + 2 * T::T_TILE;  // [2]
-    uint8_t* sdS = sVt + 2 * T::T_TILE;  // [2] x 16 KB
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + 2 * 16384);
+    uint8_t* sKt = sdO + T::ROW_TILE;      // [NST]
+    uint8_t* sVt = sKt + NST * T::T_TILE;  // [NST]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sVt + NST * T::T_TILE);
     uint64_t* q_full = bars;
-    uint64_t* kv_full = bars + 1;   // [2]
-    uint64_t* kv_empty = bars + 3;  // [2]
-    uint64_t* s_full = bars + 5;    // [2]
-    uint64_t* s_empty = bars + 7;   // [2]
-    uint64_t* ds_full = bars + 9;
-    uint64_t* ds_empty = bars + 10;  // [2]
-    uint64_t* acc_done = bars + 12;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+    uint64_t* kv_full = bars + 1;          // [NST]
+    uint64_t* kv_empty = bars + 1 + NST;   // [NST]
+    uint64_t* s_full = bars + 1 + 2 * NST;  // [2]
+    uint64_t* s_empty = s_full + 2;         // [2]
+    uint64_t* ds_full = s_full + 4;
+    uint64_t* dq_done = s_full + 5;
+    uint64_t* acc_done = s_full + 6;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 8);
 
     const AttnProblem& f = p.f;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -312,14 +327,16 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_con
 
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NST; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
             mbar_init(&s_empty[i], 4);
-            mbar_init(&ds_empty[i], 1);
         }
         mbar_init(ds_full, 4);
+        mbar_init(dq_done, 1);
         mbar_init(acc_done, 1);
         fence_barrier_init();
     }
@@ -335,8 +352,8 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_con
             load_row_tile<HD>(sQ, &tm.a128, &tm.a32, q_full, col, q0);
             load_row_tile<HD>(sdO, &tm.b128, &tm.b32, q_full, col, q0);
             for (int j = 0; j < nkv; ++j) {
-                const int b = j & 1;
-                if (j >= 2) mbar_wait(&kv_empty[b], ((j - 2) >> 1) & 1);
+                const int b = j % NST;
+                if (j >= NST) mbar_wait(&kv_empty[b], ((j / NST) - 1) & 1);
                 mbar_arrive_expect_tx(&kv_full[b], 2 * T::T_TILE);
                 tma_load_2d(sKt + b * T::T_TILE, &tm.ta, &kv_full[b], j * BKV, col);
                 tma_load_2d(sVt + b * T::T_TILE, &tm.tb, &kv_full[b], j * BKV, col);
@@ -345,21 +362,21 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_con
     } else if (warp == 1) {
         const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO);
         auto issue_dq = [&](int j) {
-            const int b = j & 1;
-            mma_chunk_x_t<HD>(tmem + DQ_COL, smem_u32(sdS + b * 16384), smem_u32(sKt + b * T::T_TILE), j > 0);
-            umma_commit(&ds_empty[b]);
+            const int b = j % NST;
+            mma_tmem_x_t<HD>(tmem + DQ_COL, tmem + DS_COL, smem_u32(sKt + b * T::T_TILE), j > 0);
+            umma_commit(dq_done);
             umma_commit(&kv_empty[b]);
         };
         mbar_wait(q_full, 0);
         for (int j = 0; j < nkv; ++j) {
-            const int b = j & 1;
-            mbar_wait(&kv_full[b], (j >> 1) & 1);
-            if (j >= 2) mbar_wait(&s_empty[b], ((j - 2) >> 1) & 1);
+            const int b = j % NST, sb = j & 1;
+            mbar_wait(&kv_full[b], (j / NST) & 1);
+            if (j >= 2) mbar_wait(&s_empty[sb], ((j - 2) >> 1) & 1);
             tc_fence_after();
             if (elect_one()) {
-                mma_rows_x_t<HD>(tmem + b * 128, aQ, smem_u32(sKt + b * T::T_TILE));
-                mma_rows_x_t<HD>(tmem + b * 128 + 64, adO, smem_u32(sVt + b * T::T_TILE));
-                umma_commit(&s_full[b]);
+                mma_rows_x_t<HD>(tmem + sb * 128, aQ, smem_u32(sKt + b * T::T_TILE));
+                mma_rows_x_t<HD>(tmem + sb * 128 + 64, adO, smem_u32(sVt + b * T::T_TILE));
+                umma_commit(&s_full[sb]);
             }
             __syncwarp();
             if (j >= 1) {
@@ -385,18 +402,18 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_con
         const float lse2 = q < f.Nq ? f.lse[(int64_t)h * f.Nq + q] * kLog2e : 0.0f;
         const float Dq = q < f.Nq ? p.Dvec[(int64_t)h * f.Nq + q] : 0.0f;
         for (int j = 0; j < nkv; ++j) {
-            const int b = j & 1;
-            mbar_wait(&s_full[b], (j >> 1) & 1);
+            const int sb = j & 1;
+            mbar_wait(&s_full[sb], (j >> 1) & 1);
             tc_fence_after();
             float s[BKV], dp[BKV];
-            tmem_ld32(tmem + lane_base + b * 128, reinterpret_cast<uint32_t*>(s));
-            tmem_ld32(tmem + lane_base + b * 128 + 32, reinterpret_cast<uint32_t*>(s + 32));
-            tmem_ld32(tmem + lane_base + b * 128 + 64, reinterpret_cast<uint32_t*>(dp));
-            tmem_ld32(tmem + lane_base + b * 128 + 96, reinterpret_cast<uint32_t*>(dp + 32));
+            tmem_ld32(tmem + lane_base + sb * 128, reinterpret_cast<uint32_t*>(s));
+            tmem_ld32(tmem + lane_base + sb * 128 + 32, reinterpret_cast<uint32_t*>(s + 32));
+            tmem_ld32(tmem + lane_base + sb * 128 + 64, reinterpret_cast<uint32_t*>(dp));
+            tmem_ld32(tmem + lane_base + sb * 128 + 96, reinterpret_cast<uint32_t*>(dp + 32));
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&s_empty[b]);
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
             uint32_t dk[BKV / 2];
             const bool full = (j + 1) * BKV <= f.Nk;
 #pragma unroll
@@ -406,9 +423,12 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_con
                 const float p1 = v1 ? ex2f(fmaf(s[c + 1], kLog2e, -lse2)) : 0.0f;
                 dk[c / 2] = pack_bf16(p0 * (dp[c] - Dq), p1 * (dp[c + 1] - Dq));
             }
-            if (j >= 2) mbar_wait(&ds_empty[b], ((j - 2) >> 1) & 1);
-            st_row64(sdS + b * 16384, row, dk);
-            fence_proxy_async();
+            if (j >= 1) {
+                mbar_wait(dq_done, (j - 1) & 1);  // dQ += dS_{j-1} K has read the dS columns
+                tc_fence_after();
+            }
+            tmem_st32(tmem + lane_base + DS_COL, dk);
+            tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(ds_full);
@@ -440,7 +460,7 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
         make_tmap_sw(&m.b32, f.v, W, f.Nk, f.v_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
         make_tmap_sw(&m.ta, qt, f.Nq, W, qt_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
         make_tmap_sw(&m.tb, dot, f.Nq, W, dot_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
-        const int smem = 2 * T::ROW_TILE + 4 * T::T_TILE + 4 * 16384 + 4 * 64 * 4 + 256 + 1024;
+        const int smem = 2 * T::ROW_TILE + 8 * T::T_TILE + 8 * 64 * 4 + 256 + 1024;
         static bool set = false;
         if (!set) {
             MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -457,7 +477,7 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
         make_tmap_sw(&m.b32, p.dO, W, f.Nq, p.do_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
         make_tmap_sw(&m.ta, kt, f.Nk, W, kt_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
         make_tmap_sw(&m.tb, vt, f.Nk, W, vt_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
-        const int smem = 2 * T::ROW_TILE + 4 * T::T_TILE + 2 * 16384 + 256 + 1024;
+        const int smem = 2 * T::ROW_TILE + 8 * T::T_TILE + 256 + 1024;
         static bool set = false;
         if (!set) {
             MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
