@@ -26,7 +26,12 @@ struct AttnProblem {
     // tensor-core path: V^T ([heads*hd][>= Nk], row h*hd+d holds v[:, h*hd+d]); null -> computed internally
     const void* vt = nullptr;
     int64_t vt_ld = 0;
+    // per-head stride of lse (and of the backward's Dvec); 0 -> Nq.  The tensor-core backward
+    // streams lse/D with bulk copies and wants it padded to a multiple of 64.
+    int64_t lse_ld = 0;
 };
+
+__host__ __device__ inline int64_t lse_stride(const AttnProblem& p) { return p.lse_ld ? p.lse_ld : p.Nq; }
 
 struct AttnBwdProblem {
     AttnProblem f;

@@ -188,16 +188,13 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
             const int st = i % NST;
             if (i >= NST) mbar_wait(&qd_empty[st], ((i / NST) - 1) & 1);
             if (lane == 0) {
-                mbar_arrive_expect_tx(&qd_full[st], 2 * T::T_TILE);
+                // Q^T / dO^T tiles + this tile's lse and D rows (lse/D padded per head to a multiple of 64)
+                mbar_arrive_expect_tx(&qd_full[st], 2 * T::T_TILE + 2 * BQ * 4);
                 tma_load_2d(sQt + st * T::T_TILE, &tm.ta, &qd_full[st], i * BQ, col);
                 tma_load_2d(sdOt + st * T::T_TILE, &tm.tb, &qd_full[st], i * BQ, col);
+                bulk_load(sLse + st * BQ, f.lse + (int64_t)h * lse_stride(f) + i * BQ, BQ * 4, &qd_full[st]);
+                bulk_load(sD + st * BQ, p.Dvec + (int64_t)h * lse_stride(f) + i * BQ, BQ * 4, &qd_full[st]);
             }
-            for (int c = lane; c < BQ; c += 32) {
-                const int q = i * BQ + c;
-                sLse[st * BQ + c] = q < f.Nq ? f.lse[(int64_t)h * f.Nq + q] * kLog2e : 0.0f;
-                sD[st * BQ + c] = q < f.Nq ? p.Dvec[(int64_t)h * f.Nq + q] : 0.0f;
-            }
-            mbar_arrive(&lse_full[st]);
         }
     } else if (warp == 1) {
         const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
@@ -244,7 +241,7 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
         const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
         for (int i = 0; i < nq; ++i) {
             const int st = i % NST;
-            mbar_wait(&lse_full[st], (i / NST) & 1);
+            mbar_wait(&qd_full[st], (i / NST) & 1);  // lse / D rows of this tile have landed
             mbar_wait(s_full, i & 1);
             tc_fence_after();
             float s[BQ], dp[BQ];
@@ -263,8 +260,8 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
 #pragma unroll
             for (int c = 0; c < BQ; c += 2) {
                 const bool v0 = full || i * BQ + c < f.Nq, v1 = full || i * BQ + c + 1 < f.Nq;
-                const float p0 = v0 ? ex2f(fmaf(s[c], kLog2e, -lse2[c])) : 0.0f;
-                const float p1 = v1 ? ex2f(fmaf(s[c + 1], kLog2e, -lse2[c + 1])) : 0.0f;
+                const float p0 = v0 ? ex2f((s[c] - lse2[c]) * kLog2e) : 0.0f;  // lse rows are natural-log
+                const float p1 = v1 ? ex2f((s[c + 1] - lse2[c + 1]) * kLog2e) : 0.0f;
                 pk[c / 2] = pack_bf16(p0, p1);
                 dk[c / 2] = pack_bf16(p0 * (dp[c] - Dq[c]), p1 * (dp[c + 1] - Dq[c + 1]));  // autodiff.cpp:820
             }
@@ -399,8 +396,8 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_con
         const int wq = warp - 4, row = wq * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
         const int q = q0 + row;
-        const float lse2 = q < f.Nq ? f.lse[(int64_t)h * f.Nq + q] * kLog2e : 0.0f;
-        const float Dq = q < f.Nq ? p.Dvec[(int64_t)h * f.Nq + q] : 0.0f;
+        const float lse2 = q < f.Nq ? f.lse[(int64_t)h * lse_stride(f) + q] * kLog2e : 0.0f;
+        const float Dq = q < f.Nq ? p.Dvec[(int64_t)h * lse_stride(f) + q] : 0.0f;
         for (int j = 0; j < nkv; ++j) {
             const int sb = j & 1;
             mbar_wait(&s_full[sb], (j >> 1) & 1);
@@ -507,13 +504,29 @@ void attn_bwd_tc(const AttnBwdProblem& p, cudaStream_t s) {
     const void* kt = p.kt ? p.kt : make_t(f.k, f.k_ld, f.Nk, &kt_ld);
     const void* vt = f.vt ? f.vt : make_t(f.v, f.v_ld, f.Nk, &vt_ld);
     const void* dot = p.dot ? p.dot : make_t(p.dO, p.do_ld, f.Nq, &dot_ld);
+    // lse / D rows are streamed with bulk copies: per-head stride must be a multiple of 64 covering Nq
+    AttnBwdProblem q = p;
+    const int64_t need = (static_cast<int64_t>(f.Nq) + 63) / 64 * 64;
+    std::vector<float*> ftmp;
+    if (lse_stride(f) < need || lse_stride(f) % 64 != 0) {
+        float *lse = nullptr, *dv = nullptr;
+        MGV_CUDA(cudaMallocAsync(&lse, sizeof(float) * need * f.heads, s));
+        MGV_CUDA(cudaMallocAsync(&dv, sizeof(float) * need * f.heads, s));
+        MGV_CUDA(cudaMemcpy2DAsync(lse, need * sizeof(float), f.lse, lse_stride(f) * sizeof(float),
+                                   f.Nq * sizeof(float), f.heads, cudaMemcpyDeviceToDevice, s));
+        q.f.lse = lse;
+        q.f.lse_ld = need;
+        q.Dvec = dv;
+        ftmp = {lse, dv};
+    }
     switch (f.hd) {
-        case 64: launch_bwd<64>(p, qt, qt_ld, kt, kt_ld, vt, vt_ld, dot, dot_ld, s); break;
-        case 128: launch_bwd<128>(p, qt, qt_ld, kt, kt_ld, vt, vt_ld, dot, dot_ld, s); break;
-        case 144: launch_bwd<144>(p, qt, qt_ld, kt, kt_ld, vt, vt_ld, dot, dot_ld, s); break;
+        case 64: launch_bwd<64>(q, qt, qt_ld, kt, kt_ld, vt, vt_ld, dot, dot_ld, s); break;
+        case 128: launch_bwd<128>(q, qt, qt_ld, kt, kt_ld, vt, vt_ld, dot, dot_ld, s); break;
+        case 144: launch_bwd<144>(q, qt, qt_ld, kt, kt_ld, vt, vt_ld, dot, dot_ld, s); break;
         default: throw std::runtime_error("attn_bwd_tc: unsupported head_dim");
     }
     for (auto* d : tmp) MGV_CUDA(cudaFreeAsync(d, s));
+    for (auto* d : ftmp) MGV_CUDA(cudaFreeAsync(d, s));
 }
 
 }  // namespace mgv

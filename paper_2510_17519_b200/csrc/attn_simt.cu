@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(NT) attn_fwd_simt_kernel(AttnProblem p) {
         const int i = e / hd, d = e % hd, q = q0 + i;
         if (q < p.Nq) static_cast<T*>(p.o)[(int64_t)q * p.o_ld + h * hd + d] = to_t<T>(sO[e] / sL[i]);
     }
-    if (tid < BQ && q0 + tid < p.Nq) p.lse[(int64_t)h * p.Nq + q0 + tid] = sM[tid] + logf(sL[tid]);
+    if (tid < BQ && q0 + tid < p.Nq) p.lse[(int64_t)h * lse_stride(p) + q0 + tid] = sM[tid] + logf(sL[tid]);
 }
 
 // D[h][q] = sum_d dO * O
@@ -108,7 +108,7 @@ __global__ void attn_bwd_dvec_kernel(AttnBwdProblem p) {
         acc += ld_el<T>(p.dO, q * p.do_ld + h * hd + d) * ld_el<T>(p.f.o, q * p.f.o_ld + h * hd + d);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffff, acc, o);
-    if (lane == 0) p.Dvec[(int64_t)h * p.f.Nq + q] = acc;
+    if (lane == 0) p.Dvec[(int64_t)h * lse_stride(p.f) + q] = acc;
 }
 
 // Shared tile math for both backward passes: given sQ, sdO (BQ rows), sK, sV (BK rows), lse/D for the q rows,
@@ -158,8 +158,8 @@ __global__ void __launch_bounds__(NT) attn_bwd_dq_simt_kernel(AttnBwdProblem p) 
     for (int e = tid; e < BQ * hd; e += NT) sAcc[e] = 0.0f;
     if (tid < BQ) {
         const int q = q0 + tid;
-        sLse[tid] = q < f.Nq ? f.lse[(int64_t)h * f.Nq + q] : 0.0f;
-        sD[tid] = q < f.Nq ? p.Dvec[(int64_t)h * f.Nq + q] : 0.0f;
+        sLse[tid] = q < f.Nq ? f.lse[(int64_t)h * lse_stride(f) + q] : 0.0f;
+        sD[tid] = q < f.Nq ? p.Dvec[(int64_t)h * lse_stride(f) + q] : 0.0f;
     }
     for (int k0 = 0; k0 < f.Nk; k0 += BK) {
         __syncthreads();
@@ -210,8 +210,8 @@ __global__ void __launch_bounds__(NT) attn_bwd_dkv_simt_kernel(AttnBwdProblem p)
         load_rows<T>(sdO, hd, p.dO, p.do_ld, q0, BQ, f.Nq, h, hd);
         if (tid < BQ) {
             const int q = q0 + tid;
-            sLse[tid] = q < f.Nq ? f.lse[(int64_t)h * f.Nq + q] : 0.0f;
-            sD[tid] = q < f.Nq ? p.Dvec[(int64_t)h * f.Nq + q] : 0.0f;
+            sLse[tid] = q < f.Nq ? f.lse[(int64_t)h * lse_stride(f) + q] : 0.0f;
+            sD[tid] = q < f.Nq ? p.Dvec[(int64_t)h * lse_stride(f) + q] : 0.0f;
         }
         __syncthreads();
         bwd_tile_p_ds(sQ, sdO, sK, sV, sLse, sD, sP, sdS, hd, q0, f.Nq, k0, f.Nk);

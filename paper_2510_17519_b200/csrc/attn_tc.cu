@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_tc_kernel(const __grid_consta
                 dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
             }
         }
-        if (q < p.Nq) p.lse[(int64_t)h * p.Nq + q] = (m2 + __log2f(l)) * 0.6931471805599453f;
+        if (q < p.Nq) p.lse[(int64_t)h * lse_stride(p) + q] = (m2 + __log2f(l)) * 0.6931471805599453f;
     }
     tc_fence_before();
     __syncthreads();

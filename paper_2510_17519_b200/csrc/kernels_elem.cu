@@ -753,19 +753,61 @@ __global__ void mod_wgrad_kernel(const float* dm, const double* gb, int n_u, int
         }
     }
 }
-// dgb[u, j] = sum_k dm[u, k] W_mod[k, j] ; one warp per (u, j) would stride W by rows -> use column-parallel threads
-__global__ void mod_dgrad_kernel(const float* dm, const float* w, int n_u, int H, double* dgb) {
+// out[r, j] = sum_k in[r, k] W[k, j] for R <= 3 rows, fp64 accumulation, split over K:
+// thread = column j of one K-slice; all rows share each W read.  part[ks][r][j], then a
+// fixed-order reduce over the slices (deterministic).
+constexpr int VM_KS = 48;
+template <class TI, int R>
+__global__ void vecmat_part_kernel(const TI* in, int64_t in_ld, int rows, const float* W, int K, int J, double* part) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    const int u = blockIdx.y;
-    if (j >= H) return;
-    double acc = 0.0;
-    for (int k = 0; k < 6 * H; ++k) acc += static_cast<double>(dm[(int64_t)u * 6 * H + k]) * w[(int64_t)k * H + j];
-    dgb[(int64_t)u * H + j] = acc;
+    const int ks = blockIdx.y;
+    if (j >= J) return;
+    const int per = (K + VM_KS - 1) / VM_KS;
+    const int k0 = ks * per, k1 = min(K, k0 + per);
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    for (int k = k0; k < k1; ++k) {
+        const double w = static_cast<double>(W[(int64_t)k * J + j]);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            if (r < rows) acc[r] += static_cast<double>(in[(int64_t)r * in_ld + k]) * w;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        if (r < rows) part[((int64_t)ks * R + r) * J + j] = acc[r];
+}
+// out[r, j] = sum_ks part[ks][r][j]  (x silu'(z[r, j]) when z != null)
+template <int R>
+__global__ void vecmat_reduce_kernel(const double* part, int rows, int J, const double* z, double* out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= J) return;
+    for (int r = 0; r < rows; ++r) {
+        double acc = 0.0;
+        for (int ks = 0; ks < VM_KS; ++ks) acc += part[((int64_t)ks * R + r) * J + j];
+        if (z) {
+            const double zz = z[(int64_t)r * J + j];
+            const double sg = 1.0 / (1.0 + exp(-zz));
+            acc *= sg + zz * sg * (1.0 - sg);
+        }
+        out[(int64_t)r * J + j] = acc;
+    }
+}
+template <class TI>
+static void vecmat(const TI* in, int64_t in_ld, int rows, const float* W, int K, int J, const double* z, double* out,
+                   cudaStream_t s) {
+    if (rows > 3) throw std::runtime_error("vecmat: at most 3 rows");
+    double* part = nullptr;
+    MGV_CUDA(cudaMallocAsync(&part, sizeof(double) * VM_KS * 3 * (size_t)J, s));
+    vecmat_part_kernel<TI, 3><<<dim3((J + 255) / 256, VM_KS), 256, 0, s>>>(in, in_ld, rows, W, K, J, part); ::mgv::note_launch();
+    vecmat_reduce_kernel<3><<<(J + 255) / 256, 256, 0, s>>>(part, rows, J, z, out); ::mgv::note_launch();
+    MGV_CUDA(cudaFreeAsync(part, s));
+    MGV_CUDA(cudaGetLastError());
 }
 void modulation_bwd(const float* dm, const double* gb, const float* w_mod, int n_u, int H, float* dw_mod,
                     float* db_mod, double* dgb, cudaStream_t s) {
     mod_wgrad_kernel<<<grid_for((int64_t)6 * H * H), 256, 0, s>>>(dm, gb, n_u, H, dw_mod, db_mod); ::mgv::note_launch();
-    mod_dgrad_kernel<<<dim3((H + 127) / 128, n_u), 128, 0, s>>>(dm, w_mod, n_u, H, dgb); ::mgv::note_launch();
+    vecmat<float>(dm, 6 * H, n_u, w_mod, 6 * H, H, nullptr, dgb, s);  // dgb = dm W_mod
     MGV_CUDA(cudaGetLastError());
 }
 __global__ void gscale_bwd_kernel(const double* dgb, const double* g, const float* gs, int n_u, int H, float* dgs,
@@ -801,23 +843,16 @@ __global__ void gmlp_out_bwd_kernel(const double* dg, int n_u, const double* h_i
         if (j == 0) db_out[k] += static_cast<float>(2.0 * dgf);  // both MLP evaluations add b_out
     }
 }
-// dz[r, j] = (sum_k dg_r[k] W_out[k, j]) * silu'(z_in[r, j])
-__global__ void gmlp_dz_kernel(const double* dg, int n_u, const double* z_in, const float* w_out, int H, double* dz) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    const int r = blockIdx.y;
-    if (j >= H) return;
-    double acc = 0.0;
-    for (int k = 0; k < H; ++k) {
-        double d = 0.0;
-        if (r < n_u)
-            d = dg[(int64_t)r * H + k];
-        else
-            for (int u = 0; u < n_u; ++u) d += dg[(int64_t)u * H + k];
-        acc += d * static_cast<double>(w_out[(int64_t)k * H + j]);
+// rows of the gmlp output gradient: dg_u (u < n_u) and the fps row sum_u dg_u
+__global__ void gmlp_rows_kernel(const double* dg, int n_u, int H, double* rows) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= H) return;
+    double f = 0.0;
+    for (int u = 0; u < n_u; ++u) {
+        rows[(int64_t)u * H + k] = dg[(int64_t)u * H + k];
+        f += dg[(int64_t)u * H + k];
     }
-    const double z = z_in[(int64_t)r * H + j];
-    const double sg = 1.0 / (1.0 + exp(-z));
-    dz[(int64_t)r * H + j] = acc * (sg + z * sg * (1.0 - sg));
+    rows[(int64_t)n_u * H + k] = f;
 }
 __global__ void gmlp_in_bwd_kernel(const double* dz, int R, const double* phi, int H, float* dw_in, float* db_in) {
     const int64_t total = (int64_t)H * 32;
@@ -837,11 +872,14 @@ void global_embed_bwd(const double* dg, int n_u, const double* phi, const double
                       const float* w_out, int H, float* dw_in, float* db_in, float* dw_out, float* db_out,
                       cudaStream_t s) {
     // scratch dz lives after h_in's rows? keep it simple: allocate per call (tiny, (n_u+1) x H doubles)
-    double* dz = nullptr;
+    double *dz = nullptr, *rows = nullptr;
     MGV_CUDA(cudaMallocAsync(&dz, sizeof(double) * (size_t)(n_u + 1) * H, s));
+    MGV_CUDA(cudaMallocAsync(&rows, sizeof(double) * (size_t)(n_u + 1) * H, s));
     gmlp_out_bwd_kernel<<<grid_for((int64_t)H * H), 256, 0, s>>>(dg, n_u, h_in, H, dw_out, db_out); ::mgv::note_launch();
-    gmlp_dz_kernel<<<dim3((H + 127) / 128, n_u + 1), 128, 0, s>>>(dg, n_u, z_in, w_out, H, dz); ::mgv::note_launch();
+    gmlp_rows_kernel<<<(H + 255) / 256, 256, 0, s>>>(dg, n_u, H, rows); ::mgv::note_launch();
+    vecmat<double>(rows, H, n_u + 1, w_out, H, H, z_in, dz, s);  // dz = (rows W_out) * silu'(z_in)
     gmlp_in_bwd_kernel<<<grid_for((int64_t)H * 32), 256, 0, s>>>(dz, n_u + 1, phi, H, dw_in, db_in); ::mgv::note_launch();
+    MGV_CUDA(cudaFreeAsync(rows, s));
     MGV_CUDA(cudaFreeAsync(dz, s));
     MGV_CUDA(cudaGetLastError());
 }
