@@ -402,12 +402,65 @@ def run_ours(args, rank, world, local):
         "gpu_launches": launches,
         "loss": loss, "grad_norm": gnorm,
     }
+    if world == 1 and not args.no_extra:
+        res["extra_configs"] = extra_configs(ctx, args)
     if world == 1 and not args.no_cpu_baseline:
         try:
             res["cpu_baseline"] = cpu_baseline_once()
         except Exception as e:  # the baseline is reported, never required
             res["cpu_baseline"] = {"value": None, "unavailable": str(e)[:200]}
     print(json.dumps(res))
+
+
+def extra_configs(ctx, args):
+    """BASELINE.json configs[1] (480p/2s forward, 10,920 tokens) and configs[4] (mixed-resolution varlen
+    batch with first-frame conditioning) through the public C ABI with host buffers (e2e timing)."""
+    import torch
+    from paper_2510_17519_b200.capi import FlowSample
+    out = {}
+    rng = np.random.default_rng(7)
+    text = np.random.default_rng(4).standard_normal((TEXT_L, TEXT_D))
+    # configs[1]: predict_velocity (forward only) on a 480p/2s latent (7, 60, 104, 24) -> 7x30x52 = 10920 tokens
+    dims = (7, 30, 52)
+    n = dims[0] * dims[1] * dims[2]
+    rows = rng.uniform(-1, 1, (n, PATCH))
+    coords = grid_coords(dims)
+    tau = np.full(n, 0.5)
+    for _ in range(2):
+        ctx.predict_velocity(rows, coords, dims, text, tau, 8.0)
+    ts = []
+    for _ in range(max(3, args.steps)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx.predict_velocity(rows, coords, dims, text, tau, 8.0)
+        ts.append(time.perf_counter() - t0)
+    ms = 1000 * statistics.median(ts)
+    f_fwd = 28.0 * n * H * H + 4.0 * n * n * H + 4.0 * n * TEXT_L * H
+    out["cfg1_480p_fwd"] = {"workload": "predict_velocity, 10B dims depth 1, latent 7x60x104x24 -> 10920 tokens",
+                            "tokens_per_s": n / (ms / 1000), "ms": ms, "block_tflops": f_fwd / (ms * 1e9),
+                            "timing": "wall clock around the C-ABI call, host buffers (e2e)"}
+    # configs[4]: mixed-resolution batch: 4 x 480p/2s clips + 4 x 720p images, first-frame mask prob 0.3
+    shapes = [(7, 30, 52)] * 4 + [(1, 45, 80)] * 4
+    samples = []
+    for k, d in enumerate(shapes):
+        nn = d[0] * d[1] * d[2]
+        co = grid_coords(d)
+        cond = (co[:, 0] == 0).astype(np.uint8) if (d[0] > 1 and rng.uniform() < 0.3) else None
+        samples.append(FlowSample(d, co, rng.uniform(-1, 1, (nn, PATCH)), rng.standard_normal((nn, PATCH)),
+                                  float(rng.uniform(0.05, 0.95)), cond))
+    tot = sum(s.clean_rows.shape[0] for s in samples)
+    ctx.flow_step(samples, text, 8.0)
+    ts = []
+    for _ in range(max(3, args.steps)):
+        t0 = time.perf_counter()
+        ctx.flow_step(samples, text, 8.0)
+        ts.append(time.perf_counter() - t0)
+    ms = 1000 * statistics.median(ts)
+    out["cfg4_varlen_mixed"] = {"workload": "flow step fwd+bwd over 4 x (7,30,52) clips + 4 x (1,45,80) images "
+                                            f"= {tot} tokens, first-frame conditioning p=0.3, samples run as batches of one",
+                                "tokens_per_s": tot / (ms / 1000), "ms": ms,
+                                "timing": "wall clock around the C-ABI call, host buffers (e2e)"}
+    return out
 
 
 def main():
@@ -417,6 +470,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the configs[1]/configs[4] side measurements")
     args = ap.parse_args()
     rank, world, local = dist_init()
     if args.impl == "reference":
