@@ -12,6 +12,28 @@
 #include "gemm.cuh"
 #include "kernels.h"
 
+#include <type_traits>
+
+namespace mgv {
+// vectorised bf16 row kernels (defined at the end of this file)
+bool use_vec(int H);
+void rms_fwd_vec_launch(const float* X, int N, int H, const float* table, int64_t tld, int sh_off, int sc_off,
+                        const int32_t* mod_id, const float* g, __nv_bfloat16* out, float* r, cudaStream_t s);
+void postnorm_resid_vec_launch(const float* X1, const __nv_bfloat16* co, int N, int H, const float* g, float* X2,
+                               float* rc, cudaStream_t s);
+void gate_bwd_vec_launch(const float* dX, const __nv_bfloat16* y, const float* table, int64_t tld, int gate_off,
+                         const int32_t* mod_id, int n_u, int N, int H, __nv_bfloat16* dY, float* part_dgate,
+                         float* part_db, cudaStream_t s);
+void rms_bwd_vec_launch(int mode, const __nv_bfloat16* dA, const float* X, const float* r, const float* table,
+                        int64_t tld, int sc_off, const int32_t* mod_id, int n_u, const float* g, int N, int H, float* dX,
+                        int accumulate, float* part_a, float* part_b, cudaStream_t s);
+void postnorm_bwd_vec_launch(const float* dX, const __nv_bfloat16* co, const float* rc, const float* g, int N, int H,
+                             __nv_bfloat16* dco, float* part_dg, cudaStream_t s);
+void colsum_vec_launch(const __nv_bfloat16* Y, int64_t ld, int N, int C, float* part, cudaStream_t s);
+template <class T>
+constexpr bool is_bf16() { return std::is_same<T, __nv_bfloat16>::value; }
+}  // namespace mgv
+
 namespace mgv {
 
 namespace {
@@ -296,11 +318,17 @@ __global__ void __launch_bounds__(RT) rms_mod_kernel(const float* X, int N, int 
 template <class T>
 void rms_mod(const float* X, int N, int H, const float* table, int64_t tld, int sh_off, int sc_off,
              const int32_t* mod_id, T* out, float* r, cudaStream_t s) {
+    if constexpr (is_bf16<T>()) {
+        if (use_vec(H)) return rms_fwd_vec_launch(X, N, H, table, tld, sh_off, sc_off, mod_id, nullptr, out, r, s);
+    }
     rms_mod_kernel<T><<<row_chunks(N), RT, 0, s>>>(X, N, H, table, tld, sh_off, sc_off, mod_id, 0, nullptr, out, r); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 template <class T>
 void rms_gain(const float* X, int N, int H, const float* g, T* out, float* r, cudaStream_t s) {
+    if constexpr (is_bf16<T>()) {
+        if (use_vec(H)) return rms_fwd_vec_launch(X, N, H, nullptr, 0, 0, 0, nullptr, g, out, r, s);
+    }
     rms_mod_kernel<T><<<row_chunks(N), RT, 0, s>>>(X, N, H, nullptr, 0, 0, 0, nullptr, 1, g, out, r); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
@@ -331,6 +359,9 @@ __global__ void __launch_bounds__(RT) postnorm_resid_kernel(const float* X1, con
 }
 template <class T>
 void postnorm_resid(const float* X1, const T* co, int N, int H, const float* g, float* X2, float* rc, cudaStream_t s) {
+    if constexpr (is_bf16<T>()) {
+        if (use_vec(H)) return postnorm_resid_vec_launch(X1, co, N, H, g, X2, rc, s);
+    }
     postnorm_resid_kernel<T><<<row_chunks(N), RT, 0, s>>>(X1, co, N, H, g, X2, rc); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
@@ -497,6 +528,10 @@ __global__ void __launch_bounds__(RT) gate_bwd_kernel(const float* dX, const T* 
 template <class T>
 void gate_bwd(const float* dX, const T* y, const float* table, int64_t tld, int gate_off, const int32_t* mod_id,
               int n_u, int N, int H, T* dY, float* part_dgate, float* part_db, cudaStream_t s) {
+    if constexpr (is_bf16<T>()) {
+        if (use_vec(H) && n_u <= 2)
+            return gate_bwd_vec_launch(dX, y, table, tld, gate_off, mod_id, n_u, N, H, dY, part_dgate, part_db, s);
+    }
     gate_bwd_kernel<T><<<row_chunks(N), RT, 0, s>>>(dX, y, table, tld, gate_off, mod_id, n_u, N, H, dY, part_dgate,
                                                    part_db); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
@@ -577,6 +612,11 @@ template <class T>
 void rms_mod_bwd(const T* dA, const float* X, const float* r, const float* table, int64_t tld, int sh_off, int sc_off,
                  const int32_t* mod_id, int n_u, int N, int H, float* dX, float* part_dsh, float* part_dsc,
                  cudaStream_t s) {
+    if constexpr (is_bf16<T>()) {
+        if (use_vec(H) && n_u <= 2)
+            return rms_bwd_vec_launch(0, dA, X, r, table, tld, sc_off, mod_id, n_u, nullptr, N, H, dX, 1, part_dsh,
+                                      part_dsc, s);
+    }
     rms_bwd_kernel<T, 0><<<row_chunks(N), RT, 0, s>>>(dA, X, r, table, tld, sh_off, sc_off, mod_id, n_u, nullptr, N, H,
                                                      dX, 1, part_dsh, part_dsc); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
@@ -584,6 +624,10 @@ void rms_mod_bwd(const T* dA, const float* X, const float* r, const float* table
 template <class T>
 void rms_gain_bwd(const T* dA, const float* X, const float* r, const float* g, int N, int H, float* dX, int accumulate,
                   float* part_dg, cudaStream_t s) {
+    if constexpr (is_bf16<T>()) {
+        if (use_vec(H))
+            return rms_bwd_vec_launch(1, dA, X, r, nullptr, 0, 0, nullptr, 1, g, N, H, dX, accumulate, part_dg, nullptr, s);
+    }
     rms_bwd_kernel<T, 1><<<row_chunks(N), RT, 0, s>>>(dA, X, r, nullptr, 0, 0, 0, nullptr, 1, g, N, H, dX, accumulate,
                                                      part_dg, nullptr); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
@@ -632,6 +676,9 @@ __global__ void __launch_bounds__(RT) postnorm_bwd_kernel(const float* dX, const
 template <class T>
 void postnorm_bwd(const float* dX, const T* co, const float* rc, const float* g, int N, int H, T* dco, float* part_dg,
                   cudaStream_t s) {
+    if constexpr (is_bf16<T>()) {
+        if (use_vec(H)) return postnorm_bwd_vec_launch(dX, co, rc, g, N, H, dco, part_dg, s);
+    }
     postnorm_bwd_kernel<T><<<row_chunks(N), RT, 0, s>>>(dX, co, rc, g, N, H, dco, part_dg); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
@@ -711,6 +758,10 @@ __global__ void colsum_kernel(const T* Y, int64_t ld, int N, int C, float* part)
 }
 template <class T>
 void colsum(const T* Y, int64_t ld, int N, int C, float* part, cudaStream_t s) {
+    if constexpr (is_bf16<T>()) {
+        if (C % 8 == 0 && ld % 8 == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0)
+            return colsum_vec_launch(Y, ld, N, C, part, s);
+    }
     dim3 grid(row_chunks(N), (C + 255) / 256);
     colsum_kernel<T><<<grid, 256, 0, s>>>(Y, ld, N, C, part); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
@@ -987,4 +1038,384 @@ void transpose_bf16(const __nv_bfloat16* in, int64_t ld_in, int rows, int cols, 
     transpose_bf16_kernel<<<grid, 256, 0, s>>>(in, ld_in, rows, cols, out, ld_out); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
+}  // namespace mgv
+
+// ======================================================================================
+// Vectorised bf16 row kernels (H % 8 == 0, H <= 4096): 16-byte accesses, 2 rows per block
+// reduction.  Dispatched from the launchers above when T = bf16.
+#include "kernels_vec.cuh"
+
+namespace mgv {
+namespace vec {
+
+using bf = __nv_bfloat16;
+
+template <int MODE>  // 0: out = n (1 + sc) + sh ; 1: out = n * g
+__global__ void __launch_bounds__(RT) rms_fwd_vec(const float* X, int N, int H, const float* table, int64_t tld,
+                                                  int sh_off, int sc_off, const int32_t* mod_id, const float* g,
+                                                  bf* out, float* rs) {
+    __shared__ float red[R][RT / 32];
+    const int G = H / 8;
+    const int r0 = blockIdx.x * kRowsPerChunk, r1 = min(N, r0 + kRowsPerChunk);
+    for (int i = r0; i < r1; i += R) {
+        float v[R][VG][8], ss[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+            ss[rr] = 0.0f;
+            const int row = i + rr;
+#pragma unroll
+            for (int k = 0; k < VG; ++k) {
+                const int grp = threadIdx.x + k * RT;
+                if (row < r1 && grp < G) {
+                    ld8(X + (int64_t)row * H + grp * 8, v[rr][k]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) v[rr][k][e] = 0.0f;
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) ss[rr] = fmaf(v[rr][k][e], v[rr][k][e], ss[rr]);
+            }
+        }
+        block_sum_r(ss, red);
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+            const int row = i + rr;
+            if (row >= r1) continue;
+            const float rstd = 1.0f / sqrtf(ss[rr] / static_cast<float>(H) + 1e-6f);
+            if (threadIdx.x == 0) rs[row] = rstd;
+            const float* tb = MODE == 0 ? table + (int64_t)mod_id[row] * tld : nullptr;
+#pragma unroll
+            for (int k = 0; k < VG; ++k) {
+                const int grp = threadIdx.x + k * RT;
+                if (grp >= G) continue;
+                float o[8], a[8], b[8];
+                if (MODE == 0) {
+                    ld8(tb + sc_off + grp * 8, a);
+                    ld8(tb + sh_off + grp * 8, b);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) o[e] = v[rr][k][e] * rstd * (1.0f + a[e]) + b[e];
+                } else {
+                    ld8(g + grp * 8, a);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) o[e] = v[rr][k][e] * rstd * a[e];
+                }
+                st8(out + (int64_t)row * H + grp * 8, o);
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(RT) postnorm_resid_vec(const float* X1, const bf* co, int N, int H, const float* g,
+                                                         float* X2, float* rc) {
+    __shared__ float red[R][RT / 32];
+    const int G = H / 8;
+    const int r0 = blockIdx.x * kRowsPerChunk, r1 = min(N, r0 + kRowsPerChunk);
+    for (int i = r0; i < r1; i += R) {
+        float v[R][VG][8], ss[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+            ss[rr] = 0.0f;
+            const int row = i + rr;
+#pragma unroll
+            for (int k = 0; k < VG; ++k) {
+                const int grp = threadIdx.x + k * RT;
+                if (row < r1 && grp < G) {
+                    ld8(co + (int64_t)row * H + grp * 8, v[rr][k]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) v[rr][k][e] = 0.0f;
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) ss[rr] = fmaf(v[rr][k][e], v[rr][k][e], ss[rr]);
+            }
+        }
+        block_sum_r(ss, red);
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+            const int row = i + rr;
+            if (row >= r1) continue;
+            const float rstd = 1.0f / sqrtf(ss[rr] / static_cast<float>(H) + 1e-6f);
+            if (threadIdx.x == 0) rc[row] = rstd;
+#pragma unroll
+            for (int k = 0; k < VG; ++k) {
+                const int grp = threadIdx.x + k * RT;
+                if (grp >= G) continue;
+                float x[8], gg[8];
+                ld8(X1 + (int64_t)row * H + grp * 8, x);
+                ld8(g + grp * 8, gg);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) x[e] += v[rr][k][e] * rstd * gg[e];
+                st8(X2 + (int64_t)row * H + grp * 8, x);
+            }
+        }
+    }
+}
+
+// dY = dX * gate[u] ; partials: grouped sum dX*y, sum dY
+__global__ void __launch_bounds__(RT) gate_bwd_vec(const float* dX, const bf* y, const float* table, int64_t tld,
+                                                   int gate_off, const int32_t* mod_id, int n_u, int N, int H, bf* dY,
+                                                   float* part_dgate, float* part_db) {
+    const int G = H / 8;
+    const int r0 = blockIdx.x * kRowsPerChunk, r1 = min(N, r0 + kRowsPerChunk);
+    float pg[2][VG][8], pb[VG][8];
+#pragma unroll
+    for (int k = 0; k < VG; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) pg[0][k][e] = pg[1][k][e] = pb[k][e] = 0.0f;
+    for (int i = r0; i < r1; ++i) {
+        const int u = mod_id[i];
+        const float* gt = table + (int64_t)u * tld + gate_off;
+#pragma unroll
+        for (int k = 0; k < VG; ++k) {
+            const int grp = threadIdx.x + k * RT;
+            if (grp >= G) continue;
+            float dx[8], yy[8], gg[8], d[8];
+            ld8(dX + (int64_t)i * H + grp * 8, dx);
+            ld8(y + (int64_t)i * H + grp * 8, yy);
+            ld8(gt + grp * 8, gg);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                d[e] = dx[e] * gg[e];
+                pb[k][e] += d[e];
+                const float t = dx[e] * yy[e];
+                if (u == 0) pg[0][k][e] += t; else pg[1][k][e] += t;
+            }
+            st8(dY + (int64_t)i * H + grp * 8, d);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < VG; ++k) {
+        const int grp = threadIdx.x + k * RT;
+        if (grp >= G) continue;
+        st8(part_db + (int64_t)blockIdx.x * H + grp * 8, pb[k]);
+        st8(part_dgate + ((int64_t)blockIdx.x * n_u + 0) * H + grp * 8, pg[0][k]);
+        if (n_u > 1) st8(part_dgate + ((int64_t)blockIdx.x * n_u + 1) * H + grp * 8, pg[1][k]);
+    }
+}
+
+// rms backward; MODE 0: dn = dA (1 + sc[u]), partials d shift / d scale (grouped); MODE 1: dn = dA g, partial d gain
+template <int MODE>
+__global__ void __launch_bounds__(RT) rms_bwd_vec(const bf* dA, const float* X, const float* rs, const float* table,
+                                                  int64_t tld, int sc_off, const int32_t* mod_id, int n_u,
+                                                  const float* g, int N, int H, float* dX, int accumulate,
+                                                  float* part_a, float* part_b) {
+    __shared__ float red[R][RT / 32];
+    const int G = H / 8;
+    const int r0 = blockIdx.x * kRowsPerChunk, r1 = min(N, r0 + kRowsPerChunk);
+    float pa[2][VG][8], pb[2][VG][8];
+#pragma unroll
+    for (int k = 0; k < VG; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) pa[0][k][e] = pa[1][k][e] = pb[0][k][e] = pb[1][k][e] = 0.0f;
+    for (int i = r0; i < r1; i += R) {
+        float xv[R][VG][8], dn[R][VG][8], dot[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+            dot[rr] = 0.0f;
+            const int row = i + rr;
+            const bool ok = row < r1;
+            const int u = (MODE == 0 && ok) ? mod_id[row] : 0;
+            const float rstd = ok ? rs[row] : 0.0f;
+            const float* tb = MODE == 0 ? table + (int64_t)u * tld + sc_off : g;
+#pragma unroll
+            for (int k = 0; k < VG; ++k) {
+                const int grp = threadIdx.x + k * RT;
+                if (ok && grp < G) {
+                    float da[8], t[8];
+                    ld8(dA + (int64_t)row * H + grp * 8, da);
+                    ld8(X + (int64_t)row * H + grp * 8, xv[rr][k]);
+                    ld8(tb + grp * 8, t);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const float n = xv[rr][k][e] * rstd;
+                        if (MODE == 0) {
+                            dn[rr][k][e] = da[e] * (1.0f + t[e]);
+                            if (u == 0) {
+                                pa[0][k][e] += da[e];
+                                pb[0][k][e] += da[e] * n;
+                            } else {
+                                pa[1][k][e] += da[e];
+                                pb[1][k][e] += da[e] * n;
+                            }
+                        } else {
+                            dn[rr][k][e] = da[e] * t[e];
+                            pa[0][k][e] += da[e] * n;
+                        }
+                        dot[rr] = fmaf(dn[rr][k][e], xv[rr][k][e], dot[rr]);
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) xv[rr][k][e] = dn[rr][k][e] = 0.0f;
+                }
+            }
+        }
+        block_sum_r(dot, red);
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+            const int row = i + rr;
+            if (row >= r1) continue;
+            const float rstd = rs[row];
+            const float kk = dot[rr] * rstd * rstd * rstd / static_cast<float>(H);
+#pragma unroll
+            for (int k = 0; k < VG; ++k) {
+                const int grp = threadIdx.x + k * RT;
+                if (grp >= G) continue;
+                float o[8];
+                if (accumulate) ld8(dX + (int64_t)row * H + grp * 8, o);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const float d = dn[rr][k][e] * rstd - xv[rr][k][e] * kk;
+                    o[e] = accumulate ? o[e] + d : d;
+                }
+                st8(dX + (int64_t)row * H + grp * 8, o);
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < VG; ++k) {
+        const int grp = threadIdx.x + k * RT;
+        if (grp >= G) continue;
+        if (MODE == 0) {
+            st8(part_a + ((int64_t)blockIdx.x * n_u + 0) * H + grp * 8, pa[0][k]);
+            st8(part_b + ((int64_t)blockIdx.x * n_u + 0) * H + grp * 8, pb[0][k]);
+            if (n_u > 1) {
+                st8(part_a + ((int64_t)blockIdx.x * n_u + 1) * H + grp * 8, pa[1][k]);
+                st8(part_b + ((int64_t)blockIdx.x * n_u + 1) * H + grp * 8, pb[1][k]);
+            }
+        } else {
+            st8(part_a + (int64_t)blockIdx.x * H + grp * 8, pa[0][k]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(RT) postnorm_bwd_vec(const float* dX, const bf* co, const float* rc, const float* g,
+                                                       int N, int H, bf* dco, float* part_dg) {
+    __shared__ float red[R][RT / 32];
+    const int G = H / 8;
+    const int r0 = blockIdx.x * kRowsPerChunk, r1 = min(N, r0 + kRowsPerChunk);
+    float pg[VG][8];
+#pragma unroll
+    for (int k = 0; k < VG; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) pg[k][e] = 0.0f;
+    for (int i = r0; i < r1; i += R) {
+        float xv[R][VG][8], dn[R][VG][8], dot[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+            dot[rr] = 0.0f;
+            const int row = i + rr;
+            const bool ok = row < r1;
+            const float rr_s = ok ? rc[row] : 0.0f;
+#pragma unroll
+            for (int k = 0; k < VG; ++k) {
+                const int grp = threadIdx.x + k * RT;
+                if (ok && grp < G) {
+                    float dx[8], gg[8];
+                    ld8(dX + (int64_t)row * H + grp * 8, dx);
+                    ld8(co + (int64_t)row * H + grp * 8, xv[rr][k]);
+                    ld8(g + grp * 8, gg);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        pg[k][e] += dx[e] * xv[rr][k][e] * rr_s;
+                        dn[rr][k][e] = dx[e] * gg[e];
+                        dot[rr] = fmaf(dn[rr][k][e], xv[rr][k][e], dot[rr]);
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) xv[rr][k][e] = dn[rr][k][e] = 0.0f;
+                }
+            }
+        }
+        block_sum_r(dot, red);
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+            const int row = i + rr;
+            if (row >= r1) continue;
+            const float rstd = rc[row];
+            const float kk = dot[rr] * rstd * rstd * rstd / static_cast<float>(H);
+#pragma unroll
+            for (int k = 0; k < VG; ++k) {
+                const int grp = threadIdx.x + k * RT;
+                if (grp >= G) continue;
+                float o[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) o[e] = dn[rr][k][e] * rstd - xv[rr][k][e] * kk;
+                st8(dco + (int64_t)row * H + grp * 8, o);
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < VG; ++k) {
+        const int grp = threadIdx.x + k * RT;
+        if (grp < G) st8(part_dg + (int64_t)blockIdx.x * H + grp * 8, pg[k]);
+    }
+}
+
+// column sums of a bf16 matrix: thread = 8 columns, CTA = (row chunk, 2048-column block)
+__global__ void __launch_bounds__(RT) colsum_vec(const bf* Y, int64_t ld, int N, int C, float* part) {
+    const int grp = blockIdx.y * RT + threadIdx.x;
+    if (grp * 8 >= C) return;
+    const int r0 = blockIdx.x * kRowsPerChunk, r1 = min(N, r0 + kRowsPerChunk);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int i = r0; i < r1; ++i) {
+        float v[8];
+        ld8(Y + (int64_t)i * ld + grp * 8, v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += v[e];
+    }
+    st8(part + (int64_t)blockIdx.x * C + grp * 8, acc);
+}
+
+}  // namespace vec
+
+bool use_vec(int H) { return H % 8 == 0 && H <= vec::RT * vec::VG * 8; }
+
+void rms_fwd_vec_launch(const float* X, int N, int H, const float* table, int64_t tld, int sh_off, int sc_off,
+                        const int32_t* mod_id, const float* g, __nv_bfloat16* out, float* r, cudaStream_t s) {
+    if (g)
+        vec::rms_fwd_vec<1><<<row_chunks(N), vec::RT, 0, s>>>(X, N, H, table, tld, sh_off, sc_off, mod_id, g, out, r);
+    else
+        vec::rms_fwd_vec<0><<<row_chunks(N), vec::RT, 0, s>>>(X, N, H, table, tld, sh_off, sc_off, mod_id, g, out, r);
+    note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
+void postnorm_resid_vec_launch(const float* X1, const __nv_bfloat16* co, int N, int H, const float* g, float* X2,
+                               float* rc, cudaStream_t s) {
+    vec::postnorm_resid_vec<<<row_chunks(N), vec::RT, 0, s>>>(X1, co, N, H, g, X2, rc);
+    note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
+void gate_bwd_vec_launch(const float* dX, const __nv_bfloat16* y, const float* table, int64_t tld, int gate_off,
+                         const int32_t* mod_id, int n_u, int N, int H, __nv_bfloat16* dY, float* part_dgate,
+                         float* part_db, cudaStream_t s) {
+    vec::gate_bwd_vec<<<row_chunks(N), vec::RT, 0, s>>>(dX, y, table, tld, gate_off, mod_id, n_u, N, H, dY, part_dgate,
+                                                       part_db);
+    note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
+void rms_bwd_vec_launch(int mode, const __nv_bfloat16* dA, const float* X, const float* r, const float* table,
+                        int64_t tld, int sc_off, const int32_t* mod_id, int n_u, const float* g, int N, int H, float* dX,
+                        int accumulate, float* part_a, float* part_b, cudaStream_t s) {
+    if (mode == 0)
+        vec::rms_bwd_vec<0><<<row_chunks(N), vec::RT, 0, s>>>(dA, X, r, table, tld, sc_off, mod_id, n_u, g, N, H, dX,
+                                                            accumulate, part_a, part_b);
+    else
+        vec::rms_bwd_vec<1><<<row_chunks(N), vec::RT, 0, s>>>(dA, X, r, table, tld, sc_off, mod_id, n_u, g, N, H, dX,
+                                                            accumulate, part_a, part_b);
+    note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
+void postnorm_bwd_vec_launch(const float* dX, const __nv_bfloat16* co, const float* rc, const float* g, int N, int H,
+                             __nv_bfloat16* dco, float* part_dg, cudaStream_t s) {
+    vec::postnorm_bwd_vec<<<row_chunks(N), vec::RT, 0, s>>>(dX, co, rc, g, N, H, dco, part_dg);
+    note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
+void colsum_vec_launch(const __nv_bfloat16* Y, int64_t ld, int N, int C, float* part, cudaStream_t s) {
+    dim3 grid(row_chunks(N), (C / 8 + vec::RT - 1) / vec::RT);
+    vec::colsum_vec<<<grid, vec::RT, 0, s>>>(Y, ld, N, C, part);
+    note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
+
 }  // namespace mgv
