@@ -26,5 +26,6 @@ def _declare(L):
     P, I, I64, F, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_float, ctypes.c_double
     L.mgv_dev_gemm.argtypes = [I, P, I64, I, P, I64, I, I, I, I, P, I64, F, I, P]
     L.mgv_dev_gemm.restype = I
+    L.mgv_dev_set_gemm_mode.argtypes = [I]
     from . import capi
     capi.declare(L)

@@ -8,6 +8,7 @@
 namespace mgv {
 
 static std::atomic<int64_t> g_launches{0};
+int g_gemm_mode = 1;
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
@@ -72,6 +73,9 @@ extern "C" {
 
 // C[M,N] (fp32, ldc) (+)= alpha * sum_k A(m,k) B(n,k).  bf16 != 0: tcgen05 path on bf16
 // operands; else IEEE fp32 SIMT path on fp32 operands.  Returns 0 or a CUDA error code.
+// 0: 1-CTA tcgen05 GEMM (+ weight-tile multicast over CTA pairs), 1: CTA-pair (cta_group::2) GEMM
+void mgv_dev_set_gemm_mode(int mode) { g_gemm_mode = mode; }
+
 int mgv_dev_gemm(int bf16, const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb, int b_mn, int M, int N,
                  int K, float* C, int64_t ldc, float alpha, int accumulate, void* stream) {
     try {

@@ -96,6 +96,8 @@ void gemm_f32_launch(const Mat& A, const Mat& B, int M, int N, int K, const Epi&
 template <int BN, bool A_MN, bool B_MN, class Epi>
 void gemm_tc_launch(const Mat& A, const Mat& B, int M, int N, int K, const Epi& epi, cudaStream_t s) {
     using C = GemmCfg<BN>;
+    const int num_m = (M + kGemmBM - 1) / kGemmBM, num_n = (N + BN - 1) / BN;
+    const int MC = num_m >= 2 ? 2 : 1;  // B-tile multicast over CTA pairs
     CUtensorMap ta, tb;
     if (A_MN)
         make_tmap_bf16(&ta, A.p, M, K, A.ld, 64, kGemmBK);
@@ -104,18 +106,82 @@ void gemm_tc_launch(const Mat& A, const Mat& B, int M, int N, int K, const Epi& 
     if (B_MN)
         make_tmap_bf16(&tb, B.p, N, K, B.ld, 64, kGemmBK);
     else
-        make_tmap_bf16(&tb, B.p, K, N, B.ld, kGemmBK, BN);
-    auto kern = gemm_bf16_tc_kernel<BN, A_MN, B_MN, Epi>;
-    static bool attr_set = false;  // one per instantiation
+        make_tmap_bf16(&tb, B.p, K, N, B.ld, kGemmBK, BN / MC);
+    if (MC == 1) {
+        auto kern = gemm_bf16_tc_kernel<BN, A_MN, B_MN, 1, Epi>;
+        static bool attr_set = false;  // one per instantiation
+        if (!attr_set) {
+            MGV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+            attr_set = true;
+        }
+        const int tiles = num_m * num_n;
+        const int grid = tiles < num_sms() ? tiles : num_sms();
+        kern<<<grid, kGemmThreads, C::SMEM, s>>>(ta, tb, M, N, K, epi); ::mgv::note_launch();
+    } else {
+        auto kern = gemm_bf16_tc_kernel<BN, A_MN, B_MN, 2, Epi>;
+        static bool attr_set = false;
+        if (!attr_set) {
+            MGV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+            attr_set = true;
+        }
+        const int pair_tiles = ((num_m + 1) / 2) * num_n;
+        const int clusters = pair_tiles < num_sms() / 2 ? pair_tiles : num_sms() / 2;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2 * clusters);
+        cfg.blockDim = dim3(kGemmThreads);
+        cfg.dynamicSmemBytes = C::SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        MGV_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, epi));
+        note_launch();
+    }
+    MGV_CUDA(cudaGetLastError());
+}
+
+template <int BN, bool A_MN, bool B_MN, class Epi>
+void gemm_tc2_launch(const Mat& A, const Mat& B, int M, int N, int K, const Epi& epi, cudaStream_t s) {
+    using C = Gemm2Cfg<BN>;
+    CUtensorMap ta, tb;
+    if (A_MN)
+        make_tmap_bf16(&ta, A.p, M, K, A.ld, 64, kGemmBK);
+    else
+        make_tmap_bf16(&ta, A.p, K, M, A.ld, kGemmBK, kGemmBM);
+    if (B_MN)
+        make_tmap_bf16(&tb, B.p, N, K, B.ld, 64, kGemmBK);
+    else
+        make_tmap_bf16(&tb, B.p, K, N, B.ld, kGemmBK, BN / 2);
+    auto kern = gemm_bf16_tc2_kernel<BN, A_MN, B_MN, Epi>;
+    static bool attr_set = false;
     if (!attr_set) {
         MGV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         attr_set = true;
     }
-    const int tiles = ((M + kGemmBM - 1) / kGemmBM) * ((N + BN - 1) / BN);
-    const int grid = tiles < num_sms() ? tiles : num_sms();
-    kern<<<grid, kGemmThreads, C::SMEM, s>>>(ta, tb, M, N, K, epi); ::mgv::note_launch();
+    const int tiles = ((M + 2 * kGemmBM - 1) / (2 * kGemmBM)) * ((N + BN - 1) / BN);
+    const int clusters = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MGV_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, epi));
+    note_launch();
     MGV_CUDA(cudaGetLastError());
 }
+
+extern int g_gemm_mode;  // 0: 1-CTA (+B multicast pairs), 1: CTA-pair UMMA (default)
 
 // Dispatch on precision and operand majors.  bf16: A/B are __nv_bfloat16; fp32: float.
 template <class Epi>
@@ -127,6 +193,13 @@ void gemm(bool bf16, const Mat& A, const Mat& B, int M, int N, int K, const Epi&
         else if (!am && bm) gemm_f32_launch<false, true>(A, B, M, N, K, epi, s);
         else if (am && bm) gemm_f32_launch<true, true>(A, B, M, N, K, epi, s);
         else gemm_f32_launch<true, false>(A, B, M, N, K, epi, s);
+        return;
+    }
+    if (g_gemm_mode == 1 && M > kGemmBM) {
+        if (!am && !bm) gemm_tc2_launch<256, false, false>(A, B, M, N, K, epi, s);
+        else if (!am && bm) gemm_tc2_launch<256, false, true>(A, B, M, N, K, epi, s);
+        else if (am && bm) gemm_tc2_launch<256, true, true>(A, B, M, N, K, epi, s);
+        else throw std::runtime_error("gemm: MN-major A with K-major B is not used");
         return;
     }
     if (!am && !bm) gemm_tc_launch<256, false, false>(A, B, M, N, K, epi, s);

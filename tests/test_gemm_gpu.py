@@ -19,10 +19,17 @@ def run(bf16, A, a_mn, B, b_mn, M, N, K, alpha=1.0, acc=False, C=None):
     return C
 
 
+@pytest.mark.parametrize("mode", [1, 0])
 @pytest.mark.parametrize("bf16", [True, False])
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, True)])
-@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 520, 200), (1000, 96, 3456), (64, 700, 4096), (777, 333, 96)])
-def test_gemm(bf16, a_mn, b_mn, M, N, K):
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 520, 200), (1000, 96, 3456), (64, 700, 4096), (777, 333, 96),
+                                   (4096, 3456, 3456)])
+def test_gemm(mode, bf16, a_mn, b_mn, M, N, K):
+    """mode 1: CTA-pair (cta_group::2) kernel; mode 0: 1-CTA kernel with weight-tile multicast."""
+    from paper_2510_17519_b200._lib import lib
+    if not bf16 and mode == 0:
+        pytest.skip("fp32 path has a single kernel")
+    lib().mgv_dev_set_gemm_mode(mode)
     torch.manual_seed(M * 7 + N + K)
     dt = torch.bfloat16 if bf16 else torch.float32
     # storage shapes: K-major (rows, K) ; MN-major (K, rows); pad ld to a multiple of 8
