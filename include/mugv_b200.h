@@ -75,6 +75,13 @@ mgv_status mgv_ctx_set_stream(mgv_ctx* ctx, void* stream);
  * mgv_flow_step then all-reduces gradients (sum) and scales the loss by 1/global_batch. */
 mgv_status mgv_nccl_unique_id(uint8_t out[128]);
 mgv_status mgv_ctx_set_dp(mgv_ctx* ctx, int rank, int world, const uint8_t nccl_id[128]);
+/* Tensor parallel (Megatron head/column split); must precede mgv_params_upload.
+ * nccl_id != NULL: this context is TP rank `rank` of `size` over NCCL (one all-reduce per residual
+ * branch in forward and backward; sharded-parameter gradients are summed after the step, so every rank
+ * returns the full gradients).  nccl_id == NULL: all `size` ranks are emulated in this context (same
+ * shard views and partial sums, accumulated in place of the all-reduce) -- the single-GPU check of the
+ * sharded path.  `size` must divide heads.  Not combinable with mgv_ctx_set_dp. */
+mgv_status mgv_ctx_set_tp(mgv_ctx* ctx, int size, int rank, const uint8_t* nccl_id);
 
 /* Upload (or replace) the dit.* ParameterSet.  names/data/numel are n parallel arrays (any order). */
 mgv_status mgv_params_upload(mgv_ctx* ctx, const mgv_dit_cfg* cfg, int64_t n, const char* const* names,

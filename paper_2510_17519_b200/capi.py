@@ -67,6 +67,8 @@ def declare(L):
     L.mgv_nccl_unique_id.restype = I
     L.mgv_ctx_set_dp.argtypes = [P, I, I, P]
     L.mgv_ctx_set_dp.restype = I
+    L.mgv_ctx_set_tp.argtypes = [P, I, I, P]
+    L.mgv_ctx_set_tp.restype = I
     L.mgv_params_upload.argtypes = [P, ctypes.POINTER(mgv_dit_cfg), I64, P, P, P]
     L.mgv_params_upload.restype = I
     L.mgv_param_count.argtypes = [P]
@@ -107,7 +109,7 @@ def declare(L):
 
 # symbols include/mugv_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = ["mgv_ctx_create", "mgv_ctx_destroy", "mgv_last_error", "mgv_ctx_set_stream", "mgv_nccl_unique_id",
-           "mgv_ctx_set_dp", "mgv_params_upload", "mgv_param_count", "mgv_param_name", "mgv_param_numel",
+           "mgv_ctx_set_dp", "mgv_ctx_set_tp", "mgv_params_upload", "mgv_param_count", "mgv_param_name", "mgv_param_numel",
            "mgv_predict_velocity", "mgv_dit_forward", "mgv_flow_step", "mgv_flow_loss", "mgv_latent_rows",
            "mgv_rows_to_grid", "mgv_flow_step_device", "mgv_last_step_ms", "mgv_last_step_launches",
            "mgv_prof_enable", "mgv_prof_count", "mgv_prof_entry"]
@@ -216,6 +218,11 @@ class Context:
     def set_dp(self, rank: int, world: int, nccl_id: bytes):
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
         self._check(self._L.mgv_ctx_set_dp(self.h, rank, world, buf))
+
+    def set_tp(self, size: int, rank: int = 0, nccl_id: bytes | None = None):
+        """Megatron tensor parallelism (call before upload).  nccl_id None: emulate all ranks here."""
+        buf = None if nccl_id is None else (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
+        self._check(self._L.mgv_ctx_set_tp(self.h, size, rank, buf))
 
     @staticmethod
     def nccl_unique_id() -> bytes:

@@ -92,6 +92,9 @@ mgv_status mgv_nccl_unique_id(uint8_t out[128]) {
 mgv_status mgv_ctx_set_dp(mgv_ctx* ctx, int rank, int world, const uint8_t nccl_id[128]) {
     return guard(ctx, [&] { ctx->model->set_dp(rank, world, nccl_id); });
 }
+mgv_status mgv_ctx_set_tp(mgv_ctx* ctx, int size, int rank, const uint8_t* nccl_id) {
+    return guard(ctx, [&] { ctx->model->set_tp(size, rank, nccl_id); });
+}
 
 mgv_status mgv_params_upload(mgv_ctx* ctx, const mgv_dit_cfg* cfg, int64_t n, const char* const* names,
                              const double* const* data, const int64_t* numel) {

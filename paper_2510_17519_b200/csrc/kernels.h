@@ -56,11 +56,18 @@ void rms_gain(const float* X, int N, int H, const float* g, T* out, float* r, cu
 // X2 = X1 + rms(co) * g   (dit.cpp:305)
 template <class T>
 void postnorm_resid(const float* X1, const T* co, int N, int H, const float* g, float* X2, float* rc, cudaStream_t s);
+// Row strides of the q/k views the QK-norm kernels read and write (a tensor-parallel rank sees a
+// column slice of the full buffers): q at column 0 and k at column *_koff of rows with stride *_ld;
+// the inverse norms iq/ik at [n * i_ld + h].
+struct QKLayout {
+    int64_t in_ld, in_koff, out_ld, out_koff, i_ld;
+};
+inline QKLayout qk_layout_full(int64_t H, int heads) { return QKLayout{3 * H, H, 2 * H, H, heads}; }
 // per head: q <- rope(temp_h * q / |q|), k <- rope(k / |k|)   (dit.cpp:289-294)
-// qkv: (N, 3H) raw projection; qk_out: (N, 2H) rotated q | k; iq/ik: (N, heads) inverse norms
+// qkv: raw projection; qk_out: rotated q | k; iq/ik inverse norms.  Hl = heads * hd (this view's width)
 template <class T>
-void qk_norm_rope(const T* qkv, int N, int H, int heads, const float* temp, const float2* cs, T* qk_out, float* iq,
-                  float* ik, cudaStream_t s);
+void qk_norm_rope(const T* qkv, const QKLayout& L, int N, int Hl, int heads, const float* temp, const float2* cs,
+                  T* qk_out, float* iq, float* ik, cudaStream_t s);
 
 // ---- flow loss (flowtrain.cpp:22-42, autodiff.cpp:466-491)
 // part (row_chunks(N)) double partial sums of squared error over unmasked rows; dV = coef * (V - vt) on unmasked rows
@@ -93,10 +100,23 @@ void rms_gain_bwd(const T* dA, const float* X, const float* r, const float* g, i
 template <class T>
 void postnorm_bwd(const float* dX, const T* co, const float* rc, const float* g, int N, int H, T* dco, float* part_dg,
                   cudaStream_t s);
-// dqkv[:, 0:2H] holds d(rotated q | k) on entry, raw-projection grads on exit; part_dtemp[c][h]
+// dqkv (same layout as qkv: L.in_ld / L.in_koff) holds d(rotated q | k) on entry, raw-projection grads on
+// exit; part_dtemp[c][h]
 template <class T>
-void qk_norm_rope_bwd(T* dqkv, const T* qkv, int N, int H, int heads, const float* temp, const float2* cs,
-                      const float* iq, const float* ik, float* part_dtemp, cudaStream_t s);
+void qk_norm_rope_bwd(T* dqkv, const T* qkv, const QKLayout& L, int N, int Hl, int heads, const float* temp,
+                      const float2* cs, const float* iq, const float* ik, float* part_dtemp, cudaStream_t s);
+// ---- tensor-parallel glue (partial sums arrive in fp32 after the all-reduce)
+// y = part + bias ; Xout = Xin + y * gate[mod_id] ; y_out (T) kept for the gate gradient   (dit.cpp:297, 311)
+template <class T>
+void bias_gate_resid(const float* part, const float* bias, const float* table, int64_t tld, int gate_off,
+                     const int32_t* mod_id, const float* Xin, float* Xout, T* y_out, int N, int H, cudaStream_t s);
+// out = part + bias (bias may be null), as T
+template <class T>
+void bias_to(const float* part, const float* bias, T* out, int N, int H, cudaStream_t s);
+// rank-major row permutation of chunked weights: dst row (vr, c, j) <- src row (c, vr, j)
+// (C chunks of R rows, each split into P shards); inverse = 1 maps back
+void permute_shard_rows(const float* src, float* dst, int C, int R, int P, int64_t cols, int inverse, cudaStream_t s);
+void permute_shard_rows(const double* src, double* dst, int C, int R, int P, int64_t cols, int inverse, cudaStream_t s);
 // part[c][j] = sum over chunk rows of Y[i, j]   (bias gradients)
 template <class T>
 void colsum(const T* Y, int64_t ld, int N, int C, float* part, cudaStream_t s);

@@ -368,8 +368,9 @@ void postnorm_resid(const float* X1, const T* co, int N, int H, const float* g, 
 
 // One warp per (token, head, q|k); lane owns rotation pairs lane, lane+32, lane+64 (hd <= 192).
 template <class T>
-__global__ void __launch_bounds__(256) qk_norm_rope_kernel(const T* qkv, int N, int H, int heads, const float* temp,
-                                                           const float2* cs, T* qk, float* iq, float* ik) {
+__global__ void __launch_bounds__(256) qk_norm_rope_kernel(const T* qkv, QKLayout Lq, int N, int H, int heads,
+                                                           const float* temp, const float2* cs, T* qk, float* iq,
+                                                           float* ik) {
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
     const int lane = threadIdx.x & 31;
     const int hd = H / heads, P = hd / 2;
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(const T* qkv, int N, 
     const int which = static_cast<int>(gw % 2);  // 0 q, 1 k
     const int h = static_cast<int>((gw / 2) % heads);
     const int64_t n = gw / (2 * heads);
-    const T* src = qkv + n * 3 * H + which * H + h * hd;
+    const T* src = qkv + n * Lq.in_ld + which * Lq.in_koff + h * hd;
     float a[3], b[3];
     float ss = 0.0f;
 #pragma unroll
@@ -389,9 +390,9 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(const T* qkv, int N, 
     }
     ss = warp_sum(ss);
     const float iv = 1.0f / sqrtf(ss + static_cast<float>(kEps));  // autodiff.cpp:727
-    if (lane == 0) (which == 0 ? iq : ik)[n * heads + h] = iv;
+    if (lane == 0) (which == 0 ? iq : ik)[n * Lq.i_ld + h] = iv;
     const float sc = which == 0 ? iv * temp[h] : iv;  // mul_head_scalar on q (dit.cpp:292)
-    T* dst = qk + n * 2 * H + which * H + h * hd;
+    T* dst = qk + n * Lq.out_ld + which * Lq.out_koff + h * hd;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const int p = lane + 32 * c;
@@ -404,10 +405,10 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(const T* qkv, int N, 
     }
 }
 template <class T>
-void qk_norm_rope(const T* qkv, int N, int H, int heads, const float* temp, const float2* cs, T* qk, float* iq,
-                  float* ik, cudaStream_t s) {
+void qk_norm_rope(const T* qkv, const QKLayout& L, int N, int H, int heads, const float* temp, const float2* cs, T* qk,
+                  float* iq, float* ik, cudaStream_t s) {
     const int64_t warps = (int64_t)N * heads * 2;
-    qk_norm_rope_kernel<T><<<grid_for(warps * 32), 256, 0, s>>>(qkv, N, H, heads, temp, cs, qk, iq, ik); ::mgv::note_launch();
+    qk_norm_rope_kernel<T><<<grid_for(warps * 32), 256, 0, s>>>(qkv, L, N, H, heads, temp, cs, qk, iq, ik); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -685,9 +686,9 @@ void postnorm_bwd(const float* dX, const T* co, const float* rc, const float* g,
 
 // QK-norm + temperature + RoPE backward.  CTA = chunk of rows; warp w owns heads w, w+8, ... (deterministic dtemp).
 template <class T>
-__global__ void __launch_bounds__(256) qk_norm_rope_bwd_kernel(T* dqkv, const T* qkv, int N, int H, int heads,
-                                                               const float* temp, const float2* cs, const float* iq,
-                                                               const float* ik, float* part_dtemp) {
+__global__ void __launch_bounds__(256) qk_norm_rope_bwd_kernel(T* dqkv, const T* qkv, QKLayout Lq, int N, int H,
+                                                               int heads, const float* temp, const float2* cs,
+                                                               const float* iq, const float* ik, float* part_dtemp) {
     const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
     const int hd = H / heads, P = hd / 2;
     const int r0 = blockIdx.x * kRowsPerChunk, r1 = min(N, r0 + kRowsPerChunk);
@@ -696,9 +697,9 @@ __global__ void __launch_bounds__(256) qk_norm_rope_bwd_kernel(T* dqkv, const T*
         for (int n = r0; n < r1; ++n) {
 #pragma unroll 1
             for (int which = 0; which < 2; ++which) {
-                const T* x = qkv + (int64_t)n * 3 * H + which * H + h * hd;
-                T* dx = dqkv + (int64_t)n * 3 * H + which * H + h * hd;
-                const float iv = (which == 0 ? iq : ik)[(int64_t)n * heads + h];
+                const T* x = qkv + (int64_t)n * Lq.in_ld + which * Lq.in_koff + h * hd;
+                T* dx = dqkv + (int64_t)n * Lq.in_ld + which * Lq.in_koff + h * hd;
+                const float iv = (which == 0 ? iq : ik)[(int64_t)n * Lq.i_ld + h];
                 float xa[3], xb[3], ga[3], gb[3];
                 float dot = 0.0f, tdot = 0.0f;
 #pragma unroll
@@ -740,9 +741,9 @@ __global__ void __launch_bounds__(256) qk_norm_rope_bwd_kernel(T* dqkv, const T*
     }
 }
 template <class T>
-void qk_norm_rope_bwd(T* dqkv, const T* qkv, int N, int H, int heads, const float* temp, const float2* cs,
-                      const float* iq, const float* ik, float* part_dtemp, cudaStream_t s) {
-    qk_norm_rope_bwd_kernel<T><<<row_chunks(N), 256, 0, s>>>(dqkv, qkv, N, H, heads, temp, cs, iq, ik, part_dtemp); ::mgv::note_launch();
+void qk_norm_rope_bwd(T* dqkv, const T* qkv, const QKLayout& L, int N, int H, int heads, const float* temp,
+                      const float2* cs, const float* iq, const float* ik, float* part_dtemp, cudaStream_t s) {
+    qk_norm_rope_bwd_kernel<T><<<row_chunks(N), 256, 0, s>>>(dqkv, qkv, L, N, H, heads, temp, cs, iq, ik, part_dtemp); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -959,6 +960,69 @@ void fill_f32(float* p, int64_t n, float v, cudaStream_t s) {
 }
 
 // ============================================================ instantiations
+// ============================================================ tensor-parallel glue
+template <class T>
+__global__ void bias_gate_resid_kernel(const float* part, const float* bias, const float* table, int64_t tld,
+                                       int gate_off, const int32_t* mod_id, const float* Xin, float* Xout, T* y_out,
+                                       int N, int H) {
+    const int64_t n = (int64_t)N * H;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = e / H;
+        const int j = static_cast<int>(e - m * H);
+        const float y = part[e] + bias[j];
+        const float g = table[(int64_t)mod_id[m] * tld + gate_off + j];
+        Xout[e] = Xin[e] + y * g;  // same expression as EpiGateResid
+        y_out[e] = to_t<T>(y);
+    }
+}
+template <class T>
+void bias_gate_resid(const float* part, const float* bias, const float* table, int64_t tld, int gate_off,
+                     const int32_t* mod_id, const float* Xin, float* Xout, T* y_out, int N, int H, cudaStream_t s) {
+    bias_gate_resid_kernel<T><<<grid_for((int64_t)N * H), 256, 0, s>>>(part, bias, table, tld, gate_off, mod_id, Xin,
+                                                                         Xout, y_out, N, H);
+    ::mgv::note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
+template <class T>
+__global__ void bias_to_kernel(const float* part, const float* bias, T* out, int N, int H) {
+    const int64_t n = (int64_t)N * H;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        out[e] = to_t<T>(part[e] + (bias ? bias[e % H] : 0.0f));
+}
+template <class T>
+void bias_to(const float* part, const float* bias, T* out, int N, int H, cudaStream_t s) {
+    bias_to_kernel<T><<<grid_for((int64_t)N * H), 256, 0, s>>>(part, bias, out, N, H);
+    ::mgv::note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
+// dst row (v, c, j) <- src row (c, v, j) for C chunks of R = P * Rs rows (inverse swaps the roles)
+template <class E>
+__global__ void permute_shard_rows_kernel(const E* src, E* dst, int C, int R, int P, int64_t cols, int inverse) {
+    const int Rs = R / P;
+    const int64_t n = (int64_t)C * R * cols;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = e / cols, col = e - row * cols;
+        const int c = static_cast<int>(row / R), rr = static_cast<int>(row % R);
+        const int v = rr / Rs, j = rr % Rs;
+        const int64_t rank_major = ((int64_t)v * C + c) * Rs + j;  // row index in the rank-major layout
+        if (inverse)
+            dst[row * cols + col] = src[rank_major * cols + col];
+        else
+            dst[rank_major * cols + col] = src[row * cols + col];
+    }
+}
+void permute_shard_rows(const float* src, float* dst, int C, int R, int P, int64_t cols, int inverse, cudaStream_t s) {
+    permute_shard_rows_kernel<float><<<grid_for((int64_t)C * R * cols), 256, 0, s>>>(src, dst, C, R, P, cols, inverse);
+    ::mgv::note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
+void permute_shard_rows(const double* src, double* dst, int C, int R, int P, int64_t cols, int inverse,
+                        cudaStream_t s) {
+    permute_shard_rows_kernel<double><<<grid_for((int64_t)C * R * cols), 256, 0, s>>>(src, dst, C, R, P, cols, inverse);
+    ::mgv::note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
+
 #define INST(T)                                                                                                       \
     template void prep_flow_sample<T>(const double*, const double*, const int32_t*, int, int, double, int, T*, float*, \
                                       uint8_t*, int32_t*, cudaStream_t);                                              \
@@ -968,8 +1032,11 @@ void fill_f32(float* p, int64_t n, float v, cudaStream_t s) {
                              cudaStream_t);                                                                           \
     template void rms_gain<T>(const float*, int, int, const float*, T*, float*, cudaStream_t);                        \
     template void postnorm_resid<T>(const float*, const T*, int, int, const float*, float*, float*, cudaStream_t);    \
-    template void qk_norm_rope<T>(const T*, int, int, int, const float*, const float2*, T*, float*, float*,           \
-                                  cudaStream_t);                                                                      \
+    template void qk_norm_rope<T>(const T*, const QKLayout&, int, int, int, const float*, const float2*, T*, float*,  \
+                                  float*, cudaStream_t);                                                              \
+    template void bias_gate_resid<T>(const float*, const float*, const float*, int64_t, int, const int32_t*,          \
+                                     const float*, float*, T*, int, int, cudaStream_t);                               \
+    template void bias_to<T>(const float*, const float*, T*, int, int, cudaStream_t);                                 \
     template void flow_loss_fwd<T>(const float*, const float*, const uint8_t*, int, int, double*, cudaStream_t);      \
     template void flow_loss_bwd<T>(const float*, const float*, const uint8_t*, int, int, float, const int*, T*,       \
                                    cudaStream_t);                                                                    \
@@ -981,8 +1048,8 @@ void fill_f32(float* p, int64_t n, float v, cudaStream_t s) {
                                   cudaStream_t);                                                                      \
     template void postnorm_bwd<T>(const float*, const T*, const float*, const float*, int, int, T*, float*,           \
                                   cudaStream_t);                                                                      \
-    template void qk_norm_rope_bwd<T>(T*, const T*, int, int, int, const float*, const float2*, const float*,         \
-                                      const float*, float*, cudaStream_t);                                            \
+    template void qk_norm_rope_bwd<T>(T*, const T*, const QKLayout&, int, int, int, const float*, const float2*,      \
+                                      const float*, const float*, float*, cudaStream_t);                              \
     template void colsum<T>(const T*, int64_t, int, int, float*, cudaStream_t);
 INST(float)
 INST(__nv_bfloat16)

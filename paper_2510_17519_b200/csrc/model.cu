@@ -81,6 +81,9 @@ struct Model::WS {
     double *dg, *dgb, *loss_part, *scal;
     int* cnt;
     int q_splits_x = 1;
+    // tensor parallel: fp32 partial sums of the row-parallel GEMMs (the all-reduce buffer)
+    int tp = 1;
+    float* tpp = nullptr;
 };
 
 namespace {
@@ -157,6 +160,7 @@ void layout_ws(Model::WS& w, S& a, const Cfg& c, bool grads) {
     w.Y = a.takeT(N * H, e);
     w.V = a.template take<float>(N * D);
     w.dV = a.takeT(N * D, e);
+    w.tpp = w.tp > 1 ? a.template take<float>(N * H) : nullptr;
     w.loss_part = a.template take<double>(row_chunks(N) + 1024);
     w.scal = a.template take<double>(8);
     w.cnt = a.template take<int>(8);
@@ -260,6 +264,7 @@ Model::~Model() {
     }
     if (grad_buf_) cudaFree(grad_buf_);
     if (comm_) ncclCommDestroy(comm_);
+    if (tp_comm_) ncclCommDestroy(tp_comm_);
     delete ws_;
 }
 
@@ -276,6 +281,75 @@ void Model::set_dp(int rank, int world, const uint8_t id[128]) {
     std::memcpy(&uid, id, sizeof(uid));
     MGV_CUDA(cudaSetDevice(device_));
     MGV_NCCL(ncclCommInitRank(&comm_, world, uid, rank));
+}
+
+void Model::set_tp(int size, int rank, const uint8_t* id) {
+    if (size < 1 || rank < 0 || rank >= size) throw InputError("bad tensor-parallel rank/size");
+    if (have_params_ && size != tp_) throw ConfigError("set_tp must precede the parameter upload");
+    if (size > 1 && world_ > 1) throw ConfigError("data and tensor parallelism cannot be combined in one context");
+    if (tp_comm_) {
+        ncclCommDestroy(tp_comm_);
+        tp_comm_ = nullptr;
+    }
+    tp_ = size;
+    tp_rank_ = id ? rank : 0;
+    tp_virtual_ = id == nullptr;
+    if (size == 1 || !id) return;
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    MGV_CUDA(cudaSetDevice(device_));
+    MGV_NCCL(ncclCommInitRank(&tp_comm_, size, uid, rank));
+}
+
+std::vector<int> Model::tp_ranks() const {
+    std::vector<int> r;
+    if (tp_virtual_)
+        for (int v = 0; v < tp_; ++v) r.push_back(v);
+    else
+        r.push_back(tp_rank_);
+    return r;
+}
+
+void Model::tp_allreduce(float* buf, int64_t n, cudaStream_t s) {
+    if (tp_ == 1 || tp_virtual_) return;  // emulated ranks accumulate the partials in place
+    prof_.begin("tp_allreduce", s);
+    MGV_NCCL(ncclAllReduce(buf, buf, n, ncclFloat, ncclSum, tp_comm_, s));
+    prof_.end(s);
+}
+
+// Sharded parameters: rank r computes only its rows / columns of these gradients, the rest
+// of its replicated gradient buffer stays zero, so a sum over TP ranks assembles the full gradient.
+static bool is_tp_sharded(const std::string& n) {
+    static const char* sh[] = {"attn.qkv.w", "attn.qkv.b", "attn.temp",  "attn.out.w", "xattn.q.w", "xattn.q.b",
+                               "xattn.kv.w", "xattn.kv.b", "xattn.out.w", "ffn.in.w",  "ffn.in.b",  "ffn.out.w"};
+    if (n.rfind("dit.blk.", 0) != 0) return false;
+    for (const char* m : sh) {
+        const size_t l = std::strlen(m);
+        if (n.size() >= l && n.compare(n.size() - l, l, m) == 0 && n[n.size() - l - 1] == '.') return true;
+    }
+    return false;
+}
+void Model::tp_allreduce_grads(cudaStream_t s) {
+    if (tp_ == 1 || tp_virtual_) return;
+    prof_.begin("tp_allreduce", s);
+    MGV_NCCL(ncclGroupStart());
+    for (DevParam* p : sorted_)
+        if (is_tp_sharded(p->name)) MGV_NCCL(ncclAllReduce(p->grad, p->grad, p->numel, ncclFloat, ncclSum, tp_comm_, s));
+    MGV_NCCL(ncclGroupEnd());
+    prof_.end(s);
+}
+
+// Chunked row layouts re-ordered rank-major under TP, so each rank's rows of every chunk are
+// contiguous (qkv: chunks q|k|v, expansion.cpp:143-180 chunk layout; xattn.kv: k|v).
+static int tp_row_chunks(const std::string& n) {
+    auto ends = [&](const char* m) {
+        const size_t l = std::strlen(m);
+        return n.size() >= l && n.compare(n.size() - l, l, m) == 0;
+    };
+    if (n.rfind("dit.blk.", 0) != 0) return 0;
+    if (ends(".attn.qkv.w") || ends(".attn.qkv.b")) return 3;
+    if (ends(".xattn.kv.w") || ends(".xattn.kv.b")) return 2;
+    return 0;
 }
 
 static bool is_matrix(const std::string& n) {
@@ -304,6 +378,8 @@ static int grid_of(int64_t n) { return static_cast<int>(std::min<int64_t>((n + 2
 void Model::upload(const Cfg& cfg, int64_t n, const char* const* names, const double* const* data,
                    const int64_t* numel) {
     validate_cfg(cfg);
+    if (tp_ > 1 && (cfg.heads % tp_ != 0 || (cfg.hidden / tp_) % 8 != 0))
+        throw ConfigError("tensor parallel size must divide heads, with hidden/size a multiple of 8");
     MGV_CUDA(cudaSetDevice(device_));
     const int64_t H = cfg.hidden, D = cfg.D();
     // expected dit.* names and shapes (dit.cpp:143-183)
@@ -386,7 +462,7 @@ void Model::upload(const Cfg& cfg, int64_t n, const char* const* names, const do
     double* staging = nullptr;
     int64_t stage_n = 0;
     for (auto& kv : params_) stage_n = std::max(stage_n, kv.second.numel);
-    MGV_CUDA(cudaMalloc(&staging, sizeof(double) * stage_n));
+    MGV_CUDA(cudaMalloc(&staging, sizeof(double) * stage_n * (tp_ > 1 ? 2 : 1)));
     for (auto& kv : params_) {
         DevParam& p = kv.second;
         const int64_t gi = given[p.name];
@@ -394,7 +470,12 @@ void Model::upload(const Cfg& cfg, int64_t n, const char* const* names, const do
             throw DimensionError("parameter " + p.name + " has " + std::to_string(numel[gi]) + " elements, expected " +
                                  std::to_string(p.numel));
         MGV_CUDA(cudaMemcpyAsync(staging, data[gi], sizeof(double) * p.numel, cudaMemcpyHostToDevice, stream_));
-        f64_to_f32_bf16<<<grid_of(p.numel), 256, 0, stream_>>>(staging, p.numel, p.f32, p.bf); ::mgv::note_launch();
+        const double* src = staging;
+        if (const int C = tp_ > 1 ? tp_row_chunks(p.name) : 0) {
+            permute_shard_rows(staging, staging + stage_n, C, static_cast<int>(H), tp_, p.numel / (C * H), 0, stream_);
+            src = staging + stage_n;
+        }
+        f64_to_f32_bf16<<<grid_of(p.numel), 256, 0, stream_>>>(src, p.numel, p.f32, p.bf); ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
     }
     MGV_CUDA(cudaStreamSynchronize(stream_));
@@ -445,6 +526,7 @@ static void attention_bwd(bool bf16, const AttnBwdProblem& p, cudaStream_t s) {
 // ------------------------------------------------------------------ block forward (dit.cpp:279-313)
 template <class T>
 void Model::block_fwd(int i, int64_t N) {
+    if (tp_ > 1) return block_fwd_tp<T>(i, N);
     WS& w = *ws_;
     const bool bf = bf16_;
     cudaStream_t s = stream_;
@@ -459,7 +541,7 @@ void Model::block_fwd(int i, int64_t N) {
     rms_mod<T>(Xin, n, H, tab, tld, 0, H, w.mod_id, tp<T>(b.a), b.r0, s);
     gemm(bf, KM(b.a, H), KM(W(blk(i, "attn.qkv.w")), H), n, 3 * H, H,
          EpiStore<T>{tp<T>(b.qkv), 3 * H, P(blk(i, "attn.qkv.b")).f32, 1.0f, n, int(3 * H)}, s);  // dit.cpp:288
-    qk_norm_rope<T>(tp<T>(b.qkv), n, H, nh, P(blk(i, "attn.temp")).f32, w.cs, tp<T>(b.qk), b.iq, b.ik, s);  // :289-294
+    qk_norm_rope<T>(tp<T>(b.qkv), qk_layout_full(H, nh), n, H, nh, P(blk(i, "attn.temp")).f32, w.cs, tp<T>(b.qk), b.iq, b.ik, s);  // :289-294
     AttnProblem ap{b.qk, 2 * H, off<T>(b.qk, H), 2 * H, off<T>(b.qkv, 2 * H), 3 * H, b.O, H, b.lse,
                    n, n, int(nh), int(hd)};
     prof_.begin("attn_fwd", s);
@@ -498,6 +580,7 @@ void Model::block_fwd(int i, int64_t N) {
 // ------------------------------------------------------------------ block backward
 template <class T>
 void Model::block_bwd(int i, int64_t N) {
+    if (tp_ > 1) return block_bwd_tp<T>(i, N);
     WS& w = *ws_;
     const bool bf = bf16_;
     cudaStream_t s = stream_;
@@ -560,7 +643,7 @@ void Model::block_bwd(int i, int64_t N) {
     ab.f.lse_ld = (N + 63) / 64 * 64;
     attention_bwd<T>(bf, ab, s);
     prof_.end(s);
-    qk_norm_rope_bwd<T>(tp<T>(w.sB), tp<T>(b.qkv), n, H, nh, P(blk(i, "attn.temp")).f32, w.cs, b.iq, b.ik, w.part1, s);
+    qk_norm_rope_bwd<T>(tp<T>(w.sB), tp<T>(b.qkv), qk_layout_full(H, nh), n, H, nh, P(blk(i, "attn.temp")).f32, w.cs, b.iq, b.ik, w.part1, s);
     reduce_chunks(w.part1, chunks, nh, G(blk(i, "attn.temp")), 1.0f, 1, s);
     colsum<T>(tp<T>(w.sB), 3 * H, n, 3 * H, w.part1, s);
     reduce_chunks(w.part1, chunks, 3 * H, G(blk(i, "attn.qkv.b")), 1.0f, 1, s);
@@ -570,6 +653,214 @@ void Model::block_bwd(int i, int64_t N) {
     reduce_chunks_grouped(w.part1, chunks, nu, H, dm, 6 * H, 1.0f, 0, s);      // d sh1
     reduce_chunks_grouped(w.part2, chunks, nu, H, dm + H, 6 * H, 1.0f, 0, s);  // d sc1
     // ---- shared modulation head (dit.cpp:280-283)
+    modulation_bwd(dm, w.gb[i], P("dit.mod.w").f32, nu, H, G("dit.mod.w"), G("dit.mod.b"), w.dgb, s);
+    gscale_bwd(w.dgb, w.g, P(blk(i, "gscale")).f32, nu, H, G(blk(i, "gscale")), w.dg, s);
+}
+
+// ------------------------------------------------------------------ tensor-parallel block
+// Megatron head/column split: rank r owns heads [r nh/P, (r+1) nh/P) of the self- and cross-attention
+// (its rows of the rank-major qkv / kv weights and of xattn.q, its entries of attn.temp) and rows
+// [r 4H/P, (r+1) 4H/P) of ffn.in; attn.out / xattn.out / ffn.out are row-parallel (column slices), so
+// each residual branch ends in one all-reduce of an N x H fp32 partial.  Norms, gains, modulation and
+// the heads are replicated.  A rank's slices are views (pointer offset + leading dimension) into the
+// activation and weight buffers, so the emulated ranks of one process share the full-size buffers.
+template <class T>
+void Model::block_fwd_tp(int i, int64_t N) {
+    WS& w = *ws_;
+    const bool bf = bf16_;
+    cudaStream_t s = stream_;
+    const int64_t H = cfg_.H(), nh = cfg_.heads, hd = cfg_.hd(), L = w.L, td = cfg_.text_dim;
+    const int64_t Hr = H / tp_, nhr = nh / tp_, Fr = 4 * H / tp_, lld = (N + 63) / 64 * 64;
+    Blk& b = w.blk[w.grads ? i : 0];
+    const float* Xin = w.X[w.grads ? i : (i % 2)];
+    float* Xout = w.X[w.grads ? i + 1 : ((i + 1) % 2)];
+    const float* tab = w.table[i];
+    const int64_t tld = 6 * H;
+    const int n = static_cast<int>(N);
+    const std::vector<int> ranks = tp_ranks();
+    auto acc = [&](size_t k) { return tp_virtual_ && k > 0 ? 1 : 0; };
+    float* part = w.tpp;
+    // self-attention (dit.cpp:287-297): column-parallel qkv, local heads, row-parallel out-proj
+    rms_mod<T>(Xin, n, H, tab, tld, 0, H, w.mod_id, tp<T>(b.a), b.r0, s);
+    for (size_t k = 0; k < ranks.size(); ++k) {
+        const int64_t r = ranks[k];
+        void* qkv_r = off<T>(b.qkv, r * 3 * Hr);
+        void* qk_r = off<T>(b.qk, r * 2 * Hr);
+        gemm(bf, KM(b.a, H), KM(off<T>(W(blk(i, "attn.qkv.w")), r * 3 * Hr * H), H), n, int(3 * Hr), H,
+             EpiStore<T>{tp<T>(qkv_r), 3 * H, P(blk(i, "attn.qkv.b")).f32 + r * 3 * Hr, 1.0f, n, int(3 * Hr)}, s);
+        qk_norm_rope<T>(tp<T>(qkv_r), QKLayout{3 * H, Hr, 2 * H, Hr, nh}, n, int(Hr), int(nhr),
+                        P(blk(i, "attn.temp")).f32 + r * nhr, w.cs, tp<T>(qk_r), b.iq + r * nhr, b.ik + r * nhr, s);
+        AttnProblem ap{qk_r, 2 * H, off<T>(qk_r, Hr), 2 * H, off<T>(qkv_r, 2 * Hr), 3 * H, off<T>(b.O, r * Hr), H,
+                       b.lse + r * nhr * lld, n, n, int(nhr), int(hd)};
+        ap.lse_ld = lld;
+        prof_.begin("attn_fwd", s);
+        attention_fwd<T>(bf, ap, s);
+        prof_.end(s);
+        gemm(bf, KM(off<T>(b.O, r * Hr), H), KM(off<T>(W(blk(i, "attn.out.w")), r * Hr), H), n, H, int(Hr),
+             EpiF32{part, H, nullptr, 1.0f, acc(k), n, int(H)}, s);
+    }
+    tp_allreduce(part, N * H, s);
+    bias_gate_resid<T>(part, P(blk(i, "attn.out.b")).f32, tab, tld, int(2 * H), w.mod_id, Xin, b.X1, tp<T>(b.ao), n,
+                       int(H), s);
+    // cross-attention (dit.cpp:300-305)
+    rms_gain<T>(b.X1, n, H, P(blk(i, "xattn.prenorm.g")).f32, tp<T>(b.cn), b.r1, s);
+    const float xscale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd)));
+    for (size_t k = 0; k < ranks.size(); ++k) {
+        const int64_t r = ranks[k];
+        void* kv_r = off<T>(b.kv, r * 2 * Hr);
+        gemm(bf, KM(b.cn, H), KM(off<T>(W(blk(i, "xattn.q.w")), r * Hr * H), H), n, int(Hr), H,
+             EpiStore<T>{tp<T>(off<T>(b.cqs, r * Hr)), H, P(blk(i, "xattn.q.b")).f32 + r * Hr, xscale, n, int(Hr)}, s);
+        gemm(bf, KM(w.text, td), KM(off<T>(W(blk(i, "xattn.kv.w")), r * 2 * Hr * td), td), int(L), int(2 * Hr), td,
+             EpiStore<T>{tp<T>(kv_r), 2 * H, P(blk(i, "xattn.kv.b")).f32 + r * 2 * Hr, 1.0f, int(L), int(2 * Hr)}, s);
+        AttnProblem xp{off<T>(b.cqs, r * Hr), H, kv_r, 2 * H, off<T>(kv_r, Hr), 2 * H, off<T>(b.Ox, r * Hr), H,
+                       b.lse_x + r * nhr * lld, n, int(L), int(nhr), int(hd)};
+        xp.lse_ld = lld;
+        prof_.begin("xattn_fwd", s);
+        attention_fwd<T>(bf, xp, s);
+        prof_.end(s);
+        gemm(bf, KM(off<T>(b.Ox, r * Hr), H), KM(off<T>(W(blk(i, "xattn.out.w")), r * Hr), H), n, H, int(Hr),
+             EpiF32{part, H, nullptr, 1.0f, acc(k), n, int(H)}, s);
+    }
+    tp_allreduce(part, N * H, s);
+    bias_to<T>(part, P(blk(i, "xattn.out.b")).f32, tp<T>(b.co), n, int(H), s);
+    postnorm_resid<T>(b.X1, tp<T>(b.co), n, H, P(blk(i, "xattn.postnorm.g")).f32, b.X2, b.rc, s);
+    // feed-forward (dit.cpp:308-311): column-parallel ffn.in, row-parallel ffn.out
+    rms_mod<T>(b.X2, n, H, tab, tld, 3 * H, 4 * H, w.mod_id, tp<T>(b.f), b.r2, s);
+    for (size_t k = 0; k < ranks.size(); ++k) {
+        const int64_t r = ranks[k];
+        gemm(bf, KM(b.f, H), KM(off<T>(W(blk(i, "ffn.in.w")), r * Fr * H), H), n, int(Fr), H,
+             EpiBiasSilu<T>{tp<T>(off<T>(b.z, r * Fr)), tp<T>(off<T>(b.h, r * Fr)), 4 * H,
+                            P(blk(i, "ffn.in.b")).f32 + r * Fr, n, int(Fr)},
+             s);
+        gemm(bf, KM(off<T>(b.h, r * Fr), 4 * H), KM(off<T>(W(blk(i, "ffn.out.w")), r * Fr), 4 * H), n, H, int(Fr),
+             EpiF32{part, H, nullptr, 1.0f, acc(k), n, int(H)}, s);
+    }
+    tp_allreduce(part, N * H, s);
+    bias_gate_resid<T>(part, P(blk(i, "ffn.out.b")).f32, tab, tld, int(5 * H), w.mod_id, b.X2, Xout, tp<T>(b.ff), n,
+                       int(H), s);
+}
+
+template <class T>
+void Model::block_bwd_tp(int i, int64_t N) {
+    WS& w = *ws_;
+    const bool bf = bf16_;
+    cudaStream_t s = stream_;
+    const int64_t H = cfg_.H(), nh = cfg_.heads, hd = cfg_.hd(), L = w.L, td = cfg_.text_dim;
+    const int64_t Hr = H / tp_, nhr = nh / tp_, Fr = 4 * H / tp_, lld = (N + 63) / 64 * 64;
+    const int n = static_cast<int>(N), nu = w.n_u, chunks = row_chunks(n);
+    Blk& b = w.blk[i];
+    const float* Xin = w.X[i];
+    const float* tab = w.table[i];
+    const int64_t tld = 6 * H;
+    float* dX = w.dX;
+    float* dm = w.dm;
+    const std::vector<int> ranks = tp_ranks();
+    auto acc = [&](size_t k) { return tp_virtual_ && k > 0 ? 1 : 0; };
+    float* part = w.tpp;
+    // ---- FFN (dit.cpp:308-311)
+    gate_bwd<T>(dX, tp<T>(b.ff), tab, tld, 5 * H, w.mod_id, nu, n, H, tp<T>(w.s1), w.part1, w.part2, s);
+    reduce_chunks_grouped(w.part1, chunks, nu, H, dm + 5 * H, 6 * H, 1.0f, 0, s);  // d gt2
+    reduce_chunks(w.part2, chunks, H, G(blk(i, "ffn.out.b")), 1.0f, 1, s);
+    for (size_t k = 0; k < ranks.size(); ++k) {
+        const int64_t r = ranks[k];
+        void* dz_r = off<T>(w.sA, r * Fr);
+        gemm(bf, MN(w.s1, H), MN(off<T>(b.h, r * Fr), 4 * H), H, int(Fr), n,
+             EpiF32{G(blk(i, "ffn.out.w")) + r * Fr, 4 * H, nullptr, 1.0f, 1, int(H), int(Fr)}, s);
+        gemm(bf, KM(w.s1, H), MN(off<T>(W(blk(i, "ffn.out.w")), r * Fr), 4 * H), n, int(Fr), H,
+             EpiSiluBwd<T>{tp<T>(dz_r), tp<T>(off<T>(b.z, r * Fr)), 4 * H, n, int(Fr)}, s);
+        colsum<T>(tp<T>(dz_r), 4 * H, n, int(Fr), w.part1, s);
+        reduce_chunks(w.part1, chunks, int(Fr), G(blk(i, "ffn.in.b")) + r * Fr, 1.0f, 1, s);
+        gemm(bf, MN(dz_r, 4 * H), MN(b.f, H), int(Fr), H, n,
+             EpiF32{G(blk(i, "ffn.in.w")) + r * Fr * H, H, nullptr, 1.0f, 1, int(Fr), int(H)}, s);
+        gemm(bf, KM(dz_r, 4 * H), MN(off<T>(W(blk(i, "ffn.in.w")), r * Fr * H), H), n, H, int(Fr),
+             EpiF32{part, H, nullptr, 1.0f, acc(k), n, int(H)}, s);  // df partial
+    }
+    tp_allreduce(part, N * H, s);
+    convert_f32<T>(part, N * H, tp<T>(w.s1), s);
+    rms_mod_bwd<T>(tp<T>(w.s1), b.X2, b.r2, tab, tld, 3 * H, 4 * H, w.mod_id, nu, n, H, dX, w.part1, w.part2, s);
+    reduce_chunks_grouped(w.part1, chunks, nu, H, dm + 3 * H, 6 * H, 1.0f, 0, s);  // d sh2
+    reduce_chunks_grouped(w.part2, chunks, nu, H, dm + 4 * H, 6 * H, 1.0f, 0, s);  // d sc2
+    // ---- cross-attention (dit.cpp:300-305)
+    postnorm_bwd<T>(dX, tp<T>(b.co), b.rc, P(blk(i, "xattn.postnorm.g")).f32, n, H, tp<T>(w.s1), w.part1, s);
+    reduce_chunks(w.part1, chunks, H, G(blk(i, "xattn.postnorm.g")), 1.0f, 1, s);
+    colsum<T>(tp<T>(w.s1), H, n, H, w.part1, s);
+    reduce_chunks(w.part1, chunks, H, G(blk(i, "xattn.out.b")), 1.0f, 1, s);
+    for (size_t k = 0; k < ranks.size(); ++k) {  // all ranks read the full dco (s1) before dq overwrites it
+        const int64_t r = ranks[k];
+        gemm(bf, MN(w.s1, H), MN(off<T>(b.Ox, r * Hr), H), H, int(Hr), n,
+             EpiF32{G(blk(i, "xattn.out.w")) + r * Hr, H, nullptr, 1.0f, 1, int(H), int(Hr)}, s);
+        gemm(bf, KM(w.s1, H), MN(off<T>(W(blk(i, "xattn.out.w")), r * Hr), H), n, int(Hr), H,
+             EpiStore<T>{tp<T>(off<T>(w.s2, r * Hr)), H, nullptr, 1.0f, n, int(Hr)}, s);
+    }
+    const float xscale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd)));
+    for (size_t k = 0; k < ranks.size(); ++k) {
+        const int64_t r = ranks[k];
+        void* kv_r = off<T>(b.kv, r * 2 * Hr);
+        void* dkv_r = off<T>(w.dkv, r * 2 * Hr);
+        void* dq_r = off<T>(w.s1, r * Hr);
+        AttnBwdProblem xb{AttnProblem{off<T>(b.cqs, r * Hr), H, kv_r, 2 * H, off<T>(kv_r, Hr), 2 * H,
+                                      off<T>(b.Ox, r * Hr), H, b.lse_x + r * nhr * lld, n, int(L), int(nhr), int(hd)},
+                          off<T>(w.s2, r * Hr), H, w.Dvec + r * nhr * lld, dq_r, H, dkv_r, 2 * H, off<T>(dkv_r, Hr),
+                          2 * H, w.dkv_part + r * (int64_t)w.q_splits_x * nhr * L * 2 * hd, w.q_splits_x};
+        xb.f.lse_ld = lld;
+        prof_.begin("xattn_bwd", s);
+        attention_bwd<T>(bf, xb, s);
+        prof_.end(s);
+        gemm(bf, MN(dkv_r, 2 * H), MN(w.text, td), int(2 * Hr), td, int(L),
+             EpiF32{G(blk(i, "xattn.kv.w")) + r * 2 * Hr * td, td, nullptr, 1.0f, 1, int(2 * Hr), int(td)}, s);
+        colsum<T>(tp<T>(dkv_r), 2 * H, int(L), int(2 * Hr), w.part1, s);
+        reduce_chunks(w.part1, row_chunks(int(L)), int(2 * Hr), G(blk(i, "xattn.kv.b")) + r * 2 * Hr, 1.0f, 1, s);
+        colsum<T>(tp<T>(dq_r), H, n, int(Hr), w.part1, s);
+        reduce_chunks(w.part1, chunks, int(Hr), G(blk(i, "xattn.q.b")) + r * Hr, xscale, 1, s);
+        gemm(bf, MN(dq_r, H), MN(b.cn, H), int(Hr), H, n,
+             EpiF32{G(blk(i, "xattn.q.w")) + r * Hr * H, H, nullptr, xscale, 1, int(Hr), int(H)}, s);
+        gemm(bf, KM(dq_r, H), MN(off<T>(W(blk(i, "xattn.q.w")), r * Hr * H), H), n, H, int(Hr),
+             EpiF32{part, H, nullptr, xscale, acc(k), n, int(H)}, s);  // dcn partial
+    }
+    tp_allreduce(part, N * H, s);
+    convert_f32<T>(part, N * H, tp<T>(w.s2), s);
+    rms_gain_bwd<T>(tp<T>(w.s2), b.X1, b.r1, P(blk(i, "xattn.prenorm.g")).f32, n, H, dX, 1, w.part1, s);
+    reduce_chunks(w.part1, chunks, H, G(blk(i, "xattn.prenorm.g")), 1.0f, 1, s);
+    // ---- self-attention (dit.cpp:287-297)
+    gate_bwd<T>(dX, tp<T>(b.ao), tab, tld, 2 * H, w.mod_id, nu, n, H, tp<T>(w.s1), w.part1, w.part2, s);
+    reduce_chunks_grouped(w.part1, chunks, nu, H, dm + 2 * H, 6 * H, 1.0f, 0, s);  // d gt1
+    reduce_chunks(w.part2, chunks, H, G(blk(i, "attn.out.b")), 1.0f, 1, s);
+    for (size_t k = 0; k < ranks.size(); ++k) {
+        const int64_t r = ranks[k];
+        gemm(bf, MN(w.s1, H), MN(off<T>(b.O, r * Hr), H), H, int(Hr), n,
+             EpiF32{G(blk(i, "attn.out.w")) + r * Hr, H, nullptr, 1.0f, 1, int(H), int(Hr)}, s);
+        gemm(bf, KM(w.s1, H), MN(off<T>(W(blk(i, "attn.out.w")), r * Hr), H), n, int(Hr), H,
+             EpiStore<T>{tp<T>(off<T>(w.s2, r * Hr)), H, nullptr, 1.0f, n, int(Hr)}, s);
+    }
+    for (size_t k = 0; k < ranks.size(); ++k) {
+        const int64_t r = ranks[k];
+        void* qkv_r = off<T>(b.qkv, r * 3 * Hr);
+        void* qk_r = off<T>(b.qk, r * 2 * Hr);
+        void* dqkv_r = off<T>(w.sB, r * 3 * Hr);
+        AttnBwdProblem ab{AttnProblem{qk_r, 2 * H, off<T>(qk_r, Hr), 2 * H, off<T>(qkv_r, 2 * Hr), 3 * H,
+                                      off<T>(b.O, r * Hr), H, b.lse + r * nhr * lld, n, n, int(nhr), int(hd)},
+                          off<T>(w.s2, r * Hr), H, w.Dvec + r * nhr * lld, dqkv_r, 3 * H, off<T>(dqkv_r, Hr), 3 * H,
+                          off<T>(dqkv_r, 2 * Hr), 3 * H, nullptr, 1};
+        ab.f.lse_ld = lld;
+        prof_.begin("attn_bwd", s);
+        attention_bwd<T>(bf, ab, s);
+        prof_.end(s);
+        qk_norm_rope_bwd<T>(tp<T>(dqkv_r), tp<T>(qkv_r), QKLayout{3 * H, Hr, 2 * H, Hr, nh}, n, int(Hr), int(nhr),
+                            P(blk(i, "attn.temp")).f32 + r * nhr, w.cs, b.iq + r * nhr, b.ik + r * nhr, w.part1, s);
+        reduce_chunks(w.part1, chunks, int(nhr), G(blk(i, "attn.temp")) + r * nhr, 1.0f, 1, s);
+        colsum<T>(tp<T>(dqkv_r), 3 * H, n, int(3 * Hr), w.part1, s);
+        reduce_chunks(w.part1, chunks, int(3 * Hr), G(blk(i, "attn.qkv.b")) + r * 3 * Hr, 1.0f, 1, s);
+        gemm(bf, MN(dqkv_r, 3 * H), MN(b.a, H), int(3 * Hr), H, n,
+             EpiF32{G(blk(i, "attn.qkv.w")) + r * 3 * Hr * H, H, nullptr, 1.0f, 1, int(3 * Hr), int(H)}, s);
+        gemm(bf, KM(dqkv_r, 3 * H), MN(off<T>(W(blk(i, "attn.qkv.w")), r * 3 * Hr * H), H), n, H, int(3 * Hr),
+             EpiF32{part, H, nullptr, 1.0f, acc(k), n, int(H)}, s);  // da partial
+    }
+    tp_allreduce(part, N * H, s);
+    convert_f32<T>(part, N * H, tp<T>(w.s1), s);
+    rms_mod_bwd<T>(tp<T>(w.s1), Xin, b.r0, tab, tld, 0, H, w.mod_id, nu, n, H, dX, w.part1, w.part2, s);
+    reduce_chunks_grouped(w.part1, chunks, nu, H, dm, 6 * H, 1.0f, 0, s);      // d sh1
+    reduce_chunks_grouped(w.part2, chunks, nu, H, dm + H, 6 * H, 1.0f, 0, s);  // d sc1
+    // ---- shared modulation head (dit.cpp:280-283), replicated
     modulation_bwd(dm, w.gb[i], P("dit.mod.w").f32, nu, H, G("dit.mod.w"), G("dit.mod.b"), w.dgb, s);
     gscale_bwd(w.dgb, w.g, P(blk(i, "gscale")).f32, nu, H, G(blk(i, "gscale")), w.dg, s);
 }
@@ -664,6 +955,7 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
     w.n_u = 2;
     w.esz = bf16_ ? 2 : 4;
     w.grads = true;
+    w.tp = tp_;
     {
         Sizer sz{true, 0, &arena_};
         layout_ws(w, sz, cfg_, true);
@@ -705,6 +997,7 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
                          tp<T>(w.dV), s);  // 2 (V - v*) / (B * n_b * D); all-masked -> 0
         backward_sample<T>(w.dV);
     }
+    tp_allreduce_grads(s);
     if (world_ > 1) {
         prof_.begin("allreduce", s);
         MGV_NCCL(ncclAllReduce(grad_buf_, grad_buf_, grad_numel_, ncclFloat, ncclSum, comm_, s));
@@ -819,9 +1112,16 @@ void Model::flow_step(int64_t n, const mgv_flow_sample* samples, const double* t
             int64_t maxn = 0;
             for (auto* p : sorted_) maxn = std::max(maxn, p->numel);
             auto* gd = static_cast<double*>(dalloc(sizeof(double) * maxn));
+            float* gp = tp_ > 1 ? static_cast<float*>(dalloc(sizeof(float) * maxn)) : nullptr;
             for (size_t k = 0; k < sorted_.size(); ++k) {
                 if (!grads_out[k]) continue;
-                f32_to_f64<<<grid_of(sorted_[k]->numel), 256, 0, stream_>>>(sorted_[k]->grad, sorted_[k]->numel, gd); ::mgv::note_launch();
+                const float* gsrc = sorted_[k]->grad;
+                if (const int C = tp_ > 1 ? tp_row_chunks(sorted_[k]->name) : 0) {  // back to the reference row order
+                    permute_shard_rows(gsrc, gp, C, static_cast<int>(cfg_.hidden), tp_,
+                                       sorted_[k]->numel / (C * cfg_.hidden), 1, stream_);
+                    gsrc = gp;
+                }
+                f32_to_f64<<<grid_of(sorted_[k]->numel), 256, 0, stream_>>>(gsrc, sorted_[k]->numel, gd); ::mgv::note_launch();
                 MGV_CUDA(cudaMemcpyAsync(grads_out[k], gd, sizeof(double) * sorted_[k]->numel, cudaMemcpyDeviceToHost,
                                          stream_));
                 MGV_CUDA(cudaStreamSynchronize(stream_));
@@ -865,6 +1165,7 @@ void Model::value_forward(const double* in, int64_t N, const int32_t* coords, co
     w.n_u = static_cast<int>(uniq.size());
     w.esz = bf16_ ? 2 : 4;
     w.grads = false;
+    w.tp = tp_;
     {
         Sizer sz{true, 0, &arena_};
         layout_ws(w, sz, cfg_, false);

@@ -107,6 +107,11 @@ public:
 
     void set_stream(cudaStream_t s) { stream_ = s; }
     void set_dp(int rank, int world, const uint8_t id[128]);
+    // Megatron tensor parallelism over `size` ranks.  id == nullptr: all `size` ranks are
+    // emulated in this process (sequentially, partial sums accumulated in place of the all-reduce);
+    // otherwise this process is TP rank `rank` of an NCCL communicator.  Must precede upload().
+    void set_tp(int size, int rank, const uint8_t* id);
+    int tp_size() const { return tp_; }
 
     void upload(const Cfg& cfg, int64_t n, const char* const* names, const double* const* data,
                 const int64_t* numel);
@@ -143,6 +148,13 @@ private:
     template <class T>
     void block_bwd(int i, int64_t N);
     template <class T>
+    void block_fwd_tp(int i, int64_t N);
+    template <class T>
+    void block_bwd_tp(int i, int64_t N);
+    std::vector<int> tp_ranks() const;  // the TP ranks this process computes
+    void tp_allreduce(float* buf, int64_t n, cudaStream_t s);
+    void tp_allreduce_grads(cudaStream_t s);
+    template <class T>
     void value_forward(const double* in, int64_t N, const int32_t* coords, const int64_t dims[3],
                        const double* text, int64_t L, const double* tau, double fps, double* out, bool velocity);
 
@@ -169,6 +181,10 @@ private:
     // NCCL data parallel
     ncclComm_t comm_ = nullptr;
     int rank_ = 0, world_ = 1;
+    // tensor parallel
+    ncclComm_t tp_comm_ = nullptr;
+    int tp_ = 1, tp_rank_ = 0;
+    bool tp_virtual_ = false;
 
     // ---- per-sample workspace views (set by plan_workspace / forward)
 public:
