@@ -17,6 +17,12 @@ def lib() -> ctypes.CDLL:
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise RuntimeError(f"{LIB_PATH} is missing: build the CUDA library first (make -C {_HERE}/csrc)")
+        # Load torch first when it is installed: its bundled libnccl.so.2 (2.28) then satisfies our
+        # libnccl.so.2 dependency, instead of the older system copy that torch cannot run against.
+        try:
+            import torch  # noqa: F401
+        except ImportError:
+            pass
         _lib = ctypes.CDLL(LIB_PATH)
         _declare(_lib)
     return _lib
