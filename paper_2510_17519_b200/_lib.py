@@ -8,7 +8,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmugv_b200.so")
+# MGV_LIB_PATH lets the A/B tools in tools/ load an alternative build of the same library
+LIB_PATH = os.environ.get("MGV_LIB_PATH") or os.path.join(_HERE, "libmugv_b200.so")
 _lib = None
 
 

@@ -90,6 +90,17 @@ __device__ __forceinline__ void mma_tmem_x_t(uint32_t d, uint32_t a_tmem, uint32
                     (acc_first || ks > 0) ? 1u : 0u);
 }
 
+// As mma_tmem_x_t, with the 64-token A operand held as two 16-column halves at a_tmem (tokens 0..31)
+// and a_tmem + 32 (tokens 32..63): each compute warp of a lane group owns one half of the columns.
+template <int HD>
+__device__ __forceinline__ void mma_tmem2_x_t(uint32_t d, uint32_t a_tmem, uint32_t bt, bool acc_first) {
+    constexpr uint32_t id = idesc_bf16_f32(128, HD, false, false);
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks)
+        umma_f16_ts(d, a_tmem + (ks >> 1) * 32 + (ks & 1) * 8, smem_desc(bt + ks * 32, 16, 1024, kSwizzle128), id,
+                    (acc_first || ks > 0) ? 1u : 0u);
+}
+
 // thread row -> 64 bf16 values of a 128 x 64 SW128 K-major chunk
 __device__ __forceinline__ void st_row64(uint8_t* chunk, int row, const uint32_t* pk) {
     const uint32_t base = smem_u32(chunk) + row * 128;
@@ -100,9 +111,10 @@ __device__ __forceinline__ void st_row64(uint8_t* chunk, int row, const uint32_t
 }
 
 template <int HD>
-__device__ __forceinline__ void store_acc_row(uint32_t taddr, __nv_bfloat16* out, bool valid) {
+__device__ __forceinline__ void store_acc_row(uint32_t taddr, __nv_bfloat16* out, bool valid, int c0 = 0,
+                                              int c1 = HD / 16) {
 #pragma unroll 1
-    for (int c = 0; c < HD / 16; ++c) {
+    for (int c = c0; c < c1; ++c) {
         uint32_t r[16];
         tmem_ld16(taddr + c * 16, r);
         tmem_wait_ld();
@@ -124,32 +136,62 @@ struct BwdMaps {
 
 }  // namespace
 
-// =====================================================================================  dK / dV
-// TMEM: S^T [0,64) dP^T [64,128) P^T [128,160) dS^T [160,192) dV [192,192+HD) dK [DK,DK+HD)
 template <int HD>
-__global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_constant__ BwdMaps tm, AttnBwdProblem p) {
-    constexpr int BKV = 128, BQ = 64, NST = 4;
+__device__ __forceinline__ void mma_tmem_rows_x_t(uint32_t d, uint32_t a_tmem, uint32_t bt) {
+    constexpr uint32_t id = idesc_bf16_f32(128, 64, false, true);
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk)
+        umma_f16_ts(d, a_tmem + kk * 8, smem_desc(bt + kk * 2048, 16, 1024, kSwizzle128), id, kk > 0 ? 1u : 0u);
+}
+
+// thread's row of a row-major bf16 matrix (HD values, 16-byte aligned) -> TMEM columns [taddr, taddr + HD/2)
+// in the A-operand layout (two consecutive K elements per 32-bit column, the lower one in the low half)
+template <int HD>
+__device__ __forceinline__ void row_to_tmem(uint32_t taddr, const __nv_bfloat16* src, bool valid) {
+    constexpr int W = HD / 2;
+    uint32_t r[W];
+#pragma unroll
+    for (int u = 0; u < W / 4; ++u) {
+        const uint4 x = valid ? reinterpret_cast<const uint4*>(src)[u] : make_uint4(0, 0, 0, 0);
+        r[4 * u] = x.x;
+        r[4 * u + 1] = x.y;
+        r[4 * u + 2] = x.z;
+        r[4 * u + 3] = x.w;
+    }
+#pragma unroll
+    for (int c = 0; c < W; c += 8) tmem_st8(taddr + c, r + c);
+}
+
+// =====================================================================================  dK / dV
+// K stays in TMEM (the A operand of S^T = K Q^T, a TS MMA); V is an SS operand of dP^T = V dO^T.
+// P^T (bf16) is written over the first half of S^T and dS^T over the first half of dP^T; the MMA
+// issue order  dV(i) -> S^T(i+1) -> dK(i) -> dP^T(i+1)  keeps every overwrite behind its reader and
+// lets the softmax of step i+1 run under dK(i) and dP^T(i+1).
+// TMEM: S^T|P^T [0,64)  dP^T|dS^T [64,128)  dV [128,128+HD)  dK [DK,DK+HD)  K (bf16 pairs) after.
+template <int HD>
+__global__ void __launch_bounds__(384, 1) attn_bwd_dkv_tc_kernel(const __grid_constant__ BwdMaps tm, AttnBwdProblem p) {
+    constexpr int BKV = 128, BQ = 64, NST = 5;
     using T = BT<HD>;
-    constexpr int P_COL = 128, DS_COL = 160, DV_COL = 192, DK_COL = 192 + ((HD + 15) / 16) * 16;
-    static_assert(DK_COL + HD <= 512, "TMEM budget");
+    constexpr int S_COL = 0, DP_COL = 64, DV_COL = 128, DK_COL = 128 + ((HD + 15) / 16) * 16;
+    constexpr int KA_COL = DK_COL + ((HD + 15) / 16) * 16;
+    static_assert(KA_COL + HD / 2 <= 512, "TMEM budget");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sK = smem;
-    uint8_t* sV = sK + T::ROW_TILE;
+    uint8_t* sV = smem;
     uint8_t* sQt = sV + T::ROW_TILE;        // [NST]
     uint8_t* sdOt = sQt + NST * T::T_TILE;  // [NST]
-    float* sLse = reinterpret_cast<float*>(sdOt + NST * T::T_TILE);  // [NST][64] (log2 domain)
+    float* sLse = reinterpret_cast<float*>(sdOt + NST * T::T_TILE);  // [NST][64]
     float* sD = sLse + NST * BQ;                                      // [NST][64]
     uint64_t* bars = reinterpret_cast<uint64_t*>(sD + NST * BQ);
-    uint64_t* kv_full = bars;
+    uint64_t* v_full = bars;
     uint64_t* qd_full = bars + 1;         // [NST]
     uint64_t* qd_empty = bars + 1 + NST;  // [NST]
-    uint64_t* lse_full = bars + 1 + 2 * NST;  // [NST]
-    uint64_t* s_full = bars + 1 + 3 * NST;
-    uint64_t* s_empty = s_full + 1;
+    uint64_t* s_full = bars + 1 + 2 * NST;
+    uint64_t* dp_full = s_full + 1;
     uint64_t* p_full = s_full + 2;
-    uint64_t* pd_done = s_full + 3;
+    uint64_t* ds_full = s_full + 3;
     uint64_t* acc_done = s_full + 4;
+    uint64_t* ka_ready = s_full + 5;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 6);
 
     const AttnProblem& f = p.f;
@@ -159,182 +201,17 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dkv_tc_kernel(const __grid_co
     const int col = h * HD;
 
     if (threadIdx.x == 0) {
-        mbar_init(kv_full, 1);
+        mbar_init(v_full, 1);
         for (int i = 0; i < NST; ++i) {
             mbar_init(&qd_full[i], 1);
             mbar_init(&qd_empty[i], 1);
-            mbar_init(&lse_full[i], 32);
         }
         mbar_init(s_full, 1);
-        mbar_init(s_empty, 4);
-        mbar_init(p_full, 4);
-        mbar_init(pd_done, 1);
+        mbar_init(dp_full, 1);
+        mbar_init(p_full, 8);
+        mbar_init(ds_full, 8);
         mbar_init(acc_done, 1);
-        fence_barrier_init();
-    }
-    if (warp == 2) tmem_alloc<512>(tmem_slot);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            mbar_arrive_expect_tx(kv_full, 2 * T::ROW_TILE);
-            load_row_tile<HD>(sK, &tm.a128, &tm.a32, kv_full, col, k0);
-            load_row_tile<HD>(sV, &tm.b128, &tm.b32, kv_full, col, k0);
-        }
-        for (int i = 0; i < nq; ++i) {
-            const int st = i % NST;
-            if (i >= NST) mbar_wait(&qd_empty[st], ((i / NST) - 1) & 1);
-            if (lane == 0) {
-                // Q^T / dO^T tiles + this tile's lse and D rows (lse/D padded per head to a multiple of 64)
-                mbar_arrive_expect_tx(&qd_full[st], 2 * T::T_TILE + 2 * BQ * 4);
-                tma_load_2d(sQt + st * T::T_TILE, &tm.ta, &qd_full[st], i * BQ, col);
-                tma_load_2d(sdOt + st * T::T_TILE, &tm.tb, &qd_full[st], i * BQ, col);
-                bulk_load(sLse + st * BQ, f.lse + (int64_t)h * lse_stride(f) + i * BQ, BQ * 4, &qd_full[st]);
-                bulk_load(sD + st * BQ, p.Dvec + (int64_t)h * lse_stride(f) + i * BQ, BQ * 4, &qd_full[st]);
-            }
-        }
-    } else if (warp == 1) {
-        const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-        mbar_wait(kv_full, 0);
-        auto issue_s = [&](int i) {
-            const int st = i % NST;
-            mma_rows_x_t<HD>(tmem + 0, aK, smem_u32(sQt + st * T::T_TILE));
-            mma_rows_x_t<HD>(tmem + 64, aV, smem_u32(sdOt + st * T::T_TILE));
-        };
-        if (nq > 0) {
-            mbar_wait(&qd_full[0], 0);
-            tc_fence_after();
-            if (elect_one()) {
-                issue_s(0);
-                umma_commit(s_full);
-            }
-            __syncwarp();
-        }
-        for (int i = 0; i < nq; ++i) {
-            const int st = i % NST;
-            if (i + 1 < nq) {
-                mbar_wait(&qd_full[(i + 1) % NST], ((i + 1) / NST) & 1);
-                mbar_wait(s_empty, i & 1);  // elementwise(i) has read S^T_i / dP^T_i
-                tc_fence_after();
-                if (elect_one()) {
-                    issue_s(i + 1);
-                    umma_commit(s_full);
-                }
-                __syncwarp();
-            }
-            mbar_wait(p_full, i & 1);
-            tc_fence_after();
-            if (elect_one()) {
-                mma_tmem_x_t<HD>(tmem + DV_COL, tmem + P_COL, smem_u32(sdOt + st * T::T_TILE), i > 0);
-                mma_tmem_x_t<HD>(tmem + DK_COL, tmem + DS_COL, smem_u32(sQt + st * T::T_TILE), i > 0);
-                umma_commit(pd_done);
-                umma_commit(&qd_empty[st]);
-                if (i == nq - 1) umma_commit(acc_done);
-            }
-            __syncwarp();
-        }
-    } else if (warp >= 4) {
-        const int wq = warp - 4, row = wq * 32 + lane;
-        const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
-        for (int i = 0; i < nq; ++i) {
-            const int st = i % NST;
-            mbar_wait(&qd_full[st], (i / NST) & 1);  // lse / D rows of this tile have landed
-            mbar_wait(s_full, i & 1);
-            tc_fence_after();
-            float s[BQ], dp[BQ];
-            tmem_ld32(tmem + lane_base + 0, reinterpret_cast<uint32_t*>(s));
-            tmem_ld32(tmem + lane_base + 32, reinterpret_cast<uint32_t*>(s + 32));
-            tmem_ld32(tmem + lane_base + 64, reinterpret_cast<uint32_t*>(dp));
-            tmem_ld32(tmem + lane_base + 96, reinterpret_cast<uint32_t*>(dp + 32));
-            tmem_wait_ld();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(s_empty);
-            const float* lse2 = sLse + st * BQ;
-            const float* Dq = sD + st * BQ;
-            uint32_t pk[BQ / 2], dk[BQ / 2];
-            const bool full = (i + 1) * BQ <= f.Nq;
-#pragma unroll
-            for (int c = 0; c < BQ; c += 2) {
-                const bool v0 = full || i * BQ + c < f.Nq, v1 = full || i * BQ + c + 1 < f.Nq;
-                const float p0 = v0 ? ex2f((s[c] - lse2[c]) * kLog2e) : 0.0f;  // lse rows are natural-log
-                const float p1 = v1 ? ex2f((s[c + 1] - lse2[c + 1]) * kLog2e) : 0.0f;
-                pk[c / 2] = pack_bf16(p0, p1);
-                dk[c / 2] = pack_bf16(p0 * (dp[c] - Dq[c]), p1 * (dp[c + 1] - Dq[c + 1]));  // autodiff.cpp:820
-            }
-            if (i >= 1) {
-                mbar_wait(pd_done, (i - 1) & 1);  // dV/dK of tile i-1 have read P^T / dS^T
-                tc_fence_after();
-            }
-            tmem_st32(tmem + lane_base + P_COL, pk);
-            tmem_st32(tmem + lane_base + DS_COL, dk);
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(p_full);
-        }
-        if (nq > 0) mbar_wait(acc_done, 0);
-        tc_fence_after();
-        const int kv = k0 + row;
-        const bool valid = kv < f.Nk && nq > 0;
-        store_acc_row<HD>(tmem + lane_base + DV_COL, static_cast<__nv_bfloat16*>(p.dv) + (int64_t)kv * p.dv_ld + col,
-                          valid);
-        store_acc_row<HD>(tmem + lane_base + DK_COL, static_cast<__nv_bfloat16*>(p.dk) + (int64_t)kv * p.dk_ld + col,
-                          valid);
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    if (warp == 2) tmem_dealloc<512>(tmem);
-}
-
-// =====================================================================================  dQ
-// TMEM: S[b] [b*128, b*128+64) dP[b] [b*128+64, b*128+128) dQ [256, 256+HD) dS [DS, DS+32)
-template <int HD>
-__global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_constant__ BwdMaps tm, AttnBwdProblem p) {
-    constexpr int BMQ = 128, BKV = 64, NST = 4;
-    using T = BT<HD>;
-    constexpr int DQ_COL = 256, DS_COL = 256 + ((HD + 15) / 16) * 16;
-    static_assert(DS_COL + 32 <= 512, "TMEM budget");
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;
-    uint8_t* sdO = sQ + T::ROW_TILE;
-    uint8_t* sKt = sdO + T::ROW_TILE;      // [NST]
-    uint8_t* sVt = sKt + NST * T::T_TILE;  // [NST]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sVt + NST * T::T_TILE);
-    uint64_t* q_full = bars;
-    uint64_t* kv_full = bars + 1;          // [NST]
-    uint64_t* kv_empty = bars + 1 + NST;   // [NST]
-    uint64_t* s_full = bars + 1 + 2 * NST;  // [2]
-    uint64_t* s_empty = s_full + 2;         // [2]
-    uint64_t* ds_full = s_full + 4;
-    uint64_t* dq_done = s_full + 5;
-    uint64_t* acc_done = s_full + 6;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 8);
-
-    const AttnProblem& f = p.f;
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int h = blockIdx.y, q0 = blockIdx.x * BMQ;
-    const int nkv = (f.Nk + BKV - 1) / BKV;
-    const int col = h * HD;
-
-    if (threadIdx.x == 0) {
-        mbar_init(q_full, 1);
-        for (int i = 0; i < NST; ++i) {
-            mbar_init(&kv_full[i], 1);
-            mbar_init(&kv_empty[i], 1);
-        }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&s_full[i], 1);
-            mbar_init(&s_empty[i], 4);
-        }
-        mbar_init(ds_full, 4);
-        mbar_init(dq_done, 1);
-        mbar_init(acc_done, 1);
+        mbar_init(ka_ready, 4);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -345,9 +222,191 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_con
 
     if (warp == 0) {
         if (elect_one()) {
-            mbar_arrive_expect_tx(q_full, 2 * T::ROW_TILE);
-            load_row_tile<HD>(sQ, &tm.a128, &tm.a32, q_full, col, q0);
-            load_row_tile<HD>(sdO, &tm.b128, &tm.b32, q_full, col, q0);
+            mbar_arrive_expect_tx(v_full, T::ROW_TILE);
+            load_row_tile<HD>(sV, &tm.b128, &tm.b32, v_full, col, k0);
+            for (int i = 0; i < nq; ++i) {
+                const int st = i % NST;
+                if (i >= NST) mbar_wait(&qd_empty[st], ((i / NST) - 1) & 1);
+                // Q^T / dO^T tiles + this tile's lse and D rows (lse/D padded per head to a multiple of 64)
+                mbar_arrive_expect_tx(&qd_full[st], 2 * T::T_TILE + 2 * BQ * 4);
+                tma_load_2d(sQt + st * T::T_TILE, &tm.ta, &qd_full[st], i * BQ, col);
+                tma_load_2d(sdOt + st * T::T_TILE, &tm.tb, &qd_full[st], i * BQ, col);
+                bulk_load(sLse + st * BQ, f.lse + (int64_t)h * lse_stride(f) + i * BQ, BQ * 4, &qd_full[st]);
+                bulk_load(sD + st * BQ, p.Dvec + (int64_t)h * lse_stride(f) + i * BQ, BQ * 4, &qd_full[st]);
+            }
+        }
+    } else if (warp == 1) {
+        const uint32_t aV = smem_u32(sV);
+        auto issue_s = [&](int i) {
+            mma_tmem_rows_x_t<HD>(tmem + S_COL, tmem + KA_COL, smem_u32(sQt + (i % NST) * T::T_TILE));
+            umma_commit(s_full);
+        };
+        auto issue_dp = [&](int i) {
+            mma_rows_x_t<HD>(tmem + DP_COL, aV, smem_u32(sdOt + (i % NST) * T::T_TILE));
+            umma_commit(dp_full);
+        };
+        mbar_wait(ka_ready, 0);
+        mbar_wait(v_full, 0);
+        if (nq > 0) {
+            mbar_wait(&qd_full[0], 0);
+            tc_fence_after();
+            if (elect_one()) {
+                issue_s(0);
+                issue_dp(0);
+            }
+            __syncwarp();
+        }
+        for (int i = 0; i < nq; ++i) {
+            const int st = i % NST;
+            mbar_wait(p_full, i & 1);
+            tc_fence_after();
+            if (elect_one()) mma_tmem2_x_t<HD>(tmem + DV_COL, tmem + S_COL, smem_u32(sdOt + st * T::T_TILE), i > 0);
+            __syncwarp();
+            if (i + 1 < nq) {  // S^T_{i+1} overwrites P^T_i: issued after dV_i, which reads it
+                mbar_wait(&qd_full[(i + 1) % NST], ((i + 1) / NST) & 1);
+                tc_fence_after();
+                if (elect_one()) issue_s(i + 1);
+                __syncwarp();
+            }
+            mbar_wait(ds_full, i & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                mma_tmem2_x_t<HD>(tmem + DK_COL, tmem + DP_COL, smem_u32(sQt + st * T::T_TILE), i > 0);
+                umma_commit(&qd_empty[st]);
+                if (i + 1 < nq) issue_dp(i + 1);  // overwrites dS^T_i: after dK_i
+                if (i == nq - 1) umma_commit(acc_done);
+            }
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        // two warps per TMEM lane group: warp hf handles query columns [32 hf, 32 hf + 32) of each tile
+        const int g = warp & 3, hf = (warp - 4) >> 2, row = g * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(g * 32) << 16;
+        const int kv = k0 + row;
+        const bool kvv = kv < f.Nk;
+        if (hf == 0) {
+            row_to_tmem<HD>(tmem + lane_base + KA_COL,
+                            static_cast<const __nv_bfloat16*>(f.k) + (int64_t)(kvv ? kv : 0) * f.k_ld + col, kvv);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(ka_ready);
+        }
+        constexpr int HQ = BQ / 2;
+        for (int i = 0; i < nq; ++i) {
+            const int st = i % NST;
+            mbar_wait(&qd_full[st], (i / NST) & 1);  // lse / D rows of this tile have landed
+            mbar_wait(s_full, i & 1);
+            tc_fence_after();
+            float s[HQ], dp[HQ];
+            tmem_ld32(tmem + lane_base + S_COL + hf * HQ, reinterpret_cast<uint32_t*>(s));
+            tmem_wait_ld();
+            const float* lse2 = sLse + st * BQ + hf * HQ;
+            const float* Dq = sD + st * BQ + hf * HQ;
+            const int qb = i * BQ + hf * HQ;
+            const bool full = qb + HQ <= f.Nq;
+            uint32_t pk[HQ / 2];
+#pragma unroll
+            for (int c = 0; c < HQ; c += 2) {
+                const bool v0 = full || qb + c < f.Nq, v1 = full || qb + c + 1 < f.Nq;
+                s[c] = v0 ? ex2f((s[c] - lse2[c]) * kLog2e) : 0.0f;  // lse rows are natural-log
+                s[c + 1] = v1 ? ex2f((s[c + 1] - lse2[c + 1]) * kLog2e) : 0.0f;
+                pk[c / 2] = pack_bf16(s[c], s[c + 1]);
+            }
+            tmem_st16(tmem + lane_base + S_COL + hf * HQ, pk);  // P^T over this warp's own S^T columns
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(p_full);
+            mbar_wait(dp_full, i & 1);
+            tc_fence_after();
+            tmem_ld32(tmem + lane_base + DP_COL + hf * HQ, reinterpret_cast<uint32_t*>(dp));
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < HQ; c += 2)
+                pk[c / 2] = pack_bf16(s[c] * (dp[c] - Dq[c]), s[c + 1] * (dp[c + 1] - Dq[c + 1]));  // autodiff.cpp:820
+            tmem_st16(tmem + lane_base + DP_COL + hf * HQ, pk);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(ds_full);
+        }
+        if (nq > 0) mbar_wait(acc_done, 0);
+        tc_fence_after();
+        const bool valid = kvv && nq > 0;
+        if (hf == 0)
+            store_acc_row<HD>(tmem + lane_base + DV_COL,
+                              static_cast<__nv_bfloat16*>(p.dv) + (int64_t)kv * p.dv_ld + col, valid);
+        else
+            store_acc_row<HD>(tmem + lane_base + DK_COL,
+                              static_cast<__nv_bfloat16*>(p.dk) + (int64_t)kv * p.dk_ld + col, valid);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// =====================================================================================  dQ
+// Q and dO stay in TMEM for the whole CTA (they are the A operands of S = Q K^T and dP = dO V^T), so
+// every MMA of this pass is TS-form: only the 64-token K^T / V^T tiles are read from shared memory,
+// and the products run at the tensor rate instead of the shared-memory operand rate of SS MMAs.
+// TMEM: S[b] [64b, 64b+64)  dP [128,192)  dS [192,224)  dQ [224,224+HD)  Q, dO (bf16 pairs) after.
+template <int HD>
+__global__ void __launch_bounds__(384, 1) attn_bwd_dq_tc_kernel(const __grid_constant__ BwdMaps tm, AttnBwdProblem p) {
+    constexpr int BMQ = 128, BKV = 64, NST = 6;
+    using T = BT<HD>;
+    constexpr int DP_COL = 128, DS_COL = 192, DQ_COL = 224;
+    constexpr int QA_COL = DQ_COL + ((HD + 15) / 16) * 16, DOA_COL = QA_COL + HD / 2;
+    static_assert(DOA_COL + HD / 2 <= 512, "TMEM budget");
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sKt = smem;                   // [NST]
+    uint8_t* sVt = sKt + NST * T::T_TILE;  // [NST]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sVt + NST * T::T_TILE);
+    uint64_t* kv_full = bars;             // [NST]
+    uint64_t* kv_empty = bars + NST;      // [NST]
+    uint64_t* s_full = bars + 2 * NST;    // [2]
+    uint64_t* s_empty = s_full + 2;       // [2]
+    uint64_t* dp_full = s_full + 4;
+    uint64_t* dp_empty = s_full + 5;
+    uint64_t* ds_full = s_full + 6;
+    uint64_t* dq_done = s_full + 7;
+    uint64_t* acc_done = s_full + 8;
+    uint64_t* qa_ready = s_full + 9;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 10);
+
+    const AttnProblem& f = p.f;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int h = blockIdx.y, q0 = blockIdx.x * BMQ;
+    const int nkv = (f.Nk + BKV - 1) / BKV;
+    const int col = h * HD;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_empty[i], 8);
+        }
+        mbar_init(dp_full, 1);
+        mbar_init(dp_empty, 8);
+        mbar_init(ds_full, 8);
+        mbar_init(dq_done, 1);
+        mbar_init(acc_done, 1);
+        mbar_init(qa_ready, 8);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (elect_one()) {
             for (int j = 0; j < nkv; ++j) {
                 const int b = j % NST;
                 if (j >= NST) mbar_wait(&kv_empty[b], ((j / NST) - 1) & 1);
@@ -357,23 +416,28 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_con
             }
         }
     } else if (warp == 1) {
-        const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO);
         auto issue_dq = [&](int j) {
             const int b = j % NST;
             mma_tmem_x_t<HD>(tmem + DQ_COL, tmem + DS_COL, smem_u32(sKt + b * T::T_TILE), j > 0);
             umma_commit(dq_done);
             umma_commit(&kv_empty[b]);
         };
-        mbar_wait(q_full, 0);
+        mbar_wait(qa_ready, 0);
         for (int j = 0; j < nkv; ++j) {
             const int b = j % NST, sb = j & 1;
             mbar_wait(&kv_full[b], (j / NST) & 1);
             if (j >= 2) mbar_wait(&s_empty[sb], ((j - 2) >> 1) & 1);
             tc_fence_after();
             if (elect_one()) {
-                mma_rows_x_t<HD>(tmem + sb * 128, aQ, smem_u32(sKt + b * T::T_TILE));
-                mma_rows_x_t<HD>(tmem + sb * 128 + 64, adO, smem_u32(sVt + b * T::T_TILE));
+                mma_tmem_rows_x_t<HD>(tmem + sb * 64, tmem + QA_COL, smem_u32(sKt + b * T::T_TILE));
                 umma_commit(&s_full[sb]);
+            }
+            __syncwarp();
+            if (j >= 1) mbar_wait(dp_empty, (j - 1) & 1);  // elementwise(j-1) has read dP_{j-1}
+            tc_fence_after();
+            if (elect_one()) {
+                mma_tmem_rows_x_t<HD>(tmem + DP_COL, tmem + DOA_COL, smem_u32(sVt + b * T::T_TILE));
+                umma_commit(dp_full);
             }
             __syncwarp();
             if (j >= 1) {
@@ -393,38 +457,57 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_con
             __syncwarp();
         }
     } else if (warp >= 4) {
-        const int wq = warp - 4, row = wq * 32 + lane;
-        const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
+        // two warps per TMEM lane group: warp hf handles key columns [32 hf, 32 hf + 32) of each tile
+        const int g = warp & 3, hf = (warp - 4) >> 2, row = g * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(g * 32) << 16;
         const int q = q0 + row;
-        const float lse2 = q < f.Nq ? f.lse[(int64_t)h * lse_stride(f) + q] * kLog2e : 0.0f;
-        const float Dq = q < f.Nq ? p.Dvec[(int64_t)h * lse_stride(f) + q] : 0.0f;
+        const bool qv = q < f.Nq;
+        const int64_t qi = qv ? q : 0;
+        if (hf == 0)
+            row_to_tmem<HD>(tmem + lane_base + QA_COL, static_cast<const __nv_bfloat16*>(f.q) + qi * f.q_ld + col, qv);
+        else
+            row_to_tmem<HD>(tmem + lane_base + DOA_COL, static_cast<const __nv_bfloat16*>(p.dO) + qi * p.do_ld + col,
+                            qv);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(qa_ready);
+        const float lse2 = qv ? f.lse[(int64_t)h * lse_stride(f) + q] * kLog2e : 0.0f;
+        const float Dq = qv ? p.Dvec[(int64_t)h * lse_stride(f) + q] : 0.0f;
+        constexpr int HK = BKV / 2;
         for (int j = 0; j < nkv; ++j) {
             const int sb = j & 1;
             mbar_wait(&s_full[sb], (j >> 1) & 1);
             tc_fence_after();
-            float s[BKV], dp[BKV];
-            tmem_ld32(tmem + lane_base + sb * 128, reinterpret_cast<uint32_t*>(s));
-            tmem_ld32(tmem + lane_base + sb * 128 + 32, reinterpret_cast<uint32_t*>(s + 32));
-            tmem_ld32(tmem + lane_base + sb * 128 + 64, reinterpret_cast<uint32_t*>(dp));
-            tmem_ld32(tmem + lane_base + sb * 128 + 96, reinterpret_cast<uint32_t*>(dp + 32));
+            float s[HK], dp[HK];
+            tmem_ld32(tmem + lane_base + sb * 64 + hf * HK, reinterpret_cast<uint32_t*>(s));
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[sb]);
-            uint32_t dk[BKV / 2];
-            const bool full = (j + 1) * BKV <= f.Nk;
+            const int kb = j * BKV + hf * HK;
+            const bool full = kb + HK <= f.Nk;
 #pragma unroll
-            for (int c = 0; c < BKV; c += 2) {
-                const bool v0 = full || j * BKV + c < f.Nk, v1 = full || j * BKV + c + 1 < f.Nk;
-                const float p0 = v0 ? ex2f(fmaf(s[c], kLog2e, -lse2)) : 0.0f;
-                const float p1 = v1 ? ex2f(fmaf(s[c + 1], kLog2e, -lse2)) : 0.0f;
-                dk[c / 2] = pack_bf16(p0 * (dp[c] - Dq), p1 * (dp[c + 1] - Dq));
+            for (int c = 0; c < HK; ++c) {
+                const bool v = full || kb + c < f.Nk;
+                s[c] = v ? ex2f(fmaf(s[c], kLog2e, -lse2)) : 0.0f;  // P
             }
+            mbar_wait(dp_full, j & 1);
+            tc_fence_after();
+            tmem_ld32(tmem + lane_base + DP_COL + hf * HK, reinterpret_cast<uint32_t*>(dp));
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dp_empty);
+            uint32_t dk[HK / 2];
+#pragma unroll
+            for (int c = 0; c < HK; c += 2)
+                dk[c / 2] = pack_bf16(s[c] * (dp[c] - Dq), s[c + 1] * (dp[c + 1] - Dq));  // autodiff.cpp:820
             if (j >= 1) {
                 mbar_wait(dq_done, (j - 1) & 1);  // dQ += dS_{j-1} K has read the dS columns
                 tc_fence_after();
             }
-            tmem_st32(tmem + lane_base + DS_COL, dk);
+            tmem_st16(tmem + lane_base + DS_COL + hf * (HK / 2), dk);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
@@ -432,8 +515,9 @@ __global__ void __launch_bounds__(256, 1) attn_bwd_dq_tc_kernel(const __grid_con
         }
         if (nkv > 0) mbar_wait(acc_done, 0);
         tc_fence_after();
+        constexpr int NC = HD / 16, C0 = (NC + 1) / 2;
         store_acc_row<HD>(tmem + lane_base + DQ_COL, static_cast<__nv_bfloat16*>(p.dq) + (int64_t)q * p.dq_ld + col,
-                          q < f.Nq && nkv > 0);
+                          qv && nkv > 0, hf == 0 ? 0 : C0, hf == 0 ? C0 : NC);
     }
     tc_fence_before();
     __syncthreads();
@@ -451,36 +535,35 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
     attn_bwd_dvec(p, s);
     {
         BwdMaps m;
-        make_tmap_sw(&m.a128, f.k, W, f.Nk, f.k_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-        make_tmap_sw(&m.a32, f.k, W, f.Nk, f.k_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
+        if (reinterpret_cast<uintptr_t>(f.k) % 16 || f.k_ld % 8)
+            throw std::runtime_error("attn_bwd_tc: k must be 16-byte aligned with ld % 8 == 0");
         make_tmap_sw(&m.b128, f.v, W, f.Nk, f.v_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
         make_tmap_sw(&m.b32, f.v, W, f.Nk, f.v_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
         make_tmap_sw(&m.ta, qt, f.Nq, W, qt_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
         make_tmap_sw(&m.tb, dot, f.Nq, W, dot_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
-        const int smem = 2 * T::ROW_TILE + 8 * T::T_TILE + 8 * 64 * 4 + 256 + 1024;
+        const int smem = T::ROW_TILE + 10 * T::T_TILE + 10 * 64 * 4 + 256 + 1024;
         static bool set = false;
         if (!set) {
             MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             set = true;
         }
-        attn_bwd_dkv_tc_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads), 256, smem, s>>>(m, p); ::mgv::note_launch();
+        attn_bwd_dkv_tc_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads), 384, smem, s>>>(m, p); ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
     }
     {
         BwdMaps m;
-        make_tmap_sw(&m.a128, f.q, W, f.Nq, f.q_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-        make_tmap_sw(&m.a32, f.q, W, f.Nq, f.q_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
-        make_tmap_sw(&m.b128, p.dO, W, f.Nq, p.do_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-        make_tmap_sw(&m.b32, p.dO, W, f.Nq, p.do_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
         make_tmap_sw(&m.ta, kt, f.Nk, W, kt_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
         make_tmap_sw(&m.tb, vt, f.Nk, W, vt_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
-        const int smem = 2 * T::ROW_TILE + 8 * T::T_TILE + 256 + 1024;
+        // Q / dO rows are read straight into TMEM with 16-byte loads
+        if ((reinterpret_cast<uintptr_t>(f.q) | reinterpret_cast<uintptr_t>(p.dO)) % 16 || f.q_ld % 8 || p.do_ld % 8)
+            throw std::runtime_error("attn_bwd_tc: q / dO must be 16-byte aligned with ld % 8 == 0");
+        const int smem = 12 * T::T_TILE + 256 + 1024;
         static bool set = false;
         if (!set) {
             MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             set = true;
         }
-        attn_bwd_dq_tc_kernel<HD><<<dim3((f.Nq + 127) / 128, f.heads), 256, smem, s>>>(m, p); ::mgv::note_launch();
+        attn_bwd_dq_tc_kernel<HD><<<dim3((f.Nq + 127) / 128, f.heads), 384, smem, s>>>(m, p); ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
     }
 }
