@@ -27,6 +27,18 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 
+#ifdef MGV_ATTN_TRACE  // development timeline of one CTA (tools/trace_attn.py); not in the product build
+__device__ unsigned long long g_attn_trace[8][64];
+#define ATR(ev, j)                                                                              \
+    do {                                                                                        \
+        if (blockIdx.x == 7 && blockIdx.y == 0 && (j) < 64) g_attn_trace[ev][j] = clock64();   \
+    } while (0)
+#else
+#define ATR(ev, j) \
+    do {           \
+    } while (0)
+#endif
+
 template <int HD>
 struct BT {
     static constexpr int NF = HD / 64;
@@ -90,16 +102,31 @@ __device__ __forceinline__ void mma_tmem_x_t(uint32_t d, uint32_t a_tmem, uint32
                     (acc_first || ks > 0) ? 1u : 0u);
 }
 
-// As mma_tmem_x_t, with the 64-token A operand held as two 16-column halves at a_tmem (tokens 0..31)
-// and a_tmem + 32 (tokens 32..63): each compute warp of a lane group owns one half of the columns.
-template <int HD>
-__device__ __forceinline__ void mma_tmem2_x_t(uint32_t d, uint32_t a_tmem, uint32_t bt, bool acc_first) {
+// As mma_tmem_x_t, with the 64-token A operand split over the compute warps of a lane group: warp w
+// owns tokens [w W, w W + W) and keeps their bf16 pairs at columns [a_tmem + w W, a_tmem + w W + W/2).
+template <int HD, int W>
+__device__ __forceinline__ void mma_tmem_split_x_t(uint32_t d, uint32_t a_tmem, uint32_t bt, bool acc_first) {
     constexpr uint32_t id = idesc_bf16_f32(128, HD, false, false);
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks)
-        umma_f16_ts(d, a_tmem + (ks >> 1) * 32 + (ks & 1) * 8, smem_desc(bt + ks * 32, 16, 1024, kSwizzle128), id,
-                    (acc_first || ks > 0) ? 1u : 0u);
+        umma_f16_ts(d, a_tmem + (16 * ks / W) * W + (16 * ks % W) / 2, smem_desc(bt + ks * 32, 16, 1024, kSwizzle128),
+                    id, (acc_first || ks > 0) ? 1u : 0u);
 }
+template <int N>
+__device__ __forceinline__ void tmem_ldn(uint32_t taddr, float* r) {
+    if constexpr (N == 16)
+        tmem_ld16(taddr, reinterpret_cast<uint32_t*>(r));
+    else
+        tmem_ld32(taddr, reinterpret_cast<uint32_t*>(r));
+}
+template <int N>
+__device__ __forceinline__ void tmem_stn(uint32_t taddr, const uint32_t* r) {
+    if constexpr (N == 8)
+        tmem_st8(taddr, r);
+    else
+        tmem_st16(taddr, r);
+}
+constexpr int kCWq = 2;  // compute warps per TMEM lane group in the dQ pass
 
 // thread row -> 64 bf16 values of a 128 x 64 SW128 K-major chunk
 __device__ __forceinline__ void st_row64(uint8_t* chunk, int row, const uint32_t* pk) {
@@ -260,7 +287,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_tc_kernel(const __grid_co
             const int st = i % NST;
             mbar_wait(p_full, i & 1);
             tc_fence_after();
-            if (elect_one()) mma_tmem2_x_t<HD>(tmem + DV_COL, tmem + S_COL, smem_u32(sdOt + st * T::T_TILE), i > 0);
+            if (elect_one()) mma_tmem_split_x_t<HD, 32>(tmem + DV_COL, tmem + S_COL, smem_u32(sdOt + st * T::T_TILE), i > 0);
             __syncwarp();
             if (i + 1 < nq) {  // S^T_{i+1} overwrites P^T_i: issued after dV_i, which reads it
                 mbar_wait(&qd_full[(i + 1) % NST], ((i + 1) / NST) & 1);
@@ -271,7 +298,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_tc_kernel(const __grid_co
             mbar_wait(ds_full, i & 1);
             tc_fence_after();
             if (elect_one()) {
-                mma_tmem2_x_t<HD>(tmem + DK_COL, tmem + DP_COL, smem_u32(sQt + st * T::T_TILE), i > 0);
+                mma_tmem_split_x_t<HD, 32>(tmem + DK_COL, tmem + DP_COL, smem_u32(sQt + st * T::T_TILE), i > 0);
                 umma_commit(&qd_empty[st]);
                 if (i + 1 < nq) issue_dp(i + 1);  // overwrites dS^T_i: after dK_i
                 if (i == nq - 1) umma_commit(acc_done);
@@ -353,7 +380,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_tc_kernel(const __grid_co
 // and the products run at the tensor rate instead of the shared-memory operand rate of SS MMAs.
 // TMEM: S[b] [64b, 64b+64)  dP [128,192)  dS [192,224)  dQ [224,224+HD)  Q, dO (bf16 pairs) after.
 template <int HD>
-__global__ void __launch_bounds__(384, 1) attn_bwd_dq_tc_kernel(const __grid_constant__ BwdMaps tm, AttnBwdProblem p) {
+__global__ void __launch_bounds__(128 + 128 * kCWq, 1) attn_bwd_dq_tc_kernel(const __grid_constant__ BwdMaps tm, AttnBwdProblem p) {
     constexpr int BMQ = 128, BKV = 64, NST = 6;
     using T = BT<HD>;
     constexpr int DP_COL = 128, DS_COL = 192, DQ_COL = 224;
@@ -389,11 +416,11 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_tc_kernel(const __grid_con
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&s_empty[i], 8);
+            mbar_init(&s_empty[i], 4 * kCWq);
         }
         mbar_init(dp_full, 1);
-        mbar_init(dp_empty, 8);
-        mbar_init(ds_full, 8);
+        mbar_init(dp_empty, 4 * kCWq);
+        mbar_init(ds_full, 4 * kCWq);
         mbar_init(dq_done, 1);
         mbar_init(acc_done, 1);
         mbar_init(qa_ready, 8);
@@ -422,37 +449,44 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_tc_kernel(const __grid_con
             umma_commit(dq_done);
             umma_commit(&kv_empty[b]);
         };
-        mbar_wait(qa_ready, 0);
-        for (int j = 0; j < nkv; ++j) {
-            const int b = j % NST, sb = j & 1;
+        auto issue_s = [&](int j) {  // S_j into buffer j & 1
+            const int b = j % NST;
             mbar_wait(&kv_full[b], (j / NST) & 1);
-            if (j >= 2) mbar_wait(&s_empty[sb], ((j - 2) >> 1) & 1);
+            if (j >= 2) mbar_wait(&s_empty[j & 1], ((j - 2) >> 1) & 1);
             tc_fence_after();
             if (elect_one()) {
-                mma_tmem_rows_x_t<HD>(tmem + sb * 64, tmem + QA_COL, smem_u32(sKt + b * T::T_TILE));
-                umma_commit(&s_full[sb]);
+                mma_tmem_rows_x_t<HD>(tmem + (j & 1) * 64, tmem + QA_COL, smem_u32(sKt + b * T::T_TILE));
+                umma_commit(&s_full[j & 1]);
             }
             __syncwarp();
-            if (j >= 1) mbar_wait(dp_empty, (j - 1) & 1);  // elementwise(j-1) has read dP_{j-1}
-            tc_fence_after();
+        };
+        auto issue_dp = [&](int j) {
             if (elect_one()) {
-                mma_tmem_rows_x_t<HD>(tmem + DP_COL, tmem + DOA_COL, smem_u32(sVt + b * T::T_TILE));
+                mma_tmem_rows_x_t<HD>(tmem + DP_COL, tmem + DOA_COL, smem_u32(sVt + (j % NST) * T::T_TILE));
                 umma_commit(dp_full);
             }
             __syncwarp();
-            if (j >= 1) {
-                mbar_wait(ds_full, (j - 1) & 1);
+        };
+        // issue order per step j:  S(j+2) [S_j read] -> dP(j+1) [dP_j read] -> dQ(j) [dS_j ready]
+        mbar_wait(qa_ready, 0);
+        if (nkv > 0) issue_s(0);
+        if (nkv > 1) issue_s(1);
+        if (nkv > 0) issue_dp(0);
+        for (int j = 0; j < nkv; ++j) {
+            if (j + 2 < nkv) issue_s(j + 2);
+            if (lane == 0) ATR(0, j);
+            if (j + 1 < nkv) {
+                mbar_wait(dp_empty, j & 1);
                 tc_fence_after();
-                if (elect_one()) issue_dq(j - 1);
-                __syncwarp();
+                if (lane == 0) ATR(1, j);
+                issue_dp(j + 1);
             }
-        }
-        if (nkv > 0) {
-            mbar_wait(ds_full, (nkv - 1) & 1);
+            mbar_wait(ds_full, j & 1);
             tc_fence_after();
+            if (lane == 0) ATR(2, j);
             if (elect_one()) {
-                issue_dq(nkv - 1);
-                umma_commit(acc_done);
+                issue_dq(j);
+                if (j == nkv - 1) umma_commit(acc_done);
             }
             __syncwarp();
         }
@@ -463,61 +497,88 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_tc_kernel(const __grid_con
         const int q = q0 + row;
         const bool qv = q < f.Nq;
         const int64_t qi = qv ? q : 0;
-        if (hf == 0)
-            row_to_tmem<HD>(tmem + lane_base + QA_COL, static_cast<const __nv_bfloat16*>(f.q) + qi * f.q_ld + col, qv);
-        else
-            row_to_tmem<HD>(tmem + lane_base + DOA_COL, static_cast<const __nv_bfloat16*>(p.dO) + qi * p.do_ld + col,
-                            qv);
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(qa_ready);
+        if (hf < 2) {  // warp slices 0 / 1 stage Q / dO into TMEM
+            if (hf == 0)
+                row_to_tmem<HD>(tmem + lane_base + QA_COL, static_cast<const __nv_bfloat16*>(f.q) + qi * f.q_ld + col,
+                                qv);
+            else
+                row_to_tmem<HD>(tmem + lane_base + DOA_COL,
+                                static_cast<const __nv_bfloat16*>(p.dO) + qi * p.do_ld + col, qv);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(qa_ready);
+        }
         const float lse2 = qv ? f.lse[(int64_t)h * lse_stride(f) + q] * kLog2e : 0.0f;
         const float Dq = qv ? p.Dvec[(int64_t)h * lse_stride(f) + q] : 0.0f;
-        constexpr int HK = BKV / 2;
-        for (int j = 0; j < nkv; ++j) {
-            const int sb = j & 1;
-            mbar_wait(&s_full[sb], (j >> 1) & 1);
+        constexpr int HK = BKV / kCWq;
+        // Software-pipelined like the dK/dV pass: iteration j loads S_{j+1} and dP_j together and computes
+        // dS_j next to P_{j+1}.
+        auto softmax = [&](float* x, int j) {  // x <- exp(x - lse) for key tile j (zero past Nk)
+            const int kb = j * BKV + hf * HK;
+            if (kb + HK <= f.Nk) {
+#pragma unroll
+                for (int c = 0; c < HK; ++c) x[c] = ex2f(fmaf(x[c], kLog2e, -lse2));
+            } else {
+#pragma unroll
+                for (int c = 0; c < HK; ++c) x[c] = kb + c < f.Nk ? ex2f(fmaf(x[c], kLog2e, -lse2)) : 0.0f;
+            }
+        };
+        float pr[HK];
+        if (nkv > 0) {
+            mbar_wait(&s_full[0], 0);
             tc_fence_after();
-            float s[HK], dp[HK];
-            tmem_ld32(tmem + lane_base + sb * 64 + hf * HK, reinterpret_cast<uint32_t*>(s));
+            tmem_ldn<HK>(tmem + lane_base + hf * HK, pr);
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&s_empty[sb]);
-            const int kb = j * BKV + hf * HK;
-            const bool full = kb + HK <= f.Nk;
-#pragma unroll
-            for (int c = 0; c < HK; ++c) {
-                const bool v = full || kb + c < f.Nk;
-                s[c] = v ? ex2f(fmaf(s[c], kLog2e, -lse2)) : 0.0f;  // P
+            if (lane == 0) mbar_arrive(&s_empty[0]);
+            softmax(pr, 0);
+        }
+        for (int j = 0; j < nkv; ++j) {
+            const bool more = j + 1 < nkv;
+            float sn[HK], dp[HK];
+            if (more) {
+                mbar_wait(&s_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+                tc_fence_after();
+                tmem_ldn<HK>(tmem + lane_base + ((j + 1) & 1) * 64 + hf * HK, sn);
             }
+            if (warp == 4 && lane == 0) ATR(3, j);
             mbar_wait(dp_full, j & 1);
             tc_fence_after();
-            tmem_ld32(tmem + lane_base + DP_COL + hf * HK, reinterpret_cast<uint32_t*>(dp));
+            if (warp == 4 && lane == 0) ATR(4, j);
+            tmem_ldn<HK>(tmem + lane_base + DP_COL + hf * HK, dp);
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(dp_empty);
+            if (lane == 0) {
+                if (more) mbar_arrive(&s_empty[(j + 1) & 1]);
+                mbar_arrive(dp_empty);
+            }
             uint32_t dk[HK / 2];
 #pragma unroll
             for (int c = 0; c < HK; c += 2)
-                dk[c / 2] = pack_bf16(s[c] * (dp[c] - Dq), s[c + 1] * (dp[c + 1] - Dq));  // autodiff.cpp:820
+                dk[c / 2] = pack_bf16(pr[c] * (dp[c] - Dq), pr[c + 1] * (dp[c + 1] - Dq));  // autodiff.cpp:820
+            if (more) softmax(sn, j + 1);
+            if (warp == 4 && lane == 0) ATR(5, j);
             if (j >= 1) {
                 mbar_wait(dq_done, (j - 1) & 1);  // dQ += dS_{j-1} K has read the dS columns
                 tc_fence_after();
             }
-            tmem_st16(tmem + lane_base + DS_COL + hf * (HK / 2), dk);
+            tmem_stn<HK / 2>(tmem + lane_base + DS_COL + hf * (HK / 2), dk);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(ds_full);
+            if (warp == 4 && lane == 0) ATR(6, j);
+#pragma unroll
+            for (int c = 0; c < HK; ++c) pr[c] = sn[c];
         }
         if (nkv > 0) mbar_wait(acc_done, 0);
         tc_fence_after();
-        constexpr int NC = HD / 16, C0 = (NC + 1) / 2;
+        constexpr int NC = HD / 16;
         store_acc_row<HD>(tmem + lane_base + DQ_COL, static_cast<__nv_bfloat16*>(p.dq) + (int64_t)q * p.dq_ld + col,
-                          qv && nkv > 0, hf == 0 ? 0 : C0, hf == 0 ? C0 : NC);
+                          qv && nkv > 0, hf * NC / kCWq, (hf + 1) * NC / kCWq);
     }
     tc_fence_before();
     __syncthreads();
@@ -563,7 +624,7 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
             MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             set = true;
         }
-        attn_bwd_dq_tc_kernel<HD><<<dim3((f.Nq + 127) / 128, f.heads), 384, smem, s>>>(m, p); ::mgv::note_launch();
+        attn_bwd_dq_tc_kernel<HD><<<dim3((f.Nq + 127) / 128, f.heads), 128 + 128 * kCWq, smem, s>>>(m, p); ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
     }
 }
@@ -613,3 +674,9 @@ void attn_bwd_tc(const AttnBwdProblem& p, cudaStream_t s) {
 }
 
 }  // namespace mgv
+
+#ifdef MGV_ATTN_TRACE
+extern "C" int mgv_dev_attn_trace(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, mgv::g_attn_trace, sizeof(mgv::g_attn_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
