@@ -116,7 +116,7 @@ void gemm_tc_launch(const Mat& A, const Mat& B, int M, int N, int K, const Epi& 
         }
         const int tiles = num_m * num_n;
         const int grid = tiles < num_sms() ? tiles : num_sms();
-        kern<<<grid, kGemmThreads, C::SMEM, s>>>(ta, tb, M, N, K, epi); ::mgv::note_launch();
+        kern<<<grid, gemm_threads<Epi>(), C::SMEM, s>>>(ta, tb, M, N, K, epi); ::mgv::note_launch();
     } else {
         auto kern = gemm_bf16_tc_kernel<BN, A_MN, B_MN, 2, Epi>;
         static bool attr_set = false;
@@ -128,7 +128,7 @@ void gemm_tc_launch(const Mat& A, const Mat& B, int M, int N, int K, const Epi& 
         const int clusters = pair_tiles < num_sms() / 2 ? pair_tiles : num_sms() / 2;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(2 * clusters);
-        cfg.blockDim = dim3(kGemmThreads);
+        cfg.blockDim = dim3(gemm_threads<Epi>());
         cfg.dynamicSmemBytes = C::SMEM;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
@@ -166,7 +166,7 @@ void gemm_tc2_launch(const Mat& A, const Mat& B, int M, int N, int K, const Epi&
     const int clusters = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * clusters);
-    cfg.blockDim = dim3(kGemmThreads);
+    cfg.blockDim = dim3(gemm_threads<Epi>());
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];

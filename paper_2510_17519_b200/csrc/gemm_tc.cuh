@@ -21,7 +21,27 @@ namespace mgv {
 
 constexpr int kGemmBM = 128;
 constexpr int kGemmBK = 64;
-constexpr int kGemmThreads = 256;
+// Epilogue warps per CTA: 4 (one per TMEM lane group) for the light epilogues; the SiLU epilogues
+// (two exponentials-worth of MUFU work and two outputs per element) use 8, two per lane group, each
+// draining half of the columns.  Extra warps cost power in the power-capped GEMMs, so they are only
+// spent where the epilogue would otherwise outlast the main loop.
+template <class Epi>
+struct EpiWarps {
+    static constexpr int value = 4;
+};
+template <class T>
+struct EpiWarps<EpiBiasSilu<T>> {
+    static constexpr int value = 8;
+};
+template <class T>
+struct EpiWarps<EpiSiluBwd<T>> {
+    static constexpr int value = 8;
+};
+constexpr int kGemmThreadsMax = 128 + 32 * 8;
+template <class Epi>
+constexpr int gemm_threads() {
+    return 128 + 32 * EpiWarps<Epi>::value;
+}
 
 // Grouped rasterisation: tiles are walked in groups of kRasterGroup M-tiles x all N-tiles, so the
 // concurrently resident tiles share a few A slabs and a few B slabs (L2 reuse in both operands).
@@ -32,6 +52,25 @@ __device__ __forceinline__ void raster(int t, int num_m, int num_n, int& mt, int
     const int rows = min(kRasterGroup, num_m - g * kRasterGroup);
     mt = g * kRasterGroup + r % rows;
     nt = r / rows;
+}
+
+// Drain one accumulator: epilogue warp wq reads TMEM lane group (wq % 4) and column half (wq / 4) of
+// the BN-column tile, 16 columns per tcgen05.ld, loading the next chunk while the current one is in
+// the epilogue functor.
+template <int BN, class Epi>
+__device__ __forceinline__ void epilogue_rows(uint32_t acc_base, int wq, int lane, int m0, int n0, const Epi& epi) {
+    constexpr int W = BN / (EpiWarps<Epi>::value / 4), NCH = W / 16;
+    const int g = wq & 3, hf = wq >> 2;
+    const int row = m0 + g * 32 + lane;
+    const uint32_t base = acc_base + hf * W + (static_cast<uint32_t>(g * 32) << 16);
+    uint32_t r[2][16];
+    tmem_ld16(base, r[0]);
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+        tmem_wait_ld();
+        if (c + 1 < NCH) tmem_ld16(base + (c + 1) * 16, r[(c + 1) & 1]);
+        epi(row, n0 + hf * W + c * 16, reinterpret_cast<const float*>(r[c & 1]), 16);
+    }
 }
 
 template <int BN>
@@ -50,7 +89,7 @@ struct GemmCfg {
 // shared memory, and every MMA commit releases the stage in both CTAs.  L2->SM traffic per FLOP drops
 // by a third (the kernel is otherwise L2-bandwidth-bound); the MMA / TMEM / epilogue path is unchanged.
 template <int BN, bool A_MN, bool B_MN, int MC, class Epi>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(kGemmThreadsMax, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                         int N, int K, Epi epi) {
     using C = GemmCfg<BN>;
@@ -82,7 +121,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 4);
+            mbar_init(&tempty[s], EpiWarps<Epi>::value);
         }
         fence_barrier_init();
     }
@@ -181,7 +220,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        const int wq = warp - 4;
+        const int wq = warp - 4;  // epilogue warp index
         int acc = 0;
         uint32_t aphase = 0;
         for (int t = cid; t < tiles; t += nclusters) {
@@ -190,15 +229,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const int m0 = (mt_ * MC + rank) * BM, n0 = nt_ * BN;
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
-            const int row = m0 + wq * 32 + lane;
-            const uint32_t base = tmem + acc * BN + (static_cast<uint32_t>(wq * 32) << 16);
-#pragma unroll 1
-            for (int c = 0; c < BN / 16; ++c) {
-                uint32_t r[16];
-                tmem_ld16(base + c * 16, r);
-                tmem_wait_ld();
-                epi(row, n0 + c * 16, reinterpret_cast<const float*>(r), 16);
-            }
+            epilogue_rows<BN>(tmem + acc * BN, wq, lane, m0, n0, epi);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -235,7 +266,7 @@ struct Gemm2Cfg {
 };
 
 template <int BN, bool A_MN, bool B_MN, class Epi>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(kGemmThreadsMax, 1)
     gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                          int N, int K, Epi epi) {
     using C = Gemm2Cfg<BN>;
@@ -267,7 +298,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+            mbar_init(&tempty[s], 2 * EpiWarps<Epi>::value);  // epilogue warps of both CTAs (leader's is used)
         }
         fence_barrier_init();
     }
@@ -353,7 +384,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        const int wq = warp - 4;
+        const int wq = warp - 4;  // epilogue warp index
         const uint32_t tempty_leader = mapa(smem_u32(tempty), 0);
         int acc = 0;
         uint32_t aphase = 0;
@@ -363,15 +394,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const int m0 = mt_ * 2 * BM + rank * BM, n0 = nt_ * BN;
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
-            const int row = m0 + wq * 32 + lane;
-            const uint32_t base = tmem + acc * BN + (static_cast<uint32_t>(wq * 32) << 16);
-#pragma unroll 1
-            for (int c = 0; c < BN / 16; ++c) {
-                uint32_t r[16];
-                tmem_ld16(base + c * 16, r);
-                tmem_wait_ld();
-                epi(row, n0 + c * 16, reinterpret_cast<const float*>(r), 16);
-            }
+            epilogue_rows<BN>(tmem + acc * BN, wq, lane, m0, n0, epi);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);

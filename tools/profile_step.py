@@ -12,6 +12,7 @@ from paper_2510_17519_b200.capi import Context, mgv_flow_sample, paper_config  #
 ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--grid", default="16,45,80")
+ap.add_argument("--kernels", action="store_true")
 args = ap.parse_args()
 grid = tuple(int(x) for x in args.grid.split(","))
 cfg = paper_config(depth=1)
@@ -30,3 +31,21 @@ ds[0].coords, ds[0].clean_rows, ds[0].noise, ds[0].t = d_coords.data_ptr(), d_cl
 for k in range(1 + args.steps):
     loss, gn = ctx.flow_step_device(ds, d_text.data_ptr(), 64, 8.0)
     print(f"step {k}: loss {loss:.6f} grad_norm {gn:.6f} ms {ctx.last_step_ms():.2f} launches {ctx.last_step_launches()}")
+
+if args.kernels and args.steps > 0:
+    # per-kernel device time over `steps` profiled steps (CUPTI activity records)
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for k in range(args.steps):
+            ctx.flow_step_device(ds, d_text.data_ptr(), 64, 8.0)
+        torch.cuda.synchronize()
+    tot, cnt = {}, {}
+    for e in prof.events():
+        if e.device_type.name == "CUDA":
+            tot[e.name] = tot.get(e.name, 0.0) + e.device_time_total / 1000.0
+            cnt[e.name] = cnt.get(e.name, 0) + 1
+    T = sum(tot.values())
+    print(f"total kernel time per step: {T / args.steps:.2f} ms")
+    for k, v in sorted(tot.items(), key=lambda x: -x[1])[:40]:
+        print(f"  {v / args.steps:8.3f} ms {100 * v / T:5.1f}% x{cnt[k] // args.steps:3d}  {k[:110]}")
