@@ -13,6 +13,7 @@
 // once per step by a tiled transpose, so no MMA ever splits head_dim 144 into
 // 128 + 16.  The MMA warp issues the next tile's S/dP products under the
 // current tile's elementwise work.
+#include <algorithm>
 #include <cfloat>
 #include <vector>
 
@@ -156,6 +157,38 @@ __device__ __forceinline__ void store_acc_row(uint32_t taddr, __nv_bfloat16* out
     }
 }
 
+template <int HD>
+__device__ __forceinline__ void store_acc_row_f32(uint32_t taddr, float* out, bool valid) {
+#pragma unroll 1
+    for (int c = 0; c < HD / 16; ++c) {
+        uint32_t r[16];
+        tmem_ld16(taddr + c * 16, r);
+        tmem_wait_ld();
+        if (valid) {
+            float4* dst = reinterpret_cast<float4*>(out + c * 16);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                dst[e] = make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]),
+                                     __uint_as_float(r[4 * e + 2]), __uint_as_float(r[4 * e + 3]));
+        }
+    }
+}
+
+// dV | dK = sum over the query splits in split order (deterministic), to bf16
+__global__ void reduce_dkv_parts(const float* part, int splits, int Nk, int64_t W, __nv_bfloat16* dv, int64_t dv_ld,
+                                 __nv_bfloat16* dk, int64_t dk_ld) {
+    const int64_t n = (int64_t)Nk * 2 * W;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        float acc = 0.0f;
+        for (int z = 0; z < splits; ++z) acc += part[(int64_t)z * n + e];
+        const int64_t row = e / (2 * W), c = e % (2 * W);
+        if (c < W)
+            dv[row * dv_ld + c] = __float2bfloat16_rn(acc);
+        else
+            dk[row * dk_ld + (c - W)] = __float2bfloat16_rn(acc);
+    }
+}
+
 struct BwdMaps {
     CUtensorMap a128, a32, b128, b32;  // row tiles (dkv: K, V ; dq: Q, dO)
     CUtensorMap ta, tb;                // transposed tiles (dkv: Q^T, dO^T ; dq: K^T, V^T)
@@ -195,8 +228,11 @@ __device__ __forceinline__ void row_to_tmem(uint32_t taddr, const __nv_bfloat16*
 // issue order  dV(i) -> S^T(i+1) -> dK(i) -> dP^T(i+1)  keeps every overwrite behind its reader and
 // lets the softmax of step i+1 run under dK(i) and dP^T(i+1).
 // TMEM: S^T|P^T [0,64)  dP^T|dS^T [64,128)  dV [128,128+HD)  dK [DK,DK+HD)  K (bf16 pairs) after.
+// gridDim.z > 1 splits the query range (few key tiles, e.g. cross-attention over 64 text tokens):
+// split z then writes fp32 partial dV | dK rows to part[z] (Nk x 2 heads*HD) for reduce_dkv_parts.
 template <int HD>
-__global__ void __launch_bounds__(384, 1) attn_bwd_dkv_tc_kernel(const __grid_constant__ BwdMaps tm, AttnBwdProblem p) {
+__global__ void __launch_bounds__(384, 1) attn_bwd_dkv_tc_kernel(const __grid_constant__ BwdMaps tm, AttnBwdProblem p,
+                                                                 float* part) {
     constexpr int BKV = 128, BQ = 64, NST = 5;
     using T = BT<HD>;
     constexpr int S_COL = 0, DP_COL = 64, DV_COL = 128, DK_COL = 128 + ((HD + 15) / 16) * 16;
@@ -224,7 +260,9 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_tc_kernel(const __grid_co
     const AttnProblem& f = p.f;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int h = blockIdx.y, k0 = blockIdx.x * BKV;
-    const int nq = (f.Nq + BQ - 1) / BQ;
+    const int nq_all = (f.Nq + BQ - 1) / BQ;
+    const int i0 = static_cast<int>((int64_t)blockIdx.z * nq_all / gridDim.z);
+    const int nq = static_cast<int>((int64_t)(blockIdx.z + 1) * nq_all / gridDim.z) - i0;  // this split's tiles
     const int col = h * HD;
 
     if (threadIdx.x == 0) {
@@ -256,10 +294,11 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_tc_kernel(const __grid_co
                 if (i >= NST) mbar_wait(&qd_empty[st], ((i / NST) - 1) & 1);
                 // Q^T / dO^T tiles + this tile's lse and D rows (lse/D padded per head to a multiple of 64)
                 mbar_arrive_expect_tx(&qd_full[st], 2 * T::T_TILE + 2 * BQ * 4);
-                tma_load_2d(sQt + st * T::T_TILE, &tm.ta, &qd_full[st], i * BQ, col);
-                tma_load_2d(sdOt + st * T::T_TILE, &tm.tb, &qd_full[st], i * BQ, col);
-                bulk_load(sLse + st * BQ, f.lse + (int64_t)h * lse_stride(f) + i * BQ, BQ * 4, &qd_full[st]);
-                bulk_load(sD + st * BQ, p.Dvec + (int64_t)h * lse_stride(f) + i * BQ, BQ * 4, &qd_full[st]);
+                const int qt = (i0 + i) * BQ;
+                tma_load_2d(sQt + st * T::T_TILE, &tm.ta, &qd_full[st], qt, col);
+                tma_load_2d(sdOt + st * T::T_TILE, &tm.tb, &qd_full[st], qt, col);
+                bulk_load(sLse + st * BQ, f.lse + (int64_t)h * lse_stride(f) + qt, BQ * 4, &qd_full[st]);
+                bulk_load(sD + st * BQ, p.Dvec + (int64_t)h * lse_stride(f) + qt, BQ * 4, &qd_full[st]);
             }
         }
     } else if (warp == 1) {
@@ -330,7 +369,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_tc_kernel(const __grid_co
             tmem_wait_ld();
             const float* lse2 = sLse + st * BQ + hf * HQ;
             const float* Dq = sD + st * BQ + hf * HQ;
-            const int qb = i * BQ + hf * HQ;
+            const int qb = (i0 + i) * BQ + hf * HQ;
             const bool full = qb + HQ <= f.Nq;
             uint32_t pk[HQ / 2];
 #pragma unroll
@@ -361,12 +400,17 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_tc_kernel(const __grid_co
         if (nq > 0) mbar_wait(acc_done, 0);
         tc_fence_after();
         const bool valid = kvv && nq > 0;
-        if (hf == 0)
+        if (part) {  // fp32 partial rows of this query split: [dV | dK]
+            const int64_t W = (int64_t)f.heads * HD;
+            float* prow = part + ((int64_t)blockIdx.z * f.Nk + (kvv ? kv : 0)) * 2 * W + (hf ? W : 0) + col;
+            store_acc_row_f32<HD>(tmem + lane_base + (hf ? DK_COL : DV_COL), prow, kvv);
+        } else if (hf == 0) {
             store_acc_row<HD>(tmem + lane_base + DV_COL,
                               static_cast<__nv_bfloat16*>(p.dv) + (int64_t)kv * p.dv_ld + col, valid);
-        else
+        } else {
             store_acc_row<HD>(tmem + lane_base + DK_COL,
                               static_cast<__nv_bfloat16*>(p.dk) + (int64_t)kv * p.dk_ld + col, valid);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -608,8 +652,23 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
             MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             set = true;
         }
-        attn_bwd_dkv_tc_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads), 384, smem, s>>>(m, p); ::mgv::note_launch();
+        // few key tiles (cross-attention): split the query range so the grid still covers the SMs
+        const int kv_ctas = (f.Nk + 127) / 128 * f.heads, nq_all = (f.Nq + 63) / 64;
+        const int splits = std::max(1, std::min({num_sms() / std::max(kv_ctas, 1), nq_all / 8, 16}));
+        float* part = nullptr;
+        if (splits > 1) MGV_CUDA(cudaMallocAsync(&part, sizeof(float) * splits * f.Nk * 2 * W, s));
+        attn_bwd_dkv_tc_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem, s>>>(m, p, part);
+        ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
+        if (splits > 1) {
+            const int64_t n = (int64_t)f.Nk * 2 * W;
+            reduce_dkv_parts<<<static_cast<int>(std::min<int64_t>((n + 255) / 256, 4096)), 256, 0, s>>>(
+                part, splits, f.Nk, W, static_cast<__nv_bfloat16*>(p.dv), p.dv_ld, static_cast<__nv_bfloat16*>(p.dk),
+                p.dk_ld);
+            ::mgv::note_launch();
+            MGV_CUDA(cudaGetLastError());
+            MGV_CUDA(cudaFreeAsync(part, s));
+        }
     }
     {
         BwdMaps m;

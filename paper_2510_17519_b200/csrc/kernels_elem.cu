@@ -767,24 +767,41 @@ void colsum(const T* Y, int64_t ld, int N, int C, float* part, cudaStream_t s) {
     colsum_kernel<T><<<grid, 256, 0, s>>>(Y, ld, N, C, part); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
-__global__ void reduce_chunks_kernel(const float* part, int chunks, int groups, int C, float* out, int64_t out_stride,
-                                     float alpha, int accumulate) {
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= (int64_t)groups * C) return;
-    const int gidx = static_cast<int>(e / C), j = static_cast<int>(e % C);
+// Block = 32 consecutive (group, column) entries x 8 warps.  Warp r sums chunks r, r + 8, r + 16, ... and
+// the 8 partial sums are then added in warp order: a fixed reduction tree, so the result is deterministic
+// while 8 x total/32 warps share the (chunks x total) reads.
+__global__ void __launch_bounds__(256) reduce_chunks_kernel(const float* part, int chunks, int groups, int C,
+                                                            float* out, int64_t out_stride, float alpha,
+                                                            int accumulate) {
+    __shared__ float red[8][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t total = (int64_t)groups * C;
+    const int64_t e = blockIdx.x * 32LL + tx;
     float acc = 0.0f;
-    for (int c = 0; c < chunks; ++c) acc += part[((int64_t)c * groups + gidx) * C + j];
-    float* o = out + gidx * out_stride + j;
-    *o = accumulate ? *o + alpha * acc : alpha * acc;
+    if (e < total) {
+        int c = ty;
+#pragma unroll 4
+        for (; c < chunks; c += 8) acc += part[(int64_t)c * total + e];
+    }
+    red[ty][tx] = acc;
+    __syncthreads();
+    if (ty == 0 && e < total) {
+        float sum = 0.0f;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) sum += red[r][tx];
+        const int gidx = static_cast<int>(e / C), j = static_cast<int>(e % C);
+        float* o = out + gidx * out_stride + j;
+        *o = accumulate ? *o + alpha * sum : alpha * sum;
+    }
 }
 void reduce_chunks(const float* part, int chunks, int C, float* out, float alpha, int accumulate, cudaStream_t s) {
-    reduce_chunks_kernel<<<grid_for(C), 256, 0, s>>>(part, chunks, 1, C, out, 0, alpha, accumulate); ::mgv::note_launch();
+    reduce_chunks_kernel<<<(C + 31) / 32, 256, 0, s>>>(part, chunks, 1, C, out, 0, alpha, accumulate); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 void reduce_chunks_grouped(const float* part, int chunks, int groups, int C, float* out, int64_t out_stride,
                            float alpha, int accumulate, cudaStream_t s) {
-    reduce_chunks_kernel<<<grid_for((int64_t)groups * C), 256, 0, s>>>(part, chunks, groups, C, out, out_stride, alpha,
-                                                                     accumulate); ::mgv::note_launch();
+    reduce_chunks_kernel<<<static_cast<int>(((int64_t)groups * C + 31) / 32), 256, 0, s>>>(
+        part, chunks, groups, C, out, out_stride, alpha, accumulate); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 

@@ -88,7 +88,7 @@ def call_bwd(tc, qbuf, kbuf, o, lse, dO, Nq, Nk, heads, hd, q_splits=1):
 @pytest.mark.parametrize("tc", [1, 0])
 @pytest.mark.parametrize("Nq,Nk,heads,hd,unit", [(300, 300, 2, 144, True), (1000, 64, 3, 144, False),
                                                  (256, 256, 2, 64, False), (2048, 2048, 2, 144, True),
-                                                 (130, 400, 1, 128, False)])
+                                                 (130, 400, 1, 128, False), (4000, 64, 2, 144, False)])
 def test_attn_bwd(tc, Nq, Nk, heads, hd, unit):
     qbuf, kbuf, H = make(Nq, Nk, heads, hd, unit, 7 * Nq + Nk + hd)
     o, lse = call_fwd(1, qbuf, kbuf, Nq, Nk, heads, hd)

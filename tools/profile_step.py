@@ -41,11 +41,14 @@ if args.kernels and args.steps > 0:
             ctx.flow_step_device(ds, d_text.data_ptr(), 64, 8.0)
         torch.cuda.synchronize()
     tot, cnt = {}, {}
+    per = __import__("os").environ.get("PER_LAUNCH")
     for e in prof.events():
+        if per and e.device_type.name == "CUDA" and per in e.name:
+            print(f"  launch {e.device_time_total / 1000.0:9.3f} ms  {e.name[:60]}")
         if e.device_type.name == "CUDA":
             tot[e.name] = tot.get(e.name, 0.0) + e.device_time_total / 1000.0
             cnt[e.name] = cnt.get(e.name, 0) + 1
     T = sum(tot.values())
     print(f"total kernel time per step: {T / args.steps:.2f} ms")
-    for k, v in sorted(tot.items(), key=lambda x: -x[1])[:40]:
+    for k, v in sorted(tot.items(), key=lambda x: -x[1])[:int(__import__("os").environ.get("TOPK", "40"))]:
         print(f"  {v / args.steps:8.3f} ms {100 * v / T:5.1f}% x{cnt[k] // args.steps:3d}  {k[:110]}")
