@@ -24,17 +24,31 @@
 
 namespace mgv {
 
+// dK/dV pass variant: 0 = single-CTA kernel (default), 1 = 2-CTA cluster kernel.  The cluster kernel is
+// correct (tests/test_attn_gpu.py runs both) but measured 2.5x slower at 57.6K tokens: its two per-step
+// cross-SM handoffs (P^T out, dS^T back) put ~3600 clk of exchange latency on every step; kept selectable
+// (mgv_dev_set_dkv_pair) as the starting point for a deeper-pipelined exchange.
+static int g_dkv_pair = 0;
+
 namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 
 #ifdef MGV_ATTN_TRACE  // development timeline of one CTA (tools/trace_attn.py); not in the product build
 __device__ unsigned long long g_attn_trace[8][64];
+__device__ unsigned long long g_attn_trace2[8][64];
 #define ATR(ev, j)                                                                              \
     do {                                                                                        \
         if (blockIdx.x == 7 && blockIdx.y == 0 && (j) < 64) g_attn_trace[ev][j] = clock64();   \
     } while (0)
+#define ATR2(ev, j)                                                                                  \
+    do {                                                                                             \
+        if ((blockIdx.x >> 1) == 7 && blockIdx.y == 0 && (j) < 64) g_attn_trace2[ev][j] = clock64(); \
+    } while (0)
 #else
+#define ATR2(ev, j) \
+    do {            \
+    } while (0)
 #define ATR(ev, j) \
     do {           \
     } while (0)
@@ -418,6 +432,325 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_tc_kernel(const __grid_co
     if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// =====================================================================================  dK / dV, CTA pair
+// The dK/dV pass with its TMEM split over a 2-CTA cluster that owns one 128-key tile: head_dim is cut
+// into LO + HI columns (144 = 80 + 64, each a valid MMA N).  CTA 0 keeps K in TMEM and computes
+// S^T = K Q^T and P = exp(S^T - lse); CTA 1 keeps V in TMEM and computes dP^T = V dO^T and
+// dS = P (dP - D).  P^T and dS^T (bf16, 16 KB per step) are exchanged through distributed shared
+// memory, so each CTA accumulates dV and dK for its own head_dim columns:
+//   CTA 0:  dV[:, :LO] += P^T dO[:, :LO]  (TS, P^T in TMEM)    dK[:, :LO] += dS^T Q[:, :LO]  (SS, received)
+//   CTA 1:  dV[:, LO:] += P^T dO[:, LO:]  (SS, received)       dK[:, LO:] += dS^T Q[:, LO:]  (TS)
+// Every product now has a TMEM-resident or 64-token shared-memory A operand instead of re-reading the
+// 128 x 144 K / V tile from shared memory each step, and the per-SM tensor work per step drops from
+// 4 to ~2.4 k-step units.  The exchange buffers are double-buffered; receivers release them with
+// cluster-scope mbarrier arrivals (tensor-core reads via multicast tcgen05.commit).
+// TMEM (per CTA): S^T|P^T or dP^T|dS^T [0,64) [64,128)   dV part [128, 128+W)   dK part after   K or V.
+template <int HD>
+struct PairSplit {
+    static constexpr int LO = ((HD / 2 + 15) / 16) * 16, HI = HD - LO;
+    static_assert(HI > 0 && HI % 16 == 0, "head_dim split must give two multiple-of-16 halves");
+};
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "LAB_WAITC:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@P1 bra.uni DONEC;\n\t"
+        "bra.uni LAB_WAITC;\n\t"
+        "DONEC:\n\t}" ::"r"(addr),
+        "r"(parity), "r"(1000000)
+        : "memory");
+}
+// Exchanged P^T / dS^T tiles are two 128 x 32 K-major SW64 tiles (query columns [0,32) and [32,64)), so
+// the 32 rows x 32 columns a compute warp produces are one contiguous 2 KB block: the warp stages it in
+// its own shared memory and one lane bulk-copies it into the peer CTA (cp.async.bulk shared::cluster),
+// completing on the peer's mbarrier.
+__device__ __forceinline__ uint32_t sw64_off(int row, int chunk) {
+    return row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4);
+}
+__device__ __forceinline__ void st_row_sw64(uint32_t block, int row, const uint32_t* pk) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(block + sw64_off(row, u)), "r"(pk[4 * u]),
+                     "r"(pk[4 * u + 1]), "r"(pk[4 * u + 2]), "r"(pk[4 * u + 3])
+                     : "memory");
+}
+__device__ __forceinline__ void ld_row_sw64(uint32_t block, int row, float* v) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        uint32_t w[4];
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                     : "r"(block + sw64_off(row, u)));
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+            v[8 * u + 2 * e] = f.x;
+            v[8 * u + 2 * e + 1] = f.y;
+        }
+    }
+}
+__device__ __forceinline__ void bulk_copy_to_peer(uint32_t dst_cluster, uint32_t src, uint32_t bytes,
+                                                  uint32_t bar_cluster) {
+    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     dst_cluster),
+                 "r"(src), "r"(bytes), "r"(bar_cluster)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// remote arrive that also announces `bytes` of complete_tx still to come on that barrier phase
+__device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t bar_cluster, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar_cluster),
+                 "r"(bytes)
+                 : "memory");
+}
+// D[128 x N] (+)= A[128 x 64] . B with A the exchanged pair of SW64 tiles and B read K-major (N rows)
+template <int N>
+__device__ __forceinline__ void mma_x64pair_x_t(uint32_t d, uint32_t a, uint32_t bt, bool acc_first) {
+    constexpr uint32_t id = idesc_bf16_f32(128, N, false, false);
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks)
+        umma_f16_ss(d, smem_desc(a + (ks >> 1) * 8192 + (ks & 1) * 32, 16, 512, kSwizzle64),
+                    smem_desc(bt + ks * 32, 16, 1024, kSwizzle128), id, (acc_first || ks > 0) ? 1u : 0u);
+}
+
+template <int HD>
+__global__ void __launch_bounds__(384, 1) attn_bwd_dkv_pair_kernel(const __grid_constant__ BwdMaps tm, AttnBwdProblem p) {
+    constexpr int BKV = 128, BQ = 64, HQ = 32, NST = 4;
+    using T = BT<HD>;
+    constexpr int LO = PairSplit<HD>::LO, HI = PairSplit<HD>::HI;
+    // TMEM: S^T / dP^T [0,64) [64,128); own packed P^T / dS^T [128,160) [160,192); dV part, dK part; K / V
+    constexpr int X_COL = 128, DV_COL = 192, A_COL = DV_COL + 2 * LO;
+    static_assert(A_COL + HD / 2 <= 512, "TMEM budget");
+    constexpr int XB = BKV * BQ * 2;  // one exchanged bf16 tile (16 KB)
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQt = smem;                    // [NST]
+    uint8_t* sdOt = sQt + NST * T::T_TILE;  // [NST]
+    uint8_t* xbuf = sdOt + NST * T::T_TILE;  // [2] received tiles: CTA 0 <- dS^T, CTA 1 <- P^T
+    uint8_t* stg = xbuf + 2 * XB;            // [2][8 warps] 2 KB staging blocks of the outgoing tile
+    float* sRow = reinterpret_cast<float*>(stg + 2 * XB);  // [NST][64]: lse (CTA 0) or D (CTA 1)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sRow + NST * BQ);
+    uint64_t* qd_full = bars;             // [NST]
+    uint64_t* qd_empty = bars + NST;      // [NST]
+    uint64_t* s_full = bars + 2 * NST;    // [2] S^T (CTA 0) / dP^T (CTA 1) in TMEM
+    uint64_t* s_empty = s_full + 2;       // [2] ... read by the compute warps
+    uint64_t* x_full = s_full + 4;        // [2] own packed P^T / dS^T stored to TMEM
+    uint64_t* x_done = s_full + 6;        // [2] ... consumed by this CTA's MMA
+    uint64_t* recv = s_full + 8;          // [2] peer's tile landed in xbuf
+    uint64_t* xfree = s_full + 10;        // [2] the peer may overwrite my outgoing buffer b
+    uint64_t* acc_done = s_full + 12;
+    uint64_t* a_ready = s_full + 13;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 14);
+
+    const AttnProblem& f = p.f;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_ctarank(), peer = rank ^ 1;
+    const int h = blockIdx.y, k0 = (blockIdx.x >> 1) * BKV;
+    const int nq = (f.Nq + BQ - 1) / BQ;
+    const int col = h * HD;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&qd_full[i], 1);
+            mbar_init(&qd_empty[i], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&s_full[b], 1);
+            mbar_init(&s_empty[b], 8);
+            mbar_init(&x_full[b], 8);
+            mbar_init(&x_done[b], 1);
+            mbar_init(&recv[b], 8);
+            // CTA 0's outgoing P^T buffer is freed by CTA 1's dV MMA (commit) and its 8 compute warps;
+            // CTA 1's outgoing dS^T buffer by CTA 0's dK MMA
+            mbar_init(&xfree[b], rank == 0 ? 9 : 1);
+        }
+        mbar_init(acc_done, 1);
+        mbar_init(a_ready, 4);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();  // barriers of both CTAs initialised before any remote arrival
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t xbuf_peer = mapa(smem_u32(xbuf), peer);
+    const uint32_t recv_peer = mapa(smem_u32(recv), peer);
+    const uint32_t xfree_peer = mapa(smem_u32(xfree), peer);
+
+    if (warp == 0) {
+        if (elect_one()) {
+            const float* rowsrc = rank == 0 ? f.lse : p.Dvec;
+            for (int i = 0; i < nq; ++i) {
+                const int st = i % NST;
+                if (i >= NST) mbar_wait(&qd_empty[st], ((i / NST) - 1) & 1);
+                mbar_arrive_expect_tx(&qd_full[st], 2 * T::T_TILE + BQ * 4);
+                tma_load_2d(sQt + st * T::T_TILE, &tm.ta, &qd_full[st], i * BQ, col);
+                tma_load_2d(sdOt + st * T::T_TILE, &tm.tb, &qd_full[st], i * BQ, col);
+                bulk_load(sRow + st * BQ, rowsrc + (int64_t)h * lse_stride(f) + i * BQ, BQ * 4, &qd_full[st]);
+            }
+        }
+    } else if (warp == 1) {
+        // CTA 0: S^T(i) = K Q^T ; CTA 1: dP^T(i) = V dO^T   (TS, A resident in TMEM), two steps ahead
+        auto issue_s = [&](int i) {
+            const int st = i % NST;
+            mbar_wait(&qd_full[st], (i / NST) & 1);
+            if (i >= 2) mbar_wait(&s_empty[i & 1], ((i - 2) >> 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                mma_tmem_rows_x_t<HD>(tmem + (i & 1) * 64, tmem + A_COL,
+                                      smem_u32((rank == 0 ? sQt : sdOt) + st * T::T_TILE));
+                umma_commit(&s_full[i & 1]);
+            }
+            __syncwarp();
+        };
+        auto qt_of = [&](int i) { return smem_u32(sQt + (i % NST) * T::T_TILE); };
+        auto dot_of = [&](int i) { return smem_u32(sdOt + (i % NST) * T::T_TILE); };
+        mbar_wait(a_ready, 0);
+        if (nq > 0) issue_s(0);
+        if (nq > 1) issue_s(1);
+        if (rank == 0) {
+            // per step i:  S^T(i+2) -> dV(i) [own P^T_i] -> dK(i-1) [dS^T_{i-1} from CTA 1, one step behind]
+            auto issue_dk = [&](int j) {
+                mbar_wait_cluster(&recv[j & 1], (j >> 1) & 1);
+                tc_fence_after();
+                if (elect_one()) {
+                    mma_x64pair_x_t<LO>(tmem + DV_COL + LO, smem_u32(xbuf + (j & 1) * XB), qt_of(j), j > 0);
+                    umma_commit_mc(&xfree[j & 1], 1u << peer);  // CTA 1 may refill xbuf[j & 1]
+                    umma_commit(&qd_empty[j % NST]);
+                    if (j == nq - 1) umma_commit(acc_done);
+                }
+                __syncwarp();
+            };
+            for (int i = 0; i < nq; ++i) {
+                const int b = i & 1;
+                if (i + 2 < nq) issue_s(i + 2);
+                mbar_wait(&x_full[b], (i >> 1) & 1);
+                tc_fence_after();
+                if (elect_one()) {
+                    mma_tmem_x_t<LO>(tmem + DV_COL, tmem + X_COL + b * 32, dot_of(i), i > 0);
+                    umma_commit(&x_done[b]);
+                }
+                __syncwarp();
+                if (i >= 1) issue_dk(i - 1);
+            }
+            if (nq > 0) issue_dk(nq - 1);
+        } else {
+            // per step i:  dP^T(i+2) -> dV(i) [P^T_i from CTA 0] -> dK(i) [own dS^T_i]
+            for (int i = 0; i < nq; ++i) {
+                const int b = i & 1;
+                if (i + 2 < nq) issue_s(i + 2);
+                mbar_wait_cluster(&recv[b], (i >> 1) & 1);
+                tc_fence_after();
+                if (elect_one()) {
+                    mma_x64pair_x_t<HI>(tmem + DV_COL, smem_u32(xbuf + b * XB), dot_of(i) + LO * 128, i > 0);
+                    umma_commit_mc(&xfree[b], 1u << peer);  // (with CTA 1's compute warps) CTA 0 may refill
+                }
+                __syncwarp();
+                mbar_wait(&x_full[b], (i >> 1) & 1);
+                tc_fence_after();
+                if (elect_one()) {
+                    mma_tmem_x_t<HI>(tmem + DV_COL + HI, tmem + X_COL + b * 32, qt_of(i) + LO * 128, i > 0);
+                    umma_commit(&x_done[b]);
+                    umma_commit(&qd_empty[i % NST]);
+                    if (i == nq - 1) umma_commit(acc_done);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp >= 4) {
+        // two warps per TMEM lane group: warp hf handles query columns [32 hf, 32 hf + 32) of each step
+        const int g = warp & 3, hf = (warp - 4) >> 2, row = g * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(g * 32) << 16;
+        const int kv = k0 + row;
+        const bool kvv = kv < f.Nk;
+        if (hf == 0) {  // stage K (CTA 0) or V (CTA 1) rows as the A operand
+            const void* src = rank == 0 ? f.k : f.v;
+            const int64_t ld = rank == 0 ? f.k_ld : f.v_ld;
+            row_to_tmem<HD>(tmem + lane_base + A_COL,
+                            static_cast<const __nv_bfloat16*>(src) + (int64_t)(kvv ? kv : 0) * ld + col, kvv);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(a_ready);
+        }
+        for (int i = 0; i < nq; ++i) {
+            const int st = i % NST, b = i & 1;
+            mbar_wait(&qd_full[st], (i / NST) & 1);  // lse / D rows of this tile
+            mbar_wait(&s_full[b], (i >> 1) & 1);
+            tc_fence_after();
+            if (warp == 4 && lane == 0) ATR2(rank * 4 + 0, i);
+            float x[HQ];
+            tmem_ld32(tmem + lane_base + b * 64 + hf * HQ, reinterpret_cast<uint32_t*>(x));
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[b]);
+            const float* rv = sRow + st * BQ + hf * HQ;
+            const int qb = i * BQ + hf * HQ;
+            uint32_t pk[HQ / 2];
+            if (rank == 0) {  // P = exp(S^T - lse)
+                if (qb + HQ <= f.Nq) {
+#pragma unroll
+                    for (int c = 0; c < HQ; ++c) x[c] = ex2f((x[c] - rv[c]) * kLog2e);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < HQ; ++c) x[c] = qb + c < f.Nq ? ex2f((x[c] - rv[c]) * kLog2e) : 0.0f;
+                }
+            } else {  // dS = P (dP - D), P from CTA 0
+                mbar_wait_cluster(&recv[b], (i >> 1) & 1);
+                float pv[HQ];
+                ld_row_sw64(smem_u32(xbuf + b * XB) + hf * (XB / 2) + g * 2048, lane, pv);
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(xfree_peer + b * 8);  // done reading xbuf[b]
+#pragma unroll
+                for (int c = 0; c < HQ; ++c) x[c] = pv[c] * (x[c] - rv[c]);  // autodiff.cpp:820
+            }
+#pragma unroll
+            for (int c = 0; c < HQ; c += 2) pk[c / 2] = pack_bf16(x[c], x[c + 1]);
+            if (i >= 2) {
+                mbar_wait(&x_done[b], ((i - 2) >> 1) & 1);  // own MMA done with step i-2's packed tile
+                tc_fence_after();
+            }
+            tmem_st16(tmem + lane_base + X_COL + b * 32 + hf * (HQ / 2), pk);
+            tmem_wait_st();
+            if (warp == 4 && lane == 0) ATR2(rank * 4 + 1, i);
+            // stage this warp's 32 x 32 block (SW64) and bulk-copy it into the peer's tile
+            const uint32_t blk = smem_u32(stg) + (b * 8 + hf * 4 + g) * 2048;
+            if (i >= 2) {
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // step i-2's copy read
+                __syncwarp();
+            }
+            st_row_sw64(blk, lane, pk);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (i >= 2) mbar_wait_cluster(&xfree[b], ((i - 2) >> 1) & 1);  // peer done with step i-2's tile
+            if (warp == 4 && lane == 0) ATR2(rank * 4 + 2, i);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&x_full[b]);
+                mbar_arrive_expect_tx_cluster(recv_peer + b * 8, 2048);
+                bulk_copy_to_peer(xbuf_peer + b * XB + hf * (XB / 2) + g * 2048, blk, 2048, recv_peer + b * 8);
+            }
+            if (warp == 4 && lane == 0) ATR2(rank * 4 + 3, i);
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // outgoing copies done
+        if (nq > 0) mbar_wait(acc_done, 0);
+        tc_fence_after();
+        const bool valid = kvv && nq > 0;
+        const int W = rank == 0 ? LO : HI, c0 = rank == 0 ? 0 : LO;
+        __nv_bfloat16* out = hf == 0 ? static_cast<__nv_bfloat16*>(p.dv) + (int64_t)kv * p.dv_ld
+                                     : static_cast<__nv_bfloat16*>(p.dk) + (int64_t)kv * p.dk_ld;
+        store_acc_row<HD>(tmem + lane_base + (hf == 0 ? DV_COL : DV_COL + W), out + col + c0, valid, 0, W / 16);
+    }
+    tc_fence_before();
+    cluster_sync();  // no CTA leaves while its peer may still write into it
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 // =====================================================================================  dQ
 // Q and dO stay in TMEM for the whole CTA (they are the A operands of S = Q K^T and dP = dO V^T), so
 // every MMA of this pass is TS-form: only the 64-token K^T / V^T tiles are read from shared memory,
@@ -657,7 +990,31 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
         const int splits = std::max(1, std::min({num_sms() / std::max(kv_ctas, 1), nq_all / 8, 16}));
         float* part = nullptr;
         if (splits > 1) MGV_CUDA(cudaMallocAsync(&part, sizeof(float) * splits * f.Nk * 2 * W, s));
-        attn_bwd_dkv_tc_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem, s>>>(m, p, part);
+        if (splits == 1 && g_dkv_pair) {
+            // one 2-CTA cluster per key tile (head_dim split over the pair, P^T / dS^T exchanged via DSMEM)
+            const int psmem = 8 * T::T_TILE + 4 * 128 * 64 * 2 + 4 * 64 * 4 + 256 + 1024;
+            static bool pset = false;
+            if (!pset) {
+                MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_pair_kernel<HD>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, psmem));
+                pset = true;
+            }
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(2 * ((f.Nk + 127) / 128), f.heads);
+            cfg.blockDim = dim3(384);
+            cfg.dynamicSmemBytes = psmem;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            MGV_CUDA(cudaLaunchKernelEx(&cfg, attn_bwd_dkv_pair_kernel<HD>, m, p));
+        } else {
+            attn_bwd_dkv_tc_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem, s>>>(m, p, part);
+        }
         ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
         if (splits > 1) {
@@ -738,4 +1095,33 @@ void attn_bwd_tc(const AttnBwdProblem& p, cudaStream_t s) {
 extern "C" int mgv_dev_attn_trace(unsigned long long* out) {
     return cudaMemcpyFromSymbol(out, mgv::g_attn_trace, sizeof(mgv::g_attn_trace)) == cudaSuccess ? 0 : 1;
 }
+extern "C" int mgv_dev_attn_trace2(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, mgv::g_attn_trace2, sizeof(mgv::g_attn_trace2)) == cudaSuccess ? 0 : 1;
+}
 #endif
+
+extern "C" int mgv_dev_set_dkv_pair(int on) {
+    mgv::g_dkv_pair = on ? 1 : 0;
+    return 0;
+}
+
+// diagnostics: how many 2-CTA clusters of the dK/dV pair kernel can be resident at once (head_dim 144)
+extern "C" int mgv_dev_dkv_pair_clusters() {
+    using T = mgv::BT<144>;
+    const int psmem = 8 * T::T_TILE + 4 * 128 * 64 * 2 + 4 * 64 * 4 + 256 + 1024;
+    cudaFuncSetAttribute(mgv::attn_bwd_dkv_pair_kernel<144>, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * 450, 24);
+    cfg.blockDim = dim3(384);
+    cfg.dynamicSmemBytes = psmem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = -1;
+    if (cudaOccupancyMaxActiveClusters(&n, mgv::attn_bwd_dkv_pair_kernel<144>, &cfg) != cudaSuccess) return -1;
+    return n;
+}
