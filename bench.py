@@ -4,8 +4,8 @@
 Workload (BASELINE.json configs[2]): one MUG-V-10B-shaped DiT block (H=3456,
 24 heads x 144, FFN 13824, text 64 x 4096; depth 1 plus the patch / final /
 velocity heads) on a 720p/5s latent 16x90x160x24 -> 16x45x80 = 57,600 tokens,
-the flow-matching training step forward + backward (FlowTrainer::step,
-flowtrain.cpp:257-279, without the AdamW update), one sample per GPU,
+the full flow-matching training step: forward + backward + grad norm + AdamW
+update (FlowTrainer::step, flowtrain.cpp:257-289, optim.cpp:7-24), one sample per GPU,
 synthetic latents and random-init weights.  Multi-GPU = data parallel over
 NCCL (weak scaling: one sample per rank; gradients all-reduced in-library).
 
@@ -39,6 +39,8 @@ sys.path.insert(0, ROOT)
 METRIC = "DiT-block video tokens/sec at 57.6K-token 10B shape; attention TFLOP/s vs peak"
 GRID = (16, 45, 80)  # token grid (U, H', W') of the 720p/5s latent (16, 90, 160, 24)
 H, HEADS, HD, TEXT_L, TEXT_D, PATCH = 3456, 24, 144, 64, 4096, 96
+# AdamW hyper-parameters of the timed training step (optim.hpp:14-18 defaults, small lr)
+ADAMW = dict(lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0)
 REF_SAMPLE = (2, 2, 4)  # bounded CPU sample: latent (U, h, w) = (2, 2, 4) x 24 ch -> grid 2x1x2 = 4 tokens
 
 
@@ -176,6 +178,7 @@ def _ref_worker(args):
     cfg = O.paper_config(depth=1)
     gs = O.gate_std_for(cfg.hidden)
     ref = O.RefModel(cfg, 1 + seed, 2, gs, gs / 4)
+    opt = O.RefAdamW(ADAMW["lr"], ADAMW["beta1"], ADAMW["beta2"], ADAMW["eps"], ADAMW["weight_decay"])
     text = O.Rng(4).normal_tensor((TEXT_L, TEXT_D))
     U, h, w = REF_SAMPLE
     g = O.Rng(3 + seed).uniform_tensor((U, h, w, 24), -1.0, 1.0)
@@ -186,7 +189,8 @@ def _ref_worker(args):
         if conn.recv() != "go":
             break
         t0 = time.perf_counter()
-        ref.flow_fwdbwd(s, text, 8.0, grads=True, with_V=False)
+        out = ref.flow_fwdbwd(s, text, 8.0, grads=True, with_V=False)
+        opt.update_model(ref, out["grads"])  # the full FlowTrainer::step (flowtrain.cpp:257-282)
         times.append(time.perf_counter() - t0)
         conn.send(times[-1])
     conn.close()
@@ -211,7 +215,7 @@ def cpu_baseline_once():
         dt = a.recv()
         p.join()
         return {"value": ref_tokens() / dt, "unit": "tokens/s", "cores": 1, "kind": "reference",
-                "sample": f"reference FlowTrainer::step fwd+bwd (no AdamW), 10B dims depth 1, {ref_tokens()} tokens "
+                "sample": f"reference FlowTrainer::step (fwd+bwd+AdamW), 10B dims depth 1, {ref_tokens()} tokens "
                           f"(latent {REF_SAMPLE[0]}x{REF_SAMPLE[1]}x{REF_SAMPLE[2]}x24), text 64x4096, "
                           f"1 thread: {dt:.1f} s"}
     # numpy port (oracle.py) when the compiled reference is absent
@@ -264,7 +268,7 @@ def run_reference(args, rank, world):
         p.join()
     ms = 1000.0 * sum(step_s) / len(step_s)
     value = procs_n * ref_tokens() / (ms / 1000.0)
-    sample = (f"{procs_n} processes x 1 reference sample each (FlowTrainer::step fwd+bwd without AdamW, 10B dims "
+    sample = (f"{procs_n} processes x 1 reference sample each (FlowTrainer::step fwd+bwd+AdamW, 10B dims "
               f"depth 1, {ref_tokens()} tokens, text 64x4096) per step; bounded stand-in for the 57.6K-token sample, "
               f"which the reference cannot run (637 GB fp64 attention probabilities)")
     print(json.dumps({
@@ -292,6 +296,7 @@ def run_ours(args, rank, world, local):
         uid = [Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx.set_dp(rank, world, uid[0])
+    ctx.set_adamw(**ADAMW)  # the timed step is the full FlowTrainer::step: fwd + bwd + grad norm + AdamW
     ctx.upload(cfg, synthetic_params(cfg, seed=1234))
 
     U, Hp, Wp = GRID
@@ -388,7 +393,7 @@ def run_ours(args, rank, world, local):
         "dtype": "bf16", "data": "synthetic latents + random-init 10B-shaped weights",
         "config": {"workload": "MUG-V 10B DiT block (H3456, 24x144 heads, FFN 13824, text 64x4096), depth 1 + "
                                "patch/final/velocity heads, 720p/5s latent 16x90x160x24 -> 57600 tokens, flow-matching "
-                               "fwd+bwd (FlowTrainer::step without AdamW), 1 sample per GPU",
+                               "fwd+bwd + grad norm + AdamW update (the full FlowTrainer::step), 1 sample per GPU",
                    "tokens_per_sample": N, "samples_per_gpu": 1, "global_batch": world, "parallelism": f"dp{world}",
                    "l2": "working set ~17 GB >> 126 MB L2 (no flush needed)"},
         "roofline": roof,

@@ -83,6 +83,16 @@ mgv_status mgv_ctx_set_dp(mgv_ctx* ctx, int rank, int world, const uint8_t nccl_
  * sharded path.  `size` must divide heads.  Not combinable with mgv_ctx_set_dp. */
 mgv_status mgv_ctx_set_tp(mgv_ctx* ctx, int size, int rank, const uint8_t* nccl_id);
 
+/* AdamW (replaces mugv::AdamW, optim.hpp:12-29 / optim.cpp:7-24): when lr > 0, every mgv_flow_step /
+ * mgv_flow_step_device ends with AdamW::update over all dit.* parameters on device (fp32 masters, m and v
+ * resident, bf16 operand copies refreshed) -- the full FlowTrainer::step (flowtrain.cpp:257-282).  The
+ * update is skipped when the loss is not finite (the step then fails with MGV_ERR_NUMERIC, as the
+ * reference throws before updating).  Uploading parameters resets the optimizer state. */
+mgv_status mgv_ctx_set_adamw(mgv_ctx* ctx, double lr, double beta1, double beta2, double eps, double weight_decay);
+int64_t mgv_adamw_steps(mgv_ctx* ctx); /* AdamW::step_count (optim.hpp:24) */
+/* Read parameter i (sorted-name order, mgv_param_name) back in the reference layout, fp64. */
+mgv_status mgv_param_download(mgv_ctx* ctx, int64_t i, double* out);
+
 /* Upload (or replace) the dit.* ParameterSet.  names/data/numel are n parallel arrays (any order). */
 mgv_status mgv_params_upload(mgv_ctx* ctx, const mgv_dit_cfg* cfg, int64_t n, const char* const* names,
                              const double* const* data, const int64_t* numel);

@@ -20,6 +20,7 @@
 #include <string>
 #include <vector>
 
+#include "mugv/optim.hpp"
 #include "mugv/dit.hpp"
 #include "mugv/flowtrain.hpp"
 
@@ -257,6 +258,51 @@ int ref_dit_forward(void* h, const RefCfg* c, const int64_t* dims, const double*
         std::memcpy(tx.data(), text, sizeof(double) * static_cast<size_t>(tx.numel()));
         dit::TokenGrid o = dit::dit_forward(geom, tx, dit::GlobalSignals{ts, fps}, hh->p, cfg);
         std::memcpy(out, o.tokens.data(), sizeof(double) * static_cast<size_t>(o.tokens.numel()));
+    });
+}
+
+// ---- AdamW::update (optim.cpp:7-24) on caller-owned tensors ----
+void* ref_adamw_create(double lr, double beta1, double beta2, double eps, double weight_decay) {
+    auto* o = new AdamW(lr);
+    o->beta1 = beta1;
+    o->beta2 = beta2;
+    o->eps = eps;
+    o->weight_decay = weight_decay;
+    return o;
+}
+void ref_adamw_destroy(void* o) { delete static_cast<AdamW*>(o); }
+// params[i] (numel[i] doubles) are updated in place from grads[i]; the optimizer keeps m, v by name
+int ref_adamw_update(void* o, int64_t n, const char* const* names, double* const* params, const double* const* grads,
+                     const int64_t* numel) {
+    return guard([&] {
+        ParameterSet ps;
+        std::map<std::string, Tensor> gs;
+        for (int64_t i = 0; i < n; ++i) {
+            Tensor w({numel[i]}), g({numel[i]});
+            std::memcpy(w.data(), params[i], sizeof(double) * static_cast<size_t>(numel[i]));
+            std::memcpy(g.data(), grads[i], sizeof(double) * static_cast<size_t>(numel[i]));
+            ps.set(names[i], w);
+            gs.emplace(names[i], g);
+        }
+        static_cast<AdamW*>(o)->update(ps, gs);
+        for (int64_t i = 0; i < n; ++i)
+            std::memcpy(params[i], ps.at(names[i]).data(), sizeof(double) * static_cast<size_t>(numel[i]));
+    });
+}
+
+// AdamW::update on a parameter handle's own tensors (the reference FlowTrainer::step's last line,
+// flowtrain.cpp:278); grads in ref_params_name order
+int ref_adamw_update_params(void* o, void* h, const double* const* grads) {
+    return guard([&] {
+        auto* hh = static_cast<Handle*>(h);
+        std::map<std::string, Tensor> gs;
+        for (size_t i = 0; i < hh->names.size(); ++i) {
+            const Tensor& w = hh->p.at(hh->names[i]);
+            Tensor g(w.shape());
+            std::memcpy(g.data(), grads[i], sizeof(double) * static_cast<size_t>(w.numel()));
+            gs.emplace(hh->names[i], std::move(g));
+        }
+        static_cast<AdamW*>(o)->update(hh->p, gs);
     });
 }
 

@@ -69,6 +69,12 @@ def declare(L):
     L.mgv_ctx_set_dp.restype = I
     L.mgv_ctx_set_tp.argtypes = [P, I, I, P]
     L.mgv_ctx_set_tp.restype = I
+    L.mgv_ctx_set_adamw.argtypes = [P, D, D, D, D, D]
+    L.mgv_ctx_set_adamw.restype = I
+    L.mgv_adamw_steps.argtypes = [P]
+    L.mgv_adamw_steps.restype = I64
+    L.mgv_param_download.argtypes = [P, I64, P]
+    L.mgv_param_download.restype = I
     L.mgv_params_upload.argtypes = [P, ctypes.POINTER(mgv_dit_cfg), I64, P, P, P]
     L.mgv_params_upload.restype = I
     L.mgv_param_count.argtypes = [P]
@@ -109,7 +115,8 @@ def declare(L):
 
 # symbols include/mugv_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = ["mgv_ctx_create", "mgv_ctx_destroy", "mgv_last_error", "mgv_ctx_set_stream", "mgv_nccl_unique_id",
-           "mgv_ctx_set_dp", "mgv_ctx_set_tp", "mgv_params_upload", "mgv_param_count", "mgv_param_name", "mgv_param_numel",
+           "mgv_ctx_set_dp", "mgv_ctx_set_tp", "mgv_ctx_set_adamw", "mgv_adamw_steps", "mgv_param_download",
+           "mgv_params_upload", "mgv_param_count", "mgv_param_name", "mgv_param_numel",
            "mgv_predict_velocity", "mgv_dit_forward", "mgv_flow_step", "mgv_flow_loss", "mgv_latent_rows",
            "mgv_rows_to_grid", "mgv_flow_step_device", "mgv_last_step_ms", "mgv_last_step_launches",
            "mgv_prof_enable", "mgv_prof_count", "mgv_prof_entry"]
@@ -219,6 +226,24 @@ class Context:
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
         self._check(self._L.mgv_ctx_set_dp(self.h, rank, world, buf))
 
+    def set_adamw(self, lr: float = 1e-3, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+                  weight_decay: float = 0.0):
+        """Run AdamW::update (optim.cpp:7-24) on device after every flow step; lr <= 0 disables."""
+        self._check(self._L.mgv_ctx_set_adamw(self.h, lr, beta1, beta2, eps, weight_decay))
+
+    def adamw_steps(self) -> int:
+        return int(self._L.mgv_adamw_steps(self.h))
+
+    def download(self) -> dict:
+        """All dit.* parameters (reference layout) as fp64 arrays keyed by name."""
+        out = {}
+        for i in range(int(self._L.mgv_param_count(self.h))):
+            name = self._L.mgv_param_name(self.h, i).decode()
+            buf = np.empty(int(self._L.mgv_param_numel(self.h, i)), dtype=np.float64)
+            self._check(self._L.mgv_param_download(self.h, i, buf.ctypes.data))
+            out[name] = buf
+        return out
+
     def set_tp(self, size: int, rank: int = 0, nccl_id: bytes | None = None):
         """Megatron tensor parallelism (call before upload).  nccl_id None: emulate all ranks here."""
         buf = None if nccl_id is None else (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
@@ -265,7 +290,8 @@ class Context:
         return out
 
     def flow_step(self, samples, text, fps=8.0, grads=False, velocity=False):
-        """FlowTrainer::step forward+backward (no AdamW): returns dict(loss, grad_norm[, grads][, V])."""
+        """FlowTrainer::step: forward+backward (+ AdamW::update when set_adamw is on); returns dict(loss,
+        grad_norm[, grads][, V]) -- the gradients are the ones the optimizer consumed."""
         n = len(samples)
         cs = (mgv_flow_sample * n)(*[s.to_c() for s in samples])
         text = _f64(text)

@@ -92,6 +92,16 @@ mgv_status mgv_nccl_unique_id(uint8_t out[128]) {
 mgv_status mgv_ctx_set_dp(mgv_ctx* ctx, int rank, int world, const uint8_t nccl_id[128]) {
     return guard(ctx, [&] { ctx->model->set_dp(rank, world, nccl_id); });
 }
+mgv_status mgv_ctx_set_adamw(mgv_ctx* ctx, double lr, double beta1, double beta2, double eps, double weight_decay) {
+    return guard(ctx, [&] { ctx->model->set_adamw(lr, beta1, beta2, eps, weight_decay); });
+}
+int64_t mgv_adamw_steps(mgv_ctx* ctx) { return ctx ? ctx->model->adamw_steps() : 0; }
+mgv_status mgv_param_download(mgv_ctx* ctx, int64_t i, double* out) {
+    return guard(ctx, [&] {
+        if (!out) throw mgv::InputError("null output");
+        ctx->model->download_param(i, out);
+    });
+}
 mgv_status mgv_ctx_set_tp(mgv_ctx* ctx, int size, int rank, const uint8_t* nccl_id) {
     return guard(ctx, [&] { ctx->model->set_tp(size, rank, nccl_id); });
 }

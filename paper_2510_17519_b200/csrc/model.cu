@@ -86,6 +86,12 @@ struct Model::WS {
     float* tpp = nullptr;
 };
 
+struct AdamParam {
+    float* w;
+    __nv_bfloat16* wb;
+    int64_t off, n;
+};
+
 namespace {
 struct Sizer {  // measures then lays out the arena
     bool measure;
@@ -265,6 +271,9 @@ Model::~Model() {
     if (grad_buf_) cudaFree(grad_buf_);
     if (comm_) ncclCommDestroy(comm_);
     if (tp_comm_) ncclCommDestroy(tp_comm_);
+    if (opt_m_) cudaFree(opt_m_);
+    if (opt_v_) cudaFree(opt_v_);
+    if (param_table_) cudaFree(param_table_);
     delete ws_;
 }
 
@@ -352,6 +361,51 @@ static int tp_row_chunks(const std::string& n) {
     return 0;
 }
 
+void Model::set_adamw(double lr, double beta1, double beta2, double eps, double weight_decay) {
+    if (!(beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 && beta2 < 1.0 && eps >= 0.0 && weight_decay >= 0.0))
+        throw ConfigError("AdamW hyper-parameters out of range");
+    adam_.on = lr > 0.0;
+    adam_.lr = lr;
+    adam_.b1 = beta1;
+    adam_.b2 = beta2;
+    adam_.eps = eps;
+    adam_.wd = weight_decay;
+    adam_.step = 0;
+    if (adam_.on && have_params_) alloc_adam_state();
+}
+
+void Model::alloc_adam_state() {
+    MGV_CUDA(cudaSetDevice(device_));
+    if (!opt_m_) MGV_CUDA(cudaMalloc(&opt_m_, sizeof(float) * grad_numel_));
+    if (!opt_v_) MGV_CUDA(cudaMalloc(&opt_v_, sizeof(float) * grad_numel_));
+    MGV_CUDA(cudaMemsetAsync(opt_m_, 0, sizeof(float) * grad_numel_, stream_));
+    MGV_CUDA(cudaMemsetAsync(opt_v_, 0, sizeof(float) * grad_numel_, stream_));
+    MGV_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// Multi-tensor AdamW (optim.cpp:7-24), one grid row per parameter: m, v, w updated in place, the bf16
+// operand copy refreshed.  Skipped entirely when the step's loss is not finite (FlowTrainer::step throws
+// before AdamW::update, flowtrain.cpp:276).
+__global__ void adamw_kernel(const AdamParam* table, const float* grad, float* m, float* v, const double* loss_acc,
+                             float lr, float b1, float b2, float eps, float wd, float inv_bc1, float inv_bc2) {
+    if (!isfinite(*loss_acc)) return;
+    const AdamParam q = table[blockIdx.y];
+    const float* g = grad + q.off;
+    float* mm = m + q.off;
+    float* vv = v + q.off;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < q.n; e += (int64_t)gridDim.x * blockDim.x) {
+        const float gi = g[e];
+        const float mi = b1 * mm[e] + (1.0f - b1) * gi;
+        const float vi = b2 * vv[e] + (1.0f - b2) * gi * gi;
+        mm[e] = mi;
+        vv[e] = vi;
+        const float mh = mi * inv_bc1, vh = vi * inv_bc2;
+        const float w = q.w[e] - lr * (mh / (sqrtf(vh) + eps) + wd * q.w[e]);
+        q.w[e] = w;
+        if (q.wb) q.wb[e] = __float2bfloat16_rn(w);
+    }
+}
+
 static bool is_matrix(const std::string& n) {
     static const char* mats[] = {"patch.w", "attn.qkv.w", "attn.out.w", "xattn.q.w", "xattn.kv.w",
                                  "xattn.out.w", "ffn.in.w", "ffn.out.w", "final.w", "out.w"};
@@ -374,6 +428,28 @@ __global__ void f32_to_f64(const float* src, int64_t n, double* dst) {
         dst[e] = static_cast<double>(src[e]);
 }
 static int grid_of(int64_t n) { return static_cast<int>(std::min<int64_t>((n + 255) / 256, 1 << 20)); }
+
+void Model::download_param(int64_t i, double* out) {
+    if (i < 0 || i >= static_cast<int64_t>(sorted_.size())) throw InputError("parameter index out of range");
+    MGV_CUDA(cudaSetDevice(device_));
+    const DevParam& q = *sorted_[i];
+    float* tmp = nullptr;
+    double* d = nullptr;
+    MGV_CUDA(cudaMallocAsync(&tmp, sizeof(float) * q.numel, stream_));
+    MGV_CUDA(cudaMallocAsync(&d, sizeof(double) * q.numel, stream_));
+    const float* src = q.f32;
+    if (const int C = tp_ > 1 ? tp_row_chunks(q.name) : 0) {  // back to the reference row order
+        permute_shard_rows(q.f32, tmp, C, static_cast<int>(cfg_.hidden), tp_, q.numel / (C * cfg_.hidden), 1, stream_);
+        src = tmp;
+    }
+    f32_to_f64<<<grid_of(q.numel), 256, 0, stream_>>>(src, q.numel, d);
+    note_launch();
+    MGV_CUDA(cudaMemcpyAsync(out, d, sizeof(double) * q.numel, cudaMemcpyDeviceToHost, stream_));
+    MGV_CUDA(cudaFreeAsync(tmp, stream_));
+    MGV_CUDA(cudaFreeAsync(d, stream_));
+    MGV_CUDA(cudaStreamSynchronize(stream_));
+}
+
 
 void Model::upload(const Cfg& cfg, int64_t n, const char* const* names, const double* const* data,
                    const int64_t* numel) {
@@ -457,7 +533,17 @@ void Model::upload(const Cfg& cfg, int64_t n, const char* const* names, const do
             kv.second.grad = grad_buf_ + kv.second.grad_off;
             sorted_.push_back(&kv.second);
         }
+        std::vector<AdamParam> table;
+        for (DevParam* q : sorted_) table.push_back(AdamParam{q->f32, q->bf, q->grad_off, q->numel});
+        if (param_table_) cudaFree(param_table_);
+        MGV_CUDA(cudaMalloc(&param_table_, sizeof(AdamParam) * table.size()));
+        MGV_CUDA(cudaMemcpy(param_table_, table.data(), sizeof(AdamParam) * table.size(), cudaMemcpyHostToDevice));
+        if (opt_m_) cudaFree(opt_m_);
+        if (opt_v_) cudaFree(opt_v_);
+        opt_m_ = opt_v_ = nullptr;
     }
+    adam_.step = 0;  // new weights: fresh optimizer state (FlowTrainer owns a fresh AdamW)
+    if (adam_.on) alloc_adam_state();
     cfg_ = cfg;
     double* staging = nullptr;
     int64_t stage_n = 0;
@@ -1005,6 +1091,23 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
         prof_.end(s);
     }
     sumsq(grad_buf_, grad_numel_, w.loss_part, w.scal + 2, s);  // grad_norm (flowtrain.cpp:284-289)
+    if (adam_.on) {  // AdamW::update (flowtrain.cpp:278), on device, skipped if the loss is not finite
+        if (!opt_m_) alloc_adam_state();
+        ++adam_.step;
+        const double bc1 = 1.0 - std::pow(adam_.b1, static_cast<double>(adam_.step));
+        const double bc2 = 1.0 - std::pow(adam_.b2, static_cast<double>(adam_.step));
+        int64_t maxn = 0;
+        for (auto* q : sorted_) maxn = std::max(maxn, q->numel);
+        const dim3 grid(static_cast<unsigned>(std::min<int64_t>((maxn + 255) / 256, 1184)),
+                        static_cast<unsigned>(sorted_.size()));
+        prof_.begin("adamw", s);
+        adamw_kernel<<<grid, 256, 0, s>>>(static_cast<const AdamParam*>(param_table_), grad_buf_, opt_m_, opt_v_,
+                                          w.scal, float(adam_.lr), float(adam_.b1), float(adam_.b2),
+                                          float(adam_.eps), float(adam_.wd), float(1.0 / bc1), float(1.0 / bc2));
+        note_launch();
+        MGV_CUDA(cudaGetLastError());
+        prof_.end(s);
+    }
     double host[3] = {0, 0, 0};
     MGV_CUDA(cudaMemcpyAsync(host, w.scal, sizeof(double) * 3, cudaMemcpyDeviceToHost, s));
     MGV_CUDA(cudaEventRecord(e1, s));
@@ -1017,7 +1120,10 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     *loss = host[0] / static_cast<double>(B_global);  // flowtrain.cpp:273
-    if (!std::isfinite(*loss)) throw NumericError("flow loss is not finite");  // flowtrain.cpp:276
+    if (!std::isfinite(*loss)) {  // flowtrain.cpp:276 (the device AdamW step was skipped)
+        if (adam_.on) --adam_.step;
+        throw NumericError("flow loss is not finite");
+    }
     *grad_norm = std::sqrt(host[2]);
 }
 

@@ -112,6 +112,11 @@ public:
     // otherwise this process is TP rank `rank` of an NCCL communicator.  Must precede upload().
     void set_tp(int size, int rank, const uint8_t* id);
     int tp_size() const { return tp_; }
+    // AdamW::update after every flow step (optim.cpp:7-24, flowtrain.cpp:278); lr <= 0 disables
+    void set_adamw(double lr, double beta1, double beta2, double eps, double weight_decay);
+    int64_t adamw_steps() const { return adam_.step; }
+    // parameter i (sorted-name order) in the reference layout, fp64
+    void download_param(int64_t i, double* out);
 
     void upload(const Cfg& cfg, int64_t n, const char* const* names, const double* const* data,
                 const int64_t* numel);
@@ -181,6 +186,16 @@ private:
     // NCCL data parallel
     ncclComm_t comm_ = nullptr;
     int rank_ = 0, world_ = 1;
+    // AdamW state: m, v in the gradient buffer's layout; per-parameter table for the multi-tensor update
+    struct Adam {
+        bool on = false;
+        double lr = 0, b1 = 0.9, b2 = 0.999, eps = 1e-8, wd = 0;
+        int64_t step = 0;
+    } adam_;
+    float* opt_m_ = nullptr;
+    float* opt_v_ = nullptr;
+    void* param_table_ = nullptr;
+    void alloc_adam_state();
     // tensor parallel
     ncclComm_t tp_comm_ = nullptr;
     int tp_ = 1, tp_rank_ = 0;

@@ -1,0 +1,60 @@
+"""The full FlowTrainer::step on device: flow fwd+bwd, grad norm and AdamW::update (optim.cpp:7-24), two steps
+in a row against the fp64 oracle (whose AdamW is pinned to the reference's in tests/test_oracle.py).
+
+eps = 1 keeps the Adam direction m_hat / (sqrt(v_hat) + eps) a smooth function of the gradient; with the
+default 1e-8 it is sign(g) for every element and near-zero gradients flip it on round-off alone."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.golden.make_golden import CASES, build_case
+from tests.gpu_common import nerr, to_cfg, to_samples
+
+pytestmark = pytest.mark.gpu
+HP = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1.0, weight_decay=0.01)
+
+
+@pytest.mark.parametrize("prec,tp", [("fp32", 1), ("fp32", 2), ("bf16", 1)])
+def test_two_training_steps(prec, tp):
+    from paper_2510_17519_b200.capi import Context
+    cfg, P, text, samples = build_case("hd144", CASES["hd144"])
+    P0 = {k: v.copy() for k, v in P.items()}
+    ctx = Context(0, prec)
+    if tp > 1:
+        ctx.set_tp(tp)
+    ctx.set_adamw(**HP)
+    ctx.upload(to_cfg(cfg), P)
+    g1 = ctx.flow_step(to_samples(samples), text, 8.0, grads=False)
+    g2 = ctx.flow_step(to_samples(samples), text, 8.0, grads=False)
+    assert ctx.adamw_steps() == 2
+    got = ctx.download()
+    ref = {k: v.copy() for k, v in P.items()}
+    opt = O.AdamW(HP["lr"], HP["beta1"], HP["beta2"], HP["eps"], HP["weight_decay"])
+    r1 = O.flow_fwdbwd(ref, cfg, samples, text, 8.0, grads=True)
+    opt.update(ref, r1["grads"])
+    r2 = O.flow_fwdbwd(ref, cfg, samples, text, 8.0, grads=True)
+    opt.update(ref, r2["grads"])
+    tol = 1e-4 if prec == "fp32" else 5e-2
+    assert abs(g1["loss"] - r1["loss"]) / abs(r1["loss"]) <= tol
+    assert abs(g2["loss"] - r2["loss"]) / abs(r2["loss"]) <= tol  # the second step runs on updated weights
+    # the update (w - w0) within tol, normwise per parameter, beyond the fp32 rounding of the stored weight
+    errs = {}
+    for k in ref:
+        upd = ref[k].ravel() - P0[k].ravel()
+        excess = np.abs(got[k] - ref[k].ravel()) - 4 * 2.0 ** -24 * np.abs(ref[k].ravel())
+        errs[k] = max(float(excess.max()), 0.0) / max(float(np.abs(upd).max()), 1e-30)
+    worst = max(errs, key=errs.get)
+    print(f"{prec} tp{tp}: worst update error {worst} {errs[worst]:.2e}")
+    assert errs[worst] <= tol, (worst, errs[worst])
+
+
+def test_adamw_disabled_leaves_weights():
+    from paper_2510_17519_b200.capi import Context
+    cfg, P, text, samples = build_case("tiny", CASES["tiny"])
+    ctx = Context(0, "fp32")
+    ctx.upload(to_cfg(cfg), P)
+    ctx.flow_step(to_samples(samples), text, 8.0, grads=False)
+    got = ctx.download()
+    assert ctx.adamw_steps() == 0
+    for k in P:
+        assert np.array_equal(got[k], P[k].astype(np.float32).astype(np.float64).ravel()), k

@@ -134,3 +134,20 @@ def test_restatement_matches_live_reference_10b_width():
     assert nerr(o["V"][0], r["V"][0]) < 1e-12
     for k in init:
         assert nerr(o["grads"][k], r["grads"][k]) < 1e-10 or np.abs(r["grads"][k]).max() == 0, k
+
+
+def test_adamw_restatement_matches_reference():
+    """oracle.AdamW (optim.cpp:7-24 restated) vs the reference's own AdamW::update, three steps."""
+    ref_lib_available = os.path.exists(os.path.join(os.path.dirname(O.__file__), "_ref", "libmugv_ref.so"))
+    if not ref_lib_available:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(3)
+    P = {"dit.a": rng.standard_normal((4, 5)), "dit.b": rng.standard_normal(7)}
+    Q = {k: v.copy() for k, v in P.items()}
+    mine, theirs = O.AdamW(1e-2, 0.8, 0.95, 1e-6, 0.1), O.RefAdamW(1e-2, 0.8, 0.95, 1e-6, 0.1)
+    for step in range(3):
+        G = {k: rng.standard_normal(v.shape) for k, v in P.items()}
+        mine.update(P, G)
+        theirs.update(Q, G)
+        for k in P:
+            assert np.allclose(P[k], Q[k], rtol=0, atol=1e-14), (step, k)
