@@ -83,6 +83,16 @@ mgv_status mgv_ctx_set_dp(mgv_ctx* ctx, int rank, int world, const uint8_t nccl_
  * sharded path.  `size` must divide heads.  Not combinable with mgv_ctx_set_dp. */
 mgv_status mgv_ctx_set_tp(mgv_ctx* ctx, int size, int rank, const uint8_t* nccl_id);
 
+/* flow::forward_sample_rows (direction -1: Euler t 1 -> 0, x <- x - dt v) and flow::reverse_sample_rows
+ * (direction +1: t 0 -> 1, x <- x + dt v), flowtrain.cpp:135-172 / flowtrain.hpp:66-76, with the model
+ * velocity of flow::model_velocity (:102-107): x_start (N x 4c_z) on the grid dims/coords, `steps` >= 1
+ * steps run on device, conditioned rows (mask `conditioned`, N bytes, may be NULL) re-imposed from
+ * condition_latents (N x 4c_z) before and after every step.  Errors as the reference (InputError for
+ * steps < 1 or a unit-misaligned mask, DimensionError for shape mismatches). */
+mgv_status mgv_sample_rows(mgv_ctx* ctx, const double* x_start, int64_t N, const int32_t* coords,
+                           const int64_t dims[3], const double* text, int64_t L, const uint8_t* conditioned,
+                           const double* condition_latents, int64_t steps, int direction, double fps, double* out);
+
 /* AdamW (replaces mugv::AdamW, optim.hpp:12-29 / optim.cpp:7-24): when lr > 0, every mgv_flow_step /
  * mgv_flow_step_device ends with AdamW::update over all dit.* parameters on device (fp32 masters, m and v
  * resident, bf16 operand copies refreshed) -- the full FlowTrainer::step (flowtrain.cpp:257-282).  The

@@ -261,6 +261,32 @@ int ref_dit_forward(void* h, const RefCfg* c, const int64_t* dims, const double*
     });
 }
 
+// ---- sampler: forward_sample_rows (direction -1) / reverse_sample_rows (+1), flowtrain.cpp:135-172, with
+// model_velocity (:102-107) on the handle's parameters; cond may be null (no_condition)
+int ref_sample_rows(void* h, const RefCfg* c, const int64_t* dims, const double* x_start, const double* text,
+                    int64_t L, const uint8_t* cond, const double* cond_latents, int64_t steps, int direction,
+                    double fps, double* out) {
+    return guard([&] {
+        auto* hh = static_cast<Handle*>(h);
+        auto cfg = to_cfg(c);
+        dit::TokenGrid geom = geom_of(dims, cfg.c_z);
+        const int64_t N = geom.n(), D = cfg.patch_dim();
+        Tensor x({N, D}), tx({L, cfg.text_dim});
+        std::memcpy(x.data(), x_start, sizeof(double) * static_cast<size_t>(x.numel()));
+        std::memcpy(tx.data(), text, sizeof(double) * static_cast<size_t>(tx.numel()));
+        flow::ConditionMask mask = flow::no_condition(N);
+        if (cond) {
+            mask.conditioned.assign(cond, cond + N);
+            mask.condition_latents = Tensor({N, D});
+            std::memcpy(mask.condition_latents.data(), cond_latents, sizeof(double) * static_cast<size_t>(N * D));
+        }
+        auto vel = flow::model_velocity(hh->p, cfg, geom, tx, fps);
+        Tensor y = direction < 0 ? flow::forward_sample_rows(vel, geom, x, mask, steps)
+                                 : flow::reverse_sample_rows(vel, geom, x, mask, steps);
+        std::memcpy(out, y.data(), sizeof(double) * static_cast<size_t>(y.numel()));
+    });
+}
+
 // ---- AdamW::update (optim.cpp:7-24) on caller-owned tensors ----
 void* ref_adamw_create(double lr, double beta1, double beta2, double eps, double weight_decay) {
     auto* o = new AdamW(lr);

@@ -69,6 +69,8 @@ def declare(L):
     L.mgv_ctx_set_dp.restype = I
     L.mgv_ctx_set_tp.argtypes = [P, I, I, P]
     L.mgv_ctx_set_tp.restype = I
+    L.mgv_sample_rows.argtypes = [P, P, I64, P, P, P, I64, P, P, I64, I, D, P]
+    L.mgv_sample_rows.restype = I
     L.mgv_ctx_set_adamw.argtypes = [P, D, D, D, D, D]
     L.mgv_ctx_set_adamw.restype = I
     L.mgv_adamw_steps.argtypes = [P]
@@ -115,7 +117,7 @@ def declare(L):
 
 # symbols include/mugv_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = ["mgv_ctx_create", "mgv_ctx_destroy", "mgv_last_error", "mgv_ctx_set_stream", "mgv_nccl_unique_id",
-           "mgv_ctx_set_dp", "mgv_ctx_set_tp", "mgv_ctx_set_adamw", "mgv_adamw_steps", "mgv_param_download",
+           "mgv_ctx_set_dp", "mgv_ctx_set_tp", "mgv_sample_rows", "mgv_ctx_set_adamw", "mgv_adamw_steps", "mgv_param_download",
            "mgv_params_upload", "mgv_param_count", "mgv_param_name", "mgv_param_numel",
            "mgv_predict_velocity", "mgv_dit_forward", "mgv_flow_step", "mgv_flow_loss", "mgv_latent_rows",
            "mgv_rows_to_grid", "mgv_flow_step_device", "mgv_last_step_ms", "mgv_last_step_launches",
@@ -225,6 +227,21 @@ class Context:
     def set_dp(self, rank: int, world: int, nccl_id: bytes):
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
         self._check(self._L.mgv_ctx_set_dp(self.h, rank, world, buf))
+
+    def sample_rows(self, x_start, coords, dims, text, steps, direction=-1, fps=8.0, cond=None, cond_latents=None):
+        """flow::forward_sample_rows (direction -1) / reverse_sample_rows (+1) on device."""
+        x = _f64(x_start)
+        out = np.empty_like(x)
+        co = np.ascontiguousarray(coords, dtype=np.int32)
+        d = np.asarray(dims, dtype=np.int64)
+        tx = _f64(text)
+        cm = None if cond is None else np.ascontiguousarray(cond, dtype=np.uint8)
+        cl = None if cond_latents is None else _f64(cond_latents)
+        self._check(self._L.mgv_sample_rows(self.h, x.ctypes.data, x.shape[0], co.ctypes.data, d.ctypes.data,
+                                            tx.ctypes.data, tx.shape[0], None if cm is None else cm.ctypes.data,
+                                            None if cl is None else cl.ctypes.data, steps, direction, fps,
+                                            out.ctypes.data))
+        return out
 
     def set_adamw(self, lr: float = 1e-3, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
                   weight_decay: float = 0.0):

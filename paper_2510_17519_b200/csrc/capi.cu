@@ -92,6 +92,16 @@ mgv_status mgv_nccl_unique_id(uint8_t out[128]) {
 mgv_status mgv_ctx_set_dp(mgv_ctx* ctx, int rank, int world, const uint8_t nccl_id[128]) {
     return guard(ctx, [&] { ctx->model->set_dp(rank, world, nccl_id); });
 }
+mgv_status mgv_sample_rows(mgv_ctx* ctx, const double* x_start, int64_t N, const int32_t* coords,
+                           const int64_t dims[3], const double* text, int64_t L, const uint8_t* conditioned,
+                           const double* condition_latents, int64_t steps, int direction, double fps, double* out) {
+    return guard(ctx, [&] {
+        if (!x_start || !coords || !dims || !text || !out) throw mgv::InputError("null argument");
+        if (direction != 1 && direction != -1) throw mgv::InputError("direction must be -1 (t 1->0) or +1 (t 0->1)");
+        ctx->model->sample_rows(x_start, N, coords, dims, text, L, conditioned, condition_latents, steps, direction, fps,
+                                out);
+    });
+}
 mgv_status mgv_ctx_set_adamw(mgv_ctx* ctx, double lr, double beta1, double beta2, double eps, double weight_decay) {
     return guard(ctx, [&] { ctx->model->set_adamw(lr, beta1, beta2, eps, weight_decay); });
 }

@@ -1309,6 +1309,107 @@ void Model::value_forward(const double* in, int64_t N, const int32_t* coords, co
     MGV_CUDA(cudaStreamSynchronize(s));
 }
 
+// ------------------------------------------------------------------ sampler (flowtrain.cpp:111-172)
+// x += coef * v in fp64 (the reference's Euler state is fp64), then impose: conditioned rows <- latents
+__global__ void euler_impose_kernel(double* x, const float* v, int64_t N, int64_t D, double coef,
+                                    const uint8_t* cond, const double* cl) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N * D; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / D;
+        if (cond && cond[i])
+            x[e] = cl[e];  // impose (flowtrain.cpp:111-117)
+        else if (v)
+            x[e] += coef * static_cast<double>(v[e]);
+    }
+}
+
+template <class T>
+void Model::sample_impl(const double* x_start, int64_t N, const int32_t* coords, const int64_t dims[3],
+                        const double* text, int64_t L, const uint8_t* cond, const double* cond_latents,
+                        int64_t steps, int direction, double fps, double* out) {
+    if (!have_params_) throw InputError("no parameters uploaded");
+    if (steps < 1) throw InputError("steps must be >= 1");  // flowtrain.cpp:137, :160
+    if (N != dims[0] * dims[1] * dims[2] || N < 1) throw DimensionError("rows do not match the token grid");
+    if (L < 1) throw DimensionError("text embeddings must be (L, text_dim)");
+    const int64_t D = cfg_.D();
+    bool any = false;
+    if (cond) {  // validate_mask (flowtrain.cpp:61-81)
+        std::vector<int> unit(static_cast<size_t>(dims[0]), -1);
+        for (int64_t i = 0; i < N; ++i) {
+            const int u = coords[3 * i];
+            if (u < 0 || u >= dims[0]) throw DimensionError("condition mask does not match the token grid");
+            const int f = cond[i] ? 1 : 0;
+            int& seen = unit[static_cast<size_t>(u)];
+            if (seen == -1)
+                seen = f;
+            else if (seen != f)
+                throw InputError("conditioned tokens must cover whole latent units");
+            any = any || f;
+        }
+        if (any && !cond_latents) throw InputError("condition mask lacks clean latents for its conditioned tokens");
+    }
+    WS& w = *ws_;
+    cudaStream_t s = stream_;
+    w.N = N;
+    w.L = L;
+    w.n_u = any ? 2 : 1;  // per-token timesteps {tc, 0 at conditioned tokens} (flowtrain.cpp:119-124)
+    w.esz = bf16_ ? 2 : 4;
+    w.grads = false;
+    w.tp = tp_;
+    {
+        Sizer sz{true, 0, &arena_};
+        layout_ws(w, sz, cfg_, false);
+        arena_.reserve(sz.bytes);
+        arena_.reset();
+        Sizer real{false, 0, &arena_};
+        layout_ws(w, real, cfg_, false);
+    }
+    std::vector<int32_t> mid(static_cast<size_t>(N), 0);
+    if (any)
+        for (int64_t i = 0; i < N; ++i) mid[static_cast<size_t>(i)] = cond[i] ? 1 : 0;
+    double *x = nullptr, *cl = nullptr, *din = nullptr;
+    uint8_t* cm = nullptr;
+    MGV_CUDA(cudaMallocAsync(&x, sizeof(double) * N * D, s));
+    MGV_CUDA(cudaMallocAsync(&din, sizeof(double) * L * cfg_.text_dim, s));
+    if (any) {
+        MGV_CUDA(cudaMallocAsync(&cl, sizeof(double) * N * D, s));
+        MGV_CUDA(cudaMallocAsync(&cm, N, s));
+        MGV_CUDA(cudaMemcpyAsync(cl, cond_latents, sizeof(double) * N * D, cudaMemcpyHostToDevice, s));
+        MGV_CUDA(cudaMemcpyAsync(cm, cond, N, cudaMemcpyHostToDevice, s));
+    }
+    MGV_CUDA(cudaMemcpyAsync(x, x_start, sizeof(double) * N * D, cudaMemcpyHostToDevice, s));
+    MGV_CUDA(cudaMemcpyAsync(w.coords, coords, sizeof(int32_t) * 3 * N, cudaMemcpyHostToDevice, s));
+    MGV_CUDA(cudaMemcpyAsync(w.mod_id, mid.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, s));
+    MGV_CUDA(cudaMemcpyAsync(din, text, sizeof(double) * L * cfg_.text_dim, cudaMemcpyHostToDevice, s));
+    convert_rows<T>(din, L * cfg_.text_dim, tp<T>(w.text), s);
+    const int grid = grid_of(N * D);
+    euler_impose_kernel<<<grid, 256, 0, s>>>(x, nullptr, N, D, 0.0, cm, cl);  // impose(x) before the first step
+    note_launch();
+    const double dt = 1.0 / static_cast<double>(steps);
+    DevSample dummy;
+    for (int64_t k = 0; k < steps; ++k) {
+        const double tc = direction < 0 ? 1.0 - static_cast<double>(k) * dt : static_cast<double>(k) * dt;
+        set_taus(w.taus, tc, s);  // {tc, 0}
+        convert_rows<T>(x, N * D, tp<T>(w.rows), s);
+        forward_sample<T>(dummy, w.rows, nullptr, w.n_u, nullptr, fps, false, true, nullptr);  // velocity
+        euler_impose_kernel<<<grid, 256, 0, s>>>(x, w.V, N, D, direction < 0 ? -dt : dt, cm, cl);
+        note_launch();
+    }
+    MGV_CUDA(cudaMemcpyAsync(out, x, sizeof(double) * N * D, cudaMemcpyDeviceToHost, s));
+    for (void* q : {static_cast<void*>(x), static_cast<void*>(din), static_cast<void*>(cl), static_cast<void*>(cm)})
+        if (q) MGV_CUDA(cudaFreeAsync(q, s));
+    MGV_CUDA(cudaStreamSynchronize(s));
+}
+
+void Model::sample_rows(const double* x_start, int64_t N, const int32_t* coords, const int64_t dims[3],
+                        const double* text, int64_t L, const uint8_t* cond, const double* cond_latents, int64_t steps,
+                        int direction, double fps, double* out) {
+    MGV_CUDA(cudaSetDevice(device_));
+    if (bf16_)
+        sample_impl<__nv_bfloat16>(x_start, N, coords, dims, text, L, cond, cond_latents, steps, direction, fps, out);
+    else
+        sample_impl<float>(x_start, N, coords, dims, text, L, cond, cond_latents, steps, direction, fps, out);
+}
+
 void Model::predict_velocity(const double* rows, int64_t N, const int32_t* coords, const int64_t dims[3],
                              const double* text, int64_t L, const double* tau, double fps, double* out) {
     MGV_CUDA(cudaSetDevice(device_));

@@ -127,6 +127,12 @@ public:
                           const double* text, int64_t L, const double* tau, double fps, double* out);
     void dit_forward(const double* tokens, int64_t N, const int32_t* coords, const int64_t dims[3],
                      const double* text, int64_t L, const double* tau, double fps, double* out);
+    // forward_sample_rows / reverse_sample_rows (flowtrain.cpp:135-172): `steps` Euler steps of the
+    // probability-flow ODE on device (direction -1: t 1 -> 0, x -= dt v; +1: t 0 -> 1, x += dt v),
+    // conditioned rows re-imposed after every step.  cond / cond_latents may be null.
+    void sample_rows(const double* x_start, int64_t N, const int32_t* coords, const int64_t dims[3],
+                     const double* text, int64_t L, const uint8_t* cond, const double* cond_latents, int64_t steps,
+                     int direction, double fps, double* out);
     void flow_step(int64_t n, const mgv_flow_sample* samples, const double* text, int64_t L, double fps,
                    double* loss, double* grad_norm, double* const* grads_out, double* const* v_out);
     // Device-resident inputs (benchmark `value` path): no host<->device traffic except the two scalars.
@@ -159,6 +165,10 @@ private:
     std::vector<int> tp_ranks() const;  // the TP ranks this process computes
     void tp_allreduce(float* buf, int64_t n, cudaStream_t s);
     void tp_allreduce_grads(cudaStream_t s);
+    template <class T>
+    void sample_impl(const double* x_start, int64_t N, const int32_t* coords, const int64_t dims[3],
+                     const double* text, int64_t L, const uint8_t* cond, const double* cond_latents, int64_t steps,
+                     int direction, double fps, double* out);
     template <class T>
     void value_forward(const double* in, int64_t N, const int32_t* coords, const int64_t dims[3],
                        const double* text, int64_t L, const double* tau, double fps, double* out, bool velocity);

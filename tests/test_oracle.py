@@ -151,3 +151,23 @@ def test_adamw_restatement_matches_reference():
         theirs.update(Q, G)
         for k in P:
             assert np.allclose(P[k], Q[k], rtol=0, atol=1e-14), (step, k)
+
+
+@pytest.mark.parametrize("direction,cond", [(-1, False), (-1, True), (1, True)])
+def test_sampler_restatement_matches_reference(direction, cond):
+    """oracle.sample_rows (flowtrain.cpp:135-172 restated) vs the reference's forward/reverse_sample_rows."""
+    if not os.path.exists(os.path.join(os.path.dirname(O.__file__), "_ref", "libmugv_ref.so")):
+        pytest.skip("oracle/_ref not built")
+    cfg = O.DitConfig(depth=1, hidden=24, heads=2, text_dim=6, c_z=2, rope_split=(4, 4, 4))
+    ref = O.RefModel(cfg, 1, 2, 0.2, 0.05)
+    P = O.open_gates(O.init_dit_params(cfg, O.Rng(1)), 2, 0.2, 0.05)  # bit-equal to ref's (test above)
+    dims = (2, 2, 3)
+    coords = O.grid_coords(dims)
+    N, D = coords.shape[0], 4 * cfg.c_z
+    x0 = O.Rng(7).normal_tensor((N, D))
+    text = O.Rng(4).normal_tensor((3, 6))
+    cm = (coords[:, 0] == 0).astype(np.uint8) if cond else None
+    cl = O.Rng(8).normal_tensor((N, D)) if cond else None
+    mine = O.sample_rows(P, cfg, x0, coords, text, 8.0, 3, direction, cm, cl)
+    theirs = O.ref_sample_rows(ref, dims, x0, text, 8.0, 3, direction, cm, cl)
+    assert np.abs(mine - theirs).max() <= 1e-12 * max(1.0, np.abs(theirs).max())
