@@ -218,23 +218,6 @@ __device__ __forceinline__ void mma_tmem_rows_x_t(uint32_t d, uint32_t a_tmem, u
         umma_f16_ts(d, a_tmem + kk * 8, smem_desc(bt + kk * 2048, 16, 1024, kSwizzle128), id, kk > 0 ? 1u : 0u);
 }
 
-// thread's row of a row-major bf16 matrix (HD values, 16-byte aligned) -> TMEM columns [taddr, taddr + HD/2)
-// in the A-operand layout (two consecutive K elements per 32-bit column, the lower one in the low half)
-template <int HD>
-__device__ __forceinline__ void row_to_tmem(uint32_t taddr, const __nv_bfloat16* src, bool valid) {
-    constexpr int W = HD / 2;
-    uint32_t r[W];
-#pragma unroll
-    for (int u = 0; u < W / 4; ++u) {
-        const uint4 x = valid ? reinterpret_cast<const uint4*>(src)[u] : make_uint4(0, 0, 0, 0);
-        r[4 * u] = x.x;
-        r[4 * u + 1] = x.y;
-        r[4 * u + 2] = x.z;
-        r[4 * u + 3] = x.w;
-    }
-#pragma unroll
-    for (int c = 0; c < W; c += 8) tmem_st8(taddr + c, r + c);
-}
 
 // =====================================================================================  dK / dV
 // K stays in TMEM (the A operand of S^T = K Q^T, a TS MMA); V is an SS operand of dP^T = V dO^T.

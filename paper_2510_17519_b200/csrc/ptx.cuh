@@ -238,6 +238,33 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
                  "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
 }
 
+__device__ __forceinline__ void tmem_st4x(uint32_t taddr, const uint32_t* r) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
+                 "r"(r[2]), "r"(r[3]));
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
+// thread's row of a row-major bf16 matrix (HD values, 16-byte aligned) -> TMEM columns [taddr, taddr + HD/2)
+// in the A-operand layout (two consecutive K elements per 32-bit column, the lower one in the low half)
+template <int HD>
+__device__ __forceinline__ void row_to_tmem(uint32_t taddr, const __nv_bfloat16* src, bool valid) {
+    constexpr int W = HD / 2;
+    uint32_t r[W];
+#pragma unroll
+    for (int u = 0; u < W / 4; ++u) {
+        const uint4 x = valid ? reinterpret_cast<const uint4*>(src)[u] : make_uint4(0, 0, 0, 0);
+        r[4 * u] = x.x;
+        r[4 * u + 1] = x.y;
+        r[4 * u + 2] = x.z;
+        r[4 * u + 3] = x.w;
+    }
+#pragma unroll
+    for (int c = 0; c < W; c += 8) tmem_st8(taddr + c, r + c);
+}
+
 // ---------------------------------------------------------------- descriptors
 // Layout codes of the shared-memory descriptor (bits 61..63).
 enum : uint32_t { kSwizzleNone = 0, kSwizzle128 = 2, kSwizzle64 = 4, kSwizzle32 = 6 };
