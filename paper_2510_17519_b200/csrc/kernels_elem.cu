@@ -29,6 +29,13 @@ void rms_bwd_vec_launch(int mode, const __nv_bfloat16* dA, const float* X, const
                         int accumulate, float* part_a, float* part_b, cudaStream_t s);
 void postnorm_bwd_vec_launch(const float* dX, const __nv_bfloat16* co, const float* rc, const float* g, int N, int H,
                              __nv_bfloat16* dco, float* part_dg, cudaStream_t s);
+void qk_norm_rope_vec_launch(const __nv_bfloat16* qkv, const QKLayout& L, int N, int hd, int heads,
+                             const float* temp, const float2* cs, __nv_bfloat16* qk, float* iq, float* ik,
+                             cudaStream_t s);
+void qk_norm_rope_bwd_vec_launch(__nv_bfloat16* dqkv, const __nv_bfloat16* qkv, const QKLayout& L, int N, int hd,
+                                 int heads, const float* temp, const float2* cs, const float* iq, const float* ik,
+                                 float* part_dtemp, cudaStream_t s);
+bool qk_vec_ok(const void* a, const void* b, const QKLayout& L, int hd);
 void colsum_vec_launch(const __nv_bfloat16* Y, int64_t ld, int N, int C, float* part, cudaStream_t s);
 template <class T>
 constexpr bool is_bf16() { return std::is_same<T, __nv_bfloat16>::value; }
@@ -407,6 +414,9 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(const T* qkv, QKLayou
 template <class T>
 void qk_norm_rope(const T* qkv, const QKLayout& L, int N, int H, int heads, const float* temp, const float2* cs, T* qk,
                   float* iq, float* ik, cudaStream_t s) {
+    if constexpr (is_bf16<T>())
+        if (qk_vec_ok(qkv, qk, L, H / heads))
+            return qk_norm_rope_vec_launch(qkv, L, N, H / heads, heads, temp, cs, qk, iq, ik, s);
     const int64_t warps = (int64_t)N * heads * 2;
     qk_norm_rope_kernel<T><<<grid_for(warps * 32), 256, 0, s>>>(qkv, L, N, H, heads, temp, cs, qk, iq, ik); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
@@ -743,6 +753,9 @@ __global__ void __launch_bounds__(256) qk_norm_rope_bwd_kernel(T* dqkv, const T*
 template <class T>
 void qk_norm_rope_bwd(T* dqkv, const T* qkv, const QKLayout& L, int N, int H, int heads, const float* temp,
                       const float2* cs, const float* iq, const float* ik, float* part_dtemp, cudaStream_t s) {
+    if constexpr (is_bf16<T>())
+        if (qk_vec_ok(dqkv, qkv, L, H / heads))
+            return qk_norm_rope_bwd_vec_launch(dqkv, qkv, L, N, H / heads, heads, temp, cs, iq, ik, part_dtemp, s);
     qk_norm_rope_bwd_kernel<T><<<row_chunks(N), 256, 0, s>>>(dqkv, qkv, L, N, H, heads, temp, cs, iq, ik, part_dtemp); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
@@ -1450,7 +1463,166 @@ __global__ void __launch_bounds__(RT) colsum_vec(const bf* Y, int64_t ld, int N,
     st8(part + (int64_t)blockIdx.x * C + grp * 8, acc);
 }
 
+
+// ---- QK-norm + temperature + RoPE (dit.cpp:289-294), bf16, head_dim % 8 == 0: lane l < hd/8 owns the
+// 8 consecutive elements [8l, 8l+8) = rotation pairs [4l, 4l+4) of one (token, q|k, head) vector, so
+// each vector is one 16-byte load / store per lane instead of hd/2 4-byte ones.
+__device__ __forceinline__ float warp_sum_v(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+    return v;
+}
+__device__ __forceinline__ void ld_cs4(const float2* cs, float* c, float* sn) {  // 4 (cos, sin) pairs
+    const float4 a = reinterpret_cast<const float4*>(cs)[0], b = reinterpret_cast<const float4*>(cs)[1];
+    c[0] = a.x; sn[0] = a.y; c[1] = a.z; sn[1] = a.w; c[2] = b.x; sn[2] = b.y; c[3] = b.z; sn[3] = b.w;
+}
+constexpr int QKV = 4;  // vectors (heads) per warp in flight
+__global__ void __launch_bounds__(256) qk_norm_rope_vec(const bf* qkv, QKLayout Lq, int N, int hd, int heads,
+                                                        const float* temp, const float2* cs, bf* qk, float* iq,
+                                                        float* ik) {
+    const int hg = (heads + QKV - 1) / QKV;  // head groups
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+    const int lane = threadIdx.x & 31;
+    if (gw >= (int64_t)N * 2 * hg) return;
+    const int h0 = static_cast<int>(gw % hg) * QKV;
+    const int which = static_cast<int>((gw / hg) % 2);
+    const int64_t n = gw / (2 * hg);
+    const bool act = lane < hd / 8;
+    float v[QKV][8];
+#pragma unroll
+    for (int u = 0; u < QKV; ++u) {  // all loads first (independent, in flight together)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[u][e] = 0.0f;
+        if (act && h0 + u < heads) ld8(qkv + n * Lq.in_ld + which * Lq.in_koff + (h0 + u) * hd + 8 * lane, v[u]);
+    }
+    float c[4] = {0, 0, 0, 0}, sn[4] = {0, 0, 0, 0};
+    if (act) ld_cs4(cs + n * (hd / 2) + 4 * lane, c, sn);
+    float ss[QKV];
+#pragma unroll
+    for (int u = 0; u < QKV; ++u) {
+        ss[u] = 0.0f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ss[u] = fmaf(v[u][e], v[u][e], ss[u]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < QKV; ++u) ss[u] += __shfl_xor_sync(0xffffffff, ss[u], o);
+#pragma unroll
+    for (int u = 0; u < QKV; ++u) {
+        const int h = h0 + u;
+        if (h >= heads) break;
+        const float iv = 1.0f / sqrtf(ss[u] + 1e-6f);  // autodiff.cpp:727
+        if (lane == 0) (which == 0 ? iq : ik)[n * Lq.i_ld + h] = iv;
+        if (!act) continue;
+        const float sc = which == 0 ? iv * temp[h] : iv;  // dit.cpp:292
+        float o[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float x0 = v[u][2 * k] * sc, x1 = v[u][2 * k + 1] * sc;
+            o[2 * k] = x0 * c[k] - x1 * sn[k];  // autodiff.cpp:864-865
+            o[2 * k + 1] = x0 * sn[k] + x1 * c[k];
+        }
+        st8(qk + n * Lq.out_ld + which * Lq.out_koff + h * hd + 8 * lane, o);
+    }
+}
+
+// backward: CTA = (chunk of kRowsPerChunk rows, 8 heads), warp = one head over the chunk (fixed-order dtemp
+// partials); two rows x (q, k) are processed per iteration so four vectors' loads are in flight
+constexpr int QRU = 1;  // rows per iteration of the backward (x (q, k) vectors in flight)
+__global__ void __launch_bounds__(256) qk_norm_rope_bwd_vec(bf* dqkv, const bf* qkv, QKLayout Lq, int N, int hd,
+                                                            int heads, const float* temp, const float2* cs,
+                                                            const float* iq, const float* ik, float* part_dtemp) {
+    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+    const bool act = lane < hd / 8;
+    const int r0 = blockIdx.x * kRowsPerChunk, r1 = min(N, r0 + kRowsPerChunk);
+    for (int h = blockIdx.y * 8 + warp; h < heads; h += 8 * gridDim.y) {  // one head per warp
+        const float tq = temp[h];
+        float dtemp = 0.0f;
+        for (int n0 = r0; n0 < r1; n0 += QRU) {
+            // vectors u = 2 * (row - n0) + which: QRU rows x (q, k), loads all in flight
+            float c[QRU][4], sn[QRU][4], d[2 * QRU][8], x[2 * QRU][8], iv[2 * QRU];
+            int64_t off[2 * QRU];
+            bool ok[2 * QRU];
+#pragma unroll
+            for (int rr = 0; rr < QRU; ++rr) {
+                const int n = n0 + rr;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) c[rr][k] = sn[rr][k] = 0.0f;
+                if (act && n < r1) ld_cs4(cs + (int64_t)n * (hd / 2) + 4 * lane, c[rr], sn[rr]);
+#pragma unroll
+                for (int which = 0; which < 2; ++which) {
+                    const int u = 2 * rr + which;
+                    ok[u] = n < r1;
+                    off[u] = (int64_t)n * Lq.in_ld + which * Lq.in_koff + h * hd + 8 * lane;
+                    iv[u] = ok[u] ? (which == 0 ? iq : ik)[(int64_t)n * Lq.i_ld + h] : 0.0f;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) d[u][e] = x[u][e] = 0.0f;
+                    if (act && ok[u]) {
+                        ld8(dqkv + off[u], d[u]);
+                        ld8(qkv + off[u], x[u]);
+                    }
+                }
+            }
+            float ga[2 * QRU][4], gb[2 * QRU][4], tdot[2 * QRU], dot[2 * QRU];
+#pragma unroll
+            for (int u = 0; u < 2 * QRU; ++u) {
+                const int rr = u >> 1, which = u & 1;
+                const float sc = which == 0 ? tq : 1.0f;
+                tdot[u] = dot[u] = 0.0f;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    // inverse rotation (autodiff.cpp:888-898)
+                    ga[u][k] = d[u][2 * k] * c[rr][k] + d[u][2 * k + 1] * sn[rr][k];
+                    gb[u][k] = -d[u][2 * k] * sn[rr][k] + d[u][2 * k + 1] * c[rr][k];
+                    tdot[u] += (ga[u][k] * x[u][2 * k] + gb[u][k] * x[u][2 * k + 1]) * iv[u];  // d temp
+                    ga[u][k] *= sc;
+                    gb[u][k] *= sc;
+                    dot[u] += ga[u][k] * x[u][2 * k] + gb[u][k] * x[u][2 * k + 1];
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int u = 0; u < 2 * QRU; ++u) {
+                    dot[u] += __shfl_xor_sync(0xffffffff, dot[u], o);
+                    tdot[u] += __shfl_xor_sync(0xffffffff, tdot[u], o);
+                }
+#pragma unroll
+            for (int rr = 0; rr < QRU; ++rr)  // q of row n0, n0 + 1, ...: the sequential order
+                if (ok[2 * rr]) dtemp += tdot[2 * rr];
+#pragma unroll
+            for (int u = 0; u < 2 * QRU; ++u) {
+                if (!act || !ok[u]) continue;
+                const float kk = dot[u] * iv[u] * iv[u] * iv[u];  // autodiff.cpp:746-748
+                float o8[8];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    o8[2 * k] = ga[u][k] * iv[u] - x[u][2 * k] * kk;
+                    o8[2 * k + 1] = gb[u][k] * iv[u] - x[u][2 * k + 1] * kk;
+                }
+                st8(dqkv + off[u], o8);
+            }
+        }
+        if (lane == 0) part_dtemp[(int64_t)blockIdx.x * heads + h] = dtemp;
+    }
+}
 }  // namespace vec
+void qk_norm_rope_bwd_vec_launch(__nv_bfloat16* dqkv, const __nv_bfloat16* qkv, const QKLayout& L, int N, int hd, int heads,
+                                 const float* temp, const float2* cs, const float* iq, const float* ik,
+                                 float* part_dtemp, cudaStream_t s) {
+    vec::qk_norm_rope_bwd_vec<<<dim3(row_chunks(N), (heads + 7) / 8), 256, 0, s>>>(dqkv, qkv, L, N, hd, heads, temp, cs, iq, ik, part_dtemp);
+    ::mgv::note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
+void qk_norm_rope_vec_launch(const __nv_bfloat16* qkv, const QKLayout& L, int N, int hd, int heads, const float* temp,
+                             const float2* cs, __nv_bfloat16* qk, float* iq, float* ik, cudaStream_t s) {
+    const int64_t threads = (int64_t)N * 2 * ((heads + vec::QKV - 1) / vec::QKV) * 32;
+    vec::qk_norm_rope_vec<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(qkv, L, N, hd, heads, temp, cs, qk,
+                                                                                 iq, ik);
+    ::mgv::note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
 
 bool use_vec(int H) { return H % 8 == 0 && H <= vec::RT * vec::VG * 8; }
 
@@ -1502,4 +1674,13 @@ void colsum_vec_launch(const __nv_bfloat16* Y, int64_t ld, int N, int C, float* 
     MGV_CUDA(cudaGetLastError());
 }
 
+}  // namespace mgv
+
+namespace mgv {
+// 16-byte vector path: head_dim % 8 == 0 (<= 256), 16-byte aligned bases, row strides / k offsets multiple of 8
+bool qk_vec_ok(const void* a, const void* b, const QKLayout& L, int hd) {
+    auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    return hd % 8 == 0 && hd <= 256 && al(a) && al(b) && L.in_ld % 8 == 0 && L.in_koff % 8 == 0 && L.out_ld % 8 == 0 &&
+           L.out_koff % 8 == 0;
+}
 }  // namespace mgv
