@@ -20,6 +20,10 @@
  *   mgv_flow_loss            flow::flow_loss                        proj/include/mugv/flowtrain.hpp:26
  *   mgv_latent_rows          dit::latent_rows                       proj/include/mugv/dit.hpp:58
  *   mgv_rows_to_grid         dit::rows_to_grid                      proj/include/mugv/dit.hpp:62
+ *   mgv_ckpt_load / _read    mugv::load_checkpoint                  proj/include/mugv/params.hpp:60, params.cpp:128-225
+ *   mgv_ckpt_save            mugv::save_checkpoint                  proj/include/mugv/params.hpp:59, params.cpp:92-126
+ *   mgv_params_upload_ckpt   load_checkpoint -> ParameterSet handed to the hot path (device upload, no fp64 trip)
+ *   mgv_params_save          save_checkpoint of the trained dit.* parameters (device fp32 masters)
  */
 #ifndef MUGV_B200_H
 #define MUGV_B200_H
@@ -41,7 +45,8 @@ typedef enum {
     MGV_ERR_NUMERIC = 4,   /* NumericError */
     MGV_ERR_CUDA = 5,
     MGV_ERR_NCCL = 6,
-    MGV_ERR_INTERNAL = 7
+    MGV_ERR_INTERNAL = 7,
+    MGV_ERR_CHECKPOINT = 8 /* CheckpointError; kind from mgv_ckpt_last_error_kind() */
 } mgv_status;
 
 typedef enum { MGV_PREC_FP32 = 0, MGV_PREC_BF16 = 1 } mgv_precision;
@@ -152,6 +157,49 @@ int64_t mgv_last_step_launches(mgv_ctx* ctx);
 mgv_status mgv_prof_enable(mgv_ctx* ctx, int on);
 int64_t mgv_prof_count(mgv_ctx* ctx);
 const char* mgv_prof_entry(mgv_ctx* ctx, int64_t i, double* ms, int64_t* launches);
+
+/* ---- MUGVCKPT checkpoint container (proj/include/mugv/params.hpp:54-61, proj/src/params.cpp:92-225) ----
+ * Host-only (no device needed).  The writer emits the same bytes as mugv::save_checkpoint for the same
+ * ParameterSet; the reader applies the reference's validation with its CheckpointError kinds
+ * (errors.hpp:43): a failing call returns MGV_ERR_CHECKPOINT and sets the calling thread's
+ * mgv_ckpt_last_error() / mgv_ckpt_last_error_kind().  Entries are in sorted-name order. */
+typedef struct mgv_ckpt mgv_ckpt;
+typedef enum { MGV_CKPT_F32 = 0, MGV_CKPT_F64 = 1 } mgv_ckpt_dtype_t; /* Dtype (params.hpp:14) */
+typedef enum {
+    MGV_CKPT_BAD_MAGIC = 0,
+    MGV_CKPT_TRUNCATED = 1,
+    MGV_CKPT_BAD_HEADER = 2,
+    MGV_CKPT_BAD_OFFSETS = 3,
+    MGV_CKPT_IO = 4
+} mgv_ckpt_error_kind; /* CheckpointError::Kind, same order */
+const char* mgv_ckpt_last_error(void);
+int mgv_ckpt_last_error_kind(void); /* -1 when the last error was not a CheckpointError */
+mgv_status mgv_ckpt_load(const char* path, mgv_ckpt** out);
+void mgv_ckpt_free(mgv_ckpt* ck);
+int64_t mgv_ckpt_count(const mgv_ckpt* ck);
+const char* mgv_ckpt_name(const mgv_ckpt* ck, int64_t i);
+int mgv_ckpt_dtype(const mgv_ckpt* ck, int64_t i); /* mgv_ckpt_dtype_t */
+int mgv_ckpt_rank(const mgv_ckpt* ck, int64_t i);
+const int64_t* mgv_ckpt_shape(const mgv_ckpt* ck, int64_t i);
+int64_t mgv_ckpt_numel(const mgv_ckpt* ck, int64_t i);
+int64_t mgv_ckpt_find(const mgv_ckpt* ck, const char* name); /* -1 if absent */
+/* widened to fp64 exactly as the reference loads it (f32 payloads -> double) */
+mgv_status mgv_ckpt_read(const mgv_ckpt* ck, int64_t i, double* out);
+int64_t mgv_ckpt_meta_count(const mgv_ckpt* ck);
+const char* mgv_ckpt_meta_key(const mgv_ckpt* ck, int64_t i); /* sorted keys */
+const char* mgv_ckpt_meta_value(const mgv_ckpt* ck, int64_t i);
+/* save_checkpoint of n tensors (any order; dtypes NULL = all f64) plus string metadata.  MGV_ERR_INPUT for
+ * the reserved name "__meta__" (params.cpp:93), duplicates or ill-formed UTF-8. */
+mgv_status mgv_ckpt_save(const char* path, int64_t n, const char* const* names, const double* const* data,
+                         const int* dtypes, const int* ranks, const int64_t* const* shapes, int64_t n_meta,
+                         const char* const* meta_keys, const char* const* meta_values);
+/* mgv_params_upload from a loaded checkpoint's dit.* entries: f32 payloads go to the device fp32 masters
+ * bit-exactly, f64 payloads are rounded once (as mgv_params_upload does). */
+mgv_status mgv_params_upload_ckpt(mgv_ctx* ctx, const mgv_dit_cfg* cfg, const mgv_ckpt* ck);
+/* save_checkpoint of the context's dit.* parameters (e.g. after AdamW steps), dtype f32 (the fp32 masters,
+ * bit-exact) or f64 (widened), with string metadata. */
+mgv_status mgv_params_save(mgv_ctx* ctx, const char* path, int dtype, int64_t n_meta, const char* const* meta_keys,
+                           const char* const* meta_values);
 
 #ifdef __cplusplus
 }

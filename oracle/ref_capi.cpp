@@ -13,8 +13,10 @@
 //   - the per-sample loop of FlowTrainer::step   proj/src/flowtrain.cpp:257-279 (minus AdamW)
 //   - dit::predict_velocity / dit::dit_forward   proj/src/dit.cpp:361-396
 //   - flow::make_batch                           proj/src/flowtrain.cpp:231-250
+//   - save_checkpoint / load_checkpoint          proj/src/params.cpp:92-225
 #include <cmath>
 #include <cstring>
+#include <iterator>
 #include <exception>
 #include <memory>
 #include <string>
@@ -23,12 +25,14 @@
 #include "mugv/optim.hpp"
 #include "mugv/dit.hpp"
 #include "mugv/flowtrain.hpp"
+#include "mugv/params.hpp"
 
 using namespace mugv;
 
 namespace {
 
 thread_local std::string g_err;
+thread_local int g_ckpt_kind = -1;
 
 struct RefCfg {
     int64_t depth, hidden, heads, text_dim, c_z;
@@ -74,6 +78,10 @@ int guard(F&& f) {
     } catch (const NumericError& e) {
         g_err = e.what();
         return 4;
+    } catch (const CheckpointError& e) {
+        g_err = e.what();
+        g_ckpt_kind = static_cast<int>(e.kind);
+        return 8;
     } catch (const std::exception& e) {
         g_err = e.what();
         return 9;
@@ -85,6 +93,55 @@ int guard(F&& f) {
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+int ref_last_ckpt_kind() { return g_ckpt_kind; }
+
+// ---- checkpoint container (params.cpp:92-225) ----
+// dtypes: 0 = f32, 1 = f64 (Dtype order of params.hpp:14)
+int ref_ckpt_save(const char* path, int64_t n, const char* const* names, const double* const* data, const int* dtypes,
+                  const int* ranks, const int64_t* const* shapes, int64_t n_meta, const char* const* keys,
+                  const char* const* values) {
+    g_ckpt_kind = -1;
+    return guard([&] {
+        ParameterSet ps;
+        for (int64_t k = 0; k < n; ++k) {
+            std::vector<int64_t> shape(shapes[k], shapes[k] + ranks[k]);
+            Tensor t(shape);
+            std::memcpy(t.data(), data[k], sizeof(double) * static_cast<size_t>(t.numel()));
+            ps.set(names[k], std::move(t), dtypes[k] == 0 ? Dtype::f32 : Dtype::f64);
+        }
+        for (int64_t k = 0; k < n_meta; ++k) ps.metadata[keys[k]] = values[k];
+        save_checkpoint(ps, path);
+    });
+}
+void* ref_ckpt_load(const char* path) {
+    g_ckpt_kind = -1;
+    Handle* h = nullptr;
+    guard([&] {
+        auto hh = std::make_unique<Handle>();
+        hh->p = load_checkpoint(path);
+        hh->refresh();
+        h = hh.release();
+    });
+    return h;
+}
+int ref_params_dtype(void* h, int64_t i) {
+    auto* hh = static_cast<Handle*>(h);
+    return hh->p.entry(hh->names[static_cast<size_t>(i)]).dtype == Dtype::f32 ? 0 : 1;
+}
+int ref_params_rank(void* h, int64_t i) {
+    auto* hh = static_cast<Handle*>(h);
+    return static_cast<int>(hh->p.at(hh->names[static_cast<size_t>(i)]).shape().size());
+}
+const int64_t* ref_params_shape(void* h, int64_t i) {
+    auto* hh = static_cast<Handle*>(h);
+    return hh->p.at(hh->names[static_cast<size_t>(i)]).shape().data();
+}
+int64_t ref_params_meta_count(void* h) { return static_cast<int64_t>(static_cast<Handle*>(h)->p.metadata.size()); }
+const char* ref_params_meta(void* h, int64_t i, int value) {
+    auto it = static_cast<Handle*>(h)->p.metadata.begin();
+    std::advance(it, i);
+    return value ? it->second.c_str() : it->first.c_str();
+}
 
 // ---- Rng pins ----
 void ref_rng_normal_fill(uint64_t seed, int64_t skip_uniform, int64_t n, double stddev, double* out) {

@@ -16,7 +16,7 @@ from ._lib import lib as _lib
 P, I, I64, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
 
 STATUS = {0: "OK", 1: "DimensionError", 2: "ConfigError", 3: "InputError", 4: "NumericError", 5: "CudaError",
-          6: "NcclError", 7: "InternalError"}
+          6: "NcclError", 7: "InternalError", 8: "CheckpointError"}
 
 
 class MugvError(RuntimeError):
@@ -41,6 +41,15 @@ class InputError(MugvError):
 class NumericError(MugvError):
     pass
 
+
+class CheckpointError(MugvError):
+    """mugv::CheckpointError (errors.hpp:41-45); .ckpt_kind is one of CKPT_KINDS."""
+    def __init__(self, status, msg, kind):
+        super().__init__(status, msg)
+        self.ckpt_kind = kind
+
+
+CKPT_KINDS = {0: "BadMagic", 1: "Truncated", 2: "BadHeader", 3: "BadOffsets", 4: "Io"}  # CheckpointError::Kind
 
 _EXC = {1: DimensionError, 2: ConfigError, 3: InputError, 4: NumericError}
 
@@ -111,6 +120,43 @@ def declare(L):
     L.mgv_prof_count.restype = I64
     L.mgv_prof_entry.argtypes = [P, I64, ctypes.POINTER(D), ctypes.POINTER(I64)]
     L.mgv_prof_entry.restype = ctypes.c_char_p
+    CP = ctypes.c_char_p
+    L.mgv_ckpt_last_error.argtypes = []
+    L.mgv_ckpt_last_error.restype = CP
+    L.mgv_ckpt_last_error_kind.argtypes = []
+    L.mgv_ckpt_last_error_kind.restype = I
+    L.mgv_ckpt_load.argtypes = [CP, ctypes.POINTER(P)]
+    L.mgv_ckpt_load.restype = I
+    L.mgv_ckpt_free.argtypes = [P]
+    L.mgv_ckpt_free.restype = None
+    L.mgv_ckpt_count.argtypes = [P]
+    L.mgv_ckpt_count.restype = I64
+    L.mgv_ckpt_name.argtypes = [P, I64]
+    L.mgv_ckpt_name.restype = CP
+    L.mgv_ckpt_dtype.argtypes = [P, I64]
+    L.mgv_ckpt_dtype.restype = I
+    L.mgv_ckpt_rank.argtypes = [P, I64]
+    L.mgv_ckpt_rank.restype = I
+    L.mgv_ckpt_shape.argtypes = [P, I64]
+    L.mgv_ckpt_shape.restype = ctypes.POINTER(I64)
+    L.mgv_ckpt_numel.argtypes = [P, I64]
+    L.mgv_ckpt_numel.restype = I64
+    L.mgv_ckpt_find.argtypes = [P, CP]
+    L.mgv_ckpt_find.restype = I64
+    L.mgv_ckpt_read.argtypes = [P, I64, P]
+    L.mgv_ckpt_read.restype = I
+    L.mgv_ckpt_meta_count.argtypes = [P]
+    L.mgv_ckpt_meta_count.restype = I64
+    L.mgv_ckpt_meta_key.argtypes = [P, I64]
+    L.mgv_ckpt_meta_key.restype = CP
+    L.mgv_ckpt_meta_value.argtypes = [P, I64]
+    L.mgv_ckpt_meta_value.restype = CP
+    L.mgv_ckpt_save.argtypes = [CP, I64, P, P, P, P, P, I64, P, P]
+    L.mgv_ckpt_save.restype = I
+    L.mgv_params_upload_ckpt.argtypes = [P, ctypes.POINTER(mgv_dit_cfg), P]
+    L.mgv_params_upload_ckpt.restype = I
+    L.mgv_params_save.argtypes = [P, CP, I, I64, P, P]
+    L.mgv_params_save.restype = I
     L.mgv_dev_attn_fwd.restype = I
     L.mgv_dev_attn_bwd.restype = I
 
@@ -121,7 +167,105 @@ EXPORTS = ["mgv_ctx_create", "mgv_ctx_destroy", "mgv_last_error", "mgv_ctx_set_s
            "mgv_params_upload", "mgv_param_count", "mgv_param_name", "mgv_param_numel",
            "mgv_predict_velocity", "mgv_dit_forward", "mgv_flow_step", "mgv_flow_loss", "mgv_latent_rows",
            "mgv_rows_to_grid", "mgv_flow_step_device", "mgv_last_step_ms", "mgv_last_step_launches",
-           "mgv_prof_enable", "mgv_prof_count", "mgv_prof_entry"]
+           "mgv_prof_enable", "mgv_prof_count", "mgv_prof_entry",
+           "mgv_ckpt_last_error", "mgv_ckpt_last_error_kind", "mgv_ckpt_load", "mgv_ckpt_free", "mgv_ckpt_count",
+           "mgv_ckpt_name", "mgv_ckpt_dtype", "mgv_ckpt_rank", "mgv_ckpt_shape", "mgv_ckpt_numel", "mgv_ckpt_find",
+           "mgv_ckpt_read", "mgv_ckpt_meta_count", "mgv_ckpt_meta_key", "mgv_ckpt_meta_value", "mgv_ckpt_save",
+           "mgv_params_upload_ckpt", "mgv_params_save"]
+
+
+# ---------------------------------------------------------------- MUGVCKPT (params.hpp:54-61)
+F32, F64 = 0, 1  # Dtype (params.hpp:14)
+
+
+def _ckpt_raise(st):
+    L = _lib()
+    msg = L.mgv_ckpt_last_error().decode(errors="replace")
+    if st == 8:
+        raise CheckpointError(st, msg, CKPT_KINDS.get(L.mgv_ckpt_last_error_kind(), "?"))
+    raise _EXC.get(st, MugvError)(st, msg)
+
+
+class Checkpoint:
+    """A loaded MUGVCKPT file (mugv::load_checkpoint, params.cpp:128-225): sorted entries, host-side."""
+
+    def __init__(self, path: str):
+        L = _lib()
+        h = P()
+        st = L.mgv_ckpt_load(str(path).encode(), ctypes.byref(h))
+        if st != 0:
+            _ckpt_raise(st)
+        self._L, self.h = L, h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.mgv_ckpt_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def names(self) -> list:
+        return [self._L.mgv_ckpt_name(self.h, i).decode() for i in range(self._L.mgv_ckpt_count(self.h))]
+
+    def dtype(self, name: str) -> int:
+        return self._L.mgv_ckpt_dtype(self.h, self._index(name))
+
+    def _index(self, name: str) -> int:
+        i = self._L.mgv_ckpt_find(self.h, name.encode())
+        if i < 0:
+            raise InputError(3, f'no parameter named "{name}"')
+        return i
+
+    def __getitem__(self, name: str) -> np.ndarray:
+        i = self._index(name)
+        r = self._L.mgv_ckpt_rank(self.h, i)
+        sp = self._L.mgv_ckpt_shape(self.h, i)
+        shape = tuple(int(sp[k]) for k in range(r))
+        out = np.empty(int(self._L.mgv_ckpt_numel(self.h, i)), dtype=np.float64)
+        st = self._L.mgv_ckpt_read(self.h, i, out.ctypes.data)
+        if st != 0:
+            _ckpt_raise(st)
+        return out.reshape(shape)
+
+    def metadata(self) -> dict:
+        n = self._L.mgv_ckpt_meta_count(self.h)
+        return {self._L.mgv_ckpt_meta_key(self.h, i).decode(): self._L.mgv_ckpt_meta_value(self.h, i).decode()
+                for i in range(n)}
+
+    def to_dict(self) -> dict:
+        return {k: self[k] for k in self.names()}
+
+
+def _meta_arrays(meta):
+    keys = list(meta or {})
+    ck = (ctypes.c_char_p * max(1, len(keys)))(*[k.encode() for k in keys])
+    cv = (ctypes.c_char_p * max(1, len(keys)))(*[str(meta[k]).encode() for k in keys])
+    return len(keys), ck, cv
+
+
+def load_checkpoint(path: str) -> Checkpoint:
+    return Checkpoint(path)
+
+
+def save_checkpoint(path: str, params: dict, dtypes: dict | None = None, metadata: dict | None = None):
+    """mugv::save_checkpoint (params.cpp:92-126): name -> array, optional name -> F32/F64, string metadata."""
+    names = list(params)
+    arrs = [np.ascontiguousarray(params[k], dtype=np.float64) for k in names]
+    n = len(names)
+    cn = (ctypes.c_char_p * max(1, n))(*[k.encode() for k in names])
+    dp = (P * max(1, n))(*[a.ctypes.data for a in arrs])
+    dt = (I * max(1, n))(*[int((dtypes or {}).get(k, F64)) for k in names])
+    rk = (I * max(1, n))(*[a.ndim for a in arrs])
+    shp = [(I64 * max(1, a.ndim))(*a.shape) for a in arrs]
+    sp = (P * max(1, n))(*[ctypes.addressof(x) for x in shp])
+    nm, mk, mv = _meta_arrays(metadata)
+    st = _lib().mgv_ckpt_save(str(path).encode(), n, cn, dp, dt, rk, sp, nm, mk, mv)
+    if st != 0:
+        _ckpt_raise(st)
 
 
 @dataclass
@@ -219,6 +363,8 @@ class Context:
     def _check(self, st):
         if st != 0:
             msg = self._L.mgv_last_error(self.h).decode()
+            if st == 8:
+                raise CheckpointError(st, msg, CKPT_KINDS.get(self._L.mgv_ckpt_last_error_kind(), "?"))
             raise _EXC.get(st, MugvError)(st, msg)
 
     def set_stream(self, stream_ptr: int):
@@ -286,6 +432,19 @@ class Context:
         self.cfg = cfg
         self.names = [self._L.mgv_param_name(self.h, i).decode() for i in range(self._L.mgv_param_count(self.h))]
         self.numels = [self._L.mgv_param_numel(self.h, i) for i in range(len(self.names))]
+
+    def upload_checkpoint(self, cfg: DitConfig, ck: "Checkpoint"):
+        """mgv_params_upload_ckpt: the checkpoint's dit.* entries straight to the device."""
+        c = cfg.to_c()
+        self._check(self._L.mgv_params_upload_ckpt(self.h, ctypes.byref(c), ck.h))
+        self.cfg = cfg
+        self.names = [self._L.mgv_param_name(self.h, i).decode() for i in range(self._L.mgv_param_count(self.h))]
+        self.numels = [self._L.mgv_param_numel(self.h, i) for i in range(len(self.names))]
+
+    def save_checkpoint(self, path: str, dtype: int = F32, metadata: dict | None = None):
+        """mgv_params_save: save_checkpoint of the device dit.* parameters."""
+        nm, mk, mv = _meta_arrays(metadata)
+        self._check(self._L.mgv_params_save(self.h, str(path).encode(), int(dtype), nm, mk, mv))
 
     def predict_velocity(self, rows, coords, dims, text, timesteps, fps=8.0):
         rows, text, ts = _f64(rows), _f64(text), _f64(timesteps)

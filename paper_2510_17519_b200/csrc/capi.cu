@@ -5,6 +5,7 @@
 #include <memory>
 #include <string>
 
+#include "ckpt.h"
 #include "gemm.cuh"
 #include "kernels.h"
 #include "model.h"
@@ -40,6 +41,13 @@ mgv_status guard(mgv_ctx* ctx, F&& f) {
     } catch (const mgv::NcclError& e) {
         ctx->err = e.what();
         return MGV_ERR_NCCL;
+    } catch (const mgv::CheckpointError& e) {
+        ctx->err = e.what();
+        mgv::note_ckpt_error(e.what(), e.kind);
+        return MGV_ERR_CHECKPOINT;
+    } catch (const mgv::CkptInputError& e) {
+        ctx->err = e.what();
+        return MGV_ERR_INPUT;
     } catch (const std::exception& e) {
         ctx->err = e.what();
         return MGV_ERR_INTERNAL;
@@ -121,6 +129,64 @@ mgv_status mgv_params_upload(mgv_ctx* ctx, const mgv_dit_cfg* cfg, int64_t n, co
     return guard(ctx, [&] {
         if (!cfg) throw mgv::InputError("null config");
         ctx->model->upload(to_cfg(cfg), n, names, data, numel);
+    });
+}
+
+mgv_status mgv_params_upload_ckpt(mgv_ctx* ctx, const mgv_dit_cfg* cfg, const mgv_ckpt* ck) {
+    return guard(ctx, [&] {
+        if (!cfg || !ck) throw mgv::InputError("null argument");
+        // host copies in each payload's own width (the payload is little-endian and may be unaligned)
+        std::vector<std::vector<float>> f32s;
+        std::vector<std::vector<double>> f64s;
+        std::vector<const char*> names;
+        std::vector<const void*> data;
+        std::vector<uint8_t> is_f32;
+        std::vector<int64_t> numel;
+        f32s.reserve(ck->ck.entries.size());
+        f64s.reserve(ck->ck.entries.size());
+        for (const mgv::CkptEntry& e : ck->ck.entries) {
+            if (e.name.rfind("dit.", 0) != 0) continue;  // register_params(..., "dit.") (flowtrain.cpp:260)
+            names.push_back(e.name.c_str());
+            numel.push_back(e.numel);
+            is_f32.push_back(e.dtype == mgv::kF32);
+            if (e.dtype == mgv::kF32) {
+                f32s.emplace_back(static_cast<size_t>(e.numel));
+                ck->ck.read_f32(e, f32s.back().data());
+                data.push_back(f32s.back().data());
+            } else {
+                f64s.emplace_back(static_cast<size_t>(e.numel));
+                ck->ck.read_f64(e, f64s.back().data());
+                data.push_back(f64s.back().data());
+            }
+        }
+        ctx->model->upload(to_cfg(cfg), static_cast<int64_t>(names.size()), names.data(), data.data(), is_f32.data(),
+                           numel.data());
+    });
+}
+
+mgv_status mgv_params_save(mgv_ctx* ctx, const char* path, int dtype, int64_t n_meta, const char* const* meta_keys,
+                           const char* const* meta_values) {
+    return guard(ctx, [&] {
+        if (!path || (n_meta > 0 && (!meta_keys || !meta_values))) throw mgv::InputError("null argument");
+        if (dtype != MGV_CKPT_F32 && dtype != MGV_CKPT_F64) throw mgv::InputError("unknown dtype");
+        const auto& ps = ctx->model->sorted_params();
+        if (ps.empty()) throw mgv::InputError("no parameters uploaded");
+        std::vector<std::vector<double>> host(ps.size());
+        std::vector<mgv::CkptTensorIn> ts(ps.size());
+        for (size_t k = 0; k < ps.size(); ++k) {
+            host[k].resize(static_cast<size_t>(ps[k]->numel));
+            ctx->model->download_param(static_cast<int64_t>(k), host[k].data());  // fp32 master, widened exactly
+            ts[k].name = ps[k]->name;
+            ts[k].dtype = dtype == MGV_CKPT_F32 ? mgv::kF32 : mgv::kF64;
+            ts[k].shape = ps[k]->shape;
+            ts[k].f64 = host[k].data();
+        }
+        std::map<std::string, std::string> meta;
+        for (int64_t k = 0; k < n_meta; ++k) {
+            if (!meta_keys[k] || !meta_values[k]) throw mgv::InputError("null metadata argument");
+            meta[meta_keys[k]] = meta_values[k];
+        }
+        mgv::save_checkpoint(std::move(ts), meta, path);
     });
 }
 

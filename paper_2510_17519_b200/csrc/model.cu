@@ -451,8 +451,8 @@ void Model::download_param(int64_t i, double* out) {
 }
 
 
-void Model::upload(const Cfg& cfg, int64_t n, const char* const* names, const double* const* data,
-                   const int64_t* numel) {
+void Model::upload(const Cfg& cfg, int64_t n, const char* const* names, const void* const* data,
+                   const uint8_t* is_f32, const int64_t* numel) {
     validate_cfg(cfg);
     if (tp_ > 1 && (cfg.heads % tp_ != 0 || (cfg.hidden / tp_) % 8 != 0))
         throw ConfigError("tensor parallel size must divide heads, with hidden/size a multiple of 8");
@@ -548,14 +548,22 @@ void Model::upload(const Cfg& cfg, int64_t n, const char* const* names, const do
     double* staging = nullptr;
     int64_t stage_n = 0;
     for (auto& kv : params_) stage_n = std::max(stage_n, kv.second.numel);
-    MGV_CUDA(cudaMalloc(&staging, sizeof(double) * stage_n * (tp_ > 1 ? 2 : 1)));
+    // staging: [0, n) fp64 input | [n, 2n) permuted rows (TP) | [2n, 3n) raw fp32 input (widened exactly)
+    MGV_CUDA(cudaMalloc(&staging, sizeof(double) * stage_n * 3));
     for (auto& kv : params_) {
         DevParam& p = kv.second;
         const int64_t gi = given[p.name];
         if (numel[gi] != p.numel)
             throw DimensionError("parameter " + p.name + " has " + std::to_string(numel[gi]) + " elements, expected " +
                                  std::to_string(p.numel));
-        MGV_CUDA(cudaMemcpyAsync(staging, data[gi], sizeof(double) * p.numel, cudaMemcpyHostToDevice, stream_));
+        if (is_f32 && is_f32[gi]) {
+            float* raw = reinterpret_cast<float*>(staging + 2 * stage_n);
+            MGV_CUDA(cudaMemcpyAsync(raw, data[gi], sizeof(float) * p.numel, cudaMemcpyHostToDevice, stream_));
+            f32_to_f64<<<grid_of(p.numel), 256, 0, stream_>>>(raw, p.numel, staging);
+            ::mgv::note_launch();
+        } else {
+            MGV_CUDA(cudaMemcpyAsync(staging, data[gi], sizeof(double) * p.numel, cudaMemcpyHostToDevice, stream_));
+        }
         const double* src = staging;
         if (const int C = tp_ > 1 ? tp_row_chunks(p.name) : 0) {
             permute_shard_rows(staging, staging + stage_n, C, static_cast<int>(H), tp_, p.numel / (C * H), 0, stream_);

@@ -119,6 +119,11 @@ public:
     void download_param(int64_t i, double* out);
 
     void upload(const Cfg& cfg, int64_t n, const char* const* names, const double* const* data,
+                const int64_t* numel) {
+        upload(cfg, n, names, reinterpret_cast<const void* const*>(data), nullptr, numel);
+    }
+    // is_f32[i] != 0: data[i] is float (a checkpoint's f32 payload, uploaded bit-exactly); nullptr = all fp64
+    void upload(const Cfg& cfg, int64_t n, const char* const* names, const void* const* data, const uint8_t* is_f32,
                 const int64_t* numel);
     const std::vector<DevParam*>& sorted_params() const { return sorted_; }
 
