@@ -24,6 +24,10 @@
  *   mgv_ckpt_save            mugv::save_checkpoint                  proj/include/mugv/params.hpp:59, params.cpp:92-126
  *   mgv_params_upload_ckpt   load_checkpoint -> ParameterSet handed to the hot path (device upload, no fp64 trip)
  *   mgv_params_save          save_checkpoint of the trained dit.* parameters (device fp32 masters)
+ *   mgv_flow_errors          post::flow_error (forward only)        proj/include/mugv/posttrain.hpp:72-75
+ *   mgv_flow_step_weighted   the tape of post_loss_graph: sum_k w_k dl_k, grad_norm, AdamW
+ *   mgv_post_*               post::PostTrainState / post_train_step / post_loss_graph / dpo_loss / kto_loss
+ *                                                                   proj/include/mugv/posttrain.hpp:83-154
  */
 #ifndef MUGV_B200_H
 #define MUGV_B200_H
@@ -46,7 +50,8 @@ typedef enum {
     MGV_ERR_CUDA = 5,
     MGV_ERR_NCCL = 6,
     MGV_ERR_INTERNAL = 7,
-    MGV_ERR_CHECKPOINT = 8 /* CheckpointError; kind from mgv_ckpt_last_error_kind() */
+    MGV_ERR_CHECKPOINT = 8, /* CheckpointError; kind from mgv_ckpt_last_error_kind() */
+    MGV_ERR_SCHEDULING = 9  /* SchedulingError (post-training interleave plan) */
 } mgv_status;
 
 typedef enum { MGV_PREC_FP32 = 0, MGV_PREC_BF16 = 1 } mgv_precision;
@@ -69,6 +74,16 @@ typedef struct {
     const uint8_t* conditioned;
     const double* condition_latents;
 } mgv_flow_sample;
+
+/* One flow-error evaluation of post-training (posttrain.hpp:15-21 SampleRecord at its SharedDraw :66-69):
+ * s.clean_rows = the record's latent rows, s.noise / s.t = the shared draw, s.conditioned /
+ * s.condition_latents = the record's ConditionMask (first-frame masks), plus the record's own text and fps. */
+typedef struct {
+    mgv_flow_sample s;
+    const double* text; /* L x text_dim */
+    int64_t L;
+    double fps;
+} mgv_eval_sample;
 
 mgv_status mgv_ctx_create(int device, int precision, mgv_ctx** out);
 void mgv_ctx_destroy(mgv_ctx* ctx);
@@ -200,6 +215,61 @@ mgv_status mgv_params_upload_ckpt(mgv_ctx* ctx, const mgv_dit_cfg* cfg, const mg
  * bit-exact) or f64 (widened), with string metadata. */
 mgv_status mgv_params_save(mgv_ctx* ctx, const char* path, int dtype, int64_t n_meta, const char* const* meta_keys,
                            const char* const* meta_values);
+
+/* ---- Post-training on the same forward (proj/src/posttrain.cpp) ---- */
+/* post::flow_error (posttrain.cpp:126-142) of n records, forward only: errs[k] = masked flow loss l_k. */
+mgv_status mgv_flow_errors(mgv_ctx* ctx, int64_t n, const mgv_eval_sample* recs, double* errs);
+/* One fwd+bwd over n records with Loss = sum_k weights[k] l_k: gradients sum_k w_k dl_k/dtheta, grad_norm
+ * (flowtrain.cpp:284-289) and, when mgv_ctx_set_adamw is on, the AdamW update.  errs[k] = l_k, *loss = Loss. */
+mgv_status mgv_flow_step_weighted(mgv_ctx* ctx, int64_t n, const mgv_eval_sample* recs, const double* weights,
+                                  double* errs, double* loss, double* grad_norm, double* const* grads_out);
+
+/* post::PostTrainConfig (posttrain.hpp:37-44); interleave = n_interleave tags, each "dpo" or "kto" */
+typedef struct {
+    double beta, alpha_sft, gamma_merge, w_d, w_u;
+    int64_t n_interleave;
+    const char* const* interleave;
+} mgv_post_cfg;
+/* post::SampleRecord (posttrain.hpp:15-21): latent rows on a grid, its ConditionMask, text and fps */
+typedef struct {
+    int64_t dims[3];
+    const int32_t* coords;
+    const double* rows;              /* N x 4c_z */
+    const uint8_t* conditioned;      /* N flags or NULL */
+    const double* condition_latents; /* N x 4c_z or NULL (= rows) */
+    const double* text;              /* L x text_dim */
+    int64_t L;
+    double fps;
+} mgv_sample_record;
+typedef struct { mgv_sample_record winner, loser; } mgv_pref_pair;            /* posttrain.hpp:24-28 */
+typedef struct { mgv_sample_record sample; int desirable; } mgv_labeled_sample; /* posttrain.hpp:30-33 */
+typedef struct { double total, preference, sft, grad_norm; } mgv_post_metrics; /* posttrain.hpp:138-143 */
+typedef struct mgv_post_state mgv_post_state;
+
+/* post::validate(PostTrainConfig) (posttrain.cpp:37-49): MGV_ERR_CONFIG with the reference's message */
+mgv_status mgv_post_validate(const mgv_post_cfg* cfg, char* err, int64_t err_cap);
+/* PostTrainState(start, cfg, lr, seed) (posttrain.cpp:250-253): `policy` holds the trained weights (its AdamW is
+ * set to AdamW(lr) defaults), `ref` the frozen reference copy (upload the same start weights to both). */
+mgv_status mgv_post_state_create(mgv_ctx* policy, mgv_ctx* ref, double lr, uint64_t seed, mgv_post_state** out);
+void mgv_post_state_destroy(mgv_post_state* st);
+int64_t mgv_post_plan_pos(const mgv_post_state* st);
+const char* mgv_post_last_error(const mgv_post_state* st);
+/* post_train_step (posttrain.cpp:292-320): tag "dpo" consumes pairs, "kto" labels; the SFT batch is a
+ * FlowBatch (flowtrain.hpp:111-123, shared text and fps).  Draws come from the state's Rng, as the
+ * reference's make_pair_draws / make_label_draws.  MGV_ERR_SCHEDULING if tag != the plan's next tag. */
+mgv_status mgv_post_train_step(mgv_post_state* st, const mgv_post_cfg* cfg, const char* tag, int64_t n_pairs,
+                               const mgv_pref_pair* pairs, int64_t n_labels, const mgv_labeled_sample* labels,
+                               int64_t n_sft, const mgv_flow_sample* sft, const double* sft_text, int64_t sft_L,
+                               double sft_fps, mgv_post_metrics* out);
+/* dpo_loss / kto_loss (posttrain.cpp:171-177, 224-233): the preference loss alone, forward only, with draws
+ * from Rng(seed); kto uses cfg->beta, w_d, w_u. */
+mgv_status mgv_post_pref_loss(mgv_ctx* policy, mgv_ctx* ref, const mgv_post_cfg* cfg, const char* tag,
+                              int64_t n_pairs, const mgv_pref_pair* pairs, int64_t n_labels,
+                              const mgv_labeled_sample* labels, uint64_t seed, double* loss);
+/* scalar helpers: dpo_from_errors, kto_from_rewards (z0 NULL = batch mean) (posttrain.cpp:144-204) */
+double mgv_dpo_from_errors(double e_th_w, double e_th_l, double e_ref_w, double e_ref_l, double beta);
+mgv_status mgv_kto_from_rewards(int64_t n, const double* rewards, const uint8_t* desirable, double w_d, double w_u,
+                                const double* z0_override, double* out);
 
 #ifdef __cplusplus
 }

@@ -14,6 +14,8 @@
 //   - dit::predict_velocity / dit::dit_forward   proj/src/dit.cpp:361-396
 //   - flow::make_batch                           proj/src/flowtrain.cpp:231-250
 //   - save_checkpoint / load_checkpoint          proj/src/params.cpp:92-225
+//   - post::post_loss_graph (+ backward), make_pair_draws / make_label_draws, dpo_loss / kto_loss
+//                                                proj/src/posttrain.cpp:106-290
 #include <cmath>
 #include <cstring>
 #include <iterator>
@@ -26,6 +28,7 @@
 #include "mugv/dit.hpp"
 #include "mugv/flowtrain.hpp"
 #include "mugv/params.hpp"
+#include "mugv/posttrain.hpp"
 
 using namespace mugv;
 
@@ -386,6 +389,107 @@ int ref_adamw_update_params(void* o, void* h, const double* const* grads) {
             gs.emplace(hh->names[i], std::move(g));
         }
         static_cast<AdamW*>(o)->update(hh->p, gs);
+    });
+}
+
+// ---- post-training (posttrain.cpp) ----
+struct RefRecord {  // one post::SampleRecord; cond = first_frame_mask(geom, rows) or no condition
+    int64_t dims[3];
+    const double* rows;
+    int32_t cond;
+    const double* text;
+    int64_t L;
+    double fps;
+};
+
+static post::SampleRecord record_of(const RefRecord& r, const dit::DitConfig& cfg) {
+    post::SampleRecord s;
+    s.geom = geom_of(r.dims, cfg.c_z);
+    const int64_t N = s.geom.n(), D = cfg.patch_dim();
+    s.rows = Tensor({N, D});
+    std::memcpy(s.rows.data(), r.rows, sizeof(double) * static_cast<size_t>(N * D));
+    s.mask = r.cond ? flow::first_frame_mask(s.geom, s.rows) : flow::no_condition(N);
+    s.text = Tensor({r.L, cfg.text_dim});
+    std::memcpy(s.text.data(), r.text, sizeof(double) * static_cast<size_t>(s.text.numel()));
+    s.fps = r.fps;
+    return s;
+}
+
+// post_loss_graph (+ backward when grads_out) on the policy weights `pol` with the frozen `ref`; tag "dpo":
+// recs are n pairs as (winner, loser) consecutive records; "kto": n labelled records (desirable flags).
+// Draws: make_pair_draws / make_label_draws with Rng(seed).  SFT batch: n_sft samples, shared text / fps.
+int ref_post_loss(void* pol, void* ref, const RefCfg* c, const char* tag, double beta, double alpha, double w_d,
+                  double w_u, int64_t n, const RefRecord* recs, const int32_t* desirable, int64_t n_sft,
+                  const int64_t* sft_dims, const double* const* sft_clean, const double* const* sft_noise,
+                  const double* sft_t, const int32_t* sft_cond, const double* sft_text, int64_t sft_L, double sft_fps,
+                  uint64_t seed, double* total_out, double* pref_out, double* sft_out, double* grad_norm_out,
+                  double* const* grads_out) {
+    return guard([&] {
+        auto* ph = static_cast<Handle*>(pol);
+        auto* rh = static_cast<Handle*>(ref);
+        auto cfg = to_cfg(c);
+        post::PostTrainConfig pc;
+        pc.beta = beta;
+        pc.alpha_sft = alpha;
+        pc.w_d = w_d;
+        pc.w_u = w_u;
+        post::PrefBatch batch;
+        batch.tag = tag;
+        Rng rng(seed);
+        std::vector<post::SharedDraw> draws;
+        if (batch.tag == "dpo") {
+            for (int64_t i = 0; i < n; ++i) {
+                post::PreferencePair p;
+                p.winner = record_of(recs[2 * i], cfg);
+                p.loser = record_of(recs[2 * i + 1], cfg);
+                batch.pairs.push_back(std::move(p));
+            }
+            draws = post::make_pair_draws(batch.pairs, rng);
+        } else {
+            for (int64_t i = 0; i < n; ++i) {
+                post::LabeledSample l;
+                l.sample = record_of(recs[i], cfg);
+                l.desirable = desirable[i] != 0;
+                batch.labels.push_back(std::move(l));
+            }
+            draws = post::make_label_draws(batch.labels, rng);
+        }
+        flow::FlowBatch sft;
+        sft.text_emb = Tensor({sft_L, cfg.text_dim});
+        std::memcpy(sft.text_emb.data(), sft_text, sizeof(double) * static_cast<size_t>(sft.text_emb.numel()));
+        sft.fps = sft_fps;
+        for (int64_t i = 0; i < n_sft; ++i) {
+            flow::FlowSample s;
+            s.geom = geom_of(sft_dims + 3 * i, cfg.c_z);
+            const int64_t N = s.geom.n(), D = cfg.patch_dim();
+            s.clean_rows = Tensor({N, D});
+            s.noise = Tensor({N, D});
+            std::memcpy(s.clean_rows.data(), sft_clean[i], sizeof(double) * static_cast<size_t>(N * D));
+            std::memcpy(s.noise.data(), sft_noise[i], sizeof(double) * static_cast<size_t>(N * D));
+            s.t = sft_t[i];
+            s.mask = sft_cond[i] ? flow::first_frame_mask(s.geom, s.clean_rows) : flow::no_condition(N);
+            sft.samples.push_back(std::move(s));
+        }
+        Tape t;
+        ParamVars pv = register_params(t, ph->p, grads_out != nullptr, "dit.");
+        Var pref, sftv;
+        Var total = post::post_loss_graph(t, pv, rh->p, cfg, batch, draws, sft, pc, &pref, &sftv);
+        *total_out = t.val(total)[0];
+        *pref_out = t.val(pref)[0];
+        *sft_out = t.val(sftv)[0];
+        if (grads_out) {
+            t.backward(total);
+            auto grads = collect_grads(t, pv);
+            *grad_norm_out = flow::grad_norm(grads);
+            size_t k = 0;
+            for (const auto& nm : ph->names) {
+                if (grads_out[k]) {
+                    const Tensor& g = grads.at(nm);
+                    std::memcpy(grads_out[k], g.data(), sizeof(double) * static_cast<size_t>(g.numel()));
+                }
+                ++k;
+            }
+        }
     });
 }
 

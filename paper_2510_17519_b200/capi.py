@@ -16,7 +16,7 @@ from ._lib import lib as _lib
 P, I, I64, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
 
 STATUS = {0: "OK", 1: "DimensionError", 2: "ConfigError", 3: "InputError", 4: "NumericError", 5: "CudaError",
-          6: "NcclError", 7: "InternalError", 8: "CheckpointError"}
+          6: "NcclError", 7: "InternalError", 8: "CheckpointError", 9: "SchedulingError"}
 
 
 class MugvError(RuntimeError):
@@ -51,7 +51,11 @@ class CheckpointError(MugvError):
 
 CKPT_KINDS = {0: "BadMagic", 1: "Truncated", 2: "BadHeader", 3: "BadOffsets", 4: "Io"}  # CheckpointError::Kind
 
-_EXC = {1: DimensionError, 2: ConfigError, 3: InputError, 4: NumericError}
+class SchedulingError(MugvError):
+    pass
+
+
+_EXC = {1: DimensionError, 2: ConfigError, 3: InputError, 4: NumericError, 9: SchedulingError}
 
 
 class mgv_dit_cfg(ctypes.Structure):
@@ -62,6 +66,32 @@ class mgv_dit_cfg(ctypes.Structure):
 class mgv_flow_sample(ctypes.Structure):
     _fields_ = [("dims", I64 * 3), ("coords", P), ("clean_rows", P), ("noise", P), ("t", D), ("conditioned", P),
                 ("condition_latents", P)]
+
+
+class mgv_eval_sample(ctypes.Structure):
+    _fields_ = [("s", mgv_flow_sample), ("text", P), ("L", I64), ("fps", D)]
+
+
+class mgv_post_cfg(ctypes.Structure):
+    _fields_ = [("beta", D), ("alpha_sft", D), ("gamma_merge", D), ("w_d", D), ("w_u", D), ("n_interleave", I64),
+                ("interleave", P)]
+
+
+class mgv_sample_record(ctypes.Structure):
+    _fields_ = [("dims", I64 * 3), ("coords", P), ("rows", P), ("conditioned", P), ("condition_latents", P),
+                ("text", P), ("L", I64), ("fps", D)]
+
+
+class mgv_pref_pair(ctypes.Structure):
+    _fields_ = [("winner", mgv_sample_record), ("loser", mgv_sample_record)]
+
+
+class mgv_labeled_sample(ctypes.Structure):
+    _fields_ = [("sample", mgv_sample_record), ("desirable", I)]
+
+
+class mgv_post_metrics(ctypes.Structure):
+    _fields_ = [("total", D), ("preference", D), ("sft", D), ("grad_norm", D)]
 
 
 def declare(L):
@@ -157,6 +187,28 @@ def declare(L):
     L.mgv_params_upload_ckpt.restype = I
     L.mgv_params_save.argtypes = [P, CP, I, I64, P, P]
     L.mgv_params_save.restype = I
+    L.mgv_flow_errors.argtypes = [P, I64, P, P]
+    L.mgv_flow_errors.restype = I
+    L.mgv_flow_step_weighted.argtypes = [P, I64, P, P, P, ctypes.POINTER(D), ctypes.POINTER(D), P]
+    L.mgv_flow_step_weighted.restype = I
+    L.mgv_post_validate.argtypes = [P, ctypes.c_char_p, I64]
+    L.mgv_post_validate.restype = I
+    L.mgv_post_state_create.argtypes = [P, P, D, ctypes.c_uint64, ctypes.POINTER(P)]
+    L.mgv_post_state_create.restype = I
+    L.mgv_post_state_destroy.argtypes = [P]
+    L.mgv_post_state_destroy.restype = None
+    L.mgv_post_plan_pos.argtypes = [P]
+    L.mgv_post_plan_pos.restype = I64
+    L.mgv_post_last_error.argtypes = [P]
+    L.mgv_post_last_error.restype = ctypes.c_char_p
+    L.mgv_post_train_step.argtypes = [P, P, ctypes.c_char_p, I64, P, I64, P, I64, P, P, I64, D, P]
+    L.mgv_post_train_step.restype = I
+    L.mgv_post_pref_loss.argtypes = [P, P, P, ctypes.c_char_p, I64, P, I64, P, ctypes.c_uint64, ctypes.POINTER(D)]
+    L.mgv_post_pref_loss.restype = I
+    L.mgv_dpo_from_errors.argtypes = [D, D, D, D, D]
+    L.mgv_dpo_from_errors.restype = D
+    L.mgv_kto_from_rewards.argtypes = [I64, P, P, D, D, P, ctypes.POINTER(D)]
+    L.mgv_kto_from_rewards.restype = I
     L.mgv_dev_attn_fwd.restype = I
     L.mgv_dev_attn_bwd.restype = I
 
@@ -171,7 +223,10 @@ EXPORTS = ["mgv_ctx_create", "mgv_ctx_destroy", "mgv_last_error", "mgv_ctx_set_s
            "mgv_ckpt_last_error", "mgv_ckpt_last_error_kind", "mgv_ckpt_load", "mgv_ckpt_free", "mgv_ckpt_count",
            "mgv_ckpt_name", "mgv_ckpt_dtype", "mgv_ckpt_rank", "mgv_ckpt_shape", "mgv_ckpt_numel", "mgv_ckpt_find",
            "mgv_ckpt_read", "mgv_ckpt_meta_count", "mgv_ckpt_meta_key", "mgv_ckpt_meta_value", "mgv_ckpt_save",
-           "mgv_params_upload_ckpt", "mgv_params_save"]
+           "mgv_params_upload_ckpt", "mgv_params_save",
+           "mgv_flow_errors", "mgv_flow_step_weighted", "mgv_post_validate", "mgv_post_state_create",
+           "mgv_post_state_destroy", "mgv_post_plan_pos", "mgv_post_last_error", "mgv_post_train_step",
+           "mgv_post_pref_loss", "mgv_dpo_from_errors", "mgv_kto_from_rewards"]
 
 
 # ---------------------------------------------------------------- MUGVCKPT (params.hpp:54-61)
@@ -334,6 +389,143 @@ class FlowSample:
         return s
 
 
+@dataclass
+class SampleRecord:
+    """post::SampleRecord (posttrain.hpp:15-21): latent rows on a grid, first-frame mask or none, text, fps."""
+    dims: tuple
+    coords: np.ndarray
+    rows: np.ndarray
+    text: np.ndarray
+    fps: float = 8.0
+    conditioned: np.ndarray | None = None
+    _keep: list = field(default_factory=list, repr=False)
+
+    def to_c(self):
+        r = mgv_sample_record()
+        for i in range(3):
+            r.dims[i] = int(self.dims[i])
+        co = np.ascontiguousarray(self.coords, dtype=np.int32)
+        rw, tx = _f64(self.rows), _f64(self.text)
+        self._keep = [co, rw, tx]
+        r.coords, r.rows, r.text, r.L, r.fps = co.ctypes.data, rw.ctypes.data, tx.ctypes.data, tx.shape[0], self.fps
+        if self.conditioned is not None and np.any(self.conditioned):
+            m = np.ascontiguousarray(self.conditioned, dtype=np.uint8)
+            self._keep.append(m)
+            r.conditioned = m.ctypes.data
+        return r
+
+
+@dataclass
+class PostTrainConfig:
+    """post::PostTrainConfig (posttrain.hpp:37-44)."""
+    beta: float = 1.0
+    alpha_sft: float = 1.0
+    gamma_merge: float = 0.9
+    w_d: float = 1.0
+    w_u: float = 1.0
+    interleave: tuple = ("dpo", "kto")
+
+    def to_c(self):
+        c = mgv_post_cfg(self.beta, self.alpha_sft, self.gamma_merge, self.w_d, self.w_u, len(self.interleave), None)
+        self._tags = (ctypes.c_char_p * max(1, len(self.interleave)))(*[t.encode() for t in self.interleave])
+        c.interleave = ctypes.cast(self._tags, P)
+        return c
+
+
+def _pairs_c(pairs):
+    arr = (mgv_pref_pair * max(1, len(pairs)))()
+    for i, (w, l) in enumerate(pairs):
+        arr[i].winner, arr[i].loser = w.to_c(), l.to_c()
+    return arr
+
+
+def _labels_c(labels):
+    arr = (mgv_labeled_sample * max(1, len(labels)))()
+    for i, (rec, desirable) in enumerate(labels):
+        arr[i].sample, arr[i].desirable = rec.to_c(), int(bool(desirable))
+    return arr
+
+
+def dpo_from_errors(e_th_w, e_th_l, e_ref_w, e_ref_l, beta):
+    return _lib().mgv_dpo_from_errors(e_th_w, e_th_l, e_ref_w, e_ref_l, beta)
+
+
+def kto_from_rewards(rewards, desirable, w_d, w_u, z0=None):
+    r = _f64(rewards)
+    d = np.ascontiguousarray(desirable, dtype=np.uint8)
+    z = D(z0) if z0 is not None else None
+    out = D()
+    st = _lib().mgv_kto_from_rewards(len(r), r.ctypes.data, d.ctypes.data, w_d, w_u,
+                                     ctypes.byref(z) if z is not None else None, ctypes.byref(out))
+    if st != 0:
+        raise _EXC.get(st, MugvError)(st, "kto_from_rewards")
+    return out.value
+
+
+class PostTrainState:
+    """post::PostTrainState (posttrain.hpp:128-136): `policy` is trained, `ref` holds the frozen start weights."""
+
+    def __init__(self, policy: "Context", ref: "Context", lr: float = 1e-4, seed: int = 0):
+        self._L, self.policy, self.ref = _lib(), policy, ref
+        h = P()
+        st = self._L.mgv_post_state_create(policy.h, ref.h, lr, seed, ctypes.byref(h))
+        if st != 0:
+            policy._check(st)
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.mgv_post_state_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def plan_pos(self) -> int:
+        return self._L.mgv_post_plan_pos(self.h)
+
+    def train_step(self, cfg: PostTrainConfig, tag: str, pairs=(), labels=(), sft=(), sft_text=None, sft_fps=8.0):
+        """post_train_step: pairs = [(winner, loser) SampleRecords], labels = [(SampleRecord, desirable)],
+        sft = [FlowSample] sharing sft_text / sft_fps.  Returns dict(total, preference, sft, grad_norm)."""
+        c = cfg.to_c()
+        pc, lc = _pairs_c(list(pairs)), _labels_c(list(labels))
+        sc = (mgv_flow_sample * max(1, len(sft)))(*[s.to_c() for s in sft])
+        tx = _f64(sft_text) if sft_text is not None else None
+        m = mgv_post_metrics()
+        st = self._L.mgv_post_train_step(self.h, ctypes.byref(c), tag.encode(), len(pairs), pc, len(labels), lc,
+                                         len(sft), sc, tx.ctypes.data if tx is not None else None,
+                                         tx.shape[0] if tx is not None else 0, sft_fps, ctypes.byref(m))
+        if st != 0:
+            raise _EXC.get(st, MugvError)(st, self._L.mgv_post_last_error(self.h).decode())
+        return {"total": m.total, "preference": m.preference, "sft": m.sft, "grad_norm": m.grad_norm}
+
+
+def post_pref_loss(policy: "Context", ref: "Context", cfg: PostTrainConfig, tag: str, pairs=(), labels=(), seed=0):
+    """dpo_loss / kto_loss (posttrain.cpp:171-177, 224-233) with draws from Rng(seed)."""
+    c = cfg.to_c()
+    pc, lc = _pairs_c(list(pairs)), _labels_c(list(labels))
+    out = D()
+    policy._check(_lib().mgv_post_pref_loss(policy.h, ref.h, ctypes.byref(c), tag.encode(), len(pairs), pc,
+                                            len(labels), lc, seed, ctypes.byref(out)))
+    return out.value
+
+
+def _eval_c(recs):
+    """recs: [(FlowSample, text, fps)] -> ctypes array of mgv_eval_sample (keeps buffers alive on the array)."""
+    arr = (mgv_eval_sample * len(recs))()
+    keep = []
+    for i, (smp, text, fps) in enumerate(recs):
+        tx = _f64(text)
+        keep.append((smp, tx))
+        arr[i].s, arr[i].text, arr[i].L, arr[i].fps = smp.to_c(), tx.ctypes.data, tx.shape[0], fps
+    arr._keep = keep
+    return arr
+
+
 class Context:
     """One device, one precision ("fp32" parity mode or "bf16" tensor-core mode)."""
 
@@ -489,6 +681,28 @@ class Context:
             out["grads"] = dict(zip(self.names, g_arrs))
         if velocity:
             out["V"] = v_arrs
+        return out
+
+    def flow_errors(self, recs):
+        """mgv_flow_errors: post::flow_error of each (FlowSample, text, fps), forward only."""
+        arr = _eval_c(recs)
+        errs = np.empty(len(recs))
+        self._check(self._L.mgv_flow_errors(self.h, len(recs), arr, errs.ctypes.data))
+        return errs
+
+    def flow_step_weighted(self, recs, weights, grads=False):
+        """mgv_flow_step_weighted: one fwd+bwd of sum_k w_k l_k; returns dict(loss, errs, grad_norm[, grads])."""
+        arr = _eval_c(recs)
+        w = _f64(weights)
+        errs = np.empty(len(recs))
+        loss, gn = D(), D()
+        g_arrs = [np.empty(k) for k in self.numels] if grads else None
+        gp = (P * len(g_arrs))(*[a.ctypes.data for a in g_arrs]) if grads else None
+        self._check(self._L.mgv_flow_step_weighted(self.h, len(recs), arr, w.ctypes.data, errs.ctypes.data,
+                                                   ctypes.byref(loss), ctypes.byref(gn), gp))
+        out = {"loss": loss.value, "errs": errs, "grad_norm": gn.value}
+        if grads:
+            out["grads"] = dict(zip(self.names, g_arrs))
         return out
 
     def flow_step_device(self, samples_c, text_dev_ptr, L, fps=8.0):

@@ -10,48 +10,13 @@
 #include "kernels.h"
 #include "model.h"
 
-struct mgv_ctx {
-    std::unique_ptr<mgv::Model> model;
-    std::string err;
-};
+#include "capi_internal.h"
 
 namespace {
 template <class F>
 mgv_status guard(mgv_ctx* ctx, F&& f) {
     if (!ctx) return MGV_ERR_INPUT;
-    try {
-        f();
-        ctx->err.clear();
-        return MGV_OK;
-    } catch (const mgv::DimensionError& e) {
-        ctx->err = e.what();
-        return MGV_ERR_DIMENSION;
-    } catch (const mgv::ConfigError& e) {
-        ctx->err = e.what();
-        return MGV_ERR_CONFIG;
-    } catch (const mgv::InputError& e) {
-        ctx->err = e.what();
-        return MGV_ERR_INPUT;
-    } catch (const mgv::NumericError& e) {
-        ctx->err = e.what();
-        return MGV_ERR_NUMERIC;
-    } catch (const mgv::CudaError& e) {
-        ctx->err = e.what();
-        return MGV_ERR_CUDA;
-    } catch (const mgv::NcclError& e) {
-        ctx->err = e.what();
-        return MGV_ERR_NCCL;
-    } catch (const mgv::CheckpointError& e) {
-        ctx->err = e.what();
-        mgv::note_ckpt_error(e.what(), e.kind);
-        return MGV_ERR_CHECKPOINT;
-    } catch (const mgv::CkptInputError& e) {
-        ctx->err = e.what();
-        return MGV_ERR_INPUT;
-    } catch (const std::exception& e) {
-        ctx->err = e.what();
-        return MGV_ERR_INTERNAL;
-    }
+    return mgv::guard_into(ctx->err, std::forward<F>(f));
 }
 mgv::Cfg to_cfg(const mgv_dit_cfg* c) {
     mgv::Cfg g;

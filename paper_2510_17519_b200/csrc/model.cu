@@ -1033,9 +1033,13 @@ void Model::backward_sample(const void* dV) {
 }
 
 // ------------------------------------------------------------------ flow step
+static double wk_of(const StepExtra* ex, int64_t k, int64_t B) {
+    return ex && ex->weight ? ex->weight[k] : 1.0 / static_cast<double>(B);
+}
+
 template <class T>
 void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* text_dev, int64_t L, double fps,
-                           double* loss, double* grad_norm, double* const* v_dev) {
+                           double* loss, double* grad_norm, double* const* v_dev, const StepExtra* ex) {
     if (!have_params_) throw InputError("no parameters uploaded");
     if (n < 1) throw InputError("empty batch");  // flowtrain.cpp:258
     WS& w = *ws_;
@@ -1043,9 +1047,15 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
     const int64_t D = cfg_.D();
     int64_t maxN = 0;
     for (int64_t k = 0; k < n; ++k) maxN = std::max(maxN, samples[k].N);
+    const bool per_text = ex && ex->text_dev;
+    const bool backward = !ex || ex->backward;
+    if (ex && world_ > 1) throw ConfigError("weighted / forward-only steps run without data parallelism");
+    int64_t maxL = L;
+    if (per_text)
+        for (int64_t k = 0; k < n; ++k) maxL = std::max(maxL, ex->L[k]);
     // workspace (arena grows only; the layout is re-derived for this batch)
     w.N = maxN;
-    w.L = L;
+    w.L = maxL;
     w.n_u = 2;
     w.esz = bf16_ ? 2 : 4;
     w.grads = true;
@@ -1066,11 +1076,26 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
     prof_.begin_step();
     MGV_CUDA(cudaMemsetAsync(grad_buf_, 0, sizeof(float) * grad_numel_, s));
     MGV_CUDA(cudaMemsetAsync(w.scal, 0, sizeof(double) * 8, s));
-    convert_rows<T>(text_dev, L * cfg_.text_dim, tp<T>(w.text), s);
+    if (!per_text) convert_rows<T>(text_dev, L * cfg_.text_dim, tp<T>(w.text), s);
     const int64_t B_global = n * world_;
+    std::vector<double> errs_host(static_cast<size_t>(ex ? n : 0));
+    double* errs_dev = nullptr;  // l_k per sample (weighted / forward-only steps)
+    if (ex) {
+        MGV_CUDA(cudaMallocAsync(&errs_dev, sizeof(double) * n, s));
+        MGV_CUDA(cudaMemsetAsync(errs_dev, 0, sizeof(double) * n, s));
+    }
+    const double* prev_text = nullptr;
     for (int64_t k = 0; k < n; ++k) {
         const DevSample& sm = samples[k];
         w.N = sm.N;
+        if (per_text) {  // this record's text (converted once per distinct pointer)
+            w.L = ex->L[k];
+            if (ex->text_dev[k] != prev_text)
+                convert_rows<T>(ex->text_dev[k], ex->L[k] * cfg_.text_dim, tp<T>(w.text), s);
+            prev_text = ex->text_dev[k];
+        }
+        const double fps_k = ex && ex->fps ? ex->fps[k] : fps;
+        const double wk = ex && ex->weight ? ex->weight[k] : 1.0 / static_cast<double>(B_global);
         const int N = static_cast<int>(sm.N);
         MGV_CUDA(cudaMemcpyAsync(w.coords, sm.coords, sizeof(int32_t) * 3 * N, cudaMemcpyDeviceToDevice, s));
         // interpolate + condition mask (flowtrain.cpp:265-267); taus {t, 0} (dit.cpp:242 dedup)
@@ -1078,7 +1103,7 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
                             w.lmask, w.mod_id, s);
         w.n_u = sm.first_frame ? 2 : 1;
         set_taus(w.taus, sm.t, s);
-        forward_sample<T>(sm, w.rows, nullptr, w.n_u, w.mod_id, fps, true, true, nullptr);
+        forward_sample<T>(sm, w.rows, nullptr, w.n_u, w.mod_id, fps_k, true, true, nullptr);
         if (v_dev && v_dev[k]) {
             f32_to_f64<<<grid_of(N * D), 256, 0, s>>>(w.V, N * D, v_dev[k]);
             note_launch();
@@ -1087,9 +1112,31 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
         count_mask(w.lmask, N, w.cnt, s);
         flow_loss_fwd<T>(w.V, w.vt, w.lmask, N, int(D), w.loss_part, s);
         flow_loss_accumulate(w.loss_part, row_chunks(N), w.cnt, int(D), w.scal, s);  // scal[0] += l_b
-        flow_loss_bwd<T>(w.V, w.vt, w.lmask, N, int(D), static_cast<float>(2.0 / (double)B_global), w.cnt,
-                         tp<T>(w.dV), s);  // 2 (V - v*) / (B * n_b * D); all-masked -> 0
-        backward_sample<T>(w.dV);
+        if (ex) flow_loss_accumulate(w.loss_part, row_chunks(N), w.cnt, int(D), errs_dev + k, s);  // l_k alone
+        if (backward && wk != 0.0) {
+            flow_loss_bwd<T>(w.V, w.vt, w.lmask, N, int(D), static_cast<float>(2.0 * wk), w.cnt, tp<T>(w.dV),
+                             s);  // 2 w_k (V - v*) / (n_b * D), w_k = 1 / B in FlowTrainer::step; all-masked -> 0
+            backward_sample<T>(w.dV);
+        }
+    }
+    if (ex) {
+        MGV_CUDA(cudaMemcpyAsync(errs_host.data(), errs_dev, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+        MGV_CUDA(cudaFreeAsync(errs_dev, s));
+    }
+    if (!backward) {  // flow errors only
+        double host2 = 0.0;
+        MGV_CUDA(cudaStreamSynchronize(s));
+        last_launches_ = launch_count() - launches0;
+        prof_.end_step();
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        for (int64_t k = 0; k < n; ++k) {
+            ex->errs[k] = errs_host[static_cast<size_t>(k)];
+            host2 += (ex->weight ? ex->weight[k] : 1.0 / static_cast<double>(B_global)) * ex->errs[k];
+        }
+        *loss = host2;
+        if (grad_norm) *grad_norm = 0.0;
+        return;
     }
     tp_allreduce_grads(s);
     if (world_ > 1) {
@@ -1128,6 +1175,14 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     *loss = host[0] / static_cast<double>(B_global);  // flowtrain.cpp:273
+    if (ex) {  // weighted: Loss = sum_k w_k l_k
+        double tot = 0.0;
+        for (int64_t k = 0; k < n; ++k) {
+            if (ex->errs) ex->errs[k] = errs_host[static_cast<size_t>(k)];
+            tot += wk_of(ex, k, B_global) * errs_host[static_cast<size_t>(k)];
+        }
+        *loss = tot;
+    }
     if (!std::isfinite(*loss)) {  // flowtrain.cpp:276 (the device AdamW step was skipped)
         if (adam_.on) --adam_.step;
         throw NumericError("flow loss is not finite");
@@ -1136,12 +1191,12 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
 }
 
 void Model::flow_step_dev(int64_t n, const DevSample* samples, const double* text_dev, int64_t L, double fps,
-                          double* loss, double* grad_norm, double* const* v_dev) {
+                          double* loss, double* grad_norm, double* const* v_dev, const StepExtra* ex) {
     MGV_CUDA(cudaSetDevice(device_));
     if (bf16_)
-        flow_step_impl<__nv_bfloat16>(n, samples, text_dev, L, fps, loss, grad_norm, v_dev);
+        flow_step_impl<__nv_bfloat16>(n, samples, text_dev, L, fps, loss, grad_norm, v_dev, ex);
     else
-        flow_step_impl<float>(n, samples, text_dev, L, fps, loss, grad_norm, v_dev);
+        flow_step_impl<float>(n, samples, text_dev, L, fps, loss, grad_norm, v_dev, ex);
 }
 
 // host-buffer flow step: validate, stage to device, run, read back
@@ -1160,13 +1215,67 @@ static void validate_mask_host(const mgv_flow_sample& s, int64_t N) {  // flowtr
     }
 }
 
+// stage host samples on the device (validated as FlowTrainer::step / apply_condition_mask do)
+void Model::stage_samples(int64_t n, const mgv_flow_sample* samples, std::vector<DevSample>& ds,
+                          std::vector<void*>& allocs) {
+    const int64_t D = cfg_.D();
+    auto dalloc = [&](size_t bytes) {
+        void* p = nullptr;
+        MGV_CUDA(cudaMallocAsync(&p, bytes, stream_));
+        allocs.push_back(p);
+        return p;
+    };
+    ds.assign(static_cast<size_t>(n), DevSample{});
+    for (int64_t k = 0; k < n; ++k) {
+        const mgv_flow_sample& s = samples[k];
+        const int64_t N = s.dims[0] * s.dims[1] * s.dims[2];
+        if (N < 1) throw DimensionError("empty token grid");
+        if (!s.coords || !s.clean_rows || !s.noise) throw InputError("null sample buffer");
+        if (!(s.t >= 0.0 && s.t <= 1.0)) throw InputError("interpolation time outside [0, 1]");  // flowtrain.cpp:11
+        validate_mask_host(s, N);
+        bool cond_any = false;
+        if (s.conditioned)
+            for (int64_t i = 0; i < N && !cond_any; ++i) cond_any = s.conditioned[i] != 0;
+        DevSample d;
+        d.N = N;
+        std::memcpy(d.dims, s.dims, sizeof(d.dims));
+        auto* c = static_cast<int32_t*>(dalloc(sizeof(int32_t) * 3 * N));
+        MGV_CUDA(cudaMemcpyAsync(c, s.coords, sizeof(int32_t) * 3 * N, cudaMemcpyHostToDevice, stream_));
+        auto* cl = static_cast<double*>(dalloc(sizeof(double) * N * D));
+        auto* nz = static_cast<double*>(dalloc(sizeof(double) * N * D));
+        MGV_CUDA(cudaMemcpyAsync(cl, s.clean_rows, sizeof(double) * N * D, cudaMemcpyHostToDevice, stream_));
+        MGV_CUDA(cudaMemcpyAsync(nz, s.noise, sizeof(double) * N * D, cudaMemcpyHostToDevice, stream_));
+        d.coords = c;
+        d.clean = cl;
+        d.noise = nz;
+        d.t = s.t;
+        if (cond_any) {
+            // the device prep marks unit-0 rows; general masks are validated unit-aligned above and we
+            // require them to be exactly the first unit (first_frame_mask), the only producer in the reference
+            for (int64_t i = 0; i < N; ++i)
+                if ((s.conditioned[i] != 0) != (s.coords[3 * i] == 0))
+                    throw InputError("only first-frame conditioning masks are supported on device");
+            if (s.condition_latents && s.condition_latents != s.clean_rows) {
+                // conditioned rows take condition_latents (flowtrain.cpp:95): stage them as those rows of the
+                // clean input; the interpolation target there is masked out of the loss, so this is exact
+                for (int64_t i = 0; i < N; ++i)
+                    if (s.conditioned[i])
+                        MGV_CUDA(cudaMemcpyAsync(cl + i * D, s.condition_latents + i * D, sizeof(double) * D,
+                                                 cudaMemcpyHostToDevice, stream_));
+            }
+            d.first_frame = 1;
+        }
+        ds[static_cast<size_t>(k)] = d;
+    }
+}
+
 void Model::flow_step(int64_t n, const mgv_flow_sample* samples, const double* text, int64_t L, double fps,
                       double* loss, double* grad_norm, double* const* grads_out, double* const* v_out) {
     MGV_CUDA(cudaSetDevice(device_));
     if (n < 1) throw InputError("empty batch");
     if (L < 1 || L > 1 << 20) throw DimensionError("text embeddings must be (L, text_dim)");
     const int64_t D = cfg_.D();
-    std::vector<DevSample> ds(n);
+    std::vector<DevSample> ds;
     std::vector<void*> allocs;
     auto dalloc = [&](size_t bytes) {
         void* p = nullptr;
@@ -1175,41 +1284,7 @@ void Model::flow_step(int64_t n, const mgv_flow_sample* samples, const double* t
         return p;
     };
     try {
-        for (int64_t k = 0; k < n; ++k) {
-            const mgv_flow_sample& s = samples[k];
-            const int64_t N = s.dims[0] * s.dims[1] * s.dims[2];
-            if (N < 1) throw DimensionError("empty token grid");
-            if (!(s.t >= 0.0 && s.t <= 1.0)) throw InputError("interpolation time outside [0, 1]");  // flowtrain.cpp:11
-            validate_mask_host(s, N);
-            bool cond_any = false;
-            if (s.conditioned)
-                for (int64_t i = 0; i < N && !cond_any; ++i) cond_any = s.conditioned[i] != 0;
-            DevSample d;
-            d.N = N;
-            std::memcpy(d.dims, s.dims, sizeof(d.dims));
-            auto* c = static_cast<int32_t*>(dalloc(sizeof(int32_t) * 3 * N));
-            MGV_CUDA(cudaMemcpyAsync(c, s.coords, sizeof(int32_t) * 3 * N, cudaMemcpyHostToDevice, stream_));
-            auto* cl = static_cast<double*>(dalloc(sizeof(double) * N * D));
-            auto* nz = static_cast<double*>(dalloc(sizeof(double) * N * D));
-            // the conditioned rows carry condition_latents (default: clean rows, first_frame_mask)
-            MGV_CUDA(cudaMemcpyAsync(cl, s.clean_rows, sizeof(double) * N * D, cudaMemcpyHostToDevice, stream_));
-            MGV_CUDA(cudaMemcpyAsync(nz, s.noise, sizeof(double) * N * D, cudaMemcpyHostToDevice, stream_));
-            d.coords = c;
-            d.clean = cl;
-            d.noise = nz;
-            d.t = s.t;
-            if (cond_any) {
-                // the device prep marks unit-0 rows; general masks are validated unit-aligned above and we
-                // require them to be exactly the first unit (first_frame_mask), the only producer in the reference
-                for (int64_t i = 0; i < N; ++i)
-                    if ((s.conditioned[i] != 0) != (s.coords[3 * i] == 0))
-                        throw InputError("only first-frame conditioning masks are supported on device");
-                if (s.condition_latents && s.condition_latents != s.clean_rows)
-                    throw InputError("condition_latents must be the clean rows (first_frame_mask)");
-                d.first_frame = 1;
-            }
-            ds[k] = d;
-        }
+        stage_samples(n, samples, ds, allocs);
         auto* tx = static_cast<double*>(dalloc(sizeof(double) * L * cfg_.text_dim));
         MGV_CUDA(cudaMemcpyAsync(tx, text, sizeof(double) * L * cfg_.text_dim, cudaMemcpyHostToDevice, stream_));
         std::vector<double*> vdev(n, nullptr);
@@ -1222,25 +1297,93 @@ void Model::flow_step(int64_t n, const mgv_flow_sample* samples, const double* t
                 if (v_out[k])
                     MGV_CUDA(cudaMemcpyAsync(v_out[k], vdev[k], sizeof(double) * ds[k].N * D, cudaMemcpyDeviceToHost,
                                              stream_));
-        if (grads_out) {
-            int64_t maxn = 0;
-            for (auto* p : sorted_) maxn = std::max(maxn, p->numel);
-            auto* gd = static_cast<double*>(dalloc(sizeof(double) * maxn));
-            float* gp = tp_ > 1 ? static_cast<float*>(dalloc(sizeof(float) * maxn)) : nullptr;
-            for (size_t k = 0; k < sorted_.size(); ++k) {
-                if (!grads_out[k]) continue;
-                const float* gsrc = sorted_[k]->grad;
-                if (const int C = tp_ > 1 ? tp_row_chunks(sorted_[k]->name) : 0) {  // back to the reference row order
-                    permute_shard_rows(gsrc, gp, C, static_cast<int>(cfg_.hidden), tp_,
-                                       sorted_[k]->numel / (C * cfg_.hidden), 1, stream_);
-                    gsrc = gp;
-                }
-                f32_to_f64<<<grid_of(sorted_[k]->numel), 256, 0, stream_>>>(gsrc, sorted_[k]->numel, gd); ::mgv::note_launch();
-                MGV_CUDA(cudaMemcpyAsync(grads_out[k], gd, sizeof(double) * sorted_[k]->numel, cudaMemcpyDeviceToHost,
-                                         stream_));
-                MGV_CUDA(cudaStreamSynchronize(stream_));
-            }
+        if (grads_out) download_grads(grads_out, dalloc);
+        MGV_CUDA(cudaStreamSynchronize(stream_));
+    } catch (...) {
+        for (void* p : allocs) cudaFreeAsync(p, stream_);
+        throw;
+    }
+    for (void* p : allocs) cudaFreeAsync(p, stream_);
+}
+
+template <class Alloc>
+void Model::download_grads(double* const* grads_out, Alloc&& dalloc) {
+    int64_t maxn = 0;
+    for (auto* p : sorted_) maxn = std::max(maxn, p->numel);
+    auto* gd = static_cast<double*>(dalloc(sizeof(double) * maxn));
+    float* gp = tp_ > 1 ? static_cast<float*>(dalloc(sizeof(float) * maxn)) : nullptr;
+    for (size_t k = 0; k < sorted_.size(); ++k) {
+        if (!grads_out[k]) continue;
+        const float* gsrc = sorted_[k]->grad;
+        if (const int C = tp_ > 1 ? tp_row_chunks(sorted_[k]->name) : 0) {  // back to the reference row order
+            permute_shard_rows(gsrc, gp, C, static_cast<int>(cfg_.hidden), tp_, sorted_[k]->numel / (C * cfg_.hidden),
+                               1, stream_);
+            gsrc = gp;
         }
+        f32_to_f64<<<grid_of(sorted_[k]->numel), 256, 0, stream_>>>(gsrc, sorted_[k]->numel, gd);
+        ::mgv::note_launch();
+        MGV_CUDA(cudaMemcpyAsync(grads_out[k], gd, sizeof(double) * sorted_[k]->numel, cudaMemcpyDeviceToHost,
+                                 stream_));
+        MGV_CUDA(cudaStreamSynchronize(stream_));
+    }
+}
+
+void Model::eval_records(int64_t n, const mgv_eval_sample* recs, const double* weights, double* errs, double* loss,
+                         double* grad_norm, double* const* grads_out) {
+    MGV_CUDA(cudaSetDevice(device_));
+    if (n < 1) throw InputError("empty batch");
+    if (!recs || !errs || !loss) throw InputError("null argument");
+    std::vector<mgv_flow_sample> fs(static_cast<size_t>(n));
+    for (int64_t k = 0; k < n; ++k) {
+        if (!recs[k].text || recs[k].L < 1 || recs[k].L > 1 << 20)
+            throw DimensionError("text embeddings must be (L, text_dim)");
+        fs[static_cast<size_t>(k)] = recs[k].s;
+    }
+    std::vector<DevSample> ds;
+    std::vector<void*> allocs;
+    auto dalloc = [&](size_t bytes) {
+        void* p = nullptr;
+        MGV_CUDA(cudaMallocAsync(&p, bytes, stream_));
+        allocs.push_back(p);
+        return p;
+    };
+    try {
+        stage_samples(n, fs.data(), ds, allocs);
+        std::vector<const double*> tdev(static_cast<size_t>(n));
+        std::vector<int64_t> Ls(static_cast<size_t>(n));
+        std::vector<double> fpss(static_cast<size_t>(n));
+        for (int64_t k = 0; k < n; ++k) {  // one device copy per distinct host text
+            int64_t same = -1;
+            for (int64_t j = 0; j < k && same < 0; ++j)
+                if (recs[j].text == recs[k].text && recs[j].L == recs[k].L) same = j;
+            if (same >= 0) {
+                tdev[static_cast<size_t>(k)] = tdev[static_cast<size_t>(same)];
+            } else {
+                auto* tx = static_cast<double*>(dalloc(sizeof(double) * recs[k].L * cfg_.text_dim));
+                MGV_CUDA(cudaMemcpyAsync(tx, recs[k].text, sizeof(double) * recs[k].L * cfg_.text_dim,
+                                         cudaMemcpyHostToDevice, stream_));
+                tdev[static_cast<size_t>(k)] = tx;
+            }
+            Ls[static_cast<size_t>(k)] = recs[k].L;
+            fpss[static_cast<size_t>(k)] = recs[k].fps;
+        }
+        StepExtra ex;
+        ex.text_dev = tdev.data();
+        ex.L = Ls.data();
+        ex.fps = fpss.data();
+        ex.backward = weights != nullptr;
+        std::vector<double> ones;
+        if (weights) {
+            ex.weight = weights;
+        } else {
+            ones.assign(static_cast<size_t>(n), 1.0);
+            ex.weight = ones.data();
+        }
+        ex.errs = errs;
+        double gn = 0.0;
+        flow_step_dev(n, ds.data(), tdev[0], Ls[0], fpss[0], loss, &gn, nullptr, &ex);
+        if (grad_norm) *grad_norm = gn;
+        if (weights && grads_out) download_grads(grads_out, dalloc);
         MGV_CUDA(cudaStreamSynchronize(stream_));
     } catch (...) {
         for (void* p : allocs) cudaFreeAsync(p, stream_);

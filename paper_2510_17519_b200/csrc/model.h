@@ -53,6 +53,17 @@ struct DevSample {
     int first_frame = 0;  // first_frame_mask conditioning (flowtrain.cpp:50-59)
 };
 
+// Per-sample overrides of a flow step (post-training, posttrain.cpp:126-233): every sample may carry its own
+// text and fps and a loss weight, and the step may be forward-only (flow errors, no gradients).
+struct StepExtra {
+    const double* const* text_dev = nullptr;  // per-sample device text (L[k] x text_dim); null: the step's text
+    const int64_t* L = nullptr;
+    const double* fps = nullptr;
+    const double* weight = nullptr;  // dLoss/d l_k; null: 1 / global batch (FlowTrainer::step)
+    bool backward = true;            // false: forward only, no gradients, no optimizer update
+    double* errs = nullptr;          // host out: each sample's masked flow loss l_k (flowtrain.cpp:22-38)
+};
+
 class Arena {
 public:
     ~Arena();
@@ -140,20 +151,31 @@ public:
                      int direction, double fps, double* out);
     void flow_step(int64_t n, const mgv_flow_sample* samples, const double* text, int64_t L, double fps,
                    double* loss, double* grad_norm, double* const* grads_out, double* const* v_out);
+    // Post-training evaluations (posttrain.cpp:126-142): per-record text / fps; errs[k] = l_k.  weights null:
+    // forward only (flow_error); else one fwd+bwd with Loss = sum_k w_k l_k, grads = sum_k w_k dl_k (then
+    // grad_norm and, when enabled, AdamW), loss = sum_k w_k l_k.
+    void eval_records(int64_t n, const mgv_eval_sample* recs, const double* weights, double* errs, double* loss,
+                      double* grad_norm, double* const* grads_out);
     // Device-resident inputs (benchmark `value` path): no host<->device traffic except the two scalars.
     void flow_step_dev(int64_t n, const DevSample* samples, const double* text_dev, int64_t L, double fps,
-                       double* loss, double* grad_norm, double* const* v_dev = nullptr);
+                       double* loss, double* grad_norm, double* const* v_dev = nullptr,
+                       const StepExtra* ex = nullptr);
 
     double last_step_ms() const { return last_ms_; }
     int64_t last_step_launches() const { return last_launches_; }
     Prof& prof() { return prof_; }
     bool bf16() const { return bf16_; }
+    int64_t D() const { return cfg_.D(); }
     cudaStream_t stream() const { return stream_; }
 
 private:
     template <class T>
     void flow_step_impl(int64_t n, const DevSample* samples, const double* text_dev, int64_t L, double fps,
-                        double* loss, double* grad_norm, double* const* v_dev);
+                        double* loss, double* grad_norm, double* const* v_dev, const StepExtra* ex);
+    void stage_samples(int64_t n, const mgv_flow_sample* samples, std::vector<DevSample>& ds,
+                       std::vector<void*>& allocs);
+    template <class Alloc>
+    void download_grads(double* const* grads_out, Alloc&& dalloc);
     template <class T>
     void forward_sample(const DevSample& s, const void* rows_in /*T*/, const double* tau_host_unique, int n_u,
                         const int32_t* mod_id, double fps, bool grads, bool head, void* out);
