@@ -683,6 +683,26 @@ class Context:
             out["V"] = v_arrs
         return out
 
+    def latent_rows(self, grid):
+        """mgv_latent_rows (dit::latent_rows): (U, h, w, C) grid -> (N, 4C) rows and (N, 3) coords."""
+        g = _f64(grid)
+        U, h, w, C = g.shape
+        N = U * (h // 2) * (w // 2)
+        rows = np.empty((N, 4 * C))
+        coords = np.empty((N, 3), dtype=np.int32)
+        self._check(self._L.mgv_latent_rows(self.h, g.ctypes.data, U, h, w, C, rows.ctypes.data, coords.ctypes.data))
+        return rows, coords
+
+    def rows_to_grid(self, rows, coords, dims, C):
+        """mgv_rows_to_grid (dit::rows_to_grid): rows on coords of a (U, H', W') token grid -> (U, 2H', 2W', C)."""
+        r = _f64(rows)
+        co = np.ascontiguousarray(coords, dtype=np.int32)
+        dm = (I64 * 3)(*[int(x) for x in dims])
+        out = np.empty((int(dims[0]), 2 * int(dims[1]), 2 * int(dims[2]), int(C)))
+        self._check(self._L.mgv_rows_to_grid(self.h, r.ctypes.data, co.ctypes.data, r.shape[0], dm, int(C),
+                                             out.ctypes.data))
+        return out
+
     def flow_errors(self, recs):
         """mgv_flow_errors: post::flow_error of each (FlowSample, text, fps), forward only."""
         arr = _eval_c(recs)

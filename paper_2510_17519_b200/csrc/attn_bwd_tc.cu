@@ -29,6 +29,8 @@ namespace mgv {
 // cross-SM handoffs (P^T out, dS^T back) put ~3600 clk of exchange latency on every step; kept selectable
 // (mgv_dev_set_dkv_pair) as the starting point for a deeper-pipelined exchange.
 static int g_dkv_pair = 0;
+// 0 = v8 (default: V in TMEM, P^T in its own columns), 1 = v5 (K in TMEM, P^T / dS^T aliased)
+static int g_dkv_variant = 0;
 
 namespace {
 
@@ -45,7 +47,14 @@ __device__ unsigned long long g_attn_trace2[8][64];
     do {                                                                                             \
         if ((blockIdx.x >> 1) == 7 && blockIdx.y == 0 && (j) < 64) g_attn_trace2[ev][j] = clock64(); \
     } while (0)
+#define ATR8(ev, j)                                                                             \
+    do {                                                                                        \
+        if (blockIdx.x == 7 && blockIdx.y == 0 && (j) < 64) g_attn_trace2[ev][j] = clock64();  \
+    } while (0)
 #else
+#define ATR8(ev, j) \
+    do {            \
+    } while (0)
 #define ATR2(ev, j) \
     do {            \
     } while (0)
@@ -393,6 +402,242 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_tc_kernel(const __grid_co
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(ds_full);
+        }
+        if (nq > 0) mbar_wait(acc_done, 0);
+        tc_fence_after();
+        const bool valid = kvv && nq > 0;
+        if (part) {  // fp32 partial rows of this query split: [dV | dK]
+            const int64_t W = (int64_t)f.heads * HD;
+            float* prow = part + ((int64_t)blockIdx.z * f.Nk + (kvv ? kv : 0)) * 2 * W + (hf ? W : 0) + col;
+            store_acc_row_f32<HD>(tmem + lane_base + (hf ? DK_COL : DV_COL), prow, kvv);
+        } else if (hf == 0) {
+            store_acc_row<HD>(tmem + lane_base + DV_COL,
+                              static_cast<__nv_bfloat16*>(p.dv) + (int64_t)kv * p.dv_ld + col, valid);
+        } else {
+            store_acc_row<HD>(tmem + lane_base + DK_COL,
+                              static_cast<__nv_bfloat16*>(p.dk) + (int64_t)kv * p.dk_ld + col, valid);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// =====================================================================================  dK / dV (v8)
+// The default dK/dV pass.  Against v5 above it moves V (not K) into TMEM and gives P^T its own columns:
+//   S^T  = K Q^T     SS (K row tile in shared memory)         -> free-running: S^T(i+1) is issued as soon as
+//                                                                the compute warps have loaded S^T(i)
+//   dP^T = V dO^T    TS (V columns [0,128) in TMEM, the 16-column tail of head_dim 144 one SS k-step)
+//   dV  += P^T dO    TS (P^T in its own 32 columns)
+//   dK  += dS^T Q    TS (dS^T written over the consumed dP^T columns)
+// so neither dependency loop (S^T -> softmax -> dV, dP^T -> dS -> dK -> dP^T) waits on the other product's
+// overwrite, and the one shared-memory-operand product is the one whose loop has slack.  Staging only 128
+// of V's 144 columns in TMEM is what makes the 512-column budget close:
+//   S^T [0,64)  P^T [64,96)  dP^T|dS^T [96,160)  dV [160,160+HD)  dK [.., +HD)  V (bf16 pairs) [.., +64)
+template <int HD>
+__global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v8_kernel(const __grid_constant__ BwdMaps tm, AttnBwdProblem p,
+                                                                 float* part) {
+    constexpr int BKV = 128, BQ = 64, NST = 5;
+    using T = BT<HD>;
+    constexpr int VA = HD >= 128 ? 128 : HD;  // V columns staged in TMEM
+    constexpr int VT = HD - VA;               // tail columns read from shared memory
+    static_assert(VT == 0 || VT == 16, "head_dim tail must be one 16-column k-step");
+    constexpr int HDP = ((HD + 15) / 16) * 16;
+    constexpr int S_COL = 0, P_COL = 64, DP_COL = 96, DV_COL = 160, DK_COL = DV_COL + HDP, VA_COL = DK_COL + HDP;
+    static_assert(VA_COL + VA / 2 <= 512, "TMEM budget");
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sK = smem;
+    uint8_t* sVt = sK + T::ROW_TILE;                       // 128 x 16 SW32 tail of V (HD = 144)
+    uint8_t* sQt = sVt + (VT ? 4096 : 0);                  // [NST]
+    uint8_t* sdOt = sQt + NST * T::T_TILE;                 // [NST]
+    float* sLse = reinterpret_cast<float*>(sdOt + NST * T::T_TILE);  // [NST][64]
+    float* sD = sLse + NST * BQ;                                      // [NST][64]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sD + NST * BQ);
+    uint64_t* k_full = bars;
+    uint64_t* qd_full = bars + 1;         // [NST]
+    uint64_t* qd_empty = bars + 1 + NST;  // [NST]
+    uint64_t* s_full = bars + 1 + 2 * NST;
+    uint64_t* s_empty = s_full + 1;
+    uint64_t* p_full = s_full + 2;
+    uint64_t* pv_done = s_full + 3;
+    uint64_t* dp_full = s_full + 4;
+    uint64_t* ds_full = s_full + 5;
+    uint64_t* acc_done = s_full + 6;
+    uint64_t* va_ready = s_full + 7;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 8);
+
+    const AttnProblem& f = p.f;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int h = blockIdx.y, k0 = blockIdx.x * BKV;
+    const int nq_all = (f.Nq + BQ - 1) / BQ;
+    const int i0 = static_cast<int>((int64_t)blockIdx.z * nq_all / gridDim.z);
+    const int nq = static_cast<int>((int64_t)(blockIdx.z + 1) * nq_all / gridDim.z) - i0;  // this split's tiles
+    const int col = h * HD;
+
+    if (threadIdx.x == 0) {
+        mbar_init(k_full, 1);
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&qd_full[i], 1);
+            mbar_init(&qd_empty[i], 1);
+        }
+        mbar_init(s_full, 1);
+        mbar_init(s_empty, 8);
+        mbar_init(p_full, 8);
+        mbar_init(pv_done, 1);
+        mbar_init(dp_full, 1);
+        mbar_init(ds_full, 8);
+        mbar_init(acc_done, 1);
+        mbar_init(va_ready, 4);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            mbar_arrive_expect_tx(k_full, T::ROW_TILE + (VT ? 4096 : 0));
+            load_row_tile<HD>(sK, &tm.a128, &tm.a32, k_full, col, k0);
+            if (VT) tma_load_2d(sVt, &tm.b32, k_full, col + VA, k0);
+            for (int i = 0; i < nq; ++i) {
+                const int st = i % NST;
+                if (i >= NST) mbar_wait(&qd_empty[st], ((i / NST) - 1) & 1);
+                mbar_arrive_expect_tx(&qd_full[st], 2 * T::T_TILE + 2 * BQ * 4);
+                const int qt = (i0 + i) * BQ;
+                tma_load_2d(sQt + st * T::T_TILE, &tm.ta, &qd_full[st], qt, col);
+                tma_load_2d(sdOt + st * T::T_TILE, &tm.tb, &qd_full[st], qt, col);
+                bulk_load(sLse + st * BQ, f.lse + (int64_t)h * lse_stride(f) + qt, BQ * 4, &qd_full[st]);
+                bulk_load(sD + st * BQ, p.Dvec + (int64_t)h * lse_stride(f) + qt, BQ * 4, &qd_full[st]);
+            }
+        }
+    } else if (warp == 1) {
+        const uint32_t aK = smem_u32(sK);
+        auto issue_s = [&](int i) {  // S^T(i) = K Q^T(i)
+            if (elect_one()) {
+                mma_rows_x_t<HD>(tmem + S_COL, aK, smem_u32(sQt + (i % NST) * T::T_TILE));
+                umma_commit(s_full);
+            }
+            __syncwarp();
+        };
+        auto issue_dp = [&](int i) {  // dP^T(i) = V dO^T(i): VA/16 TS k-steps + the SS tail
+            if (elect_one()) {
+                constexpr uint32_t id = idesc_bf16_f32(128, 64, false, true);
+                const uint32_t bt = smem_u32(sdOt + (i % NST) * T::T_TILE);
+#pragma unroll
+                for (int kk = 0; kk < VA / 16; ++kk)
+                    umma_f16_ts(tmem + DP_COL, tmem + VA_COL + kk * 8, smem_desc(bt + kk * 2048, 16, 1024, kSwizzle128),
+                                id, kk > 0 ? 1u : 0u);
+                if (VT)
+                    umma_f16_ss(tmem + DP_COL, smem_desc(smem_u32(sVt), 16, 256, kSwizzle32),
+                                smem_desc(bt + (VA / 16) * 2048, 16, 1024, kSwizzle128), id, 1u);
+                umma_commit(dp_full);
+            }
+            __syncwarp();
+        };
+        mbar_wait(va_ready, 0);
+        mbar_wait(k_full, 0);
+        if (nq > 0) {
+            mbar_wait(&qd_full[0], 0);
+            tc_fence_after();
+            issue_s(0);
+            issue_dp(0);
+        }
+        // per step i:  S^T(i+1) [S^T(i) loaded] -> dV(i) [P^T(i)] -> dK(i) [dS^T(i)] -> dP^T(i+1) [after dK(i)]
+        for (int i = 0; i < nq; ++i) {
+            const int st = i % NST;
+            if (i + 1 < nq) {
+                mbar_wait(s_empty, i & 1);
+                mbar_wait(&qd_full[(i + 1) % NST], ((i + 1) / NST) & 1);
+                tc_fence_after();
+                issue_s(i + 1);
+                if (lane == 0) ATR8(0, i);
+            }
+            mbar_wait(p_full, i & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                mma_tmem_x_t<HD>(tmem + DV_COL, tmem + P_COL, smem_u32(sdOt + st * T::T_TILE), i > 0);
+                umma_commit(pv_done);
+            }
+            __syncwarp();
+            if (lane == 0) ATR8(1, i);
+            mbar_wait(ds_full, i & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                mma_tmem_split_x_t<HD, 32>(tmem + DK_COL, tmem + DP_COL, smem_u32(sQt + st * T::T_TILE), i > 0);
+                umma_commit(&qd_empty[st]);
+                if (i == nq - 1) umma_commit(acc_done);
+            }
+            __syncwarp();
+            if (lane == 0) ATR8(2, i);
+            if (i + 1 < nq) issue_dp(i + 1);  // overwrites dS^T(i): behind dK(i) in the tensor pipe
+        }
+    } else if (warp >= 4) {
+        // two warps per TMEM lane group: warp hf handles query columns [32 hf, 32 hf + 32) of each tile
+        const int g = warp & 3, hf = (warp - 4) >> 2, row = g * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(g * 32) << 16;
+        const int kv = k0 + row;
+        const bool kvv = kv < f.Nk;
+        if (hf == 0) {
+            row_to_tmem<VA>(tmem + lane_base + VA_COL,
+                            static_cast<const __nv_bfloat16*>(f.v) + (int64_t)(kvv ? kv : 0) * f.v_ld + col, kvv);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(va_ready);
+        }
+        constexpr int HQ = BQ / 2;
+        for (int i = 0; i < nq; ++i) {
+            const int st = i % NST;
+            mbar_wait(&qd_full[st], (i / NST) & 1);  // lse / D rows of this tile have landed
+            mbar_wait(s_full, i & 1);
+            tc_fence_after();
+            if (warp == 4 && lane == 0) ATR8(3, i);
+            float s[HQ], dp[HQ];
+            tmem_ld32(tmem + lane_base + S_COL + hf * HQ, reinterpret_cast<uint32_t*>(s));
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(s_empty);  // the MMA warp may issue S^T(i+1) over it
+            const float* lse2 = sLse + st * BQ + hf * HQ;
+            const float* Dq = sD + st * BQ + hf * HQ;
+            const int qb = (i0 + i) * BQ + hf * HQ;
+            const bool full = qb + HQ <= f.Nq;
+            uint32_t pk[HQ / 2];
+#pragma unroll
+            for (int c = 0; c < HQ; c += 2) {
+                const bool v0 = full || qb + c < f.Nq, v1 = full || qb + c + 1 < f.Nq;
+                s[c] = v0 ? ex2f((s[c] - lse2[c]) * kLog2e) : 0.0f;  // lse rows are natural-log
+                s[c + 1] = v1 ? ex2f((s[c + 1] - lse2[c + 1]) * kLog2e) : 0.0f;
+                pk[c / 2] = pack_bf16(s[c], s[c + 1]);
+            }
+            if (i >= 1) {
+                mbar_wait(pv_done, (i - 1) & 1);  // dV(i-1) has read P^T(i-1)
+                tc_fence_after();
+            }
+            tmem_st16(tmem + lane_base + P_COL + hf * (HQ / 2), pk);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(p_full);
+            if (warp == 4 && lane == 0) ATR8(4, i);
+            mbar_wait(dp_full, i & 1);
+            tc_fence_after();
+            if (warp == 4 && lane == 0) ATR8(5, i);
+            tmem_ld32(tmem + lane_base + DP_COL + hf * HQ, reinterpret_cast<uint32_t*>(dp));
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < HQ; c += 2)
+                pk[c / 2] = pack_bf16(s[c] * (dp[c] - Dq[c]), s[c + 1] * (dp[c + 1] - Dq[c + 1]));  // autodiff.cpp:820
+            tmem_st16(tmem + lane_base + DP_COL + hf * HQ, pk);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(ds_full);
+            if (warp == 4 && lane == 0) ATR8(6, i);
         }
         if (nq > 0) mbar_wait(acc_done, 0);
         tc_fence_after();
@@ -960,12 +1205,17 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
             throw std::runtime_error("attn_bwd_tc: k must be 16-byte aligned with ld % 8 == 0");
         make_tmap_sw(&m.b128, f.v, W, f.Nk, f.v_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
         make_tmap_sw(&m.b32, f.v, W, f.Nk, f.v_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
+        make_tmap_sw(&m.a128, f.k, W, f.Nk, f.k_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+        make_tmap_sw(&m.a32, f.k, W, f.Nk, f.k_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
         make_tmap_sw(&m.ta, qt, f.Nq, W, qt_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
         make_tmap_sw(&m.tb, dot, f.Nq, W, dot_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
         const int smem = T::ROW_TILE + 10 * T::T_TILE + 10 * 64 * 4 + 256 + 1024;
+        const int smem8 = smem + (HD > 128 ? 4096 : 0);
         static bool set = false;
         if (!set) {
             MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_v8_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          smem8));
             set = true;
         }
         // few key tiles (cross-attention): split the query range so the grid still covers the SMs
@@ -996,7 +1246,10 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
             cfg.numAttrs = 1;
             MGV_CUDA(cudaLaunchKernelEx(&cfg, attn_bwd_dkv_pair_kernel<HD>, m, p));
         } else {
-            attn_bwd_dkv_tc_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem, s>>>(m, p, part);
+            if (g_dkv_variant == 1)
+                attn_bwd_dkv_tc_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem, s>>>(m, p, part);
+            else
+                attn_bwd_dkv_v8_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem8, s>>>(m, p, part);
         }
         ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
@@ -1085,6 +1338,10 @@ extern "C" int mgv_dev_attn_trace2(unsigned long long* out) {
 
 extern "C" int mgv_dev_set_dkv_pair(int on) {
     mgv::g_dkv_pair = on ? 1 : 0;
+    return 0;
+}
+extern "C" int mgv_dev_set_dkv_variant(int v) {
+    mgv::g_dkv_variant = v;
     return 0;
 }
 

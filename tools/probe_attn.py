@@ -9,6 +9,9 @@ sys.path.insert(0, ".")
 from paper_2510_17519_b200._lib import lib  # noqa: E402
 
 L = lib()
+import os  # noqa: E402
+if os.environ.get("MGV_DKV_VARIANT"):  # 0 = v8 (default), 1 = v5
+    L.mgv_dev_set_dkv_variant(int(os.environ["MGV_DKV_VARIANT"]))
 P = ctypes.c_void_p
 i64 = ctypes.c_int64
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 57600
