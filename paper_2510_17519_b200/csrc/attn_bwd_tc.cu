@@ -31,6 +31,8 @@ namespace mgv {
 static int g_dkv_pair = 0;
 // 0 = v8 (default: V in TMEM, P^T in its own columns), 1 = v5 (K in TMEM, P^T / dS^T aliased)
 static int g_dkv_variant = 0;
+// timing experiments only (tools/): bit 0 = compute warps skip TMEM traffic and math, bit 1 = no Q^T/dO^T TMA
+__device__ int g_attn_dbg = 0;
 
 namespace {
 
@@ -51,7 +53,14 @@ __device__ unsigned long long g_attn_trace2[8][64];
     do {                                                                                        \
         if (blockIdx.x == 7 && blockIdx.y == 0 && (j) < 64) g_attn_trace2[ev][j] = clock64();  \
     } while (0)
+#define ATR9(ev, j)                                                                             \
+    do {                                                                                        \
+        if (blockIdx.x == 6 && blockIdx.y == 0 && (j) < 64) g_attn_trace2[ev][j] = clock64();  \
+    } while (0)
 #else
+#define ATR9(ev, j) \
+    do {            \
+    } while (0)
 #define ATR8(ev, j) \
     do {            \
     } while (0)
@@ -506,6 +515,10 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v8_kernel(const __grid_co
             for (int i = 0; i < nq; ++i) {
                 const int st = i % NST;
                 if (i >= NST) mbar_wait(&qd_empty[st], ((i / NST) - 1) & 1);
+                if ((g_attn_dbg & 2) && i >= NST) {  // timing experiment: reuse the resident tiles, no TMA
+                    mbar_arrive(&qd_full[st]);
+                    continue;
+                }
                 mbar_arrive_expect_tx(&qd_full[st], 2 * T::T_TILE + 2 * BQ * 4);
                 const int qt = (i0 + i) * BQ;
                 tma_load_2d(sQt + st * T::T_TILE, &tm.ta, &qd_full[st], qt, col);
@@ -549,31 +562,35 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v8_kernel(const __grid_co
         // per step i:  S^T(i+1) [S^T(i) loaded] -> dV(i) [P^T(i)] -> dK(i) [dS^T(i)] -> dP^T(i+1) [after dK(i)]
         for (int i = 0; i < nq; ++i) {
             const int st = i % NST;
+            if (lane == 0) ATR8(0, i);
             if (i + 1 < nq) {
                 mbar_wait(s_empty, i & 1);
                 mbar_wait(&qd_full[(i + 1) % NST], ((i + 1) / NST) & 1);
                 tc_fence_after();
                 issue_s(i + 1);
-                if (lane == 0) ATR8(0, i);
             }
+            if (lane == 0) ATR8(1, i);
             mbar_wait(p_full, i & 1);
             tc_fence_after();
+            if (lane == 0) ATR8(2, i);
             if (elect_one()) {
                 mma_tmem_x_t<HD>(tmem + DV_COL, tmem + P_COL, smem_u32(sdOt + st * T::T_TILE), i > 0);
                 umma_commit(pv_done);
             }
             __syncwarp();
-            if (lane == 0) ATR8(1, i);
+            if (lane == 0) ATR8(3, i);
             mbar_wait(ds_full, i & 1);
             tc_fence_after();
+            if (lane == 0) ATR8(4, i);
             if (elect_one()) {
                 mma_tmem_split_x_t<HD, 32>(tmem + DK_COL, tmem + DP_COL, smem_u32(sQt + st * T::T_TILE), i > 0);
                 umma_commit(&qd_empty[st]);
                 if (i == nq - 1) umma_commit(acc_done);
             }
             __syncwarp();
-            if (lane == 0) ATR8(2, i);
+            if (lane == 0) ATR8(5, i);
             if (i + 1 < nq) issue_dp(i + 1);  // overwrites dS^T(i): behind dK(i) in the tensor pipe
+            if (lane == 0) ATR8(6, i);
         }
     } else if (warp >= 4) {
         // two warps per TMEM lane group: warp hf handles query columns [32 hf, 32 hf + 32) of each tile
@@ -595,8 +612,20 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v8_kernel(const __grid_co
             mbar_wait(&qd_full[st], (i / NST) & 1);  // lse / D rows of this tile have landed
             mbar_wait(s_full, i & 1);
             tc_fence_after();
-            if (warp == 4 && lane == 0) ATR8(3, i);
+            if (warp == 4 && lane == 0) ATR8(7, i);
             float s[HQ], dp[HQ];
+            if (g_attn_dbg & 1) {  // timing experiment: barriers only, no TMEM traffic or math
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(s_empty);
+                if (i >= 1) mbar_wait(pv_done, (i - 1) & 1);
+                if (lane == 0) mbar_arrive(p_full);
+                mbar_wait(dp_full, i & 1);
+                tc_fence_after();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(ds_full);
+                continue;
+            }
             tmem_ld32(tmem + lane_base + S_COL + hf * HQ, reinterpret_cast<uint32_t*>(s));
             tmem_wait_ld();
             tc_fence_before();
@@ -623,10 +652,8 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v8_kernel(const __grid_co
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full);
-            if (warp == 4 && lane == 0) ATR8(4, i);
             mbar_wait(dp_full, i & 1);
             tc_fence_after();
-            if (warp == 4 && lane == 0) ATR8(5, i);
             tmem_ld32(tmem + lane_base + DP_COL + hf * HQ, reinterpret_cast<uint32_t*>(dp));
             tmem_wait_ld();
 #pragma unroll
@@ -637,7 +664,6 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v8_kernel(const __grid_co
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(ds_full);
-            if (warp == 4 && lane == 0) ATR8(6, i);
         }
         if (nq > 0) mbar_wait(acc_done, 0);
         tc_fence_after();
@@ -658,6 +684,296 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v8_kernel(const __grid_co
     __syncthreads();
     tc_fence_after();
     if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// =====================================================================================  dK / dV (v9, cta_group::2)
+// v8's schedule on a 2-CTA cluster that owns 256 keys (128 per CTA): every product is one M = 256 UMMA
+// (tcgen05.mma.cta_group::2) issued by the leader CTA, so one issuing thread drives both SMs' tensor pipes.
+// A single thread issues a tcgen05.mma every ~35-45 clk, about the execution time of a 128 x 64 x 16
+// MMA, so with M = 128 the MMA warp of v8 is issue-bound (26 MMAs per 64-query step) and every barrier wait
+// drains the pipe; with M = 256 the same 26 instructions cover twice the work.
+// Operand split (the pair convention: A rows and D lanes per CTA, B rows split in half):
+//   S^T  (M keys, N = 64 queries):  B = Q[32 r .. 32 r + 32, :)     per CTA, K-major row tile (QS tile)
+//   dP^T (M keys, N = 64 queries):  B = dO[32 r .. 32 r + 32, :)    per CTA, K-major row tile (OS tile)
+//   dV   (M keys, N = hd):          B = dO^T[72 r .. 72 r + 72, :)  per CTA, K-major SW128   (OH tile)
+//   dK   (M keys, N = hd):          B = Q^T[72 r .. 72 r + 72, :)   per CTA, K-major SW128   (QH tile)
+// TMEM per CTA as v8 (its 128 key lanes).  Leader barriers (waited by the MMA warp) count both CTAs'
+// compute warps; the leader's commits are multicast to both CTAs.
+template <int HD>
+struct PairT {
+    static constexpr int HH = HD / 2;          // head_dim rows per CTA in the K-major tiles
+    static constexpr int NF = HD / 64, TAIL = HD % 64;
+    static constexpr int S_TILE = NF * 4096 + (TAIL ? 1024 : 0);  // 32 token rows x HD: SW128 chunks + SW32 tail
+    static constexpr int H_TILE = HH * 128;    // HH rows x 64 tokens (128 B rows, SW128)
+    static constexpr int STAGE = 2 * S_TILE + 2 * H_TILE;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v9_kernel(const __grid_constant__ BwdMaps tm,
+                                                                 const __grid_constant__ BwdMaps tp2,
+                                                                 AttnBwdProblem p) {
+    constexpr int BKV = 128, BQ = 64, NST = 5;
+    using T = BT<HD>;
+    using PT = PairT<HD>;
+    constexpr int VA = HD >= 128 ? 128 : HD;
+    constexpr int VT = HD - VA;
+    static_assert(VT == 0 || VT == 16, "head_dim tail must be one 16-column k-step");
+    static_assert(PT::HH % 8 == 0, "half head_dim must be whole 8-row swizzle atoms");
+    constexpr int HDP = ((HD + 15) / 16) * 16;
+    constexpr int S_COL = 0, P_COL = 64, DP_COL = 96, DV_COL = 160, DK_COL = DV_COL + HDP, VA_COL = DK_COL + HDP;
+    static_assert(VA_COL + VA / 2 <= 512, "TMEM budget");
+    constexpr uint16_t kPair = 0x3;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sK = smem;
+    uint8_t* sVt = sK + T::ROW_TILE;
+    uint8_t* sStage = sVt + (VT ? 4096 : 0);  // [NST] x {QS, OS, QH, OH}
+    float* sLse = reinterpret_cast<float*>(sStage + NST * PT::STAGE);  // [NST][64]
+    float* sD = sLse + NST * BQ;                                        // [NST][64]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sD + NST * BQ);
+    uint64_t* k_full = bars;                // leader: both CTAs' K / V tail
+    uint64_t* qd_full = bars + 1;           // [NST] leader: both CTAs' operand tiles
+    uint64_t* qd_empty = bars + 1 + NST;    // [NST] each CTA (multicast commit)
+    uint64_t* ld_full = bars + 1 + 2 * NST; // [NST] each CTA: its lse / D rows
+    uint64_t* s_full = bars + 1 + 3 * NST;  // each CTA (multicast)
+    uint64_t* s_empty = s_full + 1;         // leader, 16 arrivals
+    uint64_t* p_full = s_full + 2;          // leader, 16
+    uint64_t* pv_done = s_full + 3;         // each CTA (multicast)
+    uint64_t* dp_full = s_full + 4;         // each CTA (multicast)
+    uint64_t* ds_full = s_full + 5;         // leader, 16
+    uint64_t* acc_done = s_full + 6;        // each CTA (multicast)
+    uint64_t* va_ready = s_full + 7;        // leader, 8
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 8);
+    auto qs = [&](int st) { return sStage + st * PT::STAGE; };
+    auto os = [&](int st) { return sStage + st * PT::STAGE + PT::S_TILE; };
+    auto qh = [&](int st) { return sStage + st * PT::STAGE + 2 * PT::S_TILE; };
+    auto oh = [&](int st) { return sStage + st * PT::STAGE + 2 * PT::S_TILE + PT::H_TILE; };
+
+    const AttnProblem& f = p.f;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int rank = static_cast<int>(cluster_ctarank());
+    const bool leader = rank == 0;
+    const int h = blockIdx.y, k0 = (blockIdx.x >> 1) * 2 * BKV + rank * BKV;
+    const int nq = (f.Nq + BQ - 1) / BQ;
+    const int col = h * HD;
+
+    if (threadIdx.x == 0) {
+        mbar_init(k_full, 1);
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&qd_full[i], 1);
+            mbar_init(&qd_empty[i], 1);
+            mbar_init(&ld_full[i], 1);
+        }
+        mbar_init(s_full, 1);
+        mbar_init(s_empty, 16);
+        mbar_init(p_full, 16);
+        mbar_init(pv_done, 1);
+        mbar_init(dp_full, 1);
+        mbar_init(ds_full, 16);
+        mbar_init(acc_done, 1);
+        mbar_init(va_ready, 8);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc_pair<512>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();  // both CTAs' barriers initialised before any remote arrival / multicast
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            const uint32_t kf = mapa(smem_u32(k_full), 0), qf = mapa(smem_u32(qd_full), 0);
+            if (leader) mbar_arrive_expect_tx(k_full, 2 * (T::ROW_TILE + (VT ? 4096 : 0)));
+#pragma unroll
+            for (int c = 0; c < T::NF; ++c) tma_load_2d_pair(sK + c * 16384, &tm.a128, kf, col + c * 64, k0);
+            if (T::TAIL) tma_load_2d_pair(sK + T::NF * 16384, &tm.a32, kf, col + T::NF * 64, k0);
+            if (VT) tma_load_2d_pair(sVt, &tm.b32, kf, col + VA, k0);
+            for (int i = 0; i < nq; ++i) {
+                const int st = i % NST;
+                if (i >= NST) mbar_wait(&qd_empty[st], ((i / NST) - 1) & 1);
+                const int q0 = i * BQ;
+                if (leader) mbar_arrive_expect_tx(&qd_full[st], 2 * PT::STAGE);
+                // Q / dO rows: this CTA's 32 queries of the step (K-major over head_dim)
+#pragma unroll
+                for (int c = 0; c < PT::NF; ++c) {
+                    tma_load_2d_pair(qs(st) + c * 4096, &tp2.a128, qf + st * 8, col + c * 64, q0 + 32 * rank);
+                    tma_load_2d_pair(os(st) + c * 4096, &tp2.b128, qf + st * 8, col + c * 64, q0 + 32 * rank);
+                }
+                if (PT::TAIL) {
+                    tma_load_2d_pair(qs(st) + PT::NF * 4096, &tp2.a32, qf + st * 8, col + PT::NF * 64, q0 + 32 * rank);
+                    tma_load_2d_pair(os(st) + PT::NF * 4096, &tp2.b32, qf + st * 8, col + PT::NF * 64, q0 + 32 * rank);
+                }
+                // Q^T / dO^T: this CTA's head_dim rows of the step's 64 queries (K-major over queries)
+                tma_load_2d_pair(qh(st), &tp2.ta, qf + st * 8, q0, col + PT::HH * rank);
+                tma_load_2d_pair(oh(st), &tp2.tb, qf + st * 8, q0, col + PT::HH * rank);
+                mbar_arrive_expect_tx(&ld_full[st], 2 * BQ * 4);
+                bulk_load(sLse + st * BQ, f.lse + (int64_t)h * lse_stride(f) + q0, BQ * 4, &ld_full[st]);
+                bulk_load(sD + st * BQ, p.Dvec + (int64_t)h * lse_stride(f) + q0, BQ * 4, &ld_full[st]);
+            }
+        }
+    } else if (warp == 1) {
+        if (leader) {
+            constexpr uint32_t id64 = idesc_bf16_f32(256, 64, false, false), idhd = idesc_bf16_f32(256, HD, false, false);
+            // k-step kk (head_dim 16 kk ..) of a K-major 32-row tile: SW128 chunk kk / 4, or the SW32 tail
+            auto bdesc = [&](uint32_t b, int kk) {
+                return kk < 4 * PT::NF ? smem_desc(b + (kk / 4) * 4096 + (kk % 4) * 32, 16, 1024, kSwizzle128)
+                                       : smem_desc(b + PT::NF * 4096, 16, 256, kSwizzle32);
+            };
+            auto issue_s = [&](int i) {  // S^T(i) = K Q^T(i)
+                if (elect_one()) {
+                    const uint32_t a = smem_u32(sK), b = smem_u32(qs(i % NST));
+                    int kk = 0;
+#pragma unroll
+                    for (int c = 0; c < T::NF; ++c)
+#pragma unroll
+                        for (int k4 = 0; k4 < 4; ++k4, ++kk)
+                            umma_f16_ss_pair(tmem + S_COL, smem_desc(a + c * 16384 + k4 * 32, 16, 1024, kSwizzle128),
+                                             bdesc(b, kk), id64, kk > 0);
+                    if (T::TAIL)
+                        umma_f16_ss_pair(tmem + S_COL, smem_desc(a + T::NF * 16384, 16, 256, kSwizzle32), bdesc(b, kk),
+                                         id64, 1u);
+                    umma_commit_pair_mc(s_full, kPair);
+                }
+                __syncwarp();
+            };
+            auto issue_dp = [&](int i) {  // dP^T(i) = V dO^T(i)
+                if (elect_one()) {
+                    const uint32_t b = smem_u32(os(i % NST));
+#pragma unroll
+                    for (int kk = 0; kk < VA / 16; ++kk)
+                        umma_f16_ts_pair(tmem + DP_COL, tmem + VA_COL + kk * 8, bdesc(b, kk), id64, kk > 0 ? 1u : 0u);
+                    if (VT)
+                        umma_f16_ss_pair(tmem + DP_COL, smem_desc(smem_u32(sVt), 16, 256, kSwizzle32), bdesc(b, VA / 16),
+                                         id64, 1u);
+                    umma_commit_pair_mc(dp_full, kPair);
+                }
+                __syncwarp();
+            };
+            mbar_wait(va_ready, 0);
+            mbar_wait(k_full, 0);
+            if (nq > 0) {
+                mbar_wait(&qd_full[0], 0);
+                tc_fence_after();
+                issue_s(0);
+                issue_dp(0);
+            }
+            for (int i = 0; i < nq; ++i) {
+                const int st = i % NST;
+                if (lane == 0) ATR9(0, i);
+                if (i + 1 < nq) {
+                    mbar_wait(s_empty, i & 1);
+                    mbar_wait(&qd_full[(i + 1) % NST], ((i + 1) / NST) & 1);
+                    tc_fence_after();
+                    issue_s(i + 1);
+                }
+                if (lane == 0) ATR9(1, i);
+                mbar_wait(p_full, i & 1);
+                tc_fence_after();
+                if (lane == 0) ATR9(2, i);
+                if (elect_one()) {  // dV += P^T dO
+                    const uint32_t b = smem_u32(oh(st));
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks)
+                        umma_f16_ts_pair(tmem + DV_COL, tmem + P_COL + ks * 8, smem_desc(b + ks * 32, 16, 1024, kSwizzle128),
+                                         idhd, (i > 0 || ks > 0) ? 1u : 0u);
+                    umma_commit_pair_mc(pv_done, kPair);
+                }
+                __syncwarp();
+                if (lane == 0) ATR9(3, i);
+                mbar_wait(ds_full, i & 1);
+                tc_fence_after();
+                if (lane == 0) ATR9(4, i);
+                if (elect_one()) {  // dK += dS^T Q  (dS^T split over the two warps' query halves, as v8)
+                    const uint32_t b = smem_u32(qh(st));
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks)
+                        umma_f16_ts_pair(tmem + DK_COL, tmem + DP_COL + (16 * ks / 32) * 32 + (16 * ks % 32) / 2,
+                                         smem_desc(b + ks * 32, 16, 1024, kSwizzle128), idhd, (i > 0 || ks > 0) ? 1u : 0u);
+                    umma_commit_pair_mc(&qd_empty[st], kPair);
+                    if (i == nq - 1) umma_commit_pair_mc(acc_done, kPair);
+                }
+                __syncwarp();
+                if (lane == 0) ATR9(5, i);
+                if (i + 1 < nq) issue_dp(i + 1);
+                if (lane == 0) ATR9(6, i);
+            }
+        }
+    } else if (warp >= 4) {
+        const int g = warp & 3, hf = (warp - 4) >> 2, row = g * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(g * 32) << 16;
+        const int kv = k0 + row;
+        const bool kvv = kv < f.Nk;
+        const uint32_t s_empty_l = mapa(smem_u32(s_empty), 0), p_full_l = mapa(smem_u32(p_full), 0);
+        const uint32_t ds_full_l = mapa(smem_u32(ds_full), 0), va_ready_l = mapa(smem_u32(va_ready), 0);
+        if (hf == 0) {
+            row_to_tmem<VA>(tmem + lane_base + VA_COL,
+                            static_cast<const __nv_bfloat16*>(f.v) + (int64_t)(kvv ? kv : 0) * f.v_ld + col, kvv);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(va_ready_l);
+        }
+        constexpr int HQ = BQ / 2;
+        for (int i = 0; i < nq; ++i) {
+            const int st = i % NST;
+            mbar_wait(&ld_full[st], (i / NST) & 1);
+            mbar_wait(s_full, i & 1);
+            tc_fence_after();
+            if (warp == 4 && lane == 0) ATR9(7, i);
+            float s[HQ], dp[HQ];
+            tmem_ld32(tmem + lane_base + S_COL + hf * HQ, reinterpret_cast<uint32_t*>(s));
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(s_empty_l);
+            const float* lse2 = sLse + st * BQ + hf * HQ;
+            const float* Dq = sD + st * BQ + hf * HQ;
+            const int qb = i * BQ + hf * HQ;
+            const bool full = qb + HQ <= f.Nq;
+            uint32_t pk[HQ / 2];
+#pragma unroll
+            for (int c = 0; c < HQ; c += 2) {
+                const bool v0 = full || qb + c < f.Nq, v1 = full || qb + c + 1 < f.Nq;
+                s[c] = v0 ? ex2f((s[c] - lse2[c]) * kLog2e) : 0.0f;
+                s[c + 1] = v1 ? ex2f((s[c + 1] - lse2[c + 1]) * kLog2e) : 0.0f;
+                pk[c / 2] = pack_bf16(s[c], s[c + 1]);
+            }
+            if (i >= 1) {
+                mbar_wait(pv_done, (i - 1) & 1);
+                tc_fence_after();
+            }
+            tmem_st16(tmem + lane_base + P_COL + hf * (HQ / 2), pk);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(p_full_l);
+            mbar_wait(dp_full, i & 1);
+            tc_fence_after();
+            tmem_ld32(tmem + lane_base + DP_COL + hf * HQ, reinterpret_cast<uint32_t*>(dp));
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < HQ; c += 2)
+                pk[c / 2] = pack_bf16(s[c] * (dp[c] - Dq[c]), s[c + 1] * (dp[c + 1] - Dq[c + 1]));  // autodiff.cpp:820
+            tmem_st16(tmem + lane_base + DP_COL + hf * HQ, pk);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(ds_full_l);
+        }
+        if (nq > 0) mbar_wait(acc_done, 0);
+        tc_fence_after();
+        const bool valid = kvv && nq > 0;
+        if (hf == 0)
+            store_acc_row<HD>(tmem + lane_base + DV_COL, static_cast<__nv_bfloat16*>(p.dv) + (int64_t)kv * p.dv_ld + col,
+                              valid);
+        else
+            store_acc_row<HD>(tmem + lane_base + DK_COL, static_cast<__nv_bfloat16*>(p.dk) + (int64_t)kv * p.dk_ld + col,
+                              valid);
+    }
+    tc_fence_before();
+    cluster_sync();  // no CTA leaves while its peer may still arrive on / multicast into it
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc_pair<512>(tmem);
 }
 
 // =====================================================================================  dK / dV, CTA pair
@@ -1223,7 +1539,39 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
         const int splits = std::max(1, std::min({num_sms() / std::max(kv_ctas, 1), nq_all / 8, 16}));
         float* part = nullptr;
         if (splits > 1) MGV_CUDA(cudaMallocAsync(&part, sizeof(float) * splits * f.Nk * 2 * W, s));
-        if (splits == 1 && g_dkv_pair) {
+        if (splits == 1 && g_dkv_variant == 2) {
+            // v9: CTA pairs over 256 keys, M = 256 UMMAs (the operand tiles split as described at the kernel)
+            using PT = PairT<HD>;
+            BwdMaps m2;
+            if ((reinterpret_cast<uintptr_t>(f.q) | reinterpret_cast<uintptr_t>(p.dO)) % 16 || f.q_ld % 8 || p.do_ld % 8)
+                throw std::runtime_error("attn_bwd_tc: q / dO must be 16-byte aligned with ld % 8 == 0");
+            make_tmap_sw(&m2.a128, f.q, W, f.Nq, f.q_ld, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+            make_tmap_sw(&m2.a32, f.q, W, f.Nq, f.q_ld, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B);
+            make_tmap_sw(&m2.b128, p.dO, W, f.Nq, p.do_ld, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+            make_tmap_sw(&m2.b32, p.dO, W, f.Nq, p.do_ld, 16, 32, CU_TENSOR_MAP_SWIZZLE_32B);
+            make_tmap_sw(&m2.ta, qt, f.Nq, W, qt_ld, 64, PT::HH, CU_TENSOR_MAP_SWIZZLE_128B);
+            make_tmap_sw(&m2.tb, dot, f.Nq, W, dot_ld, 64, PT::HH, CU_TENSOR_MAP_SWIZZLE_128B);
+            const int psmem = T::ROW_TILE + (HD > 128 ? 4096 : 0) + 5 * PT::STAGE + 10 * 64 * 4 + 256 + 1024;
+            static bool pset9 = false;
+            if (!pset9) {
+                MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_v9_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              psmem));
+                pset9 = true;
+            }
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(2 * ((f.Nk + 255) / 256), f.heads);
+            cfg.blockDim = dim3(384);
+            cfg.dynamicSmemBytes = psmem;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            MGV_CUDA(cudaLaunchKernelEx(&cfg, attn_bwd_dkv_v9_kernel<HD>, m, m2, p));
+        } else if (splits == 1 && g_dkv_pair) {
             // one 2-CTA cluster per key tile (head_dim split over the pair, P^T / dS^T exchanged via DSMEM)
             const int psmem = 8 * T::T_TILE + 4 * 128 * 64 * 2 + 4 * 64 * 4 + 256 + 1024;
             static bool pset = false;
@@ -1339,6 +1687,9 @@ extern "C" int mgv_dev_attn_trace2(unsigned long long* out) {
 extern "C" int mgv_dev_set_dkv_pair(int on) {
     mgv::g_dkv_pair = on ? 1 : 0;
     return 0;
+}
+extern "C" int mgv_dev_set_attn_dbg(int v) {
+    return cudaMemcpyToSymbol(mgv::g_attn_dbg, &v, sizeof(int)) == cudaSuccess ? 0 : 1;
 }
 extern "C" int mgv_dev_set_dkv_variant(int v) {
     mgv::g_dkv_variant = v;

@@ -12,6 +12,8 @@ L = lib()
 import os  # noqa: E402
 if os.environ.get("MGV_DKV_VARIANT"):  # 0 = v8 (default), 1 = v5
     L.mgv_dev_set_dkv_variant(int(os.environ["MGV_DKV_VARIANT"]))
+if os.environ.get("MGV_ATTN_DBG"):  # timing experiments (wrong results): see attn_bwd_tc.cu g_attn_dbg
+    L.mgv_dev_set_attn_dbg(int(os.environ["MGV_ATTN_DBG"]))
 P = ctypes.c_void_p
 i64 = ctypes.c_int64
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 57600

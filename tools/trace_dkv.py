@@ -13,11 +13,12 @@ buf = (ctypes.c_ulonglong * (8 * 64))()
 lib().mgv_dev_attn_trace2(buf)
 ev = [[buf[e * 64 + j] for j in range(64)] for e in range(8)]
 t0 = ev[3][0]
-names = ["mma:S(i+1)", "mma:dV(i)", "mma:dK(i)", "cmp:S(i) ok", "cmp:P(i) st", "cmp:dP(i) ok", "cmp:dS st"]
+t0 = ev[0][0]
+names = ["mma:top", "S(i+1) iss", "p_full ok", "dV(i) iss", "ds_full ok", "dK(i) iss", "dP(i+1) iss", "cmp:S(i) ok"]
 print("step " + " ".join(f"{n:>12s}" for n in names) + "   period")
 for j in range(1, 24):
-    row = [ev[e][j] - t0 for e in range(7)]
-    print(f"{j:4d} " + " ".join(f"{v:12d}" for v in row) + f"   {ev[3][j] - ev[3][j - 1]:6d}")
+    row = [ev[e][j] - t0 for e in range(8)]
+    print(f"{j:4d} " + " ".join(f"{v:12d}" for v in row) + f"   {ev[0][j] - ev[0][j - 1]:6d}")
 
 # the dQ pass of the same run (events of tools/trace_attn.py)
 lib().mgv_dev_attn_trace(buf)
