@@ -454,6 +454,9 @@ void Model::download_param(int64_t i, double* out) {
 void Model::upload(const Cfg& cfg, int64_t n, const char* const* names, const void* const* data,
                    const uint8_t* is_f32, const int64_t* numel) {
     validate_cfg(cfg);
+    if (bf16_ && (cfg.hd() % 16 != 0 || cfg.text_dim % 8 != 0 || cfg.D() % 8 != 0))  // TMA rows / UMMA shapes
+        throw ConfigError("bf16 tensor-core mode needs head_dim % 16 == 0 and text_dim, 4 c_z multiples of 8 "
+                          "(use the fp32 parity mode for other shapes)");
     if (tp_ > 1 && (cfg.heads % tp_ != 0 || (cfg.hidden / tp_) % 8 != 0))
         throw ConfigError("tensor parallel size must divide heads, with hidden/size a multiple of 8");
     MGV_CUDA(cudaSetDevice(device_));
