@@ -36,5 +36,6 @@ def _declare(L):
     L.mgv_dev_set_gemm_mode.argtypes = [I]
     L.mgv_dev_set_dkv_pair.argtypes = [I]
     L.mgv_dev_set_dkv_variant.argtypes = [I]
+    L.mgv_dev_set_dq_variant.argtypes = [I]
     from . import capi
     capi.declare(L)

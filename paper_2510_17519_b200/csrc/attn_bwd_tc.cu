@@ -31,6 +31,8 @@ namespace mgv {
 static int g_dkv_pair = 0;
 // 0 = v8 (default: V in TMEM, P^T in its own columns), 1 = v5 (K in TMEM, P^T / dS^T aliased)
 static int g_dkv_variant = 0;
+// dQ pass variant: 0 = v7 (Q and dO in TMEM, dP single-buffered), 1 = v8 (Q in shared memory, dP double-buffered)
+static int g_dq_variant = 0;
 // timing experiments only (tools/): bit 0 = compute warps skip TMEM traffic and math, bit 1 = no Q^T/dO^T TMA
 __device__ int g_attn_dbg = 0;
 
@@ -1446,6 +1448,24 @@ __global__ void __launch_bounds__(128 + 128 * kCWq, 1) attn_bwd_dq_tc_kernel(con
             }
         };
         float pr[HK];
+        if (g_attn_dbg & 1) {  // timing experiment: barriers only, no TMEM traffic or math (wrong results)
+            for (int j = 0; j < nkv; ++j) {
+                if (j == 0) {
+                    mbar_wait(&s_full[0], 0);
+                    if (lane == 0) mbar_arrive(&s_empty[0]);
+                }
+                if (j + 1 < nkv) mbar_wait(&s_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+                mbar_wait(dp_full, j & 1);
+                tc_fence_after();
+                __syncwarp();
+                if (lane == 0) {
+                    if (j + 1 < nkv) mbar_arrive(&s_empty[(j + 1) & 1]);
+                    mbar_arrive(dp_empty);
+                }
+                if (j >= 1) mbar_wait(dq_done, (j - 1) & 1);
+                if (lane == 0) mbar_arrive(ds_full);
+            }
+        } else {
         if (nkv > 0) {
             mbar_wait(&s_full[0], 0);
             tc_fence_after();
@@ -1492,6 +1512,212 @@ __global__ void __launch_bounds__(128 + 128 * kCWq, 1) attn_bwd_dq_tc_kernel(con
             __syncwarp();
             if (lane == 0) mbar_arrive(ds_full);
             if (warp == 4 && lane == 0) ATR(6, j);
+#pragma unroll
+            for (int c = 0; c < HK; ++c) pr[c] = sn[c];
+        }
+        }
+        if (nkv > 0) mbar_wait(acc_done, 0);
+        tc_fence_after();
+        constexpr int NC = HD / 16;
+        store_acc_row<HD>(tmem + lane_base + DQ_COL, static_cast<__nv_bfloat16*>(p.dq) + (int64_t)q * p.dq_ld + col,
+                          qv && nkv > 0, hf * NC / kCWq, (hf + 1) * NC / kCWq);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// =====================================================================================  dQ (v8)
+// The dQ pass with dP double-buffered: Q moves from TMEM to a shared-memory row tile (S = Q K^T becomes an
+// SS product), which frees the 64 TMEM columns of a second dP buffer.  Both products are then issued two
+// key tiles ahead, so the dP round trip (MMA -> compute warps -> MMA) leaves the critical path.
+// TMEM: S[b] [64b, 64b+64)  dP[b] [128+64b, ..)  dS [256,288)  dQ [288,288+HD)  dO (bf16 pairs) after.
+template <int HD>
+__global__ void __launch_bounds__(128 + 128 * kCWq, 1) attn_bwd_dq_v8_kernel(const __grid_constant__ BwdMaps tm,
+                                                                            AttnBwdProblem p) {
+    constexpr int BMQ = 128, BKV = 64, NST = 5;
+    using T = BT<HD>;
+    constexpr int DP_COL = 128, DS_COL = 256, DQ_COL = 288;
+    constexpr int DOA_COL = DQ_COL + ((HD + 15) / 16) * 16;
+    static_assert(DOA_COL + HD / 2 <= 512, "TMEM budget");
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;                            // 128 query rows x HD (K-major over hd)
+    uint8_t* sKt = sQ + T::ROW_TILE;               // [NST]
+    uint8_t* sVt = sKt + NST * T::T_TILE;          // [NST]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sVt + NST * T::T_TILE);
+    uint64_t* kv_full = bars;             // [NST]
+    uint64_t* kv_empty = bars + NST;      // [NST]
+    uint64_t* s_full = bars + 2 * NST;    // [2]
+    uint64_t* s_empty = s_full + 2;       // [2]
+    uint64_t* dp_full = s_full + 4;       // [2]
+    uint64_t* dp_empty = s_full + 6;      // [2]
+    uint64_t* ds_full = s_full + 8;
+    uint64_t* dq_done = s_full + 9;
+    uint64_t* acc_done = s_full + 10;
+    uint64_t* doa_ready = s_full + 11;
+    uint64_t* q_full = s_full + 12;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 13);
+
+    const AttnProblem& f = p.f;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int h = blockIdx.y, q0 = blockIdx.x * BMQ;
+    const int nkv = (f.Nk + BKV - 1) / BKV;
+    const int col = h * HD;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_empty[i], 4 * kCWq);
+            mbar_init(&dp_full[i], 1);
+            mbar_init(&dp_empty[i], 4 * kCWq);
+        }
+        mbar_init(ds_full, 4 * kCWq);
+        mbar_init(dq_done, 1);
+        mbar_init(acc_done, 1);
+        mbar_init(doa_ready, 4);
+        mbar_init(q_full, 1);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            mbar_arrive_expect_tx(q_full, T::ROW_TILE);
+            load_row_tile<HD>(sQ, &tm.a128, &tm.a32, q_full, col, q0);
+            for (int j = 0; j < nkv; ++j) {
+                const int b = j % NST;
+                if (j >= NST) mbar_wait(&kv_empty[b], ((j / NST) - 1) & 1);
+                mbar_arrive_expect_tx(&kv_full[b], 2 * T::T_TILE);
+                tma_load_2d(sKt + b * T::T_TILE, &tm.ta, &kv_full[b], j * BKV, col);
+                tma_load_2d(sVt + b * T::T_TILE, &tm.tb, &kv_full[b], j * BKV, col);
+            }
+        }
+    } else if (warp == 1) {
+        const uint32_t aQ = smem_u32(sQ);
+        auto issue_s = [&](int j) {  // S_j = Q K_j^T into buffer j & 1 (SS)
+            const int b = j % NST;
+            mbar_wait(&kv_full[b], (j / NST) & 1);
+            if (j >= 2) mbar_wait(&s_empty[j & 1], ((j - 2) >> 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                mma_rows_x_t<HD>(tmem + (j & 1) * 64, aQ, smem_u32(sKt + b * T::T_TILE));
+                umma_commit(&s_full[j & 1]);
+            }
+            __syncwarp();
+        };
+        auto issue_dp = [&](int j) {  // dP_j = dO V_j^T into buffer j & 1 (TS)
+            if (j >= 2) mbar_wait(&dp_empty[j & 1], ((j - 2) >> 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                mma_tmem_rows_x_t<HD>(tmem + DP_COL + (j & 1) * 64, tmem + DOA_COL,
+                                      smem_u32(sVt + (j % NST) * T::T_TILE));
+                umma_commit(&dp_full[j & 1]);
+            }
+            __syncwarp();
+        };
+        // issue order per step j:  S(j+2) [S_j read] -> dP(j+2) [dP_j read] -> dQ(j) [dS_j ready]
+        mbar_wait(doa_ready, 0);
+        mbar_wait(q_full, 0);
+        for (int j = 0; j < 2 && j < nkv; ++j) {
+            issue_s(j);
+            issue_dp(j);
+        }
+        for (int j = 0; j < nkv; ++j) {
+            if (j + 2 < nkv) {
+                issue_s(j + 2);
+                issue_dp(j + 2);
+            }
+            mbar_wait(ds_full, j & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                const int b = j % NST;
+                mma_tmem_x_t<HD>(tmem + DQ_COL, tmem + DS_COL, smem_u32(sKt + b * T::T_TILE), j > 0);
+                umma_commit(dq_done);
+                umma_commit(&kv_empty[b]);
+                if (j == nkv - 1) umma_commit(acc_done);
+            }
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        const int g = warp & 3, hf = (warp - 4) >> 2, row = g * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(g * 32) << 16;
+        const int q = q0 + row;
+        const bool qv = q < f.Nq;
+        const int64_t qi = qv ? q : 0;
+        if (hf == 0) {  // stage dO rows into TMEM (A operand of dP)
+            row_to_tmem<HD>(tmem + lane_base + DOA_COL, static_cast<const __nv_bfloat16*>(p.dO) + qi * p.do_ld + col,
+                            qv);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(doa_ready);
+        }
+        const float lse2 = qv ? f.lse[(int64_t)h * lse_stride(f) + q] * kLog2e : 0.0f;
+        const float Dq = qv ? p.Dvec[(int64_t)h * lse_stride(f) + q] : 0.0f;
+        constexpr int HK = BKV / kCWq;
+        auto softmax = [&](float* x, int j) {
+            const int kb = j * BKV + hf * HK;
+            if (kb + HK <= f.Nk) {
+#pragma unroll
+                for (int c = 0; c < HK; ++c) x[c] = ex2f(fmaf(x[c], kLog2e, -lse2));
+            } else {
+#pragma unroll
+                for (int c = 0; c < HK; ++c) x[c] = kb + c < f.Nk ? ex2f(fmaf(x[c], kLog2e, -lse2)) : 0.0f;
+            }
+        };
+        float pr[HK];
+        if (nkv > 0) {
+            mbar_wait(&s_full[0], 0);
+            tc_fence_after();
+            tmem_ldn<HK>(tmem + lane_base + hf * HK, pr);
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[0]);
+            softmax(pr, 0);
+        }
+        for (int j = 0; j < nkv; ++j) {
+            const bool more = j + 1 < nkv;
+            float sn[HK], dp[HK];
+            if (more) {
+                mbar_wait(&s_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+                tc_fence_after();
+                tmem_ldn<HK>(tmem + lane_base + ((j + 1) & 1) * 64 + hf * HK, sn);
+            }
+            mbar_wait(&dp_full[j & 1], (j >> 1) & 1);
+            tc_fence_after();
+            tmem_ldn<HK>(tmem + lane_base + DP_COL + (j & 1) * 64 + hf * HK, dp);
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (more) mbar_arrive(&s_empty[(j + 1) & 1]);
+                mbar_arrive(&dp_empty[j & 1]);
+            }
+            uint32_t dk[HK / 2];
+#pragma unroll
+            for (int c = 0; c < HK; c += 2)
+                dk[c / 2] = pack_bf16(pr[c] * (dp[c] - Dq), pr[c + 1] * (dp[c + 1] - Dq));  // autodiff.cpp:820
+            if (more) softmax(sn, j + 1);
+            if (j >= 1) {
+                mbar_wait(dq_done, (j - 1) & 1);  // dQ += dS_{j-1} K has read the dS columns
+                tc_fence_after();
+            }
+            tmem_stn<HK / 2>(tmem + lane_base + DS_COL + hf * (HK / 2), dk);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(ds_full);
 #pragma unroll
             for (int c = 0; c < HK; ++c) pr[c] = sn[c];
         }
@@ -1624,7 +1850,21 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
             MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             set = true;
         }
-        attn_bwd_dq_tc_kernel<HD><<<dim3((f.Nq + 127) / 128, f.heads), 128 + 128 * kCWq, smem, s>>>(m, p); ::mgv::note_launch();
+        if (g_dq_variant == 1) {  // v8: Q in shared memory, dP double-buffered
+            make_tmap_sw(&m.a128, f.q, W, f.Nq, f.q_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+            make_tmap_sw(&m.a32, f.q, W, f.Nq, f.q_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
+            const int smem8 = T::ROW_TILE + 10 * T::T_TILE + 256 + 1024;
+            static bool set8 = false;
+            if (!set8) {
+                MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dq_v8_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              smem8));
+                set8 = true;
+            }
+            attn_bwd_dq_v8_kernel<HD><<<dim3((f.Nq + 127) / 128, f.heads), 128 + 128 * kCWq, smem8, s>>>(m, p);
+        } else {
+            attn_bwd_dq_tc_kernel<HD><<<dim3((f.Nq + 127) / 128, f.heads), 128 + 128 * kCWq, smem, s>>>(m, p);
+        }
+        ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
     }
 }
@@ -1690,6 +1930,10 @@ extern "C" int mgv_dev_set_dkv_pair(int on) {
 }
 extern "C" int mgv_dev_set_attn_dbg(int v) {
     return cudaMemcpyToSymbol(mgv::g_attn_dbg, &v, sizeof(int)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int mgv_dev_set_dq_variant(int v) {
+    mgv::g_dq_variant = v;
+    return 0;
 }
 extern "C" int mgv_dev_set_dkv_variant(int v) {
     mgv::g_dkv_variant = v;
