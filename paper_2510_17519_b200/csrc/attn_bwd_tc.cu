@@ -31,8 +31,10 @@ namespace mgv {
 static int g_dkv_pair = 0;
 // 0 = v8 (default: V in TMEM, P^T in its own columns), 1 = v5 (K in TMEM, P^T / dS^T aliased)
 static int g_dkv_variant = 0;
-// dQ pass variant: 0 = v7 (Q and dO in TMEM, dP single-buffered), 1 = v8 (Q in shared memory, dP double-buffered)
-static int g_dq_variant = 0;
+// dQ pass variant: 2 = v9 (default: 128-key steps, Q and dO in shared memory), 0 = v7 (64-key steps, Q and dO
+// in TMEM, dP single-buffered), 1 = v8 (Q in shared memory, dP double-buffered)
+static int g_dq_variant = 2;
+static int g_dq_cw = 2;  // compute warps per TMEM lane group in the v9 dQ pass (2 or 4)
 // timing experiments only (tools/): bit 0 = compute warps skip TMEM traffic and math, bit 1 = no Q^T/dO^T TMA
 __device__ int g_attn_dbg = 0;
 
@@ -1733,6 +1735,217 @@ __global__ void __launch_bounds__(128 + 128 * kCWq, 1) attn_bwd_dq_v8_kernel(con
     if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// =====================================================================================  dQ (v9)
+// 128-key steps: every product is an N = 128 (S, dP) or K = 128 (dQ) MMA, so a step of the same work issues
+// 26 instead of 44 tcgen05.mma instructions (one thread issues one per ~40 clk, which bounds v7).  To fit
+// TMEM (S 128 + dP 128 + dS 64 + dQ 144 = 464 columns) Q and dO are shared-memory A operands (SS).
+// K^T (S and dQ) and V^T (dP) have separate two-stage rings; the issue order S(j+1) -> dQ(j) -> dP(j+1)
+// releases K^T(j) one product earlier than v7's order.
+// TMEM: S [0,128)  dP [128,256)  dS [256,320)  dQ [320,320+HD).
+template <int HD, int CW>
+__global__ void __launch_bounds__(128 + 128 * CW, 1) attn_bwd_dq_v9_kernel(const __grid_constant__ BwdMaps tm,
+                                                                          AttnBwdProblem p) {
+    constexpr int BMQ = 128, BKV = 128, KW = BKV / CW;  // CW compute warps per TMEM lane group, KW keys each
+    static_assert(KW == 32 || KW == 64, "32 or 64 keys per compute warp");
+    using T = BT<HD>;
+    constexpr int S_COL = 0, DP_COL = 128, DS_COL = 256, DQ_COL = 320;
+    static_assert(DQ_COL + ((HD + 15) / 16) * 16 <= 512, "TMEM budget");
+    constexpr int KV_STAGE = 2 * T::T_TILE;  // two 64-key transposed tiles
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;
+    uint8_t* sdO = sQ + T::ROW_TILE;
+    uint8_t* sKt = sdO + T::ROW_TILE;  // [2]
+    uint8_t* sVt = sKt + 2 * KV_STAGE;  // [2]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sVt + 2 * KV_STAGE);
+    uint64_t* q_full = bars;
+    uint64_t* kf = bars + 1;  // [2]
+    uint64_t* ke = bars + 3;  // [2]
+    uint64_t* vf = bars + 5;  // [2]
+    uint64_t* ve = bars + 7;  // [2]
+    uint64_t* s_full = bars + 9;
+    uint64_t* s_empty = bars + 10;
+    uint64_t* dp_full = bars + 11;
+    uint64_t* dp_empty = bars + 12;
+    uint64_t* ds_full = bars + 13;
+    uint64_t* dq_done = bars + 14;
+    uint64_t* acc_done = bars + 15;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+    const AttnProblem& f = p.f;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int h = blockIdx.y, q0 = blockIdx.x * BMQ;
+    const int nkv = (f.Nk + BKV - 1) / BKV;
+    const int col = h * HD;
+
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&kf[i], 1);
+            mbar_init(&ke[i], 1);
+            mbar_init(&vf[i], 1);
+            mbar_init(&ve[i], 1);
+        }
+        mbar_init(s_full, 1);
+        mbar_init(s_empty, 4 * CW);
+        mbar_init(dp_full, 1);
+        mbar_init(dp_empty, 4 * CW);
+        mbar_init(ds_full, 4 * CW);
+        mbar_init(dq_done, 1);
+        mbar_init(acc_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            mbar_arrive_expect_tx(q_full, 2 * T::ROW_TILE);
+            load_row_tile<HD>(sQ, &tm.a128, &tm.a32, q_full, col, q0);
+            load_row_tile<HD>(sdO, &tm.b128, &tm.b32, q_full, col, q0);
+            for (int j = 0; j < nkv; ++j) {
+                const int b = j & 1;
+                if (j >= 2) mbar_wait(&ke[b], ((j >> 1) - 1) & 1);
+                mbar_arrive_expect_tx(&kf[b], KV_STAGE);
+                tma_load_2d(sKt + b * KV_STAGE, &tm.ta, &kf[b], j * BKV, col);
+                tma_load_2d(sKt + b * KV_STAGE + T::T_TILE, &tm.ta, &kf[b], j * BKV + 64, col);
+                if (j >= 2) mbar_wait(&ve[b], ((j >> 1) - 1) & 1);
+                mbar_arrive_expect_tx(&vf[b], KV_STAGE);
+                tma_load_2d(sVt + b * KV_STAGE, &tm.tb, &vf[b], j * BKV, col);
+                tma_load_2d(sVt + b * KV_STAGE + T::T_TILE, &tm.tb, &vf[b], j * BKV + 64, col);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t id128 = idesc_bf16_f32(128, 128, false, true), idhd = idesc_bf16_f32(128, HD, false, false);
+        // D[128 x 128] = A[128 x HD] (smem rows) . B^T with B^T the two-tile HD x 128 transposed stage (MN-major)
+        auto rows_x_t2 = [&](uint32_t d, uint32_t a, uint32_t bt) {
+            int kk = 0;
+#pragma unroll
+            for (int c = 0; c < T::NF; ++c)
+#pragma unroll
+                for (int k4 = 0; k4 < 4; ++k4, ++kk)
+                    umma_f16_ss(d, smem_desc(a + c * 16384 + k4 * 32, 16, 1024, kSwizzle128),
+                                smem_desc(bt + kk * 2048, T::T_TILE, 1024, kSwizzle128), id128, kk > 0);
+            if (T::TAIL)
+                umma_f16_ss(d, smem_desc(a + T::NF * 16384, 16, 256, kSwizzle32),
+                            smem_desc(bt + kk * 2048, T::T_TILE, 1024, kSwizzle128), id128, 1);
+        };
+        auto issue_s = [&](int j) {
+            const int b = j & 1;
+            mbar_wait(&kf[b], (j >> 1) & 1);
+            if (j >= 1) mbar_wait(s_empty, (j - 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                rows_x_t2(tmem + S_COL, smem_u32(sQ), smem_u32(sKt + b * KV_STAGE));
+                umma_commit(s_full);
+            }
+            __syncwarp();
+        };
+        auto issue_dp = [&](int j) {
+            const int b = j & 1;
+            mbar_wait(&vf[b], (j >> 1) & 1);
+            if (j >= 1) mbar_wait(dp_empty, (j - 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                rows_x_t2(tmem + DP_COL, smem_u32(sdO), smem_u32(sVt + b * KV_STAGE));
+                umma_commit(dp_full);
+                umma_commit(&ve[b]);  // V^T(j) is read by dP(j) only
+            }
+            __syncwarp();
+        };
+        mbar_wait(q_full, 0);
+        if (nkv > 0) {
+            issue_s(0);
+            issue_dp(0);
+        }
+        for (int j = 0; j < nkv; ++j) {
+            const int b = j & 1;
+            if (j + 1 < nkv) issue_s(j + 1);
+            mbar_wait(ds_full, j & 1);
+            tc_fence_after();
+            if (elect_one()) {  // dQ += dS_j K_j: 8 k-steps of 16 keys over the stage's two K^T tiles
+                const uint32_t bt = smem_u32(sKt + b * KV_STAGE);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    umma_f16_ts(tmem + DQ_COL, tmem + DS_COL + ks * 8,
+                                smem_desc(bt + (ks >> 2) * T::T_TILE + (ks & 3) * 32, 16, 1024, kSwizzle128), idhd,
+                                (j > 0 || ks > 0) ? 1u : 0u);
+                umma_commit(dq_done);
+                umma_commit(&ke[b]);  // K^T(j): S(j) and dQ(j) done
+                if (j == nkv - 1) umma_commit(acc_done);
+            }
+            __syncwarp();
+            if (j + 1 < nkv) issue_dp(j + 1);
+        }
+    } else if (warp >= 4) {
+        // CW warps per TMEM lane group: warp hf handles keys [KW hf, KW hf + KW) of each step, 32 at a time
+        const int g = warp & 3, hf = (warp - 4) >> 2, row = g * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(g * 32) << 16;
+        const int q = q0 + row;
+        const bool qv = q < f.Nq;
+        const float lse2 = qv ? f.lse[(int64_t)h * lse_stride(f) + q] * kLog2e : 0.0f;
+        const float Dq = qv ? p.Dvec[(int64_t)h * lse_stride(f) + q] : 0.0f;
+        for (int j = 0; j < nkv; ++j) {
+            float pr[KW];
+            mbar_wait(s_full, j & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int u = 0; u < KW / 32; ++u)
+                tmem_ld32(tmem + lane_base + S_COL + hf * KW + u * 32, reinterpret_cast<uint32_t*>(pr + 32 * u));
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(s_empty);
+            const int kb = j * BKV + hf * KW;
+            if (kb + KW <= f.Nk) {
+#pragma unroll
+                for (int c = 0; c < KW; ++c) pr[c] = ex2f(fmaf(pr[c], kLog2e, -lse2));
+            } else {
+#pragma unroll
+                for (int c = 0; c < KW; ++c) pr[c] = kb + c < f.Nk ? ex2f(fmaf(pr[c], kLog2e, -lse2)) : 0.0f;
+            }
+            mbar_wait(dp_full, j & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int u = 0; u < KW / 32; ++u) {
+                float dp[32];
+                tmem_ld32(tmem + lane_base + DP_COL + hf * KW + u * 32, reinterpret_cast<uint32_t*>(dp));
+                tmem_wait_ld();
+                if (u == KW / 32 - 1) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(dp_empty);
+                }
+                uint32_t dk[16];
+#pragma unroll
+                for (int c = 0; c < 32; c += 2)
+                    dk[c / 2] = pack_bf16(pr[32 * u + c] * (dp[c] - Dq), pr[32 * u + c + 1] * (dp[c + 1] - Dq));
+                if (u == 0 && j >= 1) {
+                    mbar_wait(dq_done, (j - 1) & 1);  // dQ(j-1) has read the dS columns
+                    tc_fence_after();
+                }
+                tmem_st16(tmem + lane_base + DS_COL + hf * (KW / 2) + u * 16, dk);
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(ds_full);
+        }
+        if (nkv > 0) mbar_wait(acc_done, 0);
+        tc_fence_after();
+        constexpr int NC = HD / 16;
+        store_acc_row<HD>(tmem + lane_base + DQ_COL, static_cast<__nv_bfloat16*>(p.dq) + (int64_t)q * p.dq_ld + col,
+                          qv && nkv > 0, hf * NC / CW, (hf + 1) * NC / CW);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 // ------------------------------------------------------------------ host
 template <int HD>
 static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, const void* kt, int64_t kt_ld,
@@ -1850,7 +2063,25 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
             MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             set = true;
         }
-        if (g_dq_variant == 1) {  // v8: Q in shared memory, dP double-buffered
+        if (g_dq_variant == 2) {  // v9: 128-key steps, Q and dO in shared memory
+            make_tmap_sw(&m.a128, f.q, W, f.Nq, f.q_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+            make_tmap_sw(&m.a32, f.q, W, f.Nq, f.q_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
+            make_tmap_sw(&m.b128, p.dO, W, f.Nq, p.do_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+            make_tmap_sw(&m.b32, p.dO, W, f.Nq, p.do_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
+            const int smem9 = 2 * T::ROW_TILE + 8 * T::T_TILE + 256 + 1024;
+            static bool set9 = false;
+            if (!set9) {
+                MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dq_v9_kernel<HD, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              smem9));
+                MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dq_v9_kernel<HD, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              smem9));
+                set9 = true;
+            }
+            if (g_dq_cw == 4)
+                attn_bwd_dq_v9_kernel<HD, 4><<<dim3((f.Nq + 127) / 128, f.heads), 128 + 128 * 4, smem9, s>>>(m, p);
+            else
+                attn_bwd_dq_v9_kernel<HD, 2><<<dim3((f.Nq + 127) / 128, f.heads), 128 + 128 * 2, smem9, s>>>(m, p);
+        } else if (g_dq_variant == 1) {  // v8: Q in shared memory, dP double-buffered
             make_tmap_sw(&m.a128, f.q, W, f.Nq, f.q_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
             make_tmap_sw(&m.a32, f.q, W, f.Nq, f.q_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
             const int smem8 = T::ROW_TILE + 10 * T::T_TILE + 256 + 1024;
@@ -1932,7 +2163,8 @@ extern "C" int mgv_dev_set_attn_dbg(int v) {
     return cudaMemcpyToSymbol(mgv::g_attn_dbg, &v, sizeof(int)) == cudaSuccess ? 0 : 1;
 }
 extern "C" int mgv_dev_set_dq_variant(int v) {
-    mgv::g_dq_variant = v;
+    mgv::g_dq_variant = v % 10;
+    mgv::g_dq_cw = v >= 10 ? 4 : 2;  // 12: v9 with 4 compute warps per lane group
     return 0;
 }
 extern "C" int mgv_dev_set_dkv_variant(int v) {
