@@ -386,21 +386,47 @@ void Model::alloc_adam_state() {
 // Multi-tensor AdamW (optim.cpp:7-24), one grid row per parameter: m, v, w updated in place, the bf16
 // operand copy refreshed.  Skipped entirely when the step's loss is not finite (FlowTrainer::step throws
 // before AdamW::update, flowtrain.cpp:276).
+__device__ __forceinline__ float adamw_one(float gi, float& mi, float& vi, float wi, float lr, float b1, float b2,
+                                           float eps, float wd, float inv_bc1, float inv_bc2) {
+    mi = b1 * mi + (1.0f - b1) * gi;
+    vi = b2 * vi + (1.0f - b2) * gi * gi;
+    const float mh = mi * inv_bc1, vh = vi * inv_bc2;
+    return wi - lr * (mh / (sqrtf(vh) + eps) + wd * wi);
+}
+
+// 16-byte accesses (the gradient / moment slices start at multiples of 64 elements, weights are cudaMalloc'd);
+// per-element arithmetic is the scalar formula, so results do not depend on the vector width.
 __global__ void adamw_kernel(const AdamParam* table, const float* grad, float* m, float* v, const double* loss_acc,
                              float lr, float b1, float b2, float eps, float wd, float inv_bc1, float inv_bc2) {
     if (!isfinite(*loss_acc)) return;
     const AdamParam q = table[blockIdx.y];
-    const float* g = grad + q.off;
-    float* mm = m + q.off;
-    float* vv = v + q.off;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < q.n; e += (int64_t)gridDim.x * blockDim.x) {
-        const float gi = g[e];
-        const float mi = b1 * mm[e] + (1.0f - b1) * gi;
-        const float vi = b2 * vv[e] + (1.0f - b2) * gi * gi;
-        mm[e] = mi;
-        vv[e] = vi;
-        const float mh = mi * inv_bc1, vh = vi * inv_bc2;
-        const float w = q.w[e] - lr * (mh / (sqrtf(vh) + eps) + wd * q.w[e]);
+    const float4* g4 = reinterpret_cast<const float4*>(grad + q.off);
+    float4* m4 = reinterpret_cast<float4*>(m + q.off);
+    float4* v4 = reinterpret_cast<float4*>(v + q.off);
+    float4* w4 = reinterpret_cast<float4*>(q.w);
+    const int64_t n4 = q.n / 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n4; e += stride) {
+        const float4 g = g4[e];
+        float4 mm = m4[e], vv = v4[e], w = w4[e];
+        w.x = adamw_one(g.x, mm.x, vv.x, w.x, lr, b1, b2, eps, wd, inv_bc1, inv_bc2);
+        w.y = adamw_one(g.y, mm.y, vv.y, w.y, lr, b1, b2, eps, wd, inv_bc1, inv_bc2);
+        w.z = adamw_one(g.z, mm.z, vv.z, w.z, lr, b1, b2, eps, wd, inv_bc1, inv_bc2);
+        w.w = adamw_one(g.w, mm.w, vv.w, w.w, lr, b1, b2, eps, wd, inv_bc1, inv_bc2);
+        m4[e] = mm;
+        v4[e] = vv;
+        w4[e] = w;
+        if (q.wb) {
+            __nv_bfloat162* b2p = reinterpret_cast<__nv_bfloat162*>(q.wb + 4 * e);
+            b2p[0] = __floats2bfloat162_rn(w.x, w.y);
+            b2p[1] = __floats2bfloat162_rn(w.z, w.w);
+        }
+    }
+    for (int64_t e = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < q.n; e += stride) {  // tail
+        float mi = m[q.off + e], vi = v[q.off + e];
+        const float w = adamw_one(grad[q.off + e], mi, vi, q.w[e], lr, b1, b2, eps, wd, inv_bc1, inv_bc2);
+        m[q.off + e] = mi;
+        v[q.off + e] = vi;
         q.w[e] = w;
         if (q.wb) q.wb[e] = __float2bfloat16_rn(w);
     }
@@ -1156,7 +1182,7 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
         const double bc2 = 1.0 - std::pow(adam_.b2, static_cast<double>(adam_.step));
         int64_t maxn = 0;
         for (auto* q : sorted_) maxn = std::max(maxn, q->numel);
-        const dim3 grid(static_cast<unsigned>(std::min<int64_t>((maxn + 255) / 256, 1184)),
+        const dim3 grid(static_cast<unsigned>(std::min<int64_t>((maxn / 4 + 255) / 256, 592)),
                         static_cast<unsigned>(sorted_.size()));
         prof_.begin("adamw", s);
         adamw_kernel<<<grid, 256, 0, s>>>(static_cast<const AdamParam*>(param_table_), grad_buf_, opt_m_, opt_v_,
