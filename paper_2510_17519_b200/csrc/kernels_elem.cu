@@ -131,8 +131,27 @@ __global__ void convert_f32_kernel(const float* src, int64_t n, T* dst) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
         dst[e] = to_t<T>(src[e]);
 }
+// 8 elements per thread (2 x 16-byte loads, one 16-byte bf16 store) when both pointers are 16-byte aligned
+__global__ void convert_f32_bf16_vec8(const float4* src, int64_t n8, uint4* dst) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n8; e += (int64_t)gridDim.x * blockDim.x) {
+        const float4 a = src[2 * e], b = src[2 * e + 1];
+        const __nv_bfloat162 p0 = __floats2bfloat162_rn(a.x, a.y), p1 = __floats2bfloat162_rn(a.z, a.w),
+                             p2 = __floats2bfloat162_rn(b.x, b.y), p3 = __floats2bfloat162_rn(b.z, b.w);
+        dst[e] = make_uint4(*reinterpret_cast<const uint32_t*>(&p0), *reinterpret_cast<const uint32_t*>(&p1),
+                            *reinterpret_cast<const uint32_t*>(&p2), *reinterpret_cast<const uint32_t*>(&p3));
+    }
+}
 template <class T>
 void convert_f32(const float* src, int64_t n, T* dst, cudaStream_t s) {
+    if constexpr (is_bf16<T>()) {
+        if (n % 8 == 0 && (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) % 16 == 0) {
+            convert_f32_bf16_vec8<<<grid_for(n / 8), 256, 0, s>>>(reinterpret_cast<const float4*>(src), n / 8,
+                                                                 reinterpret_cast<uint4*>(dst));
+            ::mgv::note_launch();
+            MGV_CUDA(cudaGetLastError());
+            return;
+        }
+    }
     convert_f32_kernel<T><<<grid_for(n), 256, 0, s>>>(src, n, dst); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
@@ -1292,7 +1311,7 @@ __global__ void __launch_bounds__(RT) gate_bwd_vec(const float* dX, const bf* y,
 
 // rms backward; MODE 0: dn = dA (1 + sc[u]), partials d shift / d scale (grouped); MODE 1: dn = dA g, partial d gain
 template <int MODE>
-__global__ void __launch_bounds__(RT) rms_bwd_vec(const bf* dA, const float* X, const float* rs, const float* table,
+__global__ void __launch_bounds__(RT, 2) rms_bwd_vec(const bf* dA, const float* X, const float* rs, const float* table,
                                                   int64_t tld, int sc_off, const int32_t* mod_id, int n_u,
                                                   const float* g, int N, int H, float* dX, int accumulate,
                                                   float* part_a, float* part_b) {
