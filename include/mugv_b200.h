@@ -15,8 +15,8 @@
  *   mgv_predict_velocity     dit::predict_velocity                  proj/include/mugv/dit.hpp:104-106
  *   mgv_dit_forward          dit::dit_forward                       proj/include/mugv/dit.hpp:94-95
  *                            (dit_forward_batch, dit.hpp:98-100, is a loop of this call)
- *   mgv_flow_step            flow::FlowTrainer::step minus          proj/include/mugv/flowtrain.hpp:134-151
- *                            the AdamW update (loss, grad_norm, grads)  proj/src/flowtrain.cpp:257-289
+ *   mgv_flow_step            flow::FlowTrainer::step: loss, backward, proj/include/mugv/flowtrain.hpp:134-151
+ *                            grad_norm, AdamW (mgv_ctx_set_adamw)   proj/src/flowtrain.cpp:257-289
  *   mgv_flow_loss            flow::flow_loss                        proj/include/mugv/flowtrain.hpp:26
  *   mgv_latent_rows          dit::latent_rows                       proj/include/mugv/dit.hpp:58
  *   mgv_rows_to_grid         dit::rows_to_grid                      proj/include/mugv/dit.hpp:62
