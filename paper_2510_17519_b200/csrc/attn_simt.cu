@@ -295,9 +295,41 @@ void attn_bwd_simt(const AttnBwdProblem& p, cudaStream_t s) {
     MGV_CUDA(cudaGetLastError());
 }
 
+// bf16, head_dim % 8 == 0, 16-byte aligned rows: a warp per (query, head), one 16-byte load per lane per operand
+__global__ void attn_bwd_dvec_vec_kernel(AttnBwdProblem p) {
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+    const int lane = threadIdx.x & 31;
+    const int hd = p.f.hd;
+    if (w >= (int64_t)p.f.Nq * p.f.heads) return;
+    const int h = static_cast<int>(w % p.f.heads);
+    const int64_t q = w / p.f.heads;
+    float acc = 0.0f;
+    for (int c = lane; c < hd / 8; c += 32) {
+        const uint4 a = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.dO) + q * p.do_ld + h * hd + 8 * c);
+        const uint4 b = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.f.o) + q * p.f.o_ld + h * hd + 8 * c);
+        const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&aw[j]));
+            const float2 fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&bw[j]));
+            acc = fmaf(fa.x, fb.x, acc);
+            acc = fmaf(fa.y, fb.y, acc);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffff, acc, o);
+    if (lane == 0) p.Dvec[(int64_t)h * lse_stride(p.f) + q] = acc;
+}
+
 void attn_bwd_dvec(const AttnBwdProblem& p, cudaStream_t s) {
     const int64_t rows = (int64_t)p.f.Nq * p.f.heads;
-    attn_bwd_dvec_kernel<__nv_bfloat16><<<(int)((rows * 32 + 255) / 256), 256, 0, s>>>(p); ::mgv::note_launch();
+    const bool vec = p.f.hd % 8 == 0 && p.do_ld % 8 == 0 && p.f.o_ld % 8 == 0 &&
+                     (reinterpret_cast<uintptr_t>(p.dO) | reinterpret_cast<uintptr_t>(p.f.o)) % 16 == 0;
+    if (vec)
+        attn_bwd_dvec_vec_kernel<<<(int)((rows * 32 + 255) / 256), 256, 0, s>>>(p);
+    else
+        attn_bwd_dvec_kernel<__nv_bfloat16><<<(int)((rows * 32 + 255) / 256), 256, 0, s>>>(p);
+    ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 

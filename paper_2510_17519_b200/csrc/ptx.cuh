@@ -41,8 +41,12 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef MGV_MBAR_HINT
+#define MGV_MBAR_HINT 1000000
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t addr = smem_u32(bar);
+#if MGV_MBAR_HINT > 0
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
         "LAB_WAIT:\n\t"
@@ -50,8 +54,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "@P1 bra.uni DONE;\n\t"
         "bra.uni LAB_WAIT;\n\t"
         "DONE:\n\t}" ::"r"(addr),
-        "r"(parity), "r"(1000000)
+        "r"(parity), "r"(MGV_MBAR_HINT)
         : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra.uni DONE;\n\t"
+        "bra.uni LAB_WAIT;\n\t"
+        "DONE:\n\t}" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+#endif
 }
 
 // ---------------------------------------------------------------- TMA
