@@ -19,6 +19,9 @@
  *                            grad_norm, AdamW (mgv_ctx_set_adamw)   proj/src/flowtrain.cpp:257-289
  *   mgv_flow_loss            flow::flow_loss                        proj/include/mugv/flowtrain.hpp:26
  *   mgv_latent_rows          dit::latent_rows                       proj/include/mugv/dit.hpp:58
+ *   mgv_patchify             dit::patchify                          proj/include/mugv/dit.hpp:86-87
+ *   mgv_unpatchify           dit::unpatchify                        proj/include/mugv/dit.hpp:89-90
+ *   mgv_global_embed         dit::global_embed                      proj/include/mugv/dit.hpp:83-84
  *   mgv_rows_to_grid         dit::rows_to_grid                      proj/include/mugv/dit.hpp:62
  *   mgv_ckpt_load / _read    mugv::load_checkpoint                  proj/include/mugv/params.hpp:60, params.cpp:128-225
  *   mgv_ckpt_save            mugv::save_checkpoint                  proj/include/mugv/params.hpp:59, params.cpp:92-126
@@ -140,6 +143,20 @@ mgv_status mgv_predict_velocity(mgv_ctx* ctx, const double* rows, int64_t N, con
 mgv_status mgv_dit_forward(mgv_ctx* ctx, const double* tokens, int64_t N, const int32_t* coords,
                            const int64_t dims[3], const double* text, int64_t L, const double* timesteps, double fps,
                            double* out);
+
+/* dit::patchify: (U, h, w, C) latent grid -> tokens (N x hidden) = latent_rows(grid) W_patch^T + b_patch, and
+ * the N x 3 coords.  DimensionError for odd h / w or C != c_z (dit.cpp:336-345). */
+mgv_status mgv_patchify(mgv_ctx* ctx, const double* grid, int64_t U, int64_t h, int64_t w, int64_t C, double* tokens,
+                        int32_t* coords);
+/* dit::unpatchify: tokens (N x hidden) on coords of a (U, H', W') grid -> (U, 2H', 2W', c_z) grid of the output head
+ * W_out tokens + b_out (dit.cpp:347-359). */
+mgv_status mgv_unpatchify(mgv_ctx* ctx, const double* tokens, int64_t N, const int32_t* coords, const int64_t dims[3],
+                          double* grid);
+/* dit::global_embed: g (N x hidden) = gmlp(sinusoid(1000 tau)) + gmlp(sinusoid(fps)) per token, and (if not NULL)
+ * block_scales (depth x hidden) = the per-block gscale parameters (dit.cpp:257-265).  InputError for tau outside
+ * [0, 1]. */
+mgv_status mgv_global_embed(mgv_ctx* ctx, const double* timesteps, int64_t N, double fps, double* g,
+                            double* block_scales);
 
 /* FlowTrainer::step forward + backward over n local samples (global_batch = n * world).
  * loss: mean of per-sample masked flow losses; grad_norm: sqrt of the sum of squared gradient entries;

@@ -187,6 +187,12 @@ def declare(L):
     L.mgv_params_upload_ckpt.restype = I
     L.mgv_params_save.argtypes = [P, CP, I, I64, P, P]
     L.mgv_params_save.restype = I
+    L.mgv_patchify.argtypes = [P, P, I64, I64, I64, I64, P, P]
+    L.mgv_patchify.restype = I
+    L.mgv_unpatchify.argtypes = [P, P, I64, P, P, P]
+    L.mgv_unpatchify.restype = I
+    L.mgv_global_embed.argtypes = [P, P, I64, D, P, P]
+    L.mgv_global_embed.restype = I
     L.mgv_flow_errors.argtypes = [P, I64, P, P]
     L.mgv_flow_errors.restype = I
     L.mgv_flow_step_weighted.argtypes = [P, I64, P, P, P, ctypes.POINTER(D), ctypes.POINTER(D), P]
@@ -224,6 +230,7 @@ EXPORTS = ["mgv_ctx_create", "mgv_ctx_destroy", "mgv_last_error", "mgv_ctx_set_s
            "mgv_ckpt_name", "mgv_ckpt_dtype", "mgv_ckpt_rank", "mgv_ckpt_shape", "mgv_ckpt_numel", "mgv_ckpt_find",
            "mgv_ckpt_read", "mgv_ckpt_meta_count", "mgv_ckpt_meta_key", "mgv_ckpt_meta_value", "mgv_ckpt_save",
            "mgv_params_upload_ckpt", "mgv_params_save",
+           "mgv_patchify", "mgv_unpatchify", "mgv_global_embed",
            "mgv_flow_errors", "mgv_flow_step_weighted", "mgv_post_validate", "mgv_post_state_create",
            "mgv_post_state_destroy", "mgv_post_plan_pos", "mgv_post_last_error", "mgv_post_train_step",
            "mgv_post_pref_loss", "mgv_dpo_from_errors", "mgv_kto_from_rewards"]
@@ -702,6 +709,33 @@ class Context:
         self._check(self._L.mgv_rows_to_grid(self.h, r.ctypes.data, co.ctypes.data, r.shape[0], dm, int(C),
                                              out.ctypes.data))
         return out
+
+    def patchify(self, grid):
+        """dit::patchify: (U, h, w, C) grid -> (tokens (N, hidden), coords (N, 3))."""
+        g = _f64(grid)
+        U, h, w, C = g.shape
+        N = U * (h // 2) * (w // 2)
+        tok = np.empty((N, self.cfg.hidden))
+        coords = np.empty((N, 3), dtype=np.int32)
+        self._check(self._L.mgv_patchify(self.h, g.ctypes.data, U, h, w, C, tok.ctypes.data, coords.ctypes.data))
+        return tok, coords
+
+    def unpatchify(self, tokens, coords, dims):
+        """dit::unpatchify: tokens (N, hidden) on coords of dims (U, H', W') -> (U, 2H', 2W', c_z)."""
+        t = _f64(tokens)
+        co = np.ascontiguousarray(coords, dtype=np.int32)
+        dm = (I64 * 3)(*[int(x) for x in dims])
+        out = np.empty((int(dims[0]), 2 * int(dims[1]), 2 * int(dims[2]), self.cfg.c_z))
+        self._check(self._L.mgv_unpatchify(self.h, t.ctypes.data, t.shape[0], co.ctypes.data, dm, out.ctypes.data))
+        return out
+
+    def global_embed(self, timesteps, fps=8.0):
+        """dit::global_embed: (g (N, hidden), block_scales (depth, hidden))."""
+        ts = _f64(timesteps)
+        g = np.empty((ts.shape[0], self.cfg.hidden))
+        bs = np.empty((self.cfg.depth, self.cfg.hidden))
+        self._check(self._L.mgv_global_embed(self.h, ts.ctypes.data, ts.shape[0], fps, g.ctypes.data, bs.ctypes.data))
+        return g, bs
 
     def flow_errors(self, recs):
         """mgv_flow_errors: post::flow_error of each (FlowSample, text, fps), forward only."""

@@ -171,6 +171,19 @@ mgv_status mgv_dit_forward(mgv_ctx* ctx, const double* tokens, int64_t N, const 
     return guard(ctx, [&] { ctx->model->dit_forward(tokens, N, coords, dims, text, L, timesteps, fps, out); });
 }
 
+mgv_status mgv_patchify(mgv_ctx* ctx, const double* grid, int64_t U, int64_t h, int64_t w, int64_t C, double* tokens,
+                        int32_t* coords) {
+    return guard(ctx, [&] { ctx->model->patchify(grid, U, h, w, C, tokens, coords); });
+}
+mgv_status mgv_unpatchify(mgv_ctx* ctx, const double* tokens, int64_t N, const int32_t* coords, const int64_t dims[3],
+                          double* grid) {
+    return guard(ctx, [&] { ctx->model->unpatchify(tokens, N, coords, dims, grid); });
+}
+mgv_status mgv_global_embed(mgv_ctx* ctx, const double* timesteps, int64_t N, double fps, double* g,
+                            double* block_scales) {
+    return guard(ctx, [&] { ctx->model->global_embed_host(timesteps, N, fps, g, block_scales); });
+}
+
 mgv_status mgv_flow_step(mgv_ctx* ctx, int64_t n, const mgv_flow_sample* samples, const double* text, int64_t L,
                          double fps, double* loss, double* grad_norm, double* const* grads_out,
                          double* const* velocity_out) {

@@ -1489,6 +1489,130 @@ void Model::value_forward(const double* in, int64_t N, const int32_t* coords, co
     MGV_CUDA(cudaStreamSynchronize(s));
 }
 
+// ------------------------------------------------------------------ boundary helpers (dit.cpp:257-265, 336-359)
+void Model::patchify(const double* grid, int64_t U, int64_t h, int64_t w_, int64_t C, double* tokens,
+                     int32_t* coords) {
+    MGV_CUDA(cudaSetDevice(device_));
+    if (!have_params_) throw InputError("no parameters uploaded");
+    if (!grid || !tokens || !coords) throw InputError("null argument");
+    if (U < 1 || h < 1 || w_ < 1 || C < 1) throw DimensionError("latent grid must be (U, h, w, C)");
+    if (h % 2 != 0 || w_ % 2 != 0) throw DimensionError("patchify needs even spatial dims");  // dit.cpp:95
+    if (C != cfg_.c_z) throw DimensionError("latent channels do not match c_z " + std::to_string(cfg_.c_z));
+    cudaStream_t s = stream_;
+    const int64_t H = cfg_.H(), D = cfg_.D(), N = U * (h / 2) * (w_ / 2);
+    double *dg = nullptr, *dr = nullptr, *dout = nullptr;
+    float *r32 = nullptr, *o32 = nullptr;
+    int32_t* dc = nullptr;
+    MGV_CUDA(cudaMallocAsync(&dg, sizeof(double) * N * D, s));
+    MGV_CUDA(cudaMallocAsync(&dr, sizeof(double) * N * D, s));
+    MGV_CUDA(cudaMallocAsync(&dout, sizeof(double) * N * H, s));
+    MGV_CUDA(cudaMallocAsync(&r32, sizeof(float) * N * D, s));
+    MGV_CUDA(cudaMallocAsync(&o32, sizeof(float) * N * H, s));
+    MGV_CUDA(cudaMallocAsync(&dc, sizeof(int32_t) * 3 * N, s));
+    MGV_CUDA(cudaMemcpyAsync(dg, grid, sizeof(double) * N * D, cudaMemcpyHostToDevice, s));
+    latent_rows_gather(dg, int(U), int(h), int(w_), int(C), dr, dc, s);
+    f64_to_f32_bf16<<<grid_of(N * D), 256, 0, s>>>(dr, N * D, r32, nullptr);
+    note_launch();
+    gemm(false, Mat{r32, D, Major::K}, Mat{P("dit.patch.w").f32, D, Major::K}, int(N), int(H), int(D),
+         EpiF32{o32, H, P("dit.patch.b").f32, 1.0f, 0, int(N), int(H)}, s);  // dit.cpp:343
+    f32_to_f64<<<grid_of(N * H), 256, 0, s>>>(o32, N * H, dout);
+    note_launch();
+    MGV_CUDA(cudaMemcpyAsync(tokens, dout, sizeof(double) * N * H, cudaMemcpyDeviceToHost, s));
+    MGV_CUDA(cudaMemcpyAsync(coords, dc, sizeof(int32_t) * 3 * N, cudaMemcpyDeviceToHost, s));
+    for (void* q : {static_cast<void*>(dg), static_cast<void*>(dr), static_cast<void*>(dout), static_cast<void*>(r32),
+                    static_cast<void*>(o32), static_cast<void*>(dc)})
+        MGV_CUDA(cudaFreeAsync(q, s));
+    MGV_CUDA(cudaStreamSynchronize(s));
+}
+
+void Model::unpatchify(const double* tokens, int64_t N, const int32_t* coords, const int64_t dims[3], double* grid) {
+    MGV_CUDA(cudaSetDevice(device_));
+    if (!have_params_) throw InputError("no parameters uploaded");
+    if (!tokens || !coords || !dims || !grid) throw InputError("null argument");
+    if (N < 1 || N != dims[0] * dims[1] * dims[2]) throw DimensionError("token coords do not match the grid dims");
+    cudaStream_t s = stream_;
+    const int64_t H = cfg_.H(), D = cfg_.D(), C = cfg_.c_z;
+    double *dt = nullptr, *dr = nullptr, *dg = nullptr;
+    float *t32 = nullptr, *r32 = nullptr;
+    int32_t *dc = nullptr, *seen = nullptr, *st = nullptr;
+    MGV_CUDA(cudaMallocAsync(&dt, sizeof(double) * N * H, s));
+    MGV_CUDA(cudaMallocAsync(&dr, sizeof(double) * N * D, s));
+    MGV_CUDA(cudaMallocAsync(&dg, sizeof(double) * N * D, s));
+    MGV_CUDA(cudaMallocAsync(&t32, sizeof(float) * N * H, s));
+    MGV_CUDA(cudaMallocAsync(&r32, sizeof(float) * N * D, s));
+    MGV_CUDA(cudaMallocAsync(&dc, sizeof(int32_t) * 3 * N, s));
+    MGV_CUDA(cudaMallocAsync(&seen, sizeof(int32_t) * N, s));
+    MGV_CUDA(cudaMallocAsync(&st, sizeof(int32_t), s));
+    MGV_CUDA(cudaMemcpyAsync(dt, tokens, sizeof(double) * N * H, cudaMemcpyHostToDevice, s));
+    MGV_CUDA(cudaMemcpyAsync(dc, coords, sizeof(int32_t) * 3 * N, cudaMemcpyHostToDevice, s));
+    f64_to_f32_bf16<<<grid_of(N * H), 256, 0, s>>>(dt, N * H, t32, nullptr);
+    note_launch();
+    gemm(false, Mat{t32, H, Major::K}, Mat{P("dit.out.w").f32, H, Major::K}, int(N), int(D), int(H),
+         EpiF32{r32, D, P("dit.out.b").f32, 1.0f, 0, int(N), int(D)}, s);  // dit.cpp:355
+    f32_to_f64<<<grid_of(N * D), 256, 0, s>>>(r32, N * D, dr);
+    note_launch();
+    MGV_CUDA(cudaMemsetAsync(dg, 0, sizeof(double) * N * D, s));
+    rows_to_grid_scatter(dr, dc, int(N), int(dims[0]), int(dims[1]), int(dims[2]), int(C), dg, seen, st, s);
+    int32_t status = 0;
+    MGV_CUDA(cudaMemcpyAsync(&status, st, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    MGV_CUDA(cudaMemcpyAsync(grid, dg, sizeof(double) * N * D, cudaMemcpyDeviceToHost, s));
+    for (void* q : {static_cast<void*>(dt), static_cast<void*>(dr), static_cast<void*>(dg), static_cast<void*>(t32),
+                    static_cast<void*>(r32), static_cast<void*>(dc), static_cast<void*>(seen), static_cast<void*>(st)})
+        MGV_CUDA(cudaFreeAsync(q, s));
+    MGV_CUDA(cudaStreamSynchronize(s));
+    if (status == 1) throw DimensionError("token coord outside the grid");  // dit.cpp:129-130
+    if (status == 2) throw DimensionError("duplicate token coord");         // dit.cpp:132
+}
+
+void Model::global_embed_host(const double* tau, int64_t N, double fps, double* g, double* block_scales) {
+    MGV_CUDA(cudaSetDevice(device_));
+    if (!have_params_) throw InputError("no parameters uploaded");
+    if (!tau || !g || N < 1) throw InputError("need one timestep per token");
+    cudaStream_t s = stream_;
+    const int64_t H = cfg_.H();
+    // unique timesteps (dit.cpp:239-242 validates each); g rows depend only on their timestep
+    std::vector<double> uniq;
+    std::vector<int32_t> mid(static_cast<size_t>(N));
+    std::unordered_map<uint64_t, int> seen;
+    for (int64_t i = 0; i < N; ++i) {
+        if (!(tau[i] >= 0.0 && tau[i] <= 1.0)) throw InputError("timestep outside [0, 1]");
+        uint64_t key;
+        std::memcpy(&key, &tau[i], sizeof(key));
+        if (tau[i] == 0.0) key = 0;
+        auto it = seen.find(key);
+        if (it == seen.end()) {
+            it = seen.emplace(key, static_cast<int>(uniq.size())).first;
+            uniq.push_back(tau[i]);
+        }
+        mid[static_cast<size_t>(i)] = it->second;
+    }
+    const int n_u = static_cast<int>(uniq.size());
+    double *dtau = nullptr, *phi = nullptr, *z_in = nullptr, *h_in = nullptr, *dgu = nullptr;
+    MGV_CUDA(cudaMallocAsync(&dtau, sizeof(double) * n_u, s));
+    MGV_CUDA(cudaMallocAsync(&phi, sizeof(double) * (n_u + 1) * 32, s));
+    MGV_CUDA(cudaMallocAsync(&z_in, sizeof(double) * (n_u + 1) * H, s));
+    MGV_CUDA(cudaMallocAsync(&h_in, sizeof(double) * (n_u + 1) * H, s));
+    MGV_CUDA(cudaMallocAsync(&dgu, sizeof(double) * n_u * H, s));
+    MGV_CUDA(cudaMemcpyAsync(dtau, uniq.data(), sizeof(double) * n_u, cudaMemcpyHostToDevice, s));
+    ::mgv::global_embed(dtau, n_u, fps, P("dit.gmlp.in.w").f32, P("dit.gmlp.in.b").f32, P("dit.gmlp.out.w").f32,
+                        P("dit.gmlp.out.b").f32, int(H), phi, z_in, h_in, dgu, s);
+    std::vector<double> gu(static_cast<size_t>(n_u * H));
+    MGV_CUDA(cudaMemcpyAsync(gu.data(), dgu, sizeof(double) * n_u * H, cudaMemcpyDeviceToHost, s));
+    for (void* q : {static_cast<void*>(dtau), static_cast<void*>(phi), static_cast<void*>(z_in),
+                    static_cast<void*>(h_in), static_cast<void*>(dgu)})
+        MGV_CUDA(cudaFreeAsync(q, s));
+    MGV_CUDA(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < N; ++i)
+        std::memcpy(g + i * H, gu.data() + static_cast<size_t>(mid[static_cast<size_t>(i)]) * H, sizeof(double) * H);
+    if (block_scales) {  // the per-block gscale parameters (dit.cpp:263)
+        for (int64_t i = 0; i < cfg_.depth; ++i) {
+            for (size_t k = 0; k < sorted_.size(); ++k)
+                if (sorted_[k]->name == blk(static_cast<int>(i), "gscale"))
+                    download_param(static_cast<int64_t>(k), block_scales + i * H);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ sampler (flowtrain.cpp:111-172)
 // x += coef * v in fp64 (the reference's Euler state is fp64), then impose: conditioned rows <- latents
 __global__ void euler_impose_kernel(double* x, const float* v, int64_t N, int64_t D, double coef,

@@ -143,6 +143,11 @@ public:
                           const double* text, int64_t L, const double* tau, double fps, double* out);
     void dit_forward(const double* tokens, int64_t N, const int32_t* coords, const int64_t dims[3],
                      const double* text, int64_t L, const double* tau, double fps, double* out);
+    // dit::patchify / unpatchify / global_embed (dit.hpp:83-90): the projections at either end of the block
+    // stack and the timestep/fps embedding, from the device weights (fp32 masters, IEEE-fp32 GEMMs)
+    void patchify(const double* grid, int64_t U, int64_t h, int64_t w, int64_t C, double* tokens, int32_t* coords);
+    void unpatchify(const double* tokens, int64_t N, const int32_t* coords, const int64_t dims[3], double* grid);
+    void global_embed_host(const double* tau, int64_t N, double fps, double* g, double* block_scales);
     // forward_sample_rows / reverse_sample_rows (flowtrain.cpp:135-172): `steps` Euler steps of the
     // probability-flow ODE on device (direction -1: t 1 -> 0, x -= dt v; +1: t 0 -> 1, x += dt v),
     // conditioned rows re-imposed after every step.  cond / cond_latents may be null.
