@@ -100,29 +100,19 @@ mgv_status mgv_params_upload(mgv_ctx* ctx, const mgv_dit_cfg* cfg, int64_t n, co
 mgv_status mgv_params_upload_ckpt(mgv_ctx* ctx, const mgv_dit_cfg* cfg, const mgv_ckpt* ck) {
     return guard(ctx, [&] {
         if (!cfg || !ck) throw mgv::InputError("null argument");
-        // host copies in each payload's own width (the payload is little-endian and may be unaligned)
-        std::vector<std::vector<float>> f32s;
-        std::vector<std::vector<double>> f64s;
+        // the payloads go to the device straight from the loaded file: little-endian f32 / f64 arrays that
+        // cudaMemcpy reads at any alignment, so no host-side copy of the (possibly 10B-parameter) weights
+        static_assert(__BYTE_ORDER__ == __ORDER_LITTLE_ENDIAN__, "MUGVCKPT payloads are little-endian");
         std::vector<const char*> names;
         std::vector<const void*> data;
         std::vector<uint8_t> is_f32;
         std::vector<int64_t> numel;
-        f32s.reserve(ck->ck.entries.size());
-        f64s.reserve(ck->ck.entries.size());
         for (const mgv::CkptEntry& e : ck->ck.entries) {
             if (e.name.rfind("dit.", 0) != 0) continue;  // register_params(..., "dit.") (flowtrain.cpp:260)
             names.push_back(e.name.c_str());
             numel.push_back(e.numel);
             is_f32.push_back(e.dtype == mgv::kF32);
-            if (e.dtype == mgv::kF32) {
-                f32s.emplace_back(static_cast<size_t>(e.numel));
-                ck->ck.read_f32(e, f32s.back().data());
-                data.push_back(f32s.back().data());
-            } else {
-                f64s.emplace_back(static_cast<size_t>(e.numel));
-                ck->ck.read_f64(e, f64s.back().data());
-                data.push_back(f64s.back().data());
-            }
+            data.push_back(ck->ck.payload(e));
         }
         ctx->model->upload(to_cfg(cfg), static_cast<int64_t>(names.size()), names.data(), data.data(), is_f32.data(),
                            numel.data());
