@@ -31,6 +31,7 @@ namespace mgv {
 static int g_dkv_pair = 0;
 // 0 = v8 (default: V in TMEM, P^T in its own columns), 1 = v5 (K in TMEM, P^T / dS^T aliased)
 static int g_dkv_variant = 0;
+static int g_dkv_cw = 2;  // compute warps per TMEM lane group in the v8 dK/dV pass (2 or 4)
 // dQ pass variant: 2 = v9 (default: 128-key steps, Q and dO in shared memory), 0 = v7 (64-key steps, Q and dO
 // in TMEM, dP single-buffered), 1 = v8 (Q in shared memory, dP double-buffered)
 static int g_dq_variant = 2;
@@ -448,10 +449,11 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_tc_kernel(const __grid_co
 // overwrite, and the one shared-memory-operand product is the one whose loop has slack.  Staging only 128
 // of V's 144 columns in TMEM is what makes the 512-column budget close:
 //   S^T [0,64)  P^T [64,96)  dP^T|dS^T [96,160)  dV [160,160+HD)  dK [.., +HD)  V (bf16 pairs) [.., +64)
-template <int HD>
-__global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v8_kernel(const __grid_constant__ BwdMaps tm, AttnBwdProblem p,
-                                                                 float* part) {
+template <int HD, int CW>
+__global__ void __launch_bounds__(128 + 128 * CW, 1) attn_bwd_dkv_v8_kernel(const __grid_constant__ BwdMaps tm,
+                                                                           AttnBwdProblem p, float* part) {
     constexpr int BKV = 128, BQ = 64, NST = 5;
+    static_assert(CW == 2 || CW == 4, "2 or 4 compute warps per TMEM lane group");
     using T = BT<HD>;
     constexpr int VA = HD >= 128 ? 128 : HD;  // V columns staged in TMEM
     constexpr int VT = HD - VA;               // tail columns read from shared memory
@@ -496,11 +498,11 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v8_kernel(const __grid_co
             mbar_init(&qd_empty[i], 1);
         }
         mbar_init(s_full, 1);
-        mbar_init(s_empty, 8);
-        mbar_init(p_full, 8);
+        mbar_init(s_empty, 4 * CW);
+        mbar_init(p_full, 4 * CW);
         mbar_init(pv_done, 1);
         mbar_init(dp_full, 1);
-        mbar_init(ds_full, 8);
+        mbar_init(ds_full, 4 * CW);
         mbar_init(acc_done, 1);
         mbar_init(va_ready, 4);
         fence_barrier_init();
@@ -587,7 +589,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v8_kernel(const __grid_co
             tc_fence_after();
             if (lane == 0) ATR8(4, i);
             if (elect_one()) {
-                mma_tmem_split_x_t<HD, 32>(tmem + DK_COL, tmem + DP_COL, smem_u32(sQt + st * T::T_TILE), i > 0);
+                mma_tmem_split_x_t<HD, BQ / CW>(tmem + DK_COL, tmem + DP_COL, smem_u32(sQt + st * T::T_TILE), i > 0);
                 umma_commit(&qd_empty[st]);
                 if (i == nq - 1) umma_commit(acc_done);
             }
@@ -597,7 +599,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v8_kernel(const __grid_co
             if (lane == 0) ATR8(6, i);
         }
     } else if (warp >= 4) {
-        // two warps per TMEM lane group: warp hf handles query columns [32 hf, 32 hf + 32) of each tile
+        // CW warps per TMEM lane group: warp hf handles query columns [HQ hf, HQ hf + HQ) of each tile
         const int g = warp & 3, hf = (warp - 4) >> 2, row = g * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(g * 32) << 16;
         const int kv = k0 + row;
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v8_kernel(const __grid_co
             __syncwarp();
             if (lane == 0) mbar_arrive(va_ready);
         }
-        constexpr int HQ = BQ / 2;
+        constexpr int HQ = BQ / CW;
         for (int i = 0; i < nq; ++i) {
             const int st = i % NST;
             mbar_wait(&qd_full[st], (i / NST) & 1);  // lse / D rows of this tile have landed
@@ -618,7 +620,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v8_kernel(const __grid_co
             tc_fence_after();
             if (warp == 4 && lane == 0) ATR8(7, i);
             float s[HQ], dp[HQ];
-            if (g_attn_dbg & 1) {  // timing experiment: barriers only, no TMEM traffic or math
+            if (CW == 2 && (g_attn_dbg & 1)) {  // timing experiment: barriers only, no TMEM traffic or math
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(s_empty);
@@ -630,7 +632,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v8_kernel(const __grid_co
                 if (lane == 0) mbar_arrive(ds_full);
                 continue;
             }
-            tmem_ld32(tmem + lane_base + S_COL + hf * HQ, reinterpret_cast<uint32_t*>(s));
+            tmem_ldn<HQ>(tmem + lane_base + S_COL + hf * HQ, s);
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
@@ -651,19 +653,19 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v8_kernel(const __grid_co
                 mbar_wait(pv_done, (i - 1) & 1);  // dV(i-1) has read P^T(i-1)
                 tc_fence_after();
             }
-            tmem_st16(tmem + lane_base + P_COL + hf * (HQ / 2), pk);
+            tmem_stn<HQ / 2>(tmem + lane_base + P_COL + hf * (HQ / 2), pk);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full);
             mbar_wait(dp_full, i & 1);
             tc_fence_after();
-            tmem_ld32(tmem + lane_base + DP_COL + hf * HQ, reinterpret_cast<uint32_t*>(dp));
+            tmem_ldn<HQ>(tmem + lane_base + DP_COL + hf * HQ, dp);
             tmem_wait_ld();
 #pragma unroll
             for (int c = 0; c < HQ; c += 2)
                 pk[c / 2] = pack_bf16(s[c] * (dp[c] - Dq[c]), s[c + 1] * (dp[c + 1] - Dq[c + 1]));  // autodiff.cpp:820
-            tmem_st16(tmem + lane_base + DP_COL + hf * HQ, pk);
+            tmem_stn<HQ / 2>(tmem + lane_base + DP_COL + hf * HQ, pk);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
@@ -673,15 +675,19 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v8_kernel(const __grid_co
         tc_fence_after();
         const bool valid = kvv && nq > 0;
         if (part) {  // fp32 partial rows of this query split: [dV | dK]
-            const int64_t W = (int64_t)f.heads * HD;
-            float* prow = part + ((int64_t)blockIdx.z * f.Nk + (kvv ? kv : 0)) * 2 * W + (hf ? W : 0) + col;
-            store_acc_row_f32<HD>(tmem + lane_base + (hf ? DK_COL : DV_COL), prow, kvv);
-        } else if (hf == 0) {
-            store_acc_row<HD>(tmem + lane_base + DV_COL,
-                              static_cast<__nv_bfloat16*>(p.dv) + (int64_t)kv * p.dv_ld + col, valid);
-        } else {
-            store_acc_row<HD>(tmem + lane_base + DK_COL,
-                              static_cast<__nv_bfloat16*>(p.dk) + (int64_t)kv * p.dk_ld + col, valid);
+            if (hf < 2) {
+                const int64_t W = (int64_t)f.heads * HD;
+                float* prow = part + ((int64_t)blockIdx.z * f.Nk + (kvv ? kv : 0)) * 2 * W + (hf ? W : 0) + col;
+                store_acc_row_f32<HD>(tmem + lane_base + (hf ? DK_COL : DV_COL), prow, kvv);
+            }
+        } else {  // warps [0, CW/2) store dV, the others dK, each a share of the 16-column chunks
+            constexpr int NC = HD / 16, HALF = CW / 2;
+            const bool is_v = hf < HALF;
+            const int part_i = is_v ? hf : hf - HALF;
+            __nv_bfloat16* out = is_v ? static_cast<__nv_bfloat16*>(p.dv) + (int64_t)kv * p.dv_ld + col
+                                      : static_cast<__nv_bfloat16*>(p.dk) + (int64_t)kv * p.dk_ld + col;
+            store_acc_row<HD>(tmem + lane_base + (is_v ? DV_COL : DK_COL), out, valid, part_i * NC / HALF,
+                              (part_i + 1) * NC / HALF);
         }
     }
     tc_fence_before();
@@ -1969,7 +1975,9 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
         static bool set = false;
         if (!set) {
             MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_v8_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_v8_kernel<HD, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          smem8));
+            MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_v8_kernel<HD, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           smem8));
             set = true;
         }
@@ -2036,7 +2044,12 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
             if (g_dkv_variant == 1)
                 attn_bwd_dkv_tc_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem, s>>>(m, p, part);
             else
-                attn_bwd_dkv_v8_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem8, s>>>(m, p, part);
+                if (g_dkv_cw == 4)
+                    attn_bwd_dkv_v8_kernel<HD, 4><<<dim3((f.Nk + 127) / 128, f.heads, splits), 640, smem8, s>>>(m, p,
+                                                                                                          part);
+                else
+                    attn_bwd_dkv_v8_kernel<HD, 2><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem8, s>>>(m, p,
+                                                                                                          part);
         }
         ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
@@ -2168,7 +2181,8 @@ extern "C" int mgv_dev_set_dq_variant(int v) {
     return 0;
 }
 extern "C" int mgv_dev_set_dkv_variant(int v) {
-    mgv::g_dkv_variant = v;
+    mgv::g_dkv_variant = v % 10;
+    mgv::g_dkv_cw = v >= 10 ? 4 : 2;  // 10: v8 with 4 compute warps per lane group
     return 0;
 }
 
