@@ -285,7 +285,8 @@ void Model::set_dp(int rank, int world, const uint8_t id[128]) {
     }
     rank_ = rank;
     world_ = world;
-    if (world == 1) return;
+    if (world == 1 && !id) return;  // world 1 with an id: a one-rank communicator (exercises the NCCL path)
+    if (!id) throw InputError("data parallelism needs the NCCL unique id");
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
     MGV_CUDA(cudaSetDevice(device_));
@@ -1168,7 +1169,7 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
         return;
     }
     tp_allreduce_grads(s);
-    if (world_ > 1) {
+    if (comm_) {
         prof_.begin("allreduce", s);
         MGV_NCCL(ncclAllReduce(grad_buf_, grad_buf_, grad_numel_, ncclFloat, ncclSum, comm_, s));
         MGV_NCCL(ncclAllReduce(w.scal, w.scal, 1, ncclDouble, ncclSum, comm_, s));

@@ -84,3 +84,25 @@ def test_bf16_determinism(ctxs):
     assert a["loss"] == b["loss"] and a["grad_norm"] == b["grad_norm"]
     for k in a["grads"]:
         assert np.array_equal(a["grads"][k], b["grads"][k]), k
+
+
+def test_dp_nccl_one_rank_matches_single():
+    """The data-parallel path through NCCL (one-rank communicator: ncclCommInitRank + the gradient / loss
+    all-reduces of every step) gives bit-identical loss, gradient norm, gradients and AdamW weights."""
+    from paper_2510_17519_b200.capi import Context
+    cfg, P, text, samples = build_case("hd144", CASES["hd144"])
+    outs = []
+    for dp in (False, True):
+        c = Context(0, "bf16")
+        if dp:
+            c.set_dp(0, 1, Context.nccl_unique_id())
+        c.set_adamw(lr=1e-3, eps=1.0)
+        c.upload(to_cfg(cfg), P)
+        r = c.flow_step(to_samples(samples), text, 8.0, grads=True)
+        outs.append((r, c.download()))
+        c.close()
+    (a, wa), (b, wb) = outs
+    assert a["loss"] == b["loss"] and a["grad_norm"] == b["grad_norm"]
+    for k in a["grads"]:
+        assert np.array_equal(a["grads"][k], b["grads"][k]), k
+        assert np.array_equal(wa[k], wb[k]), k
