@@ -22,6 +22,8 @@
  *   mgv_patchify             dit::patchify                          proj/include/mugv/dit.hpp:86-87
  *   mgv_unpatchify           dit::unpatchify                        proj/include/mugv/dit.hpp:89-90
  *   mgv_global_embed         dit::global_embed                      proj/include/mugv/dit.hpp:83-84
+ *   mgv_tokenize             dit::tokenize                          proj/src/dit.cpp:193-211
+ *   mgv_text_embed           dit::text_embed                        proj/include/mugv/dit.hpp:63-72, dit.cpp:213-234
  *   mgv_rows_to_grid         dit::rows_to_grid                      proj/include/mugv/dit.hpp:62
  *   mgv_ckpt_load / _read    mugv::load_checkpoint                  proj/include/mugv/params.hpp:60, params.cpp:128-225
  *   mgv_ckpt_save            mugv::save_checkpoint                  proj/include/mugv/params.hpp:59, params.cpp:92-126
@@ -145,6 +147,15 @@ mgv_status mgv_dit_forward(mgv_ctx* ctx, const double* tokens, int64_t N, const 
                            const int64_t dims[3], const double* text, int64_t L, const double* timesteps, double fps,
                            double* out);
 
+/* dit::tokenize: FNV-1a 64 ids of the whitespace-separated words modulo vocab; returns the word count (ids holds
+ * the first min(count, cap)), -1 on bad arguments.  Host-only. */
+int64_t mgv_tokenize(const char* prompt, int64_t vocab, int64_t* ids, int64_t cap);
+/* dit::text_embed: truncate to max_len ids (*truncated = 1 when cut), look up rows of embed_table (vocab x text_dim;
+ * the "text.embed" parameter, or null_row "text.null" when empty), RMS-normalise each row on the device in the
+ * reference's fp64 order (bit-identical).  out: max(1, min(n, max_len)) x text_dim.  InputError for ids outside
+ * the vocabulary. */
+mgv_status mgv_text_embed(mgv_ctx* ctx, const int64_t* ids, int64_t n, const double* embed_table, int64_t vocab,
+                          const double* null_row, int64_t text_dim, int64_t max_len, double* out, int* truncated);
 /* dit::patchify: (U, h, w, C) latent grid -> tokens (N x hidden) = latent_rows(grid) W_patch^T + b_patch, and
  * the N x 3 coords.  DimensionError for odd h / w or C != c_z (dit.cpp:336-345). */
 mgv_status mgv_patchify(mgv_ctx* ctx, const double* grid, int64_t U, int64_t h, int64_t w, int64_t C, double* tokens,

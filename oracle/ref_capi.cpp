@@ -493,4 +493,36 @@ int ref_post_loss(void* pol, void* ref, const RefCfg* c, const char* tag, double
     });
 }
 
+// ---- text conditioning (dit.cpp:185-234) ----
+int64_t ref_tokenize(const char* prompt, int64_t vocab, int64_t* ids, int64_t cap) {
+    dit::DitConfig cfg;
+    cfg.text_vocab = vocab;
+    std::vector<int64_t> v = dit::tokenize(prompt, cfg);
+    for (int64_t k = 0; k < static_cast<int64_t>(v.size()) && k < cap; ++k) ids[k] = v[static_cast<size_t>(k)];
+    return static_cast<int64_t>(v.size());
+}
+// text_embed with text params {text.embed (vocab x D), text.null (1 x D)}; out (L x D); returns L or -1
+int64_t ref_text_embed(const int64_t* ids, int64_t n, const double* table, int64_t vocab, const double* null_row,
+                       int64_t D, int64_t max_len, double* out, int* truncated) {
+    int64_t L = -1;
+    guard([&] {
+        dit::DitConfig cfg;
+        cfg.text_vocab = vocab;
+        cfg.text_dim = D;
+        cfg.text_max_len = max_len;
+        ParameterSet tp;
+        Tensor t({vocab, D}), nl({1, D});
+        std::memcpy(t.data(), table, sizeof(double) * static_cast<size_t>(vocab * D));
+        std::memcpy(nl.data(), null_row, sizeof(double) * static_cast<size_t>(D));
+        tp.set("text.embed", std::move(t));
+        tp.set("text.null", std::move(nl));
+        std::vector<int64_t> v(ids, ids + n);
+        dit::TextEmbedding e = dit::text_embed(v, tp, cfg);
+        L = e.emb.dim(0);
+        std::memcpy(out, e.emb.data(), sizeof(double) * static_cast<size_t>(e.emb.numel()));
+        *truncated = e.truncated ? 1 : 0;
+    });
+    return L;
+}
+
 }  // extern "C"

@@ -187,6 +187,10 @@ def declare(L):
     L.mgv_params_upload_ckpt.restype = I
     L.mgv_params_save.argtypes = [P, CP, I, I64, P, P]
     L.mgv_params_save.restype = I
+    L.mgv_tokenize.argtypes = [ctypes.c_char_p, I64, P, I64]
+    L.mgv_tokenize.restype = I64
+    L.mgv_text_embed.argtypes = [P, P, I64, P, I64, P, I64, I64, P, ctypes.POINTER(I)]
+    L.mgv_text_embed.restype = I
     L.mgv_patchify.argtypes = [P, P, I64, I64, I64, I64, P, P]
     L.mgv_patchify.restype = I
     L.mgv_unpatchify.argtypes = [P, P, I64, P, P, P]
@@ -230,7 +234,7 @@ EXPORTS = ["mgv_ctx_create", "mgv_ctx_destroy", "mgv_last_error", "mgv_ctx_set_s
            "mgv_ckpt_name", "mgv_ckpt_dtype", "mgv_ckpt_rank", "mgv_ckpt_shape", "mgv_ckpt_numel", "mgv_ckpt_find",
            "mgv_ckpt_read", "mgv_ckpt_meta_count", "mgv_ckpt_meta_key", "mgv_ckpt_meta_value", "mgv_ckpt_save",
            "mgv_params_upload_ckpt", "mgv_params_save",
-           "mgv_patchify", "mgv_unpatchify", "mgv_global_embed",
+           "mgv_patchify", "mgv_unpatchify", "mgv_global_embed", "mgv_tokenize", "mgv_text_embed",
            "mgv_flow_errors", "mgv_flow_step_weighted", "mgv_post_validate", "mgv_post_state_create",
            "mgv_post_state_destroy", "mgv_post_plan_pos", "mgv_post_last_error", "mgv_post_train_step",
            "mgv_post_pref_loss", "mgv_dpo_from_errors", "mgv_kto_from_rewards"]
@@ -451,6 +455,15 @@ def _labels_c(labels):
     for i, (rec, desirable) in enumerate(labels):
         arr[i].sample, arr[i].desirable = rec.to_c(), int(bool(desirable))
     return arr
+
+
+def tokenize(prompt: str, vocab: int) -> np.ndarray:
+    """dit::tokenize (dit.cpp:193-211)."""
+    L = _lib()
+    n = L.mgv_tokenize(prompt.encode(), vocab, None, 0)
+    ids = np.empty(max(n, 1), dtype=np.int64)
+    L.mgv_tokenize(prompt.encode(), vocab, ids.ctypes.data, n)
+    return ids[:n]
 
 
 def dpo_from_errors(e_th_w, e_th_l, e_ref_w, e_ref_l, beta):
@@ -709,6 +722,19 @@ class Context:
         self._check(self._L.mgv_rows_to_grid(self.h, r.ctypes.data, co.ctypes.data, r.shape[0], dm, int(C),
                                              out.ctypes.data))
         return out
+
+    def text_embed(self, ids, embed_table, null_row, max_len=64):
+        """dit::text_embed: (rows (L, text_dim), truncated)."""
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        tab = _f64(embed_table)
+        nul = _f64(null_row).ravel()
+        L = max(1, min(len(ids), max_len))
+        out = np.empty((L, tab.shape[1]))
+        tr = I()
+        self._check(self._L.mgv_text_embed(self.h, ids.ctypes.data if len(ids) else None, len(ids), tab.ctypes.data,
+                                           tab.shape[0], nul.ctypes.data, tab.shape[1], max_len, out.ctypes.data,
+                                           ctypes.byref(tr)))
+        return out, bool(tr.value)
 
     def patchify(self, grid):
         """dit::patchify: (U, h, w, C) grid -> (tokens (N, hidden), coords (N, 3))."""

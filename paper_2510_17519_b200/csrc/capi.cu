@@ -1,4 +1,6 @@
 // extern "C" boundary (include/mugv_b200.h): C types only, no exceptions cross it.
+#include <algorithm>
+#include <cctype>
 #include <cstring>
 #include <exception>
 #include <iterator>
@@ -13,6 +15,19 @@
 #include "capi_internal.h"
 
 namespace {
+// rmsnorm_rows (autodiff.cpp:686-701) of the looked-up text rows, one thread per row, the reference's
+// sequential fp64 order without contraction: bit-identical to text_embed (dit.cpp:213-234)
+__global__ void text_rms_kernel(const double* rows, int64_t L, int64_t D, double* out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= L) return;
+    const double* r = rows + i * D;
+    double ms = 0.0;
+    for (int64_t j = 0; j < D; ++j) ms = __dadd_rn(ms, __dmul_rn(r[j], r[j]));
+    ms = __ddiv_rn(ms, static_cast<double>(D));
+    const double iv = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(ms, 1e-6)));  // kNormEps (dit.cpp:13)
+    for (int64_t j = 0; j < D; ++j) out[i * D + j] = __dmul_rn(r[j], iv);
+}
+
 template <class F>
 mgv_status guard(mgv_ctx* ctx, F&& f) {
     if (!ctx) return MGV_ERR_INPUT;
@@ -159,6 +174,60 @@ mgv_status mgv_dit_forward(mgv_ctx* ctx, const double* tokens, int64_t N, const 
                            const int64_t dims[3], const double* text, int64_t L, const double* timesteps, double fps,
                            double* out) {
     return guard(ctx, [&] { ctx->model->dit_forward(tokens, N, coords, dims, text, L, timesteps, fps, out); });
+}
+
+int64_t mgv_tokenize(const char* prompt, int64_t vocab, int64_t* ids, int64_t cap) {
+    // dit::tokenize (dit.cpp:193-211): whitespace-split words, FNV-1a 64 of each, modulo the vocabulary
+    if (!prompt || vocab < 1) return -1;
+    int64_t n = 0;
+    size_t i = 0;
+    const std::string s(prompt);
+    while (i < s.size()) {
+        while (i < s.size() && std::isspace(static_cast<unsigned char>(s[i]))) ++i;
+        size_t j = i;
+        while (j < s.size() && !std::isspace(static_cast<unsigned char>(s[j]))) ++j;
+        if (j > i) {
+            uint64_t h = 1469598103934665603ull;
+            for (size_t k = i; k < j; ++k) {
+                h ^= static_cast<unsigned char>(s[k]);
+                h *= 1099511628211ull;
+            }
+            if (ids && n < cap) ids[n] = static_cast<int64_t>(h % static_cast<uint64_t>(vocab));
+            ++n;
+        }
+        i = j;
+    }
+    return n;
+}
+
+mgv_status mgv_text_embed(mgv_ctx* ctx, const int64_t* ids, int64_t n, const double* embed_table, int64_t vocab,
+                          const double* null_row, int64_t text_dim, int64_t max_len, double* out, int* truncated) {
+    return guard(ctx, [&] {
+        if (n < 0 || (n > 0 && !ids) || !embed_table || !null_row || !out || text_dim < 1 || max_len < 1)
+            throw mgv::InputError("bad text_embed arguments");
+        const int64_t use = std::min(n, max_len);  // truncate first (dit.cpp:225-229)
+        if (truncated) *truncated = n > max_len ? 1 : 0;
+        for (int64_t k = 0; k < use; ++k)
+            if (ids[k] < 0 || ids[k] >= vocab)
+                throw mgv::InputError("text id " + std::to_string(ids[k]) + " outside the vocabulary");  // :214-216
+        const int64_t L = use > 0 ? use : 1;  // empty -> the learned null row
+        std::vector<double> rows(static_cast<size_t>(L * text_dim));
+        for (int64_t k = 0; k < L; ++k)
+            std::memcpy(rows.data() + k * text_dim, use > 0 ? embed_table + ids[k] * text_dim : null_row,
+                        sizeof(double) * text_dim);
+        cudaStream_t s = ctx->model->stream();
+        double *dr = nullptr, *dout = nullptr;
+        MGV_CUDA(cudaMallocAsync(&dr, sizeof(double) * L * text_dim, s));
+        MGV_CUDA(cudaMallocAsync(&dout, sizeof(double) * L * text_dim, s));
+        MGV_CUDA(cudaMemcpyAsync(dr, rows.data(), sizeof(double) * L * text_dim, cudaMemcpyHostToDevice, s));
+        text_rms_kernel<<<static_cast<unsigned>((L + 63) / 64), 64, 0, s>>>(dr, L, text_dim, dout);
+        mgv::note_launch();
+        MGV_CUDA(cudaGetLastError());
+        MGV_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * L * text_dim, cudaMemcpyDeviceToHost, s));
+        MGV_CUDA(cudaFreeAsync(dr, s));
+        MGV_CUDA(cudaFreeAsync(dout, s));
+        MGV_CUDA(cudaStreamSynchronize(s));
+    });
 }
 
 mgv_status mgv_patchify(mgv_ctx* ctx, const double* grid, int64_t U, int64_t h, int64_t w, int64_t C, double* tokens,
