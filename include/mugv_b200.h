@@ -295,6 +295,13 @@ mgv_status mgv_post_train_step(mgv_post_state* st, const mgv_post_cfg* cfg, cons
 mgv_status mgv_post_pref_loss(mgv_ctx* policy, mgv_ctx* ref, const mgv_post_cfg* cfg, const char* tag,
                               int64_t n_pairs, const mgv_pref_pair* pairs, int64_t n_labels,
                               const mgv_labeled_sample* labels, uint64_t seed, double* loss);
+/* post::rdpo_pairs (posttrain.cpp:235-254) on the device sampler: winners[k] / losers[k] (N_k x 4c_z) for record k:
+ * winner = forward(reverse(rows)), loser = forward(fresh normals from Rng(seed), drawn record by record). */
+mgv_status mgv_rdpo_pairs(mgv_ctx* ctx, int64_t n, const mgv_sample_record* recs, int64_t steps, uint64_t seed,
+                          double* const* winners, double* const* losers);
+/* post::merge_weights (k normalised weights gamma^(k-1-i)) and post::anneal_lr (cosine decay), posttrain.cpp:51-94 */
+mgv_status mgv_merge_weights(int64_t k, double gamma, double* out);
+mgv_status mgv_anneal_lr(int64_t step, double lr_start, double lr_end, int64_t steps, double* out);
 /* scalar helpers: dpo_from_errors, kto_from_rewards (z0 NULL = batch mean) (posttrain.cpp:144-204) */
 double mgv_dpo_from_errors(double e_th_w, double e_th_l, double e_ref_w, double e_ref_l, double beta);
 mgv_status mgv_kto_from_rewards(int64_t n, const double* rewards, const uint8_t* desirable, double w_d, double w_u,

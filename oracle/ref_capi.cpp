@@ -525,4 +525,37 @@ int64_t ref_text_embed(const int64_t* ids, int64_t n, const double* table, int64
     return L;
 }
 
+// ---- post-training utilities (posttrain.cpp:51-94, 235-254) ----
+int ref_merge_weights(int64_t k, double gamma, double* out) {
+    return guard([&] {
+        std::vector<real> w = post::merge_weights(k, gamma);
+        for (int64_t i = 0; i < k; ++i) out[i] = w[static_cast<size_t>(i)];
+    });
+}
+int ref_anneal_lr(int64_t step, double lr_start, double lr_end, int64_t steps, double* out) {
+    return guard([&] {
+        post::AnnealConfig c;
+        c.lr_start = lr_start;
+        c.lr_end = lr_end;
+        c.steps = steps;
+        *out = post::anneal_lr(step, c);
+    });
+}
+// rdpo_pairs over n records (RefRecord) with the params handle h
+int ref_rdpo_pairs(void* h, const RefCfg* c, int64_t n, const RefRecord* recs, int64_t steps, uint64_t seed,
+                   double* const* winners, double* const* losers) {
+    return guard([&] {
+        auto* hh = static_cast<Handle*>(h);
+        auto cfg = to_cfg(c);
+        std::vector<post::SampleRecord> rs;
+        for (int64_t i = 0; i < n; ++i) rs.push_back(record_of(recs[i], cfg));
+        std::vector<post::PreferencePair> pairs = post::rdpo_pairs(rs, hh->p, cfg, steps, seed);
+        for (int64_t i = 0; i < n; ++i) {
+            const auto& p = pairs[static_cast<size_t>(i)];
+            std::memcpy(winners[i], p.winner.rows.data(), sizeof(double) * static_cast<size_t>(p.winner.rows.numel()));
+            std::memcpy(losers[i], p.loser.rows.data(), sizeof(double) * static_cast<size_t>(p.loser.rows.numel()));
+        }
+    });
+}
+
 }  // extern "C"

@@ -215,6 +215,12 @@ def declare(L):
     L.mgv_post_train_step.restype = I
     L.mgv_post_pref_loss.argtypes = [P, P, P, ctypes.c_char_p, I64, P, I64, P, ctypes.c_uint64, ctypes.POINTER(D)]
     L.mgv_post_pref_loss.restype = I
+    L.mgv_rdpo_pairs.argtypes = [P, I64, P, I64, ctypes.c_uint64, P, P]
+    L.mgv_rdpo_pairs.restype = I
+    L.mgv_merge_weights.argtypes = [I64, D, P]
+    L.mgv_merge_weights.restype = I
+    L.mgv_anneal_lr.argtypes = [I64, D, D, I64, ctypes.POINTER(D)]
+    L.mgv_anneal_lr.restype = I
     L.mgv_dpo_from_errors.argtypes = [D, D, D, D, D]
     L.mgv_dpo_from_errors.restype = D
     L.mgv_kto_from_rewards.argtypes = [I64, P, P, D, D, P, ctypes.POINTER(D)]
@@ -237,7 +243,8 @@ EXPORTS = ["mgv_ctx_create", "mgv_ctx_destroy", "mgv_last_error", "mgv_ctx_set_s
            "mgv_patchify", "mgv_unpatchify", "mgv_global_embed", "mgv_tokenize", "mgv_text_embed",
            "mgv_flow_errors", "mgv_flow_step_weighted", "mgv_post_validate", "mgv_post_state_create",
            "mgv_post_state_destroy", "mgv_post_plan_pos", "mgv_post_last_error", "mgv_post_train_step",
-           "mgv_post_pref_loss", "mgv_dpo_from_errors", "mgv_kto_from_rewards"]
+           "mgv_post_pref_loss", "mgv_dpo_from_errors", "mgv_kto_from_rewards", "mgv_rdpo_pairs",
+           "mgv_merge_weights", "mgv_anneal_lr"]
 
 
 # ---------------------------------------------------------------- MUGVCKPT (params.hpp:54-61)
@@ -464,6 +471,36 @@ def tokenize(prompt: str, vocab: int) -> np.ndarray:
     ids = np.empty(max(n, 1), dtype=np.int64)
     L.mgv_tokenize(prompt.encode(), vocab, ids.ctypes.data, n)
     return ids[:n]
+
+
+def merge_weights(k: int, gamma: float) -> np.ndarray:
+    """post::merge_weights (posttrain.cpp:51-63)."""
+    out = np.empty(max(k, 1))
+    st = _lib().mgv_merge_weights(k, gamma, out.ctypes.data)
+    if st != 0:
+        raise _EXC.get(st, MugvError)(st, "merge_weights")
+    return out[:k]
+
+
+def anneal_lr(step: int, lr_start: float = 1e-4, lr_end: float = 1e-6, steps: int = 1000) -> float:
+    """post::anneal_lr (posttrain.cpp:84-94)."""
+    out = D()
+    st = _lib().mgv_anneal_lr(step, lr_start, lr_end, steps, ctypes.byref(out))
+    if st != 0:
+        raise _EXC.get(st, MugvError)(st, "anneal_lr")
+    return out.value
+
+
+def rdpo_pairs(ctx: "Context", records, steps: int, seed: int):
+    """post::rdpo_pairs on the device sampler: [(winner_rows, loser_rows)] per SampleRecord."""
+    n = len(records)
+    arr = (mgv_sample_record * max(1, n))(*[r.to_c() for r in records])
+    outs = [(np.empty((r.rows.shape[0], ctx.cfg.patch_dim)), np.empty((r.rows.shape[0], ctx.cfg.patch_dim)))
+            for r in records]
+    wp = (P * max(1, n))(*[w.ctypes.data for w, _ in outs])
+    lp = (P * max(1, n))(*[l.ctypes.data for _, l in outs])
+    ctx._check(_lib().mgv_rdpo_pairs(ctx.h, n, arr, steps, seed, wp, lp))
+    return outs
 
 
 def dpo_from_errors(e_th_w, e_th_l, e_ref_w, e_ref_l, beta):

@@ -351,6 +351,69 @@ mgv_status mgv_post_pref_loss(mgv_ctx* policy, mgv_ctx* ref, const mgv_post_cfg*
     });
 }
 
+// rdpo_pairs (posttrain.cpp:235-254): per record, reverse-integrate its latents to the noise the model attributes
+// to them, then generate the winner forward from that noise and the loser forward from fresh Rng(seed) noise,
+// under the record's conditioning, on the device sampler.
+mgv_status mgv_rdpo_pairs(mgv_ctx* ctx, int64_t n, const mgv_sample_record* recs, int64_t steps, uint64_t seed,
+                          double* const* winners, double* const* losers) {
+    if (!ctx) return MGV_ERR_INPUT;
+    return mgv::guard_into(ctx->err, [&] {
+        if (n < 0 || (n > 0 && (!recs || !winners || !losers))) throw InputError("null argument");
+        if (steps < 1) throw InputError("steps must be >= 1");  // flowtrain.cpp:137
+        mgv::Model& m = *ctx->model;
+        const int64_t D = m.D();
+        HostRng rng(seed);
+        for (int64_t k = 0; k < n; ++k) {
+            const mgv_sample_record& r = recs[k];
+            check_record(r);
+            const int64_t N = n_of(r);
+            const double* cl = r.conditioned ? (r.condition_latents ? r.condition_latents : r.rows) : nullptr;
+            std::vector<double> noise_hat(static_cast<size_t>(N * D)), fresh(static_cast<size_t>(N * D));
+            m.sample_rows(r.rows, N, r.coords, r.dims, r.text, r.L, r.conditioned, cl, steps, +1, r.fps,
+                          noise_hat.data());  // reverse_sample_rows
+            m.sample_rows(noise_hat.data(), N, r.coords, r.dims, r.text, r.L, r.conditioned, cl, steps, -1, r.fps,
+                          winners[k]);  // forward_sample_rows
+            for (double& x : fresh) x = rng.normal();
+            m.sample_rows(fresh.data(), N, r.coords, r.dims, r.text, r.L, r.conditioned, cl, steps, -1, r.fps,
+                          losers[k]);
+        }
+    });
+}
+
+// merge_weights / anneal_lr (posttrain.cpp:51-94)
+mgv_status mgv_merge_weights(int64_t k, double gamma, double* out) {
+    std::string msg;
+    return mgv::guard_into(msg, [&] {
+        if (k < 1) throw InputError("need at least one checkpoint");
+        if (!(gamma > 0.0) || gamma > 1.0) throw ConfigError("gamma must lie in (0, 1]");
+        if (!out) throw InputError("null output");
+        double total = 0.0;
+        for (int64_t i = 0; i < k; ++i) {
+            out[i] = std::pow(gamma, static_cast<double>(k - 1 - i));
+            total += out[i];
+        }
+        for (int64_t i = 0; i < k; ++i) out[i] /= total;
+    });
+}
+mgv_status mgv_anneal_lr(int64_t step, double lr_start, double lr_end, int64_t steps, double* out) {
+    std::string msg;
+    return mgv::guard_into(msg, [&] {
+        if (steps < 2) throw ConfigError("anneal horizon needs at least two steps");
+        if (!(lr_start > 0.0) || !(lr_end >= 0.0) || lr_end > lr_start)
+            throw ConfigError("anneal must decay from lr_start to lr_end");
+        if (step < 0) throw InputError("anneal step must be >= 0");
+        if (!out) throw InputError("null output");
+        if (step >= steps - 1) {
+            *out = lr_end;
+        } else if (step == 0) {
+            *out = lr_start;
+        } else {
+            const double frac = static_cast<double>(step) / static_cast<double>(steps - 1);
+            *out = lr_end + (lr_start - lr_end) * 0.5 * (1.0 + std::cos(M_PI * frac));
+        }
+    });
+}
+
 double mgv_dpo_from_errors(double e_th_w, double e_th_l, double e_ref_w, double e_ref_l, double beta) {
     const double margin = beta * ((e_ref_w - e_th_w) - (e_ref_l - e_th_l));  // posttrain.cpp:144-147
     return softplus(-margin);

@@ -246,3 +246,61 @@ def test_post_schedule_and_pref_loss():
     st.close()
     pol.close()
     ref.close()
+
+
+@needs_ref
+def test_merge_weights_and_anneal_lr_match_reference():
+    import ctypes
+    from paper_2510_17519_b200 import capi
+    L = O.ref_lib()
+    for k, gamma in [(1, 0.9), (4, 0.9), (7, 0.5), (3, 1.0)]:
+        ref = np.empty(k)
+        assert L.ref_merge_weights(k, gamma, ref.ctypes.data) == 0
+        assert capi.merge_weights(k, gamma).tobytes() == ref.tobytes()
+    for step, a, b, n in [(0, 1e-4, 1e-6, 1000), (1, 1e-4, 1e-6, 1000), (500, 1e-4, 1e-6, 1000), (999, 1e-4, 1e-6, 1000),
+                          (5000, 3e-4, 0.0, 10), (1, 1.0, 1.0, 2)]:
+        ref = ctypes.c_double()
+        assert L.ref_anneal_lr(step, a, b, n, ctypes.byref(ref)) == 0
+        assert capi.anneal_lr(step, a, b, n) == ref.value
+    with pytest.raises(capi.ConfigError):
+        capi.merge_weights(3, 1.5)
+    with pytest.raises(capi.ConfigError):
+        capi.anneal_lr(0, 1e-6, 1e-4, 10)
+
+
+@pytest.mark.gpu
+@needs_ref
+def test_rdpo_pairs_match_reference():
+    """rdpo_pairs (posttrain.cpp:235-254) on the device sampler (fp32 mode) against the reference."""
+    import ctypes
+    from paper_2510_17519_b200 import capi
+    from tests.gpu_common import nerr
+    cfg = tiny_cfg()
+    pol, _ = models(cfg)
+    init = O.init_dit_params(cfg, O.Rng(1))
+    P = shaped(pol.params(), init)
+    recs, _ = records(cfg, "kto")
+    ctx = _ctx(cfg, P, "fp32", capi)
+    got = capi.rdpo_pairs(ctx, _product_records(recs, capi), steps=3, seed=77)
+    RR = type("RefRecord", (ctypes.Structure,), {"_fields_": [
+        ("dims", ctypes.c_int64 * 3), ("rows", ctypes.c_void_p), ("cond", ctypes.c_int32), ("text", ctypes.c_void_p),
+        ("L", ctypes.c_int64), ("fps", ctypes.c_double)]})
+    arr = (RR * len(recs))()
+    keep = []
+    for i, r in enumerate(recs):
+        rows, tx = np.ascontiguousarray(r.rows), np.ascontiguousarray(r.text)
+        keep += [rows, tx]
+        arr[i].dims[:] = list(r.dims)
+        arr[i].rows, arr[i].cond, arr[i].text, arr[i].L, arr[i].fps = rows.ctypes.data, int(r.cond), \
+            tx.ctypes.data, tx.shape[0], r.fps
+    W = [np.empty_like(r.rows) for r in recs]
+    Lo = [np.empty_like(r.rows) for r in recs]
+    wp = (ctypes.c_void_p * len(recs))(*[w.ctypes.data for w in W])
+    lp = (ctypes.c_void_p * len(recs))(*[x.ctypes.data for x in Lo])
+    c = O.ref_cfg(cfg)
+    assert O.ref_lib().ref_rdpo_pairs(pol.h, ctypes.addressof(c), len(recs), ctypes.addressof(arr), 3, 77, wp, lp) == 0
+    for i in range(len(recs)):
+        ew, el = nerr(got[i][0], W[i]), nerr(got[i][1], Lo[i])
+        print(f"record {i}: winner {ew:.2e} loser {el:.2e}")
+        assert ew < 1e-4 and el < 1e-4
+    ctx.close()
