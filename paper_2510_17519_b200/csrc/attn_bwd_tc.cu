@@ -32,9 +32,10 @@ static int g_dkv_pair = 0;
 // 0 = v8 (default: V in TMEM, P^T in its own columns), 1 = v5 (K in TMEM, P^T / dS^T aliased)
 static int g_dkv_variant = 0;
 static int g_dkv_cw = 2;  // compute warps per TMEM lane group in the v8 dK/dV pass (2 or 4)
-// dQ pass variant: 2 = v9 (default: 128-key steps, Q and dO in shared memory), 0 = v7 (64-key steps, Q and dO
-// in TMEM, dP single-buffered), 1 = v8 (Q in shared memory, dP double-buffered)
-static int g_dq_variant = 2;
+// dQ pass variant: 3 = v10 (default: 128-key steps, Q in TMEM, dO in shared memory, dS over dP), 2 = v9 (Q and dO
+// in shared memory), 0 = v7 (64-key steps, Q and dO in TMEM, dP single-buffered), 1 = v8 (Q in shared memory, dP
+// double-buffered)
+static int g_dq_variant = 3;
 static int g_dq_cw = 2;  // compute warps per TMEM lane group in the v9 dQ pass (2 or 4)
 // timing experiments only (tools/): bit 0 = compute warps skip TMEM traffic and math, bit 1 = no Q^T/dO^T TMA
 __device__ int g_attn_dbg = 0;
@@ -1952,6 +1953,212 @@ __global__ void __launch_bounds__(128 + 128 * CW, 1) attn_bwd_dq_v9_kernel(const
     if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// =====================================================================================  dQ (v10)
+// v9's 128-key steps with Q back in TMEM: S = Q K^T is a TS product, so the CTA's fixed A tile is no longer
+// re-read from shared memory on every key step (v9's two SS products move 2 x 74 KB of shared memory per
+// step, more than the tensor pipe's operand path sustains next to the TMA writes).  dS (bf16) is written over
+// the consumed dP columns, which makes room for Q:  the compute warp that owns keys [64 hf, 64 hf + 64) has
+// loaded all of its dP columns before it writes its dS pairs to [DP + 32 + 32 hf, +32), which lie inside its
+// own dP range, and the pipe order dQ(j) -> dP(j+1) keeps the next dP behind the dS reader.  NS K^T / V^T
+// stages (shared memory freed by Q).
+// TMEM: S [0,128)  dP|dS [128,256)  dQ [256,256+HD)  Q (bf16 pairs) [400,472).
+template <int HD, int NS>
+__global__ void __launch_bounds__(128 + 128 * 2, 1) attn_bwd_dq_v10_kernel(const __grid_constant__ BwdMaps tm,
+                                                                          AttnBwdProblem p) {
+    constexpr int BMQ = 128, BKV = 128, CW = 2, KW = BKV / CW;
+    using T = BT<HD>;
+    constexpr int HDP = ((HD + 15) / 16) * 16;
+    constexpr int S_COL = 0, DP_COL = 128, DS_COL = DP_COL + 32, DQ_COL = 256, Q_COL = 400;
+    static_assert(DQ_COL + HDP <= Q_COL && Q_COL + HD / 2 <= 512, "TMEM budget");
+    constexpr int KV_STAGE = 2 * T::T_TILE;  // two 64-key transposed tiles
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sdO = smem;
+    uint8_t* sKt = sdO + T::ROW_TILE;    // [NS]
+    uint8_t* sVt = sKt + NS * KV_STAGE;  // [NS]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sVt + NS * KV_STAGE);
+    uint64_t* do_full = bars;
+    uint64_t* kf = bars + 1;           // [NS]
+    uint64_t* ke = kf + NS;            // [NS]
+    uint64_t* vf = ke + NS;            // [NS]
+    uint64_t* ve = vf + NS;            // [NS]
+    uint64_t* s_full = ve + NS;
+    uint64_t* s_empty = s_full + 1;
+    uint64_t* dp_full = s_full + 2;
+    uint64_t* ds_full = s_full + 3;
+    uint64_t* acc_done = s_full + 4;
+    uint64_t* qa_ready = s_full + 5;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 6);
+
+    const AttnProblem& f = p.f;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int h = blockIdx.y, q0 = blockIdx.x * BMQ;
+    const int nkv = (f.Nk + BKV - 1) / BKV;
+    const int col = h * HD;
+
+    if (threadIdx.x == 0) {
+        mbar_init(do_full, 1);
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(&kf[i], 1);
+            mbar_init(&ke[i], 1);
+            mbar_init(&vf[i], 1);
+            mbar_init(&ve[i], 1);
+        }
+        mbar_init(s_full, 1);
+        mbar_init(s_empty, 4 * CW);
+        mbar_init(dp_full, 1);
+        mbar_init(ds_full, 4 * CW);
+        mbar_init(acc_done, 1);
+        mbar_init(qa_ready, 4);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            mbar_arrive_expect_tx(do_full, T::ROW_TILE);
+            load_row_tile<HD>(sdO, &tm.b128, &tm.b32, do_full, col, q0);
+            for (int j = 0; j < nkv; ++j) {
+                const int b = j % NS;
+                if (j >= NS) mbar_wait(&ke[b], ((j / NS) - 1) & 1);
+                mbar_arrive_expect_tx(&kf[b], KV_STAGE);
+                tma_load_2d(sKt + b * KV_STAGE, &tm.ta, &kf[b], j * BKV, col);
+                tma_load_2d(sKt + b * KV_STAGE + T::T_TILE, &tm.ta, &kf[b], j * BKV + 64, col);
+                if (j >= NS) mbar_wait(&ve[b], ((j / NS) - 1) & 1);
+                mbar_arrive_expect_tx(&vf[b], KV_STAGE);
+                tma_load_2d(sVt + b * KV_STAGE, &tm.tb, &vf[b], j * BKV, col);
+                tma_load_2d(sVt + b * KV_STAGE + T::T_TILE, &tm.tb, &vf[b], j * BKV + 64, col);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t id128 = idesc_bf16_f32(128, 128, false, true), idhd = idesc_bf16_f32(128, HD, false, false);
+        auto issue_s = [&](int j) {  // S = Q K^T: A = Q from TMEM, B^T = the stage's HD x 128 K^T tiles (MN-major)
+            const int b = j % NS;
+            mbar_wait(&kf[b], (j / NS) & 1);
+            if (j >= 1) mbar_wait(s_empty, (j - 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t bt = smem_u32(sKt + b * KV_STAGE);
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk)
+                    umma_f16_ts(tmem + S_COL, tmem + Q_COL + kk * 8, smem_desc(bt + kk * 2048, T::T_TILE, 1024, kSwizzle128),
+                                id128, kk > 0 ? 1u : 0u);
+                umma_commit(s_full);
+            }
+            __syncwarp();
+        };
+        auto issue_dp = [&](int j) {  // dP = dO V^T (SS); behind dQ(j-1) in the pipe, which has read dS(j-1)
+            const int b = j % NS;
+            mbar_wait(&vf[b], (j / NS) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t a = smem_u32(sdO), bt = smem_u32(sVt + b * KV_STAGE);
+                int kk = 0;
+#pragma unroll
+                for (int c = 0; c < T::NF; ++c)
+#pragma unroll
+                    for (int k4 = 0; k4 < 4; ++k4, ++kk)
+                        umma_f16_ss(tmem + DP_COL, smem_desc(a + c * 16384 + k4 * 32, 16, 1024, kSwizzle128),
+                                    smem_desc(bt + kk * 2048, T::T_TILE, 1024, kSwizzle128), id128, kk > 0);
+                if (T::TAIL)
+                    umma_f16_ss(tmem + DP_COL, smem_desc(a + T::NF * 16384, 16, 256, kSwizzle32),
+                                smem_desc(bt + kk * 2048, T::T_TILE, 1024, kSwizzle128), id128, 1);
+                umma_commit(dp_full);
+                umma_commit(&ve[b]);  // V^T(j) is read by dP(j) only
+            }
+            __syncwarp();
+        };
+        mbar_wait(qa_ready, 0);
+        mbar_wait(do_full, 0);
+        if (nkv > 0) {
+            issue_s(0);
+            issue_dp(0);
+        }
+        for (int j = 0; j < nkv; ++j) {
+            const int b = j % NS;
+            if (j + 1 < nkv) issue_s(j + 1);
+            mbar_wait(ds_full, j & 1);
+            tc_fence_after();
+            if (elect_one()) {  // dQ += dS_j K_j: 8 k-steps of 16 keys over the stage's two K^T tiles
+                const uint32_t bt = smem_u32(sKt + b * KV_STAGE);
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    umma_f16_ts(tmem + DQ_COL, tmem + DS_COL + ks * 8,
+                                smem_desc(bt + (ks >> 2) * T::T_TILE + (ks & 3) * 32, 16, 1024, kSwizzle128), idhd,
+                                (j > 0 || ks > 0) ? 1u : 0u);
+                umma_commit(&ke[b]);  // K^T(j): S(j) and dQ(j) done
+                if (j == nkv - 1) umma_commit(acc_done);
+            }
+            __syncwarp();
+            if (j + 1 < nkv) issue_dp(j + 1);
+        }
+    } else if (warp >= 4) {
+        // two warps per TMEM lane group: warp hf handles keys [64 hf, 64 hf + 64) of each step
+        const int g = warp & 3, hf = (warp - 4) >> 2, row = g * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(g * 32) << 16;
+        const int q = q0 + row;
+        const bool qv = q < f.Nq;
+        if (hf == 0) {
+            row_to_tmem<HD>(tmem + lane_base + Q_COL,
+                            static_cast<const __nv_bfloat16*>(f.q) + (int64_t)(qv ? q : 0) * f.q_ld + col, qv);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(qa_ready);
+        }
+        const float lse2 = qv ? f.lse[(int64_t)h * lse_stride(f) + q] * kLog2e : 0.0f;
+        const float Dq = qv ? p.Dvec[(int64_t)h * lse_stride(f) + q] : 0.0f;
+        for (int j = 0; j < nkv; ++j) {
+            float pr[KW];
+            mbar_wait(s_full, j & 1);
+            tc_fence_after();
+            tmem_ld32(tmem + lane_base + S_COL + hf * KW, reinterpret_cast<uint32_t*>(pr));
+            tmem_ld32(tmem + lane_base + S_COL + hf * KW + 32, reinterpret_cast<uint32_t*>(pr + 32));
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(s_empty);
+            const int kb = j * BKV + hf * KW;
+            if (kb + KW <= f.Nk) {
+#pragma unroll
+                for (int c = 0; c < KW; ++c) pr[c] = ex2f(fmaf(pr[c], kLog2e, -lse2));
+            } else {
+#pragma unroll
+                for (int c = 0; c < KW; ++c) pr[c] = kb + c < f.Nk ? ex2f(fmaf(pr[c], kLog2e, -lse2)) : 0.0f;
+            }
+            mbar_wait(dp_full, j & 1);
+            tc_fence_after();
+            float dp[KW];
+            tmem_ld32(tmem + lane_base + DP_COL + hf * KW, reinterpret_cast<uint32_t*>(dp));
+            tmem_ld32(tmem + lane_base + DP_COL + hf * KW + 32, reinterpret_cast<uint32_t*>(dp + 32));
+            tmem_wait_ld();  // all of this warp's dP columns are in registers before its dS overwrites them
+            uint32_t dk[KW / 2];
+#pragma unroll
+            for (int c = 0; c < KW; c += 2)
+                dk[c / 2] = pack_bf16(pr[c] * (dp[c] - Dq), pr[c + 1] * (dp[c + 1] - Dq));  // autodiff.cpp:820
+            tmem_st16(tmem + lane_base + DS_COL + hf * (KW / 2), dk);
+            tmem_st16(tmem + lane_base + DS_COL + hf * (KW / 2) + 16, dk + 16);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(ds_full);
+        }
+        if (nkv > 0) mbar_wait(acc_done, 0);
+        tc_fence_after();
+        constexpr int NC = HD / 16;
+        store_acc_row<HD>(tmem + lane_base + DQ_COL, static_cast<__nv_bfloat16*>(p.dq) + (int64_t)q * p.dq_ld + col,
+                          qv && nkv > 0, hf * NC / CW, (hf + 1) * NC / CW);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 // ------------------------------------------------------------------ host
 template <int HD>
 static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, const void* kt, int64_t kt_ld,
@@ -2076,7 +2283,18 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
             MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             set = true;
         }
-        if (g_dq_variant == 2) {  // v9: 128-key steps, Q and dO in shared memory
+        if (g_dq_variant == 3) {  // v10: 128-key steps, Q in TMEM, dO in shared memory, dS over dP
+            make_tmap_sw(&m.b128, p.dO, W, f.Nq, p.do_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+            make_tmap_sw(&m.b32, p.dO, W, f.Nq, p.do_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
+            const int smem10 = T::ROW_TILE + 8 * T::T_TILE + 256 + 1024;
+            static bool set10 = false;
+            if (!set10) {
+                MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dq_v10_kernel<HD, 2>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem10));
+                set10 = true;
+            }
+            attn_bwd_dq_v10_kernel<HD, 2><<<dim3((f.Nq + 127) / 128, f.heads), 128 + 128 * 2, smem10, s>>>(m, p);
+        } else if (g_dq_variant == 2) {  // v9: 128-key steps, Q and dO in shared memory
             make_tmap_sw(&m.a128, f.q, W, f.Nq, f.q_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
             make_tmap_sw(&m.a32, f.q, W, f.Nq, f.q_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
             make_tmap_sw(&m.b128, p.dO, W, f.Nq, p.do_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
