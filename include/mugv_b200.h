@@ -197,10 +197,12 @@ mgv_status mgv_flow_step_device(mgv_ctx* ctx, int64_t n, const mgv_flow_sample* 
  * and the number of kernel launches it issued. */
 double mgv_last_step_ms(mgv_ctx* ctx);
 int64_t mgv_last_step_launches(mgv_ctx* ctx);
-/* Per-phase CUDA-event timing ("attn_fwd", "attn_bwd", "blocks_fwd", ...), accumulated over steps. */
+/* Per-phase CUDA-event timing ("attn_fwd", "attn_bwd", "blocks_fwd", "gemm" = every bf16 GEMM launch, ...),
+ * accumulated over steps.  mgv_prof_entry_work: the phase's algorithmic FLOPs (2 M N K summed; "gemm" only). */
 mgv_status mgv_prof_enable(mgv_ctx* ctx, int on);
 int64_t mgv_prof_count(mgv_ctx* ctx);
 const char* mgv_prof_entry(mgv_ctx* ctx, int64_t i, double* ms, int64_t* launches);
+double mgv_prof_entry_work(mgv_ctx* ctx, int64_t i);
 
 /* ---- MUGVCKPT checkpoint container (proj/include/mugv/params.hpp:54-61, proj/src/params.cpp:92-225) ----
  * Host-only (no device needed).  The writer emits the same bytes as mugv::save_checkpoint for the same

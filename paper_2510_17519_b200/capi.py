@@ -150,6 +150,8 @@ def declare(L):
     L.mgv_prof_count.restype = I64
     L.mgv_prof_entry.argtypes = [P, I64, ctypes.POINTER(D), ctypes.POINTER(I64)]
     L.mgv_prof_entry.restype = ctypes.c_char_p
+    L.mgv_prof_entry_work.argtypes = [P, I64]
+    L.mgv_prof_entry_work.restype = D
     CP = ctypes.c_char_p
     L.mgv_ckpt_last_error.argtypes = []
     L.mgv_ckpt_last_error.restype = CP
@@ -235,7 +237,7 @@ EXPORTS = ["mgv_ctx_create", "mgv_ctx_destroy", "mgv_last_error", "mgv_ctx_set_s
            "mgv_params_upload", "mgv_param_count", "mgv_param_name", "mgv_param_numel",
            "mgv_predict_velocity", "mgv_dit_forward", "mgv_flow_step", "mgv_flow_loss", "mgv_latent_rows",
            "mgv_rows_to_grid", "mgv_flow_step_device", "mgv_last_step_ms", "mgv_last_step_launches",
-           "mgv_prof_enable", "mgv_prof_count", "mgv_prof_entry",
+           "mgv_prof_enable", "mgv_prof_count", "mgv_prof_entry", "mgv_prof_entry_work",
            "mgv_ckpt_last_error", "mgv_ckpt_last_error_kind", "mgv_ckpt_load", "mgv_ckpt_free", "mgv_ckpt_count",
            "mgv_ckpt_name", "mgv_ckpt_dtype", "mgv_ckpt_rank", "mgv_ckpt_shape", "mgv_ckpt_numel", "mgv_ckpt_find",
            "mgv_ckpt_read", "mgv_ckpt_meta_count", "mgv_ckpt_meta_key", "mgv_ckpt_meta_value", "mgv_ckpt_save",
@@ -843,5 +845,5 @@ class Context:
         for i in range(self._L.mgv_prof_count(self.h)):
             ms, n = D(), I64()
             name = self._L.mgv_prof_entry(self.h, i, ctypes.byref(ms), ctypes.byref(n)).decode()
-            out[name] = {"ms": ms.value, "launches": n.value}
+            out[name] = {"ms": ms.value, "launches": n.value, "flops": self._L.mgv_prof_entry_work(self.h, i)}
         return out

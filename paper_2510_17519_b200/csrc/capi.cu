@@ -362,5 +362,10 @@ const char* mgv_prof_entry(mgv_ctx* ctx, int64_t i, double* ms, int64_t* n) {
     *n = it->second.n;
     return it->first.c_str();
 }
+double mgv_prof_entry_work(mgv_ctx* ctx, int64_t i) {
+    auto it = ctx->model->prof().stats.begin();
+    std::advance(it, i);
+    return it->second.work;
+}
 
 }  // extern "C"

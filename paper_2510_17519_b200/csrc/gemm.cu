@@ -9,6 +9,7 @@ namespace mgv {
 
 static std::atomic<int64_t> g_launches{0};
 int g_gemm_mode = 1;
+void (*g_gemm_prof_hook)(bool, double, cudaStream_t) = nullptr;
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 

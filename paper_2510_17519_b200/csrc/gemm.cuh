@@ -182,6 +182,9 @@ void gemm_tc2_launch(const Mat& A, const Mat& B, int M, int N, int K, const Epi&
 }
 
 extern int g_gemm_mode;  // 0: 1-CTA (+B multicast pairs), 1: CTA-pair UMMA (default)
+// Benchmark-only phase timing of the tensor-core GEMMs: when set (Model, profiling on), called with
+// begin = true and the GEMM's 2 M N K before the launch and with begin = false after it.
+extern void (*g_gemm_prof_hook)(bool begin, double flops, cudaStream_t s);
 
 // Dispatch on precision and operand majors.  bf16: A/B are __nv_bfloat16; fp32: float.
 template <class Epi>
@@ -195,6 +198,15 @@ void gemm(bool bf16, const Mat& A, const Mat& B, int M, int N, int K, const Epi&
         else gemm_f32_launch<true, false>(A, B, M, N, K, epi, s);
         return;
     }
+    struct ProfScope {
+        cudaStream_t s;
+        ProfScope(double f, cudaStream_t st) : s(st) {
+            if (g_gemm_prof_hook) g_gemm_prof_hook(true, f, s);
+        }
+        ~ProfScope() {
+            if (g_gemm_prof_hook) g_gemm_prof_hook(false, 0.0, s);
+        }
+    } prof_scope(2.0 * M * N * K, s);
     if (g_gemm_mode == 1 && M > kGemmBM) {
         if (!am && !bm) gemm_tc2_launch<256, false, false>(A, B, M, N, K, epi, s);
         else if (!am && bm) gemm_tc2_launch<256, false, true>(A, B, M, N, K, epi, s);

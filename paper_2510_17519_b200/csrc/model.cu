@@ -209,9 +209,29 @@ cudaEvent_t Prof::get() {
     used_.push_back(e);
     return e;
 }
-void Prof::begin(const char* name, cudaStream_t s) {
+// The bf16 GEMMs of a profiled step are timed as one "gemm" phase (nested inside blocks_fwd / blocks_bwd).
+static Prof* g_gemm_prof = nullptr;
+static void gemm_prof_hook(bool begin, double flops, cudaStream_t s) {
+    if (!g_gemm_prof) return;
+    if (begin)
+        g_gemm_prof->begin("gemm", s, flops);
+    else
+        g_gemm_prof->end(s);
+}
+GemmProfGuard::GemmProfGuard(Prof& p) {
+    if (p.on) {
+        g_gemm_prof = &p;
+        g_gemm_prof_hook = gemm_prof_hook;
+    }
+}
+GemmProfGuard::~GemmProfGuard() {
+    g_gemm_prof = nullptr;
+    g_gemm_prof_hook = nullptr;
+}
+
+void Prof::begin(const char* name, cudaStream_t s, double work) {
     if (!on) return;
-    Pend p{name, get(), nullptr};
+    Pend p{name, get(), nullptr, work};
     MGV_CUDA(cudaEventRecord(p.a, s));
     pend_.push_back(p);
 }
@@ -232,6 +252,7 @@ void Prof::end_step() {
         Stat& st = stats[p.name];
         st.ms += ms;
         st.n += 1;
+        st.work += p.work;
     }
     pend_.clear();
     for (auto e : used_) pool_.push_back(e);
@@ -1104,6 +1125,7 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
     MGV_CUDA(cudaEventCreate(&e1));
     MGV_CUDA(cudaEventRecord(e0, s));
     prof_.begin_step();
+    GemmProfGuard gemm_prof(prof_);
     MGV_CUDA(cudaMemsetAsync(grad_buf_, 0, sizeof(float) * grad_numel_, s));
     MGV_CUDA(cudaMemsetAsync(w.scal, 0, sizeof(double) * 8, s));
     if (!per_text) convert_rows<T>(text_dev, L * cfg_.text_dim, tp<T>(w.text), s);

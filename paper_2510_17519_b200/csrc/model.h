@@ -92,11 +92,12 @@ public:
     struct Stat {
         double ms = 0.0;
         int64_t n = 0;
+        double work = 0.0;  // algorithmic FLOPs of the phase's launches (GEMM phase)
     };
     bool on = false;
     std::map<std::string, Stat> stats;
     void begin_step() { pend_.clear(); }
-    void begin(const char* name, cudaStream_t s);
+    void begin(const char* name, cudaStream_t s, double work = 0.0);
     void end(cudaStream_t s);
     void end_step();  // after the stream was synchronised
     ~Prof();
@@ -105,10 +106,17 @@ private:
     struct Pend {
         std::string name;
         cudaEvent_t a, b;
+        double work;
     };
     cudaEvent_t get();
     std::vector<Pend> pend_;
     std::vector<cudaEvent_t> pool_, used_;
+};
+
+// Routes the bf16 GEMM launches of one step into `p` as the "gemm" phase while alive (profiling only).
+struct GemmProfGuard {
+    explicit GemmProfGuard(Prof& p);
+    ~GemmProfGuard();
 };
 
 class Model {
