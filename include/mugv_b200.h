@@ -22,6 +22,8 @@
  *   mgv_patchify             dit::patchify                          proj/include/mugv/dit.hpp:86-87
  *   mgv_unpatchify           dit::unpatchify                        proj/include/mugv/dit.hpp:89-90
  *   mgv_global_embed         dit::global_embed                      proj/include/mugv/dit.hpp:83-84
+ *   mgv_fused_modulate       SPEC fused_modulate (no code in proj/)
+ *   mgv_apply_rope3d         Tape::rope3d / SPEC apply_rope3d        proj/src/autodiff.cpp:849-898
  *   mgv_tokenize             dit::tokenize                          proj/src/dit.cpp:193-211
  *   mgv_text_embed           dit::text_embed                        proj/include/mugv/dit.hpp:63-72, dit.cpp:213-234
  *   mgv_rows_to_grid         dit::rows_to_grid                      proj/include/mugv/dit.hpp:62
@@ -169,6 +171,24 @@ mgv_status mgv_unpatchify(mgv_ctx* ctx, const double* tokens, int64_t N, const i
  * [0, 1]. */
 mgv_status mgv_global_embed(mgv_ctx* ctx, const double* timesteps, int64_t N, double fps, double* g,
                             double* block_scales);
+
+/* ---- SPEC-only operators of the path (no code in proj/) ----
+ * mgv_fused_modulate: SPEC.md:616-624  out = residual + ((x + bias) * (1 + scale) + shift) over a rows x cols
+ *   fp64 buffer, bias / scale / shift with 1 (scalar), cols (per channel) or rows*cols elements, else
+ *   MGV_ERR_DIMENSION; one device pass, bit-identical to the composed three-step reference (no contraction).
+ * mgv_dev_fused_modulate_f32: the same operator on DEVICE fp32 buffers (per-channel vectors, cols % 4 == 0,
+ *   16-byte aligned), on the context stream, asynchronous; one read of x / residual, one write of out.
+ * mgv_apply_rope3d: SPEC.md:168-176, Tape::rope3d forward (autodiff.cpp:849-898): x is N x heads*hd fp64 with
+ *   hd = split[0] + split[1] + split[2], coords N x 3 (t, h, w); odd split -> MGV_ERR_CONFIG.  inverse != 0
+ *   applies the inverse rotation (the backward's rope_apply_vec(..., -1)).  Bit-identical to the reference. */
+mgv_status mgv_fused_modulate(mgv_ctx* ctx, const double* x, const double* bias, int64_t bias_n, const double* scale,
+                              int64_t scale_n, const double* shift, int64_t shift_n, const double* residual,
+                              int64_t rows, int64_t cols, double* out);
+mgv_status mgv_dev_fused_modulate_f32(mgv_ctx* ctx, const float* x, const float* bias, const float* scale,
+                                      const float* shift, const float* residual, int64_t rows, int64_t cols,
+                                      float* out);
+mgv_status mgv_apply_rope3d(mgv_ctx* ctx, const double* x, int64_t N, int64_t heads, const int64_t split[3],
+                            const int32_t* coords, double base, int inverse, double* out);
 
 /* FlowTrainer::step forward + backward over n local samples (global_batch = n * world).
  * loss: mean of per-sample masked flow losses; grad_norm: sqrt of the sum of squared gradient entries;

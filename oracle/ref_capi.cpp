@@ -16,6 +16,7 @@
 //   - save_checkpoint / load_checkpoint          proj/src/params.cpp:92-225
 //   - post::post_loss_graph (+ backward), make_pair_draws / make_label_draws, dpo_loss / kto_loss
 //                                                proj/src/posttrain.cpp:106-290
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <iterator>
@@ -24,6 +25,7 @@
 #include <string>
 #include <vector>
 
+#include "mugv/autodiff.hpp"
 #include "mugv/optim.hpp"
 #include "mugv/dit.hpp"
 #include "mugv/flowtrain.hpp"
@@ -554,6 +556,29 @@ int ref_rdpo_pairs(void* h, const RefCfg* c, int64_t n, const RefRecord* recs, i
             const auto& p = pairs[static_cast<size_t>(i)];
             std::memcpy(winners[i], p.winner.rows.data(), sizeof(double) * static_cast<size_t>(p.winner.rows.numel()));
             std::memcpy(losers[i], p.loser.rows.data(), sizeof(double) * static_cast<size_t>(p.loser.rows.numel()));
+        }
+    });
+}
+
+// ---- Tape::rope3d (autodiff.cpp:849-898): forward, or the backward's inverse rotation of `x` taken as dL/dy ----
+int ref_rope3d(const double* x, int64_t N, int heads, const int* split, const int32_t* coords, double base,
+               int inverse, double* out) {
+    return guard([&] {
+        const std::array<int, 3> sp{split[0], split[1], split[2]};
+        const int64_t D = static_cast<int64_t>(heads) * (sp[0] + sp[1] + sp[2]);
+        auto co = std::make_shared<std::vector<std::array<int, 3>>>(static_cast<size_t>(N));
+        for (int64_t i = 0; i < N; ++i) (*co)[static_cast<size_t>(i)] = {coords[3 * i], coords[3 * i + 1], coords[3 * i + 2]};
+        Tensor X({N, D});
+        std::memcpy(X.data(), x, sizeof(double) * static_cast<size_t>(N * D));
+        Tape t;
+        if (!inverse) {
+            Var y = t.rope3d(t.constant(X), co, sp, heads, base);
+            std::memcpy(out, t.val(y).data(), sizeof(double) * static_cast<size_t>(N * D));
+        } else {  // d/dx sum(rope3d(x) * X) = rope_apply_vec(X, -1) accumulated into a zero gradient
+            Var xv = t.leaf(Tensor::zeros({N, D}), true);
+            Var y = t.rope3d(xv, co, sp, heads, base);
+            t.backward(t.sum_all(t.mul(y, t.constant(X))));
+            std::memcpy(out, t.grad(xv).data(), sizeof(double) * static_cast<size_t>(N * D));
         }
     });
 }

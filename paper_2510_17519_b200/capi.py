@@ -199,6 +199,12 @@ def declare(L):
     L.mgv_unpatchify.restype = I
     L.mgv_global_embed.argtypes = [P, P, I64, D, P, P]
     L.mgv_global_embed.restype = I
+    L.mgv_fused_modulate.argtypes = [P, P, P, I64, P, I64, P, I64, P, I64, I64, P]
+    L.mgv_fused_modulate.restype = I
+    L.mgv_dev_fused_modulate_f32.argtypes = [P, P, P, P, P, P, I64, I64, P]
+    L.mgv_dev_fused_modulate_f32.restype = I
+    L.mgv_apply_rope3d.argtypes = [P, P, I64, I64, P, P, D, I, P]
+    L.mgv_apply_rope3d.restype = I
     L.mgv_flow_errors.argtypes = [P, I64, P, P]
     L.mgv_flow_errors.restype = I
     L.mgv_flow_step_weighted.argtypes = [P, I64, P, P, P, ctypes.POINTER(D), ctypes.POINTER(D), P]
@@ -242,7 +248,8 @@ EXPORTS = ["mgv_ctx_create", "mgv_ctx_destroy", "mgv_last_error", "mgv_ctx_set_s
            "mgv_ckpt_name", "mgv_ckpt_dtype", "mgv_ckpt_rank", "mgv_ckpt_shape", "mgv_ckpt_numel", "mgv_ckpt_find",
            "mgv_ckpt_read", "mgv_ckpt_meta_count", "mgv_ckpt_meta_key", "mgv_ckpt_meta_value", "mgv_ckpt_save",
            "mgv_params_upload_ckpt", "mgv_params_save",
-           "mgv_patchify", "mgv_unpatchify", "mgv_global_embed", "mgv_tokenize", "mgv_text_embed",
+           "mgv_patchify", "mgv_unpatchify", "mgv_global_embed", "mgv_fused_modulate", "mgv_dev_fused_modulate_f32",
+           "mgv_apply_rope3d", "mgv_tokenize", "mgv_text_embed",
            "mgv_flow_errors", "mgv_flow_step_weighted", "mgv_post_validate", "mgv_post_state_create",
            "mgv_post_state_destroy", "mgv_post_plan_pos", "mgv_post_last_error", "mgv_post_train_step",
            "mgv_post_pref_loss", "mgv_dpo_from_errors", "mgv_kto_from_rewards", "mgv_rdpo_pairs",
@@ -705,6 +712,35 @@ class Context:
         self._check(self._L.mgv_predict_velocity(self.h, rows.ctypes.data, rows.shape[0], co.ctypes.data, dm,
                                                   text.ctypes.data, text.shape[0], ts.ctypes.data, fps,
                                                   out.ctypes.data))
+        return out
+
+    def fused_modulate(self, x, bias, scale, shift, residual):
+        """SPEC fused_modulate: residual + ((x + bias) * (1 + scale) + shift) on a 2-D fp64
+        array; bias / scale / shift are scalars, per-channel vectors or full arrays."""
+        x, res = _f64(x), _f64(residual)
+        rows, cols = x.shape
+        b, sc, sh = (_f64(np.asarray(a)).ravel() for a in (bias, scale, shift))
+        out = np.empty_like(x)
+        self._check(self._L.mgv_fused_modulate(self.h, x.ctypes.data, b.ctypes.data, b.size, sc.ctypes.data, sc.size,
+                                               sh.ctypes.data, sh.size, res.ctypes.data, rows, cols, out.ctypes.data))
+        return out
+
+    def dev_fused_modulate_f32(self, x, bias, scale, shift, residual, out):
+        """The fp32 device form on device pointers (torch tensors or raw addresses), asynchronous on the context
+        stream."""
+        ptr = lambda a: a if isinstance(a, int) else a.data_ptr()
+        rows, cols = x.shape
+        self._check(self._L.mgv_dev_fused_modulate_f32(self.h, ptr(x), ptr(bias), ptr(scale), ptr(shift),
+                                                       ptr(residual), rows, cols, ptr(out)))
+
+    def apply_rope3d(self, x, coords, split, heads, base=10000.0, inverse=False):
+        """SPEC apply_rope3d = Tape::rope3d (autodiff.cpp:849-898) on x (N, heads * sum(split)) fp64."""
+        x = _f64(x)
+        co = np.ascontiguousarray(coords, dtype=np.int32)
+        sp = (I64 * 3)(*[int(v) for v in split])
+        out = np.empty_like(x)
+        self._check(self._L.mgv_apply_rope3d(self.h, x.ctypes.data, x.shape[0], heads, sp, co.ctypes.data, base,
+                                             1 if inverse else 0, out.ctypes.data))
         return out
 
     def dit_forward(self, tokens, coords, dims, text, timesteps, fps=8.0):

@@ -243,6 +243,28 @@ mgv_status mgv_global_embed(mgv_ctx* ctx, const double* timesteps, int64_t N, do
     return guard(ctx, [&] { ctx->model->global_embed_host(timesteps, N, fps, g, block_scales); });
 }
 
+mgv_status mgv_fused_modulate(mgv_ctx* ctx, const double* x, const double* bias, int64_t bias_n, const double* scale,
+                              int64_t scale_n, const double* shift, int64_t shift_n, const double* residual,
+                              int64_t rows, int64_t cols, double* out) {
+    return guard(ctx, [&] {
+        mgv::fused_modulate_host(x, bias, bias_n, scale, scale_n, shift, shift_n, residual, rows, cols, out,
+                                 ctx->model->stream());
+    });
+}
+mgv_status mgv_dev_fused_modulate_f32(mgv_ctx* ctx, const float* x, const float* bias, const float* scale,
+                                      const float* shift, const float* residual, int64_t rows, int64_t cols,
+                                      float* out) {
+    return guard(ctx, [&] {
+        mgv::fused_modulate_dev_f32(x, bias, scale, shift, residual, rows, cols, out, ctx->model->stream());
+    });
+}
+mgv_status mgv_apply_rope3d(mgv_ctx* ctx, const double* x, int64_t N, int64_t heads, const int64_t split[3],
+                            const int32_t* coords, double base, int inverse, double* out) {
+    return guard(ctx, [&] {
+        mgv::apply_rope3d_host(x, N, heads, split, coords, base, inverse, out, ctx->model->stream());
+    });
+}
+
 mgv_status mgv_flow_step(mgv_ctx* ctx, int64_t n, const mgv_flow_sample* samples, const double* text, int64_t L,
                          double fps, double* loss, double* grad_norm, double* const* grads_out,
                          double* const* velocity_out) {

@@ -144,4 +144,15 @@ void fill_f32(float* p, int64_t n, float v, cudaStream_t s);
 void transpose_bf16(const __nv_bfloat16* in, int64_t ld_in, int rows, int cols, __nv_bfloat16* out, int64_t ld_out,
                     cudaStream_t s);
 
+// SPEC-only operators (spec_ops.cu): fused_modulate on host fp64 buffers (bias / scale / shift
+// of 1, cols or rows*cols elements) and on device fp32 buffers (per-channel vectors); apply_rope3d
+// (SPEC.md:168-176 = Tape::rope3d, autodiff.cpp:849-898) on host fp64 buffers, inverse != 0 rotates by -theta
+void fused_modulate_host(const double* x, const double* bias, int64_t nb, const double* scale, int64_t ns,
+                         const double* shift, int64_t nh, const double* residual, int64_t rows, int64_t cols,
+                         double* out, cudaStream_t s);
+void fused_modulate_dev_f32(const float* x, const float* bias, const float* scale, const float* shift,
+                            const float* residual, int64_t rows, int64_t cols, float* out, cudaStream_t s);
+void apply_rope3d_host(const double* x, int64_t N, int64_t heads, const int64_t split[3], const int32_t* coords,
+                       double base, int inverse, double* out, cudaStream_t s);
+
 }  // namespace mgv

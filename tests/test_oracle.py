@@ -171,3 +171,21 @@ def test_sampler_restatement_matches_reference(direction, cond):
     mine = O.sample_rows(P, cfg, x0, coords, text, 8.0, 3, direction, cm, cl)
     theirs = O.ref_sample_rows(ref, dims, x0, text, 8.0, 3, direction, cm, cl)
     assert np.abs(mine - theirs).max() <= 1e-12 * max(1.0, np.abs(theirs).max())
+
+
+@needs_ref
+def test_ref_rope3d_matches_restatement():
+    """The reference veneer's Tape::rope3d (forward and the backward's inverse rotation) against the numpy
+    restatement rope_tables / rope_apply (autodiff.cpp:851-898): equal up to libm / numpy trig rounding."""
+    import ctypes
+    L = O.ref_lib()
+    rng = np.random.default_rng(5)
+    split, heads, N = (22, 22, 20), 4, 50
+    x = rng.standard_normal((N, heads * sum(split)))
+    co = rng.integers(0, 50, size=(N, 3)).astype(np.int32)
+    cos, sin = O.rope_tables(co, split)
+    for inverse, direction in ((0, 1), (1, -1)):
+        ref = np.empty_like(x)
+        assert L.ref_rope3d(x.ctypes.data, N, heads, (ctypes.c_int * 3)(*split), co.ctypes.data, 10000.0, inverse,
+                            ref.ctypes.data) == 0
+        assert np.max(np.abs(ref - O.rope_apply(x, cos, sin, heads, direction))) < 1e-13
