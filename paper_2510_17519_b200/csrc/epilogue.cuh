@@ -97,6 +97,32 @@ struct EpiStore {
     }
 };
 
+// Tensor-parallel row-parallel GEMM (attn.out / xattn.out / ffn.out and their dgrad conjugates):
+// the epilogue performs the reduce-scatter transfer of the TP exchange tile by tile.  Row m of this rank's
+// fp32 partial goes straight into this rank's slot of the mailbox of the rank that owns rows
+// [o*rpr, (o+1)*rpr), over NVLink peer memory for o != self (tp_peer.cu sums the slots in rank order).
+constexpr int kMaxTp = 8;
+struct EpiF32Peer {
+    float* box[kMaxTp];  // box[o]: this rank's slot (rpr x ldo fp32) in owner o's mailbox
+    int64_t ldo;
+    float alpha;
+    int rpr, M, N;
+    __device__ __forceinline__ void operator()(int m, int n0, const float* v, int cnt) const {
+        if (m >= M) return;
+        const int o = m / rpr;
+        float* p = box[o] + (int64_t)(m - o * rpr) * ldo + n0;
+        if (cnt == 16 && n0 + 16 <= N && al16(p)) {
+            float r[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r[j] = alpha * (v[j] + 0.0f);  // the bits EpiF32 writes
+            Vec16<float>::store(p, r);
+            return;
+        }
+        for (int j = 0; j < cnt; ++j)
+            if (n0 + j < N) p[j] = alpha * (v[j] + 0.0f);
+    }
+};
+
 // fp32 output, optionally accumulating into what is there (dgrad into dX, wgrad over samples)
 struct EpiF32 {
     float* out;
@@ -115,7 +141,7 @@ struct EpiF32 {
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
                 r[j] = alpha * (v[j] + (bias ? b[j] : 0.0f));
-                if (accumulate) r[j] += prev[j];
+                if (accumulate) r[j] = __fadd_rn(r[j], prev[j]);  // no FMA: the sum of rounded partials
             }
             Vec16<float>::store(o, r);
             return;
@@ -124,7 +150,7 @@ struct EpiF32 {
             int n = n0 + j;
             if (n < N) {
                 float r = alpha * (v[j] + (bias ? bias[n] : 0.0f));
-                o[j] = accumulate ? o[j] + r : r;
+                o[j] = accumulate ? __fadd_rn(o[j], r) : r;
             }
         }
     }

@@ -7,12 +7,14 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <unordered_map>
 
 #include "attn.h"
 #include "gemm.cuh"
 #include "kernels.h"
+#include "tp_peer.h"
 
 namespace mgv {
 
@@ -291,6 +293,7 @@ Model::~Model() {
     }
     if (grad_buf_) cudaFree(grad_buf_);
     if (comm_) ncclCommDestroy(comm_);
+    tp_peer_release();
     if (tp_comm_) ncclCommDestroy(tp_comm_);
     if (opt_m_) cudaFree(opt_m_);
     if (opt_v_) cudaFree(opt_v_);
@@ -322,6 +325,9 @@ void Model::set_tp(int size, int rank, const uint8_t* id) {
         ncclCommDestroy(tp_comm_);
         tp_comm_ = nullptr;
     }
+    tp_peer_release();
+    tpx_epoch_ = 0;
+    if (const char* x = std::getenv("MGV_TP_EXCHANGE")) tp_peer_ = std::strcmp(x, "nccl") != 0;
     tp_ = size;
     tp_rank_ = id ? rank : 0;
     tp_virtual_ = id == nullptr;
@@ -346,6 +352,125 @@ void Model::tp_allreduce(float* buf, int64_t n, cudaStream_t s) {
     prof_.begin("tp_allreduce", s);
     MGV_NCCL(ncclAllReduce(buf, buf, n, ncclFloat, ncclSum, tp_comm_, s));
     prof_.end(s);
+}
+
+// ---- peer-memory TP exchange (protocol in tp_peer.h)
+static int64_t tpx_rpr(int64_t N, int P) { return (N + P - 1) / P; }
+static float* tpx_mbox(char* base) { return reinterpret_cast<float*>(base + kTpFlagBytes); }
+static float* tpx_result(char* base, int P, int64_t rpr, int64_t H) { return tpx_mbox(base) + P * rpr * H; }
+static unsigned long long* tpx_flags(char* base, int phase) {
+    return reinterpret_cast<unsigned long long*>(base) + phase * kMaxTp;
+}
+
+// epilogue of rank src's row-parallel GEMM: its rows of owner o go to slot src of o's mailbox
+static EpiF32Peer tp_epi(char* const* base, int P, int src, float alpha, int64_t N, int64_t H) {
+    const int64_t rpr = tpx_rpr(N, P);
+    EpiF32Peer e{};
+    for (int o = 0; o < P; ++o) e.box[o] = tpx_mbox(base[o]) + src * rpr * H;
+    e.ldo = H;
+    e.alpha = alpha;
+    e.rpr = static_cast<int>(rpr);
+    e.M = static_cast<int>(N);
+    e.N = static_cast<int>(H);
+    return e;
+}
+
+void Model::tp_peer_release() {
+    if (!tpx_own_) return;
+    cudaSetDevice(device_);
+    if (!tp_virtual_)
+        for (int o = 0; o < tp_; ++o)
+            if (o != tp_rank_ && tpx_base_[o]) cudaIpcCloseMemHandle(tpx_base_[o]);
+    cudaFree(tpx_own_);
+    tpx_own_ = nullptr;
+    tpx_bytes_ = 0;
+    for (char*& b : tpx_base_) b = nullptr;
+}
+
+// Collective over the TP group when the arena grows (every rank runs the same N).  The arena of each rank
+// holds flags + mailbox + result for rpr = ceil(N/P) rows; real ranks map each other's arenas with CUDA IPC,
+// the handles travel over the TP communicator.
+void Model::tp_peer_ensure(int64_t N) {
+    if (!tp_peer_on()) return;
+    const int P = tp_;
+    const int64_t H = cfg_.H();
+    if (H % 4 != 0) throw ConfigError("the peer-memory TP exchange needs hidden % 4 == 0");
+    const int64_t need = kTpFlagBytes + 2 * P * tpx_rpr(N, P) * H * (int64_t)sizeof(float);
+    if (need <= tpx_bytes_) return;
+    MGV_CUDA(cudaSetDevice(device_));
+    MGV_CUDA(cudaStreamSynchronize(stream_));
+    if (tpx_own_ && !tp_virtual_) {  // peers must be done with the old arenas before they go away
+        float* one = nullptr;
+        MGV_CUDA(cudaMalloc(&one, sizeof(float)));
+        MGV_NCCL(ncclAllReduce(one, one, 1, ncclFloat, ncclSum, tp_comm_, stream_));
+        MGV_CUDA(cudaStreamSynchronize(stream_));
+        cudaFree(one);
+    }
+    tp_peer_release();
+    const int copies = tp_virtual_ ? P : 1;
+    MGV_CUDA(cudaMalloc(&tpx_own_, need * copies));
+    MGV_CUDA(cudaMemset(tpx_own_, 0, need * copies));
+    MGV_CUDA(cudaDeviceSynchronize());
+    tpx_bytes_ = need;
+    tpx_epoch_ = 0;
+    if (tp_virtual_) {
+        for (int o = 0; o < P; ++o) tpx_base_[o] = tpx_own_ + o * need;
+        return;
+    }
+    cudaIpcMemHandle_t mine;
+    MGV_CUDA(cudaIpcGetMemHandle(&mine, tpx_own_));
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    char* dev = nullptr;
+    MGV_CUDA(cudaMalloc(&dev, hb * P));
+    MGV_CUDA(cudaMemcpy(dev + hb * tp_rank_, &mine, hb, cudaMemcpyHostToDevice));
+    MGV_NCCL(ncclAllGather(dev + hb * tp_rank_, dev, hb, ncclChar, tp_comm_, stream_));
+    std::vector<cudaIpcMemHandle_t> all(P);
+    MGV_CUDA(cudaStreamSynchronize(stream_));
+    MGV_CUDA(cudaMemcpy(all.data(), dev, hb * P, cudaMemcpyDeviceToHost));
+    cudaFree(dev);
+    for (int o = 0; o < P; ++o) {
+        if (o == tp_rank_) {
+            tpx_base_[o] = tpx_own_;
+            continue;
+        }
+        void* p = nullptr;
+        MGV_CUDA(cudaIpcOpenMemHandle(&p, all[o], cudaIpcMemLazyEnablePeerAccess));
+        tpx_base_[o] = static_cast<char*>(p);
+    }
+}
+
+// The exchange after the row-parallel GEMMs (whose epilogues already wrote the mailboxes): returns the
+// summed N x H fp32 partial (peer mode: this rank's result region; NCCL mode: `part`, all-reduced in place).
+float* Model::tp_exchange(float* part, int64_t N, cudaStream_t s) {
+    if (!tp_peer_on()) {
+        tp_allreduce(part, N * cfg_.H(), s);
+        return part;
+    }
+    prof_.begin("tp_exchange", s);
+    const int P = tp_;
+    const int64_t H = cfg_.H(), rpr = tpx_rpr(N, P);
+    const uint64_t e = ++tpx_epoch_;
+    const std::vector<int> ranks = tp_ranks();
+    auto signal = [&](int src, int phase) {
+        TpFlagPtrs f{};
+        for (int o = 0; o < P; ++o) f.f[o] = tpx_flags(tpx_base_[o], phase) + src;
+        tp_signal(f, P, e, s);
+    };
+    for (int k : ranks) signal(k, 0);
+    for (int k : ranks) {
+        const int64_t rows = std::max<int64_t>(0, std::min<int64_t>(rpr, N - k * rpr));
+        TpDstPtrs d{};
+        int nd = 0;
+        if (tp_virtual_)  // emulated ranks share one set of activation buffers: one result region
+            d.p[nd++] = tpx_result(tpx_base_[0], P, rpr, H) + k * rpr * H;
+        else
+            for (int j = 0; j < P; ++j) d.p[nd++] = tpx_result(tpx_base_[j], P, rpr, H) + k * rpr * H;
+        tp_reduce_gather(tpx_mbox(tpx_base_[k]), P, rpr, rows, H, d, nd, tpx_flags(tpx_base_[k], 0), e, s);
+    }
+    for (int k : ranks) signal(k, 1);
+    for (int k : ranks) tp_wait(tpx_flags(tpx_base_[k], 1), P, e, s);
+    prof_.end(s);
+    return tpx_result(tpx_base_[tp_virtual_ ? 0 : tp_rank_], P, rpr, H);
 }
 
 // Sharded parameters: rank r computes only its rows / columns of these gradients, the rest
@@ -825,6 +950,15 @@ void Model::block_fwd_tp(int i, int64_t N) {
     const std::vector<int> ranks = tp_ranks();
     auto acc = [&](size_t k) { return tp_virtual_ && k > 0 ? 1 : 0; };
     float* part = w.tpp;
+    const float* sum = nullptr;
+    // row-parallel GEMM: peer mode scatters the partial into the owners' mailboxes from the epilogue
+    auto rowpar = [&](size_t k, int64_t r, const auto& A, const auto& B, int K, float alpha) {
+        if (tp_peer_on())
+            gemm(bf, A, B, n, int(H), K, tp_epi(tpx_base_, tp_, int(r), alpha, N, H), s);
+        else
+            gemm(bf, A, B, n, int(H), K, EpiF32{part, H, nullptr, alpha, acc(k), n, int(H)}, s);
+    };
+    tp_peer_ensure(N);
     // self-attention (dit.cpp:287-297): column-parallel qkv, local heads, row-parallel out-proj
     rms_mod<T>(Xin, n, H, tab, tld, 0, H, w.mod_id, tp<T>(b.a), b.r0, s);
     for (size_t k = 0; k < ranks.size(); ++k) {
@@ -841,11 +975,10 @@ void Model::block_fwd_tp(int i, int64_t N) {
         prof_.begin("attn_fwd", s);
         attention_fwd<T>(bf, ap, s);
         prof_.end(s);
-        gemm(bf, KM(off<T>(b.O, r * Hr), H), KM(off<T>(W(blk(i, "attn.out.w")), r * Hr), H), n, H, int(Hr),
-             EpiF32{part, H, nullptr, 1.0f, acc(k), n, int(H)}, s);
+        rowpar(k, r, KM(off<T>(b.O, r * Hr), H), KM(off<T>(W(blk(i, "attn.out.w")), r * Hr), H), int(Hr), 1.0f);
     }
-    tp_allreduce(part, N * H, s);
-    bias_gate_resid<T>(part, P(blk(i, "attn.out.b")).f32, tab, tld, int(2 * H), w.mod_id, Xin, b.X1, tp<T>(b.ao), n,
+    sum = tp_exchange(part, N, s);
+    bias_gate_resid<T>(sum, P(blk(i, "attn.out.b")).f32, tab, tld, int(2 * H), w.mod_id, Xin, b.X1, tp<T>(b.ao), n,
                        int(H), s);
     // cross-attention (dit.cpp:300-305)
     rms_gain<T>(b.X1, n, H, P(blk(i, "xattn.prenorm.g")).f32, tp<T>(b.cn), b.r1, s);
@@ -863,11 +996,10 @@ void Model::block_fwd_tp(int i, int64_t N) {
         prof_.begin("xattn_fwd", s);
         attention_fwd<T>(bf, xp, s);
         prof_.end(s);
-        gemm(bf, KM(off<T>(b.Ox, r * Hr), H), KM(off<T>(W(blk(i, "xattn.out.w")), r * Hr), H), n, H, int(Hr),
-             EpiF32{part, H, nullptr, 1.0f, acc(k), n, int(H)}, s);
+        rowpar(k, r, KM(off<T>(b.Ox, r * Hr), H), KM(off<T>(W(blk(i, "xattn.out.w")), r * Hr), H), int(Hr), 1.0f);
     }
-    tp_allreduce(part, N * H, s);
-    bias_to<T>(part, P(blk(i, "xattn.out.b")).f32, tp<T>(b.co), n, int(H), s);
+    sum = tp_exchange(part, N, s);
+    bias_to<T>(sum, P(blk(i, "xattn.out.b")).f32, tp<T>(b.co), n, int(H), s);
     postnorm_resid<T>(b.X1, tp<T>(b.co), n, H, P(blk(i, "xattn.postnorm.g")).f32, b.X2, b.rc, s);
     // feed-forward (dit.cpp:308-311): column-parallel ffn.in, row-parallel ffn.out
     rms_mod<T>(b.X2, n, H, tab, tld, 3 * H, 4 * H, w.mod_id, tp<T>(b.f), b.r2, s);
@@ -877,11 +1009,10 @@ void Model::block_fwd_tp(int i, int64_t N) {
              EpiBiasSilu<T>{tp<T>(off<T>(b.z, r * Fr)), tp<T>(off<T>(b.h, r * Fr)), 4 * H,
                             P(blk(i, "ffn.in.b")).f32 + r * Fr, n, int(Fr)},
              s);
-        gemm(bf, KM(off<T>(b.h, r * Fr), 4 * H), KM(off<T>(W(blk(i, "ffn.out.w")), r * Fr), 4 * H), n, H, int(Fr),
-             EpiF32{part, H, nullptr, 1.0f, acc(k), n, int(H)}, s);
+        rowpar(k, r, KM(off<T>(b.h, r * Fr), 4 * H), KM(off<T>(W(blk(i, "ffn.out.w")), r * Fr), 4 * H), int(Fr), 1.0f);
     }
-    tp_allreduce(part, N * H, s);
-    bias_gate_resid<T>(part, P(blk(i, "ffn.out.b")).f32, tab, tld, int(5 * H), w.mod_id, b.X2, Xout, tp<T>(b.ff), n,
+    sum = tp_exchange(part, N, s);
+    bias_gate_resid<T>(sum, P(blk(i, "ffn.out.b")).f32, tab, tld, int(5 * H), w.mod_id, b.X2, Xout, tp<T>(b.ff), n,
                        int(H), s);
 }
 
@@ -902,6 +1033,15 @@ void Model::block_bwd_tp(int i, int64_t N) {
     const std::vector<int> ranks = tp_ranks();
     auto acc = [&](size_t k) { return tp_virtual_ && k > 0 ? 1 : 0; };
     float* part = w.tpp;
+    const float* sum = nullptr;
+    // row-parallel GEMM: peer mode scatters the partial into the owners' mailboxes from the epilogue
+    auto rowpar = [&](size_t k, int64_t r, const auto& A, const auto& B, int K, float alpha) {
+        if (tp_peer_on())
+            gemm(bf, A, B, n, int(H), K, tp_epi(tpx_base_, tp_, int(r), alpha, N, H), s);
+        else
+            gemm(bf, A, B, n, int(H), K, EpiF32{part, H, nullptr, alpha, acc(k), n, int(H)}, s);
+    };
+    tp_peer_ensure(N);
     // ---- FFN (dit.cpp:308-311)
     gate_bwd<T>(dX, tp<T>(b.ff), tab, tld, 5 * H, w.mod_id, nu, n, H, tp<T>(w.s1), w.part1, w.part2, s);
     reduce_chunks_grouped(w.part1, chunks, nu, H, dm + 5 * H, 6 * H, 1.0f, 0, s);  // d gt2
@@ -917,11 +1057,10 @@ void Model::block_bwd_tp(int i, int64_t N) {
         reduce_chunks(w.part1, chunks, int(Fr), G(blk(i, "ffn.in.b")) + r * Fr, 1.0f, 1, s);
         gemm(bf, MN(dz_r, 4 * H), MN(b.f, H), int(Fr), H, n,
              EpiF32{G(blk(i, "ffn.in.w")) + r * Fr * H, H, nullptr, 1.0f, 1, int(Fr), int(H)}, s);
-        gemm(bf, KM(dz_r, 4 * H), MN(off<T>(W(blk(i, "ffn.in.w")), r * Fr * H), H), n, H, int(Fr),
-             EpiF32{part, H, nullptr, 1.0f, acc(k), n, int(H)}, s);  // df partial
+        rowpar(k, r, KM(dz_r, 4 * H), MN(off<T>(W(blk(i, "ffn.in.w")), r * Fr * H), H), int(Fr), 1.0f);  // df partial
     }
-    tp_allreduce(part, N * H, s);
-    convert_f32<T>(part, N * H, tp<T>(w.s1), s);
+    sum = tp_exchange(part, N, s);
+    convert_f32<T>(sum, N * H, tp<T>(w.s1), s);
     rms_mod_bwd<T>(tp<T>(w.s1), b.X2, b.r2, tab, tld, 3 * H, 4 * H, w.mod_id, nu, n, H, dX, w.part1, w.part2, s);
     reduce_chunks_grouped(w.part1, chunks, nu, H, dm + 3 * H, 6 * H, 1.0f, 0, s);  // d sh2
     reduce_chunks_grouped(w.part2, chunks, nu, H, dm + 4 * H, 6 * H, 1.0f, 0, s);  // d sc2
@@ -959,11 +1098,10 @@ void Model::block_bwd_tp(int i, int64_t N) {
         reduce_chunks(w.part1, chunks, int(Hr), G(blk(i, "xattn.q.b")) + r * Hr, xscale, 1, s);
         gemm(bf, MN(dq_r, H), MN(b.cn, H), int(Hr), H, n,
              EpiF32{G(blk(i, "xattn.q.w")) + r * Hr * H, H, nullptr, xscale, 1, int(Hr), int(H)}, s);
-        gemm(bf, KM(dq_r, H), MN(off<T>(W(blk(i, "xattn.q.w")), r * Hr * H), H), n, H, int(Hr),
-             EpiF32{part, H, nullptr, xscale, acc(k), n, int(H)}, s);  // dcn partial
+        rowpar(k, r, KM(dq_r, H), MN(off<T>(W(blk(i, "xattn.q.w")), r * Hr * H), H), int(Hr), xscale);  // dcn partial
     }
-    tp_allreduce(part, N * H, s);
-    convert_f32<T>(part, N * H, tp<T>(w.s2), s);
+    sum = tp_exchange(part, N, s);
+    convert_f32<T>(sum, N * H, tp<T>(w.s2), s);
     rms_gain_bwd<T>(tp<T>(w.s2), b.X1, b.r1, P(blk(i, "xattn.prenorm.g")).f32, n, H, dX, 1, w.part1, s);
     reduce_chunks(w.part1, chunks, H, G(blk(i, "xattn.prenorm.g")), 1.0f, 1, s);
     // ---- self-attention (dit.cpp:287-297)
@@ -997,11 +1135,11 @@ void Model::block_bwd_tp(int i, int64_t N) {
         reduce_chunks(w.part1, chunks, int(3 * Hr), G(blk(i, "attn.qkv.b")) + r * 3 * Hr, 1.0f, 1, s);
         gemm(bf, MN(dqkv_r, 3 * H), MN(b.a, H), int(3 * Hr), H, n,
              EpiF32{G(blk(i, "attn.qkv.w")) + r * 3 * Hr * H, H, nullptr, 1.0f, 1, int(3 * Hr), int(H)}, s);
-        gemm(bf, KM(dqkv_r, 3 * H), MN(off<T>(W(blk(i, "attn.qkv.w")), r * 3 * Hr * H), H), n, H, int(3 * Hr),
-             EpiF32{part, H, nullptr, 1.0f, acc(k), n, int(H)}, s);  // da partial
+        rowpar(k, r, KM(dqkv_r, 3 * H), MN(off<T>(W(blk(i, "attn.qkv.w")), r * 3 * Hr * H), H), int(3 * Hr),
+               1.0f);  // da partial
     }
-    tp_allreduce(part, N * H, s);
-    convert_f32<T>(part, N * H, tp<T>(w.s1), s);
+    sum = tp_exchange(part, N, s);
+    convert_f32<T>(sum, N * H, tp<T>(w.s1), s);
     rms_mod_bwd<T>(tp<T>(w.s1), Xin, b.r0, tab, tld, 0, H, w.mod_id, nu, n, H, dX, w.part1, w.part2, s);
     reduce_chunks_grouped(w.part1, chunks, nu, H, dm, 6 * H, 1.0f, 0, s);      // d sh1
     reduce_chunks_grouped(w.part2, chunks, nu, H, dm + H, 6 * H, 1.0f, 0, s);  // d sc1

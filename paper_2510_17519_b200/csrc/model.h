@@ -250,6 +250,16 @@ private:
     ncclComm_t tp_comm_ = nullptr;
     int tp_ = 1, tp_rank_ = 0;
     bool tp_virtual_ = false;
+    // peer-memory TP exchange (tp_peer.h); MGV_TP_EXCHANGE=nccl selects the NCCL all-reduce instead
+    bool tp_peer_ = true;
+    char* tpx_base_[8] = {};  // every rank's arena as mapped here (emulated ranks: slices of tpx_own_)
+    char* tpx_own_ = nullptr;
+    int64_t tpx_bytes_ = 0;   // capacity per rank arena
+    uint64_t tpx_epoch_ = 0;
+    bool tp_peer_on() const { return tp_ > 1 && tp_peer_; }
+    void tp_peer_ensure(int64_t N);
+    void tp_peer_release();
+    float* tp_exchange(float* part, int64_t N, cudaStream_t s);
 
     // ---- per-sample workspace views (set by plan_workspace / forward)
 public:

@@ -57,3 +57,39 @@ def test_tp_config_errors():
     ctx2.upload(to_cfg(cfg), P)
     with pytest.raises(MugvError):
         ctx2.set_tp(2)  # after upload
+
+
+# N not a multiple of P (45 tokens over 4 ranks) and a sample with fewer tokens than ranks (3 over 4): ranks
+# own ceil(N/P) rows, the last owners fewer or none.
+RAGGED = dict(CASES["cfg0"], grids=[(3, 6, 10), (1, 2, 6)], mask_prob=0.5, force_cond=[])
+
+
+@pytest.mark.parametrize("name,size", [("hd144", 2), ("cfg0", 4), ("ragged", 4)])
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_tp_peer_exchange(name, size, prec, monkeypatch):
+    """The peer-memory exchange (row-parallel GEMM epilogue scatters into the owners' mailboxes, owners sum the
+    slots in rank order and all-gather the rows; tp_peer.h) against the in-place accumulation of the partials in
+    rank order (MGV_TP_EXCHANGE=nccl with emulated ranks): the same additions in the same order, so the step must
+    be bit-identical; and against the fp64 oracle at the usual tolerance."""
+    from paper_2510_17519_b200.capi import Context
+    cfg, P, text, samples = build_case(name, RAGGED if name == "ragged" else CASES[name])
+    outs = {}
+    for mode in ["nccl", "peer"]:
+        monkeypatch.setenv("MGV_TP_EXCHANGE", mode)
+        ctx = Context(0, prec)
+        ctx.set_tp(size)
+        ctx.upload(to_cfg(cfg), P)
+        outs[mode] = ctx.flow_step(to_samples(samples), text, 8.0, grads=True, velocity=True)
+        ctx.close()
+    a, b = outs["nccl"], outs["peer"]
+    assert a["loss"] == b["loss"] and a["grad_norm"] == b["grad_norm"]
+    for i in range(len(samples)):
+        assert np.array_equal(a["V"][i], b["V"][i]), i
+    for k in a["grads"]:
+        assert np.array_equal(a["grads"][k], b["grads"][k]), k
+    ref = O.flow_fwdbwd(P, cfg, samples, text, 8.0, grads=True)
+    worst = max(nerr(b["grads"][k], g) for k, g in ref["grads"].items())
+    worst = max([worst, abs(b["loss"] - ref["loss"]) / abs(ref["loss"])] +
+                [nerr(b["V"][i], ref["V"][i]) for i in range(len(samples))])
+    print(f"tp{size} peer {name}/{prec}: worst {worst:.3e}")
+    assert worst <= TOL[prec]
