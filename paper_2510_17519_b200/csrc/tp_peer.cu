@@ -26,6 +26,9 @@ __global__ void tp_wait_kernel(const unsigned long long* flags, int P, unsigned 
     __syncthreads();
 }
 
+// All P slot loads of an element are issued before the adds (P <= kMaxTp, compile-time unrolled), the sum
+// is taken in rank order.  Peer-written data is read with ld.global.cg (L2, no L1 allocation).
+template <int PM>
 __global__ void __launch_bounds__(256) tp_reduce_gather_kernel(const float* __restrict__ mbox, int P, int64_t slot4,
                                                                int64_t n4, TpDstPtrs dst, int ndst,
                                                                const unsigned long long* flags,
@@ -35,15 +38,20 @@ __global__ void __launch_bounds__(256) tp_reduce_gather_kernel(const float* __re
     __syncthreads();
     const float4* src = reinterpret_cast<const float4*>(mbox);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-        float4 a = __ldcv(src + i);  // written by peers over NVLink: bypass L1
-        for (int k = 1; k < P; ++k) {
-            const float4 b = __ldcv(src + k * slot4 + i);
-            a.x += b.x;
-            a.y += b.y;
-            a.z += b.z;
-            a.w += b.w;
-        }
-        for (int j = 0; j < ndst; ++j) reinterpret_cast<float4*>(dst.p[j])[i] = a;
+        float4 b[PM];
+#pragma unroll
+        for (int k = 0; k < PM; ++k)
+            if (k < P) b[k] = __ldcg(src + k * slot4 + i);
+        float4 a = b[0];
+#pragma unroll
+        for (int k = 1; k < PM; ++k)
+            if (k < P) {
+                a.x += b[k].x;
+                a.y += b[k].y;
+                a.z += b[k].z;
+                a.w += b[k].w;
+            }
+        for (int j = 0; j < ndst; ++j) __stcg(reinterpret_cast<float4*>(dst.p[j]) + i, a);
     }
 }
 
@@ -63,8 +71,13 @@ void tp_reduce_gather(const float* mbox, int P, int64_t rpr, int64_t rows, int64
                       const unsigned long long* flags, uint64_t epoch, cudaStream_t s) {
     const int64_t n4 = rows > 0 ? rows * H / 4 : 0;
     const int64_t want = (n4 + 255) / 256;
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, 4LL * num_sms())));
-    tp_reduce_gather_kernel<<<grid, 256, 0, s>>>(mbox, P, rpr * H / 4, n4, dst, ndst, flags, epoch);
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, 8LL * num_sms())));
+    if (P <= 2)
+        tp_reduce_gather_kernel<2><<<grid, 256, 0, s>>>(mbox, P, rpr * H / 4, n4, dst, ndst, flags, epoch);
+    else if (P <= 4)
+        tp_reduce_gather_kernel<4><<<grid, 256, 0, s>>>(mbox, P, rpr * H / 4, n4, dst, ndst, flags, epoch);
+    else
+        tp_reduce_gather_kernel<kMaxTp><<<grid, 256, 0, s>>>(mbox, P, rpr * H / 4, n4, dst, ndst, flags, epoch);
     note_launch();
     MGV_CUDA(cudaGetLastError());
 }
