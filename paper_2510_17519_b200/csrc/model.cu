@@ -293,6 +293,7 @@ Model::~Model() {
     }
     if (grad_buf_) cudaFree(grad_buf_);
     if (comm_) ncclCommDestroy(comm_);
+    if (dp_stream_) cudaStreamDestroy(dp_stream_);
     tp_peer_release();
     if (tp_comm_) ncclCommDestroy(tp_comm_);
     if (opt_m_) cudaFree(opt_m_);
@@ -315,6 +316,53 @@ void Model::set_dp(int rank, int world, const uint8_t id[128]) {
     std::memcpy(&uid, id, sizeof(uid));
     MGV_CUDA(cudaSetDevice(device_));
     MGV_NCCL(ncclCommInitRank(&comm_, world, uid, rank));
+    if (!dp_stream_) MGV_CUDA(cudaStreamCreateWithFlags(&dp_stream_, cudaStreamNonBlocking));
+}
+
+// Gradient buckets of the data-parallel all-reduce (see model.h).  Names are sorted, so one block's
+// "dit.blk.<i>.<group>" parameters are one contiguous range of the gradient buffer.
+void Model::dp_bucket(int block, const char* group) {
+    if (!dp_overlap_) return;
+    const std::string pre = "dit.blk." + std::to_string(block) + "." + group;
+    int64_t lo = -1, hi = -1;
+    for (const DevParam* q : sorted_)
+        if (q->name.compare(0, pre.size(), pre) == 0) {
+            if (lo < 0) lo = q->grad_off;
+            hi = q->grad_off + q->numel;
+        }
+    if (lo < 0) return;
+    cudaEvent_t ev;
+    MGV_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    MGV_CUDA(cudaEventRecord(ev, stream_));
+    MGV_CUDA(cudaStreamWaitEvent(dp_stream_, ev, 0));
+    MGV_CUDA(cudaEventDestroy(ev));
+    MGV_NCCL(ncclAllReduce(grad_buf_ + lo, grad_buf_ + lo, hi - lo, ncclFloat, ncclSum, comm_, dp_stream_));
+    dp_done_.emplace_back(lo, hi - lo);
+}
+
+// The rest of the gradient buffer (every range no bucket covered) and the loss, then the step stream
+// waits for all DP collectives.
+void Model::dp_finish(double* scal) {
+    cudaEvent_t ev;
+    MGV_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    MGV_CUDA(cudaEventRecord(ev, stream_));
+    MGV_CUDA(cudaStreamWaitEvent(dp_stream_, ev, 0));
+    std::vector<std::pair<int64_t, int64_t>> done = dp_done_;
+    std::sort(done.begin(), done.end());
+    MGV_NCCL(ncclGroupStart());
+    int64_t at = 0;
+    for (const auto& d : done) {
+        if (d.first > at) MGV_NCCL(ncclAllReduce(grad_buf_ + at, grad_buf_ + at, d.first - at, ncclFloat, ncclSum, comm_, dp_stream_));
+        at = std::max(at, d.first + d.second);
+    }
+    if (at < grad_numel_)
+        MGV_NCCL(ncclAllReduce(grad_buf_ + at, grad_buf_ + at, grad_numel_ - at, ncclFloat, ncclSum, comm_, dp_stream_));
+    MGV_NCCL(ncclAllReduce(scal, scal, 1, ncclDouble, ncclSum, comm_, dp_stream_));
+    MGV_NCCL(ncclGroupEnd());
+    MGV_CUDA(cudaEventRecord(ev, dp_stream_));
+    MGV_CUDA(cudaStreamWaitEvent(stream_, ev, 0));
+    MGV_CUDA(cudaEventDestroy(ev));
+    dp_done_.clear();
 }
 
 void Model::set_tp(int size, int rank, const uint8_t* id) {
@@ -877,6 +925,7 @@ void Model::block_bwd(int i, int64_t N) {
     rms_mod_bwd<T>(tp<T>(w.s1), b.X2, b.r2, tab, tld, 3 * H, 4 * H, w.mod_id, nu, n, H, dX, w.part1, w.part2, s);
     reduce_chunks_grouped(w.part1, chunks, nu, H, dm + 3 * H, 6 * H, 1.0f, 0, s);  // d sh2
     reduce_chunks_grouped(w.part2, chunks, nu, H, dm + 4 * H, 6 * H, 1.0f, 0, s);  // d sc2
+    dp_bucket(i, "ffn.");  // ffn.* gradients are final: all-reduce them under the attention backward
     // ---- cross-attention (dit.cpp:300-305)
     postnorm_bwd<T>(dX, tp<T>(b.co), b.rc, P(blk(i, "xattn.postnorm.g")).f32, n, H, tp<T>(w.s1), w.part1, s);
     reduce_chunks(w.part1, chunks, H, G(blk(i, "xattn.postnorm.g")), 1.0f, 1, s);
@@ -901,6 +950,7 @@ void Model::block_bwd(int i, int64_t N) {
     gemm(bf, KM(w.s1, H), MN(W(blk(i, "xattn.q.w")), H), n, H, H, EpiStore<T>{tp<T>(w.s2), H, nullptr, xscale, n, int(H)}, s);
     rms_gain_bwd<T>(tp<T>(w.s2), b.X1, b.r1, P(blk(i, "xattn.prenorm.g")).f32, n, H, dX, 1, w.part1, s);
     reduce_chunks(w.part1, chunks, H, G(blk(i, "xattn.prenorm.g")), 1.0f, 1, s);
+    dp_bucket(i, "xattn.");
     // ---- self-attention (dit.cpp:287-297)
     gate_bwd<T>(dX, tp<T>(b.ao), tab, tld, 2 * H, w.mod_id, nu, n, H, tp<T>(w.s1), w.part1, w.part2, s);
     reduce_chunks_grouped(w.part1, chunks, nu, H, dm + 2 * H, 6 * H, 1.0f, 0, s);  // d gt1
@@ -1306,7 +1356,10 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
         if (backward && wk != 0.0) {
             flow_loss_bwd<T>(w.V, w.vt, w.lmask, N, int(D), static_cast<float>(2.0 * wk), w.cnt, tp<T>(w.dV),
                              s);  // 2 w_k (V - v*) / (n_b * D), w_k = 1 / B in FlowTrainer::step; all-masked -> 0
+            dp_overlap_ = comm_ != nullptr && !ex && k == n - 1;
+            dp_done_.clear();
             backward_sample<T>(w.dV);
+            dp_overlap_ = false;
         }
     }
     if (ex) {
@@ -1331,8 +1384,7 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
     tp_allreduce_grads(s);
     if (comm_) {
         prof_.begin("allreduce", s);
-        MGV_NCCL(ncclAllReduce(grad_buf_, grad_buf_, grad_numel_, ncclFloat, ncclSum, comm_, s));
-        MGV_NCCL(ncclAllReduce(w.scal, w.scal, 1, ncclDouble, ncclSum, comm_, s));
+        dp_finish(w.scal);
         prof_.end(s);
     }
     sumsq(grad_buf_, grad_numel_, w.loss_part, w.scal + 2, s);  // grad_norm (flowtrain.cpp:284-289)

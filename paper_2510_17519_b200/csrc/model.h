@@ -233,9 +233,16 @@ private:
     double last_ms_ = 0.0;
     int64_t last_launches_ = 0;
     Prof prof_;
-    // NCCL data parallel
+    // NCCL data parallel.  The gradient all-reduce is bucketed: during the last local sample's backward the
+    // FFN and cross-attention gradients of each block are all-reduced on dp_stream_ as soon as they are final
+    // (overlapping the attention backward); dp_finish reduces the rest.  All DP collectives use dp_stream_.
     ncclComm_t comm_ = nullptr;
     int rank_ = 0, world_ = 1;
+    cudaStream_t dp_stream_ = nullptr;
+    bool dp_overlap_ = false;
+    std::vector<std::pair<int64_t, int64_t>> dp_done_;  // (offset, length) of the buckets already reduced
+    void dp_bucket(int block, const char* group);
+    void dp_finish(double* scal);
     // AdamW state: m, v in the gradient buffer's layout; per-parameter table for the multi-tensor update
     struct Adam {
         bool on = false;

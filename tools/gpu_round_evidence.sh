@@ -1,0 +1,9 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/smi.txt
+timeout 900 python -m pytest tests -m gpu -x -q -rs > gpurun_out/gputests.log 2>&1; echo tests_rc=$? >> gpurun_out/gputests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$? >> gpurun_out/smoke.log
+timeout 500 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
+timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv --log-file gpurun_out/launches_final.csv python bench.py --steps 2 --warmup 1 --no-extra --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_bwd_dkv_v8 --launch-skip 1 -c 1 -o gpurun_out/dkv_final -f python bench.py --steps 1 --warmup 0 --no-extra --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+echo all_done
