@@ -316,7 +316,11 @@ void Model::set_dp(int rank, int world, const uint8_t id[128]) {
     std::memcpy(&uid, id, sizeof(uid));
     MGV_CUDA(cudaSetDevice(device_));
     MGV_NCCL(ncclCommInitRank(&comm_, world, uid, rank));
-    if (!dp_stream_) MGV_CUDA(cudaStreamCreateWithFlags(&dp_stream_, cudaStreamNonBlocking));
+    if (!dp_stream_) {  // highest priority: the all-reduce CTAs are dispatched ahead of pending attention CTAs
+        int least = 0, greatest = 0;
+        MGV_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        MGV_CUDA(cudaStreamCreateWithPriority(&dp_stream_, cudaStreamNonBlocking, greatest));
+    }
 }
 
 // Gradient buckets of the data-parallel all-reduce (see model.h).  Names are sorted, so one block's
