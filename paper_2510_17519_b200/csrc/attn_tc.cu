@@ -64,6 +64,23 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
+// packed fp32 pairs (sm_100a FFMA2 / FADD2)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)),
+          "l"(*reinterpret_cast<const uint64_t*>(&c)));
+    return *reinterpret_cast<const float2*>(&d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
+    return *reinterpret_cast<const float2*>(&d);
+}
+
 // 2^x on the FMA pipe (Cody-Waite: x = n + f, f in [0,1); degree-3 minimax for 2^f, max rel. error ~9e-5,
 // below the bf16 rounding of P).  Used for a share of the softmax exponentials so the MUFU pipe (16/clk/SM) and
 // the FMA pipe share them.  x <= 0 here (max-subtracted logits); clamped so the exponent field cannot wrap.
@@ -246,24 +263,28 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_tc_kernel(const __grid_consta
                 m_use = mx;
                 alpha = ex2(m2 - mx);
             }
-            float ps8[8];
+            // the softmax warps are issue-bound: the scale/shift and the row sum run as packed f32x2
+            // instructions (FFMA2 / FADD2), two columns per instruction
+            float2 ps2[4];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) ps8[e] = 0.0f;
+            for (int e = 0; e < 4; ++e) ps2[e] = make_float2(0.0f, 0.0f);
+            const float2 lg2 = make_float2(kLog2e, kLog2e), nm2 = make_float2(-m_use, -m_use);
             uint32_t pk[BN / 2];
 #pragma unroll
             for (int c = 0; c < BN; c += 2) {
-                float p0, p1;
+                const float2 x = ffma2(make_float2(s[c], s[c + 1]), lg2, nm2);
+                float2 pp;
                 if (POLY > 0 && (c / 2) % POLY == POLY - 1) {
-                    p0 = ex2_fma(fmaf(s[c], kLog2e, -m_use));
-                    p1 = ex2_fma(fmaf(s[c + 1], kLog2e, -m_use));
+                    pp.x = ex2_fma(x.x);
+                    pp.y = ex2_fma(x.y);
                 } else {
-                    p0 = ex2(fmaf(s[c], kLog2e, -m_use));
-                    p1 = ex2(fmaf(s[c + 1], kLog2e, -m_use));
+                    pp.x = ex2(x.x);
+                    pp.y = ex2(x.y);
                 }
-                ps8[(c / 2) & 7] += p0 + p1;
-                pk[c / 2] = pack_bf16(p0, p1);
+                ps2[(c / 2) & 3] = fadd2(ps2[(c / 2) & 3], pp);
+                pk[c / 2] = pack_bf16(pp.x, pp.y);
             }
-            const float ps = ((ps8[0] + ps8[1]) + (ps8[2] + ps8[3])) + ((ps8[4] + ps8[5]) + (ps8[6] + ps8[7]));
+            const float ps = ((ps2[0].x + ps2[0].y) + (ps2[1].x + ps2[1].y)) + ((ps2[2].x + ps2[2].y) + (ps2[3].x + ps2[3].y));
             if (j >= 1 && __any_sync(0xffffffff, alpha != 1.0f)) {
                 mbar_wait(&pv_done[t], (j - 1) & 1);  // O holds exactly PV(0..j-1)
                 tc_fence_after();
