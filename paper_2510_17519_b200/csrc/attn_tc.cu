@@ -64,23 +64,6 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
-// packed fp32 pairs (sm_100a FFMA2 / FADD2)
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
-    uint64_t d;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;"
-        : "=l"(d)
-        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)),
-          "l"(*reinterpret_cast<const uint64_t*>(&c)));
-    return *reinterpret_cast<const float2*>(&d);
-}
-__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
-    uint64_t d;
-    asm("add.rn.f32x2 %0, %1, %2;"
-        : "=l"(d)
-        : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)));
-    return *reinterpret_cast<const float2*>(&d);
-}
-
 // 2^x on the FMA pipe (Cody-Waite: x = n + f, f in [0,1); degree-3 minimax for 2^f, max rel. error ~9e-5,
 // below the bf16 rounding of P).  Used for a share of the softmax exponentials so the MUFU pipe (16/clk/SM) and
 // the FMA pipe share them.  x <= 0 here (max-subtracted logits); clamped so the exponent field cannot wrap.
