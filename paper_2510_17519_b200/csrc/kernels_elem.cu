@@ -1300,9 +1300,10 @@ __global__ void __launch_bounds__(RT) postnorm_resid_vec(const float* X1, const 
 }
 
 // dY = dX * gate[u] ; partials: grouped sum dX*y, sum dY
-__global__ void __launch_bounds__(RT) gate_bwd_vec(const float* dX, const bf* y, const float* table, int64_t tld,
-                                                   int gate_off, const int32_t* mod_id, int n_u, int N, int H, bf* dY,
-                                                   float* part_dgate, float* part_db) {
+__global__ void __launch_bounds__(RT) gate_bwd_vec(const float* __restrict__ dX, const bf* __restrict__ y,
+                                                   const float* __restrict__ table, int64_t tld, int gate_off,
+                                                   const int32_t* __restrict__ mod_id, int n_u, int N, int H,
+                                                   bf* __restrict__ dY, float* part_dgate, float* part_db) {
     const int G = H / 8;
     const int r0 = blockIdx.x * kRowsPerChunk, r1 = min(N, r0 + kRowsPerChunk);
     float pg[2][VG][8], pb[VG][8];
@@ -1310,6 +1311,7 @@ __global__ void __launch_bounds__(RT) gate_bwd_vec(const float* dX, const bf* y,
     for (int k = 0; k < VG; ++k)
 #pragma unroll
         for (int e = 0; e < 8; ++e) pg[0][k][e] = pg[1][k][e] = pb[k][e] = 0.0f;
+#pragma unroll 2  // restrict + two rows in flight: the next row's loads issue before this row's stores
     for (int i = r0; i < r1; ++i) {
         const int u = mod_id[i];
         const float* gt = table + (int64_t)u * tld + gate_off;
@@ -1369,6 +1371,8 @@ __global__ void __launch_bounds__(RT, 2) rms_bwd_vec(const bf* dA, const float* 
             for (int k = 0; k < VG; ++k) {
                 const int grp = threadIdx.x + k * RT;
                 if (ok && grp < G) {
+                    // the dX accumulate read comes after the row reduction: start it now, into L2
+                    if (accumulate) asm volatile("prefetch.global.L2 [%0];" ::"l"(dX + (int64_t)row * H + grp * 8));
                     float da[8], t[8];
                     ld8(dA + (int64_t)row * H + grp * 8, da);
                     ld8(X + (int64_t)row * H + grp * 8, xv[rr][k]);
