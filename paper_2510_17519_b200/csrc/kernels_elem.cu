@@ -1599,6 +1599,18 @@ __global__ void __launch_bounds__(256) qk_norm_rope_bwd_vec(bf* dqkv, const bf* 
             float c[QRU][4], sn[QRU][4], d[2 * QRU][8], x[2 * QRU][8], iv[2 * QRU];
             int64_t off[2 * QRU];
             bool ok[2 * QRU];
+            if (act)  // the next row group's q / k slices of dqkv and qkv: start them into L2 now
+#pragma unroll
+                for (int rr = 0; rr < QRU; ++rr) {
+                    const int nn = n0 + QRU + rr;
+                    if (nn >= r1) break;
+#pragma unroll
+                    for (int which = 0; which < 2; ++which) {
+                        const int64_t o = (int64_t)nn * Lq.in_ld + which * Lq.in_koff + h * hd + 8 * lane;
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(dqkv + o));
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(qkv + o));
+                    }
+                }
 #pragma unroll
             for (int rr = 0; rr < QRU; ++rr) {
                 const int n = n0 + rr;
