@@ -1207,6 +1207,18 @@ __global__ void __launch_bounds__(RT) rms_fwd_vec(const float* X, int N, int H, 
     const int r0 = blockIdx.x * kRowsPerChunk, r1 = min(N, r0 + kRowsPerChunk);
     for (int i = r0; i < r1; i += R) {
         float v[R][VG][8], ss[R];
+        // the next row group: start its rows into L2 while this group reduces (block barrier below)
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+            const int nrow = i + R + rr;
+            if (nrow >= r1) break;
+#pragma unroll
+            for (int k = 0; k < VG; ++k) {
+                const int grp = threadIdx.x + k * RT;
+                if (grp >= G) continue;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(X + (int64_t)nrow * H + grp * 8));
+            }
+        }
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
             ss[rr] = 0.0f;
@@ -1359,6 +1371,19 @@ __global__ void __launch_bounds__(RT, 2) rms_bwd_vec(const bf* dA, const float* 
         for (int e = 0; e < 8; ++e) pa[0][k][e] = pa[1][k][e] = pb[0][k][e] = pb[1][k][e] = 0.0f;
     for (int i = r0; i < r1; i += R) {
         float xv[R][VG][8], dn[R][VG][8], dot[R];
+        // the next row group: start its rows into L2 while this group reduces (block barrier below)
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+            const int nrow = i + R + rr;
+            if (nrow >= r1) break;
+#pragma unroll
+            for (int k = 0; k < VG; ++k) {
+                const int grp = threadIdx.x + k * RT;
+                if (grp >= G) continue;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(dA + (int64_t)nrow * H + grp * 8));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(X + (int64_t)nrow * H + grp * 8));
+            }
+        }
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
             dot[rr] = 0.0f;
@@ -1452,6 +1477,19 @@ __global__ void __launch_bounds__(RT) postnorm_bwd_vec(const float* dX, const bf
         for (int e = 0; e < 8; ++e) pg[k][e] = 0.0f;
     for (int i = r0; i < r1; i += R) {
         float xv[R][VG][8], dn[R][VG][8], dot[R];
+        // the next row group: start its rows into L2 while this group reduces (block barrier below)
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+            const int nrow = i + R + rr;
+            if (nrow >= r1) break;
+#pragma unroll
+            for (int k = 0; k < VG; ++k) {
+                const int grp = threadIdx.x + k * RT;
+                if (grp >= G) continue;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(dX + (int64_t)nrow * H + grp * 8));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(co + (int64_t)nrow * H + grp * 8));
+            }
+        }
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
             dot[rr] = 0.0f;
