@@ -130,34 +130,6 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ synthetic model + inputs
-def synthetic_params(cfg, seed):
-    """Random init with the reference's shapes and scales (dit.cpp:143-183): W ~ N(0, 1/fan_in), biases 0,
-    gains/gscale 1, temp sqrt(hd); modulation/final heads opened with the width-scaled std 0.2*sqrt(12/H)."""
-    rng = np.random.default_rng(seed)
-    Hh, D = cfg.hidden, cfg.patch_dim
-    gs = 0.2 * math.sqrt(12.0 / Hh)
-
-    def lin(o, i):
-        return (rng.standard_normal((o, i), dtype=np.float32) / math.sqrt(i)).astype(np.float64)
-
-    p = {"dit.patch.w": lin(Hh, D), "dit.patch.b": np.zeros(Hh), "dit.gmlp.in.w": lin(Hh, 32),
-         "dit.gmlp.in.b": np.zeros(Hh), "dit.gmlp.out.w": lin(Hh, Hh), "dit.gmlp.out.b": np.zeros(Hh),
-         "dit.mod.w": rng.standard_normal((6 * Hh, Hh), dtype=np.float32).astype(np.float64) * gs,
-         "dit.mod.b": rng.standard_normal(6 * Hh) * gs, "dit.final.g": np.ones(Hh),
-         "dit.final.w": rng.standard_normal((Hh, Hh), dtype=np.float32).astype(np.float64) * gs,
-         "dit.final.b": rng.standard_normal(Hh) * gs / 4, "dit.out.w": lin(D, Hh), "dit.out.b": np.zeros(D)}
-    for i in range(cfg.depth):
-        b = f"dit.blk.{i}."
-        p.update({b + "gscale": np.ones(Hh), b + "attn.qkv.w": lin(3 * Hh, Hh), b + "attn.qkv.b": np.zeros(3 * Hh),
-                  b + "attn.temp": np.full(cfg.heads, math.sqrt(cfg.head_dim)), b + "attn.out.w": lin(Hh, Hh),
-                  b + "attn.out.b": np.zeros(Hh), b + "xattn.prenorm.g": np.ones(Hh), b + "xattn.q.w": lin(Hh, Hh),
-                  b + "xattn.q.b": np.zeros(Hh), b + "xattn.kv.w": lin(2 * Hh, cfg.text_dim),
-                  b + "xattn.kv.b": np.zeros(2 * Hh), b + "xattn.out.w": lin(Hh, Hh), b + "xattn.out.b": np.zeros(Hh),
-                  b + "xattn.postnorm.g": np.ones(Hh), b + "ffn.in.w": lin(4 * Hh, Hh),
-                  b + "ffn.in.b": np.zeros(4 * Hh), b + "ffn.out.w": lin(Hh, 4 * Hh), b + "ffn.out.b": np.zeros(Hh)})
-    return p
-
-
 def grid_coords(dims):
     U, Hp, Wp = dims
     t, y, x = np.meshgrid(np.arange(U), np.arange(Hp), np.arange(Wp), indexing="ij")
@@ -172,9 +144,18 @@ def pinned(shape, dtype):
 
 # ------------------------------------------------------------------ CPU baseline (oracle/_ref)
 def _ref_worker(args):
-    """One process = one reference model; times `steps` samples of REF_SAMPLE fwd+bwd."""
+    """One process = one reference model pinned to one host core (taskset -c <core>); times `steps` samples of
+    REF_SAMPLE fwd+bwd+AdamW.  The reference library is loaded only in these child processes."""
     seed, steps, conn = args
+    try:
+        os.sched_setaffinity(0, {seed % (os.cpu_count() or 1)})
+    except (AttributeError, OSError):
+        pass
     from oracle import oracle as O
+    if O.ref_lib() is None:
+        conn.send("unavailable")
+        conn.close()
+        return
     cfg = O.paper_config(depth=1)
     gs = O.gate_std_for(cfg.hidden)
     ref = O.RefModel(cfg, 1 + seed, 2, gs, gs / 4)
@@ -201,24 +182,61 @@ def ref_tokens():
     return U * (h // 2) * (w // 2)
 
 
+def host_info():
+    info = {"nproc": os.cpu_count()}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+        info["ram_gb"] = round(int(open("/proc/meminfo").read().split("MemTotal:")[1].split()[0]) / 1e6, 1)
+    except Exception:
+        pass
+    return info
+
+
+def _sweep_fit():
+    """The committed single-core sweep of the reference (tools/cpu_sweep.py on a B200 host, profiles/): fitted
+    t = a N + b N^2 and its extrapolations, labelled as such."""
+    path = os.path.join(ROOT, "profiles", "cpu_sweep_r02.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        sw = json.load(f)
+    return {k: sw[k] for k in ("fit", "extrapolated", "host", "source") if k in sw}
+
+
 def cpu_baseline_once():
-    """Single-core run of the reference on the bounded sample (kind 'reference' if oracle/_ref exists)."""
-    from oracle import oracle as O
-    if O.ref_lib() is not None:
-        import multiprocessing as mp
+    """The reference (oracle/_ref, compiled from its unmodified sources) on ONE pinned host core, on the bounded
+    sample; the reference is loaded only in the spawned child.  Falls back to the numpy port when the compiled
+    reference is absent."""
+    import multiprocessing as mp
+    if os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libmugv_ref.so")):
         ctx = mp.get_context("spawn")
         a, b = ctx.Pipe()
         p = ctx.Process(target=_ref_worker, args=((0, 1, b),))
         p.start()
-        a.recv()
-        a.send("go")
-        dt = a.recv()
+        if a.recv() == "ready":
+            a.send("go")
+            dt = a.recv()
+            p.join()
+            return {"value": ref_tokens() / dt, "unit": "tokens/s", "cores": 1, "kind": "reference",
+                    "sample": f"reference FlowTrainer::step (fwd+bwd+AdamW), 10B dims depth 1, {ref_tokens()} tokens "
+                              f"(latent {REF_SAMPLE[0]}x{REF_SAMPLE[1]}x{REF_SAMPLE[2]}x24), text 64x4096, "
+                              f"1 thread pinned to core 0: {dt:.1f} s",
+                    "host": host_info(), "sweep": _sweep_fit()}
         p.join()
-        return {"value": ref_tokens() / dt, "unit": "tokens/s", "cores": 1, "kind": "reference",
-                "sample": f"reference FlowTrainer::step (fwd+bwd+AdamW), 10B dims depth 1, {ref_tokens()} tokens "
-                          f"(latent {REF_SAMPLE[0]}x{REF_SAMPLE[1]}x{REF_SAMPLE[2]}x24), text 64x4096, "
-                          f"1 thread: {dt:.1f} s"}
-    # numpy port (oracle.py) when the compiled reference is absent
+    # numpy port (oracle.py) in a child when the compiled reference is absent
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(1) as pool:
+        dt = pool.apply(_port_sample)
+    return {"value": ref_tokens() / dt, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"numpy fp64 port fwd+bwd, 10B dims depth 1, {ref_tokens()} tokens: {dt:.1f} s",
+            "host": host_info()}
+
+
+def _port_sample():
+    from oracle import oracle as O
     cfg = O.paper_config(depth=1)
     P = O.open_gates(O.init_dit_params(cfg, O.Rng(1)), 2, O.gate_std_for(cfg.hidden), O.gate_std_for(cfg.hidden) / 4)
     g = O.Rng(3).uniform_tensor((REF_SAMPLE[0], REF_SAMPLE[1], REF_SAMPLE[2], 24), -1.0, 1.0)
@@ -226,17 +244,14 @@ def cpu_baseline_once():
     text = O.Rng(4).normal_tensor((TEXT_L, TEXT_D))
     t0 = time.perf_counter()
     O.flow_fwdbwd(P, cfg, s, text, 8.0, grads=True)
-    dt = time.perf_counter() - t0
-    return {"value": ref_tokens() / dt, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"numpy fp64 port fwd+bwd, 10B dims depth 1, {ref_tokens()} tokens: {dt:.1f} s"}
+    return time.perf_counter() - t0
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    from oracle import oracle as O
     import multiprocessing as mp
-    if O.ref_lib() is None:
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libmugv_ref.so")):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmugv_ref.so not built"}))
         return
     try:
@@ -288,14 +303,19 @@ def run_reference(args, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "10B DiT block training step: fwd+bwd+AdamW (reference CPU path, bounded sample)",
                    "tokens_per_sample": ref_tokens(), "parallelism": f"{procs_n} host processes"},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": procs_n, "kind": "reference", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": procs_n, "kind": "reference", "sample": sample,
+                         "host": host_info(), "sweep": _sweep_fit()},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
 
 # ------------------------------------------------------------------ our arm
 def run_ours(args, rank, world, local):
     import torch
-    from paper_2510_17519_b200.capi import Context, FlowSample, mgv_flow_sample, paper_config
+    from paper_2510_17519_b200.capi import (Context, FlowSample, make_flow_sample, mgv_flow_sample, paper_config,
+                                             rng_uniform)
+
+    def rng_normal_text():  # Rng(4).normal_tensor({64, 4096}) == make_batch noise draws of Rng(4) (no t / mask use)
+        return make_flow_sample(4, TEXT_L, TEXT_D)[0]
 
     torch.cuda.set_device(local)
     cfg = paper_config(depth=1)
@@ -308,21 +328,26 @@ def run_ours(args, rank, world, local):
         dist.broadcast_object_list(uid, src=0)
         ctx.set_dp(rank, world, uid[0])
     ctx.set_adamw(**ADAMW)  # the timed step is the full FlowTrainer::step: fwd + bwd + grad norm + AdamW
-    ctx.upload(cfg, synthetic_params(cfg, seed=1234))
+    # SURVEY 8(d) weights: init_dit_params(cfg, Rng(1)) + gates opened from Rng(2) at the width-scaled std
+    gs = 0.2 * math.sqrt(12.0 / cfg.hidden)
+    ctx.init_params(cfg, seed=1, gate_seed=2, gate_std=gs, gate_b_std=gs / 4)
 
     U, Hp, Wp = GRID
     N = U * Hp * Wp
-    rng = np.random.default_rng(100 + rank)
-    coords = grid_coords(GRID)
+    # SURVEY 8(d) inputs with the reference's Rng streams: latent Rng(3 + rank).uniform_tensor(16x90x160x24, -1, 1)
+    # patchified on device (dit::latent_rows), text Rng(4).normal_tensor (64 x 4096), noise and t from
+    # make_batch(Rng(5 + rank)) (flowtrain.cpp:231-250); rank r > 0 draws its own sample
+    latent = rng_uniform(3 + rank, (U, 2 * Hp, 2 * Wp, PATCH // 4), -1.0, 1.0)
+    rows, coords = ctx.latent_rows(latent)
+    noise, t_val, _ = make_flow_sample(5 + rank, N, PATCH)
     clean_h, clean_t = pinned((N, PATCH), np.float64)
     noise_h, noise_t = pinned((N, PATCH), np.float64)
     text_h, text_t = pinned((TEXT_L, TEXT_D), np.float64)
     coords_h, coords_t = pinned((N, 3), np.int32)
-    clean_h[:] = rng.uniform(-1.0, 1.0, (N, PATCH))
-    noise_h[:] = rng.standard_normal((N, PATCH))
-    text_h[:] = np.random.default_rng(4).standard_normal((TEXT_L, TEXT_D))
+    clean_h[:] = rows
+    noise_h[:] = noise
+    text_h[:] = rng_normal_text()
     coords_h[:] = coords
-    t_val = 0.5
     # device-resident copies for the `value` figure
     d_clean, d_noise = clean_t.cuda(), noise_t.cuda()
     d_text, d_coords = text_t.cuda(), coords_t.cuda()
@@ -489,6 +514,18 @@ def extra_configs(ctx, args):
     return out
 
 
+def _relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-exec as N ranks over NCCL on this node (the driver's
+    own launch line) and return its exit code."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -498,6 +535,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the configs[1]/configs[4] side measurements")
     args = ap.parse_args()
+    if args.gpus < 1:
+        sys.exit("bench.py: --gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_relaunch_under_torchrun(args))
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if world_env != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but the launcher started {world_env} ranks")
+    if args.impl == "ours":
+        import torch
+        if torch.cuda.device_count() < world_env:
+            sys.exit(f"bench.py: {world_env} ranks need {world_env} GPUs, {torch.cuda.device_count()} visible")
     rank, world, local = dist_init()
     if args.impl == "reference":
         run_reference(args, rank, world)

@@ -12,6 +12,7 @@
  * Reference interface each entry point replaces:
  *   mgv_params_upload        ParameterSet handed to every call      proj/include/mugv/params.hpp:28-52
  *                            (weights are cached on device; re-upload when they change)
+ *   mgv_params_init          dit::init_dit_params (+ the tests' gate opening)  proj/src/dit.cpp:143-183
  *   mgv_predict_velocity     dit::predict_velocity                  proj/include/mugv/dit.hpp:104-106
  *   mgv_dit_forward          dit::dit_forward                       proj/include/mugv/dit.hpp:94-95
  *                            (dit_forward_batch, dit.hpp:98-100, is a loop of this call)
@@ -71,7 +72,10 @@ typedef struct {
 } mgv_dit_cfg;
 
 /* One flow::FlowSample (flowtrain.hpp:111-117), rows already patchified (N = dims[0]*dims[1]*dims[2]).
- * conditioned: N flags (NULL = no conditioning); condition_latents: N x 4c_z rows (NULL = clean_rows). */
+ * conditioned: N flags (NULL = no conditioning), any unit-aligned mask (flowtrain.cpp:61-100);
+ * condition_latents: N x 4c_z rows, read at conditioned rows (first_frame_mask passes clean_rows); NULL with a
+ * conditioned token is MGV_ERR_INPUT as in validate_mask (flowtrain.cpp:77-80).  mgv_flow_step_device takes
+ * device pointers here, the mask unvalidated, and NULL condition_latents = clean_rows. */
 typedef struct {
     int64_t dims[3];
     const int32_t* coords; /* N x 3 (t, py, px) */
@@ -131,6 +135,16 @@ int64_t mgv_adamw_steps(mgv_ctx* ctx); /* AdamW::step_count (optim.hpp:24) */
 /* Read parameter i (sorted-name order, mgv_param_name) back in the reference layout, fp64. */
 mgv_status mgv_param_download(mgv_ctx* ctx, int64_t i, double* out);
 
+/* dit::init_dit_params (dit.cpp:143-183) with mugv::Rng(seed), uploaded (bit-identical to the reference's weights);
+ * gate_seed != 0 then redraws dit.mod.{w,b} / dit.final.w (std gate_std) and dit.final.b (gate_b_std) from
+ * Rng(gate_seed), the tests' open_gates (test_dit.cpp:35-41). */
+mgv_status mgv_params_init(mgv_ctx* ctx, const mgv_dit_cfg* cfg, uint64_t seed, uint64_t gate_seed, double gate_std,
+                           double gate_b_std);
+/* Seeded synthetic inputs with the reference's streams: Rng(seed).uniform_tensor (rng.hpp:60-64), and
+ * flow::make_batch (flowtrain.cpp:231-250) for one sample: noise, t, and the first-frame mask draw. */
+mgv_status mgv_rng_uniform_fill(uint64_t seed, int64_t n, double lo, double hi, double* out);
+mgv_status mgv_make_flow_sample(uint64_t seed, int64_t N, int64_t D, double mask_prob, double* noise, double* t,
+                                int* conditioned);
 /* Upload (or replace) the dit.* ParameterSet.  names/data/numel are n parallel arrays (any order). */
 mgv_status mgv_params_upload(mgv_ctx* ctx, const mgv_dit_cfg* cfg, int64_t n, const char* const* names,
                              const double* const* data, const int64_t* numel);

@@ -224,10 +224,13 @@ int ref_make_batch(int64_t n, const int64_t* dims, int64_t c_z, const double* co
 // V_out[i] (N_i, 4c_z) and taps_out[i] ((depth+3) tensors concatenated: patch emb (N,H),
 // block outputs (N,H) x depth, final proj (N,H), velocity (N,4c_z)) may be null.
 // grads_out: one pointer per parameter in sorted-name order, or null.
-int ref_flow_fwdbwd(void* h, const RefCfg* c, int64_t n, const int64_t* dims, const double* const* clean,
-                    const double* const* noise, const double* t, const int32_t* cond, const double* text, int64_t L,
-                    double fps, double* loss_out, double* const* V_out, double* const* taps_out,
-                    double* const* grads_out) {
+// masks / cond_lat (both may be null): per-sample general ConditionMask flags (N_i bytes) and condition latents
+// (N_i x 4c_z); a null masks[i] falls back to cond[i] (first_frame_mask).
+int ref_flow_fwdbwd_masked(void* h, const RefCfg* c, int64_t n, const int64_t* dims, const double* const* clean,
+                           const double* const* noise, const double* t, const int32_t* cond,
+                           const uint8_t* const* masks, const double* const* cond_lat, const double* text, int64_t L,
+                           double fps, double* loss_out, double* const* V_out, double* const* taps_out,
+                           double* const* grads_out) {
     return guard([&] {
         auto* hh = static_cast<Handle*>(h);
         auto cfg = to_cfg(c);
@@ -247,6 +250,12 @@ int ref_flow_fwdbwd(void* h, const RefCfg* c, int64_t n, const int64_t* dims, co
             std::memcpy(cr.data(), clean[i], sizeof(double) * static_cast<size_t>(N * D));
             std::memcpy(nz.data(), noise[i], sizeof(double) * static_cast<size_t>(N * D));
             flow::ConditionMask mask = cond[i] ? flow::first_frame_mask(geom, cr) : flow::no_condition(N);
+            if (masks && masks[i]) {
+                mask.conditioned.assign(masks[i], masks[i] + N);
+                mask.condition_latents = Tensor({N, D});
+                std::memcpy(mask.condition_latents.data(), cond_lat && cond_lat[i] ? cond_lat[i] : clean[i],
+                            sizeof(double) * static_cast<size_t>(N * D));
+            }
             flow::Interpolated ip = flow::interpolate(cr, nz, t[i]);
             Tensor ts = Tensor::full({N}, t[i]);
             flow::MaskedInput mi = flow::apply_condition_mask(ip.x_t, ts, mask, geom);
@@ -286,6 +295,14 @@ int ref_flow_fwdbwd(void* h, const RefCfg* c, int64_t n, const int64_t* dims, co
             }
         }
     });
+}
+
+int ref_flow_fwdbwd(void* h, const RefCfg* c, int64_t n, const int64_t* dims, const double* const* clean,
+                    const double* const* noise, const double* t, const int32_t* cond, const double* text, int64_t L,
+                    double fps, double* loss_out, double* const* V_out, double* const* taps_out,
+                    double* const* grads_out) {
+    return ref_flow_fwdbwd_masked(h, c, n, dims, clean, noise, t, cond, nullptr, nullptr, text, L, fps, loss_out, V_out,
+                                  taps_out, grads_out);
 }
 
 // predict_velocity (dit.cpp:388-396) on a row-major grid of dims (U,Hp,Wp).

@@ -34,8 +34,6 @@ def _declare(L):
     L.mgv_dev_gemm.argtypes = [I, P, I64, I, P, I64, I, I, I, I, P, I64, F, I, P]
     L.mgv_dev_gemm.restype = I
     L.mgv_dev_set_gemm_mode.argtypes = [I]
-    L.mgv_dev_set_dkv_pair.argtypes = [I]
-    L.mgv_dev_set_dkv_variant.argtypes = [I]
-    L.mgv_dev_set_dq_variant.argtypes = [I]
+    L.mgv_dev_set_attn_dbg.argtypes = [I]
     from . import capi
     capi.declare(L)

@@ -117,6 +117,9 @@ def declare(L):
     L.mgv_param_download.argtypes = [P, I64, P]
     L.mgv_param_download.restype = I
     L.mgv_params_upload.argtypes = [P, ctypes.POINTER(mgv_dit_cfg), I64, P, P, P]
+    L.mgv_rng_uniform_fill.argtypes = [ctypes.c_uint64, I64, D, D, P]
+    L.mgv_make_flow_sample.argtypes = [ctypes.c_uint64, I64, I64, D, P, P, P]
+    L.mgv_params_init.argtypes = [P, ctypes.POINTER(mgv_dit_cfg), ctypes.c_uint64, ctypes.c_uint64, D, D]
     L.mgv_params_upload.restype = I
     L.mgv_param_count.argtypes = [P]
     L.mgv_param_count.restype = I64
@@ -240,7 +243,8 @@ def declare(L):
 # symbols include/mugv_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = ["mgv_ctx_create", "mgv_ctx_destroy", "mgv_last_error", "mgv_ctx_set_stream", "mgv_nccl_unique_id",
            "mgv_ctx_set_dp", "mgv_ctx_set_tp", "mgv_sample_rows", "mgv_ctx_set_adamw", "mgv_adamw_steps", "mgv_param_download",
-           "mgv_params_upload", "mgv_param_count", "mgv_param_name", "mgv_param_numel",
+           "mgv_params_upload", "mgv_params_init", "mgv_rng_uniform_fill", "mgv_make_flow_sample", "mgv_param_count",
+           "mgv_param_name", "mgv_param_numel",
            "mgv_predict_velocity", "mgv_dit_forward", "mgv_flow_step", "mgv_flow_loss", "mgv_latent_rows",
            "mgv_rows_to_grid", "mgv_flow_step_device", "mgv_last_step_ms", "mgv_last_step_launches",
            "mgv_prof_enable", "mgv_prof_count", "mgv_prof_entry", "mgv_prof_entry_work",
@@ -388,6 +392,25 @@ def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+def rng_uniform(seed: int, shape, lo: float, hi: float) -> np.ndarray:
+    """mgv_rng_uniform_fill: mugv::Rng(seed).uniform_tensor(shape, lo, hi) (the reference's stream)."""
+    out = np.empty(shape, dtype=np.float64)
+    st = _lib().mgv_rng_uniform_fill(seed, out.size, lo, hi, out.ctypes.data)
+    if st != 0:
+        raise InputError("mgv_rng_uniform_fill")
+    return out
+
+
+def make_flow_sample(seed: int, N: int, D: int, mask_prob: float = 0.0):
+    """mgv_make_flow_sample: flow::make_batch's draws for one sample from Rng(seed) -> (noise, t, conditioned)."""
+    noise = np.empty((N, D), dtype=np.float64)
+    t, c = ctypes.c_double(), ctypes.c_int()
+    st = _lib().mgv_make_flow_sample(seed, N, D, mask_prob, noise.ctypes.data, ctypes.byref(t), ctypes.byref(c))
+    if st != 0:
+        raise InputError("mgv_make_flow_sample")
+    return noise, t.value, bool(c.value)
+
+
 @dataclass
 class FlowSample:
     """flow::FlowSample (flowtrain.hpp:111-117); rows already patchified."""
@@ -396,7 +419,8 @@ class FlowSample:
     clean_rows: np.ndarray
     noise: np.ndarray
     t: float
-    conditioned: np.ndarray | None = None  # (N,) uint8 first-frame mask, or None
+    conditioned: np.ndarray | None = None  # (N,) uint8 unit-aligned condition mask, or None
+    condition_latents: np.ndarray | None = None  # (N, D) rows for conditioned tokens; None = clean_rows
     _keep: list = field(default_factory=list, repr=False)
 
     def to_c(self):
@@ -412,7 +436,12 @@ class FlowSample:
             m = np.ascontiguousarray(self.conditioned, dtype=np.uint8)
             self._keep.append(m)
             s.conditioned = m.ctypes.data
-            s.condition_latents = cl.ctypes.data
+            if self.condition_latents is None:
+                s.condition_latents = cl.ctypes.data  # first_frame_mask (flowtrain.cpp:58)
+            else:
+                lat = _f64(self.condition_latents)
+                self._keep.append(lat)
+                s.condition_latents = lat.ctypes.data
         return s
 
 
@@ -687,6 +716,16 @@ class Context:
         ne = (I64 * len(names))(*[a.size for a in arrs])
         c = cfg.to_c()
         self._check(self._L.mgv_params_upload(self.h, ctypes.byref(c), len(names), cn, dp, ne))
+        self.cfg = cfg
+        self.names = [self._L.mgv_param_name(self.h, i).decode() for i in range(self._L.mgv_param_count(self.h))]
+        self.numels = [self._L.mgv_param_numel(self.h, i) for i in range(len(self.names))]
+
+    def init_params(self, cfg: DitConfig, seed: int = 1, gate_seed: int = 0, gate_std: float = 0.0,
+                    gate_b_std: float = 0.0):
+        """mgv_params_init: dit::init_dit_params(cfg, Rng(seed)) on the context (+ gate opening from
+        Rng(gate_seed) when gate_seed != 0), bit-identical to the reference's weights."""
+        c = cfg.to_c()
+        self._check(self._L.mgv_params_init(self.h, ctypes.byref(c), seed, gate_seed, gate_std, gate_b_std))
         self.cfg = cfg
         self.names = [self._L.mgv_param_name(self.h, i).decode() for i in range(self._L.mgv_param_count(self.h))]
         self.numels = [self._L.mgv_param_numel(self.h, i) for i in range(len(self.names))]

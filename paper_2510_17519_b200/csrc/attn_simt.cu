@@ -263,11 +263,7 @@ __global__ void attn_dkv_reduce_kernel(AttnBwdProblem p) {
 template <class T>
 void attn_fwd_simt(const AttnProblem& p, cudaStream_t s) {
     const size_t smem = fwd_smem(p.hd);
-    static bool set = false;
-    if (!set) {
-        MGV_CUDA(cudaFuncSetAttribute(attn_fwd_simt_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        set = true;
-    }
+    ensure_smem(attn_fwd_simt_kernel<T>, 200 * 1024);
     dim3 grid((p.Nq + BQ - 1) / BQ, p.heads);
     attn_fwd_simt_kernel<T><<<grid, NT, smem, s>>>(p); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
@@ -276,14 +272,8 @@ void attn_fwd_simt(const AttnProblem& p, cudaStream_t s) {
 template <class T>
 void attn_bwd_simt(const AttnBwdProblem& p, cudaStream_t s) {
     const size_t smem = bwd_smem(p.f.hd);
-    static bool set = false;
-    if (!set) {
-        MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dq_simt_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      200 * 1024));
-        MGV_CUDA(cudaFuncSetAttribute(attn_bwd_dkv_simt_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      200 * 1024));
-        set = true;
-    }
+    ensure_smem(attn_bwd_dq_simt_kernel<T>, 200 * 1024);
+    ensure_smem(attn_bwd_dkv_simt_kernel<T>, 200 * 1024);
     const int64_t rows = (int64_t)p.f.Nq * p.f.heads;
     attn_bwd_dvec_kernel<T><<<(int)((rows * 32 + 255) / 256), 256, 0, s>>>(p); ::mgv::note_launch();
     attn_bwd_dq_simt_kernel<T><<<dim3((p.f.Nq + BQ - 1) / BQ, p.f.heads), NT, smem, s>>>(p); ::mgv::note_launch();

@@ -34,7 +34,6 @@ namespace {
 constexpr int BM = 128;  // queries per tile (two tiles per CTA)
 constexpr int BN = 112;  // keys per step (TMEM: 2 x (112 + 144) = 512 columns)
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kAttnPolyDefault = 0;
 
 template <int HD>
 struct FwdCfg {
@@ -64,17 +63,6 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
-// 2^x on the FMA pipe (Cody-Waite: x = n + f, f in [0,1); degree-3 minimax for 2^f, max rel. error ~9e-5,
-// below the bf16 rounding of P).  Used for a share of the softmax exponentials so the MUFU pipe (16/clk/SM) and
-// the FMA pipe share them.  x <= 0 here (max-subtracted logits); clamped so the exponent field cannot wrap.
-__device__ __forceinline__ float ex2_fma(float x) {
-    x = fmaxf(x, -126.0f);
-    const float n = floorf(x);
-    const float f = x - n;
-    const float p = fmaf(fmaf(fmaf(0.0771190897f, f, 0.2275643945f), f, 0.6951461434f), f, 1.0f);
-    return __int_as_float(__float_as_int(p) + (static_cast<int>(n) << 23));
-}
-
 template <int HD, int ROWS>
 __device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* m128, const CUtensorMap* m32,
                                           uint64_t* bar, int col0, int row0) {
@@ -86,7 +74,7 @@ __device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* m128,
 
 }  // namespace
 
-template <int HD, int POLY>  // POLY: every POLY-th pair of exponentials on the FMA pipe (0: all on MUFU)
+template <int HD>
 __global__ void __launch_bounds__(384, 1) attn_fwd_tc_kernel(const __grid_constant__ FwdMaps tm, AttnProblem p) {
     using C = FwdCfg<HD>;
     extern __shared__ uint8_t smem_raw[];
@@ -257,13 +245,8 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_tc_kernel(const __grid_consta
             for (int c = 0; c < BN; c += 2) {
                 const float2 x = ffma2(make_float2(s[c], s[c + 1]), lg2, nm2);
                 float2 pp;
-                if (POLY > 0 && (c / 2) % POLY == POLY - 1) {
-                    pp.x = ex2_fma(x.x);
-                    pp.y = ex2_fma(x.y);
-                } else {
-                    pp.x = ex2(x.x);
-                    pp.y = ex2(x.y);
-                }
+                pp.x = ex2(x.x);
+                pp.y = ex2(x.y);
                 ps2[(c / 2) & 3] = fadd2(ps2[(c / 2) & 3], pp);
                 pk[c / 2] = pack_bf16(pp.x, pp.y);
             }
@@ -338,22 +321,9 @@ static void launch_fwd(const AttnProblem& p, const void* vt, int64_t vt_ld, cuda
     make_tmap_sw(&tm.k32, p.k, W, p.Nk, p.k_ld, 16, BN, CU_TENSOR_MAP_SWIZZLE_32B);
     // V^T: rows = heads*HD (dims), cols = keys; box = 64 keys x HD dims
     make_tmap_sw(&tm.vt, vt, p.Nk, W, vt_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
-    static int poly = -1;
-    if (poly < 0) {
-        const char* e = std::getenv("MGV_ATTN_POLY");  // share of exponentials on the FMA pipe: 1 in POLY pairs
-        poly = e ? std::atoi(e) : kAttnPolyDefault;
-        if (poly != 0 && poly != 2 && poly != 4) poly = kAttnPolyDefault;
-        MGV_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel<HD, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        MGV_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel<HD, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        MGV_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel<HD, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    }
+    ensure_smem(attn_fwd_tc_kernel<HD>, C::SMEM);
     dim3 grid((p.Nq + 2 * BM - 1) / (2 * BM), p.heads);
-    if (poly == 4)
-        attn_fwd_tc_kernel<HD, 4><<<grid, 384, C::SMEM, s>>>(tm, p);
-    else if (poly == 2)
-        attn_fwd_tc_kernel<HD, 2><<<grid, 384, C::SMEM, s>>>(tm, p);
-    else
-        attn_fwd_tc_kernel<HD, 0><<<grid, 384, C::SMEM, s>>>(tm, p);
+    attn_fwd_tc_kernel<HD><<<grid, 384, C::SMEM, s>>>(tm, p);
     ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }

@@ -13,6 +13,7 @@
 #include "model.h"
 
 #include "capi_internal.h"
+#include "host_rng.h"
 
 namespace {
 // rmsnorm_rows (autodiff.cpp:686-701) of the looked-up text rows, one thread per row, the reference's
@@ -110,6 +111,106 @@ mgv_status mgv_params_upload(mgv_ctx* ctx, const mgv_dit_cfg* cfg, int64_t n, co
         if (!cfg) throw mgv::InputError("null config");
         ctx->model->upload(to_cfg(cfg), n, names, data, numel);
     });
+}
+
+// dit::init_dit_params (dit.cpp:143-183) drawn with mugv::Rng(seed) in the reference's order, then (gate_seed != 0)
+// the gate-opening draws of the tests / SURVEY 8(d) from Rng(gate_seed): dit.mod.{w,b} and dit.final.w with std
+// gate_std, dit.final.b with gate_b_std (test_dit.cpp:35-41).  Bit-identical weights to the reference's.
+mgv_status mgv_params_init(mgv_ctx* ctx, const mgv_dit_cfg* cfg, uint64_t seed, uint64_t gate_seed, double gate_std,
+                           double gate_b_std) {
+    return guard(ctx, [&] {
+        if (!cfg) throw mgv::InputError("null config");
+        const mgv::Cfg c = to_cfg(cfg);
+        mgv::validate_cfg(c);
+        const int64_t H = c.hidden, D = c.D(), F = 32;  // kFreqDim (dit.cpp:15)
+        std::vector<std::pair<std::string, std::vector<double>>> p;
+        mgv::HostRng rng(seed);
+        auto lin = [&](const std::string& n, int64_t out, int64_t in) {
+            std::vector<double> w(static_cast<size_t>(out * in));
+            rng.normal_fill(w.data(), out * in, 1.0 / std::sqrt(static_cast<double>(in)));
+            p.emplace_back(n, std::move(w));
+        };
+        auto fill = [&](const std::string& n, int64_t k, double v) { p.emplace_back(n, std::vector<double>(k, v)); };
+        lin("dit.patch.w", H, D);
+        fill("dit.patch.b", H, 0.0);
+        lin("dit.gmlp.in.w", H, F);
+        fill("dit.gmlp.in.b", H, 0.0);
+        lin("dit.gmlp.out.w", H, H);
+        fill("dit.gmlp.out.b", H, 0.0);
+        fill("dit.mod.w", 6 * H * H, 0.0);
+        fill("dit.mod.b", 6 * H, 0.0);
+        for (int64_t i = 0; i < c.depth; ++i) {
+            const std::string b = "dit.blk." + std::to_string(i) + ".";
+            fill(b + "gscale", H, 1.0);
+            lin(b + "attn.qkv.w", 3 * H, H);
+            fill(b + "attn.qkv.b", 3 * H, 0.0);
+            fill(b + "attn.temp", c.heads, std::sqrt(static_cast<double>(c.hd())));
+            lin(b + "attn.out.w", H, H);
+            fill(b + "attn.out.b", H, 0.0);
+            fill(b + "xattn.prenorm.g", H, 1.0);
+            lin(b + "xattn.q.w", H, H);
+            fill(b + "xattn.q.b", H, 0.0);
+            lin(b + "xattn.kv.w", 2 * H, c.text_dim);
+            fill(b + "xattn.kv.b", 2 * H, 0.0);
+            lin(b + "xattn.out.w", H, H);
+            fill(b + "xattn.out.b", H, 0.0);
+            fill(b + "xattn.postnorm.g", H, 1.0);
+            lin(b + "ffn.in.w", 4 * H, H);
+            fill(b + "ffn.in.b", 4 * H, 0.0);
+            lin(b + "ffn.out.w", H, 4 * H);
+            fill(b + "ffn.out.b", H, 0.0);
+        }
+        fill("dit.final.g", H, 1.0);
+        fill("dit.final.w", H * H, 0.0);
+        fill("dit.final.b", H, 0.0);
+        lin("dit.out.w", D, H);
+        fill("dit.out.b", D, 0.0);
+        if (gate_seed != 0) {  // open_gates: mod.w, mod.b, final.w, final.b in this order
+            mgv::HostRng g(gate_seed);
+            auto find = [&](const char* n) -> std::vector<double>& {
+                for (auto& e : p)
+                    if (e.first == n) return e.second;
+                throw mgv::InputError(n);
+            };
+            const char* order[4] = {"dit.mod.w", "dit.mod.b", "dit.final.w", "dit.final.b"};
+            for (int k = 0; k < 4; ++k) {
+                std::vector<double>& v = find(order[k]);
+                g.normal_fill(v.data(), static_cast<int64_t>(v.size()), k == 3 ? gate_b_std : gate_std);
+            }
+        }
+        std::vector<const char*> names;
+        std::vector<const double*> data;
+        std::vector<int64_t> numel;
+        for (auto& e : p) {
+            names.push_back(e.first.c_str());
+            data.push_back(e.second.data());
+            numel.push_back(static_cast<int64_t>(e.second.size()));
+        }
+        ctx->model->upload(c, static_cast<int64_t>(names.size()), names.data(), data.data(), numel.data());
+    });
+}
+
+// mugv::Rng(seed).uniform_tensor(n, lo, hi) (rng.hpp:60-64): the seeded synthetic latents of SURVEY 8(d)
+mgv_status mgv_rng_uniform_fill(uint64_t seed, int64_t n, double lo, double hi, double* out) {
+    if (!out || n < 0) return MGV_ERR_INPUT;
+    mgv::HostRng r(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = lo + (hi - lo) * r.uniform();
+    return MGV_OK;
+}
+
+// flow::make_batch (flowtrain.cpp:231-250) for one sample of N rows x D from Rng(seed): noise ~ N(0,1), t ~ U(0,1]
+// (redrawn while <= 0), then the mask draw: *conditioned = uniform() < mask_prob (first_frame_mask)
+mgv_status mgv_make_flow_sample(uint64_t seed, int64_t N, int64_t D, double mask_prob, double* noise, double* t,
+                                int* conditioned) {
+    if (!noise || !t || N < 0 || D < 1) return MGV_ERR_INPUT;
+    mgv::HostRng r(seed);
+    r.normal_fill(noise, N * D, 1.0);
+    double u = r.uniform();
+    while (u <= 0.0) u = r.uniform();
+    *t = u;
+    const bool c = r.uniform() < mask_prob;
+    if (conditioned) *conditioned = c ? 1 : 0;
+    return MGV_OK;
 }
 
 mgv_status mgv_params_upload_ckpt(mgv_ctx* ctx, const mgv_dit_cfg* cfg, const mgv_ckpt* ck) {
@@ -287,7 +388,8 @@ mgv_status mgv_flow_step_device(mgv_ctx* ctx, int64_t n, const mgv_flow_sample* 
             d.clean = s.clean_rows;
             d.noise = s.noise;
             d.t = s.t;
-            d.first_frame = s.conditioned != nullptr ? 1 : 0;
+            d.cond = s.conditioned;  // device flags (caller-validated, unit-aligned) or null
+            d.cond_lat = s.condition_latents;
         }
         ctx->model->flow_step_dev(n, ds.data(), text_dev, L, fps, loss, grad_norm);
     });

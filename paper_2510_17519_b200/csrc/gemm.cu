@@ -3,6 +3,7 @@
 #include "gemm.cuh"
 
 #include <atomic>
+#include <map>
 #include <mutex>
 
 namespace mgv {
@@ -13,14 +14,35 @@ void (*g_gemm_prof_hook)(bool, double, cudaStream_t) = nullptr;
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+// SM count of the CURRENT device (a process may hold contexts on several GPUs)
 int num_sms() {
-    static int n = [] {
-        int dev = 0, v = 0;
-        cudaGetDevice(&dev);
+    constexpr int kMaxDev = 64;
+    static std::atomic<int> cache[kMaxDev] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDev) dev = 0;
+    int n = cache[dev].load(std::memory_order_relaxed);
+    if (n == 0) {
+        int v = 0;
         cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        return v > 0 ? v : 148;
-    }();
+        n = v > 0 ? v : 148;
+        cache[dev].store(n, std::memory_order_relaxed);
+    }
     return n;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device context: remember, per (kernel, device), the
+// largest size already set; thread-safe.
+void ensure_smem_attr(const void* kern, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> done;
+    int dev = 0;
+    MGV_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    int& have = done[{kern, dev}];
+    if (have >= bytes) return;
+    MGV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    have = bytes;
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

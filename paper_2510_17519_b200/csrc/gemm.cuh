@@ -34,6 +34,11 @@ struct CudaError : std::runtime_error {
     } while (0)
 
 int num_sms();
+void ensure_smem_attr(const void* kern, int bytes);  // per (kernel, device), thread-safe
+template <class K>
+inline void ensure_smem(K* kern, int bytes) {
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), bytes);
+}
 // kernel-launch accounting (bench: gpu_launches)
 void note_launch();
 int64_t launch_count();
@@ -109,21 +114,13 @@ void gemm_tc_launch(const Mat& A, const Mat& B, int M, int N, int K, const Epi& 
         make_tmap_bf16(&tb, B.p, K, N, B.ld, kGemmBK, BN / MC);
     if (MC == 1) {
         auto kern = gemm_bf16_tc_kernel<BN, A_MN, B_MN, 1, Epi>;
-        static bool attr_set = false;  // one per instantiation
-        if (!attr_set) {
-            MGV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-            attr_set = true;
-        }
+        ensure_smem(kern, C::SMEM);
         const int tiles = num_m * num_n;
         const int grid = tiles < num_sms() ? tiles : num_sms();
         kern<<<grid, gemm_threads<Epi>(), C::SMEM, s>>>(ta, tb, M, N, K, epi); ::mgv::note_launch();
     } else {
         auto kern = gemm_bf16_tc_kernel<BN, A_MN, B_MN, 2, Epi>;
-        static bool attr_set = false;
-        if (!attr_set) {
-            MGV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-            attr_set = true;
-        }
+        ensure_smem(kern, C::SMEM);
         const int pair_tiles = ((num_m + 1) / 2) * num_n;
         const int clusters = pair_tiles < num_sms() / 2 ? pair_tiles : num_sms() / 2;
         cudaLaunchConfig_t cfg{};
@@ -157,11 +154,7 @@ void gemm_tc2_launch(const Mat& A, const Mat& B, int M, int N, int K, const Epi&
     else
         make_tmap_bf16(&tb, B.p, K, N, B.ld, kGemmBK, BN / 2);
     auto kern = gemm_bf16_tc2_kernel<BN, A_MN, B_MN, Epi>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        MGV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        attr_set = true;
-    }
+    ensure_smem(kern, C::SMEM);
     const int tiles = ((M + 2 * kGemmBM - 1) / (2 * kGemmBM)) * ((N + BN - 1) / BN);
     const int clusters = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
     cudaLaunchConfig_t cfg{};

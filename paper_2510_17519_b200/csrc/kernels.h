@@ -17,10 +17,11 @@ namespace mgv {
 constexpr int kRowsPerChunk = 64;
 inline int row_chunks(int N) { return (N + kRowsPerChunk - 1) / kRowsPerChunk; }
 
-// ---- K1: interpolate + first-frame condition mask (flowtrain.cpp:9-20, 83-100)
+// ---- K1: interpolate + unit-aligned condition mask (flowtrain.cpp:9-20, 83-100); cond = N device flags or null,
+// cond_lat = N x D device condition latents (read only at conditioned rows) or null (= clean)
 template <class T>
-void prep_flow_sample(const double* clean, const double* noise, const int32_t* coords, int N, int D, double t,
-                      int cond, T* rows, float* v_target, uint8_t* loss_mask, int32_t* mod_id, cudaStream_t s);
+void prep_flow_sample(const double* clean, const double* noise, const uint8_t* cond, const double* cond_lat, int N,
+                      int D, double t, T* rows, float* v_target, uint8_t* loss_mask, int32_t* mod_id, cudaStream_t s);
 // rows (fp64, host layout) -> T, plus mod ids given on device
 template <class T>
 void convert_rows(const double* src, int64_t n, T* dst, cudaStream_t s);

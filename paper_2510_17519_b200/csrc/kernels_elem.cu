@@ -92,27 +92,29 @@ inline int grid_for(int64_t n, int threads = 256) {
 
 // ============================================================ K1: sample prep
 template <class T>
-__global__ void prep_flow_sample_kernel(const double* clean, const double* noise, const int32_t* coords, int N, int D,
-                                        double t, int cond, T* rows, float* vt, uint8_t* lmask, int32_t* mod_id) {
+__global__ void prep_flow_sample_kernel(const double* clean, const double* noise, const uint8_t* cond,
+                                        const double* cond_lat, int N, int D, double t, T* rows, float* vt,
+                                        uint8_t* lmask, int32_t* mod_id) {
     const int64_t total = (int64_t)N * D;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int i = static_cast<int>(e / D);
-        const bool c = cond && coords[3 * i] == 0;  // first_frame_mask: unit 0 (flowtrain.cpp:50-59)
+        const bool c = cond && cond[i];  // apply_condition_mask (flowtrain.cpp:83-100), any unit-aligned mask
         const double x = clean[e], n = noise[e];
-        const double xt = c ? x : (1.0 - t) * x + t * n;  // interpolate (flowtrain.cpp:16)
+        // interpolate (flowtrain.cpp:16); conditioned rows <- condition_latents (flowtrain.cpp:95)
+        const double xt = c ? (cond_lat ? cond_lat[e] : x) : (1.0 - t) * x + t * n;
         rows[e] = to_t<T>(static_cast<float>(xt));
         vt[e] = static_cast<float>(n - x);
         if (e % D == 0) {
             lmask[i] = c ? 0 : 1;
-            mod_id[i] = c ? 1 : 0;  // table row 0: tau = t ; row 1: tau = 0
+            mod_id[i] = c ? 1 : 0;  // table row 0: tau = t ; row 1: tau = 0 (flowtrain.cpp:96)
         }
     }
 }
 template <class T>
-void prep_flow_sample(const double* clean, const double* noise, const int32_t* coords, int N, int D, double t,
-                      int cond, T* rows, float* vt, uint8_t* lmask, int32_t* mod_id, cudaStream_t s) {
-    prep_flow_sample_kernel<T><<<grid_for((int64_t)N * D), 256, 0, s>>>(clean, noise, coords, N, D, t, cond, rows, vt,
-                                                                        lmask, mod_id); ::mgv::note_launch();
+void prep_flow_sample(const double* clean, const double* noise, const uint8_t* cond, const double* cond_lat, int N,
+                      int D, double t, T* rows, float* vt, uint8_t* lmask, int32_t* mod_id, cudaStream_t s) {
+    prep_flow_sample_kernel<T><<<grid_for((int64_t)N * D), 256, 0, s>>>(clean, noise, cond, cond_lat, N, D, t, rows,
+                                                                        vt, lmask, mod_id); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -1105,8 +1107,8 @@ void permute_shard_rows(const double* src, double* dst, int C, int R, int P, int
 }
 
 #define INST(T)                                                                                                       \
-    template void prep_flow_sample<T>(const double*, const double*, const int32_t*, int, int, double, int, T*, float*, \
-                                      uint8_t*, int32_t*, cudaStream_t);                                              \
+    template void prep_flow_sample<T>(const double*, const double*, const uint8_t*, const double*, int, int, double, \
+                                      T*, float*, uint8_t*, int32_t*, cudaStream_t);                                  \
     template void convert_rows<T>(const double*, int64_t, T*, cudaStream_t);                                          \
     template void convert_f32<T>(const float*, int64_t, T*, cudaStream_t);                                            \
     template void rms_mod<T>(const float*, int, int, const float*, int64_t, int, int, const int32_t*, T*, float*,     \

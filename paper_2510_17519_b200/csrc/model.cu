@@ -1343,9 +1343,9 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
         const int N = static_cast<int>(sm.N);
         MGV_CUDA(cudaMemcpyAsync(w.coords, sm.coords, sizeof(int32_t) * 3 * N, cudaMemcpyDeviceToDevice, s));
         // interpolate + condition mask (flowtrain.cpp:265-267); taus {t, 0} (dit.cpp:242 dedup)
-        prep_flow_sample<T>(sm.clean, sm.noise, w.coords, N, int(D), sm.t, sm.first_frame, tp<T>(w.rows), w.vt,
-                            w.lmask, w.mod_id, s);
-        w.n_u = sm.first_frame ? 2 : 1;
+        prep_flow_sample<T>(sm.clean, sm.noise, sm.cond, sm.cond_lat, N, int(D), sm.t, tp<T>(w.rows), w.vt, w.lmask,
+                            w.mod_id, s);
+        w.n_u = sm.cond ? 2 : 1;
         set_taus(w.taus, sm.t, s);
         forward_sample<T>(sm, w.rows, nullptr, w.n_u, w.mod_id, fps_k, true, true, nullptr);
         if (v_dev && v_dev[k]) {
@@ -1496,20 +1496,30 @@ void Model::stage_samples(int64_t n, const mgv_flow_sample* samples, std::vector
         d.noise = nz;
         d.t = s.t;
         if (cond_any) {
-            // the device prep marks unit-0 rows; general masks are validated unit-aligned above and we
-            // require them to be exactly the first unit (first_frame_mask), the only producer in the reference
-            for (int64_t i = 0; i < N; ++i)
-                if ((s.conditioned[i] != 0) != (s.coords[3 * i] == 0))
-                    throw InputError("only first-frame conditioning masks are supported on device");
-            if (s.condition_latents && s.condition_latents != s.clean_rows) {
-                // conditioned rows take condition_latents (flowtrain.cpp:95): stage them as those rows of the
-                // clean input; the interpolation target there is masked out of the loss, so this is exact
-                for (int64_t i = 0; i < N; ++i)
-                    if (s.conditioned[i])
-                        MGV_CUDA(cudaMemcpyAsync(cl + i * D, s.condition_latents + i * D, sizeof(double) * D,
-                                                 cudaMemcpyHostToDevice, stream_));
+            // apply_condition_mask (flowtrain.cpp:83-100): any unit-aligned mask; validate_mask requires the
+            // condition latents (flowtrain.cpp:77-80)
+            if (!s.condition_latents)
+                throw InputError("condition mask lacks clean latents for its conditioned tokens");
+            auto* m = static_cast<uint8_t*>(dalloc(static_cast<size_t>(N)));
+            MGV_CUDA(cudaMemcpyAsync(m, s.conditioned, static_cast<size_t>(N), cudaMemcpyHostToDevice, stream_));
+            d.cond = m;
+            if (s.condition_latents != s.clean_rows) {
+                // stage only the conditioned rows, one copy per contiguous run (a latent unit is a contiguous
+                // run of rows in latent_rows order, dit.cpp:92-116); the other rows are never read
+                auto* lat = static_cast<double*>(dalloc(sizeof(double) * N * D));
+                for (int64_t i = 0; i < N;) {
+                    if (!s.conditioned[i]) {
+                        ++i;
+                        continue;
+                    }
+                    int64_t j = i;
+                    while (j < N && s.conditioned[j]) ++j;
+                    MGV_CUDA(cudaMemcpyAsync(lat + i * D, s.condition_latents + i * D, sizeof(double) * (j - i) * D,
+                                             cudaMemcpyHostToDevice, stream_));
+                    i = j;
+                }
+                d.cond_lat = lat;
             }
-            d.first_frame = 1;
         }
         ds[static_cast<size_t>(k)] = d;
     }

@@ -50,7 +50,8 @@ struct DevSample {
     const double* clean = nullptr;
     const double* noise = nullptr;
     double t = 0.0;
-    int first_frame = 0;  // first_frame_mask conditioning (flowtrain.cpp:50-59)
+    const uint8_t* cond = nullptr;     // N condition flags (ConditionMask::conditioned, flowtrain.hpp:32-41) or null
+    const double* cond_lat = nullptr;  // N x D condition latents (read at conditioned rows only) or null (= clean)
 };
 
 // Per-sample overrides of a flow step (post-training, posttrain.cpp:126-233): every sample may carry its own

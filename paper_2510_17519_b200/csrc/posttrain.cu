@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "capi_internal.h"
+#include "host_rng.h"
 
 namespace {
 
@@ -25,31 +26,7 @@ using mgv::DimensionError;
 using mgv::InputError;
 using mgv::NumericError;
 
-// mugv::Rng (rng.hpp:14-72): mt19937_64 with hand-rolled distributions (identical streams across libraries)
-class HostRng {
-public:
-    explicit HostRng(uint64_t seed) : gen_(seed) {}
-    double uniform() { return static_cast<double>(gen_() >> 11) * 0x1.0p-53; }
-    double normal() {
-        if (have_spare_) {
-            have_spare_ = false;
-            return spare_;
-        }
-        double u1 = uniform();
-        const double u2 = uniform();
-        while (u1 <= 0.0) u1 = uniform();
-        const double r = std::sqrt(-2.0 * std::log(u1));
-        const double a = 2.0 * M_PI * u2;
-        spare_ = r * std::sin(a);
-        have_spare_ = true;
-        return r * std::cos(a);
-    }
-
-private:
-    std::mt19937_64 gen_;
-    bool have_spare_ = false;
-    double spare_ = 0.0;
-};
+using HostRng = mgv::HostRng;
 
 double sigmoid(double x) {  // posttrain.cpp:12-16
     if (x >= 0.0) return 1.0 / (1.0 + std::exp(-x));
@@ -113,7 +90,8 @@ mgv_eval_sample eval_of(const mgv_sample_record& r, const Draw& d) {
     e.s.noise = d.noise.data();
     e.s.t = d.t;
     e.s.conditioned = r.conditioned;
-    e.s.condition_latents = r.condition_latents;
+    // a record's mask carries its own rows as the condition latents unless given (first_frame_mask, flowtrain.cpp:58)
+    e.s.condition_latents = r.conditioned ? (r.condition_latents ? r.condition_latents : r.rows) : nullptr;
     e.text = r.text;
     e.L = r.L;
     e.fps = r.fps;

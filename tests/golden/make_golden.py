@@ -35,6 +35,19 @@ CASES = {
                   grids=[(2, 4, 8), (3, 2, 4)], L=8, mask_prob=0.0, force_cond=[1], gate_std=O.gate_std_for(288) * 4,
                   full=False),
 }
+# Larger cases (SURVEY 8(c) parity plan items 2 and 4), fixtures sampled rather than full:
+LONG_CASES = {
+    # the benchmarked 10B width (paper_config depth 1: H3456, 24 x 144, text 64 x 4096), latent (4,8,8) -> 64 tokens,
+    # first-frame conditioning on
+    "w10b": dict(cfg=dict(depth=1, hidden=3456, heads=24, text_dim=4096, c_z=24, rope_split=(48, 48, 48)),
+                 grids=[(4, 8, 8)], L=64, mask_prob=0.0, force_cond=[0], gate_std=O.gate_std_for(3456), full=False),
+    # long N at reduced width: H288 = 2 x 144, rope (48,48,48), the 480p/2s latent (7,60,104) -> 10,920 tokens on
+    # the real 480p coordinates (the reference's Tape::mha keeps 1.9 GB of probabilities; ~9 min on one core)
+    "long480p": dict(cfg=dict(depth=1, hidden=288, heads=2, text_dim=64, c_z=24, rope_split=(48, 48, 48)),
+                     grids=[(7, 60, 104)], L=8, mask_prob=0.0, force_cond=[0], gate_std=O.gate_std_for(288) * 4,
+                     full=False),
+}
+ALL_CASES = dict(CASES, **LONG_CASES)
 SEEDS = dict(params=1, gates=2, latents=3, text=4, batch=5)
 NSAMP = 64
 
@@ -57,9 +70,11 @@ def sample_idx(n, k, seed):
     return np.sort(r.choice(n, size=min(n, k), replace=False))
 
 
-def main():
+def main(names=None):
     out_dir = os.path.dirname(os.path.abspath(__file__))
-    for name, spec in CASES.items():
+    for name, spec in ALL_CASES.items():
+        if names and name not in names:
+            continue
         cfg, P, text, samples = build_case(name, spec)
         gs = spec["gate_std"]
         ref = O.RefModel(cfg, SEEDS["params"], SEEDS["gates"], gs, gs / 4)
@@ -68,7 +83,14 @@ def main():
         r = ref.flow_fwdbwd(samples, text, 8.0, grads=True, with_taps=True)
         d = {"spec": np.array(json.dumps(dict(spec, seeds=SEEDS))), "loss": np.array(r["loss"])}
         for i, s in enumerate(samples):
-            d[f"V.{i}"] = r["V"][i]
+            if spec["full"] or r["V"][i].size <= 8192:
+                d[f"V.{i}"] = r["V"][i]
+            else:  # sampled entries + the max |V| (normwise denominators) + the norm
+                vi = sample_idx(r["V"][i].size, 4096, 200 + i)
+                d[f"Vi.{i}"] = vi
+                d[f"Vv.{i}"] = r["V"][i].ravel()[vi]
+                d[f"Vmax.{i}"] = np.array(np.abs(r["V"][i]).max())
+                d[f"Vn.{i}"] = np.array(np.linalg.norm(r["V"][i]))
             d[f"cond.{i}"] = np.array(s.cond)
             taps = r["taps"][i]
             idx = sample_idx(taps.size, 4 * NSAMP, 100 + i)
@@ -83,10 +105,11 @@ def main():
                 d[f"gi:{k}"] = idx
                 d[f"gv:{k}"] = gv[idx]
                 d[f"gn:{k}"] = np.array(np.linalg.norm(gv))
+                d[f"gm:{k}"] = np.array(np.abs(gv).max())
         path = os.path.join(out_dir, f"{name}.npz")
         np.savez_compressed(path, **d)
         print(name, "loss", r["loss"], "->", path, os.path.getsize(path), "bytes")
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:] or None)

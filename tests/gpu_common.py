@@ -13,8 +13,10 @@ def to_cfg(c: O.DitConfig) -> DitConfig:
 def to_samples(samples):
     out = []
     for s in samples:
-        cond = (s.coords[:, 0] == 0).astype(np.uint8) if s.cond else None
-        out.append(FlowSample(s.dims, s.coords, s.clean, s.noise, s.t, cond))
+        m = O.condition_flags(s)
+        cond = None if m is None else m.astype(np.uint8)
+        out.append(FlowSample(s.dims, s.coords, s.clean, s.noise, s.t, cond,
+                              None if cond is None else s.cond_latents))
     return out
 
 

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from tests.golden.make_golden import CASES, build_case
+from tests.golden.make_golden import ALL_CASES, CASES, LONG_CASES, build_case
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 needs_ref = pytest.mark.skipif(O.ref_lib() is None, reason="oracle/_ref not built (no reference sources)")
@@ -20,28 +20,51 @@ def nerr(a, b):
     return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
 
 
-@pytest.mark.parametrize("name", sorted(CASES))
-def test_restatement_matches_golden(name):
-    g = np.load(os.path.join(GOLDEN, f"{name}.npz"))
-    spec = json.loads(str(g["spec"]))
-    cfg, P, text, samples = build_case(name, CASES[name])
-    assert spec["cfg"]["hidden"] == cfg.hidden
-    out = O.flow_fwdbwd(P, cfg, samples, text, 8.0, grads=True, with_taps=True)
-    assert abs(out["loss"] - float(g["loss"])) <= 1e-12 * abs(float(g["loss"]))
+def check_against_golden(out, g, samples, tol=1e-12):
+    """Compare a flow_fwdbwd result (V, loss, grads; taps optional) with a fixture the REFERENCE produced.
+    Returns the worst normwise error per quantity (max |a-b| over the stored entries / max |ref|)."""
+    errs = {"loss": abs(out["loss"] - float(g["loss"])) / abs(float(g["loss"]))}
     for i, s in enumerate(samples):
         assert bool(g[f"cond.{i}"]) == s.cond
-        assert nerr(out["V"][i], g[f"V.{i}"]) < 1e-12
-        taps = np.concatenate([t.ravel() for t in out["taps"][i]])
-        assert nerr(taps[g[f"taps_idx.{i}"]], g[f"taps_val.{i}"]) < 1e-12
-        assert abs(np.linalg.norm(taps) - float(g[f"taps_norm.{i}"])) < 1e-12 * float(g[f"taps_norm.{i}"])
-    for k, gv in out["grads"].items():
-        gv = gv.ravel()
-        if f"g:{k}" in g:
-            assert nerr(gv, g[f"g:{k}"]) < 1e-12, k
+        V = np.asarray(out["V"][i], dtype=np.float64).ravel()
+        if f"V.{i}" in g:
+            errs[f"V{i}"] = nerr(V, g[f"V.{i}"])
         else:
-            ref_n = float(g[f"gn:{k}"])
-            assert abs(np.linalg.norm(gv) - ref_n) <= 1e-12 * max(ref_n, 1e-300) + 1e-300, k
-            assert nerr(gv[g[f"gi:{k}"]], g[f"gv:{k}"]) < 1e-11 or ref_n == 0.0, k
+            vi = g[f"Vi.{i}"]
+            errs[f"V{i}"] = float(np.abs(V[vi] - g[f"Vv.{i}"]).max() / float(g[f"Vmax.{i}"]))
+            errs[f"|V{i}|"] = abs(np.linalg.norm(V) - float(g[f"Vn.{i}"])) / float(g[f"Vn.{i}"])
+        if "taps" in out:
+            taps = np.concatenate([t.ravel() for t in out["taps"][i]])
+            assert nerr(taps[g[f"taps_idx.{i}"]], g[f"taps_val.{i}"]) < tol
+            assert abs(np.linalg.norm(taps) - float(g[f"taps_norm.{i}"])) < tol * float(g[f"taps_norm.{i}"])
+    for k, gv in out["grads"].items():
+        gv = np.asarray(gv, dtype=np.float64).ravel()
+        if f"g:{k}" in g:
+            errs[k] = nerr(gv, g[f"g:{k}"])
+            continue
+        ref_n = float(g[f"gn:{k}"])
+        if ref_n == 0.0:
+            errs[k] = float(np.abs(gv).max())
+            continue
+        den = float(g[f"gm:{k}"]) if f"gm:{k}" in g else float(np.abs(g[f"gv:{k}"]).max())
+        errs[k] = max(float(np.abs(gv[g[f"gi:{k}"]] - g[f"gv:{k}"]).max()) / den,
+                      abs(np.linalg.norm(gv) - ref_n) / ref_n)
+    return errs
+
+
+@pytest.mark.parametrize("name", sorted(ALL_CASES))
+def test_restatement_matches_golden(name):
+    path = os.path.join(GOLDEN, f"{name}.npz")
+    if name in LONG_CASES and not os.path.exists(path):
+        pytest.skip("fixture not generated (tests/golden/make_golden.py " + name + ")")
+    g = np.load(path)
+    spec = json.loads(str(g["spec"]))
+    cfg, P, text, samples = build_case(name, ALL_CASES[name])
+    assert spec["cfg"]["hidden"] == cfg.hidden
+    out = O.flow_fwdbwd(P, cfg, samples, text, 8.0, grads=True, with_taps=True)
+    errs = check_against_golden(out, g, samples)
+    worst = max(errs, key=errs.get)
+    assert errs[worst] < 1e-11, (worst, errs[worst])
 
 
 def test_flow_loss_hand_case():
@@ -189,3 +212,41 @@ def test_ref_rope3d_matches_restatement():
         assert L.ref_rope3d(x.ctypes.data, N, heads, (ctypes.c_int * 3)(*split), co.ctypes.data, 10000.0, inverse,
                             ref.ctypes.data) == 0
         assert np.max(np.abs(ref - O.rope_apply(x, cos, sin, heads, direction))) < 1e-13
+
+
+def mask_case(kind):
+    """A U=3 sample of the hd144 config with a general unit-aligned ConditionMask (flowtrain.cpp:61-100) and
+    condition latents different from the clean rows."""
+    cfg, P, text, samples = build_case("hd144", CASES["hd144"])
+    s = samples[1]  # dims (3, 1, 2): 3 latent units
+    units = s.coords[:, 0]
+    m = {"last": units == 2, "two": (units == 0) | (units == 2), "none": np.zeros_like(units, dtype=bool)}[kind]
+    s.cond = False
+    s.mask = m.astype(np.uint8)
+    s.cond_latents = O.Rng(8).normal_tensor(s.clean.shape)
+    return cfg, P, text, samples
+
+
+@needs_ref
+@pytest.mark.parametrize("kind", ["last", "two"])
+def test_general_condition_mask_matches_reference(kind):
+    """oracle.masked_input with an explicit unit-aligned mask and condition latents vs the reference's
+    validate_mask + apply_condition_mask (flowtrain.cpp:61-100) inside FlowTrainer::step's fwd+bwd."""
+    cfg, P, text, samples = mask_case(kind)
+    gs = CASES["hd144"]["gate_std"]
+    ref = O.RefModel(cfg, 1, 2, gs, gs / 4)
+    r = ref.flow_fwdbwd(samples, text, 8.0, grads=True)
+    o = O.flow_fwdbwd(P, cfg, samples, text, 8.0, grads=True)
+    assert abs(r["loss"] - o["loss"]) <= 1e-12 * abs(r["loss"])
+    for i in range(len(samples)):
+        assert nerr(o["V"][i], r["V"][i]) < 1e-12
+    for k in P:
+        assert nerr(o["grads"][k], r["grads"][k]) < 1e-11 or np.abs(r["grads"][k]).max() == 0, k
+
+
+def test_mask_must_cover_whole_units():
+    cfg, P, text, samples = mask_case("last")
+    samples[1].mask = samples[1].mask.copy()
+    samples[1].mask[np.argmax(samples[1].coords[:, 0] == 2)] = 0  # one token of unit 2 unconditioned
+    with pytest.raises(ValueError):
+        O.masked_input(samples[1])

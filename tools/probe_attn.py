@@ -10,10 +10,6 @@ from paper_2510_17519_b200._lib import lib  # noqa: E402
 
 L = lib()
 import os  # noqa: E402
-if os.environ.get("MGV_DKV_VARIANT"):  # 0 = v8 (default), 1 = v5
-    L.mgv_dev_set_dkv_variant(int(os.environ["MGV_DKV_VARIANT"]))
-if os.environ.get("MGV_DQ_VARIANT"):  # 3 = v10 (default), 2 = v9, 0 = v7, 1 = v8, 12 = v9 with 4 compute warps per lane group
-    L.mgv_dev_set_dq_variant(int(os.environ["MGV_DQ_VARIANT"]))
 if os.environ.get("MGV_ATTN_DBG"):  # timing experiments (wrong results): see attn_bwd_tc.cu g_attn_dbg
     L.mgv_dev_set_attn_dbg(int(os.environ["MGV_ATTN_DBG"]))
 P = ctypes.c_void_p
