@@ -14,6 +14,7 @@
  *                            (weights are cached on device; re-upload when they change)
  *   mgv_params_init          dit::init_dit_params (+ the tests' gate opening)  proj/src/dit.cpp:143-183
  *   mgv_predict_velocity     dit::predict_velocity                  proj/include/mugv/dit.hpp:104-106
+ *   mgv_velocity_graph       dit::velocity_rows_graph (tape node + backward closure)  proj/include/mugv/dit.hpp:124-127
  *   mgv_dit_forward          dit::dit_forward                       proj/include/mugv/dit.hpp:94-95
  *                            (dit_forward_batch, dit.hpp:98-100, is a loop of this call)
  *   mgv_flow_step            flow::FlowTrainer::step: loss, backward, proj/include/mugv/flowtrain.hpp:134-151
@@ -158,6 +159,18 @@ mgv_status mgv_predict_velocity(mgv_ctx* ctx, const double* rows, int64_t N, con
                                 const int64_t dims[3], const double* text, int64_t L, const double* timesteps,
                                 double fps, double* out);
 
+/* The tape-level builder dit::velocity_rows_graph (dit.hpp:124-127, dit.cpp:320-334) as ONE device node, for the
+ * TapeOps seam (autodiff.hpp:130-134).  Forward: velocity (N x 4c_z) and, when taps != NULL, the reference's taps
+ * in order (depth + 3 pointers, each may be NULL): patch embedding (N x hidden), each block's residual output
+ * (N x hidden) x depth, the final normed projection (N x hidden), the velocity rows (N x 4c_z).  Backward (the
+ * node's closure): dV != NULL gives the vector-Jacobian product, gradients of sum(dV * velocity) w.r.t. every
+ * dit.* parameter written to grads_out (sorted-name order, mgv_param_name; entries may be NULL).  rows and text
+ * are constants of the graph, as in every reference caller (flowtrain.cpp:268, posttrain.cpp:132,284,
+ * expansion.cpp:267-272). */
+mgv_status mgv_velocity_graph(mgv_ctx* ctx, const double* rows, int64_t N, const int32_t* coords,
+                              const int64_t dims[3], const double* text, int64_t L, const double* timesteps,
+                              double fps, double* velocity, double* const* taps, const double* dV,
+                              double* const* grads_out);
 /* dit::dit_forward: tokens (N x hidden) -> out (N x hidden). */
 mgv_status mgv_dit_forward(mgv_ctx* ctx, const double* tokens, int64_t N, const int32_t* coords,
                            const int64_t dims[3], const double* text, int64_t L, const double* timesteps, double fps,

@@ -119,6 +119,7 @@ def declare(L):
     L.mgv_params_upload.argtypes = [P, ctypes.POINTER(mgv_dit_cfg), I64, P, P, P]
     L.mgv_rng_uniform_fill.argtypes = [ctypes.c_uint64, I64, D, D, P]
     L.mgv_make_flow_sample.argtypes = [ctypes.c_uint64, I64, I64, D, P, P, P]
+    L.mgv_velocity_graph.argtypes = [P, P, I64, P, P, P, I64, P, D, P, P, P, P]
     L.mgv_params_init.argtypes = [P, ctypes.POINTER(mgv_dit_cfg), ctypes.c_uint64, ctypes.c_uint64, D, D]
     L.mgv_params_upload.restype = I
     L.mgv_param_count.argtypes = [P]
@@ -245,7 +246,7 @@ EXPORTS = ["mgv_ctx_create", "mgv_ctx_destroy", "mgv_last_error", "mgv_ctx_set_s
            "mgv_ctx_set_dp", "mgv_ctx_set_tp", "mgv_sample_rows", "mgv_ctx_set_adamw", "mgv_adamw_steps", "mgv_param_download",
            "mgv_params_upload", "mgv_params_init", "mgv_rng_uniform_fill", "mgv_make_flow_sample", "mgv_param_count",
            "mgv_param_name", "mgv_param_numel",
-           "mgv_predict_velocity", "mgv_dit_forward", "mgv_flow_step", "mgv_flow_loss", "mgv_latent_rows",
+           "mgv_predict_velocity", "mgv_velocity_graph", "mgv_dit_forward", "mgv_flow_step", "mgv_flow_loss", "mgv_latent_rows",
            "mgv_rows_to_grid", "mgv_flow_step_device", "mgv_last_step_ms", "mgv_last_step_launches",
            "mgv_prof_enable", "mgv_prof_count", "mgv_prof_entry", "mgv_prof_entry_work",
            "mgv_ckpt_last_error", "mgv_ckpt_last_error_kind", "mgv_ckpt_load", "mgv_ckpt_free", "mgv_ckpt_count",
@@ -751,6 +752,30 @@ class Context:
         self._check(self._L.mgv_predict_velocity(self.h, rows.ctypes.data, rows.shape[0], co.ctypes.data, dm,
                                                   text.ctypes.data, text.shape[0], ts.ctypes.data, fps,
                                                   out.ctypes.data))
+        return out
+
+    def velocity_graph(self, rows, coords, dims, text, timesteps, fps=8.0, taps=False, dV=None):
+        """mgv_velocity_graph: velocity_rows_graph as one node -> dict(V[, taps][, grads]) (grads = the VJP with dV)."""
+        rows, text, ts = _f64(rows), _f64(text), _f64(timesteps)
+        co = np.ascontiguousarray(coords, dtype=np.int32)
+        dm = (I64 * 3)(*[int(x) for x in dims])
+        N, H, depth = rows.shape[0], self.cfg.hidden, self.cfg.depth
+        V = np.empty((N, self.cfg.patch_dim))
+        out = {"V": V}
+        tp = None
+        if taps:
+            tl = [np.empty((N, H)) for _ in range(depth + 2)] + [np.empty((N, self.cfg.patch_dim))]
+            tp = (P * len(tl))(*[a.ctypes.data for a in tl])
+            out["taps"] = tl
+        gp, dv = None, None
+        if dV is not None:
+            dv = _f64(dV)
+            garr = [np.empty(k) for k in self.numels]
+            gp = (P * len(garr))(*[a.ctypes.data for a in garr])
+            out["grads"] = dict(zip(self.names, garr))
+        self._check(self._L.mgv_velocity_graph(self.h, rows.ctypes.data, N, co.ctypes.data, dm, text.ctypes.data,
+                                                text.shape[0], ts.ctypes.data, fps, V.ctypes.data, tp,
+                                                None if dv is None else dv.ctypes.data, gp))
         return out
 
     def fused_modulate(self, x, bias, scale, shift, residual):

@@ -271,6 +271,15 @@ mgv_status mgv_predict_velocity(mgv_ctx* ctx, const double* rows, int64_t N, con
     return guard(ctx, [&] { ctx->model->predict_velocity(rows, N, coords, dims, text, L, timesteps, fps, out); });
 }
 
+mgv_status mgv_velocity_graph(mgv_ctx* ctx, const double* rows, int64_t N, const int32_t* coords,
+                              const int64_t dims[3], const double* text, int64_t L, const double* timesteps,
+                              double fps, double* velocity, double* const* taps, const double* dV,
+                              double* const* grads_out) {
+    return guard(ctx, [&] {
+        ctx->model->velocity_graph(rows, N, coords, dims, text, L, timesteps, fps, velocity, taps, dV, grads_out);
+    });
+}
+
 mgv_status mgv_dit_forward(mgv_ctx* ctx, const double* tokens, int64_t N, const int32_t* coords,
                            const int64_t dims[3], const double* text, int64_t L, const double* timesteps, double fps,
                            double* out) {

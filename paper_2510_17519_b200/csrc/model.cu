@@ -1716,6 +1716,122 @@ void Model::value_forward(const double* in, int64_t N, const int32_t* coords, co
     MGV_CUDA(cudaStreamSynchronize(s));
 }
 
+// ------------------------------------------------------------------ tape seam: velocity_rows_graph as one node
+template <class T>
+__global__ void to_f64_kernel(const T* src, int64_t n, double* dst) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        dst[e] = static_cast<double>(static_cast<float>(src[e]));
+}
+
+// unique timesteps -> modulation rows (dit.cpp:239-242 validates each); mid[i] = row of token i
+static void dedup_taus(const double* tau, int64_t N, std::vector<double>& uniq, std::vector<int32_t>& mid) {
+    uniq.clear();
+    mid.assign(static_cast<size_t>(N), 0);
+    std::unordered_map<uint64_t, int> seen;
+    for (int64_t i = 0; i < N; ++i) {
+        if (!(tau[i] >= 0.0 && tau[i] <= 1.0)) throw InputError("timestep outside [0, 1]");
+        uint64_t key;
+        std::memcpy(&key, &tau[i], sizeof(key));
+        if (tau[i] == 0.0) key = 0;  // +0 / -0
+        auto it = seen.find(key);
+        if (it == seen.end()) {
+            it = seen.emplace(key, static_cast<int>(uniq.size())).first;
+            uniq.push_back(tau[i]);
+        }
+        mid[static_cast<size_t>(i)] = it->second;
+    }
+}
+
+template <class T>
+void Model::velocity_graph_impl(const double* rows, int64_t N, const int32_t* coords, const int64_t dims[3],
+                                const double* text, int64_t L, const double* tau, double fps, double* V_out,
+                                double* const* taps_out, const double* dV, double* const* grads_out) {
+    if (!have_params_) throw InputError("no parameters uploaded");
+    if (!rows || !coords || !dims || !text || !tau) throw InputError("null argument");
+    if (N < 1 || N != dims[0] * dims[1] * dims[2]) throw DimensionError("token count does not match the grid");
+    if (L < 1 || L > 1 << 20) throw DimensionError("text embeddings must be (L, text_dim)");
+    if (world_ > 1 || tp_ > 1) throw ConfigError("the tape node runs on a single-device context");
+    WS& w = *ws_;
+    cudaStream_t s = stream_;
+    const int64_t H = cfg_.H(), D = cfg_.D();
+    std::vector<double> uniq;
+    std::vector<int32_t> mid;
+    dedup_taus(tau, N, uniq, mid);
+    w.N = N;
+    w.L = L;
+    w.n_u = static_cast<int>(uniq.size());
+    w.esz = bf16_ ? 2 : 4;
+    w.grads = true;  // keeps every block's residual stream (the taps) and the backward's activations
+    w.tp = tp_;
+    {
+        Sizer sz{true, 0, &arena_};
+        layout_ws(w, sz, cfg_, true);
+        arena_.reserve(sz.bytes);
+        arena_.reset();
+        Sizer real{false, 0, &arena_};
+        layout_ws(w, real, cfg_, true);
+    }
+    double* din = nullptr;
+    MGV_CUDA(cudaMallocAsync(&din, sizeof(double) * std::max({N * H, N * D, L * cfg_.text_dim}), s));
+    MGV_CUDA(cudaMemcpyAsync(w.coords, coords, sizeof(int32_t) * 3 * N, cudaMemcpyHostToDevice, s));
+    MGV_CUDA(cudaMemcpyAsync(w.mod_id, mid.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, s));
+    MGV_CUDA(cudaMemcpyAsync(w.taus, uniq.data(), sizeof(double) * uniq.size(), cudaMemcpyHostToDevice, s));
+    MGV_CUDA(cudaMemcpyAsync(din, text, sizeof(double) * L * cfg_.text_dim, cudaMemcpyHostToDevice, s));
+    convert_rows<T>(din, L * cfg_.text_dim, tp<T>(w.text), s);
+    MGV_CUDA(cudaMemcpyAsync(din, rows, sizeof(double) * N * D, cudaMemcpyHostToDevice, s));
+    convert_rows<T>(din, N * D, tp<T>(w.rows), s);
+    DevSample dummy;
+    forward_sample<T>(dummy, w.rows, uniq.data(), w.n_u, nullptr, fps, true, true, nullptr);
+    auto out_f32 = [&](const float* src, int64_t n, double* host) {
+        f32_to_f64<<<grid_of(n), 256, 0, s>>>(src, n, din);
+        note_launch();
+        MGV_CUDA(cudaMemcpyAsync(host, din, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+        MGV_CUDA(cudaStreamSynchronize(s));
+    };
+    if (V_out) out_f32(w.V, N * D, V_out);
+    if (taps_out) {  // dit.cpp:326-332 tap order
+        for (int i = 0; i <= cfg_.depth; ++i)
+            if (taps_out[i]) out_f32(w.X[i], N * H, taps_out[i]);  // patch embedding, then each block's output
+        if (double* y = taps_out[cfg_.depth + 1]) {               // final normed projection (dit.cpp:315)
+            to_f64_kernel<T><<<grid_of(N * H), 256, 0, s>>>(tp<T>(w.Y), N * H, din);
+            note_launch();
+            MGV_CUDA(cudaMemcpyAsync(y, din, sizeof(double) * N * H, cudaMemcpyDeviceToHost, s));
+            MGV_CUDA(cudaStreamSynchronize(s));
+        }
+        if (taps_out[cfg_.depth + 2]) out_f32(w.V, N * D, taps_out[cfg_.depth + 2]);
+    }
+    if (dV) {
+        MGV_CUDA(cudaMemsetAsync(grad_buf_, 0, sizeof(float) * grad_numel_, s));
+        MGV_CUDA(cudaMemcpyAsync(din, dV, sizeof(double) * N * D, cudaMemcpyHostToDevice, s));
+        convert_rows<T>(din, N * D, tp<T>(w.dV), s);
+        dp_overlap_ = false;
+        backward_sample<T>(w.dV);
+        if (grads_out) {
+            std::vector<void*> allocs;
+            auto dalloc = [&](size_t bytes) {
+                void* p = nullptr;
+                MGV_CUDA(cudaMallocAsync(&p, bytes, s));
+                allocs.push_back(p);
+                return p;
+            };
+            download_grads(grads_out, dalloc);
+            for (void* p : allocs) MGV_CUDA(cudaFreeAsync(p, s));
+        }
+    }
+    MGV_CUDA(cudaFreeAsync(din, s));
+    MGV_CUDA(cudaStreamSynchronize(s));
+}
+
+void Model::velocity_graph(const double* rows, int64_t N, const int32_t* coords, const int64_t dims[3],
+                           const double* text, int64_t L, const double* tau, double fps, double* V_out,
+                           double* const* taps_out, const double* dV, double* const* grads_out) {
+    MGV_CUDA(cudaSetDevice(device_));
+    if (bf16_)
+        velocity_graph_impl<__nv_bfloat16>(rows, N, coords, dims, text, L, tau, fps, V_out, taps_out, dV, grads_out);
+    else
+        velocity_graph_impl<float>(rows, N, coords, dims, text, L, tau, fps, V_out, taps_out, dV, grads_out);
+}
+
 // ------------------------------------------------------------------ boundary helpers (dit.cpp:257-265, 336-359)
 void Model::patchify(const double* grid, int64_t U, int64_t h, int64_t w_, int64_t C, double* tokens,
                      int32_t* coords) {

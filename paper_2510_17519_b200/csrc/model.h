@@ -152,6 +152,13 @@ public:
                           const double* text, int64_t L, const double* tau, double fps, double* out);
     void dit_forward(const double* tokens, int64_t N, const int32_t* coords, const int64_t dims[3],
                      const double* text, int64_t L, const double* tau, double fps, double* out);
+    // The tape-level builder velocity_rows_graph (dit.cpp:320-334) as one device node: forward with the reference's
+    // taps (patch embedding, each block's residual output, the final normed projection, the velocity; any output
+    // pointer may be null) and, when dV is given, the vector-Jacobian product: gradients of sum(dV * V) w.r.t.
+    // every dit.* parameter (sorted-name order, overwritten) -- the node's backward closure.
+    void velocity_graph(const double* rows, int64_t N, const int32_t* coords, const int64_t dims[3],
+                        const double* text, int64_t L, const double* tau, double fps, double* V_out,
+                        double* const* taps_out, const double* dV, double* const* grads_out);
     // dit::patchify / unpatchify / global_embed (dit.hpp:83-90): the projections at either end of the block
     // stack and the timestep/fps embedding, from the device weights (fp32 masters, IEEE-fp32 GEMMs)
     void patchify(const double* grid, int64_t U, int64_t h, int64_t w, int64_t C, double* tokens, int32_t* coords);
@@ -210,6 +217,10 @@ private:
     void sample_impl(const double* x_start, int64_t N, const int32_t* coords, const int64_t dims[3],
                      const double* text, int64_t L, const uint8_t* cond, const double* cond_latents, int64_t steps,
                      int direction, double fps, double* out);
+    template <class T>
+    void velocity_graph_impl(const double* rows, int64_t N, const int32_t* coords, const int64_t dims[3],
+                             const double* text, int64_t L, const double* tau, double fps, double* V_out,
+                             double* const* taps_out, const double* dV, double* const* grads_out);
     template <class T>
     void value_forward(const double* in, int64_t N, const int32_t* coords, const int64_t dims[3],
                        const double* text, int64_t L, const double* tau, double fps, double* out, bool velocity);
