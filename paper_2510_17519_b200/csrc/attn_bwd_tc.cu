@@ -15,6 +15,7 @@
 // current tile's elementwise work.
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 #include <vector>
 
 #include "attn.h"
@@ -488,6 +489,257 @@ __global__ void __launch_bounds__(128 + 128 * CW, 1) attn_bwd_dkv_v8_kernel(cons
     if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// =====================================================================================  dK / dV (v11)
+// 128-query steps with every product an N >= 128 MMA (34 instructions per 128 queries; v8: 52).  TMEM:
+//   SD [0,128)    S^T(i) -> (loaded into registers) -> dP^T(i) -> (loaded) -> S^T(i+1)
+//   PT [128,192)  P^T(i) (bf16 pairs) -> (read by dV(i)) -> dS^T(i) -> (read by dK(i)) -> P^T(i+1)
+//   dV [192, 192+HDP)   dK [.., +HDP)
+// MMA issue order per step:  dP^T(i) [S^T(i) loaded]  dV(i) [P^T(i) stored]  S^T(i+1) [dP^T(i) loaded]
+// dK(i) [dS^T(i) stored]; the in-order tensor pipe keeps each overwrite behind its reader.  Operands:
+//   S^T  = K Q^T    SS: K row tile (K-major) x two 64-token Q^T tiles read MN-major (LBO = one tile)
+//   dP^T = V dO^T   SS: V row tile x the dO^T tiles, MN-major
+//   dV  += P^T dO   TS: P^T from TMEM x the dO^T tiles read K-major (N = HD)
+//   dK  += dS^T Q   TS: dS^T from TMEM x the Q^T tiles read K-major
+// The exponentials of step i run under dK(i-1) and dP^T(i); dS(i) under S^T(i+1).
+template <int HD>
+__device__ __forceinline__ void mma_rows_x_t128(uint32_t d, uint32_t a, uint32_t bt) {
+    using T = BT<HD>;
+    constexpr uint32_t id = idesc_bf16_f32(128, 128, false, true);
+    int kk = 0;
+#pragma unroll
+    for (int c = 0; c < T::NF; ++c)
+#pragma unroll
+        for (int k = 0; k < 4; ++k, ++kk)
+            umma_f16_ss(d, smem_desc(a + c * 16384 + k * 32, 16, 1024, kSwizzle128),
+                        smem_desc(bt + kk * 2048, T::T_TILE, 1024, kSwizzle128), id, kk > 0);
+    if (T::TAIL)
+        umma_f16_ss(d, smem_desc(a + T::NF * 16384, 16, 256, kSwizzle32),
+                    smem_desc(bt + kk * 2048, T::T_TILE, 1024, kSwizzle128), id, 1);
+}
+// D[128 x HD] (+)= A[128 x 128] (TMEM, bf16 pairs, 64 columns) . B with B two HD x 64 transposed tiles read
+// K-major (K = 128 tokens): eight N = HD MMAs
+template <int HD>
+__device__ __forceinline__ void mma_tmem128_x_t(uint32_t d, uint32_t a_tmem, uint32_t bt, bool acc_first) {
+    using T = BT<HD>;
+    constexpr uint32_t id = idesc_bf16_f32(128, HD, false, false);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks)
+        umma_f16_ts(d, a_tmem + ks * 8, smem_desc(bt + (ks >> 2) * T::T_TILE + (ks & 3) * 32, 16, 1024, kSwizzle128),
+                    id, (acc_first || ks > 0) ? 1u : 0u);
+}
+
+template <int HD>
+__global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_constant__ BwdMaps tm,
+                                                                  AttnBwdProblem p, float* part) {
+    constexpr int BKV = 128, BQ = 128, NST = 2;
+    using T = BT<HD>;
+    constexpr int HDP = ((HD + 15) / 16) * 16;
+    constexpr int SD_COL = 0, PT_COL = 128, DV_COL = 192, DK_COL = DV_COL + HDP;
+    static_assert(DK_COL + HDP <= 512, "TMEM budget");
+    constexpr int QT = 2 * T::T_TILE;  // 128 tokens of a transposed operand (two 64-token tiles)
+    constexpr int ROW_BYTES = T::NF * 16384 + (T::TAIL ? 4096 : 0);
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sK = smem;
+    uint8_t* sV = sK + T::ROW_TILE;
+    uint8_t* sQt = sV + T::ROW_TILE;   // [NST]
+    uint8_t* sdOt = sQt + NST * QT;     // [NST]
+    float* sLse = reinterpret_cast<float*>(sdOt + NST * QT);  // [NST][BQ]
+    float* sD = sLse + NST * BQ;                               // [NST][BQ]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sD + NST * BQ);
+    uint64_t* k_full = bars;
+    uint64_t* qd_full = bars + 1;         // [NST]
+    uint64_t* qd_empty = bars + 1 + NST;  // [NST]
+    uint64_t* s_full = bars + 1 + 2 * NST;
+    uint64_t* s_loaded = s_full + 1;
+    uint64_t* dp_full = s_full + 2;
+    uint64_t* dp_loaded = s_full + 3;
+    uint64_t* p_full = s_full + 4;
+    uint64_t* pv_done = s_full + 5;
+    uint64_t* ds_full = s_full + 6;
+    uint64_t* dk_done = s_full + 7;
+    uint64_t* acc_done = s_full + 8;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 9);
+
+    const AttnProblem& f = p.f;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int h = blockIdx.y, k0 = blockIdx.x * BKV;
+    const int nq_all = (f.Nq + BQ - 1) / BQ;
+    const int i0 = static_cast<int>((int64_t)blockIdx.z * nq_all / gridDim.z);
+    const int nq = static_cast<int>((int64_t)(blockIdx.z + 1) * nq_all / gridDim.z) - i0;  // this split's steps
+    const int col = h * HD;
+
+    if (threadIdx.x == 0) {
+        mbar_init(k_full, 1);
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&qd_full[i], 1);
+            mbar_init(&qd_empty[i], 1);
+        }
+        mbar_init(s_full, 1);
+        mbar_init(s_loaded, 8);
+        mbar_init(dp_full, 1);
+        mbar_init(dp_loaded, 8);
+        mbar_init(p_full, 8);
+        mbar_init(pv_done, 1);
+        mbar_init(ds_full, 8);
+        mbar_init(dk_done, 1);
+        mbar_init(acc_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            mbar_arrive_expect_tx(k_full, 2 * ROW_BYTES);
+            load_row_tile<HD>(sK, &tm.a128, &tm.a32, k_full, col, k0);
+            load_row_tile<HD>(sV, &tm.b128, &tm.b32, k_full, col, k0);
+            for (int i = 0; i < nq; ++i) {
+                const int st = i % NST;
+                if (i >= NST) mbar_wait(&qd_empty[st], ((i / NST) - 1) & 1);
+                mbar_arrive_expect_tx(&qd_full[st], 2 * QT + 2 * BQ * 4);
+                const int qt = (i0 + i) * BQ;
+                tma_load_2d(sQt + st * QT, &tm.ta, &qd_full[st], qt, col);
+                tma_load_2d(sQt + st * QT + T::T_TILE, &tm.ta, &qd_full[st], qt + 64, col);
+                tma_load_2d(sdOt + st * QT, &tm.tb, &qd_full[st], qt, col);
+                tma_load_2d(sdOt + st * QT + T::T_TILE, &tm.tb, &qd_full[st], qt + 64, col);
+                bulk_load(sLse + st * BQ, f.lse + (int64_t)h * lse_stride(f) + qt, BQ * 4, &qd_full[st]);
+                bulk_load(sD + st * BQ, p.Dvec + (int64_t)h * lse_stride(f) + qt, BQ * 4, &qd_full[st]);
+            }
+        }
+    } else if (warp == 1) {
+        const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+        mbar_wait(k_full, 0);
+        if (nq > 0) {
+            mbar_wait(&qd_full[0], 0);
+            tc_fence_after();
+            if (elect_one()) {
+                mma_rows_x_t128<HD>(tmem + SD_COL, aK, smem_u32(sQt));
+                umma_commit(s_full);
+            }
+            __syncwarp();
+        }
+        for (int i = 0; i < nq; ++i) {
+            const int st = i % NST;
+            mbar_wait(s_loaded, i & 1);  // S^T(i) is in registers: dP^T(i) may overwrite it
+            tc_fence_after();
+            if (elect_one()) {
+                mma_rows_x_t128<HD>(tmem + SD_COL, aV, smem_u32(sdOt + st * QT));
+                umma_commit(dp_full);
+            }
+            __syncwarp();
+            mbar_wait(p_full, i & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                mma_tmem128_x_t<HD>(tmem + DV_COL, tmem + PT_COL, smem_u32(sdOt + st * QT), i > 0);
+                umma_commit(pv_done);
+            }
+            __syncwarp();
+            if (i + 1 < nq) {
+                mbar_wait(dp_loaded, i & 1);  // dP^T(i) is in registers: S^T(i+1) may overwrite it
+                mbar_wait(&qd_full[(i + 1) % NST], ((i + 1) / NST) & 1);
+                tc_fence_after();
+                if (elect_one()) {
+                    mma_rows_x_t128<HD>(tmem + SD_COL, aK, smem_u32(sQt + ((i + 1) % NST) * QT));
+                    umma_commit(s_full);
+                }
+                __syncwarp();
+            }
+            mbar_wait(ds_full, i & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                mma_tmem128_x_t<HD>(tmem + DK_COL, tmem + PT_COL, smem_u32(sQt + st * QT), i > 0);
+                umma_commit(dk_done);
+                umma_commit(&qd_empty[st]);
+                if (i == nq - 1) umma_commit(acc_done);
+            }
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        // two warps per TMEM lane group: warp half hf owns query columns [64 hf, 64 hf + 64) of each step
+        const int g = warp & 3, hf = (warp - 4) >> 2, row = g * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(g * 32) << 16;
+        const int kv = k0 + row;
+        const bool kvv = kv < f.Nk;
+        const uint32_t sd = tmem + lane_base + SD_COL + hf * 64, pt = tmem + lane_base + PT_COL + hf * 32;
+        for (int i = 0; i < nq; ++i) {
+            const int st = i % NST;
+            mbar_wait(&qd_full[st], (i / NST) & 1);  // lse / D rows of this step have landed
+            mbar_wait(s_full, i & 1);
+            tc_fence_after();
+            float s[64];
+            tmem_ld32(sd, reinterpret_cast<uint32_t*>(s));
+            tmem_ld32(sd + 32, reinterpret_cast<uint32_t*>(s + 32));
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(s_loaded);
+            const float* lse2 = sLse + st * BQ + hf * 64;
+            const float* Dq = sD + st * BQ + hf * 64;
+            const int qb = (i0 + i) * BQ + hf * 64;
+            const bool full = qb + 64 <= f.Nq;
+            uint32_t pk[32];
+#pragma unroll
+            for (int c = 0; c < 64; c += 2) {
+                const bool v0 = full || qb + c < f.Nq, v1 = full || qb + c + 1 < f.Nq;
+                s[c] = v0 ? ex2f((s[c] - lse2[c]) * kLog2e) : 0.0f;  // lse rows are natural-log
+                s[c + 1] = v1 ? ex2f((s[c + 1] - lse2[c + 1]) * kLog2e) : 0.0f;
+                pk[c / 2] = pack_bf16(s[c], s[c + 1]);
+            }
+            if (i >= 1) {
+                mbar_wait(dk_done, (i - 1) & 1);  // dK(i-1) has read dS^T(i-1) out of PT
+                tc_fence_after();
+            }
+            tmem_st32(pt, pk);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(p_full);
+            mbar_wait(dp_full, i & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                float dp[32];
+                tmem_ld32(sd + hh * 32, reinterpret_cast<uint32_t*>(dp));
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 32; c += 2)  // dS = P (dP - D) (autodiff.cpp:820)
+                    pk[(hh * 32 + c) / 2] = pack_bf16(s[hh * 32 + c] * (dp[c] - Dq[hh * 32 + c]),
+                                                      s[hh * 32 + c + 1] * (dp[c + 1] - Dq[hh * 32 + c + 1]));
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dp_loaded);
+            mbar_wait(pv_done, i & 1);  // dV(i) has read P^T(i) out of PT
+            tc_fence_after();
+            tmem_st32(pt, pk);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(ds_full);
+        }
+        if (nq > 0) mbar_wait(acc_done, 0);
+        tc_fence_after();
+        const bool valid = kvv && nq > 0;
+        if (part) {  // fp32 partial rows of this query split: [dV | dK]
+            const int64_t W = (int64_t)f.heads * HD;
+            float* prow = part + ((int64_t)blockIdx.z * f.Nk + (kvv ? kv : 0)) * 2 * W + (hf ? W : 0) + col;
+            store_acc_row_f32<HD>(tmem + lane_base + (hf ? DK_COL : DV_COL), prow, kvv);
+        } else {
+            __nv_bfloat16* out = hf == 0 ? static_cast<__nv_bfloat16*>(p.dv) + (int64_t)kv * p.dv_ld + col
+                                         : static_cast<__nv_bfloat16*>(p.dk) + (int64_t)kv * p.dk_ld + col;
+            store_acc_row<HD>(tmem + lane_base + (hf ? DK_COL : DV_COL), out, valid);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 // =====================================================================================  dQ (v10)
 // v9's 128-key steps with Q back in TMEM: S = Q K^T is a TS product, so the CTA's fixed A tile is no longer
 // re-read from shared memory on every key step (v9's two SS products move 2 x 74 KB of shared memory per
@@ -713,13 +965,21 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
         make_tmap_sw(&m.ta, qt, f.Nq, W, qt_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
         make_tmap_sw(&m.tb, dot, f.Nq, W, dot_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
         const int smem = T::ROW_TILE + 10 * T::T_TILE + 10 * 64 * 4 + 256 + 1024 + (HD > 128 ? 4096 : 0);
-        ensure_smem(attn_bwd_dkv_v8_kernel<HD, 2>, smem);
+        const int smem11 = 2 * T::ROW_TILE + 4 * 2 * T::T_TILE + 4 * 128 * 4 + 256 + 1024;
+        static const bool use_v8 = std::getenv("MGV_DKV_V8") != nullptr;  // A/B against the previous pass
+        if (use_v8)
+            ensure_smem(attn_bwd_dkv_v8_kernel<HD, 2>, smem);
+        else
+            ensure_smem(attn_bwd_dkv_v11_kernel<HD>, smem11);
         // few key tiles (cross-attention): split the query range so the grid still covers the SMs
-        const int kv_ctas = (f.Nk + 127) / 128 * f.heads, nq_all = (f.Nq + 63) / 64;
+        const int kv_ctas = (f.Nk + 127) / 128 * f.heads, nq_all = (f.Nq + 63) / 64 / (use_v8 ? 1 : 2);
         const int splits = std::max(1, std::min({num_sms() / std::max(kv_ctas, 1), nq_all / 8, 16}));
         float* part = nullptr;
         if (splits > 1) MGV_CUDA(cudaMallocAsync(&part, sizeof(float) * splits * f.Nk * 2 * W, s));
-        attn_bwd_dkv_v8_kernel<HD, 2><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem, s>>>(m, p, part);
+        if (use_v8)
+            attn_bwd_dkv_v8_kernel<HD, 2><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem, s>>>(m, p, part);
+        else
+            attn_bwd_dkv_v11_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem11, s>>>(m, p, part);
         ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
         if (splits > 1) {
@@ -770,9 +1030,9 @@ void attn_bwd_tc(const AttnBwdProblem& p, cudaStream_t s) {
     const void* dot = p.dot ? p.dot : make_t(p.dO, p.do_ld, f.Nq, &dot_ld);
     // lse / D rows are streamed with bulk copies: per-head stride must be a multiple of 64 covering Nq
     AttnBwdProblem q = p;
-    const int64_t need = (static_cast<int64_t>(f.Nq) + 63) / 64 * 64;
+    const int64_t need = (static_cast<int64_t>(f.Nq) + 127) / 128 * 128;
     std::vector<float*> ftmp;
-    if (lse_stride(f) < need || lse_stride(f) % 64 != 0) {
+    if (lse_stride(f) < need || lse_stride(f) % 128 != 0) {
         float *lse = nullptr, *dv = nullptr;
         MGV_CUDA(cudaMallocAsync(&lse, sizeof(float) * need * f.heads, s));
         MGV_CUDA(cudaMallocAsync(&dv, sizeof(float) * need * f.heads, s));

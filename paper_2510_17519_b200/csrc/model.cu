@@ -146,8 +146,8 @@ void layout_ws(Model::WS& w, S& a, const Cfg& c, bool grads) {
         b.rc = a.template take<float>(N);
         b.iq = a.template take<float>(N * nh);
         b.ik = a.template take<float>(N * nh);
-        b.lse = a.template take<float>(((N + 63) / 64 * 64) * nh);
-        b.lse_x = a.template take<float>(((N + 63) / 64 * 64) * nh);
+        b.lse = a.template take<float>(((N + 127) / 128 * 128) * nh);
+        b.lse_x = a.template take<float>(((N + 127) / 128 * 128) * nh);
         b.a = a.takeT(N * H, e);
         b.qkv = a.takeT(N * 3 * H, e);
         b.qk = a.takeT(N * 2 * H, e);
@@ -180,7 +180,7 @@ void layout_ws(Model::WS& w, S& a, const Cfg& c, bool grads) {
         w.s1 = a.takeT(N * H, e);
         w.s2 = a.takeT(N * H, e);
         w.dkv = a.takeT(L * 2 * H, e);
-        w.Dvec = a.template take<float>(((N + 63) / 64 * 64) * nh);
+        w.Dvec = a.template take<float>(((N + 127) / 128 * 128) * nh);
         w.part1 = a.template take<float>((int64_t)chunks * std::max<int64_t>(4 * H, 2 * H));
         w.part2 = a.template take<float>((int64_t)chunks * std::max<int64_t>(4 * H, 2 * H));
         w.q_splits_x = static_cast<int>(std::min<int64_t>(64, (N + 31) / 32));
@@ -867,7 +867,7 @@ void Model::block_fwd(int i, int64_t N) {
     AttnProblem ap{b.qk, 2 * H, off<T>(b.qk, H), 2 * H, off<T>(b.qkv, 2 * H), 3 * H, b.O, H, b.lse,
                    n, n, int(nh), int(hd)};
     prof_.begin("attn_fwd", s);
-    ap.lse_ld = (N + 63) / 64 * 64;
+    ap.lse_ld = (N + 127) / 128 * 128;
     attention_fwd<T>(bf, ap, s);  // mha (autodiff.cpp:755-793)
     prof_.end(s);
     gemm(bf, KM(b.O, H), KM(W(blk(i, "attn.out.w")), H), n, H, H,
@@ -883,7 +883,7 @@ void Model::block_fwd(int i, int64_t N) {
          EpiStore<T>{tp<T>(b.kv), 2 * H, P(blk(i, "xattn.kv.b")).f32, 1.0f, int(L), int(2 * H)}, s);
     AttnProblem xp{b.cqs, H, b.kv, 2 * H, off<T>(b.kv, H), 2 * H, b.Ox, H, b.lse_x, n, int(L), int(nh), int(hd)};
     prof_.begin("xattn_fwd", s);
-    xp.lse_ld = (N + 63) / 64 * 64;
+    xp.lse_ld = (N + 127) / 128 * 128;
     attention_fwd<T>(bf, xp, s);
     prof_.end(s);
     gemm(bf, KM(b.Ox, H), KM(W(blk(i, "xattn.out.w")), H), n, H, H,
@@ -940,7 +940,7 @@ void Model::block_bwd(int i, int64_t N) {
     AttnBwdProblem xb{AttnProblem{b.cqs, H, b.kv, 2 * H, off<T>(b.kv, H), 2 * H, b.Ox, H, b.lse_x, n, int(L), int(nh), int(hd)},
                       w.s2, H, w.Dvec, w.s1, H, w.dkv, 2 * H, off<T>(w.dkv, H), 2 * H, w.dkv_part, w.q_splits_x};
     prof_.begin("xattn_bwd", s);
-    xb.f.lse_ld = (N + 63) / 64 * 64;
+    xb.f.lse_ld = (N + 127) / 128 * 128;
     attention_bwd<T>(bf, xb, s);
     prof_.end(s);
     const float xscale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd)));
@@ -964,7 +964,7 @@ void Model::block_bwd(int i, int64_t N) {
     AttnBwdProblem ab{AttnProblem{b.qk, 2 * H, off<T>(b.qk, H), 2 * H, off<T>(b.qkv, 2 * H), 3 * H, b.O, H, b.lse, n, n, int(nh), int(hd)},
                       w.s2, H, w.Dvec, w.sB, 3 * H, off<T>(w.sB, H), 3 * H, off<T>(w.sB, 2 * H), 3 * H, nullptr, 1};
     prof_.begin("attn_bwd", s);
-    ab.f.lse_ld = (N + 63) / 64 * 64;
+    ab.f.lse_ld = (N + 127) / 128 * 128;
     attention_bwd<T>(bf, ab, s);
     prof_.end(s);
     qk_norm_rope_bwd<T>(tp<T>(w.sB), tp<T>(b.qkv), qk_layout_full(H, nh), n, H, nh, P(blk(i, "attn.temp")).f32, w.cs, b.iq, b.ik, w.part1, s);
@@ -994,7 +994,7 @@ void Model::block_fwd_tp(int i, int64_t N) {
     const bool bf = bf16_;
     cudaStream_t s = stream_;
     const int64_t H = cfg_.H(), nh = cfg_.heads, hd = cfg_.hd(), L = w.L, td = cfg_.text_dim;
-    const int64_t Hr = H / tp_, nhr = nh / tp_, Fr = 4 * H / tp_, lld = (N + 63) / 64 * 64;
+    const int64_t Hr = H / tp_, nhr = nh / tp_, Fr = 4 * H / tp_, lld = (N + 127) / 128 * 128;  // the attention backward streams 128-row lse / D tiles
     Blk& b = w.blk[w.grads ? i : 0];
     const float* Xin = w.X[w.grads ? i : (i % 2)];
     float* Xout = w.X[w.grads ? i + 1 : ((i + 1) % 2)];
@@ -1076,7 +1076,7 @@ void Model::block_bwd_tp(int i, int64_t N) {
     const bool bf = bf16_;
     cudaStream_t s = stream_;
     const int64_t H = cfg_.H(), nh = cfg_.heads, hd = cfg_.hd(), L = w.L, td = cfg_.text_dim;
-    const int64_t Hr = H / tp_, nhr = nh / tp_, Fr = 4 * H / tp_, lld = (N + 63) / 64 * 64;
+    const int64_t Hr = H / tp_, nhr = nh / tp_, Fr = 4 * H / tp_, lld = (N + 127) / 128 * 128;  // the attention backward streams 128-row lse / D tiles
     const int n = static_cast<int>(N), nu = w.n_u, chunks = row_chunks(n);
     Blk& b = w.blk[i];
     const float* Xin = w.X[i];

@@ -12,8 +12,17 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BUILD = os.path.join(ROOT, "shim", "_build")
 SUITES = ["test_dit", "test_flow", "test_expansion", "test_posttrain"]
-# test case name -> reason (filled from the first B200 run)
-EXPECTED_FAIL = {}
+# test case name -> why it cannot pass on fp32 device arithmetic (first B200 run); every other case
+# of the four suites passes unchanged
+EXPECTED_FAIL = {
+    # central differences with h = 1e-5 (fd_check.hpp:23): fp32 evaluation noise ~1e-7 |f| / h ~ 1e-2 > 1e-3
+    "velocity model gradients match finite differences": "fp64 finite differences (test_dit.cpp:490-516)",
+    "batch loss gradients match finite differences": "fp64 finite differences (test_flow.cpp:376-412)",
+    "post loss gradients match finite differences": "fp64 finite differences (test_posttrain.cpp)",
+    # fp64-level absolute tolerances on outputs of magnitude ~1
+    "dit_forward is equivariant under token permutation": "worst < 1e-9 (test_dit.cpp:224-261); fp32 gives ~1e-7",
+    "desk model expansion preserves the function and lands near 4x": "global_dev <= 1e-5 (test_expansion.cpp:219-220)",
+}
 
 
 def run_suite(exe, env=None):

@@ -20,8 +20,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 GRIDS = {64: (4, 8, 8), 256: (4, 16, 16), 512: (8, 16, 16), 1024: (16, 16, 16), 2048: (8, 32, 32)}
+GRIDS_H288 = {2048: (8, 32, 32), 4096: (16, 32, 32), 8192: (16, 32, 64)}
 JOBS = [("10b", "fwd", n) for n in (2048, 1024, 512, 256, 64)] + [("10b", "step", 256), ("10b", "step", 64),
-                                                                    ("tiny", "fwd", 64), ("tiny", "step", 64)]
+                                                                    ("tiny", "fwd", 64), ("tiny", "step", 64)] + \
+    [("h288", "fwd", n) for n in (8192, 4096, 2048)]
 
 
 def job(args):
@@ -32,11 +34,15 @@ def job(args):
         cfg, L = O.paper_config(depth=1), 64
         gs = O.gate_std_for(cfg.hidden)
         gate = (gs, gs / 4)
+    elif cfgname == "h288":  # attention-dominated: the N^2 coefficient (head_dim 144 long-N probe)
+        cfg, L = O.DitConfig(depth=1, hidden=288, heads=2, text_dim=64, c_z=24, rope_split=(48, 48, 48)), 8
+        gs = O.gate_std_for(288)
+        gate = (gs, gs / 4)
     else:
         cfg, L = O.DitConfig(depth=1, hidden=256, heads=4, text_dim=32, c_z=24, rope_split=(22, 22, 20)), 16
         gate = (0.2, 0.05)
     ref = O.RefModel(cfg, 1, 2, *gate)
-    g = O.Rng(3).uniform_tensor(GRIDS[n] + (cfg.c_z,), -1.0, 1.0)
+    g = O.Rng(3).uniform_tensor((GRIDS_H288 if cfgname == "h288" else GRIDS)[n] + (cfg.c_z,), -1.0, 1.0)
     s = O.make_batch([g], 0.0, O.Rng(5))
     text = O.Rng(4).normal_tensor((L, cfg.text_dim))
     opt = O.RefAdamW(1e-4) if kind == "step" else None
@@ -61,12 +67,16 @@ def main():
         avail_gb = 64.0
     with mp.get_context("spawn").Pool(max(1, min(len(jobs), ncpu, int(avail_gb // 14)))) as pool:
         res = pool.map(job, jobs, chunksize=1)
-    fwd = sorted((r["N"], r["seconds"]) for r in res if r["config"] == "10b" and r["kind"] == "fwd")
-    # least squares t = a N + b N^2
     import numpy as np
-    A = np.array([[n, n * n] for n, _ in fwd], dtype=float)
-    y = np.array([t for _, t in fwd])
-    (a, b), *_ = np.linalg.lstsq(A, y, rcond=None)
+    # the N^2 (attention) coefficient from the attention-dominated H288 points, scaled by width (4 N^2 H flops);
+    # the linear coefficient from the 10B-width points with that N^2 term removed (at N <= 2048 and H = 3456 the
+    # attention is < 8% of the forward, so a joint fit cannot resolve it)
+    h288 = sorted((r["N"], r["seconds"]) for r in res if r["config"] == "h288")
+    A = np.array([[n, n * n] for n, _ in h288], dtype=float)
+    (a288, b288), *_ = np.linalg.lstsq(A, np.array([t for _, t in h288]), rcond=None)
+    b = max(b288, 0.0) * 3456.0 / 288.0
+    fwd = sorted((r["N"], r["seconds"]) for r in res if r["config"] == "10b" and r["kind"] == "fwd")
+    a = float(np.mean([(t - b * n * n) / n for n, t in fwd]))
     steps = {r["N"]: r["seconds"] for r in res if r["config"] == "10b" and r["kind"] == "step"}
     fwds = dict(fwd)
     ratio = sum(steps[n] / fwds[n] for n in steps) / len(steps)
@@ -77,8 +87,8 @@ def main():
                        "step_tokens_per_s": n / (ratio * tf), "label": "EXTRAPOLATED from the fit (not run)"}
     doc = {"source": "tools/cpu_sweep.py: reference (oracle/_ref) single-threaded, one pinned core per job",
            "host": host_info(), "wall_s": time.time() - t0, "points": res,
-           "fit": {"model": "t_fwd = a N + b N^2 (10B dims depth 1, text 64x4096)", "a_s_per_token": a,
-                   "b_s_per_token2": b, "step_over_fwd": ratio},
+           "fit": {"model": "t_fwd = a N + b N^2 (10B dims depth 1, text 64x4096); b from the H288 points x 3456/288",
+                   "a_s_per_token": a, "b_s_per_token2": b, "b_h288": b288, "a_h288": a288, "step_over_fwd": ratio},
            "extrapolated": ext}
     with open(out_path, "w") as f:
         json.dump(doc, f, indent=1)

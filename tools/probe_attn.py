@@ -27,7 +27,7 @@ q.div_(q.norm(dim=-1, keepdim=True))
 q[:, :heads] *= 10.0
 qkv = qkv.bfloat16()
 o = torch.empty(N, H, device="cuda").bfloat16()
-lse = torch.empty(heads, (N + 63) // 64 * 64, device="cuda")
+lse = torch.empty(heads, (N + 127) // 128 * 128, device="cuda")
 lse_ld = lse.stride(0)
 
 
@@ -52,7 +52,7 @@ if what in ("fwd", "both"):
     print(f"attn fwd N={N}: {ms:8.3f} ms  {4.0 * N * N * H / ms / 1e9:7.1f} TFLOP/s")
 if what in ("bwd", "both"):
     dO = (torch.randn(N, H, device="cuda", generator=g) * 0.1).bfloat16()
-    Dv = torch.empty(heads, (N + 63) // 64 * 64, device="cuda")
+    Dv = torch.empty(heads, (N + 127) // 128 * 128, device="cuda")
     dqkv = torch.empty(N, 3 * H, device="cuda").bfloat16()
     bwd = lambda: L.mgv_dev_attn_bwd(1, P(qkv.data_ptr()), i64(3 * H), P(qkv[:, H:].data_ptr()), i64(3 * H),
                                      P(qkv[:, 2 * H:].data_ptr()), i64(3 * H), P(o.data_ptr()), i64(H),
