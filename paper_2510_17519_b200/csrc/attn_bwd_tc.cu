@@ -74,6 +74,12 @@ struct BT {
     static constexpr int T_TILE = HD * 128;                          // HD rows x 64 tokens (transposed, SW128)
 };
 
+__device__ __forceinline__ float4 lds_f4(uint32_t saddr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
+    return v;
+}
+
 __device__ __forceinline__ float ex2f(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -626,6 +632,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
             const int st = i % NST;
             mbar_wait(s_loaded, i & 1);  // S^T(i) is in registers: dP^T(i) may overwrite it
             tc_fence_after();
+            if (lane == 0) ATR8(0, i);
             if (elect_one()) {
                 mma_rows_x_t128<HD>(tmem + SD_COL, aV, smem_u32(sdOt + st * QT));
                 umma_commit(dp_full);
@@ -633,6 +640,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
             __syncwarp();
             mbar_wait(p_full, i & 1);
             tc_fence_after();
+            if (lane == 0) ATR8(1, i);
             if (elect_one()) {
                 mma_tmem128_x_t<HD>(tmem + DV_COL, tmem + PT_COL, smem_u32(sdOt + st * QT), i > 0);
                 umma_commit(pv_done);
@@ -642,6 +650,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
                 mbar_wait(dp_loaded, i & 1);  // dP^T(i) is in registers: S^T(i+1) may overwrite it
                 mbar_wait(&qd_full[(i + 1) % NST], ((i + 1) / NST) & 1);
                 tc_fence_after();
+                if (lane == 0) ATR8(2, i);
                 if (elect_one()) {
                     mma_rows_x_t128<HD>(tmem + SD_COL, aK, smem_u32(sQt + ((i + 1) % NST) * QT));
                     umma_commit(s_full);
@@ -650,6 +659,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
             }
             mbar_wait(ds_full, i & 1);
             tc_fence_after();
+            if (lane == 0) ATR8(3, i);
             if (elect_one()) {
                 mma_tmem128_x_t<HD>(tmem + DK_COL, tmem + PT_COL, smem_u32(sQt + st * QT), i > 0);
                 umma_commit(dk_done);
@@ -670,6 +680,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
             mbar_wait(&qd_full[st], (i / NST) & 1);  // lse / D rows of this step have landed
             mbar_wait(s_full, i & 1);
             tc_fence_after();
+            if (warp == 4 && lane == 0) ATR8(4, i);
             float s[64];
             tmem_ld32(sd, reinterpret_cast<uint32_t*>(s));
             tmem_ld32(sd + 32, reinterpret_cast<uint32_t*>(s + 32));
@@ -677,17 +688,39 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(s_loaded);
-            const float* lse2 = sLse + st * BQ + hf * 64;
-            const float* Dq = sD + st * BQ + hf * 64;
+            // lse / D rows: 16-byte shared-memory broadcasts (one wavefront per 4 queries per warp); per-element
+            // generic loads made the compute warps' shared wavefronts outnumber the SS MMAs' operand reads
+            const uint32_t lse_s = smem_u32(sLse + st * BQ + hf * 64), d_s = smem_u32(sD + st * BQ + hf * 64);
             const int qb = (i0 + i) * BQ + hf * 64;
             const bool full = qb + 64 <= f.Nq;
             uint32_t pk[32];
+            const float2 lg2 = make_float2(kLog2e, kLog2e);
+            if (full) {  // warp-uniform: no per-column masking; packed f32x2 arithmetic (bit-identical to scalar)
 #pragma unroll
-            for (int c = 0; c < 64; c += 2) {
-                const bool v0 = full || qb + c < f.Nq, v1 = full || qb + c + 1 < f.Nq;
-                s[c] = v0 ? ex2f((s[c] - lse2[c]) * kLog2e) : 0.0f;  // lse rows are natural-log
-                s[c + 1] = v1 ? ex2f((s[c + 1] - lse2[c + 1]) * kLog2e) : 0.0f;
-                pk[c / 2] = pack_bf16(s[c], s[c + 1]);
+                for (int c4 = 0; c4 < 64; c4 += 4) {
+                    const float4 l = lds_f4(lse_s + c4 * 4);
+                    const float2 x0 = fmul2(fsub2(make_float2(s[c4], s[c4 + 1]), make_float2(l.x, l.y)), lg2);
+                    const float2 x1 = fmul2(fsub2(make_float2(s[c4 + 2], s[c4 + 3]), make_float2(l.z, l.w)), lg2);
+                    s[c4] = ex2f(x0.x);
+                    s[c4 + 1] = ex2f(x0.y);
+                    s[c4 + 2] = ex2f(x1.x);
+                    s[c4 + 3] = ex2f(x1.y);
+                    pk[c4 / 2] = pack_bf16(s[c4], s[c4 + 1]);
+                    pk[c4 / 2 + 1] = pack_bf16(s[c4 + 2], s[c4 + 3]);
+                }
+            } else {
+#pragma unroll
+                for (int c4 = 0; c4 < 64; c4 += 4) {
+                    const float4 l = lds_f4(lse_s + c4 * 4);
+                    const float lv[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int c = c4 + e;
+                        s[c] = qb + c < f.Nq ? ex2f((s[c] - lv[e]) * kLog2e) : 0.0f;  // lse rows are natural-log
+                    }
+                    pk[c4 / 2] = pack_bf16(s[c4], s[c4 + 1]);
+                    pk[c4 / 2 + 1] = pack_bf16(s[c4 + 2], s[c4 + 3]);
+                }
             }
             if (i >= 1) {
                 mbar_wait(dk_done, (i - 1) & 1);  // dK(i-1) has read dS^T(i-1) out of PT
@@ -698,23 +731,30 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full);
+            if (warp == 4 && lane == 0) ATR8(5, i);
             mbar_wait(dp_full, i & 1);
             tc_fence_after();
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                float dp[32];
-                tmem_ld32(sd + hh * 32, reinterpret_cast<uint32_t*>(dp));
-                tmem_wait_ld();
-#pragma unroll
-                for (int c = 0; c < 32; c += 2)  // dS = P (dP - D) (autodiff.cpp:820)
-                    pk[(hh * 32 + c) / 2] = pack_bf16(s[hh * 32 + c] * (dp[c] - Dq[hh * 32 + c]),
-                                                      s[hh * 32 + c + 1] * (dp[c + 1] - Dq[hh * 32 + c + 1]));
-            }
+            if (warp == 4 && lane == 0) ATR8(6, i);
+            float dp[64];
+            tmem_ld32(sd, reinterpret_cast<uint32_t*>(dp));
+            tmem_ld32(sd + 32, reinterpret_cast<uint32_t*>(dp + 32));
+            tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(dp_loaded);
+            if (lane == 0) mbar_arrive(dp_loaded);  // S^T(i+1) may now overwrite SD, under the dS math below
+#pragma unroll
+            for (int c = 0; c < 64; c += 4) {  // dS = P (dP - D) (autodiff.cpp:820), packed pairs
+                const float4 dd = lds_f4(d_s + c * 4);
+                const float2 d0 = fmul2(make_float2(s[c], s[c + 1]),
+                                        fsub2(make_float2(dp[c], dp[c + 1]), make_float2(dd.x, dd.y)));
+                const float2 d1 = fmul2(make_float2(s[c + 2], s[c + 3]),
+                                        fsub2(make_float2(dp[c + 2], dp[c + 3]), make_float2(dd.z, dd.w)));
+                pk[c / 2] = pack_bf16(d0.x, d0.y);
+                pk[c / 2 + 1] = pack_bf16(d1.x, d1.y);
+            }
             mbar_wait(pv_done, i & 1);  // dV(i) has read P^T(i) out of PT
             tc_fence_after();
+            if (warp == 4 && lane == 0) ATR8(7, i);
             tmem_st32(pt, pk);
             tmem_wait_st();
             tc_fence_before();
@@ -749,7 +789,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
 // own dP range, and the pipe order dQ(j) -> dP(j+1) keeps the next dP behind the dS reader.  NS K^T / V^T
 // stages (shared memory freed by Q).
 // TMEM: S [0,128)  dP|dS [128,256)  dQ [256,256+HD)  Q (bf16 pairs) [400,472).
-template <int HD, int NS>
+template <int HD, int NS>  // NS: K^T stages (V^T: 2; V^T is released by dP, K^T only by dQ)
 __global__ void __launch_bounds__(128 + 128 * 2, 1) attn_bwd_dq_v10_kernel(const __grid_constant__ BwdMaps tm,
                                                                           AttnBwdProblem p) {
     constexpr int BMQ = 128, BKV = 128, CW = 2, KW = BKV / CW;
@@ -758,18 +798,19 @@ __global__ void __launch_bounds__(128 + 128 * 2, 1) attn_bwd_dq_v10_kernel(const
     constexpr int S_COL = 0, DP_COL = 128, DS_COL = DP_COL + 32, DQ_COL = 256, Q_COL = 400;
     static_assert(DQ_COL + HDP <= Q_COL && Q_COL + HD / 2 <= 512, "TMEM budget");
     constexpr int KV_STAGE = 2 * T::T_TILE;  // two 64-key transposed tiles
+    constexpr int NSV = 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sdO = smem;
     uint8_t* sKt = sdO + T::ROW_TILE;    // [NS]
-    uint8_t* sVt = sKt + NS * KV_STAGE;  // [NS]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sVt + NS * KV_STAGE);
+    uint8_t* sVt = sKt + NS * KV_STAGE;  // [NSV]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sVt + NSV * KV_STAGE);
     uint64_t* do_full = bars;
     uint64_t* kf = bars + 1;           // [NS]
     uint64_t* ke = kf + NS;            // [NS]
-    uint64_t* vf = ke + NS;            // [NS]
-    uint64_t* ve = vf + NS;            // [NS]
-    uint64_t* s_full = ve + NS;
+    uint64_t* vf = ke + NS;            // [NSV]
+    uint64_t* ve = vf + NSV;           // [NSV]
+    uint64_t* s_full = ve + NSV;
     uint64_t* s_empty = s_full + 1;
     uint64_t* dp_full = s_full + 2;
     uint64_t* ds_full = s_full + 3;
@@ -788,6 +829,8 @@ __global__ void __launch_bounds__(128 + 128 * 2, 1) attn_bwd_dq_v10_kernel(const
         for (int i = 0; i < NS; ++i) {
             mbar_init(&kf[i], 1);
             mbar_init(&ke[i], 1);
+        }
+        for (int i = 0; i < NSV; ++i) {
             mbar_init(&vf[i], 1);
             mbar_init(&ve[i], 1);
         }
@@ -815,10 +858,11 @@ __global__ void __launch_bounds__(128 + 128 * 2, 1) attn_bwd_dq_v10_kernel(const
                 mbar_arrive_expect_tx(&kf[b], KV_STAGE);
                 tma_load_2d(sKt + b * KV_STAGE, &tm.ta, &kf[b], j * BKV, col);
                 tma_load_2d(sKt + b * KV_STAGE + T::T_TILE, &tm.ta, &kf[b], j * BKV + 64, col);
-                if (j >= NS) mbar_wait(&ve[b], ((j / NS) - 1) & 1);
-                mbar_arrive_expect_tx(&vf[b], KV_STAGE);
-                tma_load_2d(sVt + b * KV_STAGE, &tm.tb, &vf[b], j * BKV, col);
-                tma_load_2d(sVt + b * KV_STAGE + T::T_TILE, &tm.tb, &vf[b], j * BKV + 64, col);
+                const int bv = j % NSV;
+                if (j >= NSV) mbar_wait(&ve[bv], ((j / NSV) - 1) & 1);
+                mbar_arrive_expect_tx(&vf[bv], KV_STAGE);
+                tma_load_2d(sVt + bv * KV_STAGE, &tm.tb, &vf[bv], j * BKV, col);
+                tma_load_2d(sVt + bv * KV_STAGE + T::T_TILE, &tm.tb, &vf[bv], j * BKV + 64, col);
             }
         }
     } else if (warp == 1) {
@@ -828,6 +872,7 @@ __global__ void __launch_bounds__(128 + 128 * 2, 1) attn_bwd_dq_v10_kernel(const
             mbar_wait(&kf[b], (j / NS) & 1);
             if (j >= 1) mbar_wait(s_empty, (j - 1) & 1);
             tc_fence_after();
+            if ((threadIdx.x & 31) == 0) ATR(0, j);
             if (elect_one()) {
                 const uint32_t bt = smem_u32(sKt + b * KV_STAGE);
 #pragma unroll
@@ -839,9 +884,10 @@ __global__ void __launch_bounds__(128 + 128 * 2, 1) attn_bwd_dq_v10_kernel(const
             __syncwarp();
         };
         auto issue_dp = [&](int j) {  // dP = dO V^T (SS); behind dQ(j-1) in the pipe, which has read dS(j-1)
-            const int b = j % NS;
-            mbar_wait(&vf[b], (j / NS) & 1);
+            const int b = j % NSV;
+            mbar_wait(&vf[b], (j / NSV) & 1);
             tc_fence_after();
+            if ((threadIdx.x & 31) == 0) ATR(2, j);
             if (elect_one()) {
                 const uint32_t a = smem_u32(sdO), bt = smem_u32(sVt + b * KV_STAGE);
                 int kk = 0;
@@ -870,6 +916,7 @@ __global__ void __launch_bounds__(128 + 128 * 2, 1) attn_bwd_dq_v10_kernel(const
             if (j + 1 < nkv) issue_s(j + 1);
             mbar_wait(ds_full, j & 1);
             tc_fence_after();
+            if ((threadIdx.x & 31) == 0) ATR(1, j);
             if (elect_one()) {  // dQ += dS_j K_j: 8 k-steps of 16 keys over the stage's two K^T tiles
                 const uint32_t bt = smem_u32(sKt + b * KV_STAGE);
 #pragma unroll
@@ -903,36 +950,49 @@ __global__ void __launch_bounds__(128 + 128 * 2, 1) attn_bwd_dq_v10_kernel(const
             float pr[KW];
             mbar_wait(s_full, j & 1);
             tc_fence_after();
+            if (warp == 4 && lane == 0) ATR(3, j);
             tmem_ld32(tmem + lane_base + S_COL + hf * KW, reinterpret_cast<uint32_t*>(pr));
             tmem_ld32(tmem + lane_base + S_COL + hf * KW + 32, reinterpret_cast<uint32_t*>(pr + 32));
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(s_empty);
+            if (warp == 4 && lane == 0) ATR(4, j);
             const int kb = j * BKV + hf * KW;
-            if (kb + KW <= f.Nk) {
+            if (kb + KW <= f.Nk) {  // packed pairs: FFMA2 (bit-identical to the scalar fmaf)
+                const float2 lg2 = make_float2(kLog2e, kLog2e), nl2 = make_float2(-lse2, -lse2);
 #pragma unroll
-                for (int c = 0; c < KW; ++c) pr[c] = ex2f(fmaf(pr[c], kLog2e, -lse2));
+                for (int c = 0; c < KW; c += 2) {
+                    const float2 x = ffma2(make_float2(pr[c], pr[c + 1]), lg2, nl2);
+                    pr[c] = ex2f(x.x);
+                    pr[c + 1] = ex2f(x.y);
+                }
             } else {
 #pragma unroll
                 for (int c = 0; c < KW; ++c) pr[c] = kb + c < f.Nk ? ex2f(fmaf(pr[c], kLog2e, -lse2)) : 0.0f;
             }
+            if (warp == 4 && lane == 0) ATR(5, j);
             mbar_wait(dp_full, j & 1);
             tc_fence_after();
+            if (warp == 4 && lane == 0) ATR(6, j);
             float dp[KW];
             tmem_ld32(tmem + lane_base + DP_COL + hf * KW, reinterpret_cast<uint32_t*>(dp));
             tmem_ld32(tmem + lane_base + DP_COL + hf * KW + 32, reinterpret_cast<uint32_t*>(dp + 32));
             tmem_wait_ld();  // all of this warp's dP columns are in registers before its dS overwrites them
             uint32_t dk[KW / 2];
+            const float2 D2 = make_float2(Dq, Dq);
 #pragma unroll
-            for (int c = 0; c < KW; c += 2)
-                dk[c / 2] = pack_bf16(pr[c] * (dp[c] - Dq), pr[c + 1] * (dp[c + 1] - Dq));  // autodiff.cpp:820
+            for (int c = 0; c < KW; c += 2) {  // dS = P (dP - D) (autodiff.cpp:820), packed pairs
+                const float2 d = fmul2(make_float2(pr[c], pr[c + 1]), fsub2(make_float2(dp[c], dp[c + 1]), D2));
+                dk[c / 2] = pack_bf16(d.x, d.y);
+            }
             tmem_st16(tmem + lane_base + DS_COL + hf * (KW / 2), dk);
             tmem_st16(tmem + lane_base + DS_COL + hf * (KW / 2) + 16, dk + 16);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(ds_full);
+            if (warp == 4 && lane == 0) ATR(7, j);
         }
         if (nkv > 0) mbar_wait(acc_done, 0);
         tc_fence_after();
@@ -1001,9 +1061,9 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
             throw std::runtime_error("attn_bwd_tc: q / dO must be 16-byte aligned with ld % 8 == 0");
         make_tmap_sw(&m.b128, p.dO, W, f.Nq, p.do_ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
         make_tmap_sw(&m.b32, p.dO, W, f.Nq, p.do_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
-        const int smem = T::ROW_TILE + 8 * T::T_TILE + 256 + 1024;
-        ensure_smem(attn_bwd_dq_v10_kernel<HD, 2>, smem);
-        attn_bwd_dq_v10_kernel<HD, 2><<<dim3((f.Nq + 127) / 128, f.heads), 128 + 128 * 2, smem, s>>>(m, p);
+        const int smem = T::ROW_TILE + (3 + 2) * 2 * T::T_TILE + 256 + 1024;
+        ensure_smem(attn_bwd_dq_v10_kernel<HD, 3>, smem);
+        attn_bwd_dq_v10_kernel<HD, 3><<<dim3((f.Nq + 127) / 128, f.heads), 128 + 128 * 2, smem, s>>>(m, p);
         ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
     }
