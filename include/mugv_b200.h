@@ -146,6 +146,14 @@ mgv_status mgv_params_init(mgv_ctx* ctx, const mgv_dit_cfg* cfg, uint64_t seed, 
 mgv_status mgv_rng_uniform_fill(uint64_t seed, int64_t n, double lo, double hi, double* out);
 mgv_status mgv_make_flow_sample(uint64_t seed, int64_t N, int64_t D, double mask_prob, double* noise, double* t,
                                 int* conditioned);
+/* Memory per rank, out = {parameters (fp32 masters + bf16 operand copies), gradients, AdamW moments, step
+ * workspace (saved activations + scratch), TP exchange arena} in bytes.  mgv_plan_rank_bytes plans a step of
+ * N tokens (text length L, n_u unique timesteps) for TP degree tp without a device, with the runtime's own
+ * layout code (one real TP rank: its parameter blocks and H/P-wide activations); mgv_ctx_memory reports what a
+ * context holds now (emulated TP ranks hold all P slots). */
+mgv_status mgv_plan_rank_bytes(const mgv_dit_cfg* cfg, int precision, int tp, int64_t N, int64_t L, int64_t n_u,
+                               int train, int64_t out[5]);
+mgv_status mgv_ctx_memory(mgv_ctx* ctx, int64_t out[5]);
 /* Upload (or replace) the dit.* ParameterSet.  names/data/numel are n parallel arrays (any order). */
 mgv_status mgv_params_upload(mgv_ctx* ctx, const mgv_dit_cfg* cfg, int64_t n, const char* const* names,
                              const double* const* data, const int64_t* numel);

@@ -120,6 +120,8 @@ def declare(L):
     L.mgv_rng_uniform_fill.argtypes = [ctypes.c_uint64, I64, D, D, P]
     L.mgv_make_flow_sample.argtypes = [ctypes.c_uint64, I64, I64, D, P, P, P]
     L.mgv_velocity_graph.argtypes = [P, P, I64, P, P, P, I64, P, D, P, P, P, P]
+    L.mgv_plan_rank_bytes.argtypes = [ctypes.POINTER(mgv_dit_cfg), I, I, I64, I64, I64, I, P]
+    L.mgv_ctx_memory.argtypes = [P, P]
     L.mgv_params_init.argtypes = [P, ctypes.POINTER(mgv_dit_cfg), ctypes.c_uint64, ctypes.c_uint64, D, D]
     L.mgv_params_upload.restype = I
     L.mgv_param_count.argtypes = [P]
@@ -244,7 +246,7 @@ def declare(L):
 # symbols include/mugv_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = ["mgv_ctx_create", "mgv_ctx_destroy", "mgv_last_error", "mgv_ctx_set_stream", "mgv_nccl_unique_id",
            "mgv_ctx_set_dp", "mgv_ctx_set_tp", "mgv_sample_rows", "mgv_ctx_set_adamw", "mgv_adamw_steps", "mgv_param_download",
-           "mgv_params_upload", "mgv_params_init", "mgv_rng_uniform_fill", "mgv_make_flow_sample", "mgv_param_count",
+           "mgv_params_upload", "mgv_params_init", "mgv_plan_rank_bytes", "mgv_ctx_memory", "mgv_rng_uniform_fill", "mgv_make_flow_sample", "mgv_param_count",
            "mgv_param_name", "mgv_param_numel",
            "mgv_predict_velocity", "mgv_velocity_graph", "mgv_dit_forward", "mgv_flow_step", "mgv_flow_loss", "mgv_latent_rows",
            "mgv_rows_to_grid", "mgv_flow_step_device", "mgv_last_step_ms", "mgv_last_step_launches",
@@ -391,6 +393,19 @@ def paper_config(depth=56):
 
 def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+MEMORY_KEYS = ("params", "grads", "adamw", "workspace", "exchange")
+
+
+def plan_rank_bytes(cfg, precision: str, tp: int, N: int, L: int, n_u: int = 2, train: bool = True) -> dict:
+    """mgv_plan_rank_bytes: bytes one TP rank allocates for a step (no device needed)."""
+    out = (I64 * 5)()
+    c = cfg.to_c()
+    st = _lib().mgv_plan_rank_bytes(ctypes.byref(c), 1 if precision == "bf16" else 0, tp, N, L, n_u, int(train), out)
+    if st != 0:
+        raise ConfigError(f"mgv_plan_rank_bytes failed ({st})")
+    return dict(zip(MEMORY_KEYS, list(out)))
 
 
 def rng_uniform(seed: int, shape, lo: float, hi: float) -> np.ndarray:
@@ -720,6 +735,12 @@ class Context:
         self.cfg = cfg
         self.names = [self._L.mgv_param_name(self.h, i).decode() for i in range(self._L.mgv_param_count(self.h))]
         self.numels = [self._L.mgv_param_numel(self.h, i) for i in range(len(self.names))]
+
+    def memory(self) -> dict:
+        """mgv_ctx_memory: this context's allocations in bytes."""
+        out = (I64 * 5)()
+        self._check(self._L.mgv_ctx_memory(self.h, out))
+        return dict(zip(MEMORY_KEYS, list(out)))
 
     def init_params(self, cfg: DitConfig, seed: int = 1, gate_seed: int = 0, gate_std: float = 0.0,
                     gate_b_std: float = 0.0):

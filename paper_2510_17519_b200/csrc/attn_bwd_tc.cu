@@ -1,18 +1,19 @@
 // tcgen05 flash-attention backward for sm_100a, deterministic (no atomics):
 // the gradient of Tape::mha (autodiff.cpp:795-843) in two passes.
 //
-//   dK/dV pass  CTA per (128-key tile, head), loops over 64-query tiles:
-//                 S^T = K Q^T,  dP^T = V dO^T          (TMEM; Q^T/dO^T tiles read MN-major)
+//   dK/dV pass  CTA per (128-key tile, head), loops over 128-query steps:
+//                 S^T = K Q^T,  dP^T = V dO^T          (SS; Q^T/dO^T tiles read MN-major)
 //                 P^T = exp(S^T - lse), dS^T = P^T (dP^T - D)   (thread = key row)
-//                 dV += P^T dO, dK += dS^T Q           (ONE N=hd MMA per step: dO^T/Q^T read K-major)
-//   dQ pass     CTA per (128-query tile, head), loops over 64-key tiles:
-//                 S = Q K^T, dP = dO V^T               (double-buffered in TMEM)
+//                 dV += P^T dO, dK += dS^T Q           (TS; dO^T/Q^T read K-major, one N = hd MMA per k-step)
+//   dQ pass     CTA per (128-query tile, head), loops over 128-key steps:
+//                 S = Q K^T (TS), dP = dO V^T (SS)
 //                 dS = P (dP - D)                      (thread = query row)
-//                 dQ += dS K                           (K^T tile read K-major, N = hd)
+//                 dQ += dS K                           (TS; K^T tiles read K-major, N = hd)
 // The transposed operands (Q^T, K^T, V^T, dO^T: [heads*hd][tokens]) are made
 // once per step by a tiled transpose, so no MMA ever splits head_dim 144 into
-// 128 + 16.  The MMA warp issues the next tile's S/dP products under the
-// current tile's elementwise work.
+// 128 + 16.  The MMA warp issues the next tile's products under the current
+// tile's elementwise work.  Earlier variants (64-query dK/dV steps with V in TMEM,
+// CTA-pair / DSMEM exchanges, 64-key dQ steps) are in the history of this file.
 #include <algorithm>
 #include <cfloat>
 #include <cstdlib>
@@ -237,266 +238,9 @@ __device__ __forceinline__ void mma_tmem_rows_x_t(uint32_t d, uint32_t a_tmem, u
 }
 
 
-// =====================================================================================  dK / dV (v8)
-// The default dK/dV pass.  Against v5 above it moves V (not K) into TMEM and gives P^T its own columns:
-//   S^T  = K Q^T     SS (K row tile in shared memory)         -> free-running: S^T(i+1) is issued as soon as
-//                                                                the compute warps have loaded S^T(i)
-//   dP^T = V dO^T    TS (V columns [0,128) in TMEM, the 16-column tail of head_dim 144 one SS k-step)
-//   dV  += P^T dO    TS (P^T in its own 32 columns)
-//   dK  += dS^T Q    TS (dS^T written over the consumed dP^T columns)
-// so neither dependency loop (S^T -> softmax -> dV, dP^T -> dS -> dK -> dP^T) waits on the other product's
-// overwrite, and the one shared-memory-operand product is the one whose loop has slack.  Staging only 128
-// of V's 144 columns in TMEM is what makes the 512-column budget close:
-//   S^T [0,64)  P^T [64,96)  dP^T|dS^T [96,160)  dV [160,160+HD)  dK [.., +HD)  V (bf16 pairs) [.., +64)
-template <int HD, int CW>
-__global__ void __launch_bounds__(128 + 128 * CW, 1) attn_bwd_dkv_v8_kernel(const __grid_constant__ BwdMaps tm,
-                                                                           AttnBwdProblem p, float* part) {
-    constexpr int BKV = 128, BQ = 64, NST = 5;
-    static_assert(CW == 2 || CW == 4, "2 or 4 compute warps per TMEM lane group");
-    using T = BT<HD>;
-    constexpr int VA = HD >= 128 ? 128 : HD;  // V columns staged in TMEM
-    constexpr int VT = HD - VA;               // tail columns read from shared memory
-    static_assert(VT == 0 || VT == 16, "head_dim tail must be one 16-column k-step");
-    constexpr int HDP = ((HD + 15) / 16) * 16;
-    constexpr int S_COL = 0, P_COL = 64, DP_COL = 96, DV_COL = 160, DK_COL = DV_COL + HDP, VA_COL = DK_COL + HDP;
-    static_assert(VA_COL + VA / 2 <= 512, "TMEM budget");
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sK = smem;
-    uint8_t* sVt = sK + T::ROW_TILE;                       // 128 x 16 SW32 tail of V (HD = 144)
-    uint8_t* sQt = sVt + (VT ? 4096 : 0);                  // [NST]
-    uint8_t* sdOt = sQt + NST * T::T_TILE;                 // [NST]
-    float* sLse = reinterpret_cast<float*>(sdOt + NST * T::T_TILE);  // [NST][64]
-    float* sD = sLse + NST * BQ;                                      // [NST][64]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sD + NST * BQ);
-    uint64_t* k_full = bars;
-    uint64_t* qd_full = bars + 1;         // [NST]
-    uint64_t* qd_empty = bars + 1 + NST;  // [NST]
-    uint64_t* s_full = bars + 1 + 2 * NST;
-    uint64_t* s_empty = s_full + 1;
-    uint64_t* p_full = s_full + 2;
-    uint64_t* pv_done = s_full + 3;
-    uint64_t* dp_full = s_full + 4;
-    uint64_t* ds_full = s_full + 5;
-    uint64_t* acc_done = s_full + 6;
-    uint64_t* va_ready = s_full + 7;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 8);
-
-    const AttnProblem& f = p.f;
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int h = blockIdx.y, k0 = blockIdx.x * BKV;
-    const int nq_all = (f.Nq + BQ - 1) / BQ;
-    const int i0 = static_cast<int>((int64_t)blockIdx.z * nq_all / gridDim.z);
-    const int nq = static_cast<int>((int64_t)(blockIdx.z + 1) * nq_all / gridDim.z) - i0;  // this split's tiles
-    const int col = h * HD;
-
-    if (threadIdx.x == 0) {
-        mbar_init(k_full, 1);
-        for (int i = 0; i < NST; ++i) {
-            mbar_init(&qd_full[i], 1);
-            mbar_init(&qd_empty[i], 1);
-        }
-        mbar_init(s_full, 1);
-        mbar_init(s_empty, 4 * CW);
-        mbar_init(p_full, 4 * CW);
-        mbar_init(pv_done, 1);
-        mbar_init(dp_full, 1);
-        mbar_init(ds_full, 4 * CW);
-        mbar_init(acc_done, 1);
-        mbar_init(va_ready, 4);
-        fence_barrier_init();
-    }
-    if (warp == 2) tmem_alloc<512>(tmem_slot);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp == 0) {
-        if (elect_one()) {
-            mbar_arrive_expect_tx(k_full, T::ROW_TILE + (VT ? 4096 : 0));
-            load_row_tile<HD>(sK, &tm.a128, &tm.a32, k_full, col, k0);
-            if (VT) tma_load_2d(sVt, &tm.b32, k_full, col + VA, k0);
-            for (int i = 0; i < nq; ++i) {
-                const int st = i % NST;
-                if (i >= NST) mbar_wait(&qd_empty[st], ((i / NST) - 1) & 1);
-                if ((g_attn_dbg & 2) && i >= NST) {  // timing experiment: reuse the resident tiles, no TMA
-                    mbar_arrive(&qd_full[st]);
-                    continue;
-                }
-                mbar_arrive_expect_tx(&qd_full[st], 2 * T::T_TILE + 2 * BQ * 4);
-                const int qt = (i0 + i) * BQ;
-                tma_load_2d(sQt + st * T::T_TILE, &tm.ta, &qd_full[st], qt, col);
-                tma_load_2d(sdOt + st * T::T_TILE, &tm.tb, &qd_full[st], qt, col);
-                bulk_load(sLse + st * BQ, f.lse + (int64_t)h * lse_stride(f) + qt, BQ * 4, &qd_full[st]);
-                bulk_load(sD + st * BQ, p.Dvec + (int64_t)h * lse_stride(f) + qt, BQ * 4, &qd_full[st]);
-            }
-        }
-    } else if (warp == 1) {
-        const uint32_t aK = smem_u32(sK);
-        auto issue_s = [&](int i) {  // S^T(i) = K Q^T(i)
-            if (elect_one()) {
-                mma_rows_x_t<HD>(tmem + S_COL, aK, smem_u32(sQt + (i % NST) * T::T_TILE));
-                umma_commit(s_full);
-            }
-            __syncwarp();
-        };
-        auto issue_dp = [&](int i) {  // dP^T(i) = V dO^T(i): VA/16 TS k-steps + the SS tail
-            if (elect_one()) {
-                constexpr uint32_t id = idesc_bf16_f32(128, 64, false, true);
-                const uint32_t bt = smem_u32(sdOt + (i % NST) * T::T_TILE);
-#pragma unroll
-                for (int kk = 0; kk < VA / 16; ++kk)
-                    umma_f16_ts(tmem + DP_COL, tmem + VA_COL + kk * 8, smem_desc(bt + kk * 2048, 16, 1024, kSwizzle128),
-                                id, kk > 0 ? 1u : 0u);
-                if (VT)
-                    umma_f16_ss(tmem + DP_COL, smem_desc(smem_u32(sVt), 16, 256, kSwizzle32),
-                                smem_desc(bt + (VA / 16) * 2048, 16, 1024, kSwizzle128), id, 1u);
-                umma_commit(dp_full);
-            }
-            __syncwarp();
-        };
-        mbar_wait(va_ready, 0);
-        mbar_wait(k_full, 0);
-        if (nq > 0) {
-            mbar_wait(&qd_full[0], 0);
-            tc_fence_after();
-            issue_s(0);
-            issue_dp(0);
-        }
-        // per step i:  S^T(i+1) [S^T(i) loaded] -> dV(i) [P^T(i)] -> dK(i) [dS^T(i)] -> dP^T(i+1) [after dK(i)]
-        for (int i = 0; i < nq; ++i) {
-            const int st = i % NST;
-            if (lane == 0) ATR8(0, i);
-            if (i + 1 < nq) {
-                mbar_wait(s_empty, i & 1);
-                mbar_wait(&qd_full[(i + 1) % NST], ((i + 1) / NST) & 1);
-                tc_fence_after();
-                issue_s(i + 1);
-            }
-            if (lane == 0) ATR8(1, i);
-            mbar_wait(p_full, i & 1);
-            tc_fence_after();
-            if (lane == 0) ATR8(2, i);
-            if (elect_one()) {
-                mma_tmem_x_t<HD>(tmem + DV_COL, tmem + P_COL, smem_u32(sdOt + st * T::T_TILE), i > 0);
-                umma_commit(pv_done);
-            }
-            __syncwarp();
-            if (lane == 0) ATR8(3, i);
-            mbar_wait(ds_full, i & 1);
-            tc_fence_after();
-            if (lane == 0) ATR8(4, i);
-            if (elect_one()) {
-                mma_tmem_split_x_t<HD, BQ / CW>(tmem + DK_COL, tmem + DP_COL, smem_u32(sQt + st * T::T_TILE), i > 0);
-                umma_commit(&qd_empty[st]);
-                if (i == nq - 1) umma_commit(acc_done);
-            }
-            __syncwarp();
-            if (lane == 0) ATR8(5, i);
-            if (i + 1 < nq) issue_dp(i + 1);  // overwrites dS^T(i): behind dK(i) in the tensor pipe
-            if (lane == 0) ATR8(6, i);
-        }
-    } else if (warp >= 4) {
-        // CW warps per TMEM lane group: warp hf handles query columns [HQ hf, HQ hf + HQ) of each tile
-        const int g = warp & 3, hf = (warp - 4) >> 2, row = g * 32 + lane;
-        const uint32_t lane_base = static_cast<uint32_t>(g * 32) << 16;
-        const int kv = k0 + row;
-        const bool kvv = kv < f.Nk;
-        if (hf == 0) {
-            row_to_tmem<VA>(tmem + lane_base + VA_COL,
-                            static_cast<const __nv_bfloat16*>(f.v) + (int64_t)(kvv ? kv : 0) * f.v_ld + col, kvv);
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(va_ready);
-        }
-        constexpr int HQ = BQ / CW;
-        for (int i = 0; i < nq; ++i) {
-            const int st = i % NST;
-            mbar_wait(&qd_full[st], (i / NST) & 1);  // lse / D rows of this tile have landed
-            mbar_wait(s_full, i & 1);
-            tc_fence_after();
-            if (warp == 4 && lane == 0) ATR8(7, i);
-            float s[HQ], dp[HQ];
-            if (CW == 2 && (g_attn_dbg & 1)) {  // timing experiment: barriers only, no TMEM traffic or math
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(s_empty);
-                if (i >= 1) mbar_wait(pv_done, (i - 1) & 1);
-                if (lane == 0) mbar_arrive(p_full);
-                mbar_wait(dp_full, i & 1);
-                tc_fence_after();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(ds_full);
-                continue;
-            }
-            tmem_ldn<HQ>(tmem + lane_base + S_COL + hf * HQ, s);
-            tmem_wait_ld();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(s_empty);  // the MMA warp may issue S^T(i+1) over it
-            const float* lse2 = sLse + st * BQ + hf * HQ;
-            const float* Dq = sD + st * BQ + hf * HQ;
-            const int qb = (i0 + i) * BQ + hf * HQ;
-            const bool full = qb + HQ <= f.Nq;
-            uint32_t pk[HQ / 2];
-#pragma unroll
-            for (int c = 0; c < HQ; c += 2) {
-                const bool v0 = full || qb + c < f.Nq, v1 = full || qb + c + 1 < f.Nq;
-                s[c] = v0 ? ex2f((s[c] - lse2[c]) * kLog2e) : 0.0f;  // lse rows are natural-log
-                s[c + 1] = v1 ? ex2f((s[c + 1] - lse2[c + 1]) * kLog2e) : 0.0f;
-                pk[c / 2] = pack_bf16(s[c], s[c + 1]);
-            }
-            if (i >= 1) {
-                mbar_wait(pv_done, (i - 1) & 1);  // dV(i-1) has read P^T(i-1)
-                tc_fence_after();
-            }
-            tmem_stn<HQ / 2>(tmem + lane_base + P_COL + hf * (HQ / 2), pk);
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(p_full);
-            mbar_wait(dp_full, i & 1);
-            tc_fence_after();
-            tmem_ldn<HQ>(tmem + lane_base + DP_COL + hf * HQ, dp);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < HQ; c += 2)
-                pk[c / 2] = pack_bf16(s[c] * (dp[c] - Dq[c]), s[c + 1] * (dp[c + 1] - Dq[c + 1]));  // autodiff.cpp:820
-            tmem_stn<HQ / 2>(tmem + lane_base + DP_COL + hf * HQ, pk);
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(ds_full);
-        }
-        if (nq > 0) mbar_wait(acc_done, 0);
-        tc_fence_after();
-        const bool valid = kvv && nq > 0;
-        if (part) {  // fp32 partial rows of this query split: [dV | dK]
-            if (hf < 2) {
-                const int64_t W = (int64_t)f.heads * HD;
-                float* prow = part + ((int64_t)blockIdx.z * f.Nk + (kvv ? kv : 0)) * 2 * W + (hf ? W : 0) + col;
-                store_acc_row_f32<HD>(tmem + lane_base + (hf ? DK_COL : DV_COL), prow, kvv);
-            }
-        } else {  // warps [0, CW/2) store dV, the others dK, each a share of the 16-column chunks
-            constexpr int NC = HD / 16, HALF = CW / 2;
-            const bool is_v = hf < HALF;
-            const int part_i = is_v ? hf : hf - HALF;
-            __nv_bfloat16* out = is_v ? static_cast<__nv_bfloat16*>(p.dv) + (int64_t)kv * p.dv_ld + col
-                                      : static_cast<__nv_bfloat16*>(p.dk) + (int64_t)kv * p.dk_ld + col;
-            store_acc_row<HD>(tmem + lane_base + (is_v ? DV_COL : DK_COL), out, valid, part_i * NC / HALF,
-                              (part_i + 1) * NC / HALF);
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    if (warp == 2) tmem_dealloc<512>(tmem);
-}
-
 // =====================================================================================  dK / dV (v11)
-// 128-query steps with every product an N >= 128 MMA (34 instructions per 128 queries; v8: 52).  TMEM:
+// 128-query steps with every product an N >= 128 MMA (34 instructions per 128 queries, against 52 for the
+// 64-query-step pass it replaced).  TMEM:
 //   SD [0,128)    S^T(i) -> (loaded into registers) -> dP^T(i) -> (loaded) -> S^T(i+1)
 //   PT [128,192)  P^T(i) (bf16 pairs) -> (read by dV(i)) -> dS^T(i) -> (read by dK(i)) -> P^T(i+1)
 //   dV [192, 192+HDP)   dK [.., +HDP)
@@ -1024,22 +768,14 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
         make_tmap_sw(&m.a32, f.k, W, f.Nk, f.k_ld, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
         make_tmap_sw(&m.ta, qt, f.Nq, W, qt_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
         make_tmap_sw(&m.tb, dot, f.Nq, W, dot_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
-        const int smem = T::ROW_TILE + 10 * T::T_TILE + 10 * 64 * 4 + 256 + 1024 + (HD > 128 ? 4096 : 0);
-        const int smem11 = 2 * T::ROW_TILE + 4 * 2 * T::T_TILE + 4 * 128 * 4 + 256 + 1024;
-        static const bool use_v8 = std::getenv("MGV_DKV_V8") != nullptr;  // A/B against the previous pass
-        if (use_v8)
-            ensure_smem(attn_bwd_dkv_v8_kernel<HD, 2>, smem);
-        else
-            ensure_smem(attn_bwd_dkv_v11_kernel<HD>, smem11);
+        const int smem = 2 * T::ROW_TILE + 4 * 2 * T::T_TILE + 4 * 128 * 4 + 256 + 1024;
+        ensure_smem(attn_bwd_dkv_v11_kernel<HD>, smem);
         // few key tiles (cross-attention): split the query range so the grid still covers the SMs
-        const int kv_ctas = (f.Nk + 127) / 128 * f.heads, nq_all = (f.Nq + 63) / 64 / (use_v8 ? 1 : 2);
+        const int kv_ctas = (f.Nk + 127) / 128 * f.heads, nq_all = (f.Nq + 127) / 128;
         const int splits = std::max(1, std::min({num_sms() / std::max(kv_ctas, 1), nq_all / 8, 16}));
         float* part = nullptr;
         if (splits > 1) MGV_CUDA(cudaMallocAsync(&part, sizeof(float) * splits * f.Nk * 2 * W, s));
-        if (use_v8)
-            attn_bwd_dkv_v8_kernel<HD, 2><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem, s>>>(m, p, part);
-        else
-            attn_bwd_dkv_v11_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem11, s>>>(m, p, part);
+        attn_bwd_dkv_v11_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem, s>>>(m, p, part);
         ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
         if (splits > 1) {

@@ -213,6 +213,23 @@ mgv_status mgv_make_flow_sample(uint64_t seed, int64_t N, int64_t D, double mask
     return MGV_OK;
 }
 
+// per-rank memory of a training (or forward) step: {parameters, gradients, AdamW moments, workspace, exchange}
+mgv_status mgv_plan_rank_bytes(const mgv_dit_cfg* cfg, int precision, int tp, int64_t N, int64_t L, int64_t n_u,
+                               int train, int64_t out[5]) {
+    std::string err;
+    return mgv::guard_into(err, [&] {
+        if (!cfg || !out || N < 1 || L < 1 || n_u < 1) throw mgv::InputError("bad argument");
+        mgv::plan_rank_bytes(to_cfg(cfg), precision == MGV_PREC_BF16, tp, N, L, static_cast<int>(n_u), train != 0,
+                             out);
+    });
+}
+mgv_status mgv_ctx_memory(mgv_ctx* ctx, int64_t out[5]) {
+    return guard(ctx, [&] {
+        if (!out) throw mgv::InputError("null argument");
+        ctx->model->memory_bytes(out);
+    });
+}
+
 mgv_status mgv_params_upload_ckpt(mgv_ctx* ctx, const mgv_dit_cfg* cfg, const mgv_ckpt* ck) {
     return guard(ctx, [&] {
         if (!cfg || !ck) throw mgv::InputError("null argument");
@@ -245,7 +262,7 @@ mgv_status mgv_params_save(mgv_ctx* ctx, const char* path, int dtype, int64_t n_
         std::vector<std::vector<double>> host(ps.size());
         std::vector<mgv::CkptTensorIn> ts(ps.size());
         for (size_t k = 0; k < ps.size(); ++k) {
-            host[k].resize(static_cast<size_t>(ps[k]->numel));
+            host[k].resize(static_cast<size_t>(ps[k]->numel_full));
             ctx->model->download_param(static_cast<int64_t>(k), host[k].data());  // fp32 master, widened exactly
             ts[k].name = ps[k]->name;
             ts[k].dtype = dtype == MGV_CKPT_F32 ? mgv::kF32 : mgv::kF64;
@@ -263,7 +280,7 @@ mgv_status mgv_params_save(mgv_ctx* ctx, const char* path, int dtype, int64_t n_
 
 int64_t mgv_param_count(mgv_ctx* ctx) { return ctx ? static_cast<int64_t>(ctx->model->sorted_params().size()) : 0; }
 const char* mgv_param_name(mgv_ctx* ctx, int64_t i) { return ctx->model->sorted_params()[i]->name.c_str(); }
-int64_t mgv_param_numel(mgv_ctx* ctx, int64_t i) { return ctx->model->sorted_params()[i]->numel; }
+int64_t mgv_param_numel(mgv_ctx* ctx, int64_t i) { return ctx->model->sorted_params()[i]->numel_full; }
 
 mgv_status mgv_predict_velocity(mgv_ctx* ctx, const double* rows, int64_t N, const int32_t* coords,
                                 const int64_t dims[3], const double* text, int64_t L, const double* timesteps,

@@ -118,6 +118,10 @@ void bias_to(const float* part, const float* bias, T* out, int N, int H, cudaStr
 // (C chunks of R rows, each split into P shards); inverse = 1 maps back
 void permute_shard_rows(const float* src, float* dst, int C, int R, int P, int64_t cols, int inverse, cudaStream_t s);
 void permute_shard_rows(const double* src, double* dst, int C, int R, int P, int64_t cols, int inverse, cudaStream_t s);
+// column-parallel weights: (rows x cols) <-> P compact rank-major (rows x cols/P) blocks
+void permute_shard_cols(const float* src, float* dst, int64_t rows, int64_t cols, int P, int inverse, cudaStream_t s);
+void permute_shard_cols(const double* src, double* dst, int64_t rows, int64_t cols, int P, int inverse,
+                        cudaStream_t s);
 // part[c][j] = sum over chunk rows of Y[i, j]   (bias gradients)
 template <class T>
 void colsum(const T* Y, int64_t ld, int N, int C, float* part, cudaStream_t s);

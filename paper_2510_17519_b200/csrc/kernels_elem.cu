@@ -1094,6 +1094,31 @@ __global__ void permute_shard_rows_kernel(const E* src, E* dst, int C, int R, in
             dst[rank_major * cols + col] = src[row * cols + col];
     }
 }
+// column-parallel shard layout: (rows x cols) row-major <-> P rank-major blocks, block v = columns
+// [v cols/P, (v+1) cols/P) stored compact (rows x cols/P)
+template <class E>
+__global__ void permute_shard_cols_kernel(const E* src, E* dst, int64_t rows, int64_t cols, int P, int inverse) {
+    const int64_t cs = cols / P, n = rows * cols;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / cols, c = e - i * cols, v = c / cs, j = c - v * cs;
+        const int64_t rm = (v * rows + i) * cs + j;
+        if (inverse)
+            dst[e] = src[rm];
+        else
+            dst[rm] = src[e];
+    }
+}
+void permute_shard_cols(const float* src, float* dst, int64_t rows, int64_t cols, int P, int inverse, cudaStream_t s) {
+    permute_shard_cols_kernel<float><<<grid_for(rows * cols), 256, 0, s>>>(src, dst, rows, cols, P, inverse);
+    ::mgv::note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
+void permute_shard_cols(const double* src, double* dst, int64_t rows, int64_t cols, int P, int inverse,
+                        cudaStream_t s) {
+    permute_shard_cols_kernel<double><<<grid_for(rows * cols), 256, 0, s>>>(src, dst, rows, cols, P, inverse);
+    ::mgv::note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
 void permute_shard_rows(const float* src, float* dst, int C, int R, int P, int64_t cols, int inverse, cudaStream_t s) {
     permute_shard_rows_kernel<float><<<grid_for((int64_t)C * R * cols), 256, 0, s>>>(src, dst, C, R, P, cols, inverse);
     ::mgv::note_launch();

@@ -84,7 +84,7 @@ struct Model::WS {
     int* cnt;
     int q_splits_x = 1;
     // tensor parallel: fp32 partial sums of the row-parallel GEMMs (the all-reduce buffer)
-    int tp = 1;
+    int tp = 1, tp_slots = 1;  // slots: TP ranks whose per-rank activations live here (emulated ranks: all)
     float* tpp = nullptr;
 };
 
@@ -111,6 +111,7 @@ struct Sizer {  // measures then lays out the arena
 template <class S>
 void layout_ws(Model::WS& w, S& a, const Cfg& c, bool grads) {
     const int64_t N = w.N, L = w.L, H = c.H(), D = c.D(), nh = c.heads, hd = c.hd();
+    const int64_t Hr = H / w.tp, R = w.tp > 1 ? w.tp_slots : 1;
     const int e = w.esz;
     const int nu = w.n_u;
     w.rows = a.takeT(N * D, e);
@@ -148,19 +149,21 @@ void layout_ws(Model::WS& w, S& a, const Cfg& c, bool grads) {
         b.ik = a.template take<float>(N * nh);
         b.lse = a.template take<float>(((N + 127) / 128 * 128) * nh);
         b.lse_x = a.template take<float>(((N + 127) / 128 * 128) * nh);
+        // TP: the head / column-parallel activations are per rank (width H/P per slot, compact), the rest is
+        // replicated; R slots are held here (a real rank: 1, emulated ranks: P)
         b.a = a.takeT(N * H, e);
-        b.qkv = a.takeT(N * 3 * H, e);
-        b.qk = a.takeT(N * 2 * H, e);
-        b.O = a.takeT(N * H, e);
+        b.qkv = a.takeT(R * N * 3 * Hr, e);
+        b.qk = a.takeT(R * N * 2 * Hr, e);
+        b.O = a.takeT(R * N * Hr, e);
         b.ao = a.takeT(N * H, e);
         b.cn = a.takeT(N * H, e);
-        b.cqs = a.takeT(N * H, e);
-        b.kv = a.takeT(L * 2 * H, e);
-        b.Ox = a.takeT(N * H, e);
+        b.cqs = a.takeT(R * N * Hr, e);
+        b.kv = a.takeT(R * L * 2 * Hr, e);
+        b.Ox = a.takeT(R * N * Hr, e);
         b.co = a.takeT(N * H, e);
         b.f = a.takeT(N * H, e);
-        b.z = a.takeT(N * 4 * H, e);
-        b.h = a.takeT(N * 4 * H, e);
+        b.z = a.takeT(R * N * 4 * Hr, e);
+        b.h = a.takeT(R * N * 4 * Hr, e);
         b.ff = a.takeT(N * H, e);
     }
     w.rf = a.template take<float>(N);
@@ -175,11 +178,11 @@ void layout_ws(Model::WS& w, S& a, const Cfg& c, bool grads) {
     if (grads) {
         const int chunks = row_chunks(N);
         w.dX = a.template take<float>(N * H);
-        w.sA = a.takeT(N * 4 * H, e);
-        w.sB = a.takeT(N * 3 * H, e);
+        w.sA = a.takeT(R * N * 4 * Hr, e);
+        w.sB = a.takeT(R * N * 3 * Hr, e);
         w.s1 = a.takeT(N * H, e);
         w.s2 = a.takeT(N * H, e);
-        w.dkv = a.takeT(L * 2 * H, e);
+        w.dkv = a.takeT(R * L * 2 * Hr, e);
         w.Dvec = a.template take<float>(((N + 127) / 128 * 128) * nh);
         w.part1 = a.template take<float>((int64_t)chunks * std::max<int64_t>(4 * H, 2 * H));
         w.part2 = a.template take<float>((int64_t)chunks * std::max<int64_t>(4 * H, 2 * H));
@@ -525,27 +528,25 @@ float* Model::tp_exchange(float* part, int64_t N, cudaStream_t s) {
     return tpx_result(tpx_base_[tp_virtual_ ? 0 : tp_rank_], P, rpr, H);
 }
 
-// Sharded parameters: rank r computes only its rows / columns of these gradients, the rest
-// of its replicated gradient buffer stays zero, so a sum over TP ranks assembles the full gradient.
-static bool is_tp_sharded(const std::string& n) {
-    static const char* sh[] = {"attn.qkv.w", "attn.qkv.b", "attn.temp",  "attn.out.w", "xattn.q.w", "xattn.q.b",
-                               "xattn.kv.w", "xattn.kv.b", "xattn.out.w", "ffn.in.w",  "ffn.in.b",  "ffn.out.w"};
-    if (n.rfind("dit.blk.", 0) != 0) return false;
-    for (const char* m : sh) {
+// Shard map (expansion.cpp:143-180 chunk layout): row-parallel parameters are stored rank-major
+// (rank r's rows of every chunk contiguous), column-parallel weights as P compact (rows x cols/P) blocks; a real
+// TP rank holds only its own block, emulated ranks hold all P.  The rest is replicated.  Every rank computes its
+// blocks' gradients alone, and the replicated gradients identically from the exchanged activations, so no
+// gradient all-reduce is needed under TP.
+static int tp_shard_kind(const std::string& n) {
+    if (n.rfind("dit.blk.", 0) != 0) return 0;
+    auto ends = [&](const char* m) {
         const size_t l = std::strlen(m);
-        if (n.size() >= l && n.compare(n.size() - l, l, m) == 0 && n[n.size() - l - 1] == '.') return true;
-    }
-    return false;
+        return n.size() >= l && n.compare(n.size() - l, l, m) == 0;
+    };
+    if (ends(".attn.out.w") || ends(".xattn.out.w") || ends(".ffn.out.w")) return 2;
+    static const char* rows[] = {".attn.qkv.w", ".attn.qkv.b", ".attn.temp", ".xattn.q.w", ".xattn.q.b",
+                                 ".xattn.kv.w", ".xattn.kv.b", ".ffn.in.w", ".ffn.in.b"};
+    for (const char* m : rows)
+        if (ends(m)) return 1;
+    return 0;
 }
-void Model::tp_allreduce_grads(cudaStream_t s) {
-    if (tp_ == 1 || tp_virtual_) return;
-    prof_.begin("tp_allreduce", s);
-    MGV_NCCL(ncclGroupStart());
-    for (DevParam* p : sorted_)
-        if (is_tp_sharded(p->name)) MGV_NCCL(ncclAllReduce(p->grad, p->grad, p->numel, ncclFloat, ncclSum, tp_comm_, s));
-    MGV_NCCL(ncclGroupEnd());
-    prof_.end(s);
-}
+void Model::tp_allreduce_grads(cudaStream_t) {}  // sharded storage: nothing to reduce (see tp_shard_kind)
 
 // Chunked row layouts re-ordered rank-major under TP, so each rank's rows of every chunk are
 // contiguous (qkv: chunks q|k|v, expansion.cpp:143-180 chunk layout; xattn.kv: k|v).
@@ -658,19 +659,17 @@ void Model::download_param(int64_t i, double* out) {
     if (i < 0 || i >= static_cast<int64_t>(sorted_.size())) throw InputError("parameter index out of range");
     MGV_CUDA(cudaSetDevice(device_));
     const DevParam& q = *sorted_[i];
-    float* tmp = nullptr;
+    float *a = nullptr, *b = nullptr;
     double* d = nullptr;
-    MGV_CUDA(cudaMallocAsync(&tmp, sizeof(float) * q.numel, stream_));
-    MGV_CUDA(cudaMallocAsync(&d, sizeof(double) * q.numel, stream_));
-    const float* src = q.f32;
-    if (const int C = tp_ > 1 ? tp_row_chunks(q.name) : 0) {  // back to the reference row order
-        permute_shard_rows(q.f32, tmp, C, static_cast<int>(cfg_.hidden), tp_, q.numel / (C * cfg_.hidden), 1, stream_);
-        src = tmp;
-    }
-    f32_to_f64<<<grid_of(q.numel), 256, 0, stream_>>>(src, q.numel, d);
+    MGV_CUDA(cudaMallocAsync(&a, sizeof(float) * q.numel_full, stream_));
+    MGV_CUDA(cudaMallocAsync(&b, sizeof(float) * q.numel_full, stream_));
+    MGV_CUDA(cudaMallocAsync(&d, sizeof(double) * q.numel_full, stream_));
+    const float* src = full_view(q, q.f32, a, b);
+    f32_to_f64<<<grid_of(q.numel_full), 256, 0, stream_>>>(src, q.numel_full, d);
     note_launch();
-    MGV_CUDA(cudaMemcpyAsync(out, d, sizeof(double) * q.numel, cudaMemcpyDeviceToHost, stream_));
-    MGV_CUDA(cudaFreeAsync(tmp, stream_));
+    MGV_CUDA(cudaMemcpyAsync(out, d, sizeof(double) * q.numel_full, cudaMemcpyDeviceToHost, stream_));
+    MGV_CUDA(cudaFreeAsync(a, stream_));
+    MGV_CUDA(cudaFreeAsync(b, stream_));
     MGV_CUDA(cudaFreeAsync(d, stream_));
     MGV_CUDA(cudaStreamSynchronize(stream_));
 }
@@ -742,19 +741,31 @@ void Model::upload(const Cfg& cfg, int64_t n, const char* const* names, const vo
         sorted_.clear();
         if (grad_buf_) cudaFree(grad_buf_);
         grad_buf_ = nullptr;
-        int64_t total = 0;
         for (auto& kv : want) {
             DevParam p;
             p.name = kv.first;
             p.shape = kv.second;
-            p.numel = 1;
-            for (auto d : p.shape) p.numel *= d;
+            p.numel_full = 1;
+            for (auto d : p.shape) p.numel_full *= d;
+            p.shard = tp_ > 1 ? tp_shard_kind(p.name) : 0;
+            p.slot_numel = p.shard ? p.numel_full / tp_ : p.numel_full;
+            p.numel = p.shard && !tp_virtual_ ? p.slot_numel : p.numel_full;  // a real TP rank: its block only
             MGV_CUDA(cudaMalloc(&p.f32, sizeof(float) * p.numel));
             if (bf16_ && is_matrix(p.name)) MGV_CUDA(cudaMalloc(&p.bf, sizeof(__nv_bfloat16) * p.numel));
-            p.grad_off = total;
-            total += (p.numel + 63) / 64 * 64;
             params_[p.name] = p;
         }
+        // gradient buffer: sorted names; under TP the replicated parameters first, then the sharded blocks (the
+        // gradient norm sums the second range over the TP ranks)
+        int64_t total = 0;
+        for (int pass = 0; pass < 2; ++pass)
+            for (auto& kv : params_) {
+                if ((kv.second.shard != 0) != (pass == 1)) continue;
+                kv.second.grad_off = total;
+                total += (kv.second.numel + 63) / 64 * 64;
+            }
+        repl_numel_ = 0;
+        for (auto& kv : params_)
+            if (!kv.second.shard) repl_numel_ = std::max(repl_numel_, kv.second.grad_off + (kv.second.numel + 63) / 64 * 64);
         grad_numel_ = total;
         MGV_CUDA(cudaMalloc(&grad_buf_, sizeof(float) * total));
         for (auto& kv : params_) {
@@ -775,28 +786,33 @@ void Model::upload(const Cfg& cfg, int64_t n, const char* const* names, const vo
     cfg_ = cfg;
     double* staging = nullptr;
     int64_t stage_n = 0;
-    for (auto& kv : params_) stage_n = std::max(stage_n, kv.second.numel);
+    for (auto& kv : params_) stage_n = std::max(stage_n, kv.second.numel_full);
     // staging: [0, n) fp64 input | [n, 2n) permuted rows (TP) | [2n, 3n) raw fp32 input (widened exactly)
     MGV_CUDA(cudaMalloc(&staging, sizeof(double) * stage_n * 3));
     for (auto& kv : params_) {
         DevParam& p = kv.second;
         const int64_t gi = given[p.name];
-        if (numel[gi] != p.numel)
+        const int64_t nf = p.numel_full;
+        if (numel[gi] != nf)
             throw DimensionError("parameter " + p.name + " has " + std::to_string(numel[gi]) + " elements, expected " +
-                                 std::to_string(p.numel));
+                                 std::to_string(nf));
         if (is_f32 && is_f32[gi]) {
             float* raw = reinterpret_cast<float*>(staging + 2 * stage_n);
-            MGV_CUDA(cudaMemcpyAsync(raw, data[gi], sizeof(float) * p.numel, cudaMemcpyHostToDevice, stream_));
-            f32_to_f64<<<grid_of(p.numel), 256, 0, stream_>>>(raw, p.numel, staging);
+            MGV_CUDA(cudaMemcpyAsync(raw, data[gi], sizeof(float) * nf, cudaMemcpyHostToDevice, stream_));
+            f32_to_f64<<<grid_of(nf), 256, 0, stream_>>>(raw, nf, staging);
             ::mgv::note_launch();
         } else {
-            MGV_CUDA(cudaMemcpyAsync(staging, data[gi], sizeof(double) * p.numel, cudaMemcpyHostToDevice, stream_));
+            MGV_CUDA(cudaMemcpyAsync(staging, data[gi], sizeof(double) * nf, cudaMemcpyHostToDevice, stream_));
         }
-        const double* src = staging;
-        if (const int C = tp_ > 1 ? tp_row_chunks(p.name) : 0) {
-            permute_shard_rows(staging, staging + stage_n, C, static_cast<int>(H), tp_, p.numel / (C * H), 0, stream_);
+        const double* src = staging;  // to the rank-major shard layout
+        if (const int C = p.shard == 1 ? tp_row_chunks(p.name) : 0) {
+            permute_shard_rows(staging, staging + stage_n, C, static_cast<int>(H), tp_, nf / (C * H), 0, stream_);
+            src = staging + stage_n;
+        } else if (p.shard == 2) {
+            permute_shard_cols(staging, staging + stage_n, p.shape[0], p.shape[1], tp_, 0, stream_);
             src = staging + stage_n;
         }
+        if (p.shard && !tp_virtual_) src += tp_rank_ * p.slot_numel;  // this rank's block
         f64_to_f32_bf16<<<grid_of(p.numel), 256, 0, stream_>>>(src, p.numel, p.f32, p.bf); ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
     }
@@ -815,6 +831,39 @@ const void* Model::W(const std::string& name) const {
     return bf16_ ? static_cast<const void*>(p.bf) : static_cast<const void*>(p.f32);
 }
 float* Model::G(const std::string& name) const { return P(name).grad; }
+const float* Model::Ps(const std::string& name, int k) const {
+    const DevParam& p = P(name);
+    return p.f32 + (p.shard ? k * p.slot_numel : 0);
+}
+const void* Model::Ws(const std::string& name, int k) const {
+    const DevParam& p = P(name);
+    const int64_t o = p.shard ? k * p.slot_numel : 0;
+    return bf16_ ? static_cast<const void*>(p.bf + o) : static_cast<const void*>(p.f32 + o);
+}
+float* Model::Gs(const std::string& name, int k) const {
+    const DevParam& p = P(name);
+    return p.grad + (p.shard ? k * p.slot_numel : 0);
+}
+
+// A parameter (or its gradient, `local` = the grad slice) as the full reference tensor, fp32, on the device:
+// a real TP rank all-gathers the ranks' blocks (a collective over the TP group), then the shard layout is undone.
+const float* Model::full_view(const DevParam& q, const float* local, float* a, float* b) {
+    const float* src = local;
+    if (q.shard && !tp_virtual_) {
+        MGV_NCCL(ncclAllGather(local, a, q.slot_numel, ncclFloat, tp_comm_, stream_));
+        src = a;
+    }
+    if (const int C = q.shard == 1 ? tp_row_chunks(q.name) : 0) {
+        permute_shard_rows(src, b, C, static_cast<int>(cfg_.hidden), tp_, q.numel_full / (C * cfg_.hidden), 1,
+                           stream_);
+        return b;
+    }
+    if (q.shard == 2) {
+        permute_shard_cols(src, b, q.shape[0], q.shape[1], tp_, 1, stream_);
+        return b;
+    }
+    return src;
+}
 
 // ------------------------------------------------------------------ helpers
 namespace {
@@ -981,20 +1030,80 @@ void Model::block_bwd(int i, int64_t N) {
     gscale_bwd(w.dgb, w.g, P(blk(i, "gscale")).f32, nu, H, G(blk(i, "gscale")), w.dg, s);
 }
 
+// ------------------------------------------------------------------ memory accounting (per rank)
+// What one TP rank (or a single-device context, tp = 1) allocates for a training step over N tokens: the
+// parameters (fp32 masters + bf16 operand copies), the gradient buffer, the AdamW moments, the step workspace
+// (every block's saved activations) and the peer-exchange arena.  The same layout code the runtime uses, run in
+// measure mode, so a plan needs no device (the 56-block stack at P = 8).
+void plan_rank_bytes(const Cfg& c, bool bf16, int tp, int64_t N, int64_t L, int n_u, bool train, int64_t out[5]) {
+    validate_cfg(c);
+    if (tp < 1 || c.heads % tp != 0) throw ConfigError("tensor parallel size must divide heads");
+    const int64_t H = c.H(), D = c.D();
+    auto rnd = [](int64_t n) { return (n + 63) / 64 * 64; };
+    int64_t pf = 0, pb = 0, pg = 0;
+    auto add = [&](const std::string& name, int64_t numel, bool mat) {
+        const int64_t local = tp > 1 && tp_shard_kind(name) ? numel / tp : numel;
+        pf += 4 * local;
+        if (bf16 && mat) pb += 2 * local;
+        pg += 4 * rnd(local);
+    };
+    add("dit.patch.w", H * D, true), add("dit.patch.b", H, false), add("dit.gmlp.in.w", H * 32, false);
+    add("dit.gmlp.in.b", H, false), add("dit.gmlp.out.w", H * H, false), add("dit.gmlp.out.b", H, false);
+    add("dit.mod.w", 6 * H * H, false), add("dit.mod.b", 6 * H, false);
+    for (int i = 0; i < c.depth; ++i) {
+        const std::string b = "dit.blk." + std::to_string(i) + ".";
+        add(b + "gscale", H, false), add(b + "attn.qkv.w", 3 * H * H, true), add(b + "attn.qkv.b", 3 * H, false);
+        add(b + "attn.temp", c.heads, false), add(b + "attn.out.w", H * H, true), add(b + "attn.out.b", H, false);
+        add(b + "xattn.prenorm.g", H, false), add(b + "xattn.q.w", H * H, true), add(b + "xattn.q.b", H, false);
+        add(b + "xattn.kv.w", 2 * H * c.text_dim, true), add(b + "xattn.kv.b", 2 * H, false);
+        add(b + "xattn.out.w", H * H, true), add(b + "xattn.out.b", H, false), add(b + "xattn.postnorm.g", H, false);
+        add(b + "ffn.in.w", 4 * H * H, true), add(b + "ffn.in.b", 4 * H, false), add(b + "ffn.out.w", 4 * H * H, true);
+        add(b + "ffn.out.b", H, false);
+    }
+    add("dit.final.g", H, false), add("dit.final.w", H * H, true), add("dit.final.b", H, false);
+    add("dit.out.w", D * H, true), add("dit.out.b", D, false);
+    Model::WS w;
+    w.N = N;
+    w.L = L;
+    w.n_u = n_u;
+    w.esz = bf16 ? 2 : 4;
+    w.grads = train;
+    w.tp = tp;
+    w.tp_slots = 1;
+    Sizer sz{true, 0, nullptr};
+    layout_ws(w, sz, c, train);
+    out[0] = pf + pb;                              // parameters
+    out[1] = train ? pg : 0;                       // gradients
+    out[2] = train ? 2 * pg : 0;                   // AdamW m, v
+    out[3] = static_cast<int64_t>(sz.bytes);       // workspace (saved activations + scratch)
+    out[4] = tp > 1 ? kTpFlagBytes + 2 * tp * ((N + tp - 1) / tp) * H * 4 : 0;  // peer-exchange arena
+}
+
+void Model::memory_bytes(int64_t out[5]) const {
+    int64_t pf = 0;
+    for (const auto& kv : params_) pf += 4 * kv.second.numel + (kv.second.bf ? 2 * kv.second.numel : 0);
+    out[0] = pf;
+    out[1] = 4 * grad_numel_;
+    out[2] = (opt_m_ ? 4 * grad_numel_ : 0) + (opt_v_ ? 4 * grad_numel_ : 0);
+    out[3] = static_cast<int64_t>(arena_.cap());
+    out[4] = tpx_own_ ? tpx_bytes_ * (tp_virtual_ ? tp_ : 1) : 0;
+}
+
 // ------------------------------------------------------------------ tensor-parallel block
 // Megatron head/column split: rank r owns heads [r nh/P, (r+1) nh/P) of the self- and cross-attention
 // (its rows of the rank-major qkv / kv weights and of xattn.q, its entries of attn.temp) and rows
-// [r 4H/P, (r+1) 4H/P) of ffn.in; attn.out / xattn.out / ffn.out are row-parallel (column slices), so
-// each residual branch ends in one all-reduce of an N x H fp32 partial.  Norms, gains, modulation and
-// the heads are replicated.  A rank's slices are views (pointer offset + leading dimension) into the
-// activation and weight buffers, so the emulated ranks of one process share the full-size buffers.
+// [r 4H/P, (r+1) 4H/P) of ffn.in; attn.out / xattn.out / ffn.out are row-parallel (column blocks), so
+// each residual branch ends in one exchange of an N x H fp32 partial.  Norms, gains, modulation and the
+// heads are replicated.  Storage is partitioned: slot k (rank ranks[k]) has its own weight blocks
+// (Ws / Ps / Gs) and its own compact activations of width H/P (qkv 3H/P, qk 2H/P, O / cqs / Ox H/P,
+// kv 2H/P, z / h 4H/P); a real rank holds one slot, emulated ranks all P.
 template <class T>
 void Model::block_fwd_tp(int i, int64_t N) {
     WS& w = *ws_;
     const bool bf = bf16_;
     cudaStream_t s = stream_;
     const int64_t H = cfg_.H(), nh = cfg_.heads, hd = cfg_.hd(), L = w.L, td = cfg_.text_dim;
-    const int64_t Hr = H / tp_, nhr = nh / tp_, Fr = 4 * H / tp_, lld = (N + 127) / 128 * 128;  // the attention backward streams 128-row lse / D tiles
+    const int64_t Hr = H / tp_, nhr = nh / tp_, Fr = 4 * H / tp_, lld = (N + 127) / 128 * 128;  // 128-row lse tiles
     Blk& b = w.blk[w.grads ? i : 0];
     const float* Xin = w.X[w.grads ? i : (i % 2)];
     float* Xout = w.X[w.grads ? i + 1 : ((i + 1) % 2)];
@@ -1017,19 +1126,21 @@ void Model::block_fwd_tp(int i, int64_t N) {
     rms_mod<T>(Xin, n, H, tab, tld, 0, H, w.mod_id, tp<T>(b.a), b.r0, s);
     for (size_t k = 0; k < ranks.size(); ++k) {
         const int64_t r = ranks[k];
-        void* qkv_r = off<T>(b.qkv, r * 3 * Hr);
-        void* qk_r = off<T>(b.qk, r * 2 * Hr);
-        gemm(bf, KM(b.a, H), KM(off<T>(W(blk(i, "attn.qkv.w")), r * 3 * Hr * H), H), n, int(3 * Hr), H,
-             EpiStore<T>{tp<T>(qkv_r), 3 * H, P(blk(i, "attn.qkv.b")).f32 + r * 3 * Hr, 1.0f, n, int(3 * Hr)}, s);
-        qk_norm_rope<T>(tp<T>(qkv_r), QKLayout{3 * H, Hr, 2 * H, Hr, nh}, n, int(Hr), int(nhr),
-                        P(blk(i, "attn.temp")).f32 + r * nhr, w.cs, tp<T>(qk_r), b.iq + r * nhr, b.ik + r * nhr, s);
-        AttnProblem ap{qk_r, 2 * H, off<T>(qk_r, Hr), 2 * H, off<T>(qkv_r, 2 * Hr), 3 * H, off<T>(b.O, r * Hr), H,
+        const int kk = static_cast<int>(k);
+        void* qkv_r = off<T>(b.qkv, k * N * 3 * Hr);
+        void* qk_r = off<T>(b.qk, k * N * 2 * Hr);
+        void* O_r = off<T>(b.O, k * N * Hr);
+        gemm(bf, KM(b.a, H), KM(Ws(blk(i, "attn.qkv.w"), kk), H), n, int(3 * Hr), H,
+             EpiStore<T>{tp<T>(qkv_r), 3 * Hr, Ps(blk(i, "attn.qkv.b"), kk), 1.0f, n, int(3 * Hr)}, s);
+        qk_norm_rope<T>(tp<T>(qkv_r), QKLayout{3 * Hr, Hr, 2 * Hr, Hr, nh}, n, int(Hr), int(nhr),
+                        Ps(blk(i, "attn.temp"), kk), w.cs, tp<T>(qk_r), b.iq + r * nhr, b.ik + r * nhr, s);
+        AttnProblem ap{qk_r, 2 * Hr, off<T>(qk_r, Hr), 2 * Hr, off<T>(qkv_r, 2 * Hr), 3 * Hr, O_r, Hr,
                        b.lse + r * nhr * lld, n, n, int(nhr), int(hd)};
         ap.lse_ld = lld;
         prof_.begin("attn_fwd", s);
         attention_fwd<T>(bf, ap, s);
         prof_.end(s);
-        rowpar(k, r, KM(off<T>(b.O, r * Hr), H), KM(off<T>(W(blk(i, "attn.out.w")), r * Hr), H), int(Hr), 1.0f);
+        rowpar(k, r, KM(O_r, Hr), KM(Ws(blk(i, "attn.out.w"), kk), Hr), int(Hr), 1.0f);
     }
     sum = tp_exchange(part, N, s);
     bias_gate_resid<T>(sum, P(blk(i, "attn.out.b")).f32, tab, tld, int(2 * H), w.mod_id, Xin, b.X1, tp<T>(b.ao), n,
@@ -1039,18 +1150,21 @@ void Model::block_fwd_tp(int i, int64_t N) {
     const float xscale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd)));
     for (size_t k = 0; k < ranks.size(); ++k) {
         const int64_t r = ranks[k];
-        void* kv_r = off<T>(b.kv, r * 2 * Hr);
-        gemm(bf, KM(b.cn, H), KM(off<T>(W(blk(i, "xattn.q.w")), r * Hr * H), H), n, int(Hr), H,
-             EpiStore<T>{tp<T>(off<T>(b.cqs, r * Hr)), H, P(blk(i, "xattn.q.b")).f32 + r * Hr, xscale, n, int(Hr)}, s);
-        gemm(bf, KM(w.text, td), KM(off<T>(W(blk(i, "xattn.kv.w")), r * 2 * Hr * td), td), int(L), int(2 * Hr), td,
-             EpiStore<T>{tp<T>(kv_r), 2 * H, P(blk(i, "xattn.kv.b")).f32 + r * 2 * Hr, 1.0f, int(L), int(2 * Hr)}, s);
-        AttnProblem xp{off<T>(b.cqs, r * Hr), H, kv_r, 2 * H, off<T>(kv_r, Hr), 2 * H, off<T>(b.Ox, r * Hr), H,
-                       b.lse_x + r * nhr * lld, n, int(L), int(nhr), int(hd)};
+        const int kk = static_cast<int>(k);
+        void* kv_r = off<T>(b.kv, k * L * 2 * Hr);
+        void* cqs_r = off<T>(b.cqs, k * N * Hr);
+        void* Ox_r = off<T>(b.Ox, k * N * Hr);
+        gemm(bf, KM(b.cn, H), KM(Ws(blk(i, "xattn.q.w"), kk), H), n, int(Hr), H,
+             EpiStore<T>{tp<T>(cqs_r), Hr, Ps(blk(i, "xattn.q.b"), kk), xscale, n, int(Hr)}, s);
+        gemm(bf, KM(w.text, td), KM(Ws(blk(i, "xattn.kv.w"), kk), td), int(L), int(2 * Hr), td,
+             EpiStore<T>{tp<T>(kv_r), 2 * Hr, Ps(blk(i, "xattn.kv.b"), kk), 1.0f, int(L), int(2 * Hr)}, s);
+        AttnProblem xp{cqs_r, Hr, kv_r, 2 * Hr, off<T>(kv_r, Hr), 2 * Hr, Ox_r, Hr, b.lse_x + r * nhr * lld, n,
+                       int(L), int(nhr), int(hd)};
         xp.lse_ld = lld;
         prof_.begin("xattn_fwd", s);
         attention_fwd<T>(bf, xp, s);
         prof_.end(s);
-        rowpar(k, r, KM(off<T>(b.Ox, r * Hr), H), KM(off<T>(W(blk(i, "xattn.out.w")), r * Hr), H), int(Hr), 1.0f);
+        rowpar(k, r, KM(Ox_r, Hr), KM(Ws(blk(i, "xattn.out.w"), kk), Hr), int(Hr), 1.0f);
     }
     sum = tp_exchange(part, N, s);
     bias_to<T>(sum, P(blk(i, "xattn.out.b")).f32, tp<T>(b.co), n, int(H), s);
@@ -1059,11 +1173,12 @@ void Model::block_fwd_tp(int i, int64_t N) {
     rms_mod<T>(b.X2, n, H, tab, tld, 3 * H, 4 * H, w.mod_id, tp<T>(b.f), b.r2, s);
     for (size_t k = 0; k < ranks.size(); ++k) {
         const int64_t r = ranks[k];
-        gemm(bf, KM(b.f, H), KM(off<T>(W(blk(i, "ffn.in.w")), r * Fr * H), H), n, int(Fr), H,
-             EpiBiasSilu<T>{tp<T>(off<T>(b.z, r * Fr)), tp<T>(off<T>(b.h, r * Fr)), 4 * H,
-                            P(blk(i, "ffn.in.b")).f32 + r * Fr, n, int(Fr)},
-             s);
-        rowpar(k, r, KM(off<T>(b.h, r * Fr), 4 * H), KM(off<T>(W(blk(i, "ffn.out.w")), r * Fr), 4 * H), int(Fr), 1.0f);
+        const int kk = static_cast<int>(k);
+        void* z_r = off<T>(b.z, k * N * Fr);
+        void* h_r = off<T>(b.h, k * N * Fr);
+        gemm(bf, KM(b.f, H), KM(Ws(blk(i, "ffn.in.w"), kk), H), n, int(Fr), H,
+             EpiBiasSilu<T>{tp<T>(z_r), tp<T>(h_r), Fr, Ps(blk(i, "ffn.in.b"), kk), n, int(Fr)}, s);
+        rowpar(k, r, KM(h_r, Fr), KM(Ws(blk(i, "ffn.out.w"), kk), Fr), int(Fr), 1.0f);
     }
     sum = tp_exchange(part, N, s);
     bias_gate_resid<T>(sum, P(blk(i, "ffn.out.b")).f32, tab, tld, int(5 * H), w.mod_id, b.X2, Xout, tp<T>(b.ff), n,
@@ -1076,7 +1191,7 @@ void Model::block_bwd_tp(int i, int64_t N) {
     const bool bf = bf16_;
     cudaStream_t s = stream_;
     const int64_t H = cfg_.H(), nh = cfg_.heads, hd = cfg_.hd(), L = w.L, td = cfg_.text_dim;
-    const int64_t Hr = H / tp_, nhr = nh / tp_, Fr = 4 * H / tp_, lld = (N + 127) / 128 * 128;  // the attention backward streams 128-row lse / D tiles
+    const int64_t Hr = H / tp_, nhr = nh / tp_, Fr = 4 * H / tp_, lld = (N + 127) / 128 * 128;  // 128-row lse tiles
     const int n = static_cast<int>(N), nu = w.n_u, chunks = row_chunks(n);
     Blk& b = w.blk[i];
     const float* Xin = w.X[i];
@@ -1102,16 +1217,17 @@ void Model::block_bwd_tp(int i, int64_t N) {
     reduce_chunks(w.part2, chunks, H, G(blk(i, "ffn.out.b")), 1.0f, 1, s);
     for (size_t k = 0; k < ranks.size(); ++k) {
         const int64_t r = ranks[k];
-        void* dz_r = off<T>(w.sA, r * Fr);
-        gemm(bf, MN(w.s1, H), MN(off<T>(b.h, r * Fr), 4 * H), H, int(Fr), n,
-             EpiF32{G(blk(i, "ffn.out.w")) + r * Fr, 4 * H, nullptr, 1.0f, 1, int(H), int(Fr)}, s);
-        gemm(bf, KM(w.s1, H), MN(off<T>(W(blk(i, "ffn.out.w")), r * Fr), 4 * H), n, int(Fr), H,
-             EpiSiluBwd<T>{tp<T>(dz_r), tp<T>(off<T>(b.z, r * Fr)), 4 * H, n, int(Fr)}, s);
-        colsum<T>(tp<T>(dz_r), 4 * H, n, int(Fr), w.part1, s);
-        reduce_chunks(w.part1, chunks, int(Fr), G(blk(i, "ffn.in.b")) + r * Fr, 1.0f, 1, s);
-        gemm(bf, MN(dz_r, 4 * H), MN(b.f, H), int(Fr), H, n,
-             EpiF32{G(blk(i, "ffn.in.w")) + r * Fr * H, H, nullptr, 1.0f, 1, int(Fr), int(H)}, s);
-        rowpar(k, r, KM(dz_r, 4 * H), MN(off<T>(W(blk(i, "ffn.in.w")), r * Fr * H), H), int(Fr), 1.0f);  // df partial
+        const int kk = static_cast<int>(k);
+        void* dz_r = off<T>(w.sA, k * N * Fr);
+        gemm(bf, MN(w.s1, H), MN(off<T>(b.h, k * N * Fr), Fr), H, int(Fr), n,
+             EpiF32{Gs(blk(i, "ffn.out.w"), kk), Fr, nullptr, 1.0f, 1, int(H), int(Fr)}, s);
+        gemm(bf, KM(w.s1, H), MN(Ws(blk(i, "ffn.out.w"), kk), Fr), n, int(Fr), H,
+             EpiSiluBwd<T>{tp<T>(dz_r), tp<T>(off<T>(b.z, k * N * Fr)), Fr, n, int(Fr)}, s);
+        colsum<T>(tp<T>(dz_r), Fr, n, int(Fr), w.part1, s);
+        reduce_chunks(w.part1, chunks, int(Fr), Gs(blk(i, "ffn.in.b"), kk), 1.0f, 1, s);
+        gemm(bf, MN(dz_r, Fr), MN(b.f, H), int(Fr), H, n,
+             EpiF32{Gs(blk(i, "ffn.in.w"), kk), H, nullptr, 1.0f, 1, int(Fr), int(H)}, s);
+        rowpar(k, r, KM(dz_r, Fr), MN(Ws(blk(i, "ffn.in.w"), kk), H), int(Fr), 1.0f);  // df partial
     }
     sum = tp_exchange(part, N, s);
     convert_f32<T>(sum, N * H, tp<T>(w.s1), s);
@@ -1123,36 +1239,39 @@ void Model::block_bwd_tp(int i, int64_t N) {
     reduce_chunks(w.part1, chunks, H, G(blk(i, "xattn.postnorm.g")), 1.0f, 1, s);
     colsum<T>(tp<T>(w.s1), H, n, H, w.part1, s);
     reduce_chunks(w.part1, chunks, H, G(blk(i, "xattn.out.b")), 1.0f, 1, s);
-    for (size_t k = 0; k < ranks.size(); ++k) {  // all ranks read the full dco (s1) before dq overwrites it
-        const int64_t r = ranks[k];
-        gemm(bf, MN(w.s1, H), MN(off<T>(b.Ox, r * Hr), H), H, int(Hr), n,
-             EpiF32{G(blk(i, "xattn.out.w")) + r * Hr, H, nullptr, 1.0f, 1, int(H), int(Hr)}, s);
-        gemm(bf, KM(w.s1, H), MN(off<T>(W(blk(i, "xattn.out.w")), r * Hr), H), n, int(Hr), H,
-             EpiStore<T>{tp<T>(off<T>(w.s2, r * Hr)), H, nullptr, 1.0f, n, int(Hr)}, s);
+    for (size_t k = 0; k < ranks.size(); ++k) {  // all slots read the full dco (s1) before their dq overwrites it
+        const int kk = static_cast<int>(k);
+        gemm(bf, MN(w.s1, H), MN(off<T>(b.Ox, k * N * Hr), Hr), H, int(Hr), n,
+             EpiF32{Gs(blk(i, "xattn.out.w"), kk), Hr, nullptr, 1.0f, 1, int(H), int(Hr)}, s);
+        gemm(bf, KM(w.s1, H), MN(Ws(blk(i, "xattn.out.w"), kk), Hr), n, int(Hr), H,
+             EpiStore<T>{tp<T>(off<T>(w.s2, k * N * Hr)), Hr, nullptr, 1.0f, n, int(Hr)}, s);
     }
     const float xscale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd)));
     for (size_t k = 0; k < ranks.size(); ++k) {
         const int64_t r = ranks[k];
-        void* kv_r = off<T>(b.kv, r * 2 * Hr);
-        void* dkv_r = off<T>(w.dkv, r * 2 * Hr);
-        void* dq_r = off<T>(w.s1, r * Hr);
-        AttnBwdProblem xb{AttnProblem{off<T>(b.cqs, r * Hr), H, kv_r, 2 * H, off<T>(kv_r, Hr), 2 * H,
-                                      off<T>(b.Ox, r * Hr), H, b.lse_x + r * nhr * lld, n, int(L), int(nhr), int(hd)},
-                          off<T>(w.s2, r * Hr), H, w.Dvec + r * nhr * lld, dq_r, H, dkv_r, 2 * H, off<T>(dkv_r, Hr),
-                          2 * H, w.dkv_part + r * (int64_t)w.q_splits_x * nhr * L * 2 * hd, w.q_splits_x};
+        const int kk = static_cast<int>(k);
+        void* kv_r = off<T>(b.kv, k * L * 2 * Hr);
+        void* dkv_r = off<T>(w.dkv, k * L * 2 * Hr);
+        void* dq_r = off<T>(w.s1, k * N * Hr);
+        AttnBwdProblem xb{AttnProblem{off<T>(b.cqs, k * N * Hr), Hr, kv_r, 2 * Hr, off<T>(kv_r, Hr), 2 * Hr,
+                                      off<T>(b.Ox, k * N * Hr), Hr, b.lse_x + r * nhr * lld, n, int(L), int(nhr),
+                                      int(hd)},
+                          off<T>(w.s2, k * N * Hr), Hr, w.Dvec + r * nhr * lld, dq_r, Hr, dkv_r, 2 * Hr,
+                          off<T>(dkv_r, Hr), 2 * Hr, w.dkv_part + r * (int64_t)w.q_splits_x * nhr * L * 2 * hd,
+                          w.q_splits_x};
         xb.f.lse_ld = lld;
         prof_.begin("xattn_bwd", s);
         attention_bwd<T>(bf, xb, s);
         prof_.end(s);
-        gemm(bf, MN(dkv_r, 2 * H), MN(w.text, td), int(2 * Hr), td, int(L),
-             EpiF32{G(blk(i, "xattn.kv.w")) + r * 2 * Hr * td, td, nullptr, 1.0f, 1, int(2 * Hr), int(td)}, s);
-        colsum<T>(tp<T>(dkv_r), 2 * H, int(L), int(2 * Hr), w.part1, s);
-        reduce_chunks(w.part1, row_chunks(int(L)), int(2 * Hr), G(blk(i, "xattn.kv.b")) + r * 2 * Hr, 1.0f, 1, s);
-        colsum<T>(tp<T>(dq_r), H, n, int(Hr), w.part1, s);
-        reduce_chunks(w.part1, chunks, int(Hr), G(blk(i, "xattn.q.b")) + r * Hr, xscale, 1, s);
-        gemm(bf, MN(dq_r, H), MN(b.cn, H), int(Hr), H, n,
-             EpiF32{G(blk(i, "xattn.q.w")) + r * Hr * H, H, nullptr, xscale, 1, int(Hr), int(H)}, s);
-        rowpar(k, r, KM(dq_r, H), MN(off<T>(W(blk(i, "xattn.q.w")), r * Hr * H), H), int(Hr), xscale);  // dcn partial
+        gemm(bf, MN(dkv_r, 2 * Hr), MN(w.text, td), int(2 * Hr), td, int(L),
+             EpiF32{Gs(blk(i, "xattn.kv.w"), kk), td, nullptr, 1.0f, 1, int(2 * Hr), int(td)}, s);
+        colsum<T>(tp<T>(dkv_r), 2 * Hr, int(L), int(2 * Hr), w.part1, s);
+        reduce_chunks(w.part1, row_chunks(int(L)), int(2 * Hr), Gs(blk(i, "xattn.kv.b"), kk), 1.0f, 1, s);
+        colsum<T>(tp<T>(dq_r), Hr, n, int(Hr), w.part1, s);
+        reduce_chunks(w.part1, chunks, int(Hr), Gs(blk(i, "xattn.q.b"), kk), xscale, 1, s);
+        gemm(bf, MN(dq_r, Hr), MN(b.cn, H), int(Hr), H, n,
+             EpiF32{Gs(blk(i, "xattn.q.w"), kk), H, nullptr, xscale, 1, int(Hr), int(H)}, s);
+        rowpar(k, r, KM(dq_r, Hr), MN(Ws(blk(i, "xattn.q.w"), kk), H), int(Hr), xscale);  // dcn partial
     }
     sum = tp_exchange(part, N, s);
     convert_f32<T>(sum, N * H, tp<T>(w.s2), s);
@@ -1163,34 +1282,34 @@ void Model::block_bwd_tp(int i, int64_t N) {
     reduce_chunks_grouped(w.part1, chunks, nu, H, dm + 2 * H, 6 * H, 1.0f, 0, s);  // d gt1
     reduce_chunks(w.part2, chunks, H, G(blk(i, "attn.out.b")), 1.0f, 1, s);
     for (size_t k = 0; k < ranks.size(); ++k) {
-        const int64_t r = ranks[k];
-        gemm(bf, MN(w.s1, H), MN(off<T>(b.O, r * Hr), H), H, int(Hr), n,
-             EpiF32{G(blk(i, "attn.out.w")) + r * Hr, H, nullptr, 1.0f, 1, int(H), int(Hr)}, s);
-        gemm(bf, KM(w.s1, H), MN(off<T>(W(blk(i, "attn.out.w")), r * Hr), H), n, int(Hr), H,
-             EpiStore<T>{tp<T>(off<T>(w.s2, r * Hr)), H, nullptr, 1.0f, n, int(Hr)}, s);
+        const int kk = static_cast<int>(k);
+        gemm(bf, MN(w.s1, H), MN(off<T>(b.O, k * N * Hr), Hr), H, int(Hr), n,
+             EpiF32{Gs(blk(i, "attn.out.w"), kk), Hr, nullptr, 1.0f, 1, int(H), int(Hr)}, s);
+        gemm(bf, KM(w.s1, H), MN(Ws(blk(i, "attn.out.w"), kk), Hr), n, int(Hr), H,
+             EpiStore<T>{tp<T>(off<T>(w.s2, k * N * Hr)), Hr, nullptr, 1.0f, n, int(Hr)}, s);
     }
     for (size_t k = 0; k < ranks.size(); ++k) {
         const int64_t r = ranks[k];
-        void* qkv_r = off<T>(b.qkv, r * 3 * Hr);
-        void* qk_r = off<T>(b.qk, r * 2 * Hr);
-        void* dqkv_r = off<T>(w.sB, r * 3 * Hr);
-        AttnBwdProblem ab{AttnProblem{qk_r, 2 * H, off<T>(qk_r, Hr), 2 * H, off<T>(qkv_r, 2 * Hr), 3 * H,
-                                      off<T>(b.O, r * Hr), H, b.lse + r * nhr * lld, n, n, int(nhr), int(hd)},
-                          off<T>(w.s2, r * Hr), H, w.Dvec + r * nhr * lld, dqkv_r, 3 * H, off<T>(dqkv_r, Hr), 3 * H,
-                          off<T>(dqkv_r, 2 * Hr), 3 * H, nullptr, 1};
+        const int kk = static_cast<int>(k);
+        void* qkv_r = off<T>(b.qkv, k * N * 3 * Hr);
+        void* qk_r = off<T>(b.qk, k * N * 2 * Hr);
+        void* dqkv_r = off<T>(w.sB, k * N * 3 * Hr);
+        AttnBwdProblem ab{AttnProblem{qk_r, 2 * Hr, off<T>(qk_r, Hr), 2 * Hr, off<T>(qkv_r, 2 * Hr), 3 * Hr,
+                                      off<T>(b.O, k * N * Hr), Hr, b.lse + r * nhr * lld, n, n, int(nhr), int(hd)},
+                          off<T>(w.s2, k * N * Hr), Hr, w.Dvec + r * nhr * lld, dqkv_r, 3 * Hr, off<T>(dqkv_r, Hr),
+                          3 * Hr, off<T>(dqkv_r, 2 * Hr), 3 * Hr, nullptr, 1};
         ab.f.lse_ld = lld;
         prof_.begin("attn_bwd", s);
         attention_bwd<T>(bf, ab, s);
         prof_.end(s);
-        qk_norm_rope_bwd<T>(tp<T>(dqkv_r), tp<T>(qkv_r), QKLayout{3 * H, Hr, 2 * H, Hr, nh}, n, int(Hr), int(nhr),
-                            P(blk(i, "attn.temp")).f32 + r * nhr, w.cs, b.iq + r * nhr, b.ik + r * nhr, w.part1, s);
-        reduce_chunks(w.part1, chunks, int(nhr), G(blk(i, "attn.temp")) + r * nhr, 1.0f, 1, s);
-        colsum<T>(tp<T>(dqkv_r), 3 * H, n, int(3 * Hr), w.part1, s);
-        reduce_chunks(w.part1, chunks, int(3 * Hr), G(blk(i, "attn.qkv.b")) + r * 3 * Hr, 1.0f, 1, s);
-        gemm(bf, MN(dqkv_r, 3 * H), MN(b.a, H), int(3 * Hr), H, n,
-             EpiF32{G(blk(i, "attn.qkv.w")) + r * 3 * Hr * H, H, nullptr, 1.0f, 1, int(3 * Hr), int(H)}, s);
-        rowpar(k, r, KM(dqkv_r, 3 * H), MN(off<T>(W(blk(i, "attn.qkv.w")), r * 3 * Hr * H), H), int(3 * Hr),
-               1.0f);  // da partial
+        qk_norm_rope_bwd<T>(tp<T>(dqkv_r), tp<T>(qkv_r), QKLayout{3 * Hr, Hr, 2 * Hr, Hr, nh}, n, int(Hr), int(nhr),
+                            Ps(blk(i, "attn.temp"), kk), w.cs, b.iq + r * nhr, b.ik + r * nhr, w.part1, s);
+        reduce_chunks(w.part1, chunks, int(nhr), Gs(blk(i, "attn.temp"), kk), 1.0f, 1, s);
+        colsum<T>(tp<T>(dqkv_r), 3 * Hr, n, int(3 * Hr), w.part1, s);
+        reduce_chunks(w.part1, chunks, int(3 * Hr), Gs(blk(i, "attn.qkv.b"), kk), 1.0f, 1, s);
+        gemm(bf, MN(dqkv_r, 3 * Hr), MN(b.a, H), int(3 * Hr), H, n,
+             EpiF32{Gs(blk(i, "attn.qkv.w"), kk), H, nullptr, 1.0f, 1, int(3 * Hr), int(H)}, s);
+        rowpar(k, r, KM(dqkv_r, 3 * Hr), MN(Ws(blk(i, "attn.qkv.w"), kk), H), int(3 * Hr), 1.0f);  // da partial
     }
     sum = tp_exchange(part, N, s);
     convert_f32<T>(sum, N * H, tp<T>(w.s1), s);
@@ -1303,6 +1422,7 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
     w.esz = bf16_ ? 2 : 4;
     w.grads = true;
     w.tp = tp_;
+    w.tp_slots = tp_slots();
     {
         Sizer sz{true, 0, &arena_};
         layout_ws(w, sz, cfg_, true);
@@ -1391,7 +1511,14 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
         dp_finish(w.scal);
         prof_.end(s);
     }
-    sumsq(grad_buf_, grad_numel_, w.loss_part, w.scal + 2, s);  // grad_norm (flowtrain.cpp:284-289)
+    // grad_norm (flowtrain.cpp:284-289); under TP the sharded blocks' squares are summed over the TP group
+    if (tp_ > 1) {
+        sumsq(grad_buf_, repl_numel_, w.loss_part, w.scal + 2, s);
+        sumsq(grad_buf_ + repl_numel_, grad_numel_ - repl_numel_, w.loss_part, w.scal + 3, s);
+        if (!tp_virtual_) MGV_NCCL(ncclAllReduce(w.scal + 3, w.scal + 3, 1, ncclDouble, ncclSum, tp_comm_, s));
+    } else {
+        sumsq(grad_buf_, grad_numel_, w.loss_part, w.scal + 2, s);
+    }
     if (adam_.on) {  // AdamW::update (flowtrain.cpp:278), on device, skipped if the loss is not finite
         if (!opt_m_) alloc_adam_state();
         ++adam_.step;
@@ -1409,8 +1536,8 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
         MGV_CUDA(cudaGetLastError());
         prof_.end(s);
     }
-    double host[3] = {0, 0, 0};
-    MGV_CUDA(cudaMemcpyAsync(host, w.scal, sizeof(double) * 3, cudaMemcpyDeviceToHost, s));
+    double host[4] = {0, 0, 0, 0};
+    MGV_CUDA(cudaMemcpyAsync(host, w.scal, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
     MGV_CUDA(cudaEventRecord(e1, s));
     MGV_CUDA(cudaStreamSynchronize(s));
     float ms = 0.0f;
@@ -1433,7 +1560,7 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
         if (adam_.on) --adam_.step;
         throw NumericError("flow loss is not finite");
     }
-    *grad_norm = std::sqrt(host[2]);
+    *grad_norm = std::sqrt(host[2] + (tp_ > 1 ? host[3] : 0.0));
 }
 
 void Model::flow_step_dev(int64_t n, const DevSample* samples, const double* text_dev, int64_t L, double fps,
@@ -1565,21 +1692,18 @@ void Model::flow_step(int64_t n, const mgv_flow_sample* samples, const double* t
 template <class Alloc>
 void Model::download_grads(double* const* grads_out, Alloc&& dalloc) {
     int64_t maxn = 0;
-    for (auto* p : sorted_) maxn = std::max(maxn, p->numel);
+    for (auto* p : sorted_) maxn = std::max(maxn, p->numel_full);
     auto* gd = static_cast<double*>(dalloc(sizeof(double) * maxn));
-    float* gp = tp_ > 1 ? static_cast<float*>(dalloc(sizeof(float) * maxn)) : nullptr;
+    float* ga = tp_ > 1 ? static_cast<float*>(dalloc(sizeof(float) * maxn)) : nullptr;
+    float* gb = tp_ > 1 ? static_cast<float*>(dalloc(sizeof(float) * maxn)) : nullptr;
     for (size_t k = 0; k < sorted_.size(); ++k) {
+        if (!grads_out[k] && !(tp_ > 1 && !tp_virtual_ && sorted_[k]->shard)) continue;  // gathers are collective
+        const DevParam& q = *sorted_[k];
+        const float* gsrc = full_view(q, q.grad, ga, gb);
         if (!grads_out[k]) continue;
-        const float* gsrc = sorted_[k]->grad;
-        if (const int C = tp_ > 1 ? tp_row_chunks(sorted_[k]->name) : 0) {  // back to the reference row order
-            permute_shard_rows(gsrc, gp, C, static_cast<int>(cfg_.hidden), tp_, sorted_[k]->numel / (C * cfg_.hidden),
-                               1, stream_);
-            gsrc = gp;
-        }
-        f32_to_f64<<<grid_of(sorted_[k]->numel), 256, 0, stream_>>>(gsrc, sorted_[k]->numel, gd);
+        f32_to_f64<<<grid_of(q.numel_full), 256, 0, stream_>>>(gsrc, q.numel_full, gd);
         ::mgv::note_launch();
-        MGV_CUDA(cudaMemcpyAsync(grads_out[k], gd, sizeof(double) * sorted_[k]->numel, cudaMemcpyDeviceToHost,
-                                 stream_));
+        MGV_CUDA(cudaMemcpyAsync(grads_out[k], gd, sizeof(double) * q.numel_full, cudaMemcpyDeviceToHost, stream_));
         MGV_CUDA(cudaStreamSynchronize(stream_));
     }
 }
@@ -1679,6 +1803,7 @@ void Model::value_forward(const double* in, int64_t N, const int32_t* coords, co
     w.esz = bf16_ ? 2 : 4;
     w.grads = false;
     w.tp = tp_;
+    w.tp_slots = tp_slots();
     {
         Sizer sz{true, 0, &arena_};
         layout_ws(w, sz, cfg_, false);
@@ -1763,6 +1888,7 @@ void Model::velocity_graph_impl(const double* rows, int64_t N, const int32_t* co
     w.esz = bf16_ ? 2 : 4;
     w.grads = true;  // keeps every block's residual stream (the taps) and the backward's activations
     w.tp = tp_;
+    w.tp_slots = tp_slots();
     {
         Sizer sz{true, 0, &arena_};
         layout_ws(w, sz, cfg_, true);
@@ -2002,6 +2128,7 @@ void Model::sample_impl(const double* x_start, int64_t N, const int32_t* coords,
     w.esz = bf16_ ? 2 : 4;
     w.grads = false;
     w.tp = tp_;
+    w.tp_slots = tp_slots();
     {
         Sizer sz{true, 0, &arena_};
         layout_ws(w, sz, cfg_, false);

@@ -31,11 +31,16 @@ struct Cfg {
     int64_t D() const { return 4 * c_z; }
 };
 void validate_cfg(const Cfg& c);
+// bytes one rank allocates for a step: out = {parameters, gradients, AdamW moments, workspace, exchange arena}
+void plan_rank_bytes(const Cfg& c, bool bf16, int tp, int64_t N, int64_t L, int n_u, bool train, int64_t out[5]);
 
 struct DevParam {
     std::string name;
     std::vector<int64_t> shape;
-    int64_t numel = 0;
+    int64_t numel = 0;              // elements held by this process (a real TP rank: its shard of sharded params)
+    int64_t numel_full = 0;         // elements of the reference tensor
+    int64_t slot_numel = 0;         // elements of one TP rank's slot (numel_full / P for sharded params)
+    int shard = 0;                  // 0 replicated, 1 row-parallel (rank-major rows), 2 column-parallel (compact)
     float* f32 = nullptr;           // master copy (all params)
     __nv_bfloat16* bf = nullptr;    // tensor-core operand copy (matrices, bf16 mode)
     float* grad = nullptr;          // slice of the contiguous gradient buffer
@@ -132,6 +137,7 @@ public:
     // otherwise this process is TP rank `rank` of an NCCL communicator.  Must precede upload().
     void set_tp(int size, int rank, const uint8_t* id);
     int tp_size() const { return tp_; }
+    void memory_bytes(int64_t out[5]) const;  // this context's allocations, same categories as plan_rank_bytes
     // AdamW::update after every flow step (optim.cpp:7-24, flowtrain.cpp:278); lr <= 0 disables
     void set_adamw(double lr, double beta1, double beta2, double eps, double weight_decay);
     int64_t adamw_steps() const { return adam_.step; }
@@ -226,6 +232,11 @@ private:
                        const double* text, int64_t L, const double* tau, double fps, double* out, bool velocity);
 
     const DevParam& P(const std::string& name) const;
+    // TP rank slot k of a parameter (k indexes tp_ranks(); replicated params: the whole tensor)
+    const float* Ps(const std::string& name, int k) const;
+    const void* Ws(const std::string& name, int k) const;
+    float* Gs(const std::string& name, int k) const;
+    int tp_slots() const { return tp_ > 1 && tp_virtual_ ? tp_ : 1; }
     const void* W(const std::string& name) const;  // GEMM operand in the compute precision
     float* G(const std::string& name) const;
     std::string blk(int i, const char* s) const { return "dit.blk." + std::to_string(i) + "." + s; }
@@ -241,6 +252,8 @@ private:
     std::vector<DevParam*> sorted_;
     float* grad_buf_ = nullptr;
     int64_t grad_numel_ = 0;
+    int64_t repl_numel_ = 0;  // TP: the replicated parameters' leading range of the gradient buffer
+    const float* full_view(const DevParam& q, const float* local, float* a, float* b);
     Arena arena_;
     double last_ms_ = 0.0;
     int64_t last_launches_ = 0;

@@ -160,3 +160,21 @@ def test_tp_gloo_world2():
     for r in range(2):
         assert np.abs(outs[r] - taps[1]).max() <= 1e-12 * max(1.0, np.abs(taps[1]).max())
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_tp_storage_partitions_per_rank():
+    """Sharded storage: per-rank parameter, gradient and AdamW bytes = replicated + sharded / P, and
+    the 56-block 10B stack (configs[3]) at 10,920 tokens fits one B200 (180 GB) per rank at P = 4 and 8."""
+    from paper_2510_17519_b200.capi import paper_config, plan_rank_bytes
+    cfg = paper_config(56)
+    b = {P: plan_rank_bytes(cfg, "bf16", P, 10920, 64, 2, True) for P in (1, 2, 4, 8)}
+    # sharded parameters: qkv, out, xattn q/kv/out, ffn in/out per block (their biases and attn.temp too)
+    H, L = 3456, 4096
+    sharded = 56 * (3 * H * H + 3 * H + 24 + H * H + H * H + H + 2 * H * L + 2 * H + H * H + 4 * H * H + 4 * H + 4 * H * H)
+    for P in (2, 4, 8):
+        d_grad = b[1]["grads"] - b[P]["grads"]
+        assert abs(d_grad - 4 * sharded * (1 - 1 / P)) < 4 * 64 * 56 * 12 * P, (P, d_grad)
+        assert b[P]["adamw"] == 2 * b[P]["grads"]
+        assert b[P]["workspace"] < b[1]["workspace"]
+    tot = {P: sum(v.values()) for P, v in b.items()}
+    assert tot[4] < 180e9 and tot[8] < 180e9 and tot[1] > 180e9, tot

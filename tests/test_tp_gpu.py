@@ -93,3 +93,21 @@ def test_tp_peer_exchange(name, size, prec, monkeypatch):
                 [nerr(b["V"][i], ref["V"][i]) for i in range(len(samples))])
     print(f"tp{size} peer {name}/{prec}: worst {worst:.3e}")
     assert worst <= TOL[prec]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_planner_matches_a_real_context(prec):
+    """mgv_plan_rank_bytes (the per-rank planner used for configs[3]) reproduces what a context actually allocates
+    for the same step (tp = 1: one context is one rank)."""
+    from paper_2510_17519_b200.capi import Context, plan_rank_bytes
+    cfg, P, text, samples = build_case("hd144", CASES["hd144"])
+    ctx = Context(0, prec)
+    ctx.set_adamw(lr=1e-3)
+    ctx.upload(to_cfg(cfg), P)
+    s = samples[0]
+    ctx.flow_step(to_samples([s]), text, 8.0)
+    got = ctx.memory()
+    plan = plan_rank_bytes(to_cfg(cfg), prec, 1, s.clean.shape[0], text.shape[0], 2, True)
+    print(prec, got, plan)
+    for k in ("params", "grads", "adamw", "workspace"):
+        assert got[k] == plan[k], (k, got[k], plan[k])
