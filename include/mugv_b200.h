@@ -146,6 +146,11 @@ mgv_status mgv_params_init(mgv_ctx* ctx, const mgv_dit_cfg* cfg, uint64_t seed, 
 mgv_status mgv_rng_uniform_fill(uint64_t seed, int64_t n, double lo, double hi, double* out);
 mgv_status mgv_make_flow_sample(uint64_t seed, int64_t N, int64_t D, double mask_prob, double* noise, double* t,
                                 int* conditioned);
+/* Varlen packing (BASELINE configs[4]): on != 0 runs every multi-sample flow step as ONE packed sequence of
+ * 256-row-aligned segments with block-diagonal attention, per-sample timesteps in the modulation table and
+ * per-sample masked-mean losses (flowtrain.cpp:263-273): each sample's forward is bit-identical to running it
+ * alone; gradients equal the per-sample sum up to summation order.  Default off (samples run one by one). */
+mgv_status mgv_ctx_set_varlen(mgv_ctx* ctx, int on);
 /* Memory per rank, out = {parameters (fp32 masters + bf16 operand copies), gradients, AdamW moments, step
  * workspace (saved activations + scratch), TP exchange arena} in bytes.  mgv_plan_rank_bytes plans a step of
  * N tokens (text length L, n_u unique timesteps) for TP degree tp without a device, with the runtime's own

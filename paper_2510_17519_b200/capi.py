@@ -122,6 +122,7 @@ def declare(L):
     L.mgv_velocity_graph.argtypes = [P, P, I64, P, P, P, I64, P, D, P, P, P, P]
     L.mgv_plan_rank_bytes.argtypes = [ctypes.POINTER(mgv_dit_cfg), I, I, I64, I64, I64, I, P]
     L.mgv_ctx_memory.argtypes = [P, P]
+    L.mgv_ctx_set_varlen.argtypes = [P, I]
     L.mgv_params_init.argtypes = [P, ctypes.POINTER(mgv_dit_cfg), ctypes.c_uint64, ctypes.c_uint64, D, D]
     L.mgv_params_upload.restype = I
     L.mgv_param_count.argtypes = [P]
@@ -246,7 +247,7 @@ def declare(L):
 # symbols include/mugv_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = ["mgv_ctx_create", "mgv_ctx_destroy", "mgv_last_error", "mgv_ctx_set_stream", "mgv_nccl_unique_id",
            "mgv_ctx_set_dp", "mgv_ctx_set_tp", "mgv_sample_rows", "mgv_ctx_set_adamw", "mgv_adamw_steps", "mgv_param_download",
-           "mgv_params_upload", "mgv_params_init", "mgv_plan_rank_bytes", "mgv_ctx_memory", "mgv_rng_uniform_fill", "mgv_make_flow_sample", "mgv_param_count",
+           "mgv_params_upload", "mgv_params_init", "mgv_ctx_set_varlen", "mgv_plan_rank_bytes", "mgv_ctx_memory", "mgv_rng_uniform_fill", "mgv_make_flow_sample", "mgv_param_count",
            "mgv_param_name", "mgv_param_numel",
            "mgv_predict_velocity", "mgv_velocity_graph", "mgv_dit_forward", "mgv_flow_step", "mgv_flow_loss", "mgv_latent_rows",
            "mgv_rows_to_grid", "mgv_flow_step_device", "mgv_last_step_ms", "mgv_last_step_launches",
@@ -735,6 +736,10 @@ class Context:
         self.cfg = cfg
         self.names = [self._L.mgv_param_name(self.h, i).decode() for i in range(self._L.mgv_param_count(self.h))]
         self.numels = [self._L.mgv_param_numel(self.h, i) for i in range(len(self.names))]
+
+    def set_varlen(self, on: bool = True):
+        """mgv_ctx_set_varlen: pack multi-sample flow steps into one block-diagonal sequence."""
+        self._check(self._L.mgv_ctx_set_varlen(self.h, int(on)))
 
     def memory(self) -> dict:
         """mgv_ctx_memory: this context's allocations in bytes."""

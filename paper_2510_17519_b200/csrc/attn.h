@@ -29,6 +29,10 @@ struct AttnProblem {
     // per-head stride of lse (and of the backward's Dvec); 0 -> Nq.  The tensor-core backward
     // streams lse/D with bulk copies and wants it padded to a multiple of 64.
     int64_t lse_ld = 0;
+    // block-diagonal self-attention over packed samples (varlen): for the 128-row tile t, its segment is rows
+    // [seg[2t], seg[2t+1]); segments start on 256-row boundaries, so no query / key tile straddles two.  null: one
+    // segment [0, N).  Every tile runs exactly the key / query steps it would run alone.
+    const int* seg = nullptr;
 };
 
 __host__ __device__ inline int64_t lse_stride(const AttnProblem& p) { return p.lse_ld ? p.lse_ld : p.Nq; }

@@ -314,9 +314,14 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
     const AttnProblem& f = p.f;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int h = blockIdx.y, k0 = blockIdx.x * BKV;
-    const int nq_all = (f.Nq + BQ - 1) / BQ;
-    const int i0 = static_cast<int>((int64_t)blockIdx.z * nq_all / gridDim.z);
-    const int nq = static_cast<int>((int64_t)(blockIdx.z + 1) * nq_all / gridDim.z) - i0;  // this split's steps
+    // packed segments (AttnProblem::seg): this key tile's segment [qlo, qend) is also its query range; keys at or
+    // past qend are padding rows (P = 0)
+    const int qlo = f.seg ? f.seg[2 * (k0 / 128)] : 0, qend = f.seg ? f.seg[2 * (k0 / 128) + 1] : f.Nq;
+    const int kend = f.seg ? qend : f.Nk;
+    const int nq_all = (qend - qlo + BQ - 1) / BQ;
+    const int i0 = qlo / BQ + static_cast<int>((int64_t)blockIdx.z * nq_all / gridDim.z);
+    const int nq = static_cast<int>((int64_t)(blockIdx.z + 1) * nq_all / gridDim.z) -
+                   static_cast<int>((int64_t)blockIdx.z * nq_all / gridDim.z);  // this split's steps
     const int col = h * HD;
 
     if (threadIdx.x == 0) {
@@ -417,7 +422,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
         const int g = warp & 3, hf = (warp - 4) >> 2, row = g * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(g * 32) << 16;
         const int kv = k0 + row;
-        const bool kvv = kv < f.Nk;
+        const bool kvv = kv < f.Nk, kreal = kv < kend;
         const uint32_t sd = tmem + lane_base + SD_COL + hf * 64, pt = tmem + lane_base + PT_COL + hf * 32;
         for (int i = 0; i < nq; ++i) {
             const int st = i % NST;
@@ -436,10 +441,15 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
             // generic loads made the compute warps' shared wavefronts outnumber the SS MMAs' operand reads
             const uint32_t lse_s = smem_u32(sLse + st * BQ + hf * 64), d_s = smem_u32(sD + st * BQ + hf * 64);
             const int qb = (i0 + i) * BQ + hf * 64;
-            const bool full = qb + 64 <= f.Nq;
+            const bool full = qb + 64 <= qend;
             uint32_t pk[32];
             const float2 lg2 = make_float2(kLog2e, kLog2e);
-            if (full) {  // warp-uniform: no per-column masking; packed f32x2 arithmetic (bit-identical to scalar)
+            if (!kreal) {  // a padding key row of a packed segment
+#pragma unroll
+                for (int c = 0; c < 64; ++c) s[c] = 0.0f;
+#pragma unroll
+                for (int c = 0; c < 32; ++c) pk[c] = 0u;
+            } else if (full) {  // warp-uniform: no per-column masking; packed f32x2 arithmetic (bit-identical to scalar)
 #pragma unroll
                 for (int c4 = 0; c4 < 64; c4 += 4) {
                     const float4 l = lds_f4(lse_s + c4 * 4);
@@ -460,7 +470,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int c = c4 + e;
-                        s[c] = qb + c < f.Nq ? ex2f((s[c] - lv[e]) * kLog2e) : 0.0f;  // lse rows are natural-log
+                        s[c] = qb + c < qend ? ex2f((s[c] - lv[e]) * kLog2e) : 0.0f;  // lse rows are natural-log
                     }
                     pk[c4 / 2] = pack_bf16(s[c4], s[c4 + 1]);
                     pk[c4 / 2 + 1] = pack_bf16(s[c4 + 2], s[c4 + 3]);
@@ -565,7 +575,9 @@ __global__ void __launch_bounds__(128 + 128 * 2, 1) attn_bwd_dq_v10_kernel(const
     const AttnProblem& f = p.f;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int h = blockIdx.y, q0 = blockIdx.x * BMQ;
-    const int nkv = (f.Nk + BKV - 1) / BKV;
+    // packed segments (AttnProblem::seg): this query tile's keys are its segment's
+    const int klo = f.seg ? f.seg[2 * (q0 / 128)] : 0, khi = f.seg ? f.seg[2 * (q0 / 128) + 1] : f.Nk;
+    const int nkv = (khi - klo + BKV - 1) / BKV;
     const int col = h * HD;
 
     if (threadIdx.x == 0) {
@@ -600,13 +612,13 @@ __global__ void __launch_bounds__(128 + 128 * 2, 1) attn_bwd_dq_v10_kernel(const
                 const int b = j % NS;
                 if (j >= NS) mbar_wait(&ke[b], ((j / NS) - 1) & 1);
                 mbar_arrive_expect_tx(&kf[b], KV_STAGE);
-                tma_load_2d(sKt + b * KV_STAGE, &tm.ta, &kf[b], j * BKV, col);
-                tma_load_2d(sKt + b * KV_STAGE + T::T_TILE, &tm.ta, &kf[b], j * BKV + 64, col);
+                tma_load_2d(sKt + b * KV_STAGE, &tm.ta, &kf[b], klo + j * BKV, col);
+                tma_load_2d(sKt + b * KV_STAGE + T::T_TILE, &tm.ta, &kf[b], klo + j * BKV + 64, col);
                 const int bv = j % NSV;
                 if (j >= NSV) mbar_wait(&ve[bv], ((j / NSV) - 1) & 1);
                 mbar_arrive_expect_tx(&vf[bv], KV_STAGE);
-                tma_load_2d(sVt + bv * KV_STAGE, &tm.tb, &vf[bv], j * BKV, col);
-                tma_load_2d(sVt + bv * KV_STAGE + T::T_TILE, &tm.tb, &vf[bv], j * BKV + 64, col);
+                tma_load_2d(sVt + bv * KV_STAGE, &tm.tb, &vf[bv], klo + j * BKV, col);
+                tma_load_2d(sVt + bv * KV_STAGE + T::T_TILE, &tm.tb, &vf[bv], klo + j * BKV + 64, col);
             }
         }
     } else if (warp == 1) {
@@ -702,8 +714,8 @@ __global__ void __launch_bounds__(128 + 128 * 2, 1) attn_bwd_dq_v10_kernel(const
             __syncwarp();
             if (lane == 0) mbar_arrive(s_empty);
             if (warp == 4 && lane == 0) ATR(4, j);
-            const int kb = j * BKV + hf * KW;
-            if (kb + KW <= f.Nk) {  // packed pairs: FFMA2 (bit-identical to the scalar fmaf)
+            const int kb = klo + j * BKV + hf * KW;
+            if (kb + KW <= khi) {  // packed pairs: FFMA2 (bit-identical to the scalar fmaf)
                 const float2 lg2 = make_float2(kLog2e, kLog2e), nl2 = make_float2(-lse2, -lse2);
 #pragma unroll
                 for (int c = 0; c < KW; c += 2) {
@@ -713,7 +725,7 @@ __global__ void __launch_bounds__(128 + 128 * 2, 1) attn_bwd_dq_v10_kernel(const
                 }
             } else {
 #pragma unroll
-                for (int c = 0; c < KW; ++c) pr[c] = kb + c < f.Nk ? ex2f(fmaf(pr[c], kLog2e, -lse2)) : 0.0f;
+                for (int c = 0; c < KW; ++c) pr[c] = kb + c < khi ? ex2f(fmaf(pr[c], kLog2e, -lse2)) : 0.0f;
             }
             if (warp == 4 && lane == 0) ATR(5, j);
             mbar_wait(dp_full, j & 1);

@@ -29,6 +29,7 @@ template <class T>
 __global__ void __launch_bounds__(NT) attn_fwd_simt_kernel(AttnProblem p) {
     extern __shared__ float sm[];
     const int hd = p.hd, h = blockIdx.y, q0 = blockIdx.x * BQ, tid = threadIdx.x;
+    const int klo = p.seg ? p.seg[2 * (q0 / 128)] : 0, khi = p.seg ? p.seg[2 * (q0 / 128) + 1] : p.Nk;
     float* sQ = sm;
     float* sO = sQ + BQ * hd;
     float* sK = sO + BQ * hd;
@@ -46,11 +47,11 @@ __global__ void __launch_bounds__(NT) attn_fwd_simt_kernel(AttnProblem p) {
         sM[tid] = -FLT_MAX;
         sL[tid] = 0.0f;
     }
-    for (int k0 = 0; k0 < p.Nk; k0 += BK) {
+    for (int k0 = klo; k0 < khi; k0 += BK) {
         __syncthreads();
         for (int e = tid; e < BK * hd; e += NT) {
             const int j = e / hd, d = e % hd, kk = k0 + j;
-            const bool in = kk < p.Nk;
+            const bool in = kk < khi;
             sK[j * (hd + 1) + d] = in ? ld_el<T>(p.k, (int64_t)kk * p.k_ld + h * hd + d) : 0.0f;
             sV[e] = in ? ld_el<T>(p.v, (int64_t)kk * p.v_ld + h * hd + d) : 0.0f;
         }
@@ -59,7 +60,7 @@ __global__ void __launch_bounds__(NT) attn_fwd_simt_kernel(AttnProblem p) {
             const int i = e / BK, j = e % BK;
             float acc = 0.0f;
             for (int d = 0; d < hd; ++d) acc = fmaf(sQ[i * hd + d], sK[j * (hd + 1) + d], acc);
-            sS[i * (BK + 1) + j] = (k0 + j < p.Nk) ? acc : -FLT_MAX;
+            sS[i * (BK + 1) + j] = (k0 + j < khi) ? acc : -FLT_MAX;
         }
         __syncthreads();
         if (tid < BQ) {
@@ -69,7 +70,7 @@ __global__ void __launch_bounds__(NT) attn_fwd_simt_kernel(AttnProblem p) {
             const float alpha = expf(sM[tid] - mx);
             float sum = 0.0f;
             for (int j = 0; j < BK; ++j) {
-                const float pj = (k0 + j < p.Nk) ? expf(row[j] - mx) : 0.0f;
+                const float pj = (k0 + j < khi) ? expf(row[j] - mx) : 0.0f;
                 row[j] = pj;
                 sum += pj;
             }
@@ -144,6 +145,7 @@ __global__ void __launch_bounds__(NT) attn_bwd_dq_simt_kernel(AttnBwdProblem p) 
     extern __shared__ float sm[];
     const AttnProblem& f = p.f;
     const int hd = f.hd, h = blockIdx.y, q0 = blockIdx.x * BQ, tid = threadIdx.x;
+    const int klo = f.seg ? f.seg[2 * (q0 / 128)] : 0, khi = f.seg ? f.seg[2 * (q0 / 128) + 1] : f.Nk;
     float* sQ = sm;
     float* sdO = sQ + BQ * hd;
     float* sK = sdO + BQ * hd;
@@ -161,12 +163,12 @@ __global__ void __launch_bounds__(NT) attn_bwd_dq_simt_kernel(AttnBwdProblem p) 
         sLse[tid] = q < f.Nq ? f.lse[(int64_t)h * lse_stride(f) + q] : 0.0f;
         sD[tid] = q < f.Nq ? p.Dvec[(int64_t)h * lse_stride(f) + q] : 0.0f;
     }
-    for (int k0 = 0; k0 < f.Nk; k0 += BK) {
+    for (int k0 = klo; k0 < khi; k0 += BK) {
         __syncthreads();
-        load_rows<T>(sK, hd + 1, f.k, f.k_ld, k0, BK, f.Nk, h, hd);
-        load_rows<T>(sV, hd + 1, f.v, f.v_ld, k0, BK, f.Nk, h, hd);
+        load_rows<T>(sK, hd + 1, f.k, f.k_ld, k0, BK, khi, h, hd);
+        load_rows<T>(sV, hd + 1, f.v, f.v_ld, k0, BK, khi, h, hd);
         __syncthreads();
-        bwd_tile_p_ds(sQ, sdO, sK, sV, sLse, sD, sP, sdS, hd, q0, f.Nq, k0, f.Nk);
+        bwd_tile_p_ds(sQ, sdO, sK, sV, sLse, sD, sP, sdS, hd, q0, f.Nq, k0, khi);
         __syncthreads();
         for (int e = tid; e < BQ * hd; e += NT) {  // dQ += dS K
             const int i = e / hd, d = e % hd;
@@ -200,21 +202,23 @@ __global__ void __launch_bounds__(NT) attn_bwd_dkv_simt_kernel(AttnBwdProblem p)
     load_rows<T>(sK, hd + 1, f.k, f.k_ld, k0, BK, f.Nk, h, hd);
     load_rows<T>(sV, hd + 1, f.v, f.v_ld, k0, BK, f.Nk, h, hd);
     for (int e = tid; e < BK * hd; e += NT) sdK[e] = sdV[e] = 0.0f;
-    const int qtiles = (f.Nq + BQ - 1) / BQ;
+    const int qlo = f.seg ? f.seg[2 * (k0 / 128)] : 0, qhi = f.seg ? f.seg[2 * (k0 / 128) + 1] : f.Nq;
+    const int qtiles = (qhi - qlo + BQ - 1) / BQ;
     const int per = (qtiles + p.q_splits - 1) / p.q_splits;
     const int t0 = split * per, t1 = min(qtiles, t0 + per);
     for (int qt = t0; qt < t1; ++qt) {
-        const int q0 = qt * BQ;
+        const int q0 = qlo + qt * BQ;
         __syncthreads();
-        load_rows<T>(sQ, hd, f.q, f.q_ld, q0, BQ, f.Nq, h, hd);
-        load_rows<T>(sdO, hd, p.dO, p.do_ld, q0, BQ, f.Nq, h, hd);
+        load_rows<T>(sQ, hd, f.q, f.q_ld, q0, BQ, qhi, h, hd);
+        load_rows<T>(sdO, hd, p.dO, p.do_ld, q0, BQ, qhi, h, hd);
         if (tid < BQ) {
             const int q = q0 + tid;
-            sLse[tid] = q < f.Nq ? f.lse[(int64_t)h * lse_stride(f) + q] : 0.0f;
-            sD[tid] = q < f.Nq ? p.Dvec[(int64_t)h * lse_stride(f) + q] : 0.0f;
+            sLse[tid] = q < qhi ? f.lse[(int64_t)h * lse_stride(f) + q] : 0.0f;
+            sD[tid] = q < qhi ? p.Dvec[(int64_t)h * lse_stride(f) + q] : 0.0f;
         }
         __syncthreads();
-        bwd_tile_p_ds(sQ, sdO, sK, sV, sLse, sD, sP, sdS, hd, q0, f.Nq, k0, f.Nk);
+        // packed segments: keys past the tile's own segment end are padding rows (P = 0, so dK = dV = 0 there)
+        bwd_tile_p_ds(sQ, sdO, sK, sV, sLse, sD, sP, sdS, hd, q0, qhi, k0, f.seg ? qhi : f.Nk);
         __syncthreads();
         for (int e = tid; e < BK * hd; e += NT) {  // dV += P^T dO ; dK += dS^T Q
             const int j = e / hd, d = e % hd;

@@ -93,7 +93,9 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_tc_kernel(const __grid_consta
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int h = blockIdx.y, q0 = blockIdx.x * 2 * BM;
-    const int nkv = (p.Nk + BN - 1) / BN;
+    // packed segments (AttnProblem::seg): this CTA's 256 queries lie in one segment; its keys are that segment's
+    const int klo = p.seg ? p.seg[2 * (q0 / 128)] : 0, khi = p.seg ? p.seg[2 * (q0 / 128) + 1] : p.Nk;
+    const int nkv = (khi - klo + BN - 1) / BN;
     const int col = h * HD;
 
     if (threadIdx.x == 0) {
@@ -130,10 +132,10 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_tc_kernel(const __grid_consta
                     uint8_t* sK = sStage + st * C::STAGE;
                     uint8_t* sVt = sK + C::K_TILE;
                     mbar_arrive_expect_tx(&k_full[st], C::K_BYTES);
-                    load_rows<HD, BN>(sK, &tm.k128, &tm.k32, &k_full[st], col, j * BN);
+                    load_rows<HD, BN>(sK, &tm.k128, &tm.k32, &k_full[st], col, klo + j * BN);
                     mbar_arrive_expect_tx(&v_full[st], C::VT_TILE);
-                    tma_load_2d(sVt, &tm.vt, &v_full[st], j * BN, col);
-                    tma_load_2d(sVt + C::VT_CHUNK, &tm.vt, &v_full[st], j * BN + 64, col);
+                    tma_load_2d(sVt, &tm.vt, &v_full[st], klo + j * BN, col);
+                    tma_load_2d(sVt + C::VT_CHUNK, &tm.vt, &v_full[st], klo + j * BN + 64, col);
                 }
             }
         } else if (warp == 1) {
@@ -212,11 +214,11 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_tc_kernel(const __grid_consta
             tmem_ld32(sS + 64, reinterpret_cast<uint32_t*>(s + 64));
             tmem_ld16(sS + 96, reinterpret_cast<uint32_t*>(s + 96));
             tmem_wait_ld();
-            const int kv0 = j * BN;
-            if (kv0 + BN > p.Nk) {
+            const int kv0 = klo + j * BN;
+            if (kv0 + BN > khi) {
 #pragma unroll
                 for (int c = 0; c < BN; ++c)
-                    if (kv0 + c >= p.Nk) s[c] = -FLT_MAX;
+                    if (kv0 + c >= khi) s[c] = -FLT_MAX;
             }
             float mx8[8];
 #pragma unroll

@@ -213,6 +213,10 @@ mgv_status mgv_make_flow_sample(uint64_t seed, int64_t N, int64_t D, double mask
     return MGV_OK;
 }
 
+mgv_status mgv_ctx_set_varlen(mgv_ctx* ctx, int on) {
+    return guard(ctx, [&] { ctx->model->set_varlen(on != 0); });
+}
+
 // per-rank memory of a training (or forward) step: {parameters, gradients, AdamW moments, workspace, exchange}
 mgv_status mgv_plan_rank_bytes(const mgv_dit_cfg* cfg, int precision, int tp, int64_t N, int64_t L, int64_t n_u,
                                int train, int64_t out[5]) {

@@ -21,7 +21,8 @@ inline int row_chunks(int N) { return (N + kRowsPerChunk - 1) / kRowsPerChunk; }
 // cond_lat = N x D device condition latents (read only at conditioned rows) or null (= clean)
 template <class T>
 void prep_flow_sample(const double* clean, const double* noise, const uint8_t* cond, const double* cond_lat, int N,
-                      int D, double t, T* rows, float* v_target, uint8_t* loss_mask, int32_t* mod_id, cudaStream_t s);
+                      int D, double t, T* rows, float* v_target, uint8_t* loss_mask, int32_t* mod_id, cudaStream_t s,
+                      int id_t = 0, int id_0 = 1);
 // rows (fp64, host layout) -> T, plus mod ids given on device
 template <class T>
 void convert_rows(const double* src, int64_t n, T* dst, cudaStream_t s);

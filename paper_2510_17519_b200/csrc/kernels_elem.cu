@@ -94,7 +94,7 @@ inline int grid_for(int64_t n, int threads = 256) {
 template <class T>
 __global__ void prep_flow_sample_kernel(const double* clean, const double* noise, const uint8_t* cond,
                                         const double* cond_lat, int N, int D, double t, T* rows, float* vt,
-                                        uint8_t* lmask, int32_t* mod_id) {
+                                        uint8_t* lmask, int32_t* mod_id, int id_t, int id_0) {
     const int64_t total = (int64_t)N * D;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int i = static_cast<int>(e / D);
@@ -106,15 +106,17 @@ __global__ void prep_flow_sample_kernel(const double* clean, const double* noise
         vt[e] = static_cast<float>(n - x);
         if (e % D == 0) {
             lmask[i] = c ? 0 : 1;
-            mod_id[i] = c ? 1 : 0;  // table row 0: tau = t ; row 1: tau = 0 (flowtrain.cpp:96)
+            mod_id[i] = c ? id_0 : id_t;  // modulation-table rows of tau = t and tau = 0 (flowtrain.cpp:96)
         }
     }
 }
 template <class T>
 void prep_flow_sample(const double* clean, const double* noise, const uint8_t* cond, const double* cond_lat, int N,
-                      int D, double t, T* rows, float* vt, uint8_t* lmask, int32_t* mod_id, cudaStream_t s) {
+                      int D, double t, T* rows, float* vt, uint8_t* lmask, int32_t* mod_id, cudaStream_t s, int id_t,
+                      int id_0) {
     prep_flow_sample_kernel<T><<<grid_for((int64_t)N * D), 256, 0, s>>>(clean, noise, cond, cond_lat, N, D, t, rows,
-                                                                        vt, lmask, mod_id); ::mgv::note_launch();
+                                                                        vt, lmask, mod_id, id_t, id_0);
+    ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 
@@ -1133,7 +1135,7 @@ void permute_shard_rows(const double* src, double* dst, int C, int R, int P, int
 
 #define INST(T)                                                                                                       \
     template void prep_flow_sample<T>(const double*, const double*, const uint8_t*, const double*, int, int, double, \
-                                      T*, float*, uint8_t*, int32_t*, cudaStream_t);                                  \
+                                      T*, float*, uint8_t*, int32_t*, cudaStream_t, int, int);                        \
     template void convert_rows<T>(const double*, int64_t, T*, cudaStream_t);                                          \
     template void convert_f32<T>(const float*, int64_t, T*, cudaStream_t);                                            \
     template void rms_mod<T>(const float*, int, int, const float*, int64_t, int, int, const int32_t*, T*, float*,     \

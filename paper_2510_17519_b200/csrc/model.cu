@@ -86,6 +86,9 @@ struct Model::WS {
     // tensor parallel: fp32 partial sums of the row-parallel GEMMs (the all-reduce buffer)
     int tp = 1, tp_slots = 1;  // slots: TP ranks whose per-rank activations live here (emulated ranks: all)
     float* tpp = nullptr;
+    // varlen packing: per 128-row tile its sample's [start, end) (AttnProblem::seg); seg = null when unpacked
+    int* segbuf = nullptr;
+    const int* seg = nullptr;
 };
 
 struct AdamParam {
@@ -166,6 +169,8 @@ void layout_ws(Model::WS& w, S& a, const Cfg& c, bool grads) {
         b.h = a.takeT(R * N * 4 * Hr, e);
         b.ff = a.takeT(N * H, e);
     }
+    w.segbuf = a.template take<int>(2 * ((N + 127) / 128));
+    w.seg = nullptr;
     w.rf = a.template take<float>(N);
     w.fin = a.takeT(N * H, e);
     w.Y = a.takeT(N * H, e);
@@ -917,6 +922,7 @@ void Model::block_fwd(int i, int64_t N) {
                    n, n, int(nh), int(hd)};
     prof_.begin("attn_fwd", s);
     ap.lse_ld = (N + 127) / 128 * 128;
+    ap.seg = w.seg;
     attention_fwd<T>(bf, ap, s);  // mha (autodiff.cpp:755-793)
     prof_.end(s);
     gemm(bf, KM(b.O, H), KM(W(blk(i, "attn.out.w")), H), n, H, H,
@@ -1014,6 +1020,7 @@ void Model::block_bwd(int i, int64_t N) {
                       w.s2, H, w.Dvec, w.sB, 3 * H, off<T>(w.sB, H), 3 * H, off<T>(w.sB, 2 * H), 3 * H, nullptr, 1};
     prof_.begin("attn_bwd", s);
     ab.f.lse_ld = (N + 127) / 128 * 128;
+    ab.f.seg = w.seg;
     attention_bwd<T>(bf, ab, s);
     prof_.end(s);
     qk_norm_rope_bwd<T>(tp<T>(w.sB), tp<T>(b.qkv), qk_layout_full(H, nh), n, H, nh, P(blk(i, "attn.temp")).f32, w.cs, b.iq, b.ik, w.part1, s);
@@ -1137,6 +1144,7 @@ void Model::block_fwd_tp(int i, int64_t N) {
         AttnProblem ap{qk_r, 2 * Hr, off<T>(qk_r, Hr), 2 * Hr, off<T>(qkv_r, 2 * Hr), 3 * Hr, O_r, Hr,
                        b.lse + r * nhr * lld, n, n, int(nhr), int(hd)};
         ap.lse_ld = lld;
+        ap.seg = w.seg;
         prof_.begin("attn_fwd", s);
         attention_fwd<T>(bf, ap, s);
         prof_.end(s);
@@ -1299,6 +1307,7 @@ void Model::block_bwd_tp(int i, int64_t N) {
                           off<T>(w.s2, k * N * Hr), Hr, w.Dvec + r * nhr * lld, dqkv_r, 3 * Hr, off<T>(dqkv_r, Hr),
                           3 * Hr, off<T>(dqkv_r, 2 * Hr), 3 * Hr, nullptr, 1};
         ab.f.lse_ld = lld;
+        ab.f.seg = w.seg;
         prof_.begin("attn_bwd", s);
         attention_bwd<T>(bf, ab, s);
         prof_.end(s);
@@ -1397,6 +1406,27 @@ void Model::backward_sample(const void* dV) {
 // ------------------------------------------------------------------ flow step
 static double wk_of(const StepExtra* ex, int64_t k, int64_t B) {
     return ex && ex->weight ? ex->weight[k] : 1.0 / static_cast<double>(B);
+}
+
+// AdamW::update (optim.cpp:7-24) over every parameter slot held here; the kernel skips the update when the step's
+// loss accumulator is not finite (FlowTrainer::step throws before updating, flowtrain.cpp:276)
+void Model::adamw_step(cudaStream_t s) {
+    WS& w = *ws_;
+    if (!opt_m_) alloc_adam_state();
+    ++adam_.step;
+    const double bc1 = 1.0 - std::pow(adam_.b1, static_cast<double>(adam_.step));
+    const double bc2 = 1.0 - std::pow(adam_.b2, static_cast<double>(adam_.step));
+    int64_t maxn = 0;
+    for (auto* q : sorted_) maxn = std::max(maxn, q->numel);
+    const dim3 grid(static_cast<unsigned>(std::min<int64_t>((maxn / 4 + 255) / 256, 592)),
+                    static_cast<unsigned>(sorted_.size()));
+    prof_.begin("adamw", s);
+    adamw_kernel<<<grid, 256, 0, s>>>(static_cast<const AdamParam*>(param_table_), grad_buf_, opt_m_, opt_v_, w.scal,
+                                      float(adam_.lr), float(adam_.b1), float(adam_.b2), float(adam_.eps),
+                                      float(adam_.wd), float(1.0 / bc1), float(1.0 / bc2));
+    note_launch();
+    MGV_CUDA(cudaGetLastError());
+    prof_.end(s);
 }
 
 template <class T>
@@ -1519,23 +1549,7 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
     } else {
         sumsq(grad_buf_, grad_numel_, w.loss_part, w.scal + 2, s);
     }
-    if (adam_.on) {  // AdamW::update (flowtrain.cpp:278), on device, skipped if the loss is not finite
-        if (!opt_m_) alloc_adam_state();
-        ++adam_.step;
-        const double bc1 = 1.0 - std::pow(adam_.b1, static_cast<double>(adam_.step));
-        const double bc2 = 1.0 - std::pow(adam_.b2, static_cast<double>(adam_.step));
-        int64_t maxn = 0;
-        for (auto* q : sorted_) maxn = std::max(maxn, q->numel);
-        const dim3 grid(static_cast<unsigned>(std::min<int64_t>((maxn / 4 + 255) / 256, 592)),
-                        static_cast<unsigned>(sorted_.size()));
-        prof_.begin("adamw", s);
-        adamw_kernel<<<grid, 256, 0, s>>>(static_cast<const AdamParam*>(param_table_), grad_buf_, opt_m_, opt_v_,
-                                          w.scal, float(adam_.lr), float(adam_.b1), float(adam_.b2),
-                                          float(adam_.eps), float(adam_.wd), float(1.0 / bc1), float(1.0 / bc2));
-        note_launch();
-        MGV_CUDA(cudaGetLastError());
-        prof_.end(s);
-    }
+    if (adam_.on) adamw_step(s);  // AdamW::update (flowtrain.cpp:278), on device, skipped if the loss is not finite
     double host[4] = {0, 0, 0, 0};
     MGV_CUDA(cudaMemcpyAsync(host, w.scal, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
     MGV_CUDA(cudaEventRecord(e1, s));
@@ -1566,10 +1580,135 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
 void Model::flow_step_dev(int64_t n, const DevSample* samples, const double* text_dev, int64_t L, double fps,
                           double* loss, double* grad_norm, double* const* v_dev, const StepExtra* ex) {
     MGV_CUDA(cudaSetDevice(device_));
+    const bool packed = varlen_ && n > 1 && !ex;
     if (bf16_)
-        flow_step_impl<__nv_bfloat16>(n, samples, text_dev, L, fps, loss, grad_norm, v_dev, ex);
+        packed ? flow_step_packed<__nv_bfloat16>(n, samples, text_dev, L, fps, loss, grad_norm, v_dev)
+               : flow_step_impl<__nv_bfloat16>(n, samples, text_dev, L, fps, loss, grad_norm, v_dev, ex);
     else
-        flow_step_impl<float>(n, samples, text_dev, L, fps, loss, grad_norm, v_dev, ex);
+        packed ? flow_step_packed<float>(n, samples, text_dev, L, fps, loss, grad_norm, v_dev)
+               : flow_step_impl<float>(n, samples, text_dev, L, fps, loss, grad_norm, v_dev, ex);
+}
+
+// Varlen packing (BASELINE configs[4]): the batch as ONE sequence of 256-row-aligned segments, one forward and
+// one backward over all of it.  Attention is block-diagonal (AttnProblem::seg: each tile sees exactly its own
+// sample's keys, with the step boundaries it has alone), the modulation table holds every sample's timestep plus
+// 0 (mod_id per token), the RoPE table follows each token's coords, and the loss is each sample's masked mean over
+// its own rows (flowtrain.cpp:263-273).  Padding rows are zero inputs with loss mask 0 and are never attended to,
+// so every sample's forward is bit-identical to running it alone (dit_forward_batch's contract,
+// test_dit.cpp:205-222); the gradients differ from per-sample accumulation only in summation order.
+template <class T>
+void Model::flow_step_packed(int64_t n, const DevSample* samples, const double* text_dev, int64_t L, double fps,
+                             double* loss, double* grad_norm, double* const* v_dev) {
+    if (!have_params_) throw InputError("no parameters uploaded");
+    WS& w = *ws_;
+    cudaStream_t s = stream_;
+    const int64_t D = cfg_.D();
+    std::vector<int64_t> base(static_cast<size_t>(n) + 1, 0);
+    for (int64_t k = 0; k < n; ++k) base[k + 1] = base[k] + (samples[k].N + 255) / 256 * 256;
+    const int64_t Np = base[n];
+    w.N = Np;
+    w.L = L;
+    w.n_u = static_cast<int>(n) + 1;
+    w.esz = bf16_ ? 2 : 4;
+    w.grads = true;
+    w.tp = tp_;
+    w.tp_slots = tp_slots();
+    {
+        Sizer sz{true, 0, &arena_};
+        layout_ws(w, sz, cfg_, true);
+        arena_.reserve(sz.bytes);
+        arena_.reset();
+        Sizer real{false, 0, &arena_};
+        layout_ws(w, real, cfg_, true);
+    }
+    const int64_t launches0 = launch_count();
+    cudaEvent_t e0, e1;
+    MGV_CUDA(cudaEventCreate(&e0));
+    MGV_CUDA(cudaEventCreate(&e1));
+    MGV_CUDA(cudaEventRecord(e0, s));
+    prof_.begin_step();
+    GemmProfGuard gemm_prof(prof_);
+    MGV_CUDA(cudaMemsetAsync(grad_buf_, 0, sizeof(float) * grad_numel_, s));
+    MGV_CUDA(cudaMemsetAsync(w.scal, 0, sizeof(double) * 8, s));
+    convert_rows<T>(text_dev, L * cfg_.text_dim, tp<T>(w.text), s);
+    // padding rows: zero inputs, zero targets, loss mask 0, coords (0, 0, 0), table row 0
+    MGV_CUDA(cudaMemsetAsync(w.rows, 0, static_cast<size_t>(w.esz) * Np * D, s));
+    MGV_CUDA(cudaMemsetAsync(w.vt, 0, sizeof(float) * Np * D, s));
+    MGV_CUDA(cudaMemsetAsync(w.lmask, 0, Np, s));
+    MGV_CUDA(cudaMemsetAsync(w.mod_id, 0, sizeof(int32_t) * Np, s));
+    MGV_CUDA(cudaMemsetAsync(w.coords, 0, sizeof(int32_t) * 3 * Np, s));
+    std::vector<double> taus(static_cast<size_t>(n) + 1, 0.0);  // t_0 .. t_{n-1}, then 0 (conditioned tokens)
+    std::vector<int> seg(static_cast<size_t>(2 * ((Np + 127) / 128)));
+    for (int64_t k = 0; k < n; ++k) {
+        const DevSample& sm = samples[k];
+        taus[static_cast<size_t>(k)] = sm.t;
+        MGV_CUDA(cudaMemcpyAsync(w.coords + 3 * base[k], sm.coords, sizeof(int32_t) * 3 * sm.N, cudaMemcpyDeviceToDevice,
+                                 s));
+        prep_flow_sample<T>(sm.clean, sm.noise, sm.cond, sm.cond_lat, static_cast<int>(sm.N), int(D), sm.t,
+                            tp<T>(off<T>(w.rows, base[k] * D)), w.vt + base[k] * D, w.lmask + base[k],
+                            w.mod_id + base[k], s, static_cast<int>(k), static_cast<int>(n));
+        for (int64_t t = base[k] / 128; t < base[k + 1] / 128; ++t) {
+            seg[static_cast<size_t>(2 * t)] = static_cast<int>(base[k]);
+            seg[static_cast<size_t>(2 * t + 1)] = static_cast<int>(base[k] + sm.N);
+        }
+    }
+    MGV_CUDA(cudaMemcpyAsync(w.taus, taus.data(), sizeof(double) * taus.size(), cudaMemcpyHostToDevice, s));
+    MGV_CUDA(cudaMemcpyAsync(w.segbuf, seg.data(), sizeof(int) * seg.size(), cudaMemcpyHostToDevice, s));
+    w.seg = w.segbuf;
+    DevSample dummy;
+    forward_sample<T>(dummy, w.rows, nullptr, w.n_u, nullptr, fps, true, true, nullptr);
+    const int64_t B_global = n * world_;
+    MGV_CUDA(cudaMemsetAsync(w.dV, 0, static_cast<size_t>(w.esz) * Np * D, s));
+    for (int64_t k = 0; k < n; ++k) {  // each sample's masked mean (autodiff.cpp:466-491) and its dV rows
+        const int Nk = static_cast<int>(samples[k].N);
+        const float* Vk = w.V + base[k] * D;
+        if (v_dev && v_dev[k]) {
+            f32_to_f64<<<grid_of(Nk * D), 256, 0, s>>>(Vk, Nk * D, v_dev[k]);
+            note_launch();
+        }
+        count_mask(w.lmask + base[k], Nk, w.cnt, s);
+        flow_loss_fwd<T>(Vk, w.vt + base[k] * D, w.lmask + base[k], Nk, int(D), w.loss_part, s);
+        flow_loss_accumulate(w.loss_part, row_chunks(Nk), w.cnt, int(D), w.scal, s);
+        flow_loss_bwd<T>(Vk, w.vt + base[k] * D, w.lmask + base[k], Nk, int(D),
+                         static_cast<float>(2.0 / static_cast<double>(B_global)), w.cnt,
+                         tp<T>(off<T>(w.dV, base[k] * D)), s);
+    }
+    dp_overlap_ = comm_ != nullptr;
+    dp_done_.clear();
+    backward_sample<T>(w.dV);
+    dp_overlap_ = false;
+    w.seg = nullptr;
+    tp_allreduce_grads(s);
+    if (comm_) {
+        prof_.begin("allreduce", s);
+        dp_finish(w.scal);
+        prof_.end(s);
+    }
+    if (tp_ > 1) {
+        sumsq(grad_buf_, repl_numel_, w.loss_part, w.scal + 2, s);
+        sumsq(grad_buf_ + repl_numel_, grad_numel_ - repl_numel_, w.loss_part, w.scal + 3, s);
+        if (!tp_virtual_) MGV_NCCL(ncclAllReduce(w.scal + 3, w.scal + 3, 1, ncclDouble, ncclSum, tp_comm_, s));
+    } else {
+        sumsq(grad_buf_, grad_numel_, w.loss_part, w.scal + 2, s);
+    }
+    if (adam_.on) adamw_step(s);
+    double host[4] = {0, 0, 0, 0};
+    MGV_CUDA(cudaMemcpyAsync(host, w.scal, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
+    MGV_CUDA(cudaEventRecord(e1, s));
+    MGV_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.0f;
+    MGV_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    last_ms_ = ms;
+    last_launches_ = launch_count() - launches0;
+    prof_.end_step();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *loss = host[0] / static_cast<double>(B_global);  // flowtrain.cpp:273
+    if (!std::isfinite(*loss)) {  // flowtrain.cpp:276 (the device AdamW step was skipped)
+        if (adam_.on) --adam_.step;
+        throw NumericError("flow loss is not finite");
+    }
+    *grad_norm = std::sqrt(host[2] + (tp_ > 1 ? host[3] : 0.0));
 }
 
 // host-buffer flow step: validate, stage to device, run, read back

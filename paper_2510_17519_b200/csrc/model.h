@@ -137,6 +137,9 @@ public:
     // otherwise this process is TP rank `rank` of an NCCL communicator.  Must precede upload().
     void set_tp(int size, int rank, const uint8_t* id);
     int tp_size() const { return tp_; }
+    // varlen packing of multi-sample flow steps (flow_step_packed); off: samples run one after another
+    void set_varlen(bool on) { varlen_ = on; }
+    bool varlen() const { return varlen_; }
     void memory_bytes(int64_t out[5]) const;  // this context's allocations, same categories as plan_rank_bytes
     // AdamW::update after every flow step (optim.cpp:7-24, flowtrain.cpp:278); lr <= 0 disables
     void set_adamw(double lr, double beta1, double beta2, double eps, double weight_decay);
@@ -199,6 +202,10 @@ private:
     template <class T>
     void flow_step_impl(int64_t n, const DevSample* samples, const double* text_dev, int64_t L, double fps,
                         double* loss, double* grad_norm, double* const* v_dev, const StepExtra* ex);
+    template <class T>
+    void flow_step_packed(int64_t n, const DevSample* samples, const double* text_dev, int64_t L, double fps,
+                          double* loss, double* grad_norm, double* const* v_dev);
+    void adamw_step(cudaStream_t s);
     void stage_samples(int64_t n, const mgv_flow_sample* samples, std::vector<DevSample>& ds,
                        std::vector<void*>& allocs);
     template <class Alloc>
@@ -248,6 +255,7 @@ private:
     cudaStream_t stream_ = nullptr;
     Cfg cfg_;
     bool have_params_ = false;
+    bool varlen_ = false;
     std::map<std::string, DevParam> params_;
     std::vector<DevParam*> sorted_;
     float* grad_buf_ = nullptr;
