@@ -500,17 +500,23 @@ def extra_configs(ctx, args):
         samples.append(FlowSample(d, co, rng.uniform(-1, 1, (nn, PATCH)), rng.standard_normal((nn, PATCH)),
                                   float(rng.uniform(0.05, 0.95)), cond))
     tot = sum(s.clean_rows.shape[0] for s in samples)
-    ctx.flow_step(samples, text, 8.0)
-    ts = []
-    for _ in range(max(3, args.steps)):
-        t0 = time.perf_counter()
+    for packed in (True, False):
+        ctx.set_varlen(packed)
         ctx.flow_step(samples, text, 8.0)
-        ts.append(time.perf_counter() - t0)
-    ms = 1000 * statistics.median(ts)
-    out["cfg4_varlen_mixed"] = {"workload": "flow step fwd+bwd over 4 x (7,30,52) clips + 4 x (1,45,80) images "
-                                            f"= {tot} tokens, first-frame conditioning p=0.3, samples run as batches of one",
-                                "tokens_per_s": tot / (ms / 1000), "ms": ms,
-                                "timing": "wall clock around the C-ABI call, host buffers (e2e)"}
+        ts = []
+        for _ in range(max(3, args.steps)):
+            t0 = time.perf_counter()
+            ctx.flow_step(samples, text, 8.0)
+            ts.append(time.perf_counter() - t0)
+        ms = 1000 * statistics.median(ts)
+        key = "cfg4_varlen_mixed" if packed else "cfg4_sequential"
+        how = ("ONE packed step: 256-row-aligned segments, block-diagonal attention (mgv_ctx_set_varlen)" if packed
+               else "samples run one after another (varlen off)")
+        out[key] = {"workload": "flow step fwd+bwd over 4 x (7,30,52) clips + 4 x (1,45,80) images "
+                                f"= {tot} tokens, first-frame conditioning p=0.3, {how}",
+                    "tokens_per_s": tot / (ms / 1000), "ms": ms,
+                    "timing": "wall clock around the C-ABI call, host buffers (e2e)"}
+    ctx.set_varlen(False)
     return out
 
 

@@ -145,6 +145,7 @@ void global_embed_bwd(const double* dg, int n_u, const double* phi, const double
                       cudaStream_t s);
 // sum of squares of a fp32 buffer into out (double), fixed order
 void sumsq(const float* x, int64_t n, double* part /*>= 1024*/, double* out, cudaStream_t s);
+void fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t s);
 void fill_f32(float* p, int64_t n, float v, cudaStream_t s);
 // out[c * ld_out + r] = in[r * ld_in + c] for r < rows, c < cols (bf16; attention operand transposes)
 void transpose_bf16(const __nv_bfloat16* in, int64_t ld_in, int rows, int cols, __nv_bfloat16* out, int64_t ld_out,

@@ -517,7 +517,19 @@ void sum_double(const double* part, int n, double* out, cudaStream_t s) {
 }
 
 // ============================================================ backward row kernels
-constexpr int MAXU = 2;  // distinct modulation rows in the backward (tau = t and tau = 0)
+constexpr int MAXU = 2;  // distinct modulation rows per 64-row chunk (tau = t and tau = 0)
+
+// The (at most two) modulation-table rows of chunk [r0, r1): ua = the first row's, ub = the other one (= ua when
+// the chunk has one).  An unpacked sample uses rows {0, 1}; a varlen-packed batch (Model::flow_step_packed) uses
+// {k, B} inside sample k's 256-row-aligned segment (its padding rows take k), so no 64-row chunk sees a third.
+__device__ __forceinline__ void chunk_rows(const int32_t* mod_id, int r0, int r1, int& ua, int& ub) {
+    ua = mod_id[r0];
+    ub = ua;
+    for (int i = r0 + 1; i < r1; ++i) {
+        const int u = mod_id[i];
+        if (u != ua) ub = u;
+    }
+}
 
 template <class T>
 __global__ void __launch_bounds__(RT) gate_bwd_kernel(const float* dX, const T* y, const float* table, int64_t tld,
@@ -531,6 +543,8 @@ __global__ void __launch_bounds__(RT) gate_bwd_kernel(const float* dX, const T* 
 #pragma unroll
         for (int u = 0; u < MAXU; ++u) pg[u][c] = 0.0f;
     }
+    int ua, ub;
+    chunk_rows(mod_id, r0, r1, ua, ub);
     for (int i = r0; i < r1; ++i) {
         const int u = mod_id[i];
         const float* gt = table + (int64_t)u * tld + gate_off;
@@ -544,9 +558,10 @@ __global__ void __launch_bounds__(RT) gate_bwd_kernel(const float* dX, const T* 
                 dY[e] = to_t<T>(d);
                 pb[c] += d;
                 const float gg = dx * to_f(y[e]);
-#pragma unroll
-                for (int uu = 0; uu < MAXU; ++uu)
-                    if (uu == u) pg[uu][c] += gg;
+                if (u == ua)
+                    pg[0][c] += gg;
+                else
+                    pg[1][c] += gg;
             }
         }
     }
@@ -555,7 +570,9 @@ __global__ void __launch_bounds__(RT) gate_bwd_kernel(const float* dX, const T* 
         const int j = threadIdx.x + c * RT;
         if (j < H) {
             part_db[(int64_t)blockIdx.x * H + j] = pb[c];
-            for (int u = 0; u < n_u; ++u) part_dgate[((int64_t)blockIdx.x * n_u + u) * H + j] = pg[u < MAXU ? u : 0][c];
+            for (int u = 0; u < n_u; ++u)
+                part_dgate[((int64_t)blockIdx.x * n_u + u) * H + j] =
+                    u == ua ? pg[0][c] : (u == ub ? pg[1][c] : 0.0f);
         }
     }
 }
@@ -563,7 +580,7 @@ template <class T>
 void gate_bwd(const float* dX, const T* y, const float* table, int64_t tld, int gate_off, const int32_t* mod_id,
               int n_u, int N, int H, T* dY, float* part_dgate, float* part_db, cudaStream_t s) {
     if constexpr (is_bf16<T>()) {
-        if (use_vec(H) && n_u <= 2)
+        if (use_vec(H))
             return gate_bwd_vec_launch(dX, y, table, tld, gate_off, mod_id, n_u, N, H, dY, part_dgate, part_db, s);
     }
     gate_bwd_kernel<T><<<row_chunks(N), RT, 0, s>>>(dX, y, table, tld, gate_off, mod_id, n_u, N, H, dY, part_dgate,
@@ -584,8 +601,11 @@ __global__ void __launch_bounds__(RT) rms_bwd_kernel(const T* dA, const float* X
     for (int c = 0; c < MAXC; ++c)
 #pragma unroll
         for (int u = 0; u < MAXU; ++u) pa[u][c] = pbv[u][c] = 0.0f;
+    int ua = 0, ub = 0;
+    if (MODE == 0) chunk_rows(mod_id, r0, r1, ua, ub);
     for (int i = r0; i < r1; ++i) {
         const int u = MODE == 0 ? mod_id[i] : 0;
+        const int slot = u == ua ? 0 : 1;
         const float* tb = MODE == 0 ? table + (int64_t)u * tld : nullptr;
         const float rr = r[i];
         float xv[MAXC], dn[MAXC];
@@ -604,7 +624,7 @@ __global__ void __launch_bounds__(RT) rms_bwd_kernel(const T* dA, const float* X
                     dn[c] = da * (1.0f + tb[sc_off + j]);
 #pragma unroll
                     for (int uu = 0; uu < MAXU; ++uu)
-                        if (uu == u) {
+                        if (uu == slot) {
                             pa[uu][c] += da;       // d shift
                             pbv[uu][c] += da * n;  // d scale
                         }
@@ -633,8 +653,8 @@ __global__ void __launch_bounds__(RT) rms_bwd_kernel(const T* dA, const float* X
         if (j < H) {
             if (MODE == 0) {
                 for (int u = 0; u < n_u; ++u) {
-                    part_a[((int64_t)blockIdx.x * n_u + u) * H + j] = pa[u < MAXU ? u : 0][c];
-                    part_b[((int64_t)blockIdx.x * n_u + u) * H + j] = pbv[u < MAXU ? u : 0][c];
+                    part_a[((int64_t)blockIdx.x * n_u + u) * H + j] = u == ua ? pa[0][c] : (u == ub ? pa[1][c] : 0.0f);
+                    part_b[((int64_t)blockIdx.x * n_u + u) * H + j] = u == ua ? pbv[0][c] : (u == ub ? pbv[1][c] : 0.0f);
                 }
             } else {
                 part_a[(int64_t)blockIdx.x * H + j] = pa[0][c];
@@ -647,7 +667,7 @@ void rms_mod_bwd(const T* dA, const float* X, const float* r, const float* table
                  const int32_t* mod_id, int n_u, int N, int H, float* dX, float* part_dsh, float* part_dsc,
                  cudaStream_t s) {
     if constexpr (is_bf16<T>()) {
-        if (use_vec(H) && n_u <= 2)
+        if (use_vec(H))
             return rms_bwd_vec_launch(0, dA, X, r, table, tld, sc_off, mod_id, n_u, nullptr, N, H, dX, 1, part_dsh,
                                       part_dsc, s);
     }
@@ -885,7 +905,7 @@ __global__ void mod_wgrad_rows_kernel(const float* dm, const double* gb, int n_u
         db[k] += static_cast<float>(b);
     }
 }
-// out[r, j] = sum_k in[r, k] W[k, j] for R <= 3 rows, fp64 accumulation, split over K:
+// out[r, j] = sum_k in[r, k] W[k, j] for R <= 3 rows per launch, fp64 accumulation, split over K:
 // thread = column j of one K-slice; all rows share each W read.  part[ks][r][j], then a
 // fixed-order reduce over the slices (deterministic).
 constexpr int VM_KS = 48;
@@ -928,11 +948,17 @@ __global__ void vecmat_reduce_kernel(const double* part, int rows, int J, const 
 template <class TI>
 static void vecmat(const TI* in, int64_t in_ld, int rows, const float* W, int K, int J, const double* z, double* out,
                    cudaStream_t s) {
-    if (rows > 3) throw std::runtime_error("vecmat: at most 3 rows");
     double* part = nullptr;
     MGV_CUDA(cudaMallocAsync(&part, sizeof(double) * VM_KS * 3 * (size_t)J, s));
-    vecmat_part_kernel<TI, 3><<<dim3((J + 255) / 256, VM_KS), 256, 0, s>>>(in, in_ld, rows, W, K, J, part); ::mgv::note_launch();
-    vecmat_reduce_kernel<3><<<(J + 255) / 256, 256, 0, s>>>(part, rows, J, z, out); ::mgv::note_launch();
+    for (int r0 = 0; r0 < rows; r0 += 3) {  // row blocks of 3 (a packed batch has one timestep row per sample)
+        const int rb = rows - r0 < 3 ? rows - r0 : 3;
+        vecmat_part_kernel<TI, 3><<<dim3((J + 255) / 256, VM_KS), 256, 0, s>>>(in + (int64_t)r0 * in_ld, in_ld, rb, W,
+                                                                                K, J, part);
+        ::mgv::note_launch();
+        vecmat_reduce_kernel<3><<<(J + 255) / 256, 256, 0, s>>>(part, rb, J, z ? z + (int64_t)r0 * J : nullptr,
+                                                                 out + (int64_t)r0 * J);
+        ::mgv::note_launch();
+    }
     MGV_CUDA(cudaFreeAsync(part, s));
     MGV_CUDA(cudaGetLastError());
 }
@@ -1038,6 +1064,13 @@ void sumsq(const float* x, int64_t n, double* part, double* out, cudaStream_t s)
 }
 __global__ void fill_kernel(float* p, int64_t n, float v) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) p[e] = v;
+}
+__global__ void fill_i32_kernel(int32_t* p, int64_t n, int32_t v) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) p[e] = v;
+}
+void fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t s) {
+    fill_i32_kernel<<<grid_for(n), 256, 0, s>>>(p, n, v); ::mgv::note_launch();
+    MGV_CUDA(cudaGetLastError());
 }
 void fill_f32(float* p, int64_t n, float v, cudaStream_t s) {
     fill_kernel<<<grid_for(n), 256, 0, s>>>(p, n, v); ::mgv::note_launch();
@@ -1352,6 +1385,8 @@ __global__ void __launch_bounds__(RT) gate_bwd_vec(const float* __restrict__ dX,
     for (int k = 0; k < VG; ++k)
 #pragma unroll
         for (int e = 0; e < 8; ++e) pg[0][k][e] = pg[1][k][e] = pb[k][e] = 0.0f;
+    int ua, ub;
+    chunk_rows(mod_id, r0, r1, ua, ub);
 #pragma unroll 2  // restrict + two rows in flight: the next row's loads issue before this row's stores
     for (int i = r0; i < r1; ++i) {
         const int u = mod_id[i];
@@ -1369,7 +1404,7 @@ __global__ void __launch_bounds__(RT) gate_bwd_vec(const float* __restrict__ dX,
                 d[e] = dx[e] * gg[e];
                 pb[k][e] += d[e];
                 const float t = dx[e] * yy[e];
-                if (u == 0) pg[0][k][e] += t; else pg[1][k][e] += t;
+                if (u == ua) pg[0][k][e] += t; else pg[1][k][e] += t;
             }
             st8(dY + (int64_t)i * H + grp * 8, d);
         }
@@ -1379,8 +1414,10 @@ __global__ void __launch_bounds__(RT) gate_bwd_vec(const float* __restrict__ dX,
         const int grp = threadIdx.x + k * RT;
         if (grp >= G) continue;
         st8(part_db + (int64_t)blockIdx.x * H + grp * 8, pb[k]);
-        st8(part_dgate + ((int64_t)blockIdx.x * n_u + 0) * H + grp * 8, pg[0][k]);
-        if (n_u > 1) st8(part_dgate + ((int64_t)blockIdx.x * n_u + 1) * H + grp * 8, pg[1][k]);
+        float zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int u = 0; u < n_u; ++u)
+            st8(part_dgate + ((int64_t)blockIdx.x * n_u + u) * H + grp * 8,
+                u == ua ? pg[0][k] : (u == ub ? pg[1][k] : zero));
     }
 }
 
@@ -1398,6 +1435,8 @@ __global__ void __launch_bounds__(RT, 2) rms_bwd_vec(const bf* dA, const float* 
     for (int k = 0; k < VG; ++k)
 #pragma unroll
         for (int e = 0; e < 8; ++e) pa[0][k][e] = pa[1][k][e] = pb[0][k][e] = pb[1][k][e] = 0.0f;
+    int ua = 0, ub = 0;
+    if (MODE == 0) chunk_rows(mod_id, r0, r1, ua, ub);
     for (int i = r0; i < r1; i += R) {
         float xv[R][VG][8], dn[R][VG][8], dot[R];
         // the next row group: start its rows into L2 while this group reduces (block barrier below)
@@ -1436,7 +1475,7 @@ __global__ void __launch_bounds__(RT, 2) rms_bwd_vec(const bf* dA, const float* 
                         const float n = xv[rr][k][e] * rstd;
                         if (MODE == 0) {
                             dn[rr][k][e] = da[e] * (1.0f + t[e]);
-                            if (u == 0) {
+                            if (u == ua) {
                                 pa[0][k][e] += da[e];
                                 pb[0][k][e] += da[e] * n;
                             } else {
@@ -1482,11 +1521,12 @@ __global__ void __launch_bounds__(RT, 2) rms_bwd_vec(const bf* dA, const float* 
         const int grp = threadIdx.x + k * RT;
         if (grp >= G) continue;
         if (MODE == 0) {
-            st8(part_a + ((int64_t)blockIdx.x * n_u + 0) * H + grp * 8, pa[0][k]);
-            st8(part_b + ((int64_t)blockIdx.x * n_u + 0) * H + grp * 8, pb[0][k]);
-            if (n_u > 1) {
-                st8(part_a + ((int64_t)blockIdx.x * n_u + 1) * H + grp * 8, pa[1][k]);
-                st8(part_b + ((int64_t)blockIdx.x * n_u + 1) * H + grp * 8, pb[1][k]);
+            float zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int u = 0; u < n_u; ++u) {
+                st8(part_a + ((int64_t)blockIdx.x * n_u + u) * H + grp * 8,
+                    u == ua ? pa[0][k] : (u == ub ? pa[1][k] : zero));
+                st8(part_b + ((int64_t)blockIdx.x * n_u + u) * H + grp * 8,
+                    u == ua ? pb[0][k] : (u == ub ? pb[1][k] : zero));
             }
         } else {
             st8(part_a + (int64_t)blockIdx.x * H + grp * 8, pa[0][k]);

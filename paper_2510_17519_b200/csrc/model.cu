@@ -189,8 +189,9 @@ void layout_ws(Model::WS& w, S& a, const Cfg& c, bool grads) {
         w.s2 = a.takeT(N * H, e);
         w.dkv = a.takeT(R * L * 2 * Hr, e);
         w.Dvec = a.template take<float>(((N + 127) / 128 * 128) * nh);
-        w.part1 = a.template take<float>((int64_t)chunks * std::max<int64_t>(4 * H, 2 * H));
-        w.part2 = a.template take<float>((int64_t)chunks * std::max<int64_t>(4 * H, 2 * H));
+        // column partials: up to 4H wide, or one H-wide row per modulation-table row (n_u, a packed batch: B + 1)
+        w.part1 = a.template take<float>((int64_t)chunks * std::max<int64_t>(4 * H, (int64_t)nu * H));
+        w.part2 = a.template take<float>((int64_t)chunks * std::max<int64_t>(4 * H, (int64_t)nu * H));
         w.q_splits_x = static_cast<int>(std::min<int64_t>(64, (N + 31) / 32));
         w.dkv_part = a.template take<float>((int64_t)w.q_splits_x * nh * L * 2 * hd);
         w.dm = a.template take<float>(nu * 6 * H);
@@ -1644,6 +1645,8 @@ void Model::flow_step_packed(int64_t n, const DevSample* samples, const double* 
         taus[static_cast<size_t>(k)] = sm.t;
         MGV_CUDA(cudaMemcpyAsync(w.coords + 3 * base[k], sm.coords, sizeof(int32_t) * 3 * sm.N, cudaMemcpyDeviceToDevice,
                                  s));
+        if (base[k + 1] > base[k] + sm.N)  // padding rows: this sample's tau = t row (<= 2 rows per 64-row chunk)
+            fill_i32(w.mod_id + base[k] + sm.N, base[k + 1] - base[k] - sm.N, static_cast<int>(k), s);
         prep_flow_sample<T>(sm.clean, sm.noise, sm.cond, sm.cond_lat, static_cast<int>(sm.N), int(D), sm.t,
                             tp<T>(off<T>(w.rows, base[k] * D)), w.vt + base[k] * D, w.lmask + base[k],
                             w.mod_id + base[k], s, static_cast<int>(k), static_cast<int>(n));
@@ -2021,6 +2024,16 @@ void Model::velocity_graph_impl(const double* rows, int64_t N, const int32_t* co
     std::vector<double> uniq;
     std::vector<int32_t> mid;
     dedup_taus(tau, N, uniq, mid);
+    if (dV)  // the backward row kernels keep two modulation rows per 64-token chunk (kernels_elem.cu chunk_rows)
+        for (int64_t r0 = 0; r0 < N; r0 += kRowsPerChunk) {
+            int a = mid[static_cast<size_t>(r0)], b = a;
+            for (int64_t i = r0; i < std::min<int64_t>(N, r0 + kRowsPerChunk); ++i) {
+                const int u = mid[static_cast<size_t>(i)];
+                if (u != a && u != b && b != a) throw InputError("the device backward takes at most two distinct "
+                                                                 "timesteps per 64 consecutive tokens");
+                if (u != a) b = u;
+            }
+        }
     w.N = N;
     w.L = L;
     w.n_u = static_cast<int>(uniq.size());
