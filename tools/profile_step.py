@@ -17,7 +17,8 @@ args = ap.parse_args()
 grid = tuple(int(x) for x in args.grid.split(","))
 cfg = paper_config(depth=1)
 ctx = Context(0, "bf16")
-ctx.upload(cfg, bench.synthetic_params(cfg, 1234))
+gs = 0.2 * (12.0 / cfg.hidden) ** 0.5
+ctx.init_params(cfg, seed=1, gate_seed=2, gate_std=gs, gate_b_std=gs / 4)
 N = grid[0] * grid[1] * grid[2]
 rng = np.random.default_rng(0)
 d_clean = torch.tensor(rng.uniform(-1, 1, (N, 96)), device="cuda")

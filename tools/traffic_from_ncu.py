@@ -23,7 +23,9 @@ by = lambda v: v.get("dram__bytes_read.sum", 0.0) + v.get("dram__bytes_write.sum
 fwd = [v for k, v in big if "attn_fwd" in k[1] and "(225, 24" in k[2]]
 bwd_idx = [i for i, (k, v) in enumerate(big) if "attn_bwd_dkv" in k[1] and "(450, 24" in k[2]][0]
 bwd = [v for k, v in big[bwd_idx - 5:bwd_idx + 2]]
+parts = {k[1].split("(")[0].split("<")[0].replace("void ", "").strip(): by(v) for k, v in big[bwd_idx - 5:bwd_idx + 2]}
 fwd_t = [v for k, v in big[:big.index(next(x for x in big if "attn_fwd" in x[0][1]))] if "(54, 900" in k[2]]
 out = {"attn_fwd": by(fwd[0]) + (by(fwd_t[-1]) if fwd_t else 0.0), "attn_bwd": sum(by(v) for v in bwd),
+       "attn_bwd_parts": parts,
        "unit": "bytes per launch (DRAM read + write, ncu, cold cache)", "source": sys.argv[1]}
 print(json.dumps(out, indent=1))
