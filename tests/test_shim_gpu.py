@@ -51,3 +51,15 @@ def test_reference_suite_through_shim(suite):
     assert res, out[-3000:]
     bad = [k for k, v in res.items() if v != "ok" and k not in EXPECTED_FAIL]
     assert not bad, (bad, out[-6000:])
+
+
+@pytest.mark.gpu
+def test_device_flow_trainer_matches_reference_trainer():
+    """shim/test_device_trainer.cpp: mugv::b200::DeviceFlowTrainer (whole step + AdamW on the device, one context
+    per trainer, weights uploaded once) against the reference FlowTrainer over three steps."""
+    exe = os.path.join(BUILD, "test_device_trainer")
+    if not os.path.exists(exe):
+        pytest.skip("shim/_build not built")
+    out, res = run_suite(exe)
+    print(out[-2000:])
+    assert res and all(v == "ok" for v in res.values()), out[-3000:]
