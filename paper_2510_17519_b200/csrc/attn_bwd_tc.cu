@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int h = blockIdx.y, k0 = blockIdx.x * BKV;
     // packed segments (AttnProblem::seg): this key tile's segment [qlo, qend) is also its query range; keys at or
-    // past qend are padding rows (P = 0)
+    // past qend are padding rows (their dK / dV rows are written as zeros)
     const int qlo = f.seg ? f.seg[2 * (k0 / 128)] : 0, qend = f.seg ? f.seg[2 * (k0 / 128) + 1] : f.Nq;
     const int kend = f.seg ? qend : f.Nk;
     const int nq_all = (qend - qlo + BQ - 1) / BQ;
@@ -444,12 +444,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
             const bool full = qb + 64 <= qend;
             uint32_t pk[32];
             const float2 lg2 = make_float2(kLog2e, kLog2e);
-            if (!kreal) {  // a padding key row of a packed segment
-#pragma unroll
-                for (int c = 0; c < 64; ++c) s[c] = 0.0f;
-#pragma unroll
-                for (int c = 0; c < 32; ++c) pk[c] = 0u;
-            } else if (full) {  // warp-uniform: no per-column masking; packed f32x2 arithmetic (bit-identical to scalar)
+            if (full) {  // warp-uniform: no per-column masking; packed f32x2 arithmetic (bit-identical to scalar)
 #pragma unroll
                 for (int c4 = 0; c4 < 64; c4 += 4) {
                     const float4 l = lds_f4(lse_s + c4 * 4);
@@ -525,7 +520,13 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
         } else {
             __nv_bfloat16* out = hf == 0 ? static_cast<__nv_bfloat16*>(p.dv) + (int64_t)kv * p.dv_ld + col
                                          : static_cast<__nv_bfloat16*>(p.dk) + (int64_t)kv * p.dk_ld + col;
-            store_acc_row<HD>(tmem + lane_base + (hf ? DK_COL : DV_COL), out, valid);
+            // every lane runs the (warp-collective) TMEM loads; a padding key row of a packed segment stores zeros
+            store_acc_row<HD>(tmem + lane_base + (hf ? DK_COL : DV_COL), out, valid && kreal);
+            if (valid && !kreal) {
+                const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll 1
+                for (int c = 0; c < HD / 8; ++c) reinterpret_cast<uint4*>(out)[c] = z;
+            }
         }
     }
     tc_fence_before();
@@ -784,7 +785,7 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
         ensure_smem(attn_bwd_dkv_v11_kernel<HD>, smem);
         // few key tiles (cross-attention): split the query range so the grid still covers the SMs
         const int kv_ctas = (f.Nk + 127) / 128 * f.heads, nq_all = (f.Nq + 127) / 128;
-        const int splits = std::max(1, std::min({num_sms() / std::max(kv_ctas, 1), nq_all / 8, 16}));
+        const int splits = f.seg ? 1 : std::max(1, std::min({num_sms() / std::max(kv_ctas, 1), nq_all / 8, 16}));
         float* part = nullptr;
         if (splits > 1) MGV_CUDA(cudaMallocAsync(&part, sizeof(float) * splits * f.Nk * 2 * W, s));
         attn_bwd_dkv_v11_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem, s>>>(m, p, part);
