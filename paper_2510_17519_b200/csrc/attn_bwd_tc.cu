@@ -278,10 +278,13 @@ __device__ __forceinline__ void mma_tmem128_x_t(uint32_t d, uint32_t a_tmem, uin
                     id, (acc_first || ks > 0) ? 1u : 0u);
 }
 
-template <int HD>
-__global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_constant__ BwdMaps tm,
-                                                                  AttnBwdProblem p, float* part) {
-    constexpr int BKV = 128, BQ = 128, NST = 2;
+// CW: compute warps per TMEM lane group (each owns 128 / CW query columns of a step).  CW = 4 (640 threads, 95
+// registers) measured 71.6 ms against 70.3 for CW = 2 at 57,600 tokens (profiles/r02/attn_bwd_cw_poly_r02.log)
+template <int HD, int CW>
+__global__ void __launch_bounds__(128 + 128 * CW, 1) attn_bwd_dkv_v11_kernel(const __grid_constant__ BwdMaps tm,
+                                                                           AttnBwdProblem p, float* part) {
+    constexpr int BKV = 128, BQ = 128, NST = 2, QW = BQ / CW;
+    static_assert(CW == 2 || CW == 4, "2 or 4 compute warps per lane group");
     using T = BT<HD>;
     constexpr int HDP = ((HD + 15) / 16) * 16;
     constexpr int SD_COL = 0, PT_COL = 128, DV_COL = 192, DK_COL = DV_COL + HDP;
@@ -331,12 +334,12 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
             mbar_init(&qd_empty[i], 1);
         }
         mbar_init(s_full, 1);
-        mbar_init(s_loaded, 8);
+        mbar_init(s_loaded, 4 * CW);
         mbar_init(dp_full, 1);
-        mbar_init(dp_loaded, 8);
-        mbar_init(p_full, 8);
+        mbar_init(dp_loaded, 4 * CW);
+        mbar_init(p_full, 4 * CW);
         mbar_init(pv_done, 1);
-        mbar_init(ds_full, 8);
+        mbar_init(ds_full, 4 * CW);
         mbar_init(dk_done, 1);
         mbar_init(acc_done, 1);
         fence_barrier_init();
@@ -418,35 +421,35 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
             __syncwarp();
         }
     } else if (warp >= 4) {
-        // two warps per TMEM lane group: warp half hf owns query columns [64 hf, 64 hf + 64) of each step
+        // CW warps per TMEM lane group: warp hf owns query columns [QW hf, QW hf + QW) of each step
         const int g = warp & 3, hf = (warp - 4) >> 2, row = g * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(g * 32) << 16;
         const int kv = k0 + row;
         const bool kvv = kv < f.Nk, kreal = kv < kend;
-        const uint32_t sd = tmem + lane_base + SD_COL + hf * 64, pt = tmem + lane_base + PT_COL + hf * 32;
+        const uint32_t sd = tmem + lane_base + SD_COL + hf * QW, pt = tmem + lane_base + PT_COL + hf * (QW / 2);
         for (int i = 0; i < nq; ++i) {
             const int st = i % NST;
             mbar_wait(&qd_full[st], (i / NST) & 1);  // lse / D rows of this step have landed
             mbar_wait(s_full, i & 1);
             tc_fence_after();
             if (warp == 4 && lane == 0) ATR8(4, i);
-            float s[64];
-            tmem_ld32(sd, reinterpret_cast<uint32_t*>(s));
-            tmem_ld32(sd + 32, reinterpret_cast<uint32_t*>(s + 32));
+            float s[QW];
+#pragma unroll
+            for (int c = 0; c < QW; c += 32) tmem_ld32(sd + c, reinterpret_cast<uint32_t*>(s + c));
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(s_loaded);
             // lse / D rows: 16-byte shared-memory broadcasts (one wavefront per 4 queries per warp); per-element
             // generic loads made the compute warps' shared wavefronts outnumber the SS MMAs' operand reads
-            const uint32_t lse_s = smem_u32(sLse + st * BQ + hf * 64), d_s = smem_u32(sD + st * BQ + hf * 64);
-            const int qb = (i0 + i) * BQ + hf * 64;
-            const bool full = qb + 64 <= qend;
-            uint32_t pk[32];
+            const uint32_t lse_s = smem_u32(sLse + st * BQ + hf * QW), d_s = smem_u32(sD + st * BQ + hf * QW);
+            const int qb = (i0 + i) * BQ + hf * QW;
+            const bool full = qb + QW <= qend;
+            uint32_t pk[QW / 2];
             const float2 lg2 = make_float2(kLog2e, kLog2e);
             if (full) {  // warp-uniform: no per-column masking; packed f32x2 arithmetic (bit-identical to scalar)
 #pragma unroll
-                for (int c4 = 0; c4 < 64; c4 += 4) {
+                for (int c4 = 0; c4 < QW; c4 += 4) {
                     const float4 l = lds_f4(lse_s + c4 * 4);
                     const float2 x0 = fmul2(fsub2(make_float2(s[c4], s[c4 + 1]), make_float2(l.x, l.y)), lg2);
                     const float2 x1 = fmul2(fsub2(make_float2(s[c4 + 2], s[c4 + 3]), make_float2(l.z, l.w)), lg2);
@@ -459,7 +462,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
                 }
             } else {
 #pragma unroll
-                for (int c4 = 0; c4 < 64; c4 += 4) {
+                for (int c4 = 0; c4 < QW; c4 += 4) {
                     const float4 l = lds_f4(lse_s + c4 * 4);
                     const float lv[4] = {l.x, l.y, l.z, l.w};
 #pragma unroll
@@ -475,7 +478,10 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
                 mbar_wait(dk_done, (i - 1) & 1);  // dK(i-1) has read dS^T(i-1) out of PT
                 tc_fence_after();
             }
-            tmem_st32(pt, pk);
+            if constexpr (QW == 64)
+                tmem_st32(pt, pk);
+            else
+                tmem_st16(pt, pk);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
@@ -484,15 +490,15 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
             mbar_wait(dp_full, i & 1);
             tc_fence_after();
             if (warp == 4 && lane == 0) ATR8(6, i);
-            float dp[64];
-            tmem_ld32(sd, reinterpret_cast<uint32_t*>(dp));
-            tmem_ld32(sd + 32, reinterpret_cast<uint32_t*>(dp + 32));
+            float dp[QW];
+#pragma unroll
+            for (int c = 0; c < QW; c += 32) tmem_ld32(sd + c, reinterpret_cast<uint32_t*>(dp + c));
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(dp_loaded);  // S^T(i+1) may now overwrite SD, under the dS math below
 #pragma unroll
-            for (int c = 0; c < 64; c += 4) {  // dS = P (dP - D) (autodiff.cpp:820), packed pairs
+            for (int c = 0; c < QW; c += 4) {  // dS = P (dP - D) (autodiff.cpp:820), packed pairs
                 const float4 dd = lds_f4(d_s + c * 4);
                 const float2 d0 = fmul2(make_float2(s[c], s[c + 1]),
                                         fsub2(make_float2(dp[c], dp[c + 1]), make_float2(dd.x, dd.y)));
@@ -504,7 +510,10 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
             mbar_wait(pv_done, i & 1);  // dV(i) has read P^T(i) out of PT
             tc_fence_after();
             if (warp == 4 && lane == 0) ATR8(7, i);
-            tmem_st32(pt, pk);
+            if constexpr (QW == 64)
+                tmem_st32(pt, pk);
+            else
+                tmem_st16(pt, pk);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
@@ -514,18 +523,23 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dkv_v11_kernel(const __grid_c
         tc_fence_after();
         const bool valid = kvv && nq > 0;
         if (part) {  // fp32 partial rows of this query split: [dV | dK]
-            const int64_t W = (int64_t)f.heads * HD;
-            float* prow = part + ((int64_t)blockIdx.z * f.Nk + (kvv ? kv : 0)) * 2 * W + (hf ? W : 0) + col;
-            store_acc_row_f32<HD>(tmem + lane_base + (hf ? DK_COL : DV_COL), prow, kvv);
-        } else {
-            __nv_bfloat16* out = hf == 0 ? static_cast<__nv_bfloat16*>(p.dv) + (int64_t)kv * p.dv_ld + col
-                                         : static_cast<__nv_bfloat16*>(p.dk) + (int64_t)kv * p.dk_ld + col;
+            if (hf < 2) {
+                const int64_t W = (int64_t)f.heads * HD;
+                float* prow = part + ((int64_t)blockIdx.z * f.Nk + (kvv ? kv : 0)) * 2 * W + (hf ? W : 0) + col;
+                store_acc_row_f32<HD>(tmem + lane_base + (hf ? DK_COL : DV_COL), prow, kvv);
+            }
+        } else {  // warps [0, CW/2) store dV, the others dK, each a share of the 16-column chunks
+            constexpr int NC = HD / 16, HALF = CW / 2;
+            const bool is_v = hf < HALF;
+            const int part_i = is_v ? hf : hf - HALF, c0 = part_i * NC / HALF, c1 = (part_i + 1) * NC / HALF;
+            __nv_bfloat16* out = is_v ? static_cast<__nv_bfloat16*>(p.dv) + (int64_t)kv * p.dv_ld + col
+                                      : static_cast<__nv_bfloat16*>(p.dk) + (int64_t)kv * p.dk_ld + col;
             // every lane runs the (warp-collective) TMEM loads; a padding key row of a packed segment stores zeros
-            store_acc_row<HD>(tmem + lane_base + (hf ? DK_COL : DV_COL), out, valid && kreal);
+            store_acc_row<HD>(tmem + lane_base + (is_v ? DV_COL : DK_COL), out, valid && kreal, c0, c1);
             if (valid && !kreal) {
                 const uint4 z = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll 1
-                for (int c = 0; c < HD / 8; ++c) reinterpret_cast<uint4*>(out)[c] = z;
+                for (int c = 2 * c0; c < 2 * c1; ++c) reinterpret_cast<uint4*>(out)[c] = z;
             }
         }
     }
@@ -782,13 +796,13 @@ static void launch_bwd(const AttnBwdProblem& p, const void* qt, int64_t qt_ld, c
         make_tmap_sw(&m.ta, qt, f.Nq, W, qt_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
         make_tmap_sw(&m.tb, dot, f.Nq, W, dot_ld, 64, HD, CU_TENSOR_MAP_SWIZZLE_128B);
         const int smem = 2 * T::ROW_TILE + 4 * 2 * T::T_TILE + 4 * 128 * 4 + 256 + 1024;
-        ensure_smem(attn_bwd_dkv_v11_kernel<HD>, smem);
+        ensure_smem(attn_bwd_dkv_v11_kernel<HD, 2>, smem);
         // few key tiles (cross-attention): split the query range so the grid still covers the SMs
         const int kv_ctas = (f.Nk + 127) / 128 * f.heads, nq_all = (f.Nq + 127) / 128;
         const int splits = f.seg ? 1 : std::max(1, std::min({num_sms() / std::max(kv_ctas, 1), nq_all / 8, 16}));
         float* part = nullptr;
         if (splits > 1) MGV_CUDA(cudaMallocAsync(&part, sizeof(float) * splits * f.Nk * 2 * W, s));
-        attn_bwd_dkv_v11_kernel<HD><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem, s>>>(m, p, part);
+        attn_bwd_dkv_v11_kernel<HD, 2><<<dim3((f.Nk + 127) / 128, f.heads, splits), 384, smem, s>>>(m, p, part);
         ::mgv::note_launch();
         MGV_CUDA(cudaGetLastError());
         if (splits > 1) {
