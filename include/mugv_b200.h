@@ -109,11 +109,14 @@ mgv_status mgv_ctx_set_stream(mgv_ctx* ctx, void* stream);
 mgv_status mgv_nccl_unique_id(uint8_t out[128]);
 mgv_status mgv_ctx_set_dp(mgv_ctx* ctx, int rank, int world, const uint8_t nccl_id[128]);
 /* Tensor parallel (Megatron head/column split); must precede mgv_params_upload.
- * nccl_id != NULL: this context is TP rank `rank` of `size` over NCCL (one all-reduce per residual
- * branch in forward and backward; sharded-parameter gradients are summed after the step, so every rank
- * returns the full gradients).  nccl_id == NULL: all `size` ranks are emulated in this context (same
- * shard views and partial sums, accumulated in place of the all-reduce) -- the single-GPU check of the
- * sharded path.  `size` must divide heads.  Not combinable with mgv_ctx_set_dp. */
+ * nccl_id != NULL: this context is TP rank `rank` of `size` over NCCL: it stores only its blocks of the
+ * sharded parameters and H/size-wide activations; one exchange per residual branch in forward and backward
+ * (NVLink peer memory fused into the row-parallel GEMM epilogue, or NCCL); no gradient all-reduce; the
+ * gradient norm is summed over the group; parameter / gradient downloads all-gather the blocks (collective).
+ * nccl_id == NULL: all `size` ranks are emulated in this context (every slot held, partial sums accumulated
+ * in place of the exchange) -- the single-GPU check of the sharded path.  `size` must divide heads.
+ * Combinable with mgv_ctx_set_dp (2-D: the DP communicator joins the ranks holding the same TP rank; the DP
+ * gradient all-reduce then runs once after the backward instead of in per-block buckets). */
 mgv_status mgv_ctx_set_tp(mgv_ctx* ctx, int size, int rank, const uint8_t* nccl_id);
 
 /* flow::forward_sample_rows (direction -1: Euler t 1 -> 0, x <- x - dt v) and flow::reverse_sample_rows

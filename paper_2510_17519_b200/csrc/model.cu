@@ -381,7 +381,6 @@ void Model::dp_finish(double* scal) {
 void Model::set_tp(int size, int rank, const uint8_t* id) {
     if (size < 1 || rank < 0 || rank >= size) throw InputError("bad tensor-parallel rank/size");
     if (have_params_ && size != tp_) throw ConfigError("set_tp must precede the parameter upload");
-    if (size > 1 && world_ > 1) throw ConfigError("data and tensor parallelism cannot be combined in one context");
     if (tp_comm_) {
         ncclCommDestroy(tp_comm_);
         tp_comm_ = nullptr;
@@ -1511,7 +1510,8 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
         if (backward && wk != 0.0) {
             flow_loss_bwd<T>(w.V, w.vt, w.lmask, N, int(D), static_cast<float>(2.0 * wk), w.cnt, tp<T>(w.dV),
                              s);  // 2 w_k (V - v*) / (n_b * D), w_k = 1 / B in FlowTrainer::step; all-masked -> 0
-            dp_overlap_ = comm_ != nullptr && !ex && k == n - 1;
+            // per-block buckets need each block's gradients contiguous: sorted names, i.e. no TP layout
+            dp_overlap_ = comm_ != nullptr && !ex && k == n - 1 && tp_ == 1;
             dp_done_.clear();
             backward_sample<T>(w.dV);
             dp_overlap_ = false;
@@ -1676,7 +1676,7 @@ void Model::flow_step_packed(int64_t n, const DevSample* samples, const double* 
                          static_cast<float>(2.0 / static_cast<double>(B_global)), w.cnt,
                          tp<T>(off<T>(w.dV, base[k] * D)), s);
     }
-    dp_overlap_ = comm_ != nullptr;
+    dp_overlap_ = comm_ != nullptr && tp_ == 1;
     dp_done_.clear();
     backward_sample<T>(w.dV);
     dp_overlap_ = false;

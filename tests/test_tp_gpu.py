@@ -111,3 +111,27 @@ def test_planner_matches_a_real_context(prec):
     print(prec, got, plan)
     for k in ("params", "grads", "adamw", "workspace"):
         assert got[k] == plan[k], (k, got[k], plan[k])
+
+
+def test_tp_with_dp_one_rank_communicator():
+    """2-D parallelism path on one GPU: emulated TP = 2 plus the DP NCCL path (one-rank communicator: gradient and
+    loss all-reduces of every step) gives bit-identical loss, gradients and AdamW weights to TP alone."""
+    from paper_2510_17519_b200.capi import Context
+    cfg, P, text, samples = build_case("hd144", CASES["hd144"])
+    outs = []
+    for dp in (False, True):
+        c = Context(0, "bf16")
+        if dp:
+            c.set_dp(0, 1, Context.nccl_unique_id())
+        c.set_tp(2)
+        c.set_adamw(lr=1e-3, eps=1.0)
+        c.upload(to_cfg(cfg), P)
+        for _ in range(2):
+            r = c.flow_step(to_samples(samples), text, 8.0, grads=True)
+        outs.append((r, c.download()))
+        c.close()
+    (a, wa), (b, wb) = outs
+    assert a["loss"] == b["loss"] and a["grad_norm"] == b["grad_norm"]
+    for k in a["grads"]:
+        assert np.array_equal(a["grads"][k], b["grads"][k]), k
+        assert np.array_equal(wa[k], wb[k]), k
