@@ -105,8 +105,9 @@ mgv_status mgv_ctx_set_stream(mgv_ctx* ctx, void* stream);
 
 /* Data parallel: rank r of `world` over NCCL; `nccl_id` is the 128-byte ncclUniqueId from rank 0.
  * mgv_flow_step then all-reduces gradients (sum) and scales the loss by 1/global_batch.  world 1 with an id
- * builds a one-rank communicator (the all-reduce path runs, as an identity). */
-mgv_status mgv_nccl_unique_id(uint8_t out[128]);
+ * builds a one-rank communicator (the all-reduce path runs, as an identity).  nccl_id NULL with world > 1: no
+ * communicator -- the step returns this rank's share (loss and gradients scaled by 1/global_batch, unreduced;
+ * their sum over the ranks is the global step; leave AdamW off in this mode). */
 mgv_status mgv_ctx_set_dp(mgv_ctx* ctx, int rank, int world, const uint8_t nccl_id[128]);
 /* Tensor parallel (Megatron head/column split); must precede mgv_params_upload.
  * nccl_id != NULL: this context is TP rank `rank` of `size` over NCCL: it stores only its blocks of the

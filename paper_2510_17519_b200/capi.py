@@ -674,8 +674,9 @@ class Context:
     def set_stream(self, stream_ptr: int):
         self._check(self._L.mgv_ctx_set_stream(self.h, stream_ptr))
 
-    def set_dp(self, rank: int, world: int, nccl_id: bytes):
-        buf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
+    def set_dp(self, rank: int, world: int, nccl_id: bytes | None):
+        """mgv_ctx_set_dp; nccl_id None with world > 1: this context computes one rank's unreduced share."""
+        buf = None if nccl_id is None else (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
         self._check(self._L.mgv_ctx_set_dp(self.h, rank, world, buf))
 
     def sample_rows(self, x_start, coords, dims, text, steps, direction=-1, fps=8.0, cond=None, cond_latents=None):

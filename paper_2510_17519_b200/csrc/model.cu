@@ -319,8 +319,11 @@ void Model::set_dp(int rank, int world, const uint8_t id[128]) {
     }
     rank_ = rank;
     world_ = world;
-    if (world == 1 && !id) return;  // world 1 with an id: a one-rank communicator (exercises the NCCL path)
-    if (!id) throw InputError("data parallelism needs the NCCL unique id");
+    // no id: no communicator.  world 1 is the plain context; world > 1 makes this context ONE rank's share of a
+    // data-parallel step (loss and gradients scaled by 1 / global batch, not reduced): the sum over the ranks
+    // is the global step, for external reducers and the decomposition test.  world 1 with an id: a one-rank
+    // communicator (exercises the NCCL path).
+    if (!id) return;
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
     MGV_CUDA(cudaSetDevice(device_));
