@@ -1,3 +1,7 @@
 O=gpurun_out/r22; mkdir -p $O
-MGV_ATTN_FWD1=1 timeout 600 python -m pytest tests/test_attn_gpu.py tests/test_varlen_gpu.py -q -x > $O/tests_fwd1.log 2>&1; echo "rc=$?" >> $O/tests_fwd1.log
-for r in 1 2 3; do for V in 0 1; do echo "== FWD1 $V $(MGV_ATTN_FWD1=$V timeout 150 python tools/probe_attn.py 57600 fwd 10 kernels 2>&1 | grep -iE 'attn fwd|attn_fwd' | tr '\n' ' ' | cut -c1-220)"; done; done > $O/ab_fwd.log
+timeout 1200 python tools/stack_train.py --depth 24 > $O/stack_train.log 2>&1; echo "rc=$?" >> $O/stack_train.log
+timeout 900 python tools/stack_fwd.py 2 > $O/stack_fwd.log 2>&1; echo "rc=$?" >> $O/stack_fwd.log
+timeout 600 python tools/tp_exchange.py --sizes 2 8 --steps 3 > $O/tp_exchange.log 2>&1; echo "rc=$?" >> $O/tp_exchange.log
+timeout 3000 python -m pytest tests -m gpu -q -rf > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
+timeout 900 python bench.py --steps 10 --warmup 3 > $O/bench.json 2> $O/bench.err
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log

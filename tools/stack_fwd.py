@@ -2,7 +2,7 @@
 through the C ABI at the 480p/2s (10,920 tokens) and 720p/5s (57,600 tokens) shapes -- BASELINE configs[3] at
 tensor-parallel size 1 (forward only: training all 56 blocks needs the TP split).
 
-Weights: one random-init block (bench.synthetic_params) shared by all 56 block names on the host, so host
+Weights: one block of init_dit_params + opened gates (tools/stack_common.py) shared by all 56 block names on the host, so host
 memory stays ~2 GB while the device holds 56 independent fp32 masters + bf16 copies (+ the fp32 gradient
 buffer the context allocates), ~110 GB.  Timing: wall clock around the C-ABI call with host fp64 buffers
 (the e2e figure), after one warm-up call.  Prints one JSON line.
@@ -18,16 +18,12 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2510_17519_b200.capi import Context, paper_config  # noqa: E402
+from tools.stack_common import shared_stack_params  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 DEPTH = 56
 cfg = paper_config(depth=DEPTH)
-one = bench.synthetic_params(paper_config(depth=1), seed=1234)
-params = {k: v for k, v in one.items() if not k.startswith("dit.blk.")}
-for i in range(DEPTH):
-    for k, v in one.items():
-        if k.startswith("dit.blk.0."):
-            params[f"dit.blk.{i}." + k[len("dit.blk.0."):]] = v
+params = shared_stack_params(DEPTH)
 n_params = sum(v.size for k, v in params.items())
 
 import torch  # noqa: E402

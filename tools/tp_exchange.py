@@ -24,11 +24,11 @@ def main():
     args = ap.parse_args()
     import numpy as np
     import torch
-    from bench import GRID, PATCH, TEXT_D, TEXT_L, grid_coords, synthetic_params
+    from bench import GRID, PATCH, TEXT_D, TEXT_L, grid_coords
     from paper_2510_17519_b200.capi import Context, mgv_flow_sample, paper_config
 
     cfg = paper_config(depth=1)
-    params = synthetic_params(cfg, seed=1234)
+    gs = 0.2 * (12.0 / cfg.hidden) ** 0.5  # SURVEY 8(d) weights: init_dit_params(Rng(1)) + gates from Rng(2)
     U, Hp, Wp = GRID
     N, H = U * Hp * Wp, cfg.hidden
     rng = np.random.default_rng(100)
@@ -48,7 +48,7 @@ def main():
             stream = torch.cuda.Stream()
             ctx.set_stream(stream.cuda_stream)
             ctx.set_tp(P)
-            ctx.upload(cfg, params)
+            ctx.init_params(cfg, seed=1, gate_seed=2, gate_std=gs, gate_b_std=gs / 4)
             step = lambda: ctx.flow_step_device(ds, d_text.data_ptr(), TEXT_L, 8.0)  # noqa: E731
             step()
             torch.cuda.synchronize()
