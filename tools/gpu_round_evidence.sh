@@ -5,5 +5,5 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 500 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv --log-file gpurun_out/launches_final.csv python bench.py --steps 2 --warmup 1 --no-extra --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_bwd_dkv_v8 --launch-skip 1 -c 1 -o gpurun_out/dkv_final -f python bench.py --steps 1 --warmup 0 --no-extra --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_bwd_dkv_v11 --launch-skip 1 -c 1 -o gpurun_out/dkv_final -f python bench.py --steps 1 --warmup 0 --no-extra --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
 echo all_done
