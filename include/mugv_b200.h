@@ -108,6 +108,7 @@ mgv_status mgv_ctx_set_stream(mgv_ctx* ctx, void* stream);
  * builds a one-rank communicator (the all-reduce path runs, as an identity).  nccl_id NULL with world > 1: no
  * communicator -- the step returns this rank's share (loss and gradients scaled by 1/global_batch, unreduced;
  * their sum over the ranks is the global step; leave AdamW off in this mode). */
+mgv_status mgv_nccl_unique_id(uint8_t out[128]);
 mgv_status mgv_ctx_set_dp(mgv_ctx* ctx, int rank, int world, const uint8_t nccl_id[128]);
 /* Tensor parallel (Megatron head/column split); must precede mgv_params_upload.
  * nccl_id != NULL: this context is TP rank `rank` of `size` over NCCL: it stores only its blocks of the
