@@ -37,7 +37,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "DiT-block video tokens/sec at 57.6K-token 10B shape; attention TFLOP/s vs peak"
-GRID = (16, 45, 80)  # token grid (U, H', W') of the 720p/5s latent (16, 90, 160, 24)
+GRID_720P = (16, 45, 80)  # token grid (U, H', W') of the 720p/5s latent (16, 90, 160, 24)
+GRID = GRID_720P
 H, HEADS, HD, TEXT_L, TEXT_D, PATCH = 3456, 24, 144, 64, 4096, 96
 # AdamW hyper-parameters of the timed training step (optim.hpp:14-18 defaults, small lr)
 ADAMW = dict(lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0)
@@ -318,15 +319,27 @@ def run_ours(args, rank, world, local):
         return make_flow_sample(4, TEXT_L, TEXT_D)[0]
 
     torch.cuda.set_device(local)
-    cfg = paper_config(depth=1)
+    GRID = tuple(args.grid)
+    tp = args.tp
+    if world % tp:
+        sys.exit(f"bench.py: --tp {tp} does not divide the {world} ranks")
+    # rank = dp_rank * tp + tp_rank: a TP group is tp consecutive ranks; DP joins the ranks with the same tp_rank
+    tp_rank, dp_rank, dp_world = rank % tp, rank // tp, world // tp
+    cfg = paper_config(depth=args.depth)
     ctx = Context(local, "bf16")
     stream = torch.cuda.Stream()
     ctx.set_stream(stream.cuda_stream)
     if world > 1:
         import torch.distributed as dist
-        uid = [Context.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ctx.set_dp(rank, world, uid[0])
+        ids = [None] * world
+        # rank r offers the TP id of its group (if tp_rank == 0) and the DP id of its DP group (if dp_rank == 0)
+        mine = (Context.nccl_unique_id() if tp > 1 and tp_rank == 0 else None,
+                Context.nccl_unique_id() if dp_world > 1 and dp_rank == 0 else None)
+        dist.all_gather_object(ids, mine)
+        if tp > 1:
+            ctx.set_tp(tp, tp_rank, ids[dp_rank * tp][0])
+        if dp_world > 1:
+            ctx.set_dp(dp_rank, dp_world, ids[tp_rank][1])
     ctx.set_adamw(**ADAMW)  # the timed step is the full FlowTrainer::step: fwd + bwd + grad norm + AdamW
     # SURVEY 8(d) weights: init_dit_params(cfg, Rng(1)) + gates opened from Rng(2) at the width-scaled std
     gs = 0.2 * math.sqrt(12.0 / cfg.hidden)
@@ -337,9 +350,9 @@ def run_ours(args, rank, world, local):
     # SURVEY 8(d) inputs with the reference's Rng streams: latent Rng(3 + rank).uniform_tensor(16x90x160x24, -1, 1)
     # patchified on device (dit::latent_rows), text Rng(4).normal_tensor (64 x 4096), noise and t from
     # make_batch(Rng(5 + rank)) (flowtrain.cpp:231-250); rank r > 0 draws its own sample
-    latent = rng_uniform(3 + rank, (U, 2 * Hp, 2 * Wp, PATCH // 4), -1.0, 1.0)
+    latent = rng_uniform(3 + dp_rank, (U, 2 * Hp, 2 * Wp, PATCH // 4), -1.0, 1.0)
     rows, coords = ctx.latent_rows(latent)
-    noise, t_val, _ = make_flow_sample(5 + rank, N, PATCH)
+    noise, t_val, _ = make_flow_sample(5 + dp_rank, N, PATCH)
     clean_h, clean_t = pinned((N, PATCH), np.float64)
     noise_h, noise_t = pinned((N, PATCH), np.float64)
     text_h, text_t = pinned((TEXT_L, TEXT_D), np.float64)
@@ -378,7 +391,7 @@ def run_ours(args, rank, world, local):
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
     prof = ctx.prof_stats()
     ctx.prof_enable(False)
-    value = world * N / (ms / 1000.0)
+    value = dp_world * N / (ms / 1000.0)
 
     # e2e through the public C ABI with pinned host buffers
     sample = FlowSample(GRID, coords_h, clean_h, noise_h, t_val, None)
@@ -401,8 +414,8 @@ def run_ours(args, rank, world, local):
     for name, st in prof.items():
         per = st["ms"] / max(1, st["launches"])
         kern[name] = {"ms_per_step": st["ms"] / args.steps, "ms_per_launch": per, "share": st["ms"] / args.steps / ms}
-    # algorithmic FLOPs per launch: self-attention fwd 4 N^2 H, bwd 8 N^2 H
-    f_fwd, f_bwd = 4.0 * N * N * H, 8.0 * N * N * H
+    # algorithmic FLOPs per launch: self-attention fwd 4 N^2 H, bwd 8 N^2 H (a TP rank: its H / tp)
+    f_fwd, f_bwd = 4.0 * N * N * H / tp, 8.0 * N * N * H / tp
     att = {}
     if "attn_fwd" in kern:
         att["fwd_tflops"] = f_fwd / (kern["attn_fwd"]["ms_per_launch"] * 1e9)
@@ -433,27 +446,34 @@ def run_ours(args, rank, world, local):
                 "peak_source": f"{pk['source']} bf16_tflops_sustained (kernel timed inside a long step)",
                 "flops_per_launch": fl}
     total_flops = 3 * (28.0 * N * H * H + 4.0 * N * N * H + 4.0 * N * TEXT_L * H + 2 * TEXT_L * TEXT_D * 2 * H)
+    total_flops *= args.depth / tp
+    par = f"dp{dp_world}" if tp == 1 else f"tp{tp}" + (f"xdp{dp_world}" if dp_world > 1 else "")
+    shape = {(16, 45, 80): "720p/5s latent 16x90x160x24 -> 57600 tokens",
+             (7, 30, 52): "480p/2s latent 7x60x104x24 -> 10920 tokens"}.get(GRID, f"token grid {GRID} -> {N} tokens")
+    stack = "depth 1" if args.depth == 1 else f"{args.depth}-block stack"
     res = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic latents + random-init 10B-shaped weights",
-        "config": {"workload": "MUG-V 10B DiT block (H3456, 24x144 heads, FFN 13824, text 64x4096), depth 1 + "
-                               "patch/final/velocity heads, 720p/5s latent 16x90x160x24 -> 57600 tokens, flow-matching "
-                               "fwd+bwd + grad norm + AdamW update (the full FlowTrainer::step), 1 sample per GPU",
-                   "tokens_per_sample": N, "samples_per_gpu": 1, "global_batch": world, "parallelism": f"dp{world}",
+        "config": {"workload": f"MUG-V 10B DiT block (H3456, 24x144 heads, FFN 13824, text 64x4096), {stack} + "
+                               f"patch/final/velocity heads, {shape}, flow-matching "
+                               "fwd+bwd + grad norm + AdamW update (the full FlowTrainer::step), 1 sample per "
+                               + ("GPU" if tp == 1 else f"TP group of {tp}"),
+                   "tokens_per_sample": N, "samples_per_gpu": 1 if tp == 1 else 1.0 / tp, "global_batch": dp_world,
+                   "parallelism": par, "depth": args.depth,
                    "l2": "working set ~17 GB >> 126 MB L2 (no flush needed)"},
         "roofline": roof,
         "attention": att,
         "block_tflops": total_flops / (ms * 1e9),
         "kernels": kern,
         "cpu_baseline": None,
-        "e2e": {"value": world * N / (e2e_ms / 1000.0), "unit": "tokens/s", "ms_per_step": e2e_ms,
+        "e2e": {"value": dp_world * N / (e2e_ms / 1000.0), "unit": "tokens/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "clocks": clk.summary(),
         "gpu_launches": launches,
         "loss": loss, "grad_norm": gnorm,
     }
-    if world == 1 and not args.no_extra:
+    if world == 1 and args.depth == 1 and GRID == GRID_720P and not args.no_extra:
         res["extra_configs"] = extra_configs(ctx, args)
     if world == 1 and not args.no_cpu_baseline:
         try:
@@ -540,6 +560,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the configs[1]/configs[4] side measurements")
+    ap.add_argument("--tp", type=int, default=1, help="tensor-parallel group size (head/column TP over NCCL + NVLink "
+                                                      "peer exchange); the other factor of --gpus is DP")
+    ap.add_argument("--depth", type=int, default=1, help="DiT blocks (configs[3]: 56, with --grid 7 30 52)")
+    ap.add_argument("--grid", type=int, nargs=3, default=list(GRID_720P), metavar=("U", "H", "W"),
+                    help="token grid (latent / 2x2 patches); 7 30 52 = the 480p/2s shape")
     args = ap.parse_args()
     if args.gpus < 1:
         sys.exit("bench.py: --gpus must be >= 1")

@@ -34,6 +34,7 @@ def _declare(L):
     L.mgv_dev_gemm.argtypes = [I, P, I64, I, P, I64, I, I, I, I, P, I64, F, I, P]
     L.mgv_dev_gemm.restype = I
     L.mgv_dev_set_gemm_mode.argtypes = [I]
+    L.mgv_dev_set_fusions.argtypes = [I]
     L.mgv_dev_set_attn_dbg.argtypes = [I]
     from . import capi
     capi.declare(L)

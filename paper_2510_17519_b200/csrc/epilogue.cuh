@@ -270,3 +270,118 @@ struct EpiSiluBwd {
 };
 
 }  // namespace mgv
+
+namespace mgv {
+
+// ---- whole-tile epilogues: the GEMM hands the functor one output row of a BN-column tile through a chunk
+// loader (ld(c, v): 16 fp32 accumulators of columns [16c, 16c+16), executed by all 32 lanes of the warp, so
+// the functor's control flow around it must be warp-uniform) instead of 16-column segments.
+template <class Epi>
+struct IsTileEpi {
+    static constexpr bool value = false;
+};
+
+// Rotation of one (x0, x1) pair, explicit roundings so every kernel that applies it (this epilogue and
+// qk_norm_rope_vec) produces the same bits:  (x0 c - x1 s, x0 s + x1 c)   (autodiff.cpp:864-865)
+__device__ __forceinline__ void rope_pair(float x0, float x1, float c, float sn, float& o0, float& o1) {
+    o0 = __fmaf_rn(x0, c, -__fmul_rn(x1, sn));
+    o1 = __fmaf_rn(x0, sn, __fmul_rn(x1, c));
+}
+
+// QKV projection with the QK-L2-norm x temperature and the 3-D RoPE fused into its epilogue (dit.cpp:288-294,
+// SURVEY K6).  The GEMM runs with BN = head_dim (HD), so every output tile is one whole head of q, k or v for
+// 128 tokens; each epilogue thread owns one token row of it:
+//   pass 1  raw = bf16(acc + bias)  -> qkv (kept for the backward and for V);  q/k: the 18 lane partials of
+//           sum(raw^2) that qk_norm_rope_vec forms (lane l: fmaf over elements [8l, 8l+8)), then its xor
+//           butterfly order, so iq / ik and the rotated output are bit-identical to the separate kernel;
+//   pass 2  (q/k only) re-read the accumulators, raw * (1/|raw| [* temp_h]), rotate pairs with the row's
+//           (cos, sin) table -> qk.
+// V tiles take pass 1 only.  Layout as QKLayout: raw q|k|v chunks of Hl columns at stride ld, rotated q|k at
+// stride qk_ld (k at qk_koff), inverse norms at iq / ik [m * i_ld + head].
+template <int HD>
+struct EpiQKNormRope {
+    __nv_bfloat16* qkv;
+    int64_t ld;
+    const float* bias;
+    __nv_bfloat16* qk;
+    int64_t qk_ld, qk_koff;
+    int64_t hl;  // columns per q|k|v chunk (heads * HD)
+    const float* temp;
+    const float2* cs;  // (N, HD/2) (cos, sin)
+    float* iq;
+    float* ik;
+    int64_t i_ld;
+    int M;
+    template <class LD>
+    __device__ __forceinline__ void tile_row(int m, int n0, LD&& ld_chunk) const {
+        constexpr int NC = HD / 16, NP = HD / 8;  // 16-column chunks; 8-element lane partials
+        static_assert(HD % 16 == 0 && NP <= 32, "head_dim");
+        const int region = static_cast<int>(n0 / hl);  // 0 q, 1 k, 2 v (warp-uniform)
+        const int h = static_cast<int>((n0 - region * hl) / HD);
+        const bool ok = m < M;
+        float part[NP];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            float v[16], b[16];
+            ld_chunk(c, v);
+            Vec16<float>::load(bias + n0 + 16 * c, b);
+            uint32_t w[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                __nv_bfloat162 p2 = __floats2bfloat162_rn(v[2 * j] + b[2 * j], v[2 * j + 1] + b[2 * j + 1]);
+                w[j] = *reinterpret_cast<uint32_t*>(&p2);
+                const float2 f = __bfloat1622float2(p2);
+                v[2 * j] = f.x;
+                v[2 * j + 1] = f.y;
+            }
+            if (ok) {
+                uint4* o = reinterpret_cast<uint4*>(qkv + (int64_t)m * ld + n0 + 16 * c);
+                o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                o[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            }
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                float ss = 0.0f;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) ss = fmaf(v[8 * hh + e], v[8 * hh + e], ss);
+                part[2 * c + hh] = ss;
+            }
+        }
+        if (region == 2) return;
+        // the xor butterfly of a 32-lane warp_sum as seen by lane 0 (lanes >= NP contribute 0)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int l = 0; l < o; ++l)
+                if (l + o < NP) part[l] = part[l] + part[l + o];
+        const float iv = 1.0f / sqrtf(part[0] + 1e-6f);  // autodiff.cpp:727
+        if (ok) (region == 0 ? iq : ik)[(int64_t)m * i_ld + h] = iv;
+        const float sc = region == 0 ? iv * temp[h] : iv;  // dit.cpp:292
+        const float4* csr = reinterpret_cast<const float4*>(cs + (int64_t)m * (HD / 2));
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            float v[16], b[16], o[16];
+            ld_chunk(c, v);
+            Vec16<float>::load(bias + n0 + 16 * c, b);
+            float4 t[4] = {make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0),
+                           make_float4(0, 0, 0, 0)};
+            if (ok) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) t[q] = csr[4 * c + q];
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float2 f = __bfloat1622float2(__floats2bfloat162_rn(v[2 * k] + b[2 * k], v[2 * k + 1] + b[2 * k + 1]));
+                const float cc = (k & 1) ? t[k >> 1].z : t[k >> 1].x, sn = (k & 1) ? t[k >> 1].w : t[k >> 1].y;
+                rope_pair(__fmul_rn(f.x, sc), __fmul_rn(f.y, sc), cc, sn, o[2 * k], o[2 * k + 1]);
+            }
+            if (ok) Vec16<__nv_bfloat16>::store(qk + (int64_t)m * qk_ld + region * qk_koff + h * HD + 16 * c, o);
+        }
+    }
+};
+template <int HD>
+struct IsTileEpi<EpiQKNormRope<HD>> {
+    static constexpr bool value = true;
+};
+
+}  // namespace mgv

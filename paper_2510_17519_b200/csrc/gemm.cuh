@@ -179,6 +179,29 @@ extern int g_gemm_mode;  // 0: 1-CTA (+B multicast pairs), 1: CTA-pair UMMA (def
 // begin = true and the GEMM's 2 M N K before the launch and with begin = false after it.
 extern void (*g_gemm_prof_hook)(bool begin, double flops, cudaStream_t s);
 
+struct GemmProfScope {
+    cudaStream_t s;
+    GemmProfScope(double f, cudaStream_t st) : s(st) {
+        if (g_gemm_prof_hook) g_gemm_prof_hook(true, f, s);
+    }
+    ~GemmProfScope() {
+        if (g_gemm_prof_hook) g_gemm_prof_hook(false, 0.0, s);
+    }
+};
+
+// bf16 tcgen05 GEMM, both operands K-major, with an explicit N tile: the whole-tile epilogues need BN = one
+// head (EpiQKNormRope: BN = head_dim).
+template <int BN, class Epi>
+void gemm_tc_bn(const Mat& A, const Mat& B, int M, int N, int K, const Epi& epi, cudaStream_t s) {
+    if (M <= 0 || N <= 0) return;
+    if (A.major != Major::K || B.major != Major::K) throw std::runtime_error("gemm_tc_bn: K-major operands only");
+    GemmProfScope prof_scope(2.0 * M * N * K, s);
+    if (g_gemm_mode == 1 && M > kGemmBM)
+        gemm_tc2_launch<BN, false, false>(A, B, M, N, K, epi, s);
+    else
+        gemm_tc_launch<BN, false, false>(A, B, M, N, K, epi, s);
+}
+
 // Dispatch on precision and operand majors.  bf16: A/B are __nv_bfloat16; fp32: float.
 template <class Epi>
 void gemm(bool bf16, const Mat& A, const Mat& B, int M, int N, int K, const Epi& epi, cudaStream_t s) {
@@ -191,15 +214,7 @@ void gemm(bool bf16, const Mat& A, const Mat& B, int M, int N, int K, const Epi&
         else gemm_f32_launch<true, false>(A, B, M, N, K, epi, s);
         return;
     }
-    struct ProfScope {
-        cudaStream_t s;
-        ProfScope(double f, cudaStream_t st) : s(st) {
-            if (g_gemm_prof_hook) g_gemm_prof_hook(true, f, s);
-        }
-        ~ProfScope() {
-            if (g_gemm_prof_hook) g_gemm_prof_hook(false, 0.0, s);
-        }
-    } prof_scope(2.0 * M * N * K, s);
+    GemmProfScope prof_scope(2.0 * M * N * K, s);
     if (g_gemm_mode == 1 && M > kGemmBM) {
         if (!am && !bm) gemm_tc2_launch<256, false, false>(A, B, M, N, K, epi, s);
         else if (!am && bm) gemm_tc2_launch<256, false, true>(A, B, M, N, K, epi, s);

@@ -63,13 +63,24 @@ __device__ __forceinline__ void epilogue_rows(uint32_t acc_base, int wq, int lan
     const int g = wq & 3, hf = wq >> 2;
     const int row = m0 + g * 32 + lane;
     const uint32_t base = acc_base + hf * W + (static_cast<uint32_t>(g * 32) << 16);
-    uint32_t r[2][16];
-    tmem_ld16(base, r[0]);
+    if constexpr (IsTileEpi<Epi>::value) {  // whole-row functor (BN = one head): chunks on demand
+        static_assert(EpiWarps<Epi>::value == 4, "tile epilogues own whole rows");
+        epi.tile_row(row, n0, [&](int c, float* v) {
+            uint32_t q[16];
+            tmem_ld16(base + c * 16, q);
+            tmem_wait_ld();
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-        tmem_wait_ld();
-        if (c + 1 < NCH) tmem_ld16(base + (c + 1) * 16, r[(c + 1) & 1]);
-        epi(row, n0 + hf * W + c * 16, reinterpret_cast<const float*>(r[c & 1]), 16);
+            for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(q[j]);
+        });
+    } else {
+        uint32_t r[2][16];
+        tmem_ld16(base, r[0]);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            tmem_wait_ld();
+            if (c + 1 < NCH) tmem_ld16(base + (c + 1) * 16, r[(c + 1) & 1]);
+            epi(row, n0 + hf * W + c * 16, reinterpret_cast<const float*>(r[c & 1]), 16);
+        }
     }
 }
 
@@ -257,7 +268,7 @@ __global__ void __launch_bounds__(kGemmThreadsMax, 1)
 // lanes it owns, then arrives on the leader's accumulator-empty barrier.
 template <int BN>
 struct Gemm2Cfg {
-    static constexpr int STAGES = 6;
+    static constexpr int STAGES = BN >= 256 ? 6 : 8;
     static constexpr int A_BYTES = kGemmBM * kGemmBK * 2;        // this CTA's 128 rows
     static constexpr int B_BYTES = (BN / 2) * kGemmBK * 2;        // this CTA's BN/2 rows
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;

@@ -58,6 +58,12 @@ void rms_gain(const float* X, int N, int H, const float* g, T* out, float* r, cu
 // X2 = X1 + rms(co) * g   (dit.cpp:305)
 template <class T>
 void postnorm_resid(const float* X1, const T* co, int N, int H, const float* g, float* X2, float* rc, cudaStream_t s);
+// postnorm_resid followed by rms_mod of X2 (dit.cpp:305 + :308) in one pass, bit-identical to the two kernels;
+// false (nothing launched) where only the two-kernel path exists (fp32 mode, H % 8 != 0 or H > 4096)
+template <class T>
+bool postnorm_resid_mod(const float* X1, const T* co, int N, int H, const float* g, float* X2, float* rc,
+                        const float* table, int64_t tld, int sh_off, int sc_off, const int32_t* mod_id, T* f, float* r2,
+                        cudaStream_t s);
 // Row strides of the q/k views the QK-norm kernels read and write (a tensor-parallel rank sees a
 // column slice of the full buffers): q at column 0 and k at column *_koff of rows with stride *_ld;
 // the inverse norms iq/ik at [n * i_ld + h].

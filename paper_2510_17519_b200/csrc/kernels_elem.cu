@@ -21,6 +21,9 @@ void rms_fwd_vec_launch(const float* X, int N, int H, const float* table, int64_
                         const int32_t* mod_id, const float* g, __nv_bfloat16* out, float* r, cudaStream_t s);
 void postnorm_resid_vec_launch(const float* X1, const __nv_bfloat16* co, int N, int H, const float* g, float* X2,
                                float* rc, cudaStream_t s);
+void postnorm_resid_mod_vec_launch(const float* X1, const __nv_bfloat16* co, int N, int H, const float* g, float* X2,
+                                   float* rc, const float* table, int64_t tld, int sh_off, int sc_off,
+                                   const int32_t* mod_id, __nv_bfloat16* f, float* r2, cudaStream_t s);
 void gate_bwd_vec_launch(const float* dX, const __nv_bfloat16* y, const float* table, int64_t tld, int gate_off,
                          const int32_t* mod_id, int n_u, int N, int H, __nv_bfloat16* dY, float* part_dgate,
                          float* part_db, cudaStream_t s);
@@ -394,6 +397,19 @@ void postnorm_resid(const float* X1, const T* co, int N, int H, const float* g, 
     }
     postnorm_resid_kernel<T><<<row_chunks(N), RT, 0, s>>>(X1, co, N, H, g, X2, rc); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
+}
+
+template <class T>
+bool postnorm_resid_mod(const float* X1, const T* co, int N, int H, const float* g, float* X2, float* rc,
+                        const float* table, int64_t tld, int sh_off, int sc_off, const int32_t* mod_id, T* f, float* r2,
+                        cudaStream_t s) {
+    if constexpr (is_bf16<T>()) {
+        if (use_vec(H)) {
+            postnorm_resid_mod_vec_launch(X1, co, N, H, g, X2, rc, table, tld, sh_off, sc_off, mod_id, f, r2, s);
+            return true;
+        }
+    }
+    return false;
 }
 
 // One warp per (token, head, q|k); lane owns rotation pairs lane, lane+32, lane+64 (hd <= 192).
@@ -1175,6 +1191,8 @@ void permute_shard_rows(const double* src, double* dst, int C, int R, int P, int
                              cudaStream_t);                                                                           \
     template void rms_gain<T>(const float*, int, int, const float*, T*, float*, cudaStream_t);                        \
     template void postnorm_resid<T>(const float*, const T*, int, int, const float*, float*, float*, cudaStream_t);    \
+    template bool postnorm_resid_mod<T>(const float*, const T*, int, int, const float*, float*, float*, const float*, \
+                                        int64_t, int, int, const int32_t*, T*, float*, cudaStream_t);                \
     template void qk_norm_rope<T>(const T*, const QKLayout&, int, int, int, const float*, const float2*, T*, float*,  \
                                   float*, cudaStream_t);                                                              \
     template void bias_gate_resid<T>(const float*, const float*, const float*, int64_t, int, const int32_t*,          \
@@ -1327,8 +1345,14 @@ __global__ void __launch_bounds__(RT) rms_fwd_vec(const float* X, int N, int H, 
     }
 }
 
+// X2 = X1 + rms(co) * g (dit.cpp:305); MOD: the FFN's modulated RMSNorm of the new rows in the same pass
+// (dit.cpp:308, f = rms(X2)(1 + sc2) + sh2 and its 1/rms r2), with rms_fwd_vec<0>'s per-thread order and block
+// reduction, so f and r2 are bit-identical to running it on X2 afterwards
+template <bool MOD>
 __global__ void __launch_bounds__(RT) postnorm_resid_vec(const float* X1, const bf* co, int N, int H, const float* g,
-                                                         float* X2, float* rc) {
+                                                         float* X2, float* rc, const float* table, int64_t tld,
+                                                         int sh_off, int sc_off, const int32_t* mod_id, bf* f,
+                                                         float* r2) {
     __shared__ float red[R][RT / 32];
     const int G = H / 8;
     const int r0 = blockIdx.x * kRowsPerChunk, r1 = min(N, r0 + kRowsPerChunk);
@@ -1352,9 +1376,11 @@ __global__ void __launch_bounds__(RT) postnorm_resid_vec(const float* X1, const 
             }
         }
         block_sum_r(ss, red);
+        float ss2[R];
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
             const int row = i + rr;
+            ss2[rr] = 0.0f;
             if (row >= r1) continue;
             const float rstd = 1.0f / sqrtf(ss[rr] / static_cast<float>(H) + 1e-6f);
             if (threadIdx.x == 0) rc[row] = rstd;
@@ -1368,6 +1394,34 @@ __global__ void __launch_bounds__(RT) postnorm_resid_vec(const float* X1, const 
 #pragma unroll
                 for (int e = 0; e < 8; ++e) x[e] += v[rr][k][e] * rstd * gg[e];
                 st8(X2 + (int64_t)row * H + grp * 8, x);
+                if (MOD) {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        v[rr][k][e] = x[e];  // co is consumed: keep the new residual row
+                        ss2[rr] = fmaf(x[e], x[e], ss2[rr]);
+                    }
+                }
+            }
+        }
+        if (!MOD) continue;
+        block_sum_r(ss2, red);
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+            const int row = i + rr;
+            if (row >= r1) continue;
+            const float rstd = 1.0f / sqrtf(ss2[rr] / static_cast<float>(H) + 1e-6f);
+            if (threadIdx.x == 0) r2[row] = rstd;
+            const float* tb = table + (int64_t)mod_id[row] * tld;
+#pragma unroll
+            for (int k = 0; k < VG; ++k) {
+                const int grp = threadIdx.x + k * RT;
+                if (grp >= G) continue;
+                float o[8], a[8], b[8];
+                ld8(tb + sc_off + grp * 8, a);
+                ld8(tb + sh_off + grp * 8, b);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) o[e] = v[rr][k][e] * rstd * (1.0f + a[e]) + b[e];
+                st8(f + (int64_t)row * H + grp * 8, o);
             }
         }
     }
@@ -1680,11 +1734,8 @@ __global__ void __launch_bounds__(256) qk_norm_rope_vec(const bf* qkv, QKLayout 
         const float sc = which == 0 ? iv * temp[h] : iv;  // dit.cpp:292
         float o[8];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float x0 = v[u][2 * k] * sc, x1 = v[u][2 * k + 1] * sc;
-            o[2 * k] = x0 * c[k] - x1 * sn[k];  // autodiff.cpp:864-865
-            o[2 * k + 1] = x0 * sn[k] + x1 * c[k];
-        }
+        for (int k = 0; k < 4; ++k)  // autodiff.cpp:864-865, the roundings of the fused QKV epilogue
+            rope_pair(__fmul_rn(v[u][2 * k], sc), __fmul_rn(v[u][2 * k + 1], sc), c[k], sn[k], o[2 * k], o[2 * k + 1]);
         st8(qk + n * Lq.out_ld + which * Lq.out_koff + h * hd + 8 * lane, o);
     }
 }
@@ -1811,7 +1862,16 @@ void rms_fwd_vec_launch(const float* X, int N, int H, const float* table, int64_
 }
 void postnorm_resid_vec_launch(const float* X1, const __nv_bfloat16* co, int N, int H, const float* g, float* X2,
                                float* rc, cudaStream_t s) {
-    vec::postnorm_resid_vec<<<row_chunks(N), vec::RT, 0, s>>>(X1, co, N, H, g, X2, rc);
+    vec::postnorm_resid_vec<false><<<row_chunks(N), vec::RT, 0, s>>>(X1, co, N, H, g, X2, rc, nullptr, 0, 0, 0,
+                                                                     nullptr, nullptr, nullptr);
+    note_launch();
+    MGV_CUDA(cudaGetLastError());
+}
+void postnorm_resid_mod_vec_launch(const float* X1, const __nv_bfloat16* co, int N, int H, const float* g, float* X2,
+                                   float* rc, const float* table, int64_t tld, int sh_off, int sc_off,
+                                   const int32_t* mod_id, __nv_bfloat16* f, float* r2, cudaStream_t s) {
+    vec::postnorm_resid_vec<true><<<row_chunks(N), vec::RT, 0, s>>>(X1, co, N, H, g, X2, rc, table, tld, sh_off, sc_off,
+                                                                    mod_id, f, r2);
     note_launch();
     MGV_CUDA(cudaGetLastError());
 }

@@ -887,6 +887,47 @@ template <class T>
 inline const void* off(const void* p, int64_t n) { return static_cast<const T*>(p) + n; }
 }  // namespace
 
+// QKV projection + QK-L2-norm x temperature + 3-D RoPE (dit.cpp:288-294).  bf16 mode: one tcgen05 GEMM with
+// BN = head_dim whose epilogue writes the raw q|k|v, the inverse norms and the rotated q|k (EpiQKNormRope,
+// bit-identical to the GEMM + qk_norm_rope_vec pair it replaces); fp32 parity mode and head dims without a
+// whole-head tile: the GEMM and the row kernel.
+// fusion switches (tests / A-B only): bit 0 the QKV epilogue, bit 1 post-norm residual + FFN modulated RMSNorm
+constexpr int kFuseQKV = 1, kFuseNormMod = 2;
+int g_fusions = kFuseQKV | kFuseNormMod;
+extern "C" void mgv_dev_set_fusions(int mask) { g_fusions = mask; }
+template <int HD>
+static bool qkv_fused_launch(const void* a, int64_t H, const void* Wq, const float* bias, int n, int64_t Hl,
+                             const QKLayout& L, const float* temp, const float2* cs, void* qkv, void* qk, float* iq,
+                             float* ik, cudaStream_t s) {
+    using bf = __nv_bfloat16;
+    EpiQKNormRope<HD> e{static_cast<bf*>(qkv), L.in_ld, bias, static_cast<bf*>(qk), L.out_ld, L.out_koff, Hl, temp,
+                        cs, iq, ik, L.i_ld, n};
+    // q | k rows of the weight with the whole-head tile; the v rows keep the 256-wide tile (a 144-wide tile
+    // moves 39% more shared-memory bytes per FLOP: its V third would cost more than it saves)
+    gemm_tc_bn<HD>(KM(a, H), KM(Wq, H), n, static_cast<int>(2 * Hl), static_cast<int>(H), e, s);
+    gemm(true, KM(a, H), KM(static_cast<const bf*>(Wq) + 2 * Hl * H, H), n, static_cast<int>(Hl), static_cast<int>(H),
+         EpiStore<bf>{static_cast<bf*>(qkv) + 2 * Hl, L.in_ld, bias + 2 * Hl, 1.0f, n, static_cast<int>(Hl)}, s);
+    return true;
+}
+template <class T>
+static void qkv_norm_rope(bool bf16, const void* a, int64_t H, const void* Wq, const float* bias, int n, int64_t Hl,
+                          int64_t heads, const QKLayout& L, const float* temp, const float2* cs, void* qkv, void* qk,
+                          float* iq, float* ik, cudaStream_t s) {
+    const int64_t hd = Hl / heads;
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+        const bool lay = L.in_ld == 3 * Hl && L.in_koff == Hl && (H % 8) == 0 && (L.out_ld % 8) == 0 &&
+                         (L.out_koff % 8) == 0;
+        if (bf16 && (g_fusions & kFuseQKV) && lay) {
+            if (hd == 144) { qkv_fused_launch<144>(a, H, Wq, bias, n, Hl, L, temp, cs, qkv, qk, iq, ik, s); return; }
+            if (hd == 128) { qkv_fused_launch<128>(a, H, Wq, bias, n, Hl, L, temp, cs, qkv, qk, iq, ik, s); return; }
+            if (hd == 64) { qkv_fused_launch<64>(a, H, Wq, bias, n, Hl, L, temp, cs, qkv, qk, iq, ik, s); return; }
+        }
+    }
+    gemm(bf16, KM(a, H), KM(Wq, H), n, static_cast<int>(3 * Hl), static_cast<int>(H),
+         EpiStore<T>{tp<T>(qkv), 3 * Hl, bias, 1.0f, n, static_cast<int>(3 * Hl)}, s);
+    qk_norm_rope<T>(tp<T>(qkv), L, n, static_cast<int>(Hl), static_cast<int>(heads), temp, cs, tp<T>(qk), iq, ik, s);
+}
+
 template <class T>
 static void attention_fwd(bool bf16, const AttnProblem& p, cudaStream_t s) {
     if (bf16 && attn_tc_supported(p.hd, p.Nk))
@@ -918,9 +959,8 @@ void Model::block_fwd(int i, int64_t N) {
     const int n = static_cast<int>(N);
     // self-attention: a = rms(x)(1+sc1)+sh1 (dit.cpp:287)
     rms_mod<T>(Xin, n, H, tab, tld, 0, H, w.mod_id, tp<T>(b.a), b.r0, s);
-    gemm(bf, KM(b.a, H), KM(W(blk(i, "attn.qkv.w")), H), n, 3 * H, H,
-         EpiStore<T>{tp<T>(b.qkv), 3 * H, P(blk(i, "attn.qkv.b")).f32, 1.0f, n, int(3 * H)}, s);  // dit.cpp:288
-    qk_norm_rope<T>(tp<T>(b.qkv), qk_layout_full(H, nh), n, H, nh, P(blk(i, "attn.temp")).f32, w.cs, tp<T>(b.qk), b.iq, b.ik, s);  // :289-294
+    qkv_norm_rope<T>(bf, b.a, H, W(blk(i, "attn.qkv.w")), P(blk(i, "attn.qkv.b")).f32, n, H, nh, qk_layout_full(H, nh),
+                     P(blk(i, "attn.temp")).f32, w.cs, b.qkv, b.qk, b.iq, b.ik, s);  // dit.cpp:288-294
     AttnProblem ap{b.qk, 2 * H, off<T>(b.qk, H), 2 * H, off<T>(b.qkv, 2 * H), 3 * H, b.O, H, b.lse,
                    n, n, int(nh), int(hd)};
     prof_.begin("attn_fwd", s);
@@ -946,9 +986,14 @@ void Model::block_fwd(int i, int64_t N) {
     prof_.end(s);
     gemm(bf, KM(b.Ox, H), KM(W(blk(i, "xattn.out.w")), H), n, H, H,
          EpiStore<T>{tp<T>(b.co), H, P(blk(i, "xattn.out.b")).f32, 1.0f, n, int(H)}, s);
-    postnorm_resid<T>(b.X1, tp<T>(b.co), n, H, P(blk(i, "xattn.postnorm.g")).f32, b.X2, b.rc, s);
+    // post-norm residual (dit.cpp:305) + the feed-forward's modulated RMSNorm (dit.cpp:308) in one pass
+    if (!(g_fusions & kFuseNormMod) ||
+        !postnorm_resid_mod<T>(b.X1, tp<T>(b.co), n, H, P(blk(i, "xattn.postnorm.g")).f32, b.X2, b.rc, tab, tld,
+                               3 * H, 4 * H, w.mod_id, tp<T>(b.f), b.r2, s)) {
+        postnorm_resid<T>(b.X1, tp<T>(b.co), n, H, P(blk(i, "xattn.postnorm.g")).f32, b.X2, b.rc, s);
+        rms_mod<T>(b.X2, n, H, tab, tld, 3 * H, 4 * H, w.mod_id, tp<T>(b.f), b.r2, s);
+    }
     // feed-forward (dit.cpp:308-311)
-    rms_mod<T>(b.X2, n, H, tab, tld, 3 * H, 4 * H, w.mod_id, tp<T>(b.f), b.r2, s);
     gemm(bf, KM(b.f, H), KM(W(blk(i, "ffn.in.w")), H), n, 4 * H, H,
          EpiBiasSilu<T>{tp<T>(b.z), tp<T>(b.h), 4 * H, P(blk(i, "ffn.in.b")).f32, n, int(4 * H)}, s);
     gemm(bf, KM(b.h, 4 * H), KM(W(blk(i, "ffn.out.w")), 4 * H), n, H, 4 * H,
@@ -1140,10 +1185,9 @@ void Model::block_fwd_tp(int i, int64_t N) {
         void* qkv_r = off<T>(b.qkv, k * N * 3 * Hr);
         void* qk_r = off<T>(b.qk, k * N * 2 * Hr);
         void* O_r = off<T>(b.O, k * N * Hr);
-        gemm(bf, KM(b.a, H), KM(Ws(blk(i, "attn.qkv.w"), kk), H), n, int(3 * Hr), H,
-             EpiStore<T>{tp<T>(qkv_r), 3 * Hr, Ps(blk(i, "attn.qkv.b"), kk), 1.0f, n, int(3 * Hr)}, s);
-        qk_norm_rope<T>(tp<T>(qkv_r), QKLayout{3 * Hr, Hr, 2 * Hr, Hr, nh}, n, int(Hr), int(nhr),
-                        Ps(blk(i, "attn.temp"), kk), w.cs, tp<T>(qk_r), b.iq + r * nhr, b.ik + r * nhr, s);
+        qkv_norm_rope<T>(bf, b.a, H, Ws(blk(i, "attn.qkv.w"), kk), Ps(blk(i, "attn.qkv.b"), kk), n, Hr, nhr,
+                         QKLayout{3 * Hr, Hr, 2 * Hr, Hr, nh}, Ps(blk(i, "attn.temp"), kk), w.cs, qkv_r, qk_r,
+                         b.iq + r * nhr, b.ik + r * nhr, s);
         AttnProblem ap{qk_r, 2 * Hr, off<T>(qk_r, Hr), 2 * Hr, off<T>(qkv_r, 2 * Hr), 3 * Hr, O_r, Hr,
                        b.lse + r * nhr * lld, n, n, int(nhr), int(hd)};
         ap.lse_ld = lld;
@@ -1179,9 +1223,13 @@ void Model::block_fwd_tp(int i, int64_t N) {
     }
     sum = tp_exchange(part, N, s);
     bias_to<T>(sum, P(blk(i, "xattn.out.b")).f32, tp<T>(b.co), n, int(H), s);
-    postnorm_resid<T>(b.X1, tp<T>(b.co), n, H, P(blk(i, "xattn.postnorm.g")).f32, b.X2, b.rc, s);
+    if (!(g_fusions & kFuseNormMod) ||
+        !postnorm_resid_mod<T>(b.X1, tp<T>(b.co), n, H, P(blk(i, "xattn.postnorm.g")).f32, b.X2, b.rc, tab, tld,
+                               3 * H, 4 * H, w.mod_id, tp<T>(b.f), b.r2, s)) {
+        postnorm_resid<T>(b.X1, tp<T>(b.co), n, H, P(blk(i, "xattn.postnorm.g")).f32, b.X2, b.rc, s);
+        rms_mod<T>(b.X2, n, H, tab, tld, 3 * H, 4 * H, w.mod_id, tp<T>(b.f), b.r2, s);
+    }
     // feed-forward (dit.cpp:308-311): column-parallel ffn.in, row-parallel ffn.out
-    rms_mod<T>(b.X2, n, H, tab, tld, 3 * H, 4 * H, w.mod_id, tp<T>(b.f), b.r2, s);
     for (size_t k = 0; k < ranks.size(); ++k) {
         const int64_t r = ranks[k];
         const int kk = static_cast<int>(k);

@@ -13,7 +13,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--grid", default="16,45,80")
 ap.add_argument("--kernels", action="store_true")
+ap.add_argument("--fusions", type=int, default=None, help="mgv_dev_set_fusions mask (A/B of the forward fusions)")
 args = ap.parse_args()
+if args.fusions is not None:
+    from paper_2510_17519_b200._lib import lib
+    lib().mgv_dev_set_fusions(args.fusions)
 grid = tuple(int(x) for x in args.grid.split(","))
 cfg = paper_config(depth=1)
 ctx = Context(0, "bf16")
