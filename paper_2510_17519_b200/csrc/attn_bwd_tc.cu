@@ -33,6 +33,13 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 
+// Timing experiments of the dK/dV pass (wrong results; tools/build_variant.sh, never in the product build):
+//   1: no Q^T / dO^T TMA after the first stages (the resident tiles are reused)
+//   2: no exponentials (P = S)      4: compute warps skip all TMEM loads / stores (they only bounce barriers)
+#ifndef MGV_DKV_X
+#define MGV_DKV_X 0
+#endif
+
 #ifdef MGV_ATTN_TRACE  // development timeline of one CTA (tools/trace_attn.py); not in the product build
 __device__ unsigned long long g_attn_trace[8][64];
 __device__ unsigned long long g_attn_trace2[8][64];
@@ -358,6 +365,10 @@ __global__ void __launch_bounds__(128 + 128 * CW, 1) attn_bwd_dkv_v11_kernel(con
             for (int i = 0; i < nq; ++i) {
                 const int st = i % NST;
                 if (i >= NST) mbar_wait(&qd_empty[st], ((i / NST) - 1) & 1);
+                if ((MGV_DKV_X & 1) && i >= NST) {
+                    mbar_arrive(&qd_full[st]);
+                    continue;
+                }
                 mbar_arrive_expect_tx(&qd_full[st], 2 * QT + 2 * BQ * 4);
                 const int qt = (i0 + i) * BQ;
                 tma_load_2d(sQt + st * QT, &tm.ta, &qd_full[st], qt, col);
@@ -434,9 +445,14 @@ __global__ void __launch_bounds__(128 + 128 * CW, 1) attn_bwd_dkv_v11_kernel(con
             tc_fence_after();
             if (warp == 4 && lane == 0) ATR8(4, i);
             float s[QW];
+            if (!(MGV_DKV_X & 4)) {
 #pragma unroll
-            for (int c = 0; c < QW; c += 32) tmem_ld32(sd + c, reinterpret_cast<uint32_t*>(s + c));
-            tmem_wait_ld();
+                for (int c = 0; c < QW; c += 32) tmem_ld32(sd + c, reinterpret_cast<uint32_t*>(s + c));
+                tmem_wait_ld();
+            } else {
+#pragma unroll
+                for (int c = 0; c < QW; ++c) s[c] = __int_as_float(lane + c);
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(s_loaded);
@@ -453,10 +469,17 @@ __global__ void __launch_bounds__(128 + 128 * CW, 1) attn_bwd_dkv_v11_kernel(con
                     const float4 l = lds_f4(lse_s + c4 * 4);
                     const float2 x0 = fmul2(fsub2(make_float2(s[c4], s[c4 + 1]), make_float2(l.x, l.y)), lg2);
                     const float2 x1 = fmul2(fsub2(make_float2(s[c4 + 2], s[c4 + 3]), make_float2(l.z, l.w)), lg2);
-                    s[c4] = ex2f(x0.x);
-                    s[c4 + 1] = ex2f(x0.y);
-                    s[c4 + 2] = ex2f(x1.x);
-                    s[c4 + 3] = ex2f(x1.y);
+                    if (MGV_DKV_X & 2) {
+                        s[c4] = x0.x;
+                        s[c4 + 1] = x0.y;
+                        s[c4 + 2] = x1.x;
+                        s[c4 + 3] = x1.y;
+                    } else {
+                        s[c4] = ex2f(x0.x);
+                        s[c4 + 1] = ex2f(x0.y);
+                        s[c4 + 2] = ex2f(x1.x);
+                        s[c4 + 3] = ex2f(x1.y);
+                    }
                     pk[c4 / 2] = pack_bf16(s[c4], s[c4 + 1]);
                     pk[c4 / 2 + 1] = pack_bf16(s[c4 + 2], s[c4 + 3]);
                 }
@@ -478,11 +501,13 @@ __global__ void __launch_bounds__(128 + 128 * CW, 1) attn_bwd_dkv_v11_kernel(con
                 mbar_wait(dk_done, (i - 1) & 1);  // dK(i-1) has read dS^T(i-1) out of PT
                 tc_fence_after();
             }
-            if constexpr (QW == 64)
-                tmem_st32(pt, pk);
-            else
-                tmem_st16(pt, pk);
-            tmem_wait_st();
+            if (!(MGV_DKV_X & 4)) {
+                if constexpr (QW == 64)
+                    tmem_st32(pt, pk);
+                else
+                    tmem_st16(pt, pk);
+                tmem_wait_st();
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full);
@@ -491,9 +516,14 @@ __global__ void __launch_bounds__(128 + 128 * CW, 1) attn_bwd_dkv_v11_kernel(con
             tc_fence_after();
             if (warp == 4 && lane == 0) ATR8(6, i);
             float dp[QW];
+            if (!(MGV_DKV_X & 4)) {
 #pragma unroll
-            for (int c = 0; c < QW; c += 32) tmem_ld32(sd + c, reinterpret_cast<uint32_t*>(dp + c));
-            tmem_wait_ld();
+                for (int c = 0; c < QW; c += 32) tmem_ld32(sd + c, reinterpret_cast<uint32_t*>(dp + c));
+                tmem_wait_ld();
+            } else {
+#pragma unroll
+                for (int c = 0; c < QW; ++c) dp[c] = s[c];
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(dp_loaded);  // S^T(i+1) may now overwrite SD, under the dS math below
@@ -510,11 +540,15 @@ __global__ void __launch_bounds__(128 + 128 * CW, 1) attn_bwd_dkv_v11_kernel(con
             mbar_wait(pv_done, i & 1);  // dV(i) has read P^T(i) out of PT
             tc_fence_after();
             if (warp == 4 && lane == 0) ATR8(7, i);
-            if constexpr (QW == 64)
-                tmem_st32(pt, pk);
-            else
-                tmem_st16(pt, pk);
-            tmem_wait_st();
+            if (!(MGV_DKV_X & 4)) {
+                if constexpr (QW == 64)
+                    tmem_st32(pt, pk);
+                else
+                    tmem_st16(pt, pk);
+                tmem_wait_st();
+            } else if (pk[0] == 0x12345678u && pk[QW / 2 - 1] == 0x9abcdef0u) {
+                p.dv = nullptr;  // keeps the math alive in the experiment build
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(ds_full);
