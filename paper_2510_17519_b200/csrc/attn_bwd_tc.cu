@@ -103,81 +103,6 @@ __device__ __forceinline__ void load_row_tile(uint8_t* dst, const CUtensorMap* m
     if (T::TAIL) tma_load_2d(dst + T::NF * 16384, m32, bar, col0 + T::NF * 64, row0);
 }
 
-// D[128 x 64] = A[128 x HD] . B^T where A is a 128-row tile K-major over hd and B^T is an
-// HD x 64 transposed tile read MN-major (N = 64 tokens, K = hd rows).
-template <int HD>
-__device__ __forceinline__ void mma_rows_x_t(uint32_t d, uint32_t a, uint32_t bt) {
-    using T = BT<HD>;
-    constexpr uint32_t id = idesc_bf16_f32(128, 64, false, true);
-    int kk = 0;
-#pragma unroll
-    for (int c = 0; c < T::NF; ++c)
-#pragma unroll
-        for (int k = 0; k < 4; ++k, ++kk)
-            umma_f16_ss(d, smem_desc(a + c * 16384 + k * 32, 16, 1024, kSwizzle128),
-                        smem_desc(bt + kk * 2048, 16, 1024, kSwizzle128), id, kk > 0);
-    if (T::TAIL)
-        umma_f16_ss(d, smem_desc(a + T::NF * 16384, 16, 256, kSwizzle32),
-                    smem_desc(bt + kk * 2048, 16, 1024, kSwizzle128), id, 1);
-}
-
-// D[128 x HD] (+)= A[128 x 64] . B where A is a 128 x 64 K-major chunk (smem) and B is the HD x 64
-// transposed tile read K-major (N = HD rows, K = 64 tokens): one N = HD MMA per 16-token step.
-template <int HD>
-__device__ __forceinline__ void mma_chunk_x_t(uint32_t d, uint32_t a, uint32_t bt, bool acc_first) {
-    constexpr uint32_t id = idesc_bf16_f32(128, HD, false, false);
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks)
-        umma_f16_ss(d, smem_desc(a + ks * 32, 16, 1024, kSwizzle128), smem_desc(bt + ks * 32, 16, 1024, kSwizzle128),
-                    id, (acc_first || ks > 0) ? 1u : 0u);
-}
-
-// D[128 x HD] (+)= A[128 x 64] . B with A read from TMEM (bf16 packed 2 per column, 32 columns)
-// and B the HD x 64 transposed tile read K-major: one N = HD MMA per 16-token step (TS form).
-template <int HD>
-__device__ __forceinline__ void mma_tmem_x_t(uint32_t d, uint32_t a_tmem, uint32_t bt, bool acc_first) {
-    constexpr uint32_t id = idesc_bf16_f32(128, HD, false, false);
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks)
-        umma_f16_ts(d, a_tmem + ks * 8, smem_desc(bt + ks * 32, 16, 1024, kSwizzle128), id,
-                    (acc_first || ks > 0) ? 1u : 0u);
-}
-
-// As mma_tmem_x_t, with the 64-token A operand split over the compute warps of a lane group: warp w
-// owns tokens [w W, w W + W) and keeps their bf16 pairs at columns [a_tmem + w W, a_tmem + w W + W/2).
-template <int HD, int W>
-__device__ __forceinline__ void mma_tmem_split_x_t(uint32_t d, uint32_t a_tmem, uint32_t bt, bool acc_first) {
-    constexpr uint32_t id = idesc_bf16_f32(128, HD, false, false);
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks)
-        umma_f16_ts(d, a_tmem + (16 * ks / W) * W + (16 * ks % W) / 2, smem_desc(bt + ks * 32, 16, 1024, kSwizzle128),
-                    id, (acc_first || ks > 0) ? 1u : 0u);
-}
-template <int N>
-__device__ __forceinline__ void tmem_ldn(uint32_t taddr, float* r) {
-    if constexpr (N == 16)
-        tmem_ld16(taddr, reinterpret_cast<uint32_t*>(r));
-    else
-        tmem_ld32(taddr, reinterpret_cast<uint32_t*>(r));
-}
-template <int N>
-__device__ __forceinline__ void tmem_stn(uint32_t taddr, const uint32_t* r) {
-    if constexpr (N == 8)
-        tmem_st8(taddr, r);
-    else
-        tmem_st16(taddr, r);
-}
-constexpr int kCWq = 2;  // compute warps per TMEM lane group in the dQ pass
-
-// thread row -> 64 bf16 values of a 128 x 64 SW128 K-major chunk
-__device__ __forceinline__ void st_row64(uint8_t* chunk, int row, const uint32_t* pk) {
-    const uint32_t base = smem_u32(chunk) + row * 128;
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(base + ((u ^ (row & 7)) << 4)), "r"(pk[4 * u]),
-                     "r"(pk[4 * u + 1]), "r"(pk[4 * u + 2]), "r"(pk[4 * u + 3]));
-}
-
 template <int HD>
 __device__ __forceinline__ void store_acc_row(uint32_t taddr, __nv_bfloat16* out, bool valid, int c0 = 0,
                                               int c1 = HD / 16) {
@@ -235,15 +160,6 @@ struct BwdMaps {
 };
 
 }  // namespace
-
-template <int HD>
-__device__ __forceinline__ void mma_tmem_rows_x_t(uint32_t d, uint32_t a_tmem, uint32_t bt) {
-    constexpr uint32_t id = idesc_bf16_f32(128, 64, false, true);
-#pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk)
-        umma_f16_ts(d, a_tmem + kk * 8, smem_desc(bt + kk * 2048, 16, 1024, kSwizzle128), id, kk > 0 ? 1u : 0u);
-}
-
 
 // =====================================================================================  dK / dV (v11)
 // 128-query steps with every product an N >= 128 MMA (34 instructions per 128 queries, against 52 for the

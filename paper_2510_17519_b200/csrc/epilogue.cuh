@@ -103,23 +103,35 @@ struct EpiStore {
 // [o*rpr, (o+1)*rpr), over NVLink peer memory for o != self (tp_peer.cu sums the slots in rank order).
 constexpr int kMaxTp = 8;
 struct EpiF32Peer {
-    float* box[kMaxTp];  // box[o]: this rank's slot (rpr x ldo fp32) in owner o's mailbox
+    void* box[kMaxTp];  // box[o]: this rank's slot (rpr x ldo) in owner o's mailbox
     int64_t ldo;
     float alpha;
     int rpr, M, N;
+    int bf16;  // payload: 0 fp32 (the bits EpiF32 writes), 1 bf16 (half the NVLink bytes)
     __device__ __forceinline__ void operator()(int m, int n0, const float* v, int cnt) const {
         if (m >= M) return;
         const int o = m / rpr;
-        float* p = box[o] + (int64_t)(m - o * rpr) * ldo + n0;
+        const int64_t off = (int64_t)(m - o * rpr) * ldo + n0;
+        float r[16];
+        const int c = cnt < 16 ? cnt : 16;
+        for (int j = 0; j < c; ++j) r[j] = alpha * (v[j] + 0.0f);
+        if (bf16) {
+            __nv_bfloat16* p = static_cast<__nv_bfloat16*>(box[o]) + off;
+            if (cnt == 16 && n0 + 16 <= N && al16(p)) {
+                Vec16<__nv_bfloat16>::store(p, r);
+                return;
+            }
+            for (int j = 0; j < c; ++j)
+                if (n0 + j < N) p[j] = __float2bfloat16_rn(r[j]);
+            return;
+        }
+        float* p = static_cast<float*>(box[o]) + off;
         if (cnt == 16 && n0 + 16 <= N && al16(p)) {
-            float r[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) r[j] = alpha * (v[j] + 0.0f);  // the bits EpiF32 writes
             Vec16<float>::store(p, r);
             return;
         }
-        for (int j = 0; j < cnt; ++j)
-            if (n0 + j < N) p[j] = alpha * (v[j] + 0.0f);
+        for (int j = 0; j < c; ++j)
+            if (n0 + j < N) p[j] = r[j];
     }
 };
 

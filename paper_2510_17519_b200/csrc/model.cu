@@ -391,6 +391,8 @@ void Model::set_tp(int size, int rank, const uint8_t* id) {
     tp_peer_release();
     tpx_epoch_ = 0;
     if (const char* x = std::getenv("MGV_TP_EXCHANGE")) tp_peer_ = std::strcmp(x, "nccl") != 0;
+    const char* pay = std::getenv("MGV_TP_PAYLOAD");
+    tpx_bf16_ = bf16_ && pay && std::strcmp(pay, "bf16") == 0;
     tp_ = size;
     tp_rank_ = id ? rank : 0;
     tp_virtual_ = id == nullptr;
@@ -419,17 +421,20 @@ void Model::tp_allreduce(float* buf, int64_t n, cudaStream_t s) {
 
 // ---- peer-memory TP exchange (protocol in tp_peer.h)
 static int64_t tpx_rpr(int64_t N, int P) { return (N + P - 1) / P; }
-static float* tpx_mbox(char* base) { return reinterpret_cast<float*>(base + kTpFlagBytes); }
-static float* tpx_result(char* base, int P, int64_t rpr, int64_t H) { return tpx_mbox(base) + P * rpr * H; }
+// esz: payload bytes per element (4 fp32, 2 bf16)
+static char* tpx_mbox(char* base) { return base + kTpFlagBytes; }
+static char* tpx_result(char* base, int P, int64_t rpr, int64_t H, int esz) { return tpx_mbox(base) + P * rpr * H * esz; }
 static unsigned long long* tpx_flags(char* base, int phase) {
     return reinterpret_cast<unsigned long long*>(base) + phase * kMaxTp;
 }
 
 // epilogue of rank src's row-parallel GEMM: its rows of owner o go to slot src of o's mailbox
-static EpiF32Peer tp_epi(char* const* base, int P, int src, float alpha, int64_t N, int64_t H) {
+static EpiF32Peer tp_epi(char* const* base, int P, int src, float alpha, int64_t N, int64_t H, bool bf16) {
     const int64_t rpr = tpx_rpr(N, P);
+    const int esz = bf16 ? 2 : 4;
     EpiF32Peer e{};
-    for (int o = 0; o < P; ++o) e.box[o] = tpx_mbox(base[o]) + src * rpr * H;
+    for (int o = 0; o < P; ++o) e.box[o] = tpx_mbox(base[o]) + src * rpr * H * esz;
+    e.bf16 = bf16 ? 1 : 0;
     e.ldo = H;
     e.alpha = alpha;
     e.rpr = static_cast<int>(rpr);
@@ -457,8 +462,8 @@ void Model::tp_peer_ensure(int64_t N) {
     if (!tp_peer_on()) return;
     const int P = tp_;
     const int64_t H = cfg_.H();
-    if (H % 4 != 0) throw ConfigError("the peer-memory TP exchange needs hidden % 4 == 0");
-    const int64_t need = kTpFlagBytes + 2 * P * tpx_rpr(N, P) * H * (int64_t)sizeof(float);
+    if (H % (tpx_bf16_ ? 8 : 4) != 0) throw ConfigError("the peer-memory TP exchange needs hidden % 4 == 0 (bf16 payload: % 8)");
+    const int64_t need = kTpFlagBytes + 2 * P * tpx_rpr(N, P) * H * (tpx_bf16_ ? 2 : 4);
     if (need <= tpx_bytes_) return;
     MGV_CUDA(cudaSetDevice(device_));
     MGV_CUDA(cudaStreamSynchronize(stream_));
@@ -512,6 +517,7 @@ float* Model::tp_exchange(float* part, int64_t N, cudaStream_t s) {
     prof_.begin("tp_exchange", s);
     const int P = tp_;
     const int64_t H = cfg_.H(), rpr = tpx_rpr(N, P);
+    const int esz = tpx_bf16_ ? 2 : 4;
     const uint64_t e = ++tpx_epoch_;
     const std::vector<int> ranks = tp_ranks();
     auto signal = [&](int src, int phase) {
@@ -525,15 +531,21 @@ float* Model::tp_exchange(float* part, int64_t N, cudaStream_t s) {
         TpDstPtrs d{};
         int nd = 0;
         if (tp_virtual_)  // emulated ranks share one set of activation buffers: one result region
-            d.p[nd++] = tpx_result(tpx_base_[0], P, rpr, H) + k * rpr * H;
+            d.p[nd++] = tpx_result(tpx_base_[0], P, rpr, H, esz) + k * rpr * H * esz;
         else
-            for (int j = 0; j < P; ++j) d.p[nd++] = tpx_result(tpx_base_[j], P, rpr, H) + k * rpr * H;
-        tp_reduce_gather(tpx_mbox(tpx_base_[k]), P, rpr, rows, H, d, nd, tpx_flags(tpx_base_[k], 0), e, s);
+            for (int j = 0; j < P; ++j) d.p[nd++] = tpx_result(tpx_base_[j], P, rpr, H, esz) + k * rpr * H * esz;
+        tp_reduce_gather(tpx_mbox(tpx_base_[k]), tpx_bf16_, P, rpr, rows, H, d, nd, tpx_flags(tpx_base_[k], 0), e, s);
     }
     for (int k : ranks) signal(k, 1);
     for (int k : ranks) tp_wait(tpx_flags(tpx_base_[k], 1), P, e, s);
+    char* res = tpx_result(tpx_base_[tp_virtual_ ? 0 : tp_rank_], P, rpr, H, esz);
+    if (tpx_bf16_) {  // the block's consumers read the fp32 sum: widen this rank's copy in place of `part`
+        tp_bf16_to_f32(res, N * H, part, s);
+        prof_.end(s);
+        return part;
+    }
     prof_.end(s);
-    return tpx_result(tpx_base_[tp_virtual_ ? 0 : tp_rank_], P, rpr, H);
+    return reinterpret_cast<float*>(res);
 }
 
 // Shard map (expansion.cpp:143-180 chunk layout): row-parallel parameters are stored rank-major
@@ -1172,7 +1184,7 @@ void Model::block_fwd_tp(int i, int64_t N) {
     // row-parallel GEMM: peer mode scatters the partial into the owners' mailboxes from the epilogue
     auto rowpar = [&](size_t k, int64_t r, const auto& A, const auto& B, int K, float alpha) {
         if (tp_peer_on())
-            gemm(bf, A, B, n, int(H), K, tp_epi(tpx_base_, tp_, int(r), alpha, N, H), s);
+            gemm(bf, A, B, n, int(H), K, tp_epi(tpx_base_, tp_, int(r), alpha, N, H, tpx_bf16_), s);
         else
             gemm(bf, A, B, n, int(H), K, EpiF32{part, H, nullptr, alpha, acc(k), n, int(H)}, s);
     };
@@ -1265,7 +1277,7 @@ void Model::block_bwd_tp(int i, int64_t N) {
     // row-parallel GEMM: peer mode scatters the partial into the owners' mailboxes from the epilogue
     auto rowpar = [&](size_t k, int64_t r, const auto& A, const auto& B, int K, float alpha) {
         if (tp_peer_on())
-            gemm(bf, A, B, n, int(H), K, tp_epi(tpx_base_, tp_, int(r), alpha, N, H), s);
+            gemm(bf, A, B, n, int(H), K, tp_epi(tpx_base_, tp_, int(r), alpha, N, H, tpx_bf16_), s);
         else
             gemm(bf, A, B, n, int(H), K, EpiF32{part, H, nullptr, alpha, acc(k), n, int(H)}, s);
     };

@@ -292,6 +292,7 @@ private:
     bool tp_virtual_ = false;
     // peer-memory TP exchange (tp_peer.h); MGV_TP_EXCHANGE=nccl selects the NCCL all-reduce instead
     bool tp_peer_ = true;
+    bool tpx_bf16_ = false;   // bf16 exchange payload (bf16 mode, MGV_TP_PAYLOAD=bf16)
     char* tpx_base_[8] = {};  // every rank's arena as mapped here (emulated ranks: slices of tpx_own_)
     char* tpx_own_ = nullptr;
     int64_t tpx_bytes_ = 0;   // capacity per rank arena

@@ -3,6 +3,7 @@
 //
 // Every TP rank owns one peer arena, mapped into all other ranks with CUDA IPC:
 //   [flags: u64 [2 phases][kMaxTp sources]] [mailbox: P slots x rpr rows x H] [result: P*rpr rows x H]
+// (payload fp32, or bf16 with MGV_TP_PAYLOAD=bf16 in bf16 mode: SURVEY 8(e)'s bytes)
 // with rpr = ceil(N / P) rows owned per rank.  One exchange (epoch e, monotonically increasing):
 //   1. the row-parallel GEMM's epilogue (EpiF32Peer) writes rows of its partial owned by rank o into
 //      slot `self` of o's mailbox (the reduce-scatter transfer, overlapped with the GEMM tile by tile);
@@ -28,12 +29,16 @@ struct TpFlagPtrs {
     unsigned long long* f[kMaxTp];
 };
 struct TpDstPtrs {
-    float* p[kMaxTp];
+    void* p[kMaxTp];
 };
 
 void tp_signal(const TpFlagPtrs& f, int n, uint64_t epoch, cudaStream_t s);
-void tp_reduce_gather(const float* mbox, int P, int64_t rpr, int64_t rows, int64_t H, const TpDstPtrs& dst, int ndst,
-                      const unsigned long long* flags, uint64_t epoch, cudaStream_t s);
+// bf16: mailbox slots and result rows are bf16 (the partials rounded once by the GEMM epilogue; the sum is fp32,
+// rounded to bf16 for the all-gather) -- half the bytes over NVLink.  H % 8 == 0.
+void tp_reduce_gather(const void* mbox, bool bf16, int P, int64_t rpr, int64_t rows, int64_t H, const TpDstPtrs& dst,
+                      int ndst, const unsigned long long* flags, uint64_t epoch, cudaStream_t s);
+// the local result region (bf16) -> the fp32 sum the block's consumers read
+void tp_bf16_to_f32(const void* in, int64_t n, float* out, cudaStream_t s);
 void tp_wait(const unsigned long long* flags, int P, uint64_t epoch, cudaStream_t s);
 
 }  // namespace mgv

@@ -135,3 +135,30 @@ def test_tp_with_dp_one_rank_communicator():
     for k in a["grads"]:
         assert np.array_equal(a["grads"][k], b["grads"][k]), k
         assert np.array_equal(wa[k], wb[k]), k
+
+
+@pytest.mark.parametrize("name,size", [("hd144", 2), ("cfg0", 4), ("ragged", 4)])
+def test_tp_bf16_payload(name, size, monkeypatch):
+    """MGV_TP_PAYLOAD=bf16 (bf16 mode): the row-parallel epilogues write bf16 partials into the mailboxes and the
+    owners all-gather bf16 sums (SURVEY 8(e)'s exchange bytes, half of fp32).  The step stays within the bf16
+    tolerance of the oracle, differs from the fp32 payload only by that rounding, and is deterministic."""
+    from paper_2510_17519_b200.capi import Context
+    cfg, P, text, samples = build_case(name, RAGGED if name == "ragged" else CASES[name])
+    monkeypatch.setenv("MGV_TP_EXCHANGE", "peer")
+    outs = []
+    for pay in ["fp32", "bf16", "bf16"]:
+        monkeypatch.setenv("MGV_TP_PAYLOAD", pay)
+        ctx = Context(0, "bf16")
+        ctx.set_tp(size)
+        ctx.upload(to_cfg(cfg), P)
+        outs.append(ctx.flow_step(to_samples(samples), text, 8.0, grads=True, velocity=True))
+        ctx.close()
+    f32, b1, b2 = outs
+    assert b1["loss"] == b2["loss"] and all(np.array_equal(b1["grads"][k], b2["grads"][k]) for k in b1["grads"])
+    assert b1["loss"] != f32["loss"] or any(not np.array_equal(b1["V"][i], f32["V"][i]) for i in range(len(samples)))
+    ref = O.flow_fwdbwd(P, cfg, samples, text, 8.0, grads=True)
+    worst = max(nerr(b1["grads"][k], g) for k, g in ref["grads"].items())
+    worst = max([worst, abs(b1["loss"] - ref["loss"]) / abs(ref["loss"])] +
+                [nerr(b1["V"][i], ref["V"][i]) for i in range(len(samples))])
+    print(f"tp{size} bf16 payload {name}: worst {worst:.3e}")
+    assert worst <= TOL["bf16"]

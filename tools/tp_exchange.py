@@ -67,7 +67,11 @@ def main():
                 x = prof["tp_exchange"]
                 rpr = -(-N // P)
                 per = x["ms"] / x["launches"]
-                nbytes = (P * P * rpr * H + N * H) * 4  # P emulated owners each read P slots; one result write
+                if os.environ.get("MGV_TP_PAYLOAD") == "bf16":  # bf16 slots / result + the local widening pass
+                    nbytes = (P * P * rpr * H + N * H) * 2 + N * H * (2 + 4)
+                    r["payload"] = "bf16"
+                else:
+                    nbytes = (P * P * rpr * H + N * H) * 4  # P emulated owners each read P slots; one result write
                 r["exchange_ms_per_call"] = per
                 r["exchange_calls_per_step"] = x["launches"] / args.steps
                 r["exchange_bytes_per_call"] = nbytes
