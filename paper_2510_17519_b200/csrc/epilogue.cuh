@@ -97,6 +97,34 @@ struct EpiStore {
     }
 };
 
+// EpiStore (bf16) that also writes the transposed copy outT[n * ldT + m] (the attention kernels' [heads*hd][tokens]
+// operands: V^T, the cross-attention q'^T, dO^T), the same rounded values, so no separate transpose pass is needed.
+// Lanes of a warp hold consecutive rows m: each transposed column is one 64-byte coalesced store per warp.
+struct EpiStoreT {
+    __nv_bfloat16* out;
+    int64_t ldo;
+    const float* bias;  // may be null
+    float alpha;
+    int M, N;
+    __nv_bfloat16* outT;
+    int64_t ldT;
+    __device__ __forceinline__ void operator()(int m, int n0, const float* v, int cnt) const {
+        if (m >= M) return;
+        __nv_bfloat16* o = out + (int64_t)m * ldo + n0;
+        float r[16];
+        const int c = cnt < 16 ? cnt : 16;
+        for (int j = 0; j < c; ++j) r[j] = alpha * (v[j] + (bias && n0 + j < N ? bias[n0 + j] : 0.0f));
+        if (cnt == 16 && n0 + 16 <= N && al16(o)) {
+            Vec16<__nv_bfloat16>::store(o, r);
+        } else {
+            for (int j = 0; j < c; ++j)
+                if (n0 + j < N) o[j] = __float2bfloat16_rn(r[j]);
+        }
+        for (int j = 0; j < c; ++j)
+            if (n0 + j < N) outT[(int64_t)(n0 + j) * ldT + m] = __float2bfloat16_rn(r[j]);
+    }
+};
+
 // Tensor-parallel row-parallel GEMM (attn.out / xattn.out / ffn.out and their dgrad conjugates):
 // the epilogue performs the reduce-scatter transfer of the TP exchange tile by tile.  Row m of this rank's
 // fp32 partial goes straight into this rank's slot of the mailbox of the rank that owns rows
@@ -324,6 +352,8 @@ struct EpiQKNormRope {
     float* ik;
     int64_t i_ld;
     int M;
+    __nv_bfloat16* qkT;  // optional: rotated q | k transposed ([2 hl][ldT]), the attention backward's Q^T / K^T
+    int64_t ldT;
     template <class LD>
     __device__ __forceinline__ void tile_row(int m, int n0, LD&& ld_chunk) const {
         constexpr int NC = HD / 16, NP = HD / 8;  // 16-column chunks; 8-element lane partials
@@ -387,7 +417,14 @@ struct EpiQKNormRope {
                 const float cc = (k & 1) ? t[k >> 1].z : t[k >> 1].x, sn = (k & 1) ? t[k >> 1].w : t[k >> 1].y;
                 rope_pair(__fmul_rn(f.x, sc), __fmul_rn(f.y, sc), cc, sn, o[2 * k], o[2 * k + 1]);
             }
-            if (ok) Vec16<__nv_bfloat16>::store(qk + (int64_t)m * qk_ld + region * qk_koff + h * HD + 16 * c, o);
+            if (ok) {
+                Vec16<__nv_bfloat16>::store(qk + (int64_t)m * qk_ld + region * qk_koff + h * HD + 16 * c, o);
+                if (qkT) {
+                    __nv_bfloat16* t = qkT + (region * hl + h * HD + 16 * c) * ldT + m;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) t[j * ldT] = __float2bfloat16_rn(o[j]);
+                }
+            }
         }
     }
 };

@@ -56,6 +56,8 @@ void Arena::reserve(size_t bytes) {
 struct Blk {
     float *X1, *X2, *r0, *r1, *r2, *rc, *iq, *ik, *lse, *lse_x;
     void *a, *qkv, *qk, *O, *ao, *cn, *cqs, *kv, *Ox, *co, *f, *z, *h, *ff;
+    // transposed attention operands written by the producing GEMM epilogues (WS::tpose): rotated q | k, v, q'
+    void *qkT = nullptr, *vT = nullptr, *cqT = nullptr;
 };
 struct Model::WS {
     int64_t N = 0, L = 0;
@@ -89,6 +91,10 @@ struct Model::WS {
     // varlen packing: per 128-row tile its sample's [start, end) (AttnProblem::seg); seg = null when unpacked
     int* segbuf = nullptr;
     const int* seg = nullptr;
+    // bf16, unsharded: the attention operands' transposes ([heads*hd][ldT]) come from GEMM epilogues
+    bool tpose = false;
+    int64_t ldT = 0;
+    void* dOT = nullptr;  // dO^T of the attention being differentiated (self, then cross)
 };
 
 struct AdamParam {
@@ -168,6 +174,11 @@ void layout_ws(Model::WS& w, S& a, const Cfg& c, bool grads) {
         b.z = a.takeT(R * N * 4 * Hr, e);
         b.h = a.takeT(R * N * 4 * Hr, e);
         b.ff = a.takeT(N * H, e);
+        if (w.tpose) {
+            b.qkT = a.takeT(2 * H * w.ldT, 2);
+            b.vT = a.takeT(H * w.ldT, 2);
+            b.cqT = a.takeT(H * w.ldT, 2);
+        }
     }
     w.segbuf = a.template take<int>(2 * ((N + 127) / 128));
     w.seg = nullptr;
@@ -188,6 +199,7 @@ void layout_ws(Model::WS& w, S& a, const Cfg& c, bool grads) {
         w.s1 = a.takeT(N * H, e);
         w.s2 = a.takeT(N * H, e);
         w.dkv = a.takeT(R * L * 2 * Hr, e);
+        if (w.tpose) w.dOT = a.takeT(H * w.ldT, 2);
         w.Dvec = a.template take<float>(((N + 127) / 128 * 128) * nh);
         // column partials: up to 4H wide, or one H-wide row per modulation-table row (n_u, a packed batch: B + 1)
         w.part1 = a.template take<float>((int64_t)chunks * std::max<int64_t>(4 * H, (int64_t)nu * H));
@@ -903,38 +915,56 @@ inline const void* off(const void* p, int64_t n) { return static_cast<const T*>(
 // BN = head_dim whose epilogue writes the raw q|k|v, the inverse norms and the rotated q|k (EpiQKNormRope,
 // bit-identical to the GEMM + qk_norm_rope_vec pair it replaces); fp32 parity mode and head dims without a
 // whole-head tile: the GEMM and the row kernel.
-// fusion switches (tests / A-B only): bit 0 the QKV epilogue, bit 1 post-norm residual + FFN modulated RMSNorm
-constexpr int kFuseQKV = 1, kFuseNormMod = 2;
-int g_fusions = kFuseQKV | kFuseNormMod;
+// fusion switches (tests / A-B only): bit 0 the QKV epilogue, bit 1 post-norm residual + FFN modulated RMSNorm,
+// bit 2 the attention operands' transposes written by the producing GEMM epilogues (needs bit 0)
+constexpr int kFuseQKV = 1, kFuseNormMod = 2, kFuseT = 4;
+int g_fusions = kFuseQKV | kFuseNormMod | kFuseT;
 extern "C" void mgv_dev_set_fusions(int mask) { g_fusions = mask; }
+// bf16, unsharded, a head_dim with the fused QKV tile: Q^T / K^T / V^T / q'^T / dO^T come from GEMM epilogues
+static void set_tpose(Model::WS& w, const Cfg& c) {
+    const int64_t hd = c.hd();
+    w.tpose = w.esz == 2 && w.tp == 1 && (g_fusions & kFuseT) && (g_fusions & kFuseQKV) &&
+              (hd == 64 || hd == 128 || hd == 144) && c.H() % 8 == 0;
+    w.ldT = w.tpose ? (w.N + 7) / 8 * 8 : 0;
+}
 template <int HD>
 static bool qkv_fused_launch(const void* a, int64_t H, const void* Wq, const float* bias, int n, int64_t Hl,
                              const QKLayout& L, const float* temp, const float2* cs, void* qkv, void* qk, float* iq,
-                             float* ik, cudaStream_t s) {
+                             float* ik, void* qkT, void* vT, int64_t ldT, cudaStream_t s) {
     using bf = __nv_bfloat16;
     EpiQKNormRope<HD> e{static_cast<bf*>(qkv), L.in_ld, bias, static_cast<bf*>(qk), L.out_ld, L.out_koff, Hl, temp,
-                        cs, iq, ik, L.i_ld, n};
+                        cs, iq, ik, L.i_ld, n, static_cast<bf*>(qkT), ldT};
     // q | k rows of the weight with the whole-head tile; the v rows keep the 256-wide tile (a 144-wide tile
     // moves 39% more shared-memory bytes per FLOP: its V third would cost more than it saves)
     gemm_tc_bn<HD>(KM(a, H), KM(Wq, H), n, static_cast<int>(2 * Hl), static_cast<int>(H), e, s);
-    gemm(true, KM(a, H), KM(static_cast<const bf*>(Wq) + 2 * Hl * H, H), n, static_cast<int>(Hl), static_cast<int>(H),
-         EpiStore<bf>{static_cast<bf*>(qkv) + 2 * Hl, L.in_ld, bias + 2 * Hl, 1.0f, n, static_cast<int>(Hl)}, s);
+    if (vT)
+        gemm(true, KM(a, H), KM(static_cast<const bf*>(Wq) + 2 * Hl * H, H), n, static_cast<int>(Hl),
+             static_cast<int>(H),
+             EpiStoreT{static_cast<bf*>(qkv) + 2 * Hl, L.in_ld, bias + 2 * Hl, 1.0f, n, static_cast<int>(Hl),
+                       static_cast<bf*>(vT), ldT},
+             s);
+    else
+        gemm(true, KM(a, H), KM(static_cast<const bf*>(Wq) + 2 * Hl * H, H), n, static_cast<int>(Hl),
+             static_cast<int>(H),
+             EpiStore<bf>{static_cast<bf*>(qkv) + 2 * Hl, L.in_ld, bias + 2 * Hl, 1.0f, n, static_cast<int>(Hl)}, s);
     return true;
 }
 template <class T>
 static void qkv_norm_rope(bool bf16, const void* a, int64_t H, const void* Wq, const float* bias, int n, int64_t Hl,
                           int64_t heads, const QKLayout& L, const float* temp, const float2* cs, void* qkv, void* qk,
-                          float* iq, float* ik, cudaStream_t s) {
+                          float* iq, float* ik, cudaStream_t s, void* qkT = nullptr, void* vT = nullptr,
+                          int64_t ldT = 0) {
     const int64_t hd = Hl / heads;
     if constexpr (std::is_same<T, __nv_bfloat16>::value) {
         const bool lay = L.in_ld == 3 * Hl && L.in_koff == Hl && (H % 8) == 0 && (L.out_ld % 8) == 0 &&
                          (L.out_koff % 8) == 0;
         if (bf16 && (g_fusions & kFuseQKV) && lay) {
-            if (hd == 144) { qkv_fused_launch<144>(a, H, Wq, bias, n, Hl, L, temp, cs, qkv, qk, iq, ik, s); return; }
-            if (hd == 128) { qkv_fused_launch<128>(a, H, Wq, bias, n, Hl, L, temp, cs, qkv, qk, iq, ik, s); return; }
-            if (hd == 64) { qkv_fused_launch<64>(a, H, Wq, bias, n, Hl, L, temp, cs, qkv, qk, iq, ik, s); return; }
+            if (hd == 144) { qkv_fused_launch<144>(a, H, Wq, bias, n, Hl, L, temp, cs, qkv, qk, iq, ik, qkT, vT, ldT, s); return; }
+            if (hd == 128) { qkv_fused_launch<128>(a, H, Wq, bias, n, Hl, L, temp, cs, qkv, qk, iq, ik, qkT, vT, ldT, s); return; }
+            if (hd == 64) { qkv_fused_launch<64>(a, H, Wq, bias, n, Hl, L, temp, cs, qkv, qk, iq, ik, qkT, vT, ldT, s); return; }
         }
     }
+    if (qkT || vT) throw std::logic_error("transposed q|k|v outputs need the fused QKV path");
     gemm(bf16, KM(a, H), KM(Wq, H), n, static_cast<int>(3 * Hl), static_cast<int>(H),
          EpiStore<T>{tp<T>(qkv), 3 * Hl, bias, 1.0f, n, static_cast<int>(3 * Hl)}, s);
     qk_norm_rope<T>(tp<T>(qkv), L, n, static_cast<int>(Hl), static_cast<int>(heads), temp, cs, tp<T>(qk), iq, ik, s);
@@ -972,9 +1002,11 @@ void Model::block_fwd(int i, int64_t N) {
     // self-attention: a = rms(x)(1+sc1)+sh1 (dit.cpp:287)
     rms_mod<T>(Xin, n, H, tab, tld, 0, H, w.mod_id, tp<T>(b.a), b.r0, s);
     qkv_norm_rope<T>(bf, b.a, H, W(blk(i, "attn.qkv.w")), P(blk(i, "attn.qkv.b")).f32, n, H, nh, qk_layout_full(H, nh),
-                     P(blk(i, "attn.temp")).f32, w.cs, b.qkv, b.qk, b.iq, b.ik, s);  // dit.cpp:288-294
+                     P(blk(i, "attn.temp")).f32, w.cs, b.qkv, b.qk, b.iq, b.ik, s, b.qkT, b.vT, w.ldT);  // dit.cpp:288-294
     AttnProblem ap{b.qk, 2 * H, off<T>(b.qk, H), 2 * H, off<T>(b.qkv, 2 * H), 3 * H, b.O, H, b.lse,
                    n, n, int(nh), int(hd)};
+    ap.vt = b.vT;  // null: the attention kernel transposes V itself
+    ap.vt_ld = w.ldT;
     prof_.begin("attn_fwd", s);
     ap.lse_ld = (N + 127) / 128 * 128;
     ap.seg = w.seg;
@@ -987,8 +1019,14 @@ void Model::block_fwd(int i, int64_t N) {
     // cross-attention (dit.cpp:300-305)
     rms_gain<T>(b.X1, n, H, P(blk(i, "xattn.prenorm.g")).f32, tp<T>(b.cn), b.r1, s);
     const float xscale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd)));
-    gemm(bf, KM(b.cn, H), KM(W(blk(i, "xattn.q.w")), H), n, H, H,
-         EpiStore<T>{tp<T>(b.cqs), H, P(blk(i, "xattn.q.b")).f32, xscale, n, int(H)}, s);
+    if (b.cqT)
+        gemm(bf, KM(b.cn, H), KM(W(blk(i, "xattn.q.w")), H), n, H, H,
+             EpiStoreT{tp<__nv_bfloat16>(b.cqs), H, P(blk(i, "xattn.q.b")).f32, xscale, n, int(H),
+                       tp<__nv_bfloat16>(b.cqT), w.ldT},
+             s);
+    else
+        gemm(bf, KM(b.cn, H), KM(W(blk(i, "xattn.q.w")), H), n, H, H,
+             EpiStore<T>{tp<T>(b.cqs), H, P(blk(i, "xattn.q.b")).f32, xscale, n, int(H)}, s);
     gemm(bf, KM(w.text, cfg_.text_dim), KM(W(blk(i, "xattn.kv.w")), cfg_.text_dim), int(L), 2 * H, cfg_.text_dim,
          EpiStore<T>{tp<T>(b.kv), 2 * H, P(blk(i, "xattn.kv.b")).f32, 1.0f, int(L), int(2 * H)}, s);
     AttnProblem xp{b.cqs, H, b.kv, 2 * H, off<T>(b.kv, H), 2 * H, b.Ox, H, b.lse_x, n, int(L), int(nh), int(hd)};
@@ -1029,6 +1067,14 @@ void Model::block_bwd(int i, int64_t N) {
     const int64_t tld = 6 * H;
     float* dX = w.dX;
     float* dm = w.dm;
+    // dO = d(out-proj input) into w.s2 (and dO^T into w.dOT when the attention operands come transposed)
+    auto store_dO = [&](const Mat& A, const Mat& B, int rows, int64_t K) {
+        if (w.tpose)
+            gemm(bf, A, B, rows, int(H), int(K),
+                 EpiStoreT{tp<__nv_bfloat16>(w.s2), H, nullptr, 1.0f, rows, int(H), tp<__nv_bfloat16>(w.dOT), w.ldT}, s);
+        else
+            gemm(bf, A, B, rows, int(H), int(K), EpiStore<T>{tp<T>(w.s2), H, nullptr, 1.0f, rows, int(H)}, s);
+    };
     // ---- FFN (dit.cpp:308-311)
     gate_bwd<T>(dX, tp<T>(b.ff), tab, tld, 5 * H, w.mod_id, nu, n, H, tp<T>(w.s1), w.part1, w.part2, s);
     reduce_chunks_grouped(w.part1, chunks, nu, H, dm + 5 * H, 6 * H, 1.0f, 0, s);  // d gt2
@@ -1051,9 +1097,15 @@ void Model::block_bwd(int i, int64_t N) {
     colsum<T>(tp<T>(w.s1), H, n, H, w.part1, s);
     reduce_chunks(w.part1, chunks, H, G(blk(i, "xattn.out.b")), 1.0f, 1, s);
     gemm(bf, MN(w.s1, H), MN(b.Ox, H), H, H, n, EpiF32{G(blk(i, "xattn.out.w")), H, nullptr, 1.0f, 1, int(H), int(H)}, s);
-    gemm(bf, KM(w.s1, H), MN(W(blk(i, "xattn.out.w")), H), n, H, H, EpiStore<T>{tp<T>(w.s2), H, nullptr, 1.0f, n, int(H)}, s);
+    store_dO(KM(w.s1, H), MN(W(blk(i, "xattn.out.w")), H), n, H);
     AttnBwdProblem xb{AttnProblem{b.cqs, H, b.kv, 2 * H, off<T>(b.kv, H), 2 * H, b.Ox, H, b.lse_x, n, int(L), int(nh), int(hd)},
                       w.s2, H, w.Dvec, w.s1, H, w.dkv, 2 * H, off<T>(w.dkv, H), 2 * H, w.dkv_part, w.q_splits_x};
+    if (w.tpose) {  // q'^T from the forward's xattn.q epilogue, dO^T from the dgrad epilogue above
+        xb.qt = b.cqT;
+        xb.qt_ld = w.ldT;
+        xb.dot = w.dOT;
+        xb.dot_ld = w.ldT;
+    }
     prof_.begin("xattn_bwd", s);
     xb.f.lse_ld = (N + 127) / 128 * 128;
     attention_bwd<T>(bf, xb, s);
@@ -1075,9 +1127,19 @@ void Model::block_bwd(int i, int64_t N) {
     reduce_chunks_grouped(w.part1, chunks, nu, H, dm + 2 * H, 6 * H, 1.0f, 0, s);  // d gt1
     reduce_chunks(w.part2, chunks, H, G(blk(i, "attn.out.b")), 1.0f, 1, s);
     gemm(bf, MN(w.s1, H), MN(b.O, H), H, H, n, EpiF32{G(blk(i, "attn.out.w")), H, nullptr, 1.0f, 1, int(H), int(H)}, s);
-    gemm(bf, KM(w.s1, H), MN(W(blk(i, "attn.out.w")), H), n, H, H, EpiStore<T>{tp<T>(w.s2), H, nullptr, 1.0f, n, int(H)}, s);
+    store_dO(KM(w.s1, H), MN(W(blk(i, "attn.out.w")), H), n, H);
     AttnBwdProblem ab{AttnProblem{b.qk, 2 * H, off<T>(b.qk, H), 2 * H, off<T>(b.qkv, 2 * H), 3 * H, b.O, H, b.lse, n, n, int(nh), int(hd)},
                       w.s2, H, w.Dvec, w.sB, 3 * H, off<T>(w.sB, H), 3 * H, off<T>(w.sB, 2 * H), 3 * H, nullptr, 1};
+    if (w.tpose) {  // Q^T / K^T / V^T from the forward's QKV epilogues, dO^T from the dgrad epilogue above
+        ab.qt = b.qkT;
+        ab.qt_ld = w.ldT;
+        ab.kt = off<__nv_bfloat16>(b.qkT, H * w.ldT);
+        ab.kt_ld = w.ldT;
+        ab.f.vt = b.vT;
+        ab.f.vt_ld = w.ldT;
+        ab.dot = w.dOT;
+        ab.dot_ld = w.ldT;
+    }
     prof_.begin("attn_bwd", s);
     ab.f.lse_ld = (N + 127) / 128 * 128;
     ab.f.seg = w.seg;
@@ -1137,6 +1199,7 @@ void plan_rank_bytes(const Cfg& c, bool bf16, int tp, int64_t N, int64_t L, int 
     w.grads = train;
     w.tp = tp;
     w.tp_slots = 1;
+    set_tpose(w, c);
     Sizer sz{true, 0, nullptr};
     layout_ws(w, sz, c, train);
     out[0] = pf + pb;                              // parameters
@@ -1516,6 +1579,7 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
     w.grads = true;
     w.tp = tp_;
     w.tp_slots = tp_slots();
+    set_tpose(w, cfg_);
     {
         Sizer sz{true, 0, &arena_};
         layout_ws(w, sz, cfg_, true);
@@ -1677,6 +1741,7 @@ void Model::flow_step_packed(int64_t n, const DevSample* samples, const double* 
     w.grads = true;
     w.tp = tp_;
     w.tp_slots = tp_slots();
+    set_tpose(w, cfg_);
     {
         Sizer sz{true, 0, &arena_};
         layout_ws(w, sz, cfg_, true);
@@ -2009,6 +2074,7 @@ void Model::value_forward(const double* in, int64_t N, const int32_t* coords, co
     w.grads = false;
     w.tp = tp_;
     w.tp_slots = tp_slots();
+    set_tpose(w, cfg_);
     {
         Sizer sz{true, 0, &arena_};
         layout_ws(w, sz, cfg_, false);
@@ -2104,6 +2170,7 @@ void Model::velocity_graph_impl(const double* rows, int64_t N, const int32_t* co
     w.grads = true;  // keeps every block's residual stream (the taps) and the backward's activations
     w.tp = tp_;
     w.tp_slots = tp_slots();
+    set_tpose(w, cfg_);
     {
         Sizer sz{true, 0, &arena_};
         layout_ws(w, sz, cfg_, true);
@@ -2344,6 +2411,7 @@ void Model::sample_impl(const double* x_start, int64_t N, const int32_t* coords,
     w.grads = false;
     w.tp = tp_;
     w.tp_slots = tp_slots();
+    set_tpose(w, cfg_);
     {
         Sizer sz{true, 0, &arena_};
         layout_ws(w, sz, cfg_, false);

@@ -1,7 +1,8 @@
-"""The forward fusions against the kernel pairs they replace -- the QKV projection with the QK-L2-norm x
-temperature + 3-D RoPE in its epilogue (EpiQKNormRope, BN = head_dim; replaces GEMM + qk_norm_rope_vec) and the
-post-norm residual with the FFN's modulated RMSNorm (replaces postnorm_resid_vec + rms_fwd_vec): the whole bf16
-training step (loss, velocity, every gradient) must be bit-identical with the fusions on and off.  Parity of the
+"""The fusions against the kernels they replace -- the QKV projection with the QK-L2-norm x temperature + 3-D RoPE
+in its epilogue (EpiQKNormRope, BN = head_dim; replaces GEMM + qk_norm_rope_vec), the post-norm residual with the
+FFN's modulated RMSNorm (replaces postnorm_resid_vec + rms_fwd_vec), and the attention operands' transposes written
+by the producing GEMM epilogues (Q^T / K^T / V^T / q'^T / dO^T; replaces five transpose_bf16 launches per step):
+the whole bf16 training step (loss, velocity, every gradient) must be bit-identical with the fusions on and off.  Parity of the
 unfused path against the oracle is test_parity_gpu.py / test_parity_golden_gpu.py; this pins the fusions to it
 exactly.
 
@@ -25,7 +26,7 @@ EXTRA = {
 
 
 def _step(name, spec, fused, tp=1):
-    """fused: bit mask of mgv_dev_set_fusions (1 QKV epilogue, 2 post-norm + modulated RMSNorm)"""
+    """fused: bit mask of mgv_dev_set_fusions (1 QKV epilogue, 2 post-norm + modulated RMSNorm, 4 transposes)"""
     from paper_2510_17519_b200._lib import lib
     from paper_2510_17519_b200.capi import Context
     cfg, P, text, samples = build_case(name, spec)
@@ -38,7 +39,7 @@ def _step(name, spec, fused, tp=1):
         out = ctx.flow_step(to_samples(samples), text, 8.0, grads=True, velocity=True)
         ctx.close()
     finally:
-        lib().mgv_dev_set_fusions(3)
+        lib().mgv_dev_set_fusions(7)
     return out
 
 
@@ -52,7 +53,7 @@ def _same(a, b):
 
 
 @pytest.mark.parametrize("name", ["cfg0", "hd144", "hd144_360", "w10b"])
-@pytest.mark.parametrize("mask", [1, 2, 3])
+@pytest.mark.parametrize("mask", [1, 2, 3, 5, 7])
 def test_fusions_bit_identical(name, mask):
     spec = dict(CASES, **LONG_CASES, **EXTRA)[name]
     _same(_step(name, spec, mask), _step(name, spec, 0))
@@ -60,4 +61,4 @@ def test_fusions_bit_identical(name, mask):
 
 @pytest.mark.parametrize("tp", [2])
 def test_fusions_bit_identical_tp(tp):
-    _same(_step("hd144_360", EXTRA["hd144_360"], 3, tp), _step("hd144_360", EXTRA["hd144_360"], 0, tp))
+    _same(_step("hd144_360", EXTRA["hd144_360"], 7, tp), _step("hd144_360", EXTRA["hd144_360"], 0, tp))
