@@ -354,23 +354,38 @@ struct EpiQKNormRope {
     int M;
     __nv_bfloat16* qkT;  // optional: rotated q | k transposed ([2 hl][ldT]), the attention backward's Q^T / K^T
     int64_t ldT;
-    template <class LD>
-    __device__ __forceinline__ void tile_row(int m, int n0, LD&& ld_chunk) const {
+    // ldi(c, r): issue the tcgen05.ld of accumulator chunk c into r (16 x u32); wt(): wait for the issued loads.
+    // Both passes keep the next chunk's TMEM load (and its bias / RoPE rows) in flight under the current chunk's math.
+    template <class LDI, class WT>
+    __device__ __forceinline__ void tile_row(int m, int n0, LDI&& ldi, WT&& wt) const {
         constexpr int NC = HD / 16, NP = HD / 8;  // 16-column chunks; 8-element lane partials
         static_assert(HD % 16 == 0 && NP <= 32, "head_dim");
         const int region = static_cast<int>(n0 / hl);  // 0 q, 1 k, 2 v (warp-uniform)
         const int h = static_cast<int>((n0 - region * hl) / HD);
         const bool ok = m < M;
+        const float4* bias4 = reinterpret_cast<const float4*>(bias + n0);
         float part[NP];
+        uint32_t r[2][16];
+        float4 b[2][4];
+        ldi(0, r[0]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) b[0][q] = bias4[q];
+        wt();
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-            float v[16], b[16];
-            ld_chunk(c, v);
-            Vec16<float>::load(bias + n0 + 16 * c, b);
+            const int cur = c & 1, nxt = cur ^ 1;
+            if (c + 1 < NC) {
+                ldi(c + 1, r[nxt]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) b[nxt][q] = bias4[4 * (c + 1) + q];
+            }
+            const float* bb = reinterpret_cast<const float*>(b[cur]);
+            float v[16];
             uint32_t w[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                __nv_bfloat162 p2 = __floats2bfloat162_rn(v[2 * j] + b[2 * j], v[2 * j + 1] + b[2 * j + 1]);
+                __nv_bfloat162 p2 = __floats2bfloat162_rn(__uint_as_float(r[cur][2 * j]) + bb[2 * j],
+                                                          __uint_as_float(r[cur][2 * j + 1]) + bb[2 * j + 1]);
                 w[j] = *reinterpret_cast<uint32_t*>(&p2);
                 const float2 f = __bfloat1622float2(p2);
                 v[2 * j] = f.x;
@@ -388,6 +403,7 @@ struct EpiQKNormRope {
                 for (int e = 0; e < 8; ++e) ss = fmaf(v[8 * hh + e], v[8 * hh + e], ss);
                 part[2 * c + hh] = ss;
             }
+            if (c + 1 < NC) wt();
         }
         if (region == 2) return;
         // the xor butterfly of a 32-lane warp_sum as seen by lane 0 (lanes >= NP contribute 0)
@@ -399,32 +415,45 @@ struct EpiQKNormRope {
         const float iv = 1.0f / sqrtf(part[0] + 1e-6f);  // autodiff.cpp:727
         if (ok) (region == 0 ? iq : ik)[(int64_t)m * i_ld + h] = iv;
         const float sc = region == 0 ? iv * temp[h] : iv;  // dit.cpp:292
-        const float4* csr = reinterpret_cast<const float4*>(cs + (int64_t)m * (HD / 2));
+        const float4* csr = reinterpret_cast<const float4*>(cs + (int64_t)(ok ? m : 0) * (HD / 2));
+        float4 t[2][4];
+        ldi(0, r[0]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            b[0][q] = bias4[q];
+            t[0][q] = csr[q];
+        }
+        wt();
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-            float v[16], b[16], o[16];
-            ld_chunk(c, v);
-            Vec16<float>::load(bias + n0 + 16 * c, b);
-            float4 t[4] = {make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0), make_float4(0, 0, 0, 0),
-                           make_float4(0, 0, 0, 0)};
-            if (ok) {
+            const int cur = c & 1, nxt = cur ^ 1;
+            if (c + 1 < NC) {
+                ldi(c + 1, r[nxt]);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) t[q] = csr[4 * c + q];
+                for (int q = 0; q < 4; ++q) {
+                    b[nxt][q] = bias4[4 * (c + 1) + q];
+                    t[nxt][q] = csr[4 * (c + 1) + q];
+                }
             }
+            const float* bb = reinterpret_cast<const float*>(b[cur]);
+            float o[16];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                const float2 f = __bfloat1622float2(__floats2bfloat162_rn(v[2 * k] + b[2 * k], v[2 * k + 1] + b[2 * k + 1]));
-                const float cc = (k & 1) ? t[k >> 1].z : t[k >> 1].x, sn = (k & 1) ? t[k >> 1].w : t[k >> 1].y;
+                const float2 f = __bfloat1622float2(__floats2bfloat162_rn(__uint_as_float(r[cur][2 * k]) + bb[2 * k],
+                                                                          __uint_as_float(r[cur][2 * k + 1]) + bb[2 * k + 1]));
+                const float4 tt = t[cur][k >> 1];
+                const float cc = (k & 1) ? tt.z : tt.x, sn = (k & 1) ? tt.w : tt.y;
                 rope_pair(__fmul_rn(f.x, sc), __fmul_rn(f.y, sc), cc, sn, o[2 * k], o[2 * k + 1]);
             }
             if (ok) {
                 Vec16<__nv_bfloat16>::store(qk + (int64_t)m * qk_ld + region * qk_koff + h * HD + 16 * c, o);
                 if (qkT) {
-                    __nv_bfloat16* t = qkT + (region * hl + h * HD + 16 * c) * ldT + m;
+                    __nv_bfloat16* tp = qkT + (region * hl + h * HD + 16 * c) * ldT + m;
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) t[j * ldT] = __float2bfloat16_rn(o[j]);
+                    for (int j = 0; j < 16; ++j) tp[j * ldT] = __float2bfloat16_rn(o[j]);
                 }
             }
+            if (c + 1 < NC) wt();
         }
     }
 };

@@ -65,13 +65,8 @@ __device__ __forceinline__ void epilogue_rows(uint32_t acc_base, int wq, int lan
     const uint32_t base = acc_base + hf * W + (static_cast<uint32_t>(g * 32) << 16);
     if constexpr (IsTileEpi<Epi>::value) {  // whole-row functor (BN = one head): chunks on demand
         static_assert(EpiWarps<Epi>::value == 4, "tile epilogues own whole rows");
-        epi.tile_row(row, n0, [&](int c, float* v) {
-            uint32_t q[16];
-            tmem_ld16(base + c * 16, q);
-            tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(q[j]);
-        });
+        epi.tile_row(
+            row, n0, [&](int c, uint32_t* q) { tmem_ld16(base + c * 16, q); }, [] { tmem_wait_ld(); });
     } else {
         uint32_t r[2][16];
         tmem_ld16(base, r[0]);
