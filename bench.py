@@ -310,6 +310,16 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------ our arm
+def rank_groups(rank, world, tp):
+    """rank = dp_rank * tp + tp_rank: a TP group is tp consecutive ranks (one node's NVLink peers), DP joins the
+    ranks holding the same tp_rank.  Returns (tp_rank, dp_rank, dp_world, tp_root, dp_root); the roots are the
+    global ranks (tp_rank 0 of this TP group, dp_rank 0 of this DP group) whose NCCL ids the group uses."""
+    if tp < 1 or world % tp:
+        raise ValueError(f"--tp {tp} does not divide the {world} ranks")
+    tp_rank, dp_rank = rank % tp, rank // tp
+    return tp_rank, dp_rank, world // tp, dp_rank * tp, tp_rank
+
+
 def run_ours(args, rank, world, local):
     import torch
     from paper_2510_17519_b200.capi import (Context, FlowSample, make_flow_sample, mgv_flow_sample, paper_config,
@@ -321,10 +331,11 @@ def run_ours(args, rank, world, local):
     torch.cuda.set_device(local)
     GRID = tuple(args.grid)
     tp = args.tp
-    if world % tp:
-        sys.exit(f"bench.py: --tp {tp} does not divide the {world} ranks")
     # rank = dp_rank * tp + tp_rank: a TP group is tp consecutive ranks; DP joins the ranks with the same tp_rank
-    tp_rank, dp_rank, dp_world = rank % tp, rank // tp, world // tp
+    try:
+        tp_rank, dp_rank, dp_world, tp_root, dp_root = rank_groups(rank, world, tp)
+    except ValueError as e:
+        sys.exit(f"bench.py: {e}")
     cfg = paper_config(depth=args.depth)
     ctx = Context(local, "bf16")
     stream = torch.cuda.Stream()
@@ -337,9 +348,9 @@ def run_ours(args, rank, world, local):
                 Context.nccl_unique_id() if dp_world > 1 and dp_rank == 0 else None)
         dist.all_gather_object(ids, mine)
         if tp > 1:
-            ctx.set_tp(tp, tp_rank, ids[dp_rank * tp][0])
+            ctx.set_tp(tp, tp_rank, ids[tp_root][0])
         if dp_world > 1:
-            ctx.set_dp(dp_rank, dp_world, ids[tp_rank][1])
+            ctx.set_dp(dp_rank, dp_world, ids[dp_root][1])
     ctx.set_adamw(**ADAMW)  # the timed step is the full FlowTrainer::step: fwd + bwd + grad norm + AdamW
     # SURVEY 8(d) weights: init_dit_params(cfg, Rng(1)) + gates opened from Rng(2) at the width-scaled std
     gs = 0.2 * math.sqrt(12.0 / cfg.hidden)
