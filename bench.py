@@ -580,6 +580,10 @@ def main():
     if args.gpus < 1:
         sys.exit("bench.py: --gpus must be >= 1")
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        if args.impl == "ours":
+            import torch
+            if torch.cuda.device_count() < args.gpus:
+                sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, {torch.cuda.device_count()} visible")
         sys.exit(_relaunch_under_torchrun(args))
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     if world_env != args.gpus:
