@@ -14,7 +14,11 @@
 
 namespace mgv {
 
-constexpr int kRowsPerChunk = 64;
+#ifndef MGV_ROWS_PER_CHUNK
+#define MGV_ROWS_PER_CHUNK 64
+#endif
+// rows per CTA of the row kernels; also the chunking of every fixed-order column reduction (bias / gain / gate grads)
+constexpr int kRowsPerChunk = MGV_ROWS_PER_CHUNK;
 inline int row_chunks(int N) { return (N + kRowsPerChunk - 1) / kRowsPerChunk; }
 
 // ---- K1: interpolate + unit-aligned condition mask (flowtrain.cpp:9-20, 83-100); cond = N device flags or null,

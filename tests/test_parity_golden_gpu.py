@@ -77,3 +77,24 @@ def test_w10b_fp32_every_entry(cases):
     worst = max(errs, key=errs.get)
     print(f"w10b fp32 every entry: worst {worst} {errs[worst]:.3e}")
     assert errs[worst] <= 1e-4, (worst, errs[worst])
+
+
+@pytest.mark.parametrize("name,size,prec", [("w10b", 2, "fp32"), ("w10b", 4, "fp32"), ("w10b", 8, "fp32"),
+                                            ("w10b", 8, "bf16"), ("long480p", 2, "fp32"), ("long480p", 2, "bf16")])
+def test_tp_step_vs_reference_golden(cases, name, size, prec):
+    """Megatron head/column TP against the reference's own fixtures at the benchmarked 10B width
+    (24 heads over P = 2 / 4 / 8 ranks: 12 / 6 / 3 heads per rank, partitioned weights, the peer-memory exchange)
+    and at 10,920 tokens: every rank of the group is emulated in one context on this GPU (mgv_ctx_set_tp(P, 0,
+    NULL)); gradients come back in reference layout (all-gathered blocks, permutation undone)."""
+    from paper_2510_17519_b200.capi import Context
+    g = np.load(os.path.join(GOLDEN, f"{name}.npz"))
+    cfg, P, text, samples = _case(cases, name)
+    ctx = Context(0, prec)
+    ctx.set_tp(size)
+    ctx.upload(to_cfg(cfg), P)
+    out = ctx.flow_step(to_samples(samples), text, 8.0, grads=True, velocity=True)
+    ctx.close()
+    errs = check_against_golden(out, g, samples)
+    worst = max(errs, key=errs.get)
+    print(f"tp{size} {name}/{prec}: worst {worst} {errs[worst]:.3e}; loss {errs['loss']:.2e}")
+    assert errs[worst] <= TOL[prec], (worst, errs[worst])
