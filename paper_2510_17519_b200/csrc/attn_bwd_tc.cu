@@ -39,6 +39,10 @@ constexpr float kLog2e = 1.4426950408889634f;
 #ifndef MGV_DKV_X
 #define MGV_DKV_X 0
 #endif
+// dQ pass timing experiment: MGV_DQ_X 2 = no exponentials
+#ifndef MGV_DQ_X
+#define MGV_DQ_X 0
+#endif
 
 #ifdef MGV_ATTN_TRACE  // development timeline of one CTA (tools/trace_attn.py); not in the product build
 __device__ unsigned long long g_attn_trace[8][64];
@@ -685,8 +689,13 @@ __global__ void __launch_bounds__(128 + 128 * 2, 1) attn_bwd_dq_v10_kernel(const
 #pragma unroll
                 for (int c = 0; c < KW; c += 2) {
                     const float2 x = ffma2(make_float2(pr[c], pr[c + 1]), lg2, nl2);
-                    pr[c] = ex2f(x.x);
-                    pr[c + 1] = ex2f(x.y);
+                    if (MGV_DQ_X & 2) {
+                        pr[c] = x.x;
+                        pr[c + 1] = x.y;
+                    } else {
+                        pr[c] = ex2f(x.x);
+                        pr[c + 1] = ex2f(x.y);
+                    }
                 }
             } else {
 #pragma unroll
