@@ -352,6 +352,8 @@ def run_ours(args, rank, world, local):
         if dp_world > 1:
             ctx.set_dp(dp_rank, dp_world, ids[dp_root][1])
     ctx.set_adamw(**ADAMW)  # the timed step is the full FlowTrainer::step: fwd + bwd + grad norm + AdamW
+    if args.recompute:
+        ctx.set_recompute(True)
     # SURVEY 8(d) weights: init_dit_params(cfg, Rng(1)) + gates opened from Rng(2) at the width-scaled std
     gs = 0.2 * math.sqrt(12.0 / cfg.hidden)
     ctx.init_params(cfg, seed=1, gate_seed=2, gate_std=gs, gate_b_std=gs / 4)
@@ -471,7 +473,7 @@ def run_ours(args, rank, world, local):
                                "fwd+bwd + grad norm + AdamW update (the full FlowTrainer::step), 1 sample per "
                                + ("GPU" if tp == 1 else f"TP group of {tp}"),
                    "tokens_per_sample": N, "samples_per_gpu": 1 if tp == 1 else 1.0 / tp, "global_batch": dp_world,
-                   "parallelism": par, "depth": args.depth,
+                   "parallelism": par, "depth": args.depth, "recompute": bool(args.recompute),
                    "l2": "working set ~17 GB >> 126 MB L2 (no flush needed)"},
         "roofline": roof,
         "attention": att,
@@ -574,6 +576,7 @@ def main():
     ap.add_argument("--tp", type=int, default=1, help="tensor-parallel group size (head/column TP over NCCL + NVLink "
                                                       "peer exchange); the other factor of --gpus is DP")
     ap.add_argument("--depth", type=int, default=1, help="DiT blocks (configs[3]: 56, with --grid 7 30 52)")
+    ap.add_argument("--recompute", action="store_true", help="per-block activation recompute (deep stacks at 57.6K)")
     ap.add_argument("--grid", type=int, nargs=3, default=list(GRID_720P), metavar=("U", "H", "W"),
                     help="token grid (latent / 2x2 patches); 7 30 52 = the 480p/2s shape")
     args = ap.parse_args()

@@ -156,11 +156,17 @@ mgv_status mgv_make_flow_sample(uint64_t seed, int64_t N, int64_t D, double mask
  * per-sample masked-mean losses (flowtrain.cpp:263-273): each sample's forward is bit-identical to running it
  * alone; gradients equal the per-sample sum up to summation order.  Default off (samples run one by one). */
 mgv_status mgv_ctx_set_varlen(mgv_ctx* ctx, int on);
+/* Per-block activation recompute for training steps (deep stacks at 57,600 tokens): on != 0
+ * keeps only every block's input residual rows; the backward re-runs each block's forward (same kernels, same
+ * inputs: bit-identical results) before differentiating it.  One extra block forward per block, ~1/depth of the
+ * activation memory.  Default off. */
+mgv_status mgv_ctx_set_recompute(mgv_ctx* ctx, int on);
 /* Memory per rank, out = {parameters (fp32 masters + bf16 operand copies), gradients, AdamW moments, step
  * workspace (saved activations + scratch), TP exchange arena} in bytes.  mgv_plan_rank_bytes plans a step of
  * N tokens (text length L, n_u unique timesteps) for TP degree tp without a device, with the runtime's own
- * layout code (one real TP rank: its parameter blocks and H/P-wide activations); mgv_ctx_memory reports what a
- * context holds now (emulated TP ranks hold all P slots). */
+ * layout code (one real TP rank: its parameter blocks and H/P-wide activations); train: 0 forward, 1 training step,
+ * 3 training step with per-block recompute (mgv_ctx_set_recompute); mgv_ctx_memory reports what a context holds
+ * now (emulated TP ranks hold all P slots). */
 mgv_status mgv_plan_rank_bytes(const mgv_dit_cfg* cfg, int precision, int tp, int64_t N, int64_t L, int64_t n_u,
                                int train, int64_t out[5]);
 mgv_status mgv_ctx_memory(mgv_ctx* ctx, int64_t out[5]);

@@ -123,6 +123,7 @@ def declare(L):
     L.mgv_plan_rank_bytes.argtypes = [ctypes.POINTER(mgv_dit_cfg), I, I, I64, I64, I64, I, P]
     L.mgv_ctx_memory.argtypes = [P, P]
     L.mgv_ctx_set_varlen.argtypes = [P, I]
+    L.mgv_ctx_set_recompute.argtypes = [P, I]
     L.mgv_params_init.argtypes = [P, ctypes.POINTER(mgv_dit_cfg), ctypes.c_uint64, ctypes.c_uint64, D, D]
     L.mgv_params_upload.restype = I
     L.mgv_param_count.argtypes = [P]
@@ -247,7 +248,7 @@ def declare(L):
 # symbols include/mugv_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = ["mgv_ctx_create", "mgv_ctx_destroy", "mgv_last_error", "mgv_ctx_set_stream", "mgv_nccl_unique_id",
            "mgv_ctx_set_dp", "mgv_ctx_set_tp", "mgv_sample_rows", "mgv_ctx_set_adamw", "mgv_adamw_steps", "mgv_param_download",
-           "mgv_params_upload", "mgv_params_init", "mgv_ctx_set_varlen", "mgv_plan_rank_bytes", "mgv_ctx_memory", "mgv_rng_uniform_fill", "mgv_make_flow_sample", "mgv_param_count",
+           "mgv_params_upload", "mgv_params_init", "mgv_ctx_set_varlen", "mgv_ctx_set_recompute", "mgv_plan_rank_bytes", "mgv_ctx_memory", "mgv_rng_uniform_fill", "mgv_make_flow_sample", "mgv_param_count",
            "mgv_param_name", "mgv_param_numel",
            "mgv_predict_velocity", "mgv_velocity_graph", "mgv_dit_forward", "mgv_flow_step", "mgv_flow_loss", "mgv_latent_rows",
            "mgv_rows_to_grid", "mgv_flow_step_device", "mgv_last_step_ms", "mgv_last_step_launches",
@@ -399,11 +400,14 @@ def _f64(a):
 MEMORY_KEYS = ("params", "grads", "adamw", "workspace", "exchange")
 
 
-def plan_rank_bytes(cfg, precision: str, tp: int, N: int, L: int, n_u: int = 2, train: bool = True) -> dict:
-    """mgv_plan_rank_bytes: bytes one TP rank allocates for a step (no device needed)."""
+def plan_rank_bytes(cfg, precision: str, tp: int, N: int, L: int, n_u: int = 2, train: bool = True,
+                    recompute: bool = False) -> dict:
+    """mgv_plan_rank_bytes: bytes one TP rank allocates for a step (no device needed); recompute: a training step with
+    per-block activation recompute."""
     out = (I64 * 5)()
     c = cfg.to_c()
-    st = _lib().mgv_plan_rank_bytes(ctypes.byref(c), 1 if precision == "bf16" else 0, tp, N, L, n_u, int(train), out)
+    flags = (3 if recompute else 1) if train else 0
+    st = _lib().mgv_plan_rank_bytes(ctypes.byref(c), 1 if precision == "bf16" else 0, tp, N, L, n_u, flags, out)
     if st != 0:
         raise ConfigError(f"mgv_plan_rank_bytes failed ({st})")
     return dict(zip(MEMORY_KEYS, list(out)))
@@ -741,6 +745,10 @@ class Context:
     def set_varlen(self, on: bool = True):
         """mgv_ctx_set_varlen: pack multi-sample flow steps into one block-diagonal sequence."""
         self._check(self._L.mgv_ctx_set_varlen(self.h, int(on)))
+
+    def set_recompute(self, on: bool = True):
+        """mgv_ctx_set_recompute: per-block activation recompute in training steps."""
+        self._check(self._L.mgv_ctx_set_recompute(self.h, int(on)))
 
     def memory(self) -> dict:
         """mgv_ctx_memory: this context's allocations in bytes."""

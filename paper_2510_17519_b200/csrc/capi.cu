@@ -217,14 +217,18 @@ mgv_status mgv_ctx_set_varlen(mgv_ctx* ctx, int on) {
     return guard(ctx, [&] { ctx->model->set_varlen(on != 0); });
 }
 
+mgv_status mgv_ctx_set_recompute(mgv_ctx* ctx, int on) {
+    return guard(ctx, [&] { ctx->model->set_recompute(on != 0); });
+}
+
 // per-rank memory of a training (or forward) step: {parameters, gradients, AdamW moments, workspace, exchange}
 mgv_status mgv_plan_rank_bytes(const mgv_dit_cfg* cfg, int precision, int tp, int64_t N, int64_t L, int64_t n_u,
                                int train, int64_t out[5]) {
     std::string err;
     return mgv::guard_into(err, [&] {
         if (!cfg || !out || N < 1 || L < 1 || n_u < 1) throw mgv::InputError("bad argument");
-        mgv::plan_rank_bytes(to_cfg(cfg), precision == MGV_PREC_BF16, tp, N, L, static_cast<int>(n_u), train != 0,
-                             out);
+        mgv::plan_rank_bytes(to_cfg(cfg), precision == MGV_PREC_BF16, tp, N, L, static_cast<int>(n_u),
+                             train == 0 ? 0 : (train & 2) ? 3 : 1, out);
     });
 }
 mgv_status mgv_ctx_memory(mgv_ctx* ctx, int64_t out[5]) {

@@ -94,6 +94,8 @@ struct Model::WS {
     // bf16, unsharded: the attention operands' transposes ([heads*hd][ldT]) come from GEMM epilogues
     bool tpose = false;
     int64_t ldT = 0;
+    // training with per-block activation recompute: one block's activations (slot 0), every block's input X kept
+    bool recompute = false;
     void* dOT = nullptr;  // dO^T of the attention being differentiated (self, then cross)
 };
 
@@ -144,7 +146,7 @@ void layout_ws(Model::WS& w, S& a, const Cfg& c, bool grads) {
     const int nX = grads ? c.depth + 1 : 2;
     w.X.assign(nX, nullptr);
     for (int i = 0; i < nX; ++i) w.X[i] = a.template take<float>(N * H);
-    const int nB = grads ? c.depth : 1;
+    const int nB = grads && !w.recompute ? c.depth : 1;
     w.blk.assign(nB, Blk{});
     for (int i = 0; i < nB; ++i) {
         Blk& b = w.blk[i];
@@ -993,7 +995,7 @@ void Model::block_fwd(int i, int64_t N) {
     const bool bf = bf16_;
     cudaStream_t s = stream_;
     const int64_t H = cfg_.H(), nh = cfg_.heads, hd = cfg_.hd(), L = w.L;
-    Blk& b = w.blk[w.grads ? i : 0];
+    Blk& b = w.blk[w.grads && !w.recompute ? i : 0];
     const float* Xin = w.X[w.grads ? i : (i % 2)];
     float* Xout = w.X[w.grads ? i + 1 : ((i + 1) % 2)];
     const float* tab = w.table[i];
@@ -1061,7 +1063,7 @@ void Model::block_bwd(int i, int64_t N) {
     cudaStream_t s = stream_;
     const int64_t H = cfg_.H(), nh = cfg_.heads, hd = cfg_.hd(), L = w.L;
     const int n = static_cast<int>(N), nu = w.n_u, chunks = row_chunks(n);
-    Blk& b = w.blk[i];
+    Blk& b = w.blk[w.recompute ? 0 : i];
     const float* Xin = w.X[i];
     const float* tab = w.table[i];
     const int64_t tld = 6 * H;
@@ -1164,7 +1166,7 @@ void Model::block_bwd(int i, int64_t N) {
 // parameters (fp32 masters + bf16 operand copies), the gradient buffer, the AdamW moments, the step workspace
 // (every block's saved activations) and the peer-exchange arena.  The same layout code the runtime uses, run in
 // measure mode, so a plan needs no device (the 56-block stack at P = 8).
-void plan_rank_bytes(const Cfg& c, bool bf16, int tp, int64_t N, int64_t L, int n_u, bool train, int64_t out[5]) {
+void plan_rank_bytes(const Cfg& c, bool bf16, int tp, int64_t N, int64_t L, int n_u, int train, int64_t out[5]) {
     validate_cfg(c);
     if (tp < 1 || c.heads % tp != 0) throw ConfigError("tensor parallel size must divide heads");
     const int64_t H = c.H(), D = c.D();
@@ -1196,7 +1198,8 @@ void plan_rank_bytes(const Cfg& c, bool bf16, int tp, int64_t N, int64_t L, int 
     w.L = L;
     w.n_u = n_u;
     w.esz = bf16 ? 2 : 4;
-    w.grads = train;
+    w.grads = train != 0;
+    w.recompute = (train & 2) != 0;
     w.tp = tp;
     w.tp_slots = 1;
     set_tpose(w, c);
@@ -1234,7 +1237,7 @@ void Model::block_fwd_tp(int i, int64_t N) {
     cudaStream_t s = stream_;
     const int64_t H = cfg_.H(), nh = cfg_.heads, hd = cfg_.hd(), L = w.L, td = cfg_.text_dim;
     const int64_t Hr = H / tp_, nhr = nh / tp_, Fr = 4 * H / tp_, lld = (N + 127) / 128 * 128;  // 128-row lse tiles
-    Blk& b = w.blk[w.grads ? i : 0];
+    Blk& b = w.blk[w.grads && !w.recompute ? i : 0];
     const float* Xin = w.X[w.grads ? i : (i % 2)];
     float* Xout = w.X[w.grads ? i + 1 : ((i + 1) % 2)];
     const float* tab = w.table[i];
@@ -1327,7 +1330,7 @@ void Model::block_bwd_tp(int i, int64_t N) {
     const int64_t H = cfg_.H(), nh = cfg_.heads, hd = cfg_.hd(), L = w.L, td = cfg_.text_dim;
     const int64_t Hr = H / tp_, nhr = nh / tp_, Fr = 4 * H / tp_, lld = (N + 127) / 128 * 128;  // 128-row lse tiles
     const int n = static_cast<int>(N), nu = w.n_u, chunks = row_chunks(n);
-    Blk& b = w.blk[i];
+    Blk& b = w.blk[w.recompute ? 0 : i];
     const float* Xin = w.X[i];
     const float* tab = w.table[i];
     const int64_t tld = 6 * H;
@@ -1517,7 +1520,16 @@ void Model::backward_sample(const void* dV) {
     reduce_chunks(w.part1, chunks, H, G("dit.final.g"), 1.0f, 1, s);
     MGV_CUDA(cudaMemsetAsync(w.dg, 0, sizeof(double) * nu * H, s));
     prof_.begin("blocks_bwd", s);
-    for (int i = static_cast<int>(cfg_.depth) - 1; i >= 0; --i) block_bwd<T>(i, w.N);
+    for (int i = static_cast<int>(cfg_.depth) - 1; i >= 0; --i) {
+        // per-block recompute: slot 0 holds the last block's activations after the forward; every other block's
+        // are rebuilt from its kept input X[i] (same kernels, same inputs: bit-identical to keeping them)
+        if (w.recompute && i + 1 < cfg_.depth) {
+            prof_.begin("recompute", s);
+            block_fwd<T>(i, w.N);
+            prof_.end(s);
+        }
+        block_bwd<T>(i, w.N);
+    }
     prof_.end(s);
     // patch embedding (rows are constants, dit.cpp:327)
     convert_f32<T>(w.dX, (int64_t)n * H, tp<T>(w.s1), s);
@@ -1579,6 +1591,7 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
     w.grads = true;
     w.tp = tp_;
     w.tp_slots = tp_slots();
+    w.recompute = recompute_ && w.grads;
     set_tpose(w, cfg_);
     {
         Sizer sz{true, 0, &arena_};
@@ -1741,6 +1754,7 @@ void Model::flow_step_packed(int64_t n, const DevSample* samples, const double* 
     w.grads = true;
     w.tp = tp_;
     w.tp_slots = tp_slots();
+    w.recompute = recompute_ && w.grads;
     set_tpose(w, cfg_);
     {
         Sizer sz{true, 0, &arena_};
@@ -2074,6 +2088,7 @@ void Model::value_forward(const double* in, int64_t N, const int32_t* coords, co
     w.grads = false;
     w.tp = tp_;
     w.tp_slots = tp_slots();
+    w.recompute = recompute_ && w.grads;
     set_tpose(w, cfg_);
     {
         Sizer sz{true, 0, &arena_};
@@ -2170,6 +2185,7 @@ void Model::velocity_graph_impl(const double* rows, int64_t N, const int32_t* co
     w.grads = true;  // keeps every block's residual stream (the taps) and the backward's activations
     w.tp = tp_;
     w.tp_slots = tp_slots();
+    w.recompute = recompute_ && w.grads;
     set_tpose(w, cfg_);
     {
         Sizer sz{true, 0, &arena_};
@@ -2411,6 +2427,7 @@ void Model::sample_impl(const double* x_start, int64_t N, const int32_t* coords,
     w.grads = false;
     w.tp = tp_;
     w.tp_slots = tp_slots();
+    w.recompute = recompute_ && w.grads;
     set_tpose(w, cfg_);
     {
         Sizer sz{true, 0, &arena_};

@@ -32,7 +32,8 @@ struct Cfg {
 };
 void validate_cfg(const Cfg& c);
 // bytes one rank allocates for a step: out = {parameters, gradients, AdamW moments, workspace, exchange arena}
-void plan_rank_bytes(const Cfg& c, bool bf16, int tp, int64_t N, int64_t L, int n_u, bool train, int64_t out[5]);
+// train: 0 forward only, 1 training step, 3 training step with per-block activation recompute
+void plan_rank_bytes(const Cfg& c, bool bf16, int tp, int64_t N, int64_t L, int n_u, int train, int64_t out[5]);
 
 struct DevParam {
     std::string name;
@@ -139,6 +140,7 @@ public:
     int tp_size() const { return tp_; }
     // varlen packing of multi-sample flow steps (flow_step_packed); off: samples run one after another
     void set_varlen(bool on) { varlen_ = on; }
+    void set_recompute(bool on) { recompute_ = on; }
     bool varlen() const { return varlen_; }
     void memory_bytes(int64_t out[5]) const;  // this context's allocations, same categories as plan_rank_bytes
     // AdamW::update after every flow step (optim.cpp:7-24, flowtrain.cpp:278); lr <= 0 disables
@@ -256,6 +258,7 @@ private:
     Cfg cfg_;
     bool have_params_ = false;
     bool varlen_ = false;
+    bool recompute_ = false;
     std::map<std::string, DevParam> params_;
     std::vector<DevParam*> sorted_;
     float* grad_buf_ = nullptr;
