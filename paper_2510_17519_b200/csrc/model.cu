@@ -94,8 +94,13 @@ struct Model::WS {
     // bf16, unsharded: the attention operands' transposes ([heads*hd][ldT]) come from GEMM epilogues
     bool tpose = false;
     int64_t ldT = 0;
-    // training with per-block activation recompute: one block's activations (slot 0), every block's input X kept
+    // training with per-block activation recompute: one block's activations (slot 0), every block's input X kept,
+    // and every block's self-attention output O and lse (the recompute re-runs the GEMMs and row kernels, not the
+    // attention forward: O / lse are small next to what they cost to recompute)
     bool recompute = false;
+    bool recompute_pass = false;  // set while re-running a block's forward inside the backward
+    std::vector<void*> Okeep;
+    std::vector<float*> lsekeep;
     void* dOT = nullptr;  // dO^T of the attention being differentiated (self, then cross)
 };
 
@@ -181,6 +186,12 @@ void layout_ws(Model::WS& w, S& a, const Cfg& c, bool grads) {
             b.vT = a.takeT(H * w.ldT, 2);
             b.cqT = a.takeT(H * w.ldT, 2);
         }
+    }
+    w.Okeep.assign(grads && w.recompute ? c.depth : 0, nullptr);
+    w.lsekeep.assign(grads && w.recompute ? c.depth : 0, nullptr);
+    for (size_t i = 0; i < w.Okeep.size(); ++i) {
+        w.Okeep[i] = a.takeT(R * N * Hr, e);
+        w.lsekeep[i] = a.template take<float>(((N + 127) / 128 * 128) * nh);
     }
     w.segbuf = a.template take<int>(2 * ((N + 127) / 128));
     w.seg = nullptr;
@@ -987,6 +998,13 @@ static void attention_bwd(bool bf16, const AttnBwdProblem& p, cudaStream_t s) {
         attn_bwd_simt<T>(p, s);
 }
 
+void Model::use_block_slot(int i) {
+    WS& w = *ws_;
+    if (!w.recompute) return;
+    w.blk[0].O = w.Okeep[static_cast<size_t>(i)];
+    w.blk[0].lse = w.lsekeep[static_cast<size_t>(i)];
+}
+
 // ------------------------------------------------------------------ block forward (dit.cpp:279-313)
 template <class T>
 void Model::block_fwd(int i, int64_t N) {
@@ -1012,7 +1030,7 @@ void Model::block_fwd(int i, int64_t N) {
     prof_.begin("attn_fwd", s);
     ap.lse_ld = (N + 127) / 128 * 128;
     ap.seg = w.seg;
-    attention_fwd<T>(bf, ap, s);  // mha (autodiff.cpp:755-793)
+    if (!w.recompute_pass) attention_fwd<T>(bf, ap, s);  // mha (autodiff.cpp:755-793); kept O / lse on recompute
     prof_.end(s);
     gemm(bf, KM(b.O, H), KM(W(blk(i, "attn.out.w")), H), n, H, H,
          EpiGateResid<T>{Xin, b.X1, H, tp<T>(b.ao), H, P(blk(i, "attn.out.b")).f32, tab + 2 * H, tld, w.mod_id, n,
@@ -1271,7 +1289,7 @@ void Model::block_fwd_tp(int i, int64_t N) {
         ap.lse_ld = lld;
         ap.seg = w.seg;
         prof_.begin("attn_fwd", s);
-        attention_fwd<T>(bf, ap, s);
+        if (!w.recompute_pass) attention_fwd<T>(bf, ap, s);  // kept O / lse on recompute
         prof_.end(s);
         rowpar(k, r, KM(O_r, Hr), KM(Ws(blk(i, "attn.out.w"), kk), Hr), int(Hr), 1.0f);
     }
@@ -1485,7 +1503,10 @@ void Model::forward_sample(const DevSample& smp, const void* rows_in, const doub
              EpiF32{w.X[0], H, P("dit.patch.b").f32, 1.0f, 0, n, int(H)}, s);
     (void)grads;
     prof_.begin("blocks_fwd", s);
-    for (int i = 0; i < cfg_.depth; ++i) block_fwd<T>(i, w.N);
+    for (int i = 0; i < cfg_.depth; ++i) {
+        use_block_slot(i);
+        block_fwd<T>(i, w.N);
+    }
     prof_.end(s);
     const float* Xf = w.X[w.grads ? cfg_.depth : (cfg_.depth % 2)];
     rms_gain<T>(Xf, n, H, P("dit.final.g").f32, tp<T>(w.fin), w.rf, s);  // dit.cpp:314
@@ -1523,9 +1544,12 @@ void Model::backward_sample(const void* dV) {
     for (int i = static_cast<int>(cfg_.depth) - 1; i >= 0; --i) {
         // per-block recompute: slot 0 holds the last block's activations after the forward; every other block's
         // are rebuilt from its kept input X[i] (same kernels, same inputs: bit-identical to keeping them)
+        use_block_slot(i);
         if (w.recompute && i + 1 < cfg_.depth) {
             prof_.begin("recompute", s);
+            w.recompute_pass = true;
             block_fwd<T>(i, w.N);
+            w.recompute_pass = false;
             prof_.end(s);
         }
         block_bwd<T>(i, w.N);
