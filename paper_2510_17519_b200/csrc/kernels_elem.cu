@@ -839,13 +839,15 @@ void colsum(const T* Y, int64_t ld, int N, int C, float* part, cudaStream_t s) {
     colsum_kernel<T><<<grid, 256, 0, s>>>(Y, ld, N, C, part); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
-// Block = 32 consecutive (group, column) entries x 8 warps.  Warp r sums chunks r, r + 8, r + 16, ... and
-// the 8 partial sums are then added in warp order: a fixed reduction tree, so the result is deterministic
-// while 8 x total/32 warps share the (chunks x total) reads.
-__global__ void __launch_bounds__(256) reduce_chunks_kernel(const float* part, int chunks, int groups, int C,
-                                                            float* out, int64_t out_stride, float alpha,
-                                                            int accumulate) {
-    __shared__ float red[8][33];
+// Block = 32 consecutive (group, column) entries x kRcWarps warps.  Warp r sums chunks r, r + kRcWarps, ... and
+// the partial sums are then added in warp order: a fixed reduction tree, so the result is deterministic while
+// kRcWarps x total/32 warps share the (chunks x total) reads (16 warps: 57 sequential loads each at 900 chunks;
+// with 8 the 108-CTA launches for H-wide gradients were latency-bound at ~20 us).
+constexpr int kRcWarps = 16;
+__global__ void __launch_bounds__(32 * kRcWarps) reduce_chunks_kernel(const float* part, int chunks, int groups,
+                                                                     int C, float* out, int64_t out_stride,
+                                                                     float alpha, int accumulate) {
+    __shared__ float red[kRcWarps][33];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int64_t total = (int64_t)groups * C;
     const int64_t e = blockIdx.x * 32LL + tx;
@@ -853,26 +855,26 @@ __global__ void __launch_bounds__(256) reduce_chunks_kernel(const float* part, i
     if (e < total) {
         int c = ty;
 #pragma unroll 4
-        for (; c < chunks; c += 8) acc += part[(int64_t)c * total + e];
+        for (; c < chunks; c += kRcWarps) acc += part[(int64_t)c * total + e];
     }
     red[ty][tx] = acc;
     __syncthreads();
     if (ty == 0 && e < total) {
         float sum = 0.0f;
 #pragma unroll
-        for (int r = 0; r < 8; ++r) sum += red[r][tx];
+        for (int r = 0; r < kRcWarps; ++r) sum += red[r][tx];
         const int gidx = static_cast<int>(e / C), j = static_cast<int>(e % C);
         float* o = out + gidx * out_stride + j;
         *o = accumulate ? *o + alpha * sum : alpha * sum;
     }
 }
 void reduce_chunks(const float* part, int chunks, int C, float* out, float alpha, int accumulate, cudaStream_t s) {
-    reduce_chunks_kernel<<<(C + 31) / 32, 256, 0, s>>>(part, chunks, 1, C, out, 0, alpha, accumulate); ::mgv::note_launch();
+    reduce_chunks_kernel<<<(C + 31) / 32, 32 * kRcWarps, 0, s>>>(part, chunks, 1, C, out, 0, alpha, accumulate); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
 void reduce_chunks_grouped(const float* part, int chunks, int groups, int C, float* out, int64_t out_stride,
                            float alpha, int accumulate, cudaStream_t s) {
-    reduce_chunks_kernel<<<static_cast<int>(((int64_t)groups * C + 31) / 32), 256, 0, s>>>(
+    reduce_chunks_kernel<<<static_cast<int>(((int64_t)groups * C + 31) / 32), 32 * kRcWarps, 0, s>>>(
         part, chunks, groups, C, out, out_stride, alpha, accumulate); ::mgv::note_launch();
     MGV_CUDA(cudaGetLastError());
 }
