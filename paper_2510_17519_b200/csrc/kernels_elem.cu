@@ -937,6 +937,9 @@ __global__ void vecmat_part_kernel(const TI* in, int64_t in_ld, int rows, const 
     double acc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    // unrolled so that several W rows are in flight per thread (the loop was load-latency bound at ~1.4 TB/s);
+    // the accumulation order is unchanged
+#pragma unroll 8
     for (int k = k0; k < k1; ++k) {
         const double w = static_cast<double>(W[(int64_t)k * J + j]);
 #pragma unroll
