@@ -35,6 +35,5 @@ def _declare(L):
     L.mgv_dev_gemm.restype = I
     L.mgv_dev_set_gemm_mode.argtypes = [I]
     L.mgv_dev_set_fusions.argtypes = [I]
-    L.mgv_dev_set_attn_dbg.argtypes = [I]
     from . import capi
     capi.declare(L)

@@ -26,8 +26,6 @@
 
 namespace mgv {
 
-// timing experiments only (tools/): bit 0 = compute warps skip TMEM traffic and math, bit 1 = no Q^T/dO^T TMA
-__device__ int g_attn_dbg = 0;
 
 namespace {
 
@@ -846,6 +844,3 @@ extern "C" int mgv_dev_attn_trace2(unsigned long long* out) {
 }
 #endif
 
-extern "C" int mgv_dev_set_attn_dbg(int v) {
-    return cudaMemcpyToSymbol(mgv::g_attn_dbg, &v, sizeof(int)) == cudaSuccess ? 0 : 1;
-}

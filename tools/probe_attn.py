@@ -10,8 +10,6 @@ from paper_2510_17519_b200._lib import lib  # noqa: E402
 
 L = lib()
 import os  # noqa: E402
-if os.environ.get("MGV_ATTN_DBG"):  # timing experiments (wrong results): see attn_bwd_tc.cu g_attn_dbg
-    L.mgv_dev_set_attn_dbg(int(os.environ["MGV_ATTN_DBG"]))
 P = ctypes.c_void_p
 i64 = ctypes.c_int64
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 57600
