@@ -362,6 +362,20 @@ void Model::set_dp(int rank, int world, const uint8_t id[128]) {
 
 // Gradient buckets of the data-parallel all-reduce (see model.h).  Names are sorted, so one block's
 // "dit.blk.<i>.<group>" parameters are one contiguous range of the gradient buffer.
+// Failure detection for the multi-GPU paths: a peer that died or a network error leaves an asynchronous error on
+// the communicator; surface it as NcclError at the end of the step (the ABI returns MGV_ERR_NCCL) instead of letting
+// the next collective hang.
+void Model::check_comms() {
+    for (ncclComm_t c : {comm_, tp_comm_}) {
+        if (!c) continue;
+        ncclResult_t r = ncclSuccess;
+        MGV_NCCL(ncclCommGetAsyncError(c, &r));
+        if (r != ncclSuccess && r != ncclInProgress)
+            throw NcclError(std::string("asynchronous NCCL error on a ") + (c == comm_ ? "data" : "tensor") +
+                            "-parallel communicator: " + ncclGetErrorString(r));
+    }
+}
+
 void Model::dp_bucket(int block, const char* group) {
     if (!dp_overlap_) return;
     const std::string pre = "dit.blk." + std::to_string(block) + "." + group;
@@ -1719,6 +1733,7 @@ void Model::flow_step_impl(int64_t n, const DevSample* samples, const double* te
     MGV_CUDA(cudaMemcpyAsync(host, w.scal, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
     MGV_CUDA(cudaEventRecord(e1, s));
     MGV_CUDA(cudaStreamSynchronize(s));
+    check_comms();
     float ms = 0.0f;
     MGV_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     last_ms_ = ms;
@@ -1865,6 +1880,7 @@ void Model::flow_step_packed(int64_t n, const DevSample* samples, const double* 
     MGV_CUDA(cudaMemcpyAsync(host, w.scal, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
     MGV_CUDA(cudaEventRecord(e1, s));
     MGV_CUDA(cudaStreamSynchronize(s));
+    check_comms();
     float ms = 0.0f;
     MGV_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     last_ms_ = ms;

@@ -217,6 +217,7 @@ private:
                         const int32_t* mod_id, double fps, bool grads, bool head, void* out);
     template <class T>
     void backward_sample(const void* dV);
+    void check_comms();          // asynchronous NCCL errors -> NcclError
     void use_block_slot(int i);  // per-block recompute: point the shared activation slot at block i's kept O / lse
     template <class T>
     void block_fwd(int i, int64_t N);
